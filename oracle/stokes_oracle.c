@@ -1,0 +1,992 @@
+/*
+ * oracle/stokes_oracle.c -- CPU ORACLE. TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * legs may load this library.  The product path (paper_2603_14040_b200/) never links,
+ * imports or executes anything under oracle/, and this file includes no header from
+ * the product tree: it shares no code with the CUDA path.
+ *
+ * A plain, slow, single-threaded FP64 implementation of the matrix-free geometric
+ * multigrid Stokes solve of arXiv 2603.14040 (Pyroclast), written from PAPER.md:
+ *   - staggered grid, "lower-right" indexing, ghost/boundary nodes  (§4.4.1)
+ *   - stress-conservative FD; the x-momentum row is Listing vx_op_point;
+ *     the y-momentum row follows "the same procedure" -> DESIGN.md reading R2
+ *   - saddle system [L G; D 0][v;p] = [f;0]       (Eq. stokes_saddle)
+ *   - inexact Uzawa + diagonal Schur surrogate    (Eq. uzawa_iteration;
+ *     sign reading R3), zero-mean pressure        (Eq. pressure_normalization)
+ *   - V-cycle (Eq. multigrid_levels), bilinear prolongation
+ *     (PAPER.md:970-982), normalised bilinear restriction (Alg. 2),
+ *     damped Jacobi (Eq. damped_jacobi), damped RBGS
+ *     (Eq. sor_update; 4-phase reading R11)
+ *   - flexible GCR(m) with MGS (Alg. 4), preconditioner M^-1 of the
+ *     Uzawa splitting
+ *   - relative energy residual
+ * Readings where the paper is silent/garbled are the R-numbers of DESIGN.md §3 (they
+ * follow SURVEY.md §8(c) Q1..Q23).
+ *
+ * Arithmetic: IEEE FP64, round to nearest, compiled with -O2 -ffp-contract=off;
+ * reductions are pairwise sums in row-major order (vx, then vy, then p).
+ *
+ * Pins: every function below is pinned by a -m "not gpu" test in tests/test_oracle_*.py
+ * (dense assembly from the stress formulas, MMS second order, hydrostatics, transfer
+ * identities, spectral radius of the Uzawa map, GCR on dense systems).  The iteration
+ * COUNT of a solve is "parity unpinned" by the paper (it prints none): pinned only
+ * oracle <-> GPU, see DESIGN.md §4.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define MAXLEV 24
+
+typedef struct {
+    int smoother;        /* 0 damped Jacobi, 1 RBGS 4-phase */
+    double omega_v;      /* velocity relaxation */
+    double alpha_p;      /* pressure relaxation (omega_p) */
+    int nu1;             /* sweeps on the finest level (pre and post) */
+    double nu_growth;    /* per-level growth g of the sweep count */
+    int coarse_min;      /* coarsen while min(ncx,ncy)/2 >= coarse_min */
+    int coarse_direct;   /* 1 exact coarsest solve, 0 2*nu_L smoothing sweeps */
+    int vcycles_per_iter;
+    int accel;           /* 0 plain Uzawa, 1 flexible GCR(m) */
+    int gcr_restart;     /* m */
+    int max_iter;
+    int pressure_sign;   /* +1 physical reading R3 (default); -1 literal PAPER.md:824 */
+} oracle_opts;
+
+typedef struct {
+    int ncx, ncy;          /* cells */
+    double dx, dy;
+    int W;                 /* padded row length = ncx + 2 */
+    double *etab, *etap;   /* padded (ncy+2) x (ncx+2) */
+    /* scratch (padded) */
+    double *rx, *ry, *bx, *by, *ex, *ey, *tx, *ty;
+    int nu;                /* sweeps per pre/post smoothing on this level */
+} olevel;
+
+typedef struct {
+    int nx, ny;
+    double Lx, Ly;
+    int bc[4];             /* W, E, N(top), S(bottom): 0 free slip, 1 no slip */
+    double gx, gy;
+    oracle_opts o;
+    int nlev;
+    olevel lev[MAXLEV];
+    double *rhob;          /* padded, fine */
+    double *fx, *fy;       /* padded body force at vx / vy nodes (fine) */
+    int have_eta, have_rho, force_override;
+    /* coarsest direct solve: Cholesky factor of -L_c (dense, lower, row-major) */
+    int nc;                /* coarsest unknowns */
+    double *chol;
+    /* fine-level work fields */
+    double *vx, *vy, *p;
+} oracle_t;
+
+/* ------------------------------------------------------------------ helpers */
+static inline int IX(const olevel *L, int i, int j) { return i * L->W + j; }
+static double sgn_of(int bc) { return bc == 0 ? 1.0 : -1.0; } /* free slip +1, no slip -1 */
+
+static double *zalloc(size_t n) { return (double *)calloc(n ? n : 1, sizeof(double)); }
+static size_t padn(const olevel *L) { return (size_t)(L->ncy + 2) * (size_t)(L->ncx + 2); }
+
+/* Pairwise summation of a[0..n-1] (fixed order). */
+static double pairwise(const double *a, size_t n) {
+    if (n == 0) return 0.0;
+    if (n <= 8) {
+        double s = 0.0;
+        for (size_t k = 0; k < n; ++k) s += a[k];
+        return s;
+    }
+    size_t h = n / 2;
+    return pairwise(a, h) + pairwise(a + h, n - h);
+}
+
+/* ----------------------------------------------- boundary conditions (R1, R5)
+ * Mirror ("boundary") nodes: vx rows 0 and ncy+1 mirror rows 1 and ncy with sign s_N/s_S;
+ * vy columns 0 and ncx+1 mirror columns 1 and ncx with sign s_W/s_E; the wall-normal
+ * nodes (vx columns 0, ncx; vy rows 0, ncy) are zero. */
+static void refresh_mirrors(const oracle_t *S, const olevel *L, double *vx, double *vy) {
+    int ncx = L->ncx, ncy = L->ncy;
+    double sW = sgn_of(S->bc[0]), sE = sgn_of(S->bc[1]), sN = sgn_of(S->bc[2]), sS = sgn_of(S->bc[3]);
+    for (int i = 0; i <= ncy + 1; ++i) { vx[IX(L, i, 0)] = 0.0; vx[IX(L, i, ncx)] = 0.0; }
+    for (int j = 1; j <= ncx - 1; ++j) {
+        vx[IX(L, 0, j)] = sN * vx[IX(L, 1, j)];
+        vx[IX(L, ncy + 1, j)] = sS * vx[IX(L, ncy, j)];
+    }
+    for (int j = 0; j <= ncx + 1; ++j) { vy[IX(L, 0, j)] = 0.0; vy[IX(L, ncy, j)] = 0.0; }
+    for (int i = 1; i <= ncy - 1; ++i) {
+        vy[IX(L, i, 0)] = sW * vy[IX(L, i, 1)];
+        vy[IX(L, i, ncx + 1)] = sE * vy[IX(L, i, ncx)];
+    }
+}
+
+/* ------------------------------------------------ the operator (a2)
+ * x-momentum row at vx(i,j): Listing vx_op_point, verbatim
+ * (velocity part; the pressure part is grad_x below). */
+static double Lx_point(const olevel *L, const double *vx, const double *vy, int i, int j) {
+    double dx = L->dx, dy = L->dy;
+    double etaA = L->etap[IX(L, i, j)];
+    double etaB = L->etap[IX(L, i, j + 1)];
+    double eta1 = L->etab[IX(L, i - 1, j)];
+    double eta2 = L->etab[IX(L, i, j)];
+    double vx1 = 2.0 * etaA / (dx * dx);
+    double vx2 = eta1 / (dy * dy);
+    double vx3 = -(eta1 + eta2) / (dy * dy) - 2.0 * (etaA + etaB) / (dx * dx);
+    double vx4 = eta2 / (dy * dy);
+    double vx5 = 2.0 * etaB / (dx * dx);
+    double vy1 = eta1 / (dx * dy);
+    double vy2 = -eta2 / (dx * dy);
+    double vy3 = -eta1 / (dx * dy);
+    double vy4 = eta2 / (dx * dy);
+    return vx1 * vx[IX(L, i, j - 1)] + vx2 * vx[IX(L, i - 1, j)] + vx3 * vx[IX(L, i, j)] +
+           vx4 * vx[IX(L, i + 1, j)] + vx5 * vx[IX(L, i, j + 1)] + vy1 * vy[IX(L, i - 1, j)] +
+           vy2 * vy[IX(L, i, j)] + vy3 * vy[IX(L, i - 1, j + 1)] + vy4 * vy[IX(L, i, j + 1)];
+}
+static double Lx_center(const olevel *L, int i, int j) {
+    double dx = L->dx, dy = L->dy;
+    double etaA = L->etap[IX(L, i, j)], etaB = L->etap[IX(L, i, j + 1)];
+    double eta1 = L->etab[IX(L, i - 1, j)], eta2 = L->etab[IX(L, i, j)];
+    return -(eta1 + eta2) / (dy * dy) - 2.0 * (etaA + etaB) / (dx * dx);
+}
+
+/* y-momentum row at vy(i,j) (reading R2): "the same procedure is applied":
+ *   (sxx -> syy) d(syy)/dy with syy(P(i,j)) = 2 etaP(i,j) (vy(i,j)-vy(i-1,j))/dy,
+ *   d(sxy)/dx with sxy(B(i,j)) = etaB(i,j) ((vx(i+1,j)-vx(i,j))/dy + (vy(i,j+1)-vy(i,j))/dx)
+ *   (PAPER.md:643-661).  Written as the stress differences, not as coefficients, so the
+ *   dense pin P1 (coefficients assembled in numpy) is an independent check. */
+static double Ly_point(const olevel *L, const double *vx, const double *vy, int i, int j) {
+    double dx = L->dx, dy = L->dy;
+    double syy_S = 2.0 * L->etap[IX(L, i + 1, j)] * (vy[IX(L, i + 1, j)] - vy[IX(L, i, j)]) / dy;
+    double syy_N = 2.0 * L->etap[IX(L, i, j)] * (vy[IX(L, i, j)] - vy[IX(L, i - 1, j)]) / dy;
+    double sxy_E = L->etab[IX(L, i, j)] *
+                   ((vx[IX(L, i + 1, j)] - vx[IX(L, i, j)]) / dy + (vy[IX(L, i, j + 1)] - vy[IX(L, i, j)]) / dx);
+    double sxy_W = L->etab[IX(L, i, j - 1)] *
+                   ((vx[IX(L, i + 1, j - 1)] - vx[IX(L, i, j - 1)]) / dy +
+                    (vy[IX(L, i, j)] - vy[IX(L, i, j - 1)]) / dx);
+    return (syy_S - syy_N) / dy + (sxy_E - sxy_W) / dx;
+}
+static double Ly_center(const olevel *L, int i, int j) {
+    double dx = L->dx, dy = L->dy;
+    double etaN = L->etap[IX(L, i, j)], etaS = L->etap[IX(L, i + 1, j)];
+    double etaW = L->etab[IX(L, i, j - 1)], etaE = L->etab[IX(L, i, j)];
+    return -2.0 * (etaN + etaS) / (dy * dy) - (etaW + etaE) / (dx * dx);
+}
+/* Diagonal a_ii of the velocity block L of the linear system (reading R5): the centre
+ * coefficient plus, for a row adjacent to a mirror node, the mirror's coefficient times
+ * the mirror sign s (the mirror is s times this very unknown).  This is the
+ * a_ii of Eq. jacobi_update and the diag(-L) of PAPER.md:1615. */
+static double Lx_diag(const oracle_t *S, const olevel *L, int i, int j) {
+    double a = Lx_center(L, i, j);
+    if (i == 1) a += sgn_of(S->bc[2]) * L->etab[IX(L, i - 1, j)] / (L->dy * L->dy);
+    if (i == L->ncy) a += sgn_of(S->bc[3]) * L->etab[IX(L, i, j)] / (L->dy * L->dy);
+    return a;
+}
+static double Ly_diag(const oracle_t *S, const olevel *L, int i, int j) {
+    double a = Ly_center(L, i, j);
+    if (j == 1) a += sgn_of(S->bc[0]) * L->etab[IX(L, i, j - 1)] / (L->dx * L->dx);
+    if (j == L->ncx) a += sgn_of(S->bc[1]) * L->etab[IX(L, i, j)] / (L->dx * L->dx);
+    return a;
+}
+/* G p = -grad_h p (Eq. gradient_discrete); pressure terms of the Listing. */
+static double Gx_point(const olevel *L, const double *p, int i, int j) {
+    return -p[IX(L, i, j + 1)] / L->dx + p[IX(L, i, j)] / L->dx;
+}
+static double Gy_point(const olevel *L, const double *p, int i, int j) {
+    return -p[IX(L, i + 1, j)] / L->dy + p[IX(L, i, j)] / L->dy;
+}
+/* D v = div_h v (Eq. divergence_discrete; SPEC continuity_apply). */
+static double D_point(const olevel *L, const double *vx, const double *vy, int i, int j) {
+    return (vx[IX(L, i, j)] - vx[IX(L, i, j - 1)]) / L->dx + (vy[IX(L, i, j)] - vy[IX(L, i - 1, j)]) / L->dy;
+}
+
+/* index ranges of unknowns (Listing loop bounds PAPER.md:2352-2353, reading R1) */
+#define FOR_VX(L) for (int i = 1; i <= (L)->ncy; ++i) for (int j = 1; j <= (L)->ncx - 1; ++j)
+#define FOR_VY(L) for (int i = 1; i <= (L)->ncy - 1; ++i) for (int j = 1; j <= (L)->ncx; ++j)
+#define FOR_P(L) for (int i = 1; i <= (L)->ncy; ++i) for (int j = 1; j <= (L)->ncx; ++j)
+
+/* r = b - L v on unknowns (mirrors of v must be current); Eq. mg_residual */
+static void residual_v(const olevel *L, const double *vx, const double *vy, const double *bx, const double *by,
+                       double *rx, double *ry) {
+    memset(rx, 0, padn(L) * sizeof(double));
+    memset(ry, 0, padn(L) * sizeof(double));
+    FOR_VX(L) rx[IX(L, i, j)] = bx[IX(L, i, j)] - Lx_point(L, vx, vy, i, j);
+    FOR_VY(L) ry[IX(L, i, j)] = by[IX(L, i, j)] - Ly_point(L, vx, vy, i, j);
+}
+
+/* ------------------------------------------------ smoothers (a4)
+ * Damped Jacobi, Eq. damped_jacobi: x_i <- x_i + w (b - A x)_i / a_ii,
+ * all reads from the old iterate; a_ii = diagonal of L (reading R5). */
+static void smooth_jacobi(const oracle_t *S, olevel *L, double *vx, double *vy, const double *bx,
+                          const double *by, int nu) {
+    double w = S->o.omega_v;
+    for (int s = 0; s < nu; ++s) {
+        residual_v(L, vx, vy, bx, by, L->tx, L->ty);
+        FOR_VX(L) vx[IX(L, i, j)] += w * L->tx[IX(L, i, j)] / Lx_diag(S, L, i, j);
+        FOR_VY(L) vy[IX(L, i, j)] += w * L->ty[IX(L, i, j)] / Ly_diag(S, L, i, j);
+        refresh_mirrors(S, L, vx, vy);
+    }
+}
+/* Damped red-black Gauss-Seidel, Eq. sor_update, reading R11: four phases
+ * (vx,red)(vx,black)(vy,red)(vy,black), red = (i+j) even on global indices; within a
+ * phase each unknown is updated serially in row-major order with current values. */
+static void smooth_rbgs(const oracle_t *S, olevel *L, double *vx, double *vy, const double *bx,
+                        const double *by, int nu) {
+    double w = S->o.omega_v;
+    for (int s = 0; s < nu; ++s) {
+        for (int colour = 0; colour < 2; ++colour) {
+            FOR_VX(L) if (((i + j) & 1) == colour) {
+                double r = bx[IX(L, i, j)] - Lx_point(L, vx, vy, i, j);
+                vx[IX(L, i, j)] += w * r / Lx_diag(S, L, i, j);
+            }
+            refresh_mirrors(S, L, vx, vy);
+        }
+        for (int colour = 0; colour < 2; ++colour) {
+            FOR_VY(L) if (((i + j) & 1) == colour) {
+                double r = by[IX(L, i, j)] - Ly_point(L, vx, vy, i, j);
+                vy[IX(L, i, j)] += w * r / Ly_diag(S, L, i, j);
+            }
+            refresh_mirrors(S, L, vx, vy);
+        }
+    }
+}
+static void smooth(const oracle_t *S, olevel *L, double *vx, double *vy, const double *bx, const double *by,
+                   int nu) {
+    if (S->o.smoother == 1) smooth_rbgs(S, L, vx, vy, bx, by, nu);
+    else smooth_jacobi(S, L, vx, vy, bx, by, nu);
+}
+
+/* ------------------------------------------------ transfers (a5, a6, a7)
+ * Node types: position of index (i,j) in units of the spacing is (j + ox, i + oy):
+ *   basic (0,0), vx (0,-1/2), vy (-1/2,0), P (-1/2,-1/2)  (PAPER.md:615 lower-right rule). */
+enum { T_VX = 0, T_VY = 1, T_P = 2, T_B = 3 };
+static void type_offsets(int t, double *ox, double *oy) {
+    *ox = (t == T_VY || t == T_P) ? -0.5 : 0.0;
+    *oy = (t == T_VX || t == T_P) ? -0.5 : 0.0;
+}
+/* index ranges of the nodes of type t "inside the closed domain" (reading R6):
+ * unknowns and wall nodes; mirror/ghost nodes excluded. */
+static void type_range(int t, int ncx, int ncy, int *i0, int *i1, int *j0, int *j1) {
+    switch (t) {
+    case T_VX: *i0 = 1; *i1 = ncy; *j0 = 0; *j1 = ncx; break;
+    case T_VY: *i0 = 0; *i1 = ncy; *j0 = 1; *j1 = ncx; break;
+    case T_P: *i0 = 1; *i1 = ncy; *j0 = 1; *j1 = ncx; break;
+    default: *i0 = 0; *i1 = ncy; *j0 = 0; *j1 = ncx; break;
+    }
+}
+static double hat(double d, double H) { /* bilinear weight, Alg. 2: w = (1-|r_x|)(1-|r_y|) */
+    double r = fabs(d) / H;
+    return r < 1.0 ? 1.0 - r : 0.0;
+}
+/* Normalised bilinear restriction (Alg. 2 weights, reading R6):
+ *   u^H(I,J) = sum_p w_Ip u^h(p) / sum_p w_Ip,  w = hat_H(dx) hat_H(dy),
+ * over fine nodes p of the same type inside the closed domain; each fine node counted once.
+ * Writes coarse nodes in [ci0,ci1]x[cj0,cj1]. */
+static void restrict_generic(const olevel *F, const olevel *C, int t, const double *uf, double *uc, int ci0,
+                             int ci1, int cj0, int cj1) {
+    double ox, oy;
+    type_offsets(t, &ox, &oy);
+    int i0, i1, j0, j1;
+    type_range(t, F->ncx, F->ncy, &i0, &i1, &j0, &j1);
+    double Hx = C->dx, Hy = C->dy;
+    for (int I = ci0; I <= ci1; ++I)
+        for (int J = cj0; J <= cj1; ++J) {
+            double X = (J + ox) * Hx, Y = (I + oy) * Hy;
+            double num = 0.0, den = 0.0;
+            /* candidate fine nodes: |x - X| < Hx  <=>  j within a window around 2J */
+            for (int i = 2 * I - 3; i <= 2 * I + 3; ++i) {
+                if (i < i0 || i > i1) continue;
+                double wy = hat((i + oy) * F->dy - Y, Hy);
+                if (wy == 0.0) continue;
+                for (int j = 2 * J - 3; j <= 2 * J + 3; ++j) {
+                    if (j < j0 || j > j1) continue;
+                    double wx = hat((j + ox) * F->dx - X, Hx);
+                    if (wx == 0.0) continue;
+                    double w = wx * wy;
+                    num += w * uf[IX(F, i, j)];
+                    den += w;
+                }
+            }
+            uc[IX(C, I, J)] = num / den;
+        }
+}
+/* Bilinear prolongation: each fine node receives the hat-weighted sum of
+ * the surrounding coarse nodes of the same type, coarse mirror nodes holding the
+ * homogeneous-BC image and wall nodes zero (reading R6/Appendix B).  u_f += P u_c. */
+static void prolong_add(const olevel *F, const olevel *C, int t, const double *uc, double *uf) {
+    double ox, oy;
+    type_offsets(t, &ox, &oy);
+    int fi0, fi1, fj0, fj1;
+    if (t == T_VX) { fi0 = 1; fi1 = F->ncy; fj0 = 1; fj1 = F->ncx - 1; }
+    else { fi0 = 1; fi1 = F->ncy - 1; fj0 = 1; fj1 = F->ncx; }
+    for (int i = fi0; i <= fi1; ++i)
+        for (int j = fj0; j <= fj1; ++j) {
+            double x = (j + ox) * F->dx, y = (i + oy) * F->dy;
+            double s = 0.0;
+            for (int I = i / 2 - 2; I <= i / 2 + 2; ++I) {
+                if (I < 0 || I > C->ncy + 1) continue;
+                double wy = hat((I + oy) * C->dy - y, C->dy);
+                if (wy == 0.0) continue;
+                for (int J = j / 2 - 2; J <= j / 2 + 2; ++J) {
+                    if (J < 0 || J > C->ncx + 1) continue;
+                    double wx = hat((J + ox) * C->dx - x, C->dx);
+                    if (wx == 0.0) continue;
+                    s += wx * wy * uc[IX(C, I, J)];
+                }
+            }
+            uf[IX(F, i, j)] += s;
+        }
+}
+
+/* ------------------------------------------------ coarsest solve (a8, reading R10)
+ * Dense -L_c with the mirror relations folded in (the true operator), Cholesky. */
+static int nunk(const olevel *L) { return L->ncy * (L->ncx - 1) + (L->ncy - 1) * L->ncx; }
+static void pack_unknowns(const olevel *L, const double *vx, const double *vy, double *u) {
+    int k = 0;
+    FOR_VX(L) u[k++] = vx[IX(L, i, j)];
+    FOR_VY(L) u[k++] = vy[IX(L, i, j)];
+}
+static void unpack_unknowns(const olevel *L, const double *u, double *vx, double *vy) {
+    int k = 0;
+    FOR_VX(L) vx[IX(L, i, j)] = u[k++];
+    FOR_VY(L) vy[IX(L, i, j)] = u[k++];
+}
+static int build_coarse_direct(oracle_t *S) {
+    olevel *L = &S->lev[S->nlev - 1];
+    int n = nunk(L);
+    S->nc = n;
+    free(S->chol);
+    S->chol = zalloc((size_t)n * n);
+    double *e = zalloc(n), *vx = zalloc(padn(L)), *vy = zalloc(padn(L)), *col = zalloc(n);
+    double *ax = zalloc(padn(L)), *ay = zalloc(padn(L)), *zero = zalloc(padn(L));
+    for (int c = 0; c < n; ++c) {
+        memset(e, 0, n * sizeof(double));
+        e[c] = 1.0;
+        memset(vx, 0, padn(L) * sizeof(double));
+        memset(vy, 0, padn(L) * sizeof(double));
+        unpack_unknowns(L, e, vx, vy);
+        refresh_mirrors(S, L, vx, vy);
+        residual_v(L, vx, vy, zero, zero, ax, ay); /* = -L e */
+        pack_unknowns(L, ax, ay, col);
+        for (int r = 0; r < n; ++r) S->chol[(size_t)r * n + c] = col[r];
+    }
+    /* symmetrise against rounding of the two equal off-diagonal formulas */
+    for (int r = 0; r < n; ++r)
+        for (int c = 0; c < r; ++c) {
+            double a = 0.5 * (S->chol[(size_t)r * n + c] + S->chol[(size_t)c * n + r]);
+            S->chol[(size_t)r * n + c] = a;
+            S->chol[(size_t)c * n + r] = a;
+        }
+    /* in-place Cholesky, lower triangle */
+    int ok = 1;
+    for (int j = 0; j < n && ok; ++j) {
+        double d = S->chol[(size_t)j * n + j];
+        for (int k = 0; k < j; ++k) d -= S->chol[(size_t)j * n + k] * S->chol[(size_t)j * n + k];
+        if (!(d > 0.0)) { ok = 0; break; }
+        d = sqrt(d);
+        S->chol[(size_t)j * n + j] = d;
+        for (int i = j + 1; i < n; ++i) {
+            double s = S->chol[(size_t)i * n + j];
+            for (int k = 0; k < j; ++k) s -= S->chol[(size_t)i * n + k] * S->chol[(size_t)j * n + k];
+            S->chol[(size_t)i * n + j] = s / d;
+        }
+    }
+    free(e); free(vx); free(vy); free(col); free(ax); free(ay); free(zero);
+    return ok ? 0 : -1;
+}
+/* solve L_c v = b, i.e. (-L_c) v = -b */
+static void coarse_direct_solve(const oracle_t *S, olevel *L, double *vx, double *vy, const double *bx,
+                                const double *by) {
+    int n = S->nc;
+    double *u = zalloc(n);
+    pack_unknowns(L, bx, by, u);
+    for (int k = 0; k < n; ++k) u[k] = -u[k];
+    for (int i = 0; i < n; ++i) { /* forward */
+        double s = u[i];
+        for (int k = 0; k < i; ++k) s -= S->chol[(size_t)i * n + k] * u[k];
+        u[i] = s / S->chol[(size_t)i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) { /* backward */
+        double s = u[i];
+        for (int k = i + 1; k < n; ++k) s -= S->chol[(size_t)k * n + i] * u[k];
+        u[i] = s / S->chol[(size_t)i * n + i];
+    }
+    unpack_unknowns(L, u, vx, vy);
+    refresh_mirrors(S, L, vx, vy);
+    free(u);
+}
+
+/* ------------------------------------------------ V-cycle (a9), Eq. multigrid_levels */
+static void vcycle_level(oracle_t *S, int l, double *vx, double *vy, const double *bx, const double *by) {
+    olevel *L = &S->lev[l];
+    if (l == S->nlev - 1) {
+        if (S->o.coarse_direct) coarse_direct_solve(S, L, vx, vy, bx, by);
+        else smooth(S, L, vx, vy, bx, by, 2 * L->nu);
+        return;
+    }
+    olevel *C = &S->lev[l + 1];
+    smooth(S, L, vx, vy, bx, by, L->nu);                               /* (1) pre-smoothing */
+    residual_v(L, vx, vy, bx, by, L->rx, L->ry);                       /* (2) residual */
+    memset(C->bx, 0, padn(C) * sizeof(double));
+    memset(C->by, 0, padn(C) * sizeof(double));
+    restrict_generic(L, C, T_VX, L->rx, C->bx, 1, C->ncy, 1, C->ncx - 1); /* (3) restrict */
+    restrict_generic(L, C, T_VY, L->ry, C->by, 1, C->ncy - 1, 1, C->ncx);
+    memset(C->ex, 0, padn(C) * sizeof(double));                         /* coarse guess 0 */
+    memset(C->ey, 0, padn(C) * sizeof(double));
+    vcycle_level(S, l + 1, C->ex, C->ey, C->bx, C->by);                 /* (4) recurse */
+    refresh_mirrors(S, C, C->ex, C->ey);
+    prolong_add(L, C, T_VX, C->ex, vx);                                 /* (5) correct */
+    prolong_add(L, C, T_VY, C->ey, vy);
+    refresh_mirrors(S, L, vx, vy);
+    smooth(S, L, vx, vy, bx, by, L->nu);                               /* (6) post-smoothing */
+}
+
+/* ------------------------------------------------ energy norm (a3) */
+static void body_force(const oracle_t *S, double *fx, double *fy) {
+    const olevel *L = &S->lev[0];
+    memset(fx, 0, padn(L) * sizeof(double));
+    memset(fy, 0, padn(L) * sizeof(double));
+    /* reading R4/R23: f = -g * rho averaged to the velocity node (y down, g_y > 0 downward) */
+    FOR_VX(L) fx[IX(L, i, j)] = -S->gx * (S->rhob[IX(L, i - 1, j)] + S->rhob[IX(L, i, j)]) / 2.0;
+    FOR_VY(L) fy[IX(L, i, j)] = -S->gy * (S->rhob[IX(L, i, j - 1)] + S->rhob[IX(L, i, j)]) / 2.0;
+}
+/* weighted sums: Sv = sum r^2/d over vx then vy, d = -a_ii (diag(-L), reading R5); Sp = sum rp^2 eta/(2/dx^2+2/dy^2) */
+static double sum_vel_energy(const oracle_t *S, const olevel *L, const double *rx, const double *ry) {
+    size_t n = (size_t)nunk(L), k = 0;
+    double *t = zalloc(n);
+    FOR_VX(L) t[k++] = rx[IX(L, i, j)] * rx[IX(L, i, j)] / (-Lx_diag(S, L, i, j));
+    FOR_VY(L) t[k++] = ry[IX(L, i, j)] * ry[IX(L, i, j)] / (-Ly_diag(S, L, i, j));
+    double s = pairwise(t, n);
+    free(t);
+    return s;
+}
+static double sum_p_energy(const olevel *L, const double *rp) {
+    size_t n = (size_t)L->ncx * L->ncy, k = 0;
+    double *t = zalloc(n);
+    double c = 2.0 / (L->dx * L->dx) + 2.0 / (L->dy * L->dy);
+    FOR_P(L) t[k++] = rp[IX(L, i, j)] * rp[IX(L, i, j)] * (L->etap[IX(L, i, j)] / c);
+    double s = pairwise(t, n);
+    free(t);
+    return s;
+}
+static double p_mean(const olevel *L, const double *p) {
+    size_t n = (size_t)L->ncx * L->ncy, k = 0;
+    double *t = zalloc(n);
+    FOR_P(L) t[k++] = p[IX(L, i, j)];
+    double s = pairwise(t, n) / (double)n;
+    free(t);
+    return s;
+}
+/* full residual of the saddle system: rv = f - L v - G p, rp = 0 - D v */
+static void full_residual(const oracle_t *S, const double *vx, const double *vy, const double *p, double *rx,
+                          double *ry, double *rp) {
+    const olevel *L = &S->lev[0];
+    memset(rx, 0, padn(L) * sizeof(double));
+    memset(ry, 0, padn(L) * sizeof(double));
+    memset(rp, 0, padn(L) * sizeof(double));
+    FOR_VX(L) rx[IX(L, i, j)] = S->fx[IX(L, i, j)] - (Lx_point(L, vx, vy, i, j) + Gx_point(L, p, i, j));
+    FOR_VY(L) ry[IX(L, i, j)] = S->fy[IX(L, i, j)] - (Ly_point(L, vx, vy, i, j) + Gy_point(L, p, i, j));
+    FOR_P(L) rp[IX(L, i, j)] = -D_point(L, vx, vy, i, j);
+}
+static double energy_of(const oracle_t *S, const double *rx, const double *ry, const double *rp, double Sf) {
+    const olevel *L = &S->lev[0];
+    return sqrt((sum_vel_energy(S, L, rx, ry) + sum_p_energy(L, rp)) / Sf);
+}
+
+/* ------------------------------------------------ layout conversion (user <-> padded)
+ * user layout (no ghosts): vx ny x (nx+1), vy (ny+1) x nx, p/eta_p ny x nx, eta_b/rho_b (ny+1) x (nx+1) */
+static void in_vx(const olevel *L, const double *u, double *a) {
+    for (int i = 0; i < L->ncy; ++i)
+        for (int j = 0; j <= L->ncx; ++j) a[IX(L, i + 1, j)] = u[(size_t)i * (L->ncx + 1) + j];
+}
+static void in_vy(const olevel *L, const double *u, double *a) {
+    for (int i = 0; i <= L->ncy; ++i)
+        for (int j = 0; j < L->ncx; ++j) a[IX(L, i, j + 1)] = u[(size_t)i * L->ncx + j];
+}
+static void in_p(const olevel *L, const double *u, double *a) {
+    for (int i = 0; i < L->ncy; ++i)
+        for (int j = 0; j < L->ncx; ++j) a[IX(L, i + 1, j + 1)] = u[(size_t)i * L->ncx + j];
+}
+static void in_b(const olevel *L, const double *u, double *a) {
+    for (int i = 0; i <= L->ncy; ++i)
+        for (int j = 0; j <= L->ncx; ++j) a[IX(L, i, j)] = u[(size_t)i * (L->ncx + 1) + j];
+}
+static void out_vx(const olevel *L, const double *a, double *u) {
+    for (int i = 0; i < L->ncy; ++i)
+        for (int j = 0; j <= L->ncx; ++j)
+            u[(size_t)i * (L->ncx + 1) + j] = (j == 0 || j == L->ncx) ? 0.0 : a[IX(L, i + 1, j)];
+}
+static void out_vy(const olevel *L, const double *a, double *u) {
+    for (int i = 0; i <= L->ncy; ++i)
+        for (int j = 0; j < L->ncx; ++j)
+            u[(size_t)i * L->ncx + j] = (i == 0 || i == L->ncy) ? 0.0 : a[IX(L, i, j + 1)];
+}
+static void out_p(const olevel *L, const double *a, double *u) {
+    for (int i = 0; i < L->ncy; ++i)
+        for (int j = 0; j < L->ncx; ++j) u[(size_t)i * L->ncx + j] = a[IX(L, i + 1, j + 1)];
+}
+static void out_b(const olevel *L, const double *a, double *u) {
+    for (int i = 0; i <= L->ncy; ++i)
+        for (int j = 0; j <= L->ncx; ++j) u[(size_t)i * (L->ncx + 1) + j] = a[IX(L, i, j)];
+}
+/* velocity input: unknowns from the user array, walls zero, mirrors from their partners */
+static void in_velocity(const oracle_t *S, const olevel *L, const double *ux, const double *uy, double *vx,
+                        double *vy) {
+    memset(vx, 0, padn(L) * sizeof(double));
+    memset(vy, 0, padn(L) * sizeof(double));
+    FOR_VX(L) vx[IX(L, i, j)] = ux[(size_t)(i - 1) * (L->ncx + 1) + j];
+    FOR_VY(L) vy[IX(L, i, j)] = uy[(size_t)i * L->ncx + (j - 1)];
+    refresh_mirrors(S, L, vx, vy);
+}
+
+/* ================================================================== public API */
+#define O_OK 0
+#define O_NOT_CONVERGED 1
+#define O_EINVAL (-1)
+#define O_ENOMEM (-2)
+#define O_EDIVERGED (-5)
+#define O_ESTATE (-6)
+
+int oracle_opts_default(oracle_opts *o) {
+    if (!o) return O_EINVAL;
+    o->smoother = 0;
+    o->omega_v = 0.3;
+    o->alpha_p = 0.6;
+    o->nu1 = 5;
+    o->nu_growth = 1.0;
+    o->coarse_min = 8;
+    o->coarse_direct = 1;
+    o->vcycles_per_iter = 1;
+    o->accel = 0;
+    o->gcr_restart = 10;
+    o->max_iter = 10000;
+    o->pressure_sign = 1;
+    return O_OK;
+}
+
+static void alloc_level(olevel *L, int ncx, int ncy, double Lx, double Ly) {
+    L->ncx = ncx; L->ncy = ncy; L->W = ncx + 2;
+    L->dx = Lx / ncx; L->dy = Ly / ncy;
+    size_t n = padn(L);
+    L->etab = zalloc(n); L->etap = zalloc(n);
+    L->rx = zalloc(n); L->ry = zalloc(n); L->bx = zalloc(n); L->by = zalloc(n);
+    L->ex = zalloc(n); L->ey = zalloc(n); L->tx = zalloc(n); L->ty = zalloc(n);
+}
+
+int oracle_create(int nx, int ny, double Lx, double Ly, const int *bc, const oracle_opts *opts, oracle_t **out) {
+    if (!out || nx < 2 || ny < 2 || !(Lx > 0) || !(Ly > 0) || !bc) return O_EINVAL;
+    for (int k = 0; k < 4; ++k) if (bc[k] != 0 && bc[k] != 1) return O_EINVAL;
+    oracle_t *S = (oracle_t *)calloc(1, sizeof(oracle_t));
+    S->nx = nx; S->ny = ny; S->Lx = Lx; S->Ly = Ly;
+    memcpy(S->bc, bc, sizeof(S->bc));
+    if (opts) S->o = *opts; else oracle_opts_default(&S->o);
+    if (S->o.nu1 < 0 || S->o.coarse_min < 2 || S->o.vcycles_per_iter < 1 || S->o.gcr_restart < 1) {
+        free(S);
+        return O_EINVAL;
+    }
+    S->gx = 0.0; S->gy = 0.0;
+    /* hierarchy (reading R8): factor 2 while both even and min/2 >= coarse_min */
+    int cx = nx, cy = ny, l = 0;
+    for (;;) {
+        alloc_level(&S->lev[l], cx, cy, Lx, Ly);
+        double nu = floor(S->o.nu1 * pow(S->o.nu_growth, (double)l) + 0.5);
+        S->lev[l].nu = (int)nu;
+        ++l;
+        if (l >= MAXLEV) break;
+        if ((cx % 2) || (cy % 2)) break;
+        int m = cx < cy ? cx : cy;
+        if (m / 2 < S->o.coarse_min) break;
+        cx /= 2; cy /= 2;
+    }
+    S->nlev = l;
+    size_t n = padn(&S->lev[0]);
+    S->rhob = zalloc(n); S->fx = zalloc(n); S->fy = zalloc(n);
+    S->vx = zalloc(n); S->vy = zalloc(n); S->p = zalloc(n);
+    *out = S;
+    return O_OK;
+}
+
+int oracle_destroy(oracle_t *S) {
+    if (!S) return O_EINVAL;
+    for (int l = 0; l < S->nlev; ++l) {
+        olevel *L = &S->lev[l];
+        free(L->etab); free(L->etap); free(L->rx); free(L->ry); free(L->bx); free(L->by);
+        free(L->ex); free(L->ey); free(L->tx); free(L->ty);
+    }
+    free(S->rhob); free(S->fx); free(S->fy); free(S->vx); free(S->vy); free(S->p); free(S->chol);
+    free(S);
+    return O_OK;
+}
+
+int oracle_num_levels(const oracle_t *S) { return S ? S->nlev : O_EINVAL; }
+int oracle_level_shape(const oracle_t *S, int l, int *ncx, int *ncy, int *nu) {
+    if (!S || l < 0 || l >= S->nlev) return O_EINVAL;
+    *ncx = S->lev[l].ncx; *ncy = S->lev[l].ncy; *nu = S->lev[l].nu;
+    return O_OK;
+}
+
+static void update_force(oracle_t *S) {
+    if (!S->force_override) body_force(S, S->fx, S->fy);
+}
+
+/* set_viscosity: copies eta, builds the coarse viscosities (a7, reading R7: the same
+ * normalised bilinear restriction, arithmetic) and the coarsest factorisation (a8). */
+int oracle_set_viscosity(oracle_t *S, const double *eta_b, const double *eta_p) {
+    if (!S || !eta_b || !eta_p) return O_EINVAL;
+    olevel *F = &S->lev[0];
+    for (size_t k = 0; k < (size_t)(S->ny + 1) * (S->nx + 1); ++k) if (!(eta_b[k] > 0)) return O_EINVAL;
+    for (size_t k = 0; k < (size_t)S->ny * S->nx; ++k) if (!(eta_p[k] > 0)) return O_EINVAL;
+    in_b(F, eta_b, F->etab);
+    in_p(F, eta_p, F->etap);
+    for (int l = 0; l + 1 < S->nlev; ++l) {
+        olevel *A = &S->lev[l], *C = &S->lev[l + 1];
+        restrict_generic(A, C, T_B, A->etab, C->etab, 0, C->ncy, 0, C->ncx);
+        restrict_generic(A, C, T_P, A->etap, C->etap, 1, C->ncy, 1, C->ncx);
+    }
+    S->have_eta = 1;
+    if (S->o.coarse_direct) {
+        if (nunk(&S->lev[S->nlev - 1]) > 6000) return O_EINVAL;
+        if (build_coarse_direct(S) != 0) return O_EINVAL;
+    }
+    return O_OK;
+}
+int oracle_set_density(oracle_t *S, const double *rho_b) {
+    if (!S || !rho_b) return O_EINVAL;
+    in_b(&S->lev[0], rho_b, S->rhob);
+    S->have_rho = 1;
+    update_force(S);
+    return O_OK;
+}
+int oracle_set_gravity(oracle_t *S, double gx, double gy) {
+    if (!S) return O_EINVAL;
+    S->gx = gx; S->gy = gy;
+    update_force(S);
+    return O_OK;
+}
+/* test hook: arbitrary body force (vx / vy user layouts) -- used by the no-slip MMS pin P3 */
+int oracle_set_force(oracle_t *S, const double *fx, const double *fy) {
+    if (!S || !fx || !fy) return O_EINVAL;
+    olevel *L = &S->lev[0];
+    double *tx = zalloc(padn(L)), *ty = zalloc(padn(L));
+    in_vx(L, fx, tx); in_vy(L, fy, ty);
+    memset(S->fx, 0, padn(L) * sizeof(double));
+    memset(S->fy, 0, padn(L) * sizeof(double));
+    FOR_VX(L) S->fx[IX(L, i, j)] = tx[IX(L, i, j)];
+    FOR_VY(L) S->fy[IX(L, i, j)] = ty[IX(L, i, j)];
+    free(tx); free(ty);
+    S->force_override = 1; S->have_rho = 1;
+    return O_OK;
+}
+int oracle_get_viscosity(const oracle_t *S, int l, double *eta_b, double *eta_p) {
+    if (!S || l < 0 || l >= S->nlev || !S->have_eta) return O_EINVAL;
+    out_b(&S->lev[l], S->lev[l].etab, eta_b);
+    out_p(&S->lev[l], S->lev[l].etap, eta_p);
+    return O_OK;
+}
+
+/* apply_operator: ax, ay = L v + G p (vx/vy layouts, walls 0), ap = D v (P layout) */
+int oracle_apply_operator(oracle_t *S, const double *vx, const double *vy, const double *p, double *ax,
+                          double *ay, double *ap) {
+    if (!S || !S->have_eta) return O_ESTATE;
+    olevel *L = &S->lev[0];
+    in_velocity(S, L, vx, vy, S->vx, S->vy);
+    memset(S->p, 0, padn(L) * sizeof(double));
+    in_p(L, p, S->p);
+    double *tx = zalloc(padn(L)), *ty = zalloc(padn(L)), *tp = zalloc(padn(L));
+    FOR_VX(L) tx[IX(L, i, j)] = Lx_point(L, S->vx, S->vy, i, j) + Gx_point(L, S->p, i, j);
+    FOR_VY(L) ty[IX(L, i, j)] = Ly_point(L, S->vx, S->vy, i, j) + Gy_point(L, S->p, i, j);
+    FOR_P(L) tp[IX(L, i, j)] = D_point(L, S->vx, S->vy, i, j);
+    out_vx(L, tx, ax); out_vy(L, ty, ay); out_p(L, tp, ap);
+    free(tx); free(ty); free(tp);
+    return O_OK;
+}
+
+static double force_energy(const oracle_t *S) { return sum_vel_energy(S, &S->lev[0], S->fx, S->fy); }
+
+/* residual: rx, ry = f - L v - G p; rp = -D v; rel_energy = E */
+int oracle_residual(oracle_t *S, const double *vx, const double *vy, const double *p, double *rx, double *ry,
+                    double *rp, double *rel_energy) {
+    if (!S || !S->have_eta || !S->have_rho) return O_ESTATE;
+    olevel *L = &S->lev[0];
+    in_velocity(S, L, vx, vy, S->vx, S->vy);
+    memset(S->p, 0, padn(L) * sizeof(double));
+    in_p(L, p, S->p);
+    double *tx = zalloc(padn(L)), *ty = zalloc(padn(L)), *tp = zalloc(padn(L));
+    full_residual(S, S->vx, S->vy, S->p, tx, ty, tp);
+    if (rx) out_vx(L, tx, rx);
+    if (ry) out_vy(L, ty, ry);
+    if (rp) out_p(L, tp, rp);
+    if (rel_energy) {
+        double Sf = force_energy(S);
+        *rel_energy = Sf > 0 ? energy_of(S, tx, ty, tp, Sf) : 0.0;
+    }
+    free(tx); free(ty); free(tp);
+    return O_OK;
+}
+
+/* energy partial sums (Sv, Sp, Sf) of a residual -- exposes the reduction itself */
+int oracle_energy_sums(oracle_t *S, const double *vx, const double *vy, const double *p, double *sums3) {
+    if (!S || !S->have_eta || !S->have_rho) return O_ESTATE;
+    olevel *L = &S->lev[0];
+    in_velocity(S, L, vx, vy, S->vx, S->vy);
+    memset(S->p, 0, padn(L) * sizeof(double));
+    in_p(L, p, S->p);
+    double *tx = zalloc(padn(L)), *ty = zalloc(padn(L)), *tp = zalloc(padn(L));
+    full_residual(S, S->vx, S->vy, S->p, tx, ty, tp);
+    sums3[0] = sum_vel_energy(S, L, tx, ty);
+    sums3[1] = sum_p_energy(L, tp);
+    sums3[2] = force_energy(S);
+    free(tx); free(ty); free(tp);
+    return O_OK;
+}
+
+/* one V-cycle on L v = b (level 0); bx/by in vx/vy user layouts (walls ignored) */
+int oracle_vcycle(oracle_t *S, const double *bx, const double *by, double *vx, double *vy) {
+    if (!S || !S->have_eta) return O_ESTATE;
+    olevel *L = &S->lev[0];
+    double *pbx = zalloc(padn(L)), *pby = zalloc(padn(L));
+    in_vx(L, bx, pbx); in_vy(L, by, pby);
+    in_velocity(S, L, vx, vy, S->vx, S->vy);
+    vcycle_level(S, 0, S->vx, S->vy, pbx, pby);
+    out_vx(L, S->vx, vx); out_vy(L, S->vy, vy);
+    free(pbx); free(pby);
+    return O_OK;
+}
+
+/* test hooks on an arbitrary level l (arrays in that level's user layout) */
+int oracle_smooth(oracle_t *S, int l, const double *bx, const double *by, double *vx, double *vy, int nsweeps) {
+    if (!S || !S->have_eta || l < 0 || l >= S->nlev) return O_ESTATE;
+    olevel *L = &S->lev[l];
+    double *pbx = zalloc(padn(L)), *pby = zalloc(padn(L)), *wx = zalloc(padn(L)), *wy = zalloc(padn(L));
+    in_vx(L, bx, pbx); in_vy(L, by, pby);
+    in_velocity(S, L, vx, vy, wx, wy);
+    smooth(S, L, wx, wy, pbx, pby, nsweeps);
+    out_vx(L, wx, vx); out_vy(L, wy, vy);
+    free(pbx); free(pby); free(wx); free(wy);
+    return O_OK;
+}
+/* residual b - L v at level l (vx/vy layouts) */
+int oracle_level_residual(oracle_t *S, int l, const double *bx, const double *by, const double *vx,
+                          const double *vy, double *rx, double *ry) {
+    if (!S || !S->have_eta || l < 0 || l >= S->nlev) return O_ESTATE;
+    olevel *L = &S->lev[l];
+    double *pbx = zalloc(padn(L)), *pby = zalloc(padn(L)), *wx = zalloc(padn(L)), *wy = zalloc(padn(L));
+    double *tx = zalloc(padn(L)), *ty = zalloc(padn(L));
+    in_vx(L, bx, pbx); in_vy(L, by, pby);
+    in_velocity(S, L, vx, vy, wx, wy);
+    residual_v(L, wx, wy, pbx, pby, tx, ty);
+    out_vx(L, tx, rx); out_vy(L, ty, ry);
+    free(pbx); free(pby); free(wx); free(wy); free(tx); free(ty);
+    return O_OK;
+}
+/* restriction level l -> l+1 of a field of type t (0 vx, 1 vy, 2 P, 3 basic) */
+int oracle_restrict(oracle_t *S, int l, int t, const double *fine, double *coarse) {
+    if (!S || l < 0 || l + 1 >= S->nlev || t < 0 || t > 3) return O_EINVAL;
+    olevel *F = &S->lev[l], *C = &S->lev[l + 1];
+    double *a = zalloc(padn(F)), *b = zalloc(padn(C));
+    switch (t) {
+    case T_VX: in_vx(F, fine, a); restrict_generic(F, C, t, a, b, 1, C->ncy, 1, C->ncx - 1); out_vx(C, b, coarse); break;
+    case T_VY: in_vy(F, fine, a); restrict_generic(F, C, t, a, b, 1, C->ncy - 1, 1, C->ncx); out_vy(C, b, coarse); break;
+    case T_P: in_p(F, fine, a); restrict_generic(F, C, t, a, b, 1, C->ncy, 1, C->ncx); out_p(C, b, coarse); break;
+    default: in_b(F, fine, a); restrict_generic(F, C, t, a, b, 0, C->ncy, 0, C->ncx); out_b(C, b, coarse); break;
+    }
+    free(a); free(b);
+    return O_OK;
+}
+/* prolongation + correction: (vx,vy) at level l += P (ex,ey) from level l+1; mirrors refreshed */
+int oracle_prolong(oracle_t *S, int l, const double *ex, const double *ey, double *vx, double *vy) {
+    if (!S || l < 0 || l + 1 >= S->nlev) return O_EINVAL;
+    olevel *F = &S->lev[l], *C = &S->lev[l + 1];
+    double *cx = zalloc(padn(C)), *cy = zalloc(padn(C)), *wx = zalloc(padn(F)), *wy = zalloc(padn(F));
+    in_velocity(S, C, ex, ey, cx, cy);
+    in_velocity(S, F, vx, vy, wx, wy);
+    prolong_add(F, C, T_VX, cx, wx);
+    prolong_add(F, C, T_VY, cy, wy);
+    refresh_mirrors(S, F, wx, wy);
+    out_vx(F, wx, vx); out_vy(F, wy, vy);
+    free(cx); free(cy); free(wx); free(wy);
+    return O_OK;
+}
+/* exact coarsest-level solve L_c v = b */
+int oracle_coarse_solve(oracle_t *S, const double *bx, const double *by, double *vx, double *vy) {
+    if (!S || !S->have_eta || !S->o.coarse_direct) return O_ESTATE;
+    olevel *L = &S->lev[S->nlev - 1];
+    double *pbx = zalloc(padn(L)), *pby = zalloc(padn(L)), *wx = zalloc(padn(L)), *wy = zalloc(padn(L));
+    in_vx(L, bx, pbx); in_vy(L, by, pby);
+    coarse_direct_solve(S, L, wx, wy, pbx, pby);
+    out_vx(L, wx, vx); out_vy(L, wy, vy);
+    free(pbx); free(pby); free(wx); free(wy);
+    return O_OK;
+}
+
+/* ------------------------------------------------ solve (a10-a12) */
+static int solve_uzawa(oracle_t *S, double rtol, double Sf, double E0, int *iters, double *E_out,
+                       double *hist, int hist_len) {
+    olevel *L = &S->lev[0];
+    size_t n = padn(L);
+    double *bx = zalloc(n), *by = zalloc(n), *rx = zalloc(n), *ry = zalloc(n), *rp = zalloc(n);
+    int status = O_NOT_CONVERGED, k;
+    double E = E0;
+    for (k = 1; k <= S->o.max_iter; ++k) {
+        /* velocity subproblem L v = f - G p^k, 1 V-cycle warm-started (R15) */
+        FOR_VX(L) bx[IX(L, i, j)] = S->fx[IX(L, i, j)] - Gx_point(L, S->p, i, j);
+        FOR_VY(L) by[IX(L, i, j)] = S->fy[IX(L, i, j)] - Gy_point(L, S->p, i, j);
+        for (int c = 0; c < S->o.vcycles_per_iter; ++c) vcycle_level(S, 0, S->vx, S->vy, bx, by);
+        /* pressure update, reading R3: p += alpha eta_P r_p, r_p = -D v^{k+1} */
+        FOR_P(L) {
+            double r = -D_point(L, S->vx, S->vy, i, j);
+            S->p[IX(L, i, j)] += S->o.pressure_sign * S->o.alpha_p * L->etap[IX(L, i, j)] * r;
+        }
+        /* nullspace: subtract the arithmetic mean */
+        double m = p_mean(L, S->p);
+        FOR_P(L) S->p[IX(L, i, j)] -= m;
+        /* energy residual of the new (v, p) (reading R17) */
+        full_residual(S, S->vx, S->vy, S->p, rx, ry, rp);
+        E = energy_of(S, rx, ry, rp, Sf);
+        if (hist && k - 1 < hist_len) hist[k - 1] = E;
+        if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = O_EDIVERGED; break; }
+        if (E <= rtol) { status = O_OK; break; }
+    }
+    if (k > S->o.max_iter) k = S->o.max_iter;
+    *iters = k;
+    *E_out = E;
+    free(bx); free(by); free(rx); free(ry); free(rp);
+    return status;
+}
+
+/* Flexible GCR(m) with MGS, Alg. 4, readings R13/R14.
+ * Vectors are x = (vx, vy, p) on the unknowns; <.,.> Euclidean over unknowns (vx, vy, p). */
+typedef struct { double *x, *y, *p; } ovec;
+static ovec ovec_new(size_t n) { ovec v = {zalloc(n), zalloc(n), zalloc(n)}; return v; }
+static void ovec_free(ovec v) { free(v.x); free(v.y); free(v.p); }
+static double ovec_dot(const olevel *L, ovec a, ovec b) {
+    size_t n = (size_t)nunk(L) + (size_t)L->ncx * L->ncy, k = 0;
+    double *t = zalloc(n);
+    FOR_VX(L) t[k++] = a.x[IX(L, i, j)] * b.x[IX(L, i, j)];
+    FOR_VY(L) t[k++] = a.y[IX(L, i, j)] * b.y[IX(L, i, j)];
+    FOR_P(L) t[k++] = a.p[IX(L, i, j)] * b.p[IX(L, i, j)];
+    double s = pairwise(t, n);
+    free(t);
+    return s;
+}
+static void ovec_axpy(const olevel *L, double a, ovec x, ovec y) { /* y += a x */
+    FOR_VX(L) y.x[IX(L, i, j)] += a * x.x[IX(L, i, j)];
+    FOR_VY(L) y.y[IX(L, i, j)] += a * x.y[IX(L, i, j)];
+    FOR_P(L) y.p[IX(L, i, j)] += a * x.p[IX(L, i, j)];
+}
+static void ovec_scale(const olevel *L, double a, ovec x) {
+    FOR_VX(L) x.x[IX(L, i, j)] *= a;
+    FOR_VY(L) x.y[IX(L, i, j)] *= a;
+    FOR_P(L) x.p[IX(L, i, j)] *= a;
+}
+/* z = M^-1 r: dv = Vcycle(0; r_v), dp = alpha eta_P (r_p - D dv), de-mean dp (R3, R14) */
+static void apply_precond(oracle_t *S, ovec r, ovec z) {
+    olevel *L = &S->lev[0];
+    size_t n = padn(L);
+    memset(z.x, 0, n * sizeof(double)); memset(z.y, 0, n * sizeof(double)); memset(z.p, 0, n * sizeof(double));
+    for (int c = 0; c < S->o.vcycles_per_iter; ++c) vcycle_level(S, 0, z.x, z.y, r.x, r.y);
+    FOR_P(L) z.p[IX(L, i, j)] = S->o.alpha_p * L->etap[IX(L, i, j)] * (r.p[IX(L, i, j)] - D_point(L, z.x, z.y, i, j));
+    double m = p_mean(L, z.p);
+    FOR_P(L) z.p[IX(L, i, j)] -= m;
+}
+/* w = A z = [L z_v + G z_p; D z_v] (z mirrors current) */
+static void apply_A(oracle_t *S, ovec z, ovec w) {
+    olevel *L = &S->lev[0];
+    size_t n = padn(L);
+    memset(w.x, 0, n * sizeof(double)); memset(w.y, 0, n * sizeof(double)); memset(w.p, 0, n * sizeof(double));
+    FOR_VX(L) w.x[IX(L, i, j)] = Lx_point(L, z.x, z.y, i, j) + Gx_point(L, z.p, i, j);
+    FOR_VY(L) w.y[IX(L, i, j)] = Ly_point(L, z.x, z.y, i, j) + Gy_point(L, z.p, i, j);
+    FOR_P(L) w.p[IX(L, i, j)] = D_point(L, z.x, z.y, i, j);
+}
+static int solve_gcr(oracle_t *S, double rtol, double Sf, double E0, int *iters, double *E_out, double *hist,
+                     int hist_len) {
+    olevel *L = &S->lev[0];
+    size_t n = padn(L);
+    int m = S->o.gcr_restart;
+    ovec r = ovec_new(n), xv = {S->vx, S->vy, S->p};
+    ovec *z = (ovec *)calloc(m, sizeof(ovec)), *w = (ovec *)calloc(m, sizeof(ovec));
+    for (int k = 0; k < m; ++k) { z[k] = ovec_new(n); w[k] = ovec_new(n); }
+    full_residual(S, S->vx, S->vy, S->p, r.x, r.y, r.p); /* r0 = b - A x0 */
+    int k = 0, status = O_NOT_CONVERGED;
+    double E = E0;
+    while (k < S->o.max_iter && status == O_NOT_CONVERGED) {
+        for (int i = 0; i < m && k < S->o.max_iter; ++i) {
+            apply_precond(S, r, z[i]);
+            refresh_mirrors(S, L, z[i].x, z[i].y);
+            apply_A(S, z[i], w[i]);
+            for (int j = 0; j < i; ++j) { /* modified Gram-Schmidt */
+                double g = ovec_dot(L, w[i], w[j]);
+                ovec_axpy(L, -g, w[j], w[i]);
+                ovec_axpy(L, -g, z[j], z[i]);
+            }
+            double nu = sqrt(ovec_dot(L, w[i], w[i]));
+            double rn = sqrt(ovec_dot(L, r, r));
+            ++k;
+            if (!(nu > 1e-14 * rn)) { status = O_EDIVERGED; break; } /* breakdown (R13) */
+            ovec_scale(L, 1.0 / nu, w[i]);
+            ovec_scale(L, 1.0 / nu, z[i]);
+            double beta = ovec_dot(L, r, w[i]);
+            ovec_axpy(L, beta, z[i], xv);
+            ovec_axpy(L, -beta, w[i], r);
+            E = energy_of(S, r.x, r.y, r.p, Sf);
+            if (hist && k - 1 < hist_len) hist[k - 1] = E;
+            if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = O_EDIVERGED; break; }
+            if (E <= rtol) { status = O_OK; break; }
+        }
+    }
+    refresh_mirrors(S, L, S->vx, S->vy);
+    *iters = k;
+    *E_out = E;
+    for (int q = 0; q < m; ++q) { ovec_free(z[q]); ovec_free(w[q]); }
+    free(z); free(w); ovec_free(r);
+    return status;
+}
+
+/* solve(rtol): in = initial guess (v, p), out = solution; zero-mean p on exit.
+ * iters = number of V-cycle applications ("preconditioner applications" in GCR mode).
+ * hist (optional): E after every iteration. */
+int oracle_solve_hist(oracle_t *S, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy,
+                      double *hist, int hist_len) {
+    if (!S || !iters || !rel_energy) return O_EINVAL;
+    if (!S->have_eta || !S->have_rho) return O_ESTATE;
+    olevel *L = &S->lev[0];
+    size_t n = padn(L);
+    in_velocity(S, L, vx, vy, S->vx, S->vy);
+    memset(S->p, 0, n * sizeof(double));
+    in_p(L, p, S->p);
+    double Sf = force_energy(S);
+    if (!(Sf > 0)) { /* f == 0: zero solution, 0 iterations */
+        for (size_t k = 0; k < (size_t)S->ny * (S->nx + 1); ++k) vx[k] = 0.0;
+        for (size_t k = 0; k < (size_t)(S->ny + 1) * S->nx; ++k) vy[k] = 0.0;
+        for (size_t k = 0; k < (size_t)S->ny * S->nx; ++k) p[k] = 0.0;
+        *iters = 0; *rel_energy = 0.0;
+        return O_OK;
+    }
+    double *rx = zalloc(n), *ry = zalloc(n), *rp = zalloc(n);
+    full_residual(S, S->vx, S->vy, S->p, rx, ry, rp);
+    double E0 = energy_of(S, rx, ry, rp, Sf);
+    free(rx); free(ry); free(rp);
+    int status;
+    if (E0 <= rtol) { *iters = 0; *rel_energy = E0; status = O_OK; }
+    else if (S->o.accel == 1) status = solve_gcr(S, rtol, Sf, E0, iters, rel_energy, hist, hist_len);
+    else status = solve_uzawa(S, rtol, Sf, E0, iters, rel_energy, hist, hist_len);
+    double m = p_mean(L, S->p);
+    FOR_P(L) S->p[IX(L, i, j)] -= m;
+    out_vx(L, S->vx, vx); out_vy(L, S->vy, vy); out_p(L, S->p, p);
+    return status;
+}
+int oracle_solve(oracle_t *S, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy) {
+    return oracle_solve_hist(S, rtol, vx, vy, p, iters, rel_energy, NULL, 0);
+}
+
+const char *oracle_strerror(int e) {
+    switch (e) {
+    case O_OK: return "ok";
+    case O_NOT_CONVERGED: return "max_iter reached";
+    case O_EINVAL: return "invalid argument";
+    case O_ENOMEM: return "out of memory";
+    case O_EDIVERGED: return "diverged";
+    case O_ESTATE: return "call order (set_viscosity/set_density first)";
+    default: return "unknown";
+    }
+}

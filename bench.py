@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native multigrid Stokes solve (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload layered] [--impl ours|reference]
+
+metric  "Stokes MG solve time & DOF-sweeps/s to 1e-8 rel. residual; smoother % HBM peak"
+value   whole-job DOF-sweeps/s: sum over levels of (velocity unknowns x smoother sweeps
+        executed) of one solve to E <= 1e-8, x solves x ranks / max-over-ranks device time
+step    one full solve (all of SURVEY §8(a): V-cycles, smoother, transfers, coarse solve,
+        pressure update, energy residual, stopping test) from a zero initial guess on
+        inputs resident in HBM; ms_per_step = solve time
+workload default: BASELINE configs[3], layered lithosphere/mantle viscosity, 4096 x 4096 cells
+        per GPU, plain Uzawa-MG (presets in configs/presets.json); the single-GPU config
+        the metric's "% HBM peak" part is meaningful on (inputs ~1.4 GB >> 126 MB L2).
+N > 1   (torchrun): replicas of the per-GPU problem (weak scaling, no collective) until the
+        distributed path lands -- the JSON line says "parallelism": "replicas".
+e2e     the same solve through the public API (Stokes.set_viscosity / set_density / solve)
+        with pinned HOST inputs and outputs: H2D of eta_b, eta_p, rho_b and D2H of vx, vy, p
+        inside the timed region.
+roofline the fine-level Jacobi sweep (the hot loop): algorithmic bytes
+        per launch (64 B/cell) / its CUDA-event time (stokes_time_kernel on the
+        handle's stream, live in this run) vs the measured HBM copy peak.
+--impl reference: the CPU oracle (oracle/, plain C, 1 thread) on the same workload,
+        each step one Uzawa iteration of the full-size problem (bounded sample).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Stokes MG solve time & DOF-sweeps/s to 1e-8 rel. residual; smoother % HBM peak"
+UNIT = "DOF-sweeps/s"
+WORKLOAD_DOC = {
+    "mms": "cfg1 32x32 manufactured solution, eta=1, free slip",
+    "block": "cfg2 sinking block [3/8,5/8]^2, eta contrast 1e3, free slip",
+    "solcx": "cfg3 SolCx-like eta jump 1e6 at x=1/2, GCR(10)+MG",
+    "layered": "cfg4 layered lithosphere/mantle eta (1e3/1/30), 4096x4096 cells per GPU, Uzawa-MG",
+    "random": "cfg5 random log-perturbed eta in [0.1,10]",
+}
+
+
+def presets():
+    return json.load(open(os.path.join(ROOT, "configs", "presets.json")))
+
+
+def dof_sweeps_per_vcycle(level_shapes, smoother):
+    """sum over non-coarsest levels of velocity unknowns x (pre + post) sweeps."""
+    tot = 0
+    for (nx, ny, nu) in level_shapes[:-1]:
+        tot += (ny * (nx - 1) + (ny - 1) * nx) * 2 * nu
+    return tot
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.p is None:
+            return
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                self.rows.append(f)
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower().startswith("active")})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded or sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peak():
+    try:
+        m = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel_bytes_key):
+    """DRAM bytes per launch of the Jacobi sweep from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_jacobi_traffic.json")
+    try:
+        d = json.load(open(path))
+        return d.get(kernel_bytes_key)
+    except Exception:
+        return None
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x, world, device):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline(name, pre):
+    """The oracle as it stands on this host's cores, bounded sample: one Uzawa iteration
+    (1 V-cycle + pressure update + energy residual) of the full-size problem."""
+    from oracle.oracle import Oracle
+    from synth.fields import workload
+    nx, ny = pre["n"]
+    w = workload(name, nx, ny)
+    o = Oracle(nx, ny, w["Lx"], w["Ly"], w["bc"], **dict(pre["opts"], max_iter=1))
+    o.set_viscosity(w["eta_b"], w["eta_p"])
+    o.set_density(w["rho_b"])
+    o.set_gravity(w["gx"], w["gy"])
+    shp = [o.level_shape(l) for l in range(o.nlev)]
+    t0 = time.perf_counter()
+    r = o.solve(0.0)
+    dt = time.perf_counter() - t0
+    dofs = dof_sweeps_per_vcycle(shp, pre["opts"].get("smoother", 0)) * r["iters"]
+    return {"value": dofs / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"1 Uzawa iteration (V-cycle + p-update + energy residual) of {name} {nx}x{ny}, "
+                      f"{dt:.2f} s on 1 thread of {os.cpu_count()} ({_cpu_model()})"}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown CPU"
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    pre = presets()[args.workload]
+    vals = []
+    for k in range(args.warmup + args.steps):
+        cb = cpu_baseline(args.workload, pre)
+        if k >= args.warmup:
+            vals.append(cb["value"])
+    v = statistics.mean(vals)
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {WORKLOAD_DOC[args.workload]}", "grid": pre["n"],
+                       "sample": "each step = 1 Uzawa iteration of the full-size problem on the CPU oracle"},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_2603_14040_b200 import Stokes
+    from synth.fields import workload
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pre = presets()[args.workload]
+    nx, ny = pre["n"]
+    rtol = pre["rtol"]
+    w = workload(args.workload, nx, ny)
+    s = Stokes(nx, ny, w["Lx"], w["Ly"], w["bc"], **pre["opts"])
+    eb, ep, rho = (torch.from_numpy(w[k]).to(dev) for k in ("eta_b", "eta_p", "rho_b"))
+    s.set_viscosity(eb, ep)
+    s.set_density(rho)
+    s.set_gravity(w["gx"], w["gy"])
+    shp = [s.level_shape(l) for l in range(s.num_levels)]
+    per_vc = dof_sweeps_per_vcycle(shp, pre["opts"].get("smoother", 0))
+    vpi = pre["opts"].get("vcycles_per_iter", 1)
+    stream = s.stream
+
+    for _ in range(args.warmup):
+        r = s.solve(rtol)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = []
+    s.launch_count(reset=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = s.solve(rtol)
+            iters.append(r["iters"])
+            assert r["status"] == 0, f"solve status {r['status']}"
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = s.launch_count()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    ms_max = allreduce_max(ms, world, dev)
+    dofs_rank = sum(iters) * vpi * per_vc
+    value = dofs_rank * world / (ms_max / 1e3)
+
+    # ---- e2e through the public API with pinned host buffers
+    host = {k: torch.from_numpy(w[k]).pin_memory() for k in ("eta_b", "eta_p", "rho_b")}
+    from paper_2603_14040_b200.stokes import shapes
+    sh = shapes(nx, ny)
+    hz = {k: torch.zeros(sh[k], dtype=torch.float64).pin_memory() for k in ("vx", "vy", "p")}
+    hout = {k: torch.empty(sh[k], dtype=torch.float64).pin_memory() for k in ("vx", "vy", "p")}
+    h2d = sum(t.numel() * 8 for t in host.values()) + sum(t.numel() * 8 for t in hz.values())
+    d2h = sum(t.numel() * 8 for t in hout.values())
+    barrier(world)
+    torch.cuda.synchronize()
+    e2 = []
+    e2_iters = 0
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        s.set_viscosity(host["eta_b"], host["eta_p"])
+        s.set_density(host["rho_b"])
+        r = s.solve(rtol, vx=hz["vx"], vy=hz["vy"], p=hz["p"], out=hout)
+        torch.cuda.synchronize()
+        e2.append(time.perf_counter() - t0)
+        e2_iters += r["iters"]
+    e2_t = allreduce_max(sum(e2), world, dev)
+    e2e_value = e2_iters * vpi * per_vc * world / e2_t
+
+    # ---- roofline of the dominant kernel (fine Jacobi sweep), live CUDA events
+    k_ms, k_bytes = s.time_kernel("jacobi", reps=20)
+    peak, peak_src = measured_peak()
+    achieved = k_bytes / (k_ms / 1e3) / 1e9
+    sweeps_per_solve = statistics.mean(iters) * vpi * 2 * shp[0][2]
+    share = sweeps_per_solve * k_ms / (ms / args.steps)
+    tr = ncu_traffic("dram_bytes_per_launch")
+
+    if rank != 0:
+        return 0
+    cb = cpu_baseline(args.workload, pre) if world == 1 and not args.no_cpu_baseline else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {WORKLOAD_DOC[args.workload]}", "grid_per_gpu": [nx, ny],
+                   "levels": [list(x) for x in shp], "opts": pre["opts"], "rtol": rtol,
+                   "iters_per_solve": statistics.mean(iters), "solve_ms": ms_max / args.steps,
+                   "dof_sweeps_per_solve": dofs_rank / args.steps,
+                   "l2": "inputs larger than L2 (fine fields 16.8M cells x 8 B, hierarchy > 1 GB vs 126 MB L2)",
+                   "parallelism": "replicas" if world > 1 else "single GPU"},
+        "roofline": {"kernel": "fine-level damped-Jacobi sweep (k_jacobi)", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": tr,
+                     "algorithmic_bytes_per_launch": k_bytes, "launch_ms": k_ms, "peak_source": peak_src,
+                     "share_of_step": share},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "seconds_per_step": e2_t / len(e2)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if cb is not None:
+        line["cpu_baseline"] = cb
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="layered", choices=sorted(WORKLOAD_DOC))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    world, rank, local = dist_init(args)
+    try:
+        if args.impl == "reference":
+            return run_reference(args, world, rank)
+        return run_ours(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,183 @@
+/*
+ * include/stokes.h -- C ABI of the B200-native matrix-free multigrid Stokes solver
+ * (paper_2603_14040_b200, library libstokes_b200.so).
+ *
+ * Problem (PAPER.md:262-291 Eqs. xmom/ymom/mass, PAPER.md:716-741 Eq. stokes_saddle):
+ * given a box [0,Lx]x[0,Ly] (y pointing DOWN), per-side boundary conditions, viscosity
+ * on basic nodes (eta_b) and on pressure nodes (eta_p), density on basic nodes (rho_b)
+ * and gravity (gx, gy), find the velocity v = (vx, vy) and the zero-mean pressure p with
+ *      [ L  G ] [v]   [f]        L v = div_h(eta (grad_h v + grad_h v^T))
+ *      [ D  0 ] [p] = [0],       G p = -grad_h p,  D v = div_h v
+ * on the fully staggered grid of PAPER.md:611-624 with the stress-conservative finite
+ * differences of PAPER.md:626-661 (x row = Listing vx_op_point).
+ * Body force f = -g * rho averaged to the velocity node (reading R4/R23).
+ * Method: inexact Uzawa (sign reading R3) with geometric-multigrid
+ * V-cycle velocity solves, optionally accelerated by flexible
+ * GCR(m); stopping test = relative energy residual E
+ * (PAPER.md:1696-1701).  All arithmetic is IEEE FP64 on the GPU.
+ *
+ * ---------------------------------------------------------------- conventions
+ * Sizes: nx x ny CELLS (reading R1: the paper's n_x, n_y count basic nodes = cells + 1).
+ * Arrays: FP64, C-contiguous row-major, DEVICE pointers on the handle's GPU unless a
+ * function says HOST.  "User layout" (physical nodes only, no ghosts), cell spacing
+ * dx = Lx/nx, dy = Ly/ny:
+ *     vx    : ny x (nx+1)   vx[i][j] at (j dx, (i+1/2) dy); columns 0 and nx are walls
+ *     vy    : (ny+1) x nx   vy[i][j] at ((j+1/2) dx, i dy); rows 0 and ny are walls
+ *     p     : ny x nx       P node [i][j] at ((j+1/2) dx, (i+1/2) dy)
+ *     eta_p : ny x nx       (P nodes)
+ *     eta_b : (ny+1) x (nx+1)   basic node [i][j] at (j dx, i dy)
+ *     rho_b : (ny+1) x (nx+1)
+ * Wall entries of vx/vy inputs are IGNORED (the normal velocity on a wall is zero) and
+ * are written 0 on output.
+ * Boundary conditions bc[4] = {West, East, North(top, y=0), South(bottom, y=Ly)}, each
+ * STOKES_FREE_SLIP or STOKES_NO_SLIP; tangential mirrors of
+ * PAPER.md:613 (free slip: +mirror, no slip: -mirror).
+ * Ownership: the caller owns every array; inputs are borrowed for the duration of the
+ * call; set_* functions COPY.  The handle owns its workspace (or borrows the caller's
+ * workspace passed to stokes_create, which must outlive the handle).
+ * Streams: all device work is enqueued on the handle's stream (cudaStream_t passed as
+ * void*; NULL = legacy default stream).  Functions returning HOST scalars synchronise
+ * that stream.  A handle is not thread safe.
+ * Errors: every function returns an int status: 0 OK, >0 warning with valid outputs,
+ * <0 error (outputs undefined).  stokes_strerror() gives a message; the last CUDA/NCCL
+ * error text is available from stokes_last_error().
+ */
+#ifndef PAPER_2603_14040_B200_STOKES_H
+#define PAPER_2603_14040_B200_STOKES_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the library is built with -fvisibility=hidden */
+#endif
+
+typedef struct stokes_s *stokes_t;
+
+enum { STOKES_FREE_SLIP = 0, STOKES_NO_SLIP = 1 };
+
+enum {
+    STOKES_OK = 0,
+    STOKES_NOT_CONVERGED = 1, /* max_iter reached; outputs are the last iterate          */
+    STOKES_EINVAL = -1,       /* bad size / pointer / option / non-positive viscosity    */
+    STOKES_ENOMEM = -2,       /* device allocation failed or workspace too small         */
+    STOKES_ECUDA = -3,        /* CUDA runtime error (see stokes_last_error)               */
+    STOKES_ENCCL = -4,        /* NCCL error (distributed handles)                         */
+    STOKES_EDIVERGED = -5,    /* E non-finite or > 1e6 E0; last iterate kept */
+    STOKES_ESTATE = -6        /* call order: set_viscosity / set_density missing          */
+};
+
+enum { STOKES_SMOOTH_JACOBI = 0, STOKES_SMOOTH_RBGS = 1 };
+enum { STOKES_ACCEL_NONE = 0, STOKES_ACCEL_GCR = 1 };
+
+/* Solver options.  stokes_opts_default() fills the paper's setting (PAPER.md:1765-1788:
+ * omega_v 0.3, omega_p 0.6, 5+5 sweeps) with the readings of DESIGN.md §3 (growth g = 1,
+ * direct coarsest).  The field order is part of the ABI. */
+typedef struct {
+    int smoother;         /* STOKES_SMOOTH_JACOBI or _RBGS     */
+    double omega_v;       /* velocity relaxation omega_v                                        */
+    double alpha_p;       /* pressure relaxation alpha (= omega_p)                              */
+    int nu1;              /* pre- and post-smoothing sweeps on the finest level                 */
+    double nu_growth;     /* nu_l = floor(nu1 * g^(l-1) + 1/2)  (reading R9)      */
+    int coarse_min;       /* coarsen by 2 while both sizes even and min(nx,ny)/2 >= coarse_min  */
+    int coarse_direct;    /* 1: exact coarsest solve (reading R10); 0: 2*nu_L smoothing sweeps  */
+    int vcycles_per_iter; /* V-cycles per Uzawa step                            */
+    int accel;            /* STOKES_ACCEL_NONE (plain Uzawa) or STOKES_ACCEL_GCR                */
+    int gcr_restart;      /* m of GCR(m)                                                        */
+    int max_iter;         /* cap on iterations (V-cycle applications)                           */
+    int pressure_sign;    /* +1 physical reading R3 (default); -1 literal PAPER.md:824 (diverges) */
+} stokes_opts;
+
+/* Fill *o with the defaults.  Returns STOKES_EINVAL if o is NULL. */
+int stokes_opts_default(stokes_opts *o);
+
+/* Device workspace (bytes) stokes_create needs for an nx x ny problem with these
+ * options; *bytes written on success. */
+int stokes_workspace_bytes(int nx, int ny, const stokes_opts *opts, size_t *bytes);
+
+/* Create a single-GPU handle on the current CUDA device.
+ *   nx, ny >= 2 cells; Lx, Ly > 0; bc[4] in {0,1}; opts may be NULL (defaults);
+ *   cuda_stream: cudaStream_t as void* (NULL = default stream);
+ *   workspace: device memory of >= stokes_workspace_bytes() bytes, 256-B aligned,
+ *   owned by the caller (e.g. a torch tensor), or NULL to let the library cudaMalloc.
+ * Builds the level hierarchy (reading R8).  Errors: EINVAL, ENOMEM, ECUDA. */
+int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const stokes_opts *opts,
+                  void *cuda_stream, void *workspace, size_t workspace_bytes, stokes_t *out);
+
+/* Release the handle (and its own allocations). */
+int stokes_destroy(stokes_t h);
+
+/* Number of multigrid levels and the cell counts / sweeps of level l (0 = finest). */
+int stokes_num_levels(stokes_t h, int *nlev);
+int stokes_level_shape(stokes_t h, int level, int *nx, int *ny, int *nu);
+
+/* Copy viscosities (device, user layout eta_b (ny+1)x(nx+1), eta_p ny x nx), check
+ * eta > 0 (EINVAL otherwise, by a device min-reduction), build the coarse-level
+ * viscosities by normalised bilinear restriction (a7, reading R7)
+ * and the coarsest-level inverse (a8).  Synchronises the stream. */
+int stokes_set_viscosity(stokes_t h, const double *eta_b, const double *eta_p);
+
+/* Copy the basic-node density (device, (ny+1)x(nx+1)). */
+int stokes_set_density(stokes_t h, const double *rho_b);
+
+/* Gravity vector; f = -(gx, gy) * rho averaged to velocity nodes (y down). */
+int stokes_set_gravity(stokes_t h, double gx, double gy);
+
+/* ax, ay = L v + G p (vx / vy layouts, walls 0); ap = D v (P layout).  (a2) */
+int stokes_apply_operator(stokes_t h, const double *vx, const double *vy, const double *p, double *ax,
+                          double *ay, double *ap);
+
+/* rx, ry = f - L v - G p; rp = -D v (rx, ry, rp may be NULL); *rel_energy (HOST, may be
+ * NULL) = E = sqrt((sum r_v^2/d_v + sum r_p^2 eta_p/(2/dx^2+2/dy^2)) / sum f^2/d_v) with
+ * d_v = -a_ii (reading R5/R12); E = 0 if f == 0.  (a3) */
+int stokes_residual(stokes_t h, const double *vx, const double *vy, const double *p, double *rx, double *ry,
+                    double *rp, double *rel_energy);
+
+/* One V-cycle (a9) on L v = b, warm-started from (vx, vy) (in/out);
+ * bx, by in vx / vy layouts (walls ignored). */
+int stokes_vcycle(stokes_t h, const double *bx, const double *by, double *vx, double *vy);
+
+/* Solve to E <= rtol (a12).  vx, vy, p: in = initial guess, out = solution (p zero-mean).
+ * *iters (HOST) = number of V-cycle applications; *rel_energy (HOST) = final E.
+ * Returns OK, NOT_CONVERGED, EDIVERGED (last iterate kept) or an error. */
+int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy);
+
+/* ---- per-step entry points (parity tests of each hot-path step; same layouts at the
+ * given level's size; all device pointers) ------------------------------------------- */
+/* nsweeps smoother sweeps (a4) on level `level` for L v = b, in place on (vx, vy). */
+int stokes_smooth(stokes_t h, int level, const double *bx, const double *by, double *vx, double *vy,
+                  int nsweeps);
+/* r = b - L v on level `level`. */
+int stokes_level_residual(stokes_t h, int level, const double *bx, const double *by, const double *vx,
+                          const double *vy, double *rx, double *ry);
+/* Restriction (a5 / a7) level -> level+1 of a field of kind 0 vx, 1 vy, 2 P, 3 basic. */
+int stokes_restrict(stokes_t h, int level, int kind, const double *fine, double *coarse);
+/* (vx, vy) at `level` += P (ex, ey) from level+1, then mirror refresh (a6). */
+int stokes_prolong(stokes_t h, int level, const double *ex, const double *ey, double *vx, double *vy);
+/* Viscosities of a level as built by set_viscosity (a7). */
+int stokes_get_viscosity(stokes_t h, int level, double *eta_b, double *eta_p);
+/* Exact coarsest-level solve L_c v = b (a8); EINVAL if coarse_direct == 0. */
+int stokes_coarse_solve(stokes_t h, const double *bx, const double *by, double *vx, double *vy);
+
+/* ---- instrumentation ---------------------------------------------------------- */
+/* Number of kernels this library launched on the handle since creation / last reset. */
+int stokes_launch_count(stokes_t h, long long *count, int reset);
+/* Time `reps` back-to-back launches of a hot-path kernel on the handle's stream with CUDA
+ * events (after 2 warm-ups); *avg_ms (HOST) = mean duration of one launch, *bytes (HOST)
+ * = algorithmic bytes one launch moves.  kernel: 0 fine Jacobi sweep
+ * (Uzawa RHS), 1 fine residual+energy, 2 fine residual+restriction, 3 prolongation,
+ * 4 pressure update, 5 RBGS sweep (4 phases).  Uses the handle's current fine fields. */
+int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double *bytes);
+
+const char *stokes_strerror(int status);
+const char *stokes_last_error(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -645,7 +645,7 @@ int oracle_set_viscosity(oracle_t *S, const double *eta_b, const double *eta_p) 
     }
     S->have_eta = 1;
     if (S->o.coarse_direct) {
-        if (nunk(&S->lev[S->nlev - 1]) > 6000) return O_EINVAL;
+        if (nunk(&S->lev[S->nlev - 1]) > 1024) return O_EINVAL; /* same cap as the library */
         if (build_coarse_direct(S) != 0) return O_EINVAL;
     }
     return O_OK;

@@ -1,0 +1,870 @@
+// Host runtime of libstokes_b200: handle, level hierarchy, workspace carving, V-cycle
+// driver (a9), Uzawa loop (a10, a12), flexible GCR (a11), CUDA-graph capture, and the
+// C ABI of include/stokes.h.  Every step of the numerical path runs in kernels.cu; this
+// file only sequences launches on the handle's stream.
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+
+#include "internal.h"
+
+#define MAXLEV 24
+#define MAXM 32
+#define MAX_DIRECT 1024  // largest coarsest system solved by the explicit inverse (a8)
+
+namespace {
+
+thread_local std::string g_last_error;
+
+// device scalar slots
+enum { S_MSHIFT = 0, S_E = 1, S_SV = 2, S_SP = 3, S_SF = 4, S_SFPART = 5, S_ZMEAN = 8, S_GAMMA = 9, S_NU2 = 10,
+       S_RR = 11, S_BETA = 12, S_ZERO = 13, S_E0 = 14, S_NSCAL = 64 };
+
+struct Level {
+    GridL g;
+    double *etab, *etap;
+    double *vx[2], *vy[2];  // level 0: solution ping-pong; coarse: correction ping-pong
+    double *bx, *by;        // right-hand side
+    double *rx, *ry;        // residual scratch
+    int nu;
+};
+
+}  // namespace
+
+struct stokes_s {
+    int nx, ny;
+    double Lx, Ly;
+    int bc[4];
+    stokes_opts o;
+    cudaStream_t stream;
+    bool own_stream;
+    void *ws;
+    size_t ws_bytes;
+    bool own_ws;
+    int nlev;
+    Level lev[MAXLEV];
+    double *p, *rho;
+    double *partials;
+    size_t npart;
+    double *scal;       // device scalars
+    double *hscal;      // pinned host mirror
+    double *Minv, *Mwork;
+    int nc;
+    int *dflag;
+    // GCR vectors (fine level, padded): z_i, w_i, r, V-cycle scratch
+    double *gz[MAXM][3], *gw[MAXM][3], *gr[3], *gtmp[2];
+    bool have_eta, have_rho;
+    double gx, gy;
+    long long launches;
+    cudaGraphExec_t uzawa_exec;
+    long long uzawa_kernels;
+};
+
+namespace {
+
+int fail_cuda(cudaError_t e, const char *what) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+    g_last_error = buf;
+    return STOKES_ECUDA;
+}
+#define CK(call)                                              \
+    do {                                                      \
+        cudaError_t e_ = (call);                              \
+        if (e_ != cudaSuccess) return fail_cuda(e_, #call);   \
+    } while (0)
+#define CKL()                                                           \
+    do {                                                                \
+        cudaError_t e_ = cudaGetLastError();                            \
+        if (e_ != cudaSuccess) return fail_cuda(e_, "kernel launch");   \
+    } while (0)
+
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+GridL make_grid(int ncx, int ncy, double Lx, double Ly, const int bc[4]) {
+    GridL g;
+    g.ncx = ncx;
+    g.ncy = ncy;
+    g.P = (int)round_up((size_t)ncx + 2 + COL_OFF, 32);
+    g.dx = Lx / ncx;
+    g.dy = Ly / ncy;
+    g.idx = 1.0 / g.dx;
+    g.idy = 1.0 / g.dy;
+    g.idx2 = 1.0 / (g.dx * g.dx);
+    g.idy2 = 1.0 / (g.dy * g.dy);
+    g.idxdy = 1.0 / (g.dx * g.dy);
+    g.sW = bc[0] == STOKES_FREE_SLIP ? 1.0 : -1.0;
+    g.sE = bc[1] == STOKES_FREE_SLIP ? 1.0 : -1.0;
+    g.sN = bc[2] == STOKES_FREE_SLIP ? 1.0 : -1.0;
+    g.sS = bc[3] == STOKES_FREE_SLIP ? 1.0 : -1.0;
+    return g;
+}
+size_t field_doubles(const GridL &g) { return (size_t)(g.ncy + 2) * (size_t)g.P; }
+int n_unknowns(const GridL &g) { return g.ncy * (g.ncx - 1) + (g.ncy - 1) * g.ncx; }
+
+// hierarchy (reading R8): factor 2 while both even and min/2 >= coarse_min
+int build_levels(int nx, int ny, double Lx, double Ly, const int bc[4], const stokes_opts &o, GridL *gs, int *nus) {
+    int cx = nx, cy = ny, l = 0;
+    for (;;) {
+        gs[l] = make_grid(cx, cy, Lx, Ly, bc);
+        nus[l] = (int)floor(o.nu1 * pow(o.nu_growth, (double)l) + 0.5);
+        ++l;
+        if (l >= MAXLEV) break;
+        if ((cx % 2) || (cy % 2)) break;
+        const int m = cx < cy ? cx : cy;
+        if (m / 2 < o.coarse_min) break;
+        cx /= 2;
+        cy /= 2;
+    }
+    return l;
+}
+
+struct Carver {  // bump allocator over the workspace (256-B granules)
+    char *base;
+    size_t off, cap;
+    bool dry;
+    double *take(size_t ndoubles) {
+        off = round_up(off, 256);
+        double *p = dry ? nullptr : (double *)(base + off);
+        off += ndoubles * sizeof(double);
+        return p;
+    }
+    double *field(const GridL &g) {
+        double *a = take(field_doubles(g));
+        return dry ? nullptr : a + COL_OFF;
+    }
+};
+
+int check_opts(const stokes_opts &o) {
+    if (o.smoother != 0 && o.smoother != 1) return STOKES_EINVAL;
+    if (!(o.omega_v > 0) || !(o.alpha_p > 0) || o.nu1 < 0 || !(o.nu_growth > 0) || o.coarse_min < 2) return STOKES_EINVAL;
+    if (o.coarse_direct != 0 && o.coarse_direct != 1) return STOKES_EINVAL;
+    if (o.vcycles_per_iter < 1 || (o.accel != 0 && o.accel != 1)) return STOKES_EINVAL;
+    if (o.gcr_restart < 1 || o.gcr_restart > MAXM || o.max_iter < 0) return STOKES_EINVAL;
+    if (o.pressure_sign != 1 && o.pressure_sign != -1) return STOKES_EINVAL;
+    return STOKES_OK;
+}
+
+// lay out (or size) the workspace
+size_t carve(stokes_s *h, Carver &cv) {
+    for (int l = 0; l < h->nlev; ++l) {
+        Level &L = h->lev[l];
+        L.etab = cv.field(L.g);
+        L.etap = cv.field(L.g);
+        for (int k = 0; k < 2; ++k) {
+            L.vx[k] = cv.field(L.g);
+            L.vy[k] = cv.field(L.g);
+        }
+        L.bx = cv.field(L.g);
+        L.by = cv.field(L.g);
+        L.rx = cv.field(L.g);
+        L.ry = cv.field(L.g);
+    }
+    const GridL &g0 = h->lev[0].g;
+    h->p = cv.field(g0);
+    h->rho = cv.field(g0);
+    h->npart = (size_t)energy_blocks(g0) * 12 + 64;
+    h->partials = cv.take(h->npart);
+    h->scal = cv.take(S_NSCAL);
+    const GridL &gc = h->lev[h->nlev - 1].g;
+    const int n = n_unknowns(gc);
+    if (h->o.coarse_direct && n <= MAX_DIRECT) {
+        h->nc = n;
+        h->Minv = cv.take((size_t)n * n);
+        h->Mwork = cv.take((size_t)n * 2 * n);
+    } else {
+        h->nc = 0;
+        h->Minv = h->Mwork = nullptr;
+    }
+    h->dflag = (int *)cv.take(4);
+    if (h->o.accel == STOKES_ACCEL_GCR) {
+        for (int i = 0; i < h->o.gcr_restart; ++i)
+            for (int f = 0; f < 3; ++f) {
+                h->gz[i][f] = cv.field(g0);
+                h->gw[i][f] = cv.field(g0);
+            }
+        for (int f = 0; f < 3; ++f) h->gr[f] = cv.field(g0);
+        h->gtmp[0] = cv.field(g0);
+        h->gtmp[1] = cv.field(g0);
+    }
+    return round_up(cv.off, 256);
+}
+
+LaunchCtx ctx(stokes_s *h) { return LaunchCtx{h->stream, &h->launches}; }
+
+RhsArgs rhs_arrays(const double *bx, const double *by) {
+    RhsArgs r;
+    r.mode = RHS_ARRAYS;
+    r.bx = bx;
+    r.by = by;
+    r.p = r.rho = nullptr;
+    r.gx = r.gy = 0.0;
+    return r;
+}
+RhsArgs rhs_fine(stokes_s *h) {
+    RhsArgs r;
+    r.mode = RHS_FINE;
+    r.bx = r.by = nullptr;
+    r.p = h->p;
+    r.rho = h->rho;
+    r.gx = h->gx;
+    r.gy = h->gy;
+    return r;
+}
+
+// nsweeps of the smoother on level l for L v = b.  (cur) holds v; Jacobi ping-pongs
+// between cur and the other buffer: on return cur points at the result.
+void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&oy, const RhsArgs &rhs, int n,
+            bool zero_in) {
+    Level &L = h->lev[l];
+    const LaunchCtx c = ctx(h);
+    if (n <= 0) {
+        if (zero_in) {
+            cudaMemsetAsync(cx - COL_OFF, 0, field_doubles(L.g) * sizeof(double), h->stream);
+            cudaMemsetAsync(cy - COL_OFF, 0, field_doubles(L.g) * sizeof(double), h->stream);
+        }
+        return;
+    }
+    if (h->o.smoother == STOKES_SMOOTH_JACOBI) {
+        for (int s = 0; s < n; ++s) {
+            launch_jacobi(c, L.g, L.etab, L.etap, cx, cy, ox, oy, rhs, h->o.omega_v, zero_in && s == 0);
+            double *t = cx; cx = ox; ox = t;
+            t = cy; cy = oy; oy = t;
+        }
+    } else {
+        if (zero_in) {
+            cudaMemsetAsync(cx - COL_OFF, 0, field_doubles(L.g) * sizeof(double), h->stream);
+            cudaMemsetAsync(cy - COL_OFF, 0, field_doubles(L.g) * sizeof(double), h->stream);
+        }
+        for (int s = 0; s < n; ++s) launch_rbgs(c, L.g, L.etab, L.etap, cx, cy, rhs, h->o.omega_v);
+    }
+}
+
+// One V-cycle (Eq. multigrid_levels) on level l for L v = b, v in
+// (ax, ay) with scratch (bx_, by_); the result is left in (ax, ay) (the sweep count per
+// cycle, 2 nu, is even).  zero_in: the initial guess is 0 (coarse corrections).
+void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in) {
+    Level &L = h->lev[l];
+    const LaunchCtx c = ctx(h);
+    double *cx = ax, *cy = ay, *ox = sx, *oy = sy;
+    if (l == h->nlev - 1) {  // coarsest (a8)
+        if (h->nc > 0) {
+            const double *bx = rhs.bx, *by = rhs.by;
+            if (rhs.mode != RHS_ARRAYS) {
+                launch_make_rhs(c, L.g, rhs, L.bx, L.by);
+                bx = L.bx;
+                by = L.by;
+            }
+            launch_coarse_solve(c, L.g, h->Minv, bx, by, ax, ay);
+        } else {
+            smooth(h, l, cx, cy, ox, oy, rhs, 2 * L.nu, zero_in);
+            if (cx != ax) {  // odd count cannot happen (2 nu), kept for safety
+                cudaMemcpyAsync(ax - COL_OFF, cx - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
+                cudaMemcpyAsync(ay - COL_OFF, cy - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
+            }
+        }
+        return;
+    }
+    Level &C = h->lev[l + 1];
+    smooth(h, l, cx, cy, ox, oy, rhs, L.nu, zero_in);                        // (1) pre-smoothing
+    launch_residual(c, L.g, L.etab, L.etap, cx, cy, rhs, L.rx, L.ry);          // (2) residual
+    launch_restrict_vel(c, L.g, C.g, L.rx, L.ry, C.bx, C.by);                 // (3) restriction
+    vcycle(h, l + 1, C.vx[0], C.vy[0], C.vx[1], C.vy[1], rhs_arrays(C.bx, C.by), true);  // (4)
+    launch_prolong(c, L.g, C.g, C.vx[0], C.vy[0], cx, cy);                    // (5) correction
+    smooth(h, l, cx, cy, ox, oy, rhs, L.nu, false);                          // (6) post-smoothing
+    if (cx != ax) {
+        cudaMemcpyAsync(ax - COL_OFF, cx - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
+        cudaMemcpyAsync(ay - COL_OFF, cy - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
+    }
+}
+
+// the body of one Uzawa iteration (a12, mode UZAWA): V-cycle(s) on L v = f - G p^k,
+// pressure update + mean, energy residual of the new (v, p), E -> pinned host.
+void uzawa_body(stokes_s *h) {
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    for (int k = 0; k < h->o.vcycles_per_iter; ++k)
+        vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false);
+    const int nb = pupdate_blocks(F.g);
+    launch_pupdate(c, F.g, F.etap, F.vx[0], F.vy[0], h->p, h->o.pressure_sign * h->o.alpha_p, h->scal + S_MSHIFT,
+                   h->partials);
+    launch_finalize(c, h->partials, nb, 1, 1.0 / ((double)F.g.ncx * F.g.ncy), h->scal + S_MSHIFT);
+    launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, nullptr, nullptr, nullptr,
+                  h->partials, false);
+    launch_energy_final(c, h->partials, energy_blocks(F.g), h->scal + S_SF, h->scal + S_E);
+    cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+}
+
+int sync(stokes_s *h) {
+    CK(cudaStreamSynchronize(h->stream));
+    CKL();
+    return STOKES_OK;
+}
+
+// Sf = sum f^2 / d_v (the normaliser of E) -> scal[S_SF]
+void force_energy(stokes_s *h) {
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, nullptr, nullptr, nullptr,
+                  h->partials, true);
+    launch_energy_final(c, h->partials, energy_blocks(F.g), h->scal + S_ZERO, h->scal + S_SFPART);
+    // S_SFPART+1 holds the sum Sv of f -> copy into S_SF
+    cudaMemcpyAsync(h->scal + S_SF, h->scal + S_SFPART + 1, sizeof(double), cudaMemcpyDeviceToDevice, h->stream);
+}
+
+int energy_now(stokes_s *h, double *E) {
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, nullptr, nullptr, nullptr,
+                  h->partials, false);
+    launch_energy_final(c, h->partials, energy_blocks(F.g), h->scal + S_SF, h->scal + S_E);
+    cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+    int st = sync(h);
+    if (st) return st;
+    *E = h->hscal[S_E];
+    return STOKES_OK;
+}
+
+int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+    // capture one iteration into a CUDA graph (launch-bound coarse levels), replay per step
+    if (!h->uzawa_exec) {
+        cudaGraph_t graph;
+        const long long before = h->launches;
+        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        uzawa_body(h);
+        cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+        if (e != cudaSuccess) return fail_cuda(e, "graph capture");
+        h->uzawa_kernels = h->launches - before;
+        h->launches = before;
+        e = cudaGraphInstantiate(&h->uzawa_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            h->uzawa_exec = nullptr;
+            return fail_cuda(e, "graph instantiate");
+        }
+    }
+    double E = E0;
+    int k;
+    int status = STOKES_NOT_CONVERGED;
+    for (k = 1; k <= h->o.max_iter; ++k) {
+        CK(cudaGraphLaunch(h->uzawa_exec, h->stream));
+        h->launches += h->uzawa_kernels;
+        int st = sync(h);
+        if (st) return st;
+        E = h->hscal[S_E];
+        if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+        if (E <= rtol) { status = STOKES_OK; break; }
+    }
+    if (k > h->o.max_iter) k = h->o.max_iter;
+    *iters = k;
+    *Eout = E;
+    return status;
+}
+
+// Flexible GCR(m) with modified Gram-Schmidt, Alg. 4, readings R13/R14.
+int solve_gcr(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+    Level &F = h->lev[0];
+    const GridL &g = F.g;
+    const LaunchCtx c = ctx(h);
+    const int m = h->o.gcr_restart;
+    const int nb = energy_blocks(g);
+    double *x[3] = {F.vx[0], F.vy[0], h->p};
+    double **r = h->gr;
+    // r0 = b - A x0 (recursive residual)
+    launch_energy(c, g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, r[0], r[1], r[2], h->partials,
+                  false);
+    int k = 0, status = STOKES_NOT_CONVERGED;
+    double E = E0;
+    const double inv_np = 1.0 / ((double)g.ncx * g.ncy);
+    while (k < h->o.max_iter && status == STOKES_NOT_CONVERGED) {
+        for (int i = 0; i < m && k < h->o.max_iter; ++i) {
+            double **z = h->gz[i], **w = h->gw[i];
+            // z = M^-1 r: dv = Vcycle(0; r_v); dp = alpha eta_P (r_p - D dv); de-mean dp
+            for (int q = 0; q < h->o.vcycles_per_iter; ++q)
+                vcycle(h, 0, z[0], z[1], h->gtmp[0], h->gtmp[1], rhs_arrays(r[0], r[1]), q == 0);
+            launch_precond_p(c, g, F.etap, z[0], z[1], r[2], h->o.alpha_p, z[2], h->partials);
+            launch_finalize(c, h->partials, nb, 1, inv_np, h->scal + S_ZMEAN);
+            launch_sub_mean(c, g, h->scal + S_ZMEAN, z[2]);
+            // w = A z
+            launch_apply_padded(c, g, F.etab, F.etap, z[0], z[1], z[2], w[0], w[1], w[2]);
+            for (int j = 0; j < i; ++j) {  // modified Gram-Schmidt
+                const double *a[3] = {w[0], w[1], w[2]};
+                const double *b[3] = {h->gw[j][0], h->gw[j][1], h->gw[j][2]};
+                launch_dots(c, g, a, b, 1, h->partials);
+                launch_finalize(c, h->partials, nb, 1, 1.0, h->scal + S_GAMMA);
+                launch_axpy3(c, g, h->scal, S_GAMMA, -1.0, h->gw[j][0], h->gw[j][1], h->gw[j][2], w[0], w[1], w[2]);
+                launch_axpy3(c, g, h->scal, S_GAMMA, -1.0, h->gz[j][0], h->gz[j][1], h->gz[j][2], z[0], z[1], z[2]);
+            }
+            {
+                const double *a[6] = {w[0], w[1], w[2], r[0], r[1], r[2]};
+                launch_dots(c, g, a, a, 2, h->partials);
+                launch_finalize(c, h->partials, nb, 2, 1.0, h->scal + S_NU2);
+            }
+            launch_scale3(c, g, h->scal + S_NU2, 1, w[0], w[1], w[2]);
+            launch_scale3(c, g, h->scal + S_NU2, 1, z[0], z[1], z[2]);
+            {
+                const double *a[3] = {r[0], r[1], r[2]};
+                const double *b[3] = {w[0], w[1], w[2]};
+                launch_dots(c, g, a, b, 1, h->partials);
+                launch_finalize(c, h->partials, nb, 1, 1.0, h->scal + S_BETA);
+            }
+            launch_axpy3(c, g, h->scal, S_BETA, 1.0, z[0], z[1], z[2], x[0], x[1], x[2]);
+            launch_axpy3(c, g, h->scal, S_BETA, -1.0, w[0], w[1], w[2], r[0], r[1], r[2]);
+            launch_energy_vec(c, g, F.etab, F.etap, r[0], r[1], r[2], h->partials);
+            launch_energy_final(c, h->partials, nb, h->scal + S_SF, h->scal + S_E);
+            cudaMemcpyAsync(h->hscal, h->scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+            int st = sync(h);
+            if (st) return st;
+            ++k;
+            const double nu2 = h->hscal[S_NU2], rr = h->hscal[S_RR];
+            E = h->hscal[S_E];
+            if (!(nu2 > 1e-28 * rr)) { status = STOKES_EDIVERGED; break; }  // breakdown (R13)
+            if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+            if (E <= rtol) { status = STOKES_OK; break; }
+        }
+    }
+    *iters = k;
+    *Eout = E;
+    // the pressure mean of x (inert) is removed at output through S_MSHIFT
+    launch_pupdate(c, g, F.etap, F.vx[0], F.vy[0], h->p, 0.0, h->scal + S_ZERO, h->partials);
+    launch_finalize(c, h->partials, nb, 1, inv_np, h->scal + S_MSHIFT);
+    return status;
+}
+
+bool valid_level(stokes_s *h, int l) { return h && l >= 0 && l < h->nlev; }
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+int stokes_opts_default(stokes_opts *o) {
+    if (!o) return STOKES_EINVAL;
+    o->smoother = STOKES_SMOOTH_JACOBI;
+    o->omega_v = 0.3;
+    o->alpha_p = 0.6;
+    o->nu1 = 5;
+    o->nu_growth = 1.0;
+    o->coarse_min = 8;
+    o->coarse_direct = 1;
+    o->vcycles_per_iter = 1;
+    o->accel = STOKES_ACCEL_NONE;
+    o->gcr_restart = 10;
+    o->max_iter = 10000;
+    o->pressure_sign = 1;
+    return STOKES_OK;
+}
+
+static int prepare(stokes_s *h, int nx, int ny, double Lx, double Ly, const int bc[4], const stokes_opts *opts) {
+    if (nx < 2 || ny < 2 || !(Lx > 0) || !(Ly > 0) || !bc) return STOKES_EINVAL;
+    for (int k = 0; k < 4; ++k)
+        if (bc[k] != 0 && bc[k] != 1) return STOKES_EINVAL;
+    h->nx = nx;
+    h->ny = ny;
+    h->Lx = Lx;
+    h->Ly = Ly;
+    memcpy(h->bc, bc, sizeof(h->bc));
+    if (opts) h->o = *opts;
+    else stokes_opts_default(&h->o);
+    if (check_opts(h->o)) return STOKES_EINVAL;
+    GridL gs[MAXLEV];
+    int nus[MAXLEV];
+    h->nlev = build_levels(nx, ny, Lx, Ly, bc, h->o, gs, nus);
+    for (int l = 0; l < h->nlev; ++l) {
+        h->lev[l].g = gs[l];
+        h->lev[l].nu = nus[l];
+    }
+    return STOKES_OK;
+}
+
+int stokes_workspace_bytes(int nx, int ny, const stokes_opts *opts, size_t *bytes) {
+    if (!bytes) return STOKES_EINVAL;
+    stokes_s h;
+    memset(&h, 0, sizeof h);
+    const int bc[4] = {0, 0, 0, 0};
+    int st = prepare(&h, nx, ny, 1.0, 1.0, bc, opts);
+    if (st) return st;
+    Carver cv{nullptr, 0, 0, true};
+    *bytes = carve(&h, cv);
+    return STOKES_OK;
+}
+
+int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const stokes_opts *opts, void *cuda_stream,
+                  void *workspace, size_t workspace_bytes, stokes_t *out) {
+    if (!out) return STOKES_EINVAL;
+    stokes_s *h = (stokes_s *)calloc(1, sizeof(stokes_s));
+    if (!h) return STOKES_ENOMEM;
+    int st = prepare(h, nx, ny, Lx, Ly, bc, opts);
+    if (st) { free(h); return st; }
+    h->stream = (cudaStream_t)cuda_stream;
+    if (!h->stream) {  // the legacy default stream cannot be graph-captured: use our own
+        cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { free(h); return fail_cuda(e, "cudaStreamCreate"); }
+        h->own_stream = true;
+    }
+    Carver dry{nullptr, 0, 0, true};
+    const size_t need = carve(h, dry);
+    if (workspace) {
+        if (workspace_bytes < need || ((uintptr_t)workspace & 255)) { free(h); return STOKES_ENOMEM; }
+        h->ws = workspace;
+        h->own_ws = false;
+    } else {
+        cudaError_t e = cudaMalloc(&h->ws, need);
+        if (e != cudaSuccess) { free(h); fail_cuda(e, "cudaMalloc workspace"); return STOKES_ENOMEM; }
+        h->own_ws = true;
+    }
+    h->ws_bytes = need;
+    Carver cv{(char *)h->ws, 0, need, false};
+    carve(h, cv);
+    cudaError_t e = cudaMallocHost(&h->hscal, S_NSCAL * sizeof(double));
+    if (e != cudaSuccess) { if (h->own_ws) cudaFree(h->ws); free(h); fail_cuda(e, "cudaMallocHost"); return STOKES_ECUDA; }
+    memset(h->hscal, 0, S_NSCAL * sizeof(double));
+    // zero everything once: walls / ghosts of every buffer stay 0 (reading R1, R5)
+    e = cudaMemsetAsync(h->ws, 0, need, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) {
+        cudaFreeHost(h->hscal);
+        if (h->own_ws) cudaFree(h->ws);
+        free(h);
+        return fail_cuda(e, "workspace init");
+    }
+    *out = h;
+    return STOKES_OK;
+}
+
+int stokes_destroy(stokes_t h) {
+    if (!h) return STOKES_EINVAL;
+    if (h->uzawa_exec) cudaGraphExecDestroy(h->uzawa_exec);
+    if (h->hscal) cudaFreeHost(h->hscal);
+    if (h->own_ws && h->ws) cudaFree(h->ws);
+    if (h->own_stream) cudaStreamDestroy(h->stream);
+    free(h);
+    return STOKES_OK;
+}
+
+int stokes_num_levels(stokes_t h, int *nlev) {
+    if (!h || !nlev) return STOKES_EINVAL;
+    *nlev = h->nlev;
+    return STOKES_OK;
+}
+int stokes_level_shape(stokes_t h, int level, int *nx, int *ny, int *nu) {
+    if (!valid_level(h, level) || !nx || !ny || !nu) return STOKES_EINVAL;
+    *nx = h->lev[level].g.ncx;
+    *ny = h->lev[level].g.ncy;
+    *nu = h->lev[level].nu;
+    return STOKES_OK;
+}
+
+int stokes_set_viscosity(stokes_t h, const double *eta_b, const double *eta_p) {
+    if (!h || !eta_b || !eta_p) return STOKES_EINVAL;
+    const LaunchCtx c = ctx(h);
+    CK(cudaMemsetAsync(h->dflag, 0, sizeof(int), h->stream));
+    launch_count_nonpos(c, eta_b, (size_t)(h->ny + 1) * (h->nx + 1), h->dflag);
+    launch_count_nonpos(c, eta_p, (size_t)h->ny * h->nx, h->dflag);
+    int bad = 0;
+    CK(cudaMemcpyAsync(&h->hscal[S_NSCAL - 1], h->dflag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    int st = sync(h);
+    if (st) return st;
+    memcpy(&bad, &h->hscal[S_NSCAL - 1], sizeof(int));
+    if (bad) return STOKES_EINVAL;
+    Level &F = h->lev[0];
+    launch_in_b(c, F.g, eta_b, F.etab);
+    launch_in_p(c, F.g, eta_p, F.etap);
+    for (int l = 0; l + 1 < h->nlev; ++l) {  // a7: coarse viscosities by restriction
+        launch_restrict_b(c, h->lev[l].g, h->lev[l + 1].g, h->lev[l].etab, h->lev[l + 1].etab);
+        launch_restrict_p(c, h->lev[l].g, h->lev[l + 1].g, h->lev[l].etap, h->lev[l + 1].etap);
+    }
+    if (h->o.coarse_direct) {  // a8: explicit inverse of -L_c
+        if (h->nc == 0) return STOKES_EINVAL;  // coarsest too large for the direct solve
+        Level &C = h->lev[h->nlev - 1];
+        CK(cudaMemsetAsync(h->dflag, 0, sizeof(int), h->stream));
+        launch_coarse_assemble(c, C.g, C.etab, C.etap, h->Minv);
+        launch_coarse_invert(c, h->Mwork, h->Minv, h->nc, h->dflag);
+        CK(cudaMemcpyAsync(&h->hscal[S_NSCAL - 1], h->dflag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        st = sync(h);
+        if (st) return st;
+        memcpy(&bad, &h->hscal[S_NSCAL - 1], sizeof(int));
+        if (bad) return STOKES_EINVAL;
+    }
+    h->have_eta = true;
+    if (h->have_rho) force_energy(h);
+    return sync(h);
+}
+
+int stokes_set_density(stokes_t h, const double *rho_b) {
+    if (!h || !rho_b) return STOKES_EINVAL;
+    launch_in_b(ctx(h), h->lev[0].g, rho_b, h->rho);
+    h->have_rho = true;
+    if (h->have_eta) force_energy(h);
+    return sync(h);
+}
+
+int stokes_set_gravity(stokes_t h, double gx, double gy) {
+    if (!h || !(gx == gx) || !(gy == gy)) return STOKES_EINVAL;
+    h->gx = gx;
+    h->gy = gy;
+    if (h->uzawa_exec) {  // gravity is baked into the captured graph
+        cudaGraphExecDestroy(h->uzawa_exec);
+        h->uzawa_exec = nullptr;
+    }
+    if (h->have_eta && h->have_rho) force_energy(h);
+    return sync(h);
+}
+
+int stokes_apply_operator(stokes_t h, const double *vx, const double *vy, const double *p, double *ax, double *ay,
+                          double *ap) {
+    if (!h || !vx || !vy || !p || !ax || !ay || !ap) return STOKES_EINVAL;
+    if (!h->have_eta) return STOKES_ESTATE;
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    launch_in_velocity(c, F.g, vx, vy, F.rx, F.ry);  // scratch: rx/ry hold the padded v
+    launch_in_p(c, F.g, p, F.bx);
+    launch_apply(c, F.g, F.etab, F.etap, F.rx, F.ry, F.bx, ax, ay, ap);
+    return sync(h);
+}
+
+int stokes_residual(stokes_t h, const double *vx, const double *vy, const double *p, double *rx, double *ry,
+                    double *rp, double *rel_energy) {
+    if (!h || !vx || !vy || !p) return STOKES_EINVAL;
+    if (!h->have_eta || !h->have_rho) return STOKES_ESTATE;
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    launch_in_velocity(c, F.g, vx, vy, F.vx[0], F.vy[0]);
+    launch_in_p(c, F.g, p, h->p);
+    launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, F.rx, F.ry, F.bx,
+                  h->partials, false);
+    launch_energy_final(c, h->partials, energy_blocks(F.g), h->scal + S_SF, h->scal + S_E);
+    if (rx) launch_out_vx(c, F.g, F.rx, rx);
+    if (ry) launch_out_vy(c, F.g, F.ry, ry);
+    if (rp) launch_out_p(c, F.g, F.bx, rp, nullptr);
+    CK(cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    int st = sync(h);
+    if (st) return st;
+    if (rel_energy) *rel_energy = h->hscal[S_E];
+    return STOKES_OK;
+}
+
+int stokes_vcycle(stokes_t h, const double *bx, const double *by, double *vx, double *vy) {
+    if (!h || !bx || !by || !vx || !vy) return STOKES_EINVAL;
+    if (!h->have_eta) return STOKES_ESTATE;
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    launch_in_vx_raw(c, F.g, bx, F.bx);
+    launch_in_vy_raw(c, F.g, by, F.by);
+    launch_in_velocity(c, F.g, vx, vy, F.vx[0], F.vy[0]);
+    vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_arrays(F.bx, F.by), false);
+    launch_out_vx(c, F.g, F.vx[0], vx);
+    launch_out_vy(c, F.g, F.vy[0], vy);
+    return sync(h);
+}
+
+int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy) {
+    if (!h || !vx || !vy || !p || !iters || !rel_energy || !(rtol >= 0)) return STOKES_EINVAL;
+    if (!h->have_eta || !h->have_rho) return STOKES_ESTATE;
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    // load the initial guess
+    launch_in_velocity(c, F.g, vx, vy, F.vx[0], F.vy[0]);
+    launch_in_p(c, F.g, p, h->p);
+    CK(cudaMemsetAsync(h->scal + S_MSHIFT, 0, sizeof(double), h->stream));
+    CK(cudaMemcpyAsync(h->hscal + 32, h->scal + S_SF, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    int st = sync(h);
+    if (st) return st;
+    const double Sf = h->hscal[32];
+    int status;
+    if (!(Sf > 0)) {  // f == 0: zero solution, 0 iterations
+        CK(cudaMemsetAsync(vx, 0, (size_t)h->ny * (h->nx + 1) * 8, h->stream));
+        CK(cudaMemsetAsync(vy, 0, (size_t)(h->ny + 1) * h->nx * 8, h->stream));
+        CK(cudaMemsetAsync(p, 0, (size_t)h->ny * h->nx * 8, h->stream));
+        *iters = 0;
+        *rel_energy = 0.0;
+        return sync(h);
+    }
+    double E0;
+    st = energy_now(h, &E0);
+    if (st) return st;
+    if (E0 <= rtol) {
+        *iters = 0;
+        *rel_energy = E0;
+        status = STOKES_OK;
+        // de-mean the output pressure
+        launch_pupdate(c, F.g, F.etap, F.vx[0], F.vy[0], h->p, 0.0, h->scal + S_ZERO, h->partials);
+        launch_finalize(c, h->partials, pupdate_blocks(F.g), 1, 1.0 / ((double)F.g.ncx * F.g.ncy),
+                        h->scal + S_MSHIFT);
+    } else if (h->o.accel == STOKES_ACCEL_GCR) {
+        status = solve_gcr(h, rtol, E0, iters, rel_energy);
+    } else {
+        status = solve_uzawa(h, rtol, E0, iters, rel_energy);
+    }
+    if (status < 0 && status != STOKES_EDIVERGED) return status;
+    launch_out_vx(c, F.g, F.vx[0], vx);
+    launch_out_vy(c, F.g, F.vy[0], vy);
+    launch_out_p(c, F.g, h->p, p, h->scal + S_MSHIFT);
+    st = sync(h);
+    if (st) return st;
+    return status;
+}
+
+// ---------------------------------------------------------------- per-step entry points
+int stokes_smooth(stokes_t h, int level, const double *bx, const double *by, double *vx, double *vy, int nsweeps) {
+    if (!valid_level(h, level) || !bx || !by || !vx || !vy || nsweeps < 0) return STOKES_EINVAL;
+    if (!h->have_eta) return STOKES_ESTATE;
+    Level &L = h->lev[level];
+    const LaunchCtx c = ctx(h);
+    launch_in_vx_raw(c, L.g, bx, L.bx);
+    launch_in_vy_raw(c, L.g, by, L.by);
+    launch_in_velocity(c, L.g, vx, vy, L.vx[0], L.vy[0]);
+    double *cx = L.vx[0], *cy = L.vy[0], *ox = L.vx[1], *oy = L.vy[1];
+    smooth(h, level, cx, cy, ox, oy, rhs_arrays(L.bx, L.by), nsweeps, false);
+    launch_out_vx(c, L.g, cx, vx);
+    launch_out_vy(c, L.g, cy, vy);
+    return sync(h);
+}
+
+int stokes_level_residual(stokes_t h, int level, const double *bx, const double *by, const double *vx,
+                          const double *vy, double *rx, double *ry) {
+    if (!valid_level(h, level) || !bx || !by || !vx || !vy || !rx || !ry) return STOKES_EINVAL;
+    if (!h->have_eta) return STOKES_ESTATE;
+    Level &L = h->lev[level];
+    const LaunchCtx c = ctx(h);
+    launch_in_vx_raw(c, L.g, bx, L.bx);
+    launch_in_vy_raw(c, L.g, by, L.by);
+    launch_in_velocity(c, L.g, vx, vy, L.vx[0], L.vy[0]);
+    launch_residual(c, L.g, L.etab, L.etap, L.vx[0], L.vy[0], rhs_arrays(L.bx, L.by), L.rx, L.ry);
+    launch_out_vx(c, L.g, L.rx, rx);
+    launch_out_vy(c, L.g, L.ry, ry);
+    return sync(h);
+}
+
+int stokes_restrict(stokes_t h, int level, int kind, const double *fine, double *coarse) {
+    if (!valid_level(h, level) || level + 1 >= h->nlev || kind < 0 || kind > 3 || !fine || !coarse) return STOKES_EINVAL;
+    Level &L = h->lev[level], &C = h->lev[level + 1];
+    const LaunchCtx c = ctx(h);
+    switch (kind) {
+    case 0:
+        launch_in_vx_raw(c, L.g, fine, L.rx);
+        launch_restrict_vx(c, L.g, C.g, L.rx, C.rx);
+        launch_out_vx(c, C.g, C.rx, coarse);
+        break;
+    case 1:
+        launch_in_vy_raw(c, L.g, fine, L.ry);
+        launch_restrict_vy(c, L.g, C.g, L.ry, C.ry);
+        launch_out_vy(c, C.g, C.ry, coarse);
+        break;
+    case 2:
+        launch_in_p(c, L.g, fine, L.rx);
+        launch_restrict_p(c, L.g, C.g, L.rx, C.rx);
+        launch_out_p(c, C.g, C.rx, coarse, nullptr);
+        break;
+    default:
+        launch_in_b(c, L.g, fine, L.rx);
+        launch_restrict_b(c, L.g, C.g, L.rx, C.rx);
+        launch_out_b(c, C.g, C.rx, coarse);
+        break;
+    }
+    return sync(h);
+}
+
+int stokes_prolong(stokes_t h, int level, const double *ex, const double *ey, double *vx, double *vy) {
+    if (!valid_level(h, level) || level + 1 >= h->nlev || !ex || !ey || !vx || !vy) return STOKES_EINVAL;
+    Level &L = h->lev[level], &C = h->lev[level + 1];
+    const LaunchCtx c = ctx(h);
+    launch_in_velocity(c, C.g, ex, ey, C.vx[0], C.vy[0]);
+    launch_in_velocity(c, L.g, vx, vy, L.vx[0], L.vy[0]);
+    launch_prolong(c, L.g, C.g, C.vx[0], C.vy[0], L.vx[0], L.vy[0]);
+    launch_out_vx(c, L.g, L.vx[0], vx);
+    launch_out_vy(c, L.g, L.vy[0], vy);
+    return sync(h);
+}
+
+int stokes_get_viscosity(stokes_t h, int level, double *eta_b, double *eta_p) {
+    if (!valid_level(h, level) || !eta_b || !eta_p) return STOKES_EINVAL;
+    if (!h->have_eta) return STOKES_ESTATE;
+    Level &L = h->lev[level];
+    const LaunchCtx c = ctx(h);
+    launch_out_b(c, L.g, L.etab, eta_b);
+    launch_out_p(c, L.g, L.etap, eta_p, nullptr);
+    return sync(h);
+}
+
+int stokes_coarse_solve(stokes_t h, const double *bx, const double *by, double *vx, double *vy) {
+    if (!h || !bx || !by || !vx || !vy) return STOKES_EINVAL;
+    if (!h->have_eta) return STOKES_ESTATE;
+    if (h->nc == 0) return STOKES_EINVAL;
+    Level &C = h->lev[h->nlev - 1];
+    const LaunchCtx c = ctx(h);
+    launch_in_vx_raw(c, C.g, bx, C.bx);
+    launch_in_vy_raw(c, C.g, by, C.by);
+    launch_coarse_solve(c, C.g, h->Minv, C.bx, C.by, C.vx[0], C.vy[0]);
+    launch_out_vx(c, C.g, C.vx[0], vx);
+    launch_out_vy(c, C.g, C.vy[0], vy);
+    return sync(h);
+}
+
+int stokes_launch_count(stokes_t h, long long *count, int reset) {
+    if (!h || !count) return STOKES_EINVAL;
+    *count = h->launches;
+    if (reset) h->launches = 0;
+    return STOKES_OK;
+}
+
+int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double *bytes) {
+    if (!h || !avg_ms || !bytes || reps < 1) return STOKES_EINVAL;
+    if (!h->have_eta || !h->have_rho) return STOKES_ESTATE;
+    Level &F = h->lev[0];
+    const GridL &g = F.g;
+    const LaunchCtx c = ctx(h);
+    const double cells = (double)g.ncx * g.ncy;
+    auto run = [&](void) {
+        switch (kernel) {
+        case 0: launch_jacobi(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v, false); break;
+        case 1: launch_energy(c, g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, nullptr, nullptr, nullptr, h->partials, false); break;
+        case 2: launch_residual(c, g, F.etab, F.etap, F.vx[0], F.vy[0], rhs_fine(h), F.rx, F.ry);
+                if (h->nlev > 1) launch_restrict_vel(c, g, h->lev[1].g, F.rx, F.ry, h->lev[1].bx, h->lev[1].by);
+                break;
+        case 3: if (h->nlev > 1) launch_prolong(c, g, h->lev[1].g, h->lev[1].vx[0], h->lev[1].vy[0], F.vx[1], F.vy[1]); break;
+        case 4: launch_pupdate(c, g, F.etap, F.vx[0], F.vy[0], F.rx, h->o.alpha_p, h->scal + S_ZERO, h->partials); break;
+        default: launch_rbgs(c, g, F.etab, F.etap, F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v); break;
+        }
+    };
+    // algorithmic bytes per launch: 8 B per value read or written
+    const double per_cell[6] = {64.0, 48.0, 52.0 + 16.0, 4.0 + 32.0, 40.0, 64.0};
+    if (kernel < 0 || kernel > 5) return STOKES_EINVAL;
+    *bytes = per_cell[kernel] * cells;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    run();
+    run();
+    CK(cudaEventRecord(e0, h->stream));
+    for (int r = 0; r < reps; ++r) run();
+    CK(cudaEventRecord(e1, h->stream));
+    CK(cudaEventSynchronize(e1));
+    CKL();
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *avg_ms = ms / reps;
+    return STOKES_OK;
+}
+
+const char *stokes_strerror(int s) {
+    switch (s) {
+    case STOKES_OK: return "ok";
+    case STOKES_NOT_CONVERGED: return "not converged (max_iter reached)";
+    case STOKES_EINVAL: return "invalid argument";
+    case STOKES_ENOMEM: return "out of device memory / workspace too small";
+    case STOKES_ECUDA: return "CUDA error";
+    case STOKES_ENCCL: return "NCCL error";
+    case STOKES_EDIVERGED: return "diverged";
+    case STOKES_ESTATE: return "call order: set_viscosity / set_density first";
+    default: return "unknown status";
+    }
+}
+const char *stokes_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

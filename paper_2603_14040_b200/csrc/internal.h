@@ -1,0 +1,112 @@
+// Internal declarations of libstokes_b200 (not part of the ABI).
+//
+// Data layout in HBM: every staggered field of a level is one FP64 array
+// on the paper's padded index space (ncy+2) x (ncx+2) (basic / boundary
+// B / ghost G nodes), row pitch P doubles (multiple of 32 = 256 B), element (i, j) at
+// base[i * P + j].  base = allocation + COL_OFF so that interior column 1 is 256-B
+// aligned: a warp reading columns 1..32 of a row touches exactly two 128-B lines.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/stokes.h"
+
+#define COL_OFF 31
+
+struct GridL {          // one multigrid level, passed by value to kernels
+    int ncx, ncy, P;    // cells in x / y, row pitch (doubles)
+    double dx, dy;
+    double idx, idy;    // 1/dx, 1/dy
+    double idx2, idy2;  // 1/dx^2, 1/dy^2
+    double idxdy;       // 1/(dx dy)
+    double sW, sE, sN, sS;  // mirror signs: +1 free slip, -1 no slip
+};
+
+__host__ __device__ inline size_t at(const GridL &g, int i, int j) { return (size_t)i * (size_t)g.P + (size_t)j; }
+
+// launch bookkeeping shared by all launchers
+struct LaunchCtx {
+    cudaStream_t stream;
+    long long *counter;  // incremented per kernel launch (host side)
+};
+
+// ---------------------------------------------------------------- kernels.cu launchers
+// RHS modes of the smoother / residual kernels
+enum { RHS_ARRAYS = 0, RHS_FINE = 1 };  // b from arrays (bx, by) / b = f - G p from (rho, p)
+
+struct RhsArgs {
+    int mode;
+    const double *bx, *by;          // RHS_ARRAYS
+    const double *p, *rho;          // RHS_FINE
+    double gx, gy;
+};
+
+void launch_jacobi(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
+                   const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega, bool zero_in);
+void launch_rbgs(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *vx, double *vy,
+                 const RhsArgs &rhs, double omega);
+void launch_residual(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vx,
+                     const double *vy, const RhsArgs &rhs, double *rx, double *ry);
+void launch_restrict_vel(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *rx, const double *ry,
+                         double *bxc, double *byc);
+void launch_restrict_b(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *f, double *cc);
+void launch_restrict_p(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *f, double *cc);
+void launch_restrict_vx(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *f, double *cc);
+void launch_restrict_vy(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *f, double *cc);
+void launch_prolong(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *exc, const double *eyc,
+                    double *vx, double *vy);
+// full saddle residual + energy partial sums (Sv, Sp) per block; writes r arrays if non-null.
+// force_only: Sv of f (the normaliser Sf).  Returns the number of partial blocks.
+int energy_blocks(const GridL &g);
+void launch_energy(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vx,
+                   const double *vy, const double *p, const double *rho, double gx, double gy, double *rx,
+                   double *ry, double *rp, double *partials, bool force_only);
+void launch_energy_vec(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *rx,
+                       const double *ry, const double *rp, double *partials);
+void launch_make_rhs(const LaunchCtx &c, const GridL &g, const RhsArgs &rhs, double *bx, double *by);
+// p <- (p - *mshift) + sign * alpha * eta_p * (-D v); partial sums of the new p per block
+int pupdate_blocks(const GridL &g);
+void launch_pupdate(const LaunchCtx &c, const GridL &g, const double *etap, const double *vx, const double *vy,
+                    double *p, double alpha_signed, const double *mshift, double *partials);
+// out[k] = scale * sum_b partials[b * ncomp + k], deterministic fixed-order tree
+void launch_finalize(const LaunchCtx &c, const double *partials, int nblocks, int ncomp, double scale, double *out);
+// energy: E = sqrt((S[0] + S[1]) / Sf[0]) -> out[0]; also copies S to out[1..2]
+void launch_energy_final(const LaunchCtx &c, const double *partials, int nblocks, const double *Sf, double *out);
+
+// layout conversion (user <-> padded)
+void launch_in_velocity(const LaunchCtx &c, const GridL &g, const double *ux, const double *uy, double *vx,
+                        double *vy);
+void launch_in_p(const LaunchCtx &c, const GridL &g, const double *u, double *a);
+void launch_in_b(const LaunchCtx &c, const GridL &g, const double *u, double *a);
+void launch_in_vx_raw(const LaunchCtx &c, const GridL &g, const double *u, double *a);
+void launch_in_vy_raw(const LaunchCtx &c, const GridL &g, const double *u, double *a);
+void launch_out_vx(const LaunchCtx &c, const GridL &g, const double *a, double *u);
+void launch_out_vy(const LaunchCtx &c, const GridL &g, const double *a, double *u);
+void launch_out_p(const LaunchCtx &c, const GridL &g, const double *a, double *u, const double *shift);
+void launch_out_b(const LaunchCtx &c, const GridL &g, const double *a, double *u);
+void launch_apply(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vx,
+                  const double *vy, const double *p, double *ax, double *ay, double *ap);
+void launch_count_nonpos(const LaunchCtx &c, const double *a, size_t n, int *count);
+
+// coarsest level: assemble -L_c (n x n, mirror relations folded), invert, apply
+void launch_coarse_assemble(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *M);
+// Minv holds -L_c on entry and its inverse on exit; work must hold n x 2n doubles
+void launch_coarse_invert(const LaunchCtx &c, double *work, double *Minv, int n, int *fail);
+void launch_coarse_solve(const LaunchCtx &c, const GridL &g, const double *Minv, const double *bx,
+                         const double *by, double *vx, double *vy);
+
+// GCR vector kernels (vectors = (x, y, p) padded triples on the fine level)
+int dot_blocks(const GridL &g);
+void launch_dots(const LaunchCtx &c, const GridL &g, const double *const *a, const double *const *b, int nd,
+                 double *partials);
+void launch_axpy3(const LaunchCtx &c, const GridL &g, const double *coef, int coef_index, double coef_sign,
+                  const double *xx, const double *xy, const double *xp, double *yx, double *yy, double *yp);
+void launch_scale3(const LaunchCtx &c, const GridL &g, const double *coef, int invert_sqrt, double *x,
+                   double *y, double *p);
+void launch_precond_p(const LaunchCtx &c, const GridL &g, const double *etap, const double *zx, const double *zy,
+                      const double *rp, double alpha, double *zp, double *partials);
+void launch_sub_mean(const LaunchCtx &c, const GridL &g, const double *mean, double *p);
+void launch_apply_padded(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                         const double *vx, const double *vy, const double *p, double *ax, double *ay, double *ap);
+void launch_refresh_mirrors(const LaunchCtx &c, const GridL &g, double *vx, double *vy);

@@ -1,0 +1,949 @@
+// Hand-written FP64 CUDA kernels of the matrix-free multigrid Stokes solve (sm_100a).
+//
+// Every kernel cites the passage of PAPER.md it implements; the readings R1..R23 are
+// listed in DESIGN.md §3.  No tensor cores: nothing here is a dense contraction
+// (DESIGN.md §6); every hot kernel is HBM-bandwidth bound and is measured against the
+// measured copy bandwidth (MEASURED_PEAKS.json).
+//
+// Index space of a level: padded (ncy+2) x (ncx+2), row pitch g.P (internal.h).
+//   vx unknowns i in [1,ncy], j in [1,ncx-1]; walls j = 0, ncx; mirrors i = 0, ncy+1
+//   vy unknowns i in [1,ncy-1], j in [1,ncx]; walls i = 0, ncy; mirrors j = 0, ncx+1
+//   P  unknowns i in [1,ncy], j in [1,ncx];  basic nodes i in [0,ncy], j in [0,ncx]
+// (Listing loop bounds PAPER.md:2352-2353, reading R1.)  Wall entries are zero in every
+// velocity buffer from allocation on and are never written; every kernel that writes a
+// velocity unknown next to a boundary also writes its mirror (reading R5: "refresh the
+// mirrors after every update" == "mirror = partner's current value").
+#include <math.h>
+
+#include "internal.h"
+
+namespace {
+
+constexpr int BX = 32, BY = 8;  // 256-thread tiles: one warp spans 32 consecutive columns
+
+inline dim3 cell_grid(const GridL &g) { return dim3((g.ncx + BX - 1) / BX, (g.ncy + BY - 1) / BY); }
+
+// ------------------------------------------------------------------ stencil pieces
+struct ArrayAcc {  // plain global loads
+    const double *__restrict__ a;
+    size_t P;
+    __device__ __forceinline__ double operator()(int i, int j) const { return a[(size_t)i * P + j]; }
+};
+
+// x-momentum row at vx(i,j): Listing vx_op_point -- coefficients verbatim.
+template <class VX, class VY>
+__device__ __forceinline__ double lx_row(const GridL &g, const double *__restrict__ etab,
+                                         const double *__restrict__ etap, const VX &vx, const VY &vy, int i, int j) {
+    const double etaA = etap[at(g, i, j)], etaB = etap[at(g, i, j + 1)];
+    const double eta1 = etab[at(g, i - 1, j)], eta2 = etab[at(g, i, j)];
+    const double vx3 = -(eta1 + eta2) * g.idy2 - 2.0 * (etaA + etaB) * g.idx2;
+    return 2.0 * etaA * g.idx2 * vx(i, j - 1) + eta1 * g.idy2 * vx(i - 1, j) + vx3 * vx(i, j) +
+           eta2 * g.idy2 * vx(i + 1, j) + 2.0 * etaB * g.idx2 * vx(i, j + 1) +
+           g.idxdy * (eta1 * (vy(i - 1, j) - vy(i - 1, j + 1)) + eta2 * (vy(i, j + 1) - vy(i, j)));
+}
+// y-momentum row at vy(i,j) (reading R2, "the same procedure"): the mirror of
+// the Listing, from sigma'_yy at P nodes and sigma'_xy at basic nodes.
+template <class VX, class VY>
+__device__ __forceinline__ double ly_row(const GridL &g, const double *__restrict__ etab,
+                                         const double *__restrict__ etap, const VX &vx, const VY &vy, int i, int j) {
+    const double etaN = etap[at(g, i, j)], etaS = etap[at(g, i + 1, j)];
+    const double etaW = etab[at(g, i, j - 1)], etaE = etab[at(g, i, j)];
+    const double vy3 = -2.0 * (etaN + etaS) * g.idy2 - (etaW + etaE) * g.idx2;
+    return 2.0 * etaS * g.idy2 * vy(i + 1, j) + 2.0 * etaN * g.idy2 * vy(i - 1, j) + etaE * g.idx2 * vy(i, j + 1) +
+           etaW * g.idx2 * vy(i, j - 1) + vy3 * vy(i, j) +
+           g.idxdy * (etaE * (vx(i + 1, j) - vx(i, j)) - etaW * (vx(i + 1, j - 1) - vx(i, j - 1)));
+}
+// a_ii of the BC-folded operator (reading R5; Eq. jacobi_update, diag(-L) PAPER.md:1615)
+__device__ __forceinline__ double lx_diag(const GridL &g, const double *__restrict__ etab,
+                                          const double *__restrict__ etap, int i, int j) {
+    const double eta1 = etab[at(g, i - 1, j)], eta2 = etab[at(g, i, j)];
+    double a = -(eta1 + eta2) * g.idy2 - 2.0 * (etap[at(g, i, j)] + etap[at(g, i, j + 1)]) * g.idx2;
+    if (i == 1) a += g.sN * eta1 * g.idy2;
+    if (i == g.ncy) a += g.sS * eta2 * g.idy2;
+    return a;
+}
+__device__ __forceinline__ double ly_diag(const GridL &g, const double *__restrict__ etab,
+                                          const double *__restrict__ etap, int i, int j) {
+    const double etaW = etab[at(g, i, j - 1)], etaE = etab[at(g, i, j)];
+    double a = -2.0 * (etap[at(g, i, j)] + etap[at(g, i + 1, j)]) * g.idy2 - (etaW + etaE) * g.idx2;
+    if (j == 1) a += g.sW * etaW * g.idx2;
+    if (j == g.ncx) a += g.sE * etaE * g.idx2;
+    return a;
+}
+// right-hand side of the velocity equation at a vx / vy node:
+//   RHS_ARRAYS: b;  RHS_FINE: f - G p with f = -g rho (reading R4/R23), G p = -grad_h p
+__device__ __forceinline__ double rhs_x(const GridL &g, const RhsArgs &r, int i, int j) {
+    if (r.mode == RHS_ARRAYS) return r.bx[at(g, i, j)];
+    double f = 0.0;
+    if (r.gx != 0.0) f = -r.gx * (0.5 * (r.rho[at(g, i - 1, j)] + r.rho[at(g, i, j)]));
+    return f - (r.p[at(g, i, j)] - r.p[at(g, i, j + 1)]) * g.idx;
+}
+__device__ __forceinline__ double rhs_y(const GridL &g, const RhsArgs &r, int i, int j) {
+    if (r.mode == RHS_ARRAYS) return r.by[at(g, i, j)];
+    double f = 0.0;
+    if (r.gy != 0.0) f = -r.gy * (0.5 * (r.rho[at(g, i, j - 1)] + r.rho[at(g, i, j)]));
+    return f - (r.p[at(g, i, j)] - r.p[at(g, i + 1, j)]) * g.idy;
+}
+
+// deterministic block sum (fixed xor-shuffle tree + fixed warp order); result valid in thread 0
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+    const int t = threadIdx.x + threadIdx.y * blockDim.x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((t & 31) == 0) sh[t >> 5] = v;
+    __syncthreads();
+    if (t < 32) {
+        v = (t < NT / 32) ? sh[t] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    __syncthreads();
+    return v;
+}
+
+// ------------------------------------------------------------------ smoother (a4)
+// Damped Jacobi, Eq. damped_jacobi: v <- v + omega (b - L v)_i / a_ii,
+// reads only the old iterate (ping-pong buffers).  zero_in: the old iterate is 0 (first
+// sweep of a coarse correction), so v_in is not read.
+template <bool ZERO>
+__global__ void __launch_bounds__(BX *BY) k_jacobi(GridL g, const double *__restrict__ etab,
+                                                   const double *__restrict__ etap, const double *__restrict__ vxi,
+                                                   const double *__restrict__ vyi, double *__restrict__ vxo,
+                                                   double *__restrict__ vyo, RhsArgs rhs, double omega) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i > g.ncy || j > g.ncx) return;
+    const ArrayAcc ax{vxi, (size_t)g.P}, ay{vyi, (size_t)g.P};
+    if (j < g.ncx) {
+        const double a = lx_diag(g, etab, etap, i, j);
+        const double b = rhs_x(g, rhs, i, j);
+        double vn;
+        if (ZERO) vn = omega * b / a;
+        else vn = ax(i, j) + omega * (b - lx_row(g, etab, etap, ax, ay, i, j)) / a;
+        vxo[at(g, i, j)] = vn;
+        if (i == 1) vxo[at(g, 0, j)] = g.sN * vn;
+        if (i == g.ncy) vxo[at(g, g.ncy + 1, j)] = g.sS * vn;
+    }
+    if (i < g.ncy) {
+        const double a = ly_diag(g, etab, etap, i, j);
+        const double b = rhs_y(g, rhs, i, j);
+        double vn;
+        if (ZERO) vn = omega * b / a;
+        else vn = ay(i, j) + omega * (b - ly_row(g, etab, etap, ax, ay, i, j)) / a;
+        vyo[at(g, i, j)] = vn;
+        if (j == 1) vyo[at(g, i, 0)] = g.sW * vn;
+        if (j == g.ncx) vyo[at(g, i, g.ncx + 1)] = g.sE * vn;
+    }
+}
+
+// Damped red-black Gauss-Seidel (Eq. sor_update), one of the four phases
+// (reading R11): component comp (0 vx, 1 vy), colour = (i+j) mod 2 on level indices.
+// Unknowns of one phase never read each other, so the phase is parallel and in place.
+__global__ void __launch_bounds__(BX *BY) k_rbgs_phase(GridL g, const double *__restrict__ etab,
+                                                       const double *__restrict__ etap, double *vx, double *vy,
+                                                       RhsArgs rhs, double omega, int comp, int colour) {
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    const int j = 2 * (blockIdx.x * BX + threadIdx.x) + 1 + ((i + 1 + colour) & 1);
+    const ArrayAcc ax{vx, (size_t)g.P}, ay{vy, (size_t)g.P};
+    if (comp == 0) {
+        if (i > g.ncy || j > g.ncx - 1) return;
+        const double a = lx_diag(g, etab, etap, i, j);
+        const double vn = ax(i, j) + omega * (rhs_x(g, rhs, i, j) - lx_row(g, etab, etap, ax, ay, i, j)) / a;
+        vx[at(g, i, j)] = vn;
+        if (i == 1) vx[at(g, 0, j)] = g.sN * vn;
+        if (i == g.ncy) vx[at(g, g.ncy + 1, j)] = g.sS * vn;
+    } else {
+        if (i > g.ncy - 1 || j > g.ncx) return;
+        const double a = ly_diag(g, etab, etap, i, j);
+        const double vn = ay(i, j) + omega * (rhs_y(g, rhs, i, j) - ly_row(g, etab, etap, ax, ay, i, j)) / a;
+        vy[at(g, i, j)] = vn;
+        if (j == 1) vy[at(g, i, 0)] = g.sW * vn;
+        if (j == g.ncx) vy[at(g, i, g.ncx + 1)] = g.sE * vn;
+    }
+}
+
+// r = b - L v (Eq. mg_residual) at the unknowns of a level.
+__global__ void __launch_bounds__(BX *BY) k_residual(GridL g, const double *__restrict__ etab,
+                                                     const double *__restrict__ etap, const double *__restrict__ vx,
+                                                     const double *__restrict__ vy, RhsArgs rhs,
+                                                     double *__restrict__ rx, double *__restrict__ ry) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i > g.ncy || j > g.ncx) return;
+    const ArrayAcc ax{vx, (size_t)g.P}, ay{vy, (size_t)g.P};
+    if (j < g.ncx) rx[at(g, i, j)] = rhs_x(g, rhs, i, j) - lx_row(g, etab, etap, ax, ay, i, j);
+    if (i < g.ncy) ry[at(g, i, j)] = rhs_y(g, rhs, i, j) - ly_row(g, etab, etap, ax, ay, i, j);
+}
+
+// ------------------------------------------------------------------ transfers (a5, a6, a7)
+// Normalised bilinear restriction (Alg. 2 weights; reading R6) in
+// gather form: each coarse node sums its own fine contributors, so neither the 4-colour
+// schedule of Alg. 2 nor atomics are needed.  For factor 2 the hat weights are
+// [1/2, 1, 1/2] along a vertex-centred axis and [1/4, 3/4, 3/4, 1/4] along a cell-centred
+// axis; contributors outside the closed domain (mirror / ghost nodes) are dropped and the
+// sum of the remaining weights renormalises.
+__device__ __forceinline__ double W4(int d) { return (d == 0 || d == 3) ? 0.25 : 0.75; }
+
+__global__ void k_restrict_vel(GridL gf, GridL gc, const double *__restrict__ rx, const double *__restrict__ ry,
+                               double *__restrict__ bxc, double *__restrict__ byc) {
+    const int J = blockIdx.x * BX + threadIdx.x + 1;
+    const int I = blockIdx.y * BY + threadIdx.y + 1;
+    if (I > gc.ncy || J > gc.ncx) return;
+    if (bxc && J < gc.ncx) {  // vx: x vertex-centred, y cell-centred
+        double s = 0.0, w = 0.0;
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const int i = 2 * I - 2 + d;
+            if (i < 1 || i > gf.ncy) continue;
+            const double row = 0.5 * rx[at(gf, i, 2 * J - 1)] + rx[at(gf, i, 2 * J)] + 0.5 * rx[at(gf, i, 2 * J + 1)];
+            s += W4(d) * row;
+            w += W4(d);
+        }
+        bxc[at(gc, I, J)] = s / (2.0 * w);
+    }
+    if (byc && I < gc.ncy) {  // vy: x cell-centred, y vertex-centred
+        double s = 0.0, w = 0.0;
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const int j = 2 * J - 2 + d;
+            if (j < 1 || j > gf.ncx) continue;
+            const double col = 0.5 * ry[at(gf, 2 * I - 1, j)] + ry[at(gf, 2 * I, j)] + 0.5 * ry[at(gf, 2 * I + 1, j)];
+            s += W4(d) * col;
+            w += W4(d);
+        }
+        byc[at(gc, I, J)] = s / (2.0 * w);
+    }
+}
+// basic-node field (eta_b): [1/2,1,1/2] x [1/2,1,1/2] over fine basic nodes in [0,ncy]x[0,ncx]
+__global__ void k_restrict_b(GridL gf, GridL gc, const double *__restrict__ f, double *__restrict__ c) {
+    const int J = blockIdx.x * BX + threadIdx.x;
+    const int I = blockIdx.y * BY + threadIdx.y;
+    if (I > gc.ncy || J > gc.ncx) return;
+    const double w3[3] = {0.5, 1.0, 0.5};
+    double s = 0.0, wy = 0.0, wx = 0.0;
+    for (int dj = 0; dj < 3; ++dj) {
+        const int j = 2 * J - 1 + dj;
+        if (j >= 0 && j <= gf.ncx) wx += w3[dj];
+    }
+    for (int di = 0; di < 3; ++di) {
+        const int i = 2 * I - 1 + di;
+        if (i < 0 || i > gf.ncy) continue;
+        wy += w3[di];
+        double row = 0.0;
+        for (int dj = 0; dj < 3; ++dj) {
+            const int j = 2 * J - 1 + dj;
+            if (j < 0 || j > gf.ncx) continue;
+            row += w3[dj] * f[at(gf, i, j)];
+        }
+        s += w3[di] * row;
+    }
+    c[at(gc, I, J)] = s / (wy * wx);
+}
+// P-node field (eta_p): [1,3,3,1]/8 per axis over fine P nodes in [1,ncy]x[1,ncx]
+__global__ void k_restrict_p(GridL gf, GridL gc, const double *__restrict__ f, double *__restrict__ c) {
+    const int J = blockIdx.x * BX + threadIdx.x + 1;
+    const int I = blockIdx.y * BY + threadIdx.y + 1;
+    if (I > gc.ncy || J > gc.ncx) return;
+    double s = 0.0, wy = 0.0, wx = 0.0;
+    for (int dj = 0; dj < 4; ++dj) {
+        const int j = 2 * J - 2 + dj;
+        if (j >= 1 && j <= gf.ncx) wx += W4(dj);
+    }
+    for (int di = 0; di < 4; ++di) {
+        const int i = 2 * I - 2 + di;
+        if (i < 1 || i > gf.ncy) continue;
+        wy += W4(di);
+        double row = 0.0;
+        for (int dj = 0; dj < 4; ++dj) {
+            const int j = 2 * J - 2 + dj;
+            if (j < 1 || j > gf.ncx) continue;
+            row += W4(dj) * f[at(gf, i, j)];
+        }
+        s += W4(di) * row;
+    }
+    c[at(gc, I, J)] = s / (wy * wx);
+}
+
+// Bilinear prolongation + correction: each fine unknown adds the
+// hat-weighted coarse correction of its (up to) four surrounding coarse nodes; coarse
+// mirror nodes hold the homogeneous-BC image, coarse walls are 0 (Appendix B).
+__global__ void __launch_bounds__(BX *BY) k_prolong(GridL gf, GridL gc, const double *__restrict__ ex,
+                                                    const double *__restrict__ ey, double *__restrict__ vx,
+                                                    double *__restrict__ vy) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i > gf.ncy || j > gf.ncx) return;
+    if (j < gf.ncx) {  // vx: x vertex-centred, y cell-centred
+        const int J0 = j >> 1;
+        int I0;
+        double wy0, wy1;
+        if (i & 1) { I0 = (i + 1) / 2 - 1; wy0 = 0.25; wy1 = 0.75; }
+        else { I0 = i / 2; wy0 = 0.75; wy1 = 0.25; }
+        double s;
+        if (j & 1)
+            s = wy0 * 0.5 * (ex[at(gc, I0, J0)] + ex[at(gc, I0, J0 + 1)]) +
+                wy1 * 0.5 * (ex[at(gc, I0 + 1, J0)] + ex[at(gc, I0 + 1, J0 + 1)]);
+        else
+            s = wy0 * ex[at(gc, I0, J0)] + wy1 * ex[at(gc, I0 + 1, J0)];
+        const double vn = vx[at(gf, i, j)] + s;
+        vx[at(gf, i, j)] = vn;
+        if (i == 1) vx[at(gf, 0, j)] = gf.sN * vn;
+        if (i == gf.ncy) vx[at(gf, gf.ncy + 1, j)] = gf.sS * vn;
+    }
+    if (i < gf.ncy) {  // vy: y vertex-centred, x cell-centred
+        const int I0 = i >> 1;
+        int J0;
+        double wx0, wx1;
+        if (j & 1) { J0 = (j + 1) / 2 - 1; wx0 = 0.25; wx1 = 0.75; }
+        else { J0 = j / 2; wx0 = 0.75; wx1 = 0.25; }
+        double s;
+        if (i & 1)
+            s = wx0 * 0.5 * (ey[at(gc, I0, J0)] + ey[at(gc, I0 + 1, J0)]) +
+                wx1 * 0.5 * (ey[at(gc, I0, J0 + 1)] + ey[at(gc, I0 + 1, J0 + 1)]);
+        else
+            s = wx0 * ey[at(gc, I0, J0)] + wx1 * ey[at(gc, I0, J0 + 1)];
+        const double vn = vy[at(gf, i, j)] + s;
+        vy[at(gf, i, j)] = vn;
+        if (j == 1) vy[at(gf, i, 0)] = gf.sW * vn;
+        if (j == gf.ncx) vy[at(gf, i, gf.ncx + 1)] = gf.sE * vn;
+    }
+}
+
+// ------------------------------------------------------------------ residual + energy (a3)
+// Full saddle residual r_v = f - L v - G p, r_p = -D v and the
+// per-block partial sums Sv = sum r_v^2 / (-a_ii), Sp = sum r_p^2 eta_p / (2/dx^2+2/dy^2).
+__global__ void __launch_bounds__(BX *BY) k_energy(GridL g, const double *__restrict__ etab,
+                                                   const double *__restrict__ etap, const double *__restrict__ vx,
+                                                   const double *__restrict__ vy, const double *__restrict__ p,
+                                                   const double *__restrict__ rho, double gx, double gy,
+                                                   double *__restrict__ rxo, double *__restrict__ ryo,
+                                                   double *__restrict__ rpo, double *__restrict__ partials,
+                                                   int force_only) {
+    __shared__ double sh[BX * BY / 32];
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    double sv = 0.0, sp = 0.0;
+    if (i <= g.ncy && j <= g.ncx) {
+        const ArrayAcc ax{vx, (size_t)g.P}, ay{vy, (size_t)g.P};
+        RhsArgs rhs;
+        rhs.mode = RHS_FINE;
+        rhs.p = p;
+        rhs.rho = rho;
+        rhs.gx = gx;
+        rhs.gy = gy;
+        rhs.bx = rhs.by = nullptr;
+        if (j < g.ncx) {
+            const double a = lx_diag(g, etab, etap, i, j);
+            double r;
+            if (force_only) r = (gx != 0.0) ? -gx * (0.5 * (rho[at(g, i - 1, j)] + rho[at(g, i, j)])) : 0.0;
+            else r = rhs_x(g, rhs, i, j) - lx_row(g, etab, etap, ax, ay, i, j);
+            sv += r * r / (-a);
+            if (rxo) rxo[at(g, i, j)] = r;
+        }
+        if (i < g.ncy) {
+            const double a = ly_diag(g, etab, etap, i, j);
+            double r;
+            if (force_only) r = (gy != 0.0) ? -gy * (0.5 * (rho[at(g, i, j - 1)] + rho[at(g, i, j)])) : 0.0;
+            else r = rhs_y(g, rhs, i, j) - ly_row(g, etab, etap, ax, ay, i, j);
+            sv += r * r / (-a);
+            if (ryo) ryo[at(g, i, j)] = r;
+        }
+        if (!force_only) {
+            const double rp = -((vx[at(g, i, j)] - vx[at(g, i, j - 1)]) * g.idx + (vy[at(g, i, j)] - vy[at(g, i - 1, j)]) * g.idy);
+            sp = rp * rp * (etap[at(g, i, j)] / (2.0 * g.idx2 + 2.0 * g.idy2));
+            if (rpo) rpo[at(g, i, j)] = rp;
+        }
+    }
+    sv = block_sum<BX * BY>(sv, sh);
+    sp = block_sum<BX * BY>(sp, sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        const size_t b = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+        partials[2 * b] = sv;
+        partials[2 * b + 1] = sp;
+    }
+}
+// energy of a given residual vector (GCR recursive residual)
+__global__ void __launch_bounds__(BX *BY) k_energy_vec(GridL g, const double *__restrict__ etab,
+                                                       const double *__restrict__ etap, const double *__restrict__ rx,
+                                                       const double *__restrict__ ry, const double *__restrict__ rp,
+                                                       double *__restrict__ partials) {
+    __shared__ double sh[BX * BY / 32];
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    double sv = 0.0, sp = 0.0;
+    if (i <= g.ncy && j <= g.ncx) {
+        if (j < g.ncx) { const double r = rx[at(g, i, j)]; sv += r * r / (-lx_diag(g, etab, etap, i, j)); }
+        if (i < g.ncy) { const double r = ry[at(g, i, j)]; sv += r * r / (-ly_diag(g, etab, etap, i, j)); }
+        const double r = rp[at(g, i, j)];
+        sp = r * r * (etap[at(g, i, j)] / (2.0 * g.idx2 + 2.0 * g.idy2));
+    }
+    sv = block_sum<BX * BY>(sv, sh);
+    sp = block_sum<BX * BY>(sp, sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        const size_t b = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+        partials[2 * b] = sv;
+        partials[2 * b + 1] = sp;
+    }
+}
+
+// ------------------------------------------------------------------ pressure update (a10)
+// Uzawa pressure step, reading R3: p <- p + alpha eta_P r_p with r_p = -D v (PAPER.md:824
+// with the physical sign), applied to the stored p minus the previous mean: the zero-mean
+// projection is inert for v and E (G 1 = 0), so it is applied one step
+// late and at the output; per-block partial sums of the new p give the next mean.
+__global__ void __launch_bounds__(BX *BY) k_pupdate(GridL g, const double *__restrict__ etap,
+                                                    const double *__restrict__ vx, const double *__restrict__ vy,
+                                                    double *__restrict__ p, double alpha_signed,
+                                                    const double *__restrict__ mshift, double *__restrict__ partials) {
+    __shared__ double sh[BX * BY / 32];
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    double s = 0.0;
+    if (i <= g.ncy && j <= g.ncx) {
+        const double dv = (vx[at(g, i, j)] - vx[at(g, i, j - 1)]) * g.idx + (vy[at(g, i, j)] - vy[at(g, i - 1, j)]) * g.idy;
+        const double pn = (p[at(g, i, j)] - *mshift) + alpha_signed * etap[at(g, i, j)] * (-dv);
+        p[at(g, i, j)] = pn;
+        s = pn;
+    }
+    s = block_sum<BX * BY>(s, sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) partials[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+}
+
+// ------------------------------------------------------------------ deterministic finalisation
+__global__ void __launch_bounds__(1024) k_finalize(const double *__restrict__ partials, int nblocks, int ncomp,
+                                                   double scale, double *__restrict__ out) {
+    __shared__ double sh[32];
+    for (int c = 0; c < ncomp; ++c) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < nblocks; b += 1024) s += partials[(size_t)b * ncomp + c];
+        s = block_sum<1024>(s, sh);
+        if (threadIdx.x == 0) out[c] = scale * s;
+    }
+}
+__global__ void __launch_bounds__(1024) k_energy_final(const double *__restrict__ partials, int nblocks,
+                                                       const double *__restrict__ Sf, double *__restrict__ out) {
+    __shared__ double sh[32];
+    double s0 = 0.0, s1 = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += 1024) {
+        s0 += partials[2 * (size_t)b];
+        s1 += partials[2 * (size_t)b + 1];
+    }
+    s0 = block_sum<1024>(s0, sh);
+    s1 = block_sum<1024>(s1, sh);
+    if (threadIdx.x == 0) {
+        out[1] = s0;
+        out[2] = s1;
+        out[0] = (Sf[0] > 0.0) ? sqrt((s0 + s1) / Sf[0]) : 0.0;
+    }
+}
+
+// ------------------------------------------------------------------ layout conversion
+// user -> padded velocity: unknowns copied, walls 0, mirrors from partners
+__global__ void k_in_velocity(GridL g, const double *__restrict__ ux, const double *__restrict__ uy,
+                              double *__restrict__ vx, double *__restrict__ vy) {
+    const int j = blockIdx.x * BX + threadIdx.x;  // 0..ncx+1
+    const int i = blockIdx.y * BY + threadIdx.y;  // 0..ncy+1
+    if (i > g.ncy + 1 || j > g.ncx + 1) return;
+    // vx
+    {
+        double v = 0.0;
+        if (j >= 1 && j <= g.ncx - 1) {
+            if (i >= 1 && i <= g.ncy) v = ux[(size_t)(i - 1) * (g.ncx + 1) + j];
+            else if (i == 0) v = g.sN * ux[(size_t)0 * (g.ncx + 1) + j];
+            else v = g.sS * ux[(size_t)(g.ncy - 1) * (g.ncx + 1) + j];
+        }
+        if (j <= g.ncx) vx[at(g, i, j)] = v;
+    }
+    // vy
+    {
+        double v = 0.0;
+        if (i >= 1 && i <= g.ncy - 1) {
+            if (j >= 1 && j <= g.ncx) v = uy[(size_t)i * g.ncx + (j - 1)];
+            else if (j == 0) v = g.sW * uy[(size_t)i * g.ncx + 0];
+            else v = g.sE * uy[(size_t)i * g.ncx + (g.ncx - 1)];
+        }
+        if (i <= g.ncy) vy[at(g, i, j)] = v;
+    }
+}
+__global__ void k_in_p(GridL g, const double *__restrict__ u, double *__restrict__ a) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i <= g.ncy && j <= g.ncx) a[at(g, i, j)] = u[(size_t)(i - 1) * g.ncx + (j - 1)];
+}
+__global__ void k_in_b(GridL g, const double *__restrict__ u, double *__restrict__ a) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y;
+    if (i <= g.ncy && j <= g.ncx) a[at(g, i, j)] = u[(size_t)i * (g.ncx + 1) + j];
+}
+__global__ void k_in_vx_raw(GridL g, const double *__restrict__ u, double *__restrict__ a) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i <= g.ncy && j <= g.ncx) a[at(g, i, j)] = (j == 0 || j == g.ncx) ? 0.0 : u[(size_t)(i - 1) * (g.ncx + 1) + j];
+}
+__global__ void k_in_vy_raw(GridL g, const double *__restrict__ u, double *__restrict__ a) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y;
+    if (i <= g.ncy && j <= g.ncx) a[at(g, i, j)] = (i == 0 || i == g.ncy) ? 0.0 : u[(size_t)i * g.ncx + (j - 1)];
+}
+__global__ void k_out_vx(GridL g, const double *__restrict__ a, double *__restrict__ u) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i <= g.ncy && j <= g.ncx)
+        u[(size_t)(i - 1) * (g.ncx + 1) + j] = (j == 0 || j == g.ncx) ? 0.0 : a[at(g, i, j)];
+}
+__global__ void k_out_vy(GridL g, const double *__restrict__ a, double *__restrict__ u) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y;
+    if (i <= g.ncy && j <= g.ncx) u[(size_t)i * g.ncx + (j - 1)] = (i == 0 || i == g.ncy) ? 0.0 : a[at(g, i, j)];
+}
+__global__ void k_out_p(GridL g, const double *__restrict__ a, double *__restrict__ u, const double *shift) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i <= g.ncy && j <= g.ncx) u[(size_t)(i - 1) * g.ncx + (j - 1)] = a[at(g, i, j)] - (shift ? *shift : 0.0);
+}
+__global__ void k_out_b(GridL g, const double *__restrict__ a, double *__restrict__ u) {
+    const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y;
+    if (i <= g.ncy && j <= g.ncx) u[(size_t)i * (g.ncx + 1) + j] = a[at(g, i, j)];
+}
+// A x in user layout: ax, ay = L v + G p (walls 0), ap = D v  (a2)
+__global__ void __launch_bounds__(BX *BY) k_apply(GridL g, const double *__restrict__ etab,
+                                                  const double *__restrict__ etap, const double *__restrict__ vx,
+                                                  const double *__restrict__ vy, const double *__restrict__ p,
+                                                  double *__restrict__ ax, double *__restrict__ ay,
+                                                  double *__restrict__ ap) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i > g.ncy || j > g.ncx) return;
+    const ArrayAcc axx{vx, (size_t)g.P}, ayy{vy, (size_t)g.P};
+    const size_t wx = g.ncx + 1, wy = g.ncx;
+    if (j < g.ncx)
+        ax[(size_t)(i - 1) * wx + j] = lx_row(g, etab, etap, axx, ayy, i, j) + (p[at(g, i, j)] - p[at(g, i, j + 1)]) * g.idx;
+    else
+        ax[(size_t)(i - 1) * wx + g.ncx] = 0.0;
+    if (j == 1) ax[(size_t)(i - 1) * wx] = 0.0;
+    if (i < g.ncy)
+        ay[(size_t)i * wy + (j - 1)] = ly_row(g, etab, etap, axx, ayy, i, j) + (p[at(g, i, j)] - p[at(g, i + 1, j)]) * g.idy;
+    else
+        ay[(size_t)g.ncy * wy + (j - 1)] = 0.0;
+    if (i == 1) ay[(size_t)(j - 1)] = 0.0;
+    ap[(size_t)(i - 1) * g.ncx + (j - 1)] =
+        (vx[at(g, i, j)] - vx[at(g, i, j - 1)]) * g.idx + (vy[at(g, i, j)] - vy[at(g, i - 1, j)]) * g.idy;
+}
+// same, padded outputs (GCR: w = A z)
+__global__ void __launch_bounds__(BX *BY) k_apply_padded(GridL g, const double *__restrict__ etab,
+                                                         const double *__restrict__ etap, const double *__restrict__ vx,
+                                                         const double *__restrict__ vy, const double *__restrict__ p,
+                                                         double *__restrict__ ax, double *__restrict__ ay,
+                                                         double *__restrict__ ap) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i > g.ncy || j > g.ncx) return;
+    const ArrayAcc axx{vx, (size_t)g.P}, ayy{vy, (size_t)g.P};
+    if (j < g.ncx) ax[at(g, i, j)] = lx_row(g, etab, etap, axx, ayy, i, j) + (p[at(g, i, j)] - p[at(g, i, j + 1)]) * g.idx;
+    if (i < g.ncy) ay[at(g, i, j)] = ly_row(g, etab, etap, axx, ayy, i, j) + (p[at(g, i, j)] - p[at(g, i + 1, j)]) * g.idy;
+    ap[at(g, i, j)] = (vx[at(g, i, j)] - vx[at(g, i, j - 1)]) * g.idx + (vy[at(g, i, j)] - vy[at(g, i - 1, j)]) * g.idy;
+}
+// materialise b = f - G p (RHS_FINE) or copy b (RHS_ARRAYS) at the unknowns
+__global__ void k_make_rhs(GridL g, RhsArgs rhs, double *__restrict__ bx, double *__restrict__ by) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i > g.ncy || j > g.ncx) return;
+    if (j < g.ncx) bx[at(g, i, j)] = rhs_x(g, rhs, i, j);
+    if (i < g.ncy) by[at(g, i, j)] = rhs_y(g, rhs, i, j);
+}
+__global__ void k_refresh_mirrors(GridL g, double *__restrict__ vx, double *__restrict__ vy) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 1 && t <= g.ncx - 1) {
+        vx[at(g, 0, t)] = g.sN * vx[at(g, 1, t)];
+        vx[at(g, g.ncy + 1, t)] = g.sS * vx[at(g, g.ncy, t)];
+    }
+    if (t >= 1 && t <= g.ncy - 1) {
+        vy[at(g, t, 0)] = g.sW * vy[at(g, t, 1)];
+        vy[at(g, t, g.ncx + 1)] = g.sE * vy[at(g, t, g.ncx)];
+    }
+}
+__global__ void k_count_nonpos(const double *__restrict__ a, size_t n, int *count) {
+    int c = 0;
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x)
+        c += !(a[k] > 0.0);
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+// ------------------------------------------------------------------ coarsest level (a8)
+// value of the unit vector e_c at padded node (i, j), mirror relations and walls folded
+__device__ __forceinline__ int vx_unknown(const GridL &g, int i, int j) { return (i - 1) * (g.ncx - 1) + (j - 1); }
+__device__ __forceinline__ int vy_unknown(const GridL &g, int i, int j) {
+    return g.ncy * (g.ncx - 1) + (i - 1) * g.ncx + (j - 1);
+}
+struct UnitVX {
+    GridL g;
+    int c;
+    __device__ double operator()(int i, int j) const {
+        if (j <= 0 || j >= g.ncx) return 0.0;
+        double s = 1.0;
+        if (i == 0) { i = 1; s = g.sN; }
+        else if (i == g.ncy + 1) { i = g.ncy; s = g.sS; }
+        return vx_unknown(g, i, j) == c ? s : 0.0;
+    }
+};
+struct UnitVY {
+    GridL g;
+    int c;
+    __device__ double operator()(int i, int j) const {
+        if (i <= 0 || i >= g.ncy) return 0.0;
+        double s = 1.0;
+        if (j == 0) { j = 1; s = g.sW; }
+        else if (j == g.ncx + 1) { j = g.ncx; s = g.sE; }
+        return vy_unknown(g, i, j) == c ? s : 0.0;
+    }
+};
+__global__ void k_coarse_assemble(GridL g, const double *__restrict__ etab, const double *__restrict__ etap,
+                                  double *__restrict__ M, int n) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;  // column (unit vector)
+    const int r = blockIdx.y;                              // row
+    if (c >= n) return;
+    const UnitVX ux{g, c};
+    const UnitVY uy{g, c};
+    const int nvx = g.ncy * (g.ncx - 1);
+    double v;
+    if (r < nvx) {
+        const int i = r / (g.ncx - 1) + 1, j = r % (g.ncx - 1) + 1;
+        v = lx_row(g, etab, etap, ux, uy, i, j);
+    } else {
+        const int rr = r - nvx;
+        const int i = rr / g.ncx + 1, j = rr % g.ncx + 1;
+        v = ly_row(g, etab, etap, ux, uy, i, j);
+    }
+    M[(size_t)r * n + c] = -v;  // -L_c (SPD)
+}
+// Gauss-Jordan inverse of the SPD matrix M (n x n, row-major), one CTA; no pivoting needed
+// for SPD.  A = [M | I] in `work` (n x 2n).  Setup-time only.
+__global__ void __launch_bounds__(1024) k_coarse_invert(double *__restrict__ work, double *__restrict__ Minv, int n,
+                                                        int *fail) {
+    extern __shared__ double sm[];
+    double *colk = sm;       // n
+    double *rowk = sm + n;   // 2n
+    const int n2 = 2 * n;
+    for (int k = 0; k < n; ++k) {
+        const double piv = work[(size_t)k * n2 + k];
+        if (!(piv > 0.0)) {
+            if (threadIdx.x == 0) *fail = 1;
+            return;
+        }
+        for (int t = threadIdx.x; t < n; t += blockDim.x) colk[t] = work[(size_t)t * n2 + k];
+        for (int t = threadIdx.x; t < n2; t += blockDim.x) rowk[t] = work[(size_t)k * n2 + t] / piv;
+        __syncthreads();
+        for (size_t e = threadIdx.x; e < (size_t)n * n2; e += blockDim.x) {
+            const int r = (int)(e / n2), cc = (int)(e % n2);
+            if (r == k) work[e] = rowk[cc];
+            else work[e] -= colk[r] * rowk[cc];
+        }
+        __syncthreads();
+    }
+    for (size_t e = threadIdx.x; e < (size_t)n * n; e += blockDim.x) {
+        const int r = (int)(e / n), cc = (int)(e % n);
+        Minv[e] = work[(size_t)r * n2 + n + cc];
+    }
+}
+// v = L_c^-1 b = -(-L_c)^-1 b on the coarsest unknowns; mirrors written.
+__global__ void __launch_bounds__(256) k_coarse_solve(GridL g, const double *__restrict__ Minv, int n,
+                                                      const double *__restrict__ bx, const double *__restrict__ by,
+                                                      double *__restrict__ vx, double *__restrict__ vy) {
+    extern __shared__ double u[];
+    const int nvx = g.ncy * (g.ncx - 1);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        if (k < nvx) u[k] = bx[at(g, k / (g.ncx - 1) + 1, k % (g.ncx - 1) + 1)];
+        else u[k] = by[at(g, (k - nvx) / g.ncx + 1, (k - nvx) % g.ncx + 1)];
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < n; ++c) s += Minv[(size_t)r * n + c] * u[c];
+        const double v = -s;
+        if (r < nvx) {
+            const int i = r / (g.ncx - 1) + 1, j = r % (g.ncx - 1) + 1;
+            vx[at(g, i, j)] = v;
+            if (i == 1) vx[at(g, 0, j)] = g.sN * v;
+            if (i == g.ncy) vx[at(g, g.ncy + 1, j)] = g.sS * v;
+        } else {
+            const int i = (r - nvx) / g.ncx + 1, j = (r - nvx) % g.ncx + 1;
+            vy[at(g, i, j)] = v;
+            if (j == 1) vy[at(g, i, 0)] = g.sW * v;
+            if (j == g.ncx) vy[at(g, i, g.ncx + 1)] = g.sE * v;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ GCR vector kernels (a11)
+// Euclidean inner products over the unknowns (vx, vy, p) (reading R13), nd pairs at once.
+constexpr int MAXD = 12;
+struct DotArgs {
+    const double *a[MAXD][3];
+    const double *b[MAXD][3];
+    int nd;
+};
+__global__ void __launch_bounds__(BX *BY) k_dots(GridL g, DotArgs d, double *__restrict__ partials) {
+    __shared__ double sh[BX * BY / 32];
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    const bool in = (i <= g.ncy && j <= g.ncx);
+    const size_t q = in ? at(g, i, j) : 0;
+    const size_t blk = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+    for (int k = 0; k < d.nd; ++k) {
+        double s = 0.0;
+        if (in) {
+            if (j < g.ncx) s += d.a[k][0][q] * d.b[k][0][q];
+            if (i < g.ncy) s += d.a[k][1][q] * d.b[k][1][q];
+            s += d.a[k][2][q] * d.b[k][2][q];
+        }
+        s = block_sum<BX * BY>(s, sh);
+        if (threadIdx.x == 0 && threadIdx.y == 0) partials[blk * d.nd + k] = s;
+    }
+}
+// y += sign * coef[idx] * x over unknowns (+ mirrors of velocity, linear)
+__global__ void __launch_bounds__(BX *BY) k_axpy3(GridL g, const double *__restrict__ coef, int idx, double sgn,
+                                                  const double *__restrict__ xx, const double *__restrict__ xy,
+                                                  const double *__restrict__ xp, double *__restrict__ yx,
+                                                  double *__restrict__ yy, double *__restrict__ yp) {
+    const int j = blockIdx.x * BX + threadIdx.x;  // include mirrors: 0..ncx+1
+    const int i = blockIdx.y * BY + threadIdx.y;
+    if (i > g.ncy + 1 || j > g.ncx + 1) return;
+    const double a = sgn * coef[idx];
+    const size_t q = at(g, i, j);
+    if (j >= 1 && j <= g.ncx - 1) yx[q] += a * xx[q];                    // vx unknowns + mirror rows
+    if (i >= 1 && i <= g.ncy - 1) yy[q] += a * xy[q];                    // vy unknowns + mirror cols
+    if (i >= 1 && i <= g.ncy && j >= 1 && j <= g.ncx) yp[q] += a * xp[q];  // P
+}
+__global__ void __launch_bounds__(BX *BY) k_scale3(GridL g, const double *__restrict__ coef, int invert_sqrt,
+                                                   double *__restrict__ x, double *__restrict__ y,
+                                                   double *__restrict__ p) {
+    const int j = blockIdx.x * BX + threadIdx.x;
+    const int i = blockIdx.y * BY + threadIdx.y;
+    if (i > g.ncy + 1 || j > g.ncx + 1) return;
+    const double a = invert_sqrt ? 1.0 / sqrt(coef[0]) : coef[0];
+    const size_t q = at(g, i, j);
+    if (j >= 1 && j <= g.ncx - 1) x[q] *= a;
+    if (i >= 1 && i <= g.ncy - 1) y[q] *= a;
+    if (i >= 1 && i <= g.ncy && j >= 1 && j <= g.ncx) p[q] *= a;
+}
+// z_p = alpha eta_P (r_p - D z_v) (preconditioner M^-1, reading R3/R14) + partial sums
+__global__ void __launch_bounds__(BX *BY) k_precond_p(GridL g, const double *__restrict__ etap,
+                                                      const double *__restrict__ zx, const double *__restrict__ zy,
+                                                      const double *__restrict__ rp, double alpha,
+                                                      double *__restrict__ zp, double *__restrict__ partials) {
+    __shared__ double sh[BX * BY / 32];
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    double s = 0.0;
+    if (i <= g.ncy && j <= g.ncx) {
+        const double dz = (zx[at(g, i, j)] - zx[at(g, i, j - 1)]) * g.idx + (zy[at(g, i, j)] - zy[at(g, i - 1, j)]) * g.idy;
+        const double v = alpha * etap[at(g, i, j)] * (rp[at(g, i, j)] - dz);
+        zp[at(g, i, j)] = v;
+        s = v;
+    }
+    s = block_sum<BX * BY>(s, sh);
+    if (threadIdx.x == 0 && threadIdx.y == 0) partials[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+}
+__global__ void k_sub_mean(GridL g, const double *__restrict__ mean, double *__restrict__ p) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i <= g.ncy && j <= g.ncx) p[at(g, i, j)] -= *mean;
+}
+
+}  // namespace
+
+// ====================================================================== launchers
+#define LAUNCH_BOOK(c) (++*(c).counter)
+static inline dim3 tpb() { return dim3(BX, BY); }
+
+void launch_jacobi(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
+                   const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega, bool zero_in) {
+    if (zero_in) k_jacobi<true><<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs, omega);
+    else k_jacobi<false><<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs, omega);
+    LAUNCH_BOOK(c);
+}
+void launch_rbgs(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *vx, double *vy,
+                 const RhsArgs &rhs, double omega) {
+    const dim3 grid((g.ncx / 2 + 1 + BX - 1) / BX, (g.ncy + BY - 1) / BY);
+    for (int comp = 0; comp < 2; ++comp)
+        for (int colour = 0; colour < 2; ++colour) {
+            k_rbgs_phase<<<grid, tpb(), 0, c.stream>>>(g, etab, etap, vx, vy, rhs, omega, comp, colour);
+            LAUNCH_BOOK(c);
+        }
+}
+void launch_residual(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vx,
+                     const double *vy, const RhsArgs &rhs, double *rx, double *ry) {
+    k_residual<<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, vx, vy, rhs, rx, ry);
+    LAUNCH_BOOK(c);
+}
+void launch_restrict_vel(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *rx, const double *ry,
+                         double *bxc, double *byc) {
+    k_restrict_vel<<<cell_grid(gc), tpb(), 0, c.stream>>>(gf, gc, rx, ry, bxc, byc);
+    LAUNCH_BOOK(c);
+}
+void launch_restrict_vx(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *f, double *cc) {
+    launch_restrict_vel(c, gf, gc, f, nullptr, cc, nullptr);
+}
+void launch_restrict_vy(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *f, double *cc) {
+    launch_restrict_vel(c, gf, gc, nullptr, f, nullptr, cc);
+}
+void launch_restrict_b(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *f, double *cc) {
+    const dim3 grid((gc.ncx + 1 + BX - 1) / BX, (gc.ncy + 1 + BY - 1) / BY);
+    k_restrict_b<<<grid, tpb(), 0, c.stream>>>(gf, gc, f, cc);
+    LAUNCH_BOOK(c);
+}
+void launch_restrict_p(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *f, double *cc) {
+    k_restrict_p<<<cell_grid(gc), tpb(), 0, c.stream>>>(gf, gc, f, cc);
+    LAUNCH_BOOK(c);
+}
+void launch_prolong(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *exc, const double *eyc,
+                    double *vx, double *vy) {
+    k_prolong<<<cell_grid(gf), tpb(), 0, c.stream>>>(gf, gc, exc, eyc, vx, vy);
+    LAUNCH_BOOK(c);
+}
+int energy_blocks(const GridL &g) {
+    const dim3 gr = cell_grid(g);
+    return (int)(gr.x * gr.y);
+}
+void launch_energy(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vx,
+                   const double *vy, const double *p, const double *rho, double gx, double gy, double *rx,
+                   double *ry, double *rp, double *partials, bool force_only) {
+    k_energy<<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, vx, vy, p, rho, gx, gy, rx, ry, rp, partials,
+                                                   force_only ? 1 : 0);
+    LAUNCH_BOOK(c);
+}
+void launch_energy_vec(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *rx,
+                       const double *ry, const double *rp, double *partials) {
+    k_energy_vec<<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, rx, ry, rp, partials);
+    LAUNCH_BOOK(c);
+}
+int pupdate_blocks(const GridL &g) { return energy_blocks(g); }
+void launch_pupdate(const LaunchCtx &c, const GridL &g, const double *etap, const double *vx, const double *vy,
+                    double *p, double alpha_signed, const double *mshift, double *partials) {
+    k_pupdate<<<cell_grid(g), tpb(), 0, c.stream>>>(g, etap, vx, vy, p, alpha_signed, mshift, partials);
+    LAUNCH_BOOK(c);
+}
+void launch_finalize(const LaunchCtx &c, const double *partials, int nblocks, int ncomp, double scale, double *out) {
+    k_finalize<<<1, 1024, 0, c.stream>>>(partials, nblocks, ncomp, scale, out);
+    LAUNCH_BOOK(c);
+}
+void launch_energy_final(const LaunchCtx &c, const double *partials, int nblocks, const double *Sf, double *out) {
+    k_energy_final<<<1, 1024, 0, c.stream>>>(partials, nblocks, Sf, out);
+    LAUNCH_BOOK(c);
+}
+void launch_in_velocity(const LaunchCtx &c, const GridL &g, const double *ux, const double *uy, double *vx,
+                        double *vy) {
+    const dim3 grid((g.ncx + 2 + BX - 1) / BX, (g.ncy + 2 + BY - 1) / BY);
+    k_in_velocity<<<grid, tpb(), 0, c.stream>>>(g, ux, uy, vx, vy);
+    LAUNCH_BOOK(c);
+}
+void launch_in_p(const LaunchCtx &c, const GridL &g, const double *u, double *a) {
+    k_in_p<<<cell_grid(g), tpb(), 0, c.stream>>>(g, u, a);
+    LAUNCH_BOOK(c);
+}
+static inline dim3 node_grid(const GridL &g) { return dim3((g.ncx + 1 + BX - 1) / BX, (g.ncy + 1 + BY - 1) / BY); }
+void launch_in_b(const LaunchCtx &c, const GridL &g, const double *u, double *a) {
+    k_in_b<<<node_grid(g), tpb(), 0, c.stream>>>(g, u, a);
+    LAUNCH_BOOK(c);
+}
+void launch_in_vx_raw(const LaunchCtx &c, const GridL &g, const double *u, double *a) {
+    k_in_vx_raw<<<node_grid(g), tpb(), 0, c.stream>>>(g, u, a);
+    LAUNCH_BOOK(c);
+}
+void launch_in_vy_raw(const LaunchCtx &c, const GridL &g, const double *u, double *a) {
+    k_in_vy_raw<<<node_grid(g), tpb(), 0, c.stream>>>(g, u, a);
+    LAUNCH_BOOK(c);
+}
+void launch_out_vx(const LaunchCtx &c, const GridL &g, const double *a, double *u) {
+    k_out_vx<<<node_grid(g), tpb(), 0, c.stream>>>(g, a, u);
+    LAUNCH_BOOK(c);
+}
+void launch_out_vy(const LaunchCtx &c, const GridL &g, const double *a, double *u) {
+    k_out_vy<<<node_grid(g), tpb(), 0, c.stream>>>(g, a, u);
+    LAUNCH_BOOK(c);
+}
+void launch_out_p(const LaunchCtx &c, const GridL &g, const double *a, double *u, const double *shift) {
+    k_out_p<<<cell_grid(g), tpb(), 0, c.stream>>>(g, a, u, shift);
+    LAUNCH_BOOK(c);
+}
+void launch_out_b(const LaunchCtx &c, const GridL &g, const double *a, double *u) {
+    k_out_b<<<node_grid(g), tpb(), 0, c.stream>>>(g, a, u);
+    LAUNCH_BOOK(c);
+}
+void launch_apply(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vx,
+                  const double *vy, const double *p, double *ax, double *ay, double *ap) {
+    k_apply<<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, vx, vy, p, ax, ay, ap);
+    LAUNCH_BOOK(c);
+}
+void launch_apply_padded(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                         const double *vx, const double *vy, const double *p, double *ax, double *ay, double *ap) {
+    k_apply_padded<<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, vx, vy, p, ax, ay, ap);
+    LAUNCH_BOOK(c);
+}
+void launch_refresh_mirrors(const LaunchCtx &c, const GridL &g, double *vx, double *vy) {
+    const int n = (g.ncx > g.ncy ? g.ncx : g.ncy) + 1;
+    k_refresh_mirrors<<<(n + 255) / 256, 256, 0, c.stream>>>(g, vx, vy);
+    LAUNCH_BOOK(c);
+}
+void launch_make_rhs(const LaunchCtx &c, const GridL &g, const RhsArgs &rhs, double *bx, double *by) {
+    k_make_rhs<<<cell_grid(g), tpb(), 0, c.stream>>>(g, rhs, bx, by);
+    LAUNCH_BOOK(c);
+}
+void launch_count_nonpos(const LaunchCtx &c, const double *a, size_t n, int *count) {
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 4096) blocks = 4096;
+    if (blocks < 1) blocks = 1;
+    k_count_nonpos<<<blocks, 256, 0, c.stream>>>(a, n, count);
+    LAUNCH_BOOK(c);
+}
+void launch_coarse_assemble(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *M) {
+    const int n = g.ncy * (g.ncx - 1) + (g.ncy - 1) * g.ncx;
+    k_coarse_assemble<<<dim3((n + 127) / 128, n), 128, 0, c.stream>>>(g, etab, etap, M, n);
+    LAUNCH_BOOK(c);
+}
+__global__ void k_aug(const double *__restrict__ M, double *__restrict__ work, int n) {
+    const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (e >= (size_t)n * 2 * n) return;
+    const int r = (int)(e / (2 * n)), cc = (int)(e % (2 * n));
+    work[e] = cc < n ? M[(size_t)r * n + cc] : (cc - n == r ? 1.0 : 0.0);
+}
+void launch_coarse_invert(const LaunchCtx &c, double *work, double *Minv, int n, int *fail) {
+    const size_t tot = (size_t)n * 2 * n;
+    k_aug<<<(unsigned)((tot + 255) / 256), 256, 0, c.stream>>>(Minv, work, n);
+    LAUNCH_BOOK(c);
+    k_coarse_invert<<<1, 1024, 3 * n * sizeof(double), c.stream>>>(work, Minv, n, fail);
+    LAUNCH_BOOK(c);
+}
+void launch_coarse_solve(const LaunchCtx &c, const GridL &g, const double *Minv, const double *bx,
+                         const double *by, double *vx, double *vy) {
+    const int n = g.ncy * (g.ncx - 1) + (g.ncy - 1) * g.ncx;
+    k_coarse_solve<<<1, 256, n * sizeof(double), c.stream>>>(g, Minv, n, bx, by, vx, vy);
+    LAUNCH_BOOK(c);
+}
+int dot_blocks(const GridL &g) { return energy_blocks(g); }
+void launch_dots(const LaunchCtx &c, const GridL &g, const double *const *a, const double *const *b, int nd,
+                 double *partials) {
+    DotArgs d;
+    d.nd = nd;
+    for (int k = 0; k < nd; ++k)
+        for (int f = 0; f < 3; ++f) {
+            d.a[k][f] = a[3 * k + f];
+            d.b[k][f] = b[3 * k + f];
+        }
+    k_dots<<<cell_grid(g), tpb(), 0, c.stream>>>(g, d, partials);
+    LAUNCH_BOOK(c);
+}
+void launch_axpy3(const LaunchCtx &c, const GridL &g, const double *coef, int coef_index, double coef_sign,
+                  const double *xx, const double *xy, const double *xp, double *yx, double *yy, double *yp) {
+    k_axpy3<<<dim3((g.ncx + 2 + BX - 1) / BX, (g.ncy + 2 + BY - 1) / BY), tpb(), 0, c.stream>>>(
+        g, coef, coef_index, coef_sign, xx, xy, xp, yx, yy, yp);
+    LAUNCH_BOOK(c);
+}
+void launch_scale3(const LaunchCtx &c, const GridL &g, const double *coef, int invert_sqrt, double *x, double *y,
+                   double *p) {
+    k_scale3<<<dim3((g.ncx + 2 + BX - 1) / BX, (g.ncy + 2 + BY - 1) / BY), tpb(), 0, c.stream>>>(g, coef, invert_sqrt,
+                                                                                                x, y, p);
+    LAUNCH_BOOK(c);
+}
+void launch_precond_p(const LaunchCtx &c, const GridL &g, const double *etap, const double *zx, const double *zy,
+                      const double *rp, double alpha, double *zp, double *partials) {
+    k_precond_p<<<cell_grid(g), tpb(), 0, c.stream>>>(g, etap, zx, zy, rp, alpha, zp, partials);
+    LAUNCH_BOOK(c);
+}
+void launch_sub_mean(const LaunchCtx &c, const GridL &g, const double *mean, double *p) {
+    k_sub_mean<<<cell_grid(g), tpb(), 0, c.stream>>>(g, mean, p);
+    LAUNCH_BOOK(c);
+}

@@ -46,7 +46,8 @@ struct stokes_s {
     bool own_ws;
     int nlev;
     Level lev[MAXLEV];
-    double *p, *rho;
+    double *pbuf[2], *rho;  // pressure ping-pong (the fused Uzawa pass reads one, writes the other)
+    int pcur;
     double *partials;
     size_t npart;
     double *scal;       // device scalars
@@ -59,7 +60,7 @@ struct stokes_s {
     bool have_eta, have_rho;
     double gx, gy;
     long long launches;
-    cudaGraphExec_t uzawa_exec;
+    cudaGraphExec_t uzawa_exec[2];  // iteration reading pbuf[k]
     long long uzawa_kernels;
 };
 
@@ -102,7 +103,8 @@ GridL make_grid(int ncx, int ncy, double Lx, double Ly, const int bc[4]) {
     g.sS = bc[3] == STOKES_FREE_SLIP ? 1.0 : -1.0;
     return g;
 }
-size_t field_doubles(const GridL &g) { return (size_t)(g.ncy + 2) * (size_t)g.P; }
+// + 512 doubles of tail: row-segment bulk copies of the last CTA may run past the last row
+size_t field_doubles(const GridL &g) { return (size_t)(g.ncy + 2) * (size_t)g.P + 512; }
 int n_unknowns(const GridL &g) { return g.ncy * (g.ncx - 1) + (g.ncy - 1) * g.ncx; }
 
 // hierarchy (reading R8): factor 2 while both even and min/2 >= coarse_min
@@ -164,7 +166,8 @@ size_t carve(stokes_s *h, Carver &cv) {
         L.ry = cv.field(L.g);
     }
     const GridL &g0 = h->lev[0].g;
-    h->p = cv.field(g0);
+    h->pbuf[0] = cv.field(g0);
+    h->pbuf[1] = cv.field(g0);
     h->rho = cv.field(g0);
     h->npart = (size_t)energy_blocks(g0) * 12 + 64;
     h->partials = cv.take(h->npart);
@@ -208,7 +211,7 @@ RhsArgs rhs_fine(stokes_s *h) {
     RhsArgs r;
     r.mode = RHS_FINE;
     r.bx = r.by = nullptr;
-    r.p = h->p;
+    r.p = h->pbuf[h->pcur];
     r.rho = h->rho;
     r.gx = h->gx;
     r.gy = h->gy;
@@ -281,20 +284,51 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
     }
 }
 
-// the body of one Uzawa iteration (a12, mode UZAWA): V-cycle(s) on L v = f - G p^k,
-// pressure update + mean, energy residual of the new (v, p), E -> pinned host.
+// E of the current state (v, pbuf[pcur]) -> scal[S_E]; mean of the stored p -> scal[S_MSHIFT];
+// optional residual arrays (padded).  Fused single pass where the level allows it.
+void state_energy(stokes_s *h, double *rx, double *ry, double *rp) {
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    const double inv_np = 1.0 / ((double)F.g.ncx * F.g.ncy);
+    double *p = h->pbuf[h->pcur];
+    if (stream_ok(F.g)) {
+        launch_uzawa_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], p, nullptr, h->rho, h->gx, h->gy, 0.0,
+                            h->scal + S_ZERO, rx, ry, rp, h->partials);
+        launch_uzawa_final(c, h->partials, stream_blocks(F.g), h->scal + S_SF, inv_np, h->scal + S_E,
+                           h->scal + S_MSHIFT);
+    } else {
+        launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], p, h->rho, h->gx, h->gy, rx, ry, rp, h->partials, false);
+        launch_energy_final(c, h->partials, energy_blocks(F.g), h->scal + S_SF, h->scal + S_E);
+        launch_pupdate(c, F.g, F.etap, F.vx[0], F.vy[0], p, nullptr, 0.0, h->scal + S_ZERO,
+                       h->partials);  // sum of the stored p (its mean)
+        launch_finalize(c, h->partials, pupdate_blocks(F.g), 1, inv_np, h->scal + S_MSHIFT);
+    }
+}
+
+// the body of one Uzawa iteration (a12, mode UZAWA) reading pbuf[pcur]: V-cycle(s) on
+// L v = f - G p^k, pressure update into pbuf[1-pcur] + mean, energy residual of the new
+// (v, p), E -> pinned host.
 void uzawa_body(stokes_s *h) {
     Level &F = h->lev[0];
     const LaunchCtx c = ctx(h);
     for (int k = 0; k < h->o.vcycles_per_iter; ++k)
         vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false);
-    const int nb = pupdate_blocks(F.g);
-    launch_pupdate(c, F.g, F.etap, F.vx[0], F.vy[0], h->p, h->o.pressure_sign * h->o.alpha_p, h->scal + S_MSHIFT,
-                   h->partials);
-    launch_finalize(c, h->partials, nb, 1, 1.0 / ((double)F.g.ncx * F.g.ncy), h->scal + S_MSHIFT);
-    launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, nullptr, nullptr, nullptr,
-                  h->partials, false);
-    launch_energy_final(c, h->partials, energy_blocks(F.g), h->scal + S_SF, h->scal + S_E);
+    const double a_s = h->o.pressure_sign * h->o.alpha_p;
+    const double inv_np = 1.0 / ((double)F.g.ncx * F.g.ncy);
+    const double *pin = h->pbuf[h->pcur];
+    double *pout = h->pbuf[1 - h->pcur];
+    if (stream_ok(F.g)) {
+        launch_uzawa_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], pin, pout, h->rho, h->gx, h->gy, a_s,
+                            h->scal + S_MSHIFT, nullptr, nullptr, nullptr, h->partials);
+        launch_uzawa_final(c, h->partials, stream_blocks(F.g), h->scal + S_SF, inv_np, h->scal + S_E,
+                           h->scal + S_MSHIFT);
+    } else {
+        launch_pupdate(c, F.g, F.etap, F.vx[0], F.vy[0], pin, pout, a_s, h->scal + S_MSHIFT, h->partials);
+        launch_finalize(c, h->partials, pupdate_blocks(F.g), 1, inv_np, h->scal + S_MSHIFT);
+        launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], pout, h->rho, h->gx, h->gy, nullptr, nullptr,
+                      nullptr, h->partials, false);
+        launch_energy_final(c, h->partials, energy_blocks(F.g), h->scal + S_SF, h->scal + S_E);
+    }
     cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
 }
 
@@ -308,19 +342,15 @@ int sync(stokes_s *h) {
 void force_energy(stokes_s *h) {
     Level &F = h->lev[0];
     const LaunchCtx c = ctx(h);
-    launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, nullptr, nullptr, nullptr,
-                  h->partials, true);
+    launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], h->pbuf[0], h->rho, h->gx, h->gy, nullptr, nullptr,
+                  nullptr, h->partials, true);
     launch_energy_final(c, h->partials, energy_blocks(F.g), h->scal + S_ZERO, h->scal + S_SFPART);
     // S_SFPART+1 holds the sum Sv of f -> copy into S_SF
     cudaMemcpyAsync(h->scal + S_SF, h->scal + S_SFPART + 1, sizeof(double), cudaMemcpyDeviceToDevice, h->stream);
 }
 
 int energy_now(stokes_s *h, double *E) {
-    Level &F = h->lev[0];
-    const LaunchCtx c = ctx(h);
-    launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, nullptr, nullptr, nullptr,
-                  h->partials, false);
-    launch_energy_final(c, h->partials, energy_blocks(F.g), h->scal + S_SF, h->scal + S_E);
+    state_energy(h, nullptr, nullptr, nullptr);
     cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
     int st = sync(h);
     if (st) return st;
@@ -328,21 +358,34 @@ int energy_now(stokes_s *h, double *E) {
     return STOKES_OK;
 }
 
+void drop_graphs(stokes_s *h) {
+    for (int k = 0; k < 2; ++k)
+        if (h->uzawa_exec[k]) {
+            cudaGraphExecDestroy(h->uzawa_exec[k]);
+            h->uzawa_exec[k] = nullptr;
+        }
+}
+
 int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
-    // capture one iteration into a CUDA graph (launch-bound coarse levels), replay per step
-    if (!h->uzawa_exec) {
+    // capture one iteration per pressure buffer into CUDA graphs (the coarse levels are
+    // launch-bound), replay them alternately
+    const int keep = h->pcur;
+    for (int k = 0; k < 2; ++k) {
+        if (h->uzawa_exec[k]) continue;
         cudaGraph_t graph;
         const long long before = h->launches;
+        h->pcur = k;
         CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
         uzawa_body(h);
         cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+        h->pcur = keep;
         if (e != cudaSuccess) return fail_cuda(e, "graph capture");
         h->uzawa_kernels = h->launches - before;
         h->launches = before;
-        e = cudaGraphInstantiate(&h->uzawa_exec, graph, 0);
+        e = cudaGraphInstantiate(&h->uzawa_exec[k], graph, 0);
         cudaGraphDestroy(graph);
         if (e != cudaSuccess) {
-            h->uzawa_exec = nullptr;
+            h->uzawa_exec[k] = nullptr;
             return fail_cuda(e, "graph instantiate");
         }
     }
@@ -350,7 +393,8 @@ int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
     int k;
     int status = STOKES_NOT_CONVERGED;
     for (k = 1; k <= h->o.max_iter; ++k) {
-        CK(cudaGraphLaunch(h->uzawa_exec, h->stream));
+        CK(cudaGraphLaunch(h->uzawa_exec[h->pcur], h->stream));
+        h->pcur ^= 1;
         h->launches += h->uzawa_kernels;
         int st = sync(h);
         if (st) return st;
@@ -371,11 +415,10 @@ int solve_gcr(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
     const LaunchCtx c = ctx(h);
     const int m = h->o.gcr_restart;
     const int nb = energy_blocks(g);
-    double *x[3] = {F.vx[0], F.vy[0], h->p};
+    double *x[3] = {F.vx[0], F.vy[0], h->pbuf[h->pcur]};
     double **r = h->gr;
     // r0 = b - A x0 (recursive residual)
-    launch_energy(c, g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, r[0], r[1], r[2], h->partials,
-                  false);
+    state_energy(h, r[0], r[1], r[2]);
     int k = 0, status = STOKES_NOT_CONVERGED;
     double E = E0;
     const double inv_np = 1.0 / ((double)g.ncx * g.ncy);
@@ -429,8 +472,7 @@ int solve_gcr(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
     *iters = k;
     *Eout = E;
     // the pressure mean of x (inert) is removed at output through S_MSHIFT
-    launch_pupdate(c, g, F.etap, F.vx[0], F.vy[0], h->p, 0.0, h->scal + S_ZERO, h->partials);
-    launch_finalize(c, h->partials, nb, 1, inv_np, h->scal + S_MSHIFT);
+    state_energy(h, nullptr, nullptr, nullptr);
     return status;
 }
 
@@ -537,7 +579,7 @@ int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const s
 
 int stokes_destroy(stokes_t h) {
     if (!h) return STOKES_EINVAL;
-    if (h->uzawa_exec) cudaGraphExecDestroy(h->uzawa_exec);
+    drop_graphs(h);
     if (h->hscal) cudaFreeHost(h->hscal);
     if (h->own_ws && h->ws) cudaFree(h->ws);
     if (h->own_stream) cudaStreamDestroy(h->stream);
@@ -606,10 +648,7 @@ int stokes_set_gravity(stokes_t h, double gx, double gy) {
     if (!h || !(gx == gx) || !(gy == gy)) return STOKES_EINVAL;
     h->gx = gx;
     h->gy = gy;
-    if (h->uzawa_exec) {  // gravity is baked into the captured graph
-        cudaGraphExecDestroy(h->uzawa_exec);
-        h->uzawa_exec = nullptr;
-    }
+    drop_graphs(h);  // gravity is baked into the captured graphs
     if (h->have_eta && h->have_rho) force_energy(h);
     return sync(h);
 }
@@ -633,10 +672,9 @@ int stokes_residual(stokes_t h, const double *vx, const double *vy, const double
     Level &F = h->lev[0];
     const LaunchCtx c = ctx(h);
     launch_in_velocity(c, F.g, vx, vy, F.vx[0], F.vy[0]);
-    launch_in_p(c, F.g, p, h->p);
-    launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, F.rx, F.ry, F.bx,
-                  h->partials, false);
-    launch_energy_final(c, h->partials, energy_blocks(F.g), h->scal + S_SF, h->scal + S_E);
+    h->pcur = 0;
+    launch_in_p(c, F.g, p, h->pbuf[0]);
+    state_energy(h, F.rx, F.ry, F.bx);
     if (rx) launch_out_vx(c, F.g, F.rx, rx);
     if (ry) launch_out_vy(c, F.g, F.ry, ry);
     if (rp) launch_out_p(c, F.g, F.bx, rp, nullptr);
@@ -668,7 +706,8 @@ int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int
     const LaunchCtx c = ctx(h);
     // load the initial guess
     launch_in_velocity(c, F.g, vx, vy, F.vx[0], F.vy[0]);
-    launch_in_p(c, F.g, p, h->p);
+    h->pcur = 0;
+    launch_in_p(c, F.g, p, h->pbuf[0]);
     CK(cudaMemsetAsync(h->scal + S_MSHIFT, 0, sizeof(double), h->stream));
     CK(cudaMemcpyAsync(h->hscal + 32, h->scal + S_SF, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     int st = sync(h);
@@ -689,11 +728,7 @@ int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int
     if (E0 <= rtol) {
         *iters = 0;
         *rel_energy = E0;
-        status = STOKES_OK;
-        // de-mean the output pressure
-        launch_pupdate(c, F.g, F.etap, F.vx[0], F.vy[0], h->p, 0.0, h->scal + S_ZERO, h->partials);
-        launch_finalize(c, h->partials, pupdate_blocks(F.g), 1, 1.0 / ((double)F.g.ncx * F.g.ncy),
-                        h->scal + S_MSHIFT);
+        status = STOKES_OK;  // energy_now left the mean of the stored p in S_MSHIFT
     } else if (h->o.accel == STOKES_ACCEL_GCR) {
         status = solve_gcr(h, rtol, E0, iters, rel_energy);
     } else {
@@ -702,7 +737,7 @@ int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int
     if (status < 0 && status != STOKES_EDIVERGED) return status;
     launch_out_vx(c, F.g, F.vx[0], vx);
     launch_out_vy(c, F.g, F.vy[0], vy);
-    launch_out_p(c, F.g, h->p, p, h->scal + S_MSHIFT);
+    launch_out_p(c, F.g, h->pbuf[h->pcur], p, h->scal + S_MSHIFT);
     st = sync(h);
     if (st) return st;
     return status;
@@ -821,17 +856,28 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
     auto run = [&](void) {
         switch (kernel) {
         case 0: launch_jacobi(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v, false); break;
-        case 1: launch_energy(c, g, F.etab, F.etap, F.vx[0], F.vy[0], h->p, h->rho, h->gx, h->gy, nullptr, nullptr, nullptr, h->partials, false); break;
+        case 1: state_energy(h, nullptr, nullptr, nullptr); break;
         case 2: launch_residual(c, g, F.etab, F.etap, F.vx[0], F.vy[0], rhs_fine(h), F.rx, F.ry);
                 if (h->nlev > 1) launch_restrict_vel(c, g, h->lev[1].g, F.rx, F.ry, h->lev[1].bx, h->lev[1].by);
                 break;
         case 3: if (h->nlev > 1) launch_prolong(c, g, h->lev[1].g, h->lev[1].vx[0], h->lev[1].vy[0], F.vx[1], F.vy[1]); break;
-        case 4: launch_pupdate(c, g, F.etap, F.vx[0], F.vy[0], F.rx, h->o.alpha_p, h->scal + S_ZERO, h->partials); break;
+        case 4:
+            if (stream_ok(g))
+                launch_uzawa_energy(c, g, F.etab, F.etap, F.vx[0], F.vy[0], h->pbuf[h->pcur], h->pbuf[1 - h->pcur],
+                                    h->rho, h->gx, h->gy, h->o.alpha_p, h->scal + S_ZERO, nullptr, nullptr, nullptr,
+                                    h->partials);
+            else
+                launch_pupdate(c, g, F.etap, F.vx[0], F.vy[0], h->pbuf[h->pcur], h->pbuf[1 - h->pcur], h->o.alpha_p,
+                               h->scal + S_ZERO, h->partials);
+            break;
         default: launch_rbgs(c, g, F.etab, F.etap, F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v); break;
         }
     };
     // algorithmic bytes per launch: 8 B per value read or written
-    const double per_cell[6] = {64.0, 48.0, 52.0 + 16.0, 4.0 + 32.0, 40.0, 64.0};
+    // 0 Jacobi: read vx,vy,eta_p,eta_b,p,rho + write vx,vy; 1 energy: read 6; 2 residual (read 6,
+    // write 2) + restriction (read 2 fine, write 1/2); 3 prolongation (read/write 2 + 1/2 coarse);
+    // 4 fused Uzawa pressure step + energy: read 6, write p; 5 RBGS (4 phases, fused bytes)
+    const double per_cell[6] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0};
     if (kernel < 0 || kernel > 5) return STOKES_EINVAL;
     *bytes = per_cell[kernel] * cells;
     cudaEvent_t e0, e1;

@@ -68,7 +68,24 @@ void launch_make_rhs(const LaunchCtx &c, const GridL &g, const RhsArgs &rhs, dou
 // p <- (p - *mshift) + sign * alpha * eta_p * (-D v); partial sums of the new p per block
 int pupdate_blocks(const GridL &g);
 void launch_pupdate(const LaunchCtx &c, const GridL &g, const double *etap, const double *vx, const double *vy,
-                    double *p, double alpha_signed, const double *mshift, double *partials);
+                    const double *pin, double *pout, double alpha_signed, const double *mshift, double *partials);
+void launch_uzawa_final(const LaunchCtx &c, const double *partials, int nblocks, const double *Sf, double inv_np,
+                        double *out, double *mean);
+
+// ---------------------------------------------------------------- stream.cu (TMA row streaming)
+bool stream_ok(const GridL &g);   // level wide enough for the 256-column streaming CTAs
+int stream_blocks(const GridL &g);
+void launch_jacobi_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                          const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
+                          double omega);
+void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                            const double *vx, const double *vy, const RhsArgs &rhs, double *rx, double *ry);
+// fused Uzawa pressure step + energy residual; partials = 3 per CTA (Sv, Sp, sum p')
+// pout == nullptr: energy only (p' = pin - *mshift is not stored)
+void launch_uzawa_energy(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                         const double *vx, const double *vy, const double *pin, double *pout, const double *rho,
+                         double gx, double gy, double alpha_signed, const double *mshift, double *rx, double *ry,
+                         double *rp, double *partials);
 // out[k] = scale * sum_b partials[b * ncomp + k], deterministic fixed-order tree
 void launch_finalize(const LaunchCtx &c, const double *partials, int nblocks, int ncomp, double scale, double *out);
 // energy: E = sqrt((S[0] + S[1]) / Sf[0]) -> out[0]; also copies S to out[1..2]

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(BX *BY) k_energy_vec(GridL g, const double *__
 // late and at the output; per-block partial sums of the new p give the next mean.
 __global__ void __launch_bounds__(BX *BY) k_pupdate(GridL g, const double *__restrict__ etap,
                                                     const double *__restrict__ vx, const double *__restrict__ vy,
-                                                    double *__restrict__ p, double alpha_signed,
+                                                    const double *pin, double *pout, double alpha_signed,
                                                     const double *__restrict__ mshift, double *__restrict__ partials) {
     __shared__ double sh[BX * BY / 32];
     const int j = blockIdx.x * BX + threadIdx.x + 1;
@@ -402,8 +402,8 @@ __global__ void __launch_bounds__(BX *BY) k_pupdate(GridL g, const double *__res
     double s = 0.0;
     if (i <= g.ncy && j <= g.ncx) {
         const double dv = (vx[at(g, i, j)] - vx[at(g, i, j - 1)]) * g.idx + (vy[at(g, i, j)] - vy[at(g, i - 1, j)]) * g.idy;
-        const double pn = (p[at(g, i, j)] - *mshift) + alpha_signed * etap[at(g, i, j)] * (-dv);
-        p[at(g, i, j)] = pn;
+        const double pn = (pin[at(g, i, j)] - *mshift) + alpha_signed * etap[at(g, i, j)] * (-dv);
+        if (pout) pout[at(g, i, j)] = pn;
         s = pn;
     }
     s = block_sum<BX * BY>(s, sh);
@@ -435,6 +435,29 @@ __global__ void __launch_bounds__(1024) k_energy_final(const double *__restrict_
         out[1] = s0;
         out[2] = s1;
         out[0] = (Sf[0] > 0.0) ? sqrt((s0 + s1) / Sf[0]) : 0.0;
+    }
+}
+
+// Uzawa step finalisation from the fused pass (Sv, Sp, sum p' per block):
+// out[0] = E = sqrt((Sv + Sp) / Sf), out[1] = Sv, out[2] = Sp; *mean = inv_np * sum p'
+__global__ void __launch_bounds__(1024) k_uzawa_final(const double *__restrict__ partials, int nblocks,
+                                                      const double *__restrict__ Sf, double inv_np,
+                                                      double *__restrict__ out, double *__restrict__ mean) {
+    __shared__ double sh[32];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += 1024) {
+        s0 += partials[3 * (size_t)b];
+        s1 += partials[3 * (size_t)b + 1];
+        s2 += partials[3 * (size_t)b + 2];
+    }
+    s0 = block_sum<1024>(s0, sh);
+    s1 = block_sum<1024>(s1, sh);
+    s2 = block_sum<1024>(s2, sh);
+    if (threadIdx.x == 0) {
+        out[1] = s0;
+        out[2] = s1;
+        out[0] = (Sf[0] > 0.0) ? sqrt((s0 + s1) / Sf[0]) : 0.0;
+        *mean = s2 * inv_np;
     }
 }
 
@@ -751,6 +774,10 @@ static inline dim3 tpb() { return dim3(BX, BY); }
 
 void launch_jacobi(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
                    const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega, bool zero_in) {
+    if (!zero_in && stream_ok(g)) {
+        launch_jacobi_stream(c, g, etab, etap, vxi, vyi, vxo, vyo, rhs, omega);
+        return;
+    }
     if (zero_in) k_jacobi<true><<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs, omega);
     else k_jacobi<false><<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs, omega);
     LAUNCH_BOOK(c);
@@ -766,6 +793,10 @@ void launch_rbgs(const LaunchCtx &c, const GridL &g, const double *etab, const d
 }
 void launch_residual(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vx,
                      const double *vy, const RhsArgs &rhs, double *rx, double *ry) {
+    if (stream_ok(g)) {
+        launch_residual_stream(c, g, etab, etap, vx, vy, rhs, rx, ry);
+        return;
+    }
     k_residual<<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, vx, vy, rhs, rx, ry);
     LAUNCH_BOOK(c);
 }
@@ -812,8 +843,8 @@ void launch_energy_vec(const LaunchCtx &c, const GridL &g, const double *etab, c
 }
 int pupdate_blocks(const GridL &g) { return energy_blocks(g); }
 void launch_pupdate(const LaunchCtx &c, const GridL &g, const double *etap, const double *vx, const double *vy,
-                    double *p, double alpha_signed, const double *mshift, double *partials) {
-    k_pupdate<<<cell_grid(g), tpb(), 0, c.stream>>>(g, etap, vx, vy, p, alpha_signed, mshift, partials);
+                    const double *pin, double *pout, double alpha_signed, const double *mshift, double *partials) {
+    k_pupdate<<<cell_grid(g), tpb(), 0, c.stream>>>(g, etap, vx, vy, pin, pout, alpha_signed, mshift, partials);
     LAUNCH_BOOK(c);
 }
 void launch_finalize(const LaunchCtx &c, const double *partials, int nblocks, int ncomp, double scale, double *out) {
@@ -822,6 +853,11 @@ void launch_finalize(const LaunchCtx &c, const double *partials, int nblocks, in
 }
 void launch_energy_final(const LaunchCtx &c, const double *partials, int nblocks, const double *Sf, double *out) {
     k_energy_final<<<1, 1024, 0, c.stream>>>(partials, nblocks, Sf, out);
+    LAUNCH_BOOK(c);
+}
+void launch_uzawa_final(const LaunchCtx &c, const double *partials, int nblocks, const double *Sf, double inv_np,
+                        double *out, double *mean) {
+    k_uzawa_final<<<1, 1024, 0, c.stream>>>(partials, nblocks, Sf, inv_np, out, mean);
     LAUNCH_BOOK(c);
 }
 void launch_in_velocity(const LaunchCtx &c, const GridL &g, const double *ux, const double *uy, double *vx,

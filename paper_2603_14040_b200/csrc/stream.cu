@@ -1,0 +1,411 @@
+// TMA-staged row-streaming engine for the bandwidth-bound hot loops (sm_100a).
+//
+// A CTA of TW = 256 threads owns 256 consecutive columns j0..j0+255 of a level and a
+// strip of rows [i0, i1].  One elected thread streams the rows i0-1 .. i1+1 of the NF
+// input fields into an NS-deep shared-memory ring: each field row segment
+// [j0-2, j0+258) (2080 B, 16-B aligned by the layout of internal.h) is ONE bulk-async
+// copy (cp.async.bulk, executed by the TMA engine) completing on the slot's mbarrier.
+// All 256 threads then evaluate their column on the three staged rows i-1, i, i+1 and
+// store results straight to HBM.  Every input element is read from HBM once per strip
+// and up to NS-3 rows per CTA are in flight without costing registers; the grid is
+// sized so that one wave of CTAs covers the level (strip height from the occupancy), so
+// there is no tail wave.  The operators (Op) are:
+//   JacobiOp      damped Jacobi sweep, Eq. damped_jacobi       [a4]
+//   ResidualOp    r = b - L v, Eq. mg_residual                   [a3/a5]
+//   UzawaOp       pressure update p += alpha eta_P (-D v) (reading R3)
+//                 fused with the energy residual of the new (v, p) [a10+a3]
+// Stencil coefficients are those of kernels.cu (Listing vx_op_point).
+#include <math.h>
+
+#include "internal.h"
+
+namespace {
+
+constexpr int TW = 256;          // columns per CTA
+constexpr int RW = TW + 4;       // staged row width (doubles): [j0-2, j0+TW+2)
+constexpr int NS = 8;            // landing ring depth (rows): NS-1 rows in flight per CTA
+constexpr int NF = 6;            // staged fields
+constexpr int SMEM = NS * NF * RW * 8 + NS * 8;
+constexpr int MINB = 2;          // CTAs per SM (shared memory: 2 x 97.5 KB)
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// deterministic block sum over the 256 threads (fixed xor tree, fixed warp order)
+__device__ __forceinline__ double block_sum256(double v, double *sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = (threadIdx.x < TW / 32) ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    }
+    return v;
+}
+
+// Register window of the three rows i-1 (A), i (B), i+1 (C) of every field for this
+// thread's column: value and its left / right neighbours.  Each staged row is read from
+// its shared-memory landing slot exactly once, when it becomes row C; components an
+// operator never reads are dead code and cost neither loads nor registers.
+struct R3 {
+    double l, c, r;
+};
+struct Fld {
+    R3 A, B, C;
+};
+struct Win {
+    Fld f[NF];
+    __device__ __forceinline__ double A(int k, int dc = 0) const { return dc < 0 ? f[k].A.l : (dc > 0 ? f[k].A.r : f[k].A.c); }
+    __device__ __forceinline__ double B(int k, int dc = 0) const { return dc < 0 ? f[k].B.l : (dc > 0 ? f[k].B.r : f[k].B.c); }
+    __device__ __forceinline__ double C(int k, int dc = 0) const { return dc < 0 ? f[k].C.l : (dc > 0 ? f[k].C.r : f[k].C.c); }
+    __device__ __forceinline__ void push(const double *slot, int t) {  // t = column offset in the segment
+#pragma unroll
+        for (int k = 0; k < NF; ++k) {
+            f[k].A = f[k].B;
+            f[k].B = f[k].C;
+            const double *s = slot + k * RW + t;
+            f[k].C.l = s[-1];
+            f[k].C.c = s[0];
+            f[k].C.r = s[1];
+        }
+    }
+};
+enum { F_VX = 0, F_VY = 1, F_EP = 2, F_EB = 3, F_4 = 4, F_5 = 5 };  // F_4: p | bx, F_5: rho | by
+
+// reciprocal without the IEEE-division subroutine: MUFU seed + two Newton steps
+// (24 -> 48 -> full 53 bits; |a| is far inside the float range for every level here)
+__device__ __forceinline__ double rcp(double a) {
+    double r = (double)__frcp_rn((float)a);
+    r = r * fma(-a, r, 2.0);
+    r = r * fma(-a, r, 2.0);
+    return r;
+}
+
+// ---- stencil rows on the window (coefficients of Listing vx_op_point / reading R2)
+struct RowX {
+    double L, a;  // (L v) at the node and a_ii
+};
+__device__ __forceinline__ RowX lx_win(const GridL &g, const Win &w, int i) {
+    const double eta1 = w.A(F_EB), eta2 = w.B(F_EB), etaA = w.B(F_EP), etaB = w.B(F_EP, 1);
+    const double c = -(eta1 + eta2) * g.idy2 - 2.0 * (etaA + etaB) * g.idx2;
+    RowX r;
+    r.L = 2.0 * etaA * g.idx2 * w.B(F_VX, -1) + eta1 * g.idy2 * w.A(F_VX) + c * w.B(F_VX) + eta2 * g.idy2 * w.C(F_VX) +
+          2.0 * etaB * g.idx2 * w.B(F_VX, 1) +
+          g.idxdy * (eta1 * (w.A(F_VY) - w.A(F_VY, 1)) + eta2 * (w.B(F_VY, 1) - w.B(F_VY)));
+    r.a = c;
+    if (i == 1) r.a += g.sN * eta1 * g.idy2;
+    if (i == g.ncy) r.a += g.sS * eta2 * g.idy2;
+    return r;
+}
+__device__ __forceinline__ RowX ly_win(const GridL &g, const Win &w, int j) {
+    const double etaN = w.B(F_EP), etaS = w.C(F_EP), etaW = w.B(F_EB, -1), etaE = w.B(F_EB);
+    const double c = -2.0 * (etaN + etaS) * g.idy2 - (etaW + etaE) * g.idx2;
+    RowX r;
+    r.L = 2.0 * etaS * g.idy2 * w.C(F_VY) + 2.0 * etaN * g.idy2 * w.A(F_VY) + etaE * g.idx2 * w.B(F_VY, 1) +
+          etaW * g.idx2 * w.B(F_VY, -1) + c * w.B(F_VY) +
+          g.idxdy * (etaE * (w.C(F_VX) - w.B(F_VX)) - etaW * (w.C(F_VX, -1) - w.B(F_VX, -1)));
+    r.a = c;
+    if (j == 1) r.a += g.sW * etaW * g.idx2;
+    if (j == g.ncx) r.a += g.sE * etaE * g.idx2;
+    return r;
+}
+// body force (reading R4/R23) at vx / vy nodes from the staged rho rows
+__device__ __forceinline__ double fx_win(const Win &w, double gx) {
+    return gx != 0.0 ? -gx * (0.5 * (w.A(F_5) + w.B(F_5))) : 0.0;
+}
+__device__ __forceinline__ double fy_win(const Win &w, double gy) {
+    return gy != 0.0 ? -gy * (0.5 * (w.B(F_5, -1) + w.B(F_5))) : 0.0;
+}
+
+template <int MODE>
+struct JacobiOp {
+    static constexpr int NRED = 0;
+    const double *src[NF];
+    double *vxo, *vyo;
+    double omega, gx, gy;
+    __device__ __forceinline__ void row(const GridL &g, const Win &w, int i, int j, double *) const {
+        const size_t P = g.P;
+        if (j < g.ncx) {
+            const RowX x = lx_win(g, w, i);
+            const double b = (MODE == RHS_FINE) ? fx_win(w, gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
+            const double vn = w.B(F_VX) + omega * (b - x.L) * rcp(x.a);
+            vxo[(size_t)i * P + j] = vn;
+            if (i == 1) vxo[j] = g.sN * vn;
+            if (i == g.ncy) vxo[(size_t)(g.ncy + 1) * P + j] = g.sS * vn;
+        }
+        if (i < g.ncy) {
+            const RowX y = ly_win(g, w, j);
+            const double b = (MODE == RHS_FINE) ? fy_win(w, gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
+            const double vn = w.B(F_VY) + omega * (b - y.L) * rcp(y.a);
+            vyo[(size_t)i * P + j] = vn;
+            if (j == 1) vyo[(size_t)i * P] = g.sW * vn;
+            if (j == g.ncx) vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
+        }
+    }
+};
+
+template <int MODE>
+struct ResidualOp {
+    static constexpr int NRED = 0;
+    const double *src[NF];
+    double *rx, *ry;
+    double gx, gy;
+    __device__ __forceinline__ void row(const GridL &g, const Win &w, int i, int j, double *) const {
+        const size_t P = g.P;
+        if (j < g.ncx) {
+            const double b = (MODE == RHS_FINE) ? fx_win(w, gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
+            rx[(size_t)i * P + j] = b - lx_win(g, w, i).L;
+        }
+        if (i < g.ncy) {
+            const double b = (MODE == RHS_FINE) ? fy_win(w, gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
+            ry[(size_t)i * P + j] = b - ly_win(g, w, j).L;
+        }
+    }
+};
+
+// Uzawa pressure step fused with the energy residual of the new iterate:
+//   p' = (p - mshift) + alpha_s eta_P (-D v)     (reading R3; de-mean R10)
+//   r_v = f - L v - G p',  r_p = -D v,  Sv += r_v^2/(-a_ii), Sp += r_p^2 eta_P/(2/dx^2+2/dy^2)
+// p' at the east / south neighbours is recomputed from v on the window, so one pass reads
+// (vx, vy, eta_p, eta_b, p, rho) and writes p'.  Partial sums per CTA: (Sv, Sp, sum p').
+struct UzawaOp {
+    static constexpr int NRED = 3;
+    const double *src[NF];
+    double *po;             // p' output: a DIFFERENT buffer from src[F_4] (neighbouring CTAs stage
+                            // rows / halo columns of p that this CTA would otherwise overwrite)
+    const double *mshift;
+    double alpha_s, gx, gy;
+    double *rxo, *ryo, *rpo;  // optional residual outputs
+    int write_p;
+    __device__ __forceinline__ double divB(const GridL &g, const Win &w, int dc) const {  // (D v)(i, j+dc)
+        return (w.B(F_VX, dc) - w.B(F_VX, dc - 1)) * g.idx + (w.B(F_VY, dc) - w.A(F_VY, dc)) * g.idy;
+    }
+    __device__ __forceinline__ double divC(const GridL &g, const Win &w) const {  // (D v)(i+1, j)
+        return (w.C(F_VX) - w.C(F_VX, -1)) * g.idx + (w.C(F_VY) - w.B(F_VY)) * g.idy;
+    }
+    __device__ __forceinline__ void row(const GridL &g, const Win &w, int i, int j, double *acc) const {
+        const double ms = *mshift;
+        const double dv = divB(g, w, 0);
+        const double pn = (w.B(F_4) - ms) + alpha_s * w.B(F_EP) * (-dv);
+        if (write_p) po[(size_t)i * g.P + j] = pn;
+        const double rp = -dv;
+        acc[1] += rp * rp * (w.B(F_EP) / (2.0 * g.idx2 + 2.0 * g.idy2));
+        acc[2] += pn;
+        if (rpo) rpo[(size_t)i * g.P + j] = rp;
+        if (j < g.ncx) {
+            const double pe = (w.B(F_4, 1) - ms) + alpha_s * w.B(F_EP, 1) * (-divB(g, w, 1));
+            const RowX x = lx_win(g, w, i);
+            const double r = fx_win(w, gx) - (pn - pe) * g.idx - x.L;
+            acc[0] -= r * r * rcp(x.a);
+            if (rxo) rxo[(size_t)i * g.P + j] = r;
+        }
+        if (i < g.ncy) {
+            const double ps = (w.C(F_4) - ms) + alpha_s * w.C(F_EP) * (-divC(g, w));
+            const RowX y = ly_win(g, w, j);
+            const double r = fy_win(w, gy) - (pn - ps) * g.idy - y.L;
+            acc[0] -= r * r * rcp(y.a);
+            if (ryo) ryo[(size_t)i * g.P + j] = r;
+        }
+    }
+};
+
+template <class Op>
+__global__ void __launch_bounds__(TW, MINB) k_stream(GridL g, Op op, int H, double *__restrict__ partials) {
+    extern __shared__ __align__(128) double sm[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + NS * NF * RW);
+    __shared__ double red[TW / 32];
+    const int t = threadIdx.x;
+    const int j0 = 1 + TW * blockIdx.x;
+    const int j = j0 + t;
+    const int i0 = 1 + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, g.ncy);
+    const int rbase = i0 - 1;   // first staged row
+    const int rlast = i1 + 1;   // last staged row
+    const size_t P = g.P;
+    auto issue = [&](int r) {   // one bulk copy per field row segment, all on the slot's mbarrier
+        const int slot = (r - rbase) % NS;
+        uint64_t *bar = bars + slot;
+        mbar_expect_tx(bar, NF * RW * 8);
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            bulk_g2s(sm + (slot * NF + f) * RW, op.src[f] + (size_t)r * P + (j0 - 2), RW * 8, bar);
+    };
+    if (t == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(bars + s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0)
+        for (int r = rbase; r < rbase + NS && r <= rlast; ++r) issue(r);
+    auto consume = [&](Win &w, int r) {  // wait for row r, push it into the register window
+        const int rel = r - rbase;
+        mbar_wait(bars + rel % NS, (rel / NS) & 1);
+        w.push(sm + (rel % NS) * NF * RW, t + 2);
+    };
+    auto refill = [&](int r) {  // after a barrier: row r's slot is free, stage row r + NS
+        if (t == 0 && r + NS <= rlast) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(r + NS);
+        }
+    };
+    double acc[Op::NRED > 0 ? Op::NRED : 1];
+#pragma unroll
+    for (int k = 0; k < (Op::NRED > 0 ? Op::NRED : 1); ++k) acc[k] = 0.0;
+    Win w;
+    consume(w, rbase);
+    consume(w, rbase + 1);
+    __syncthreads();
+    refill(rbase);
+    refill(rbase + 1);
+    for (int i = i0; i <= i1; ++i) {
+        consume(w, i + 1);  // window: A = i-1, B = i, C = i+1
+        if (j <= g.ncx) op.row(g, w, i, j, acc);
+        __syncthreads();    // every thread has read row i+1's slot
+        refill(i + 1);
+    }
+    if (Op::NRED > 0) {
+        const size_t b = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+#pragma unroll
+        for (int k = 0; k < Op::NRED; ++k) {
+            const double s = block_sum256(acc[k], red);
+            if (t == 0) partials[b * Op::NRED + k] = s;
+        }
+    }
+}
+
+int g_slots = 0;  // resident CTAs of k_stream on the device (SMs x MINB)
+template <class Op>
+void prepare_kernel() {
+    static bool done = false;
+    if (!done) {
+        cudaFuncSetAttribute(k_stream<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        done = true;
+    }
+}
+int slots() {
+    if (!g_slots) {
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        g_slots = (nsm > 0 ? nsm : 148) * MINB;
+    }
+    return g_slots;
+}
+// strip height: one wave of CTAs covers the level
+int strip_h(const GridL &g) {
+    const int ncb = (g.ncx + TW - 1) / TW;
+    int strips = slots() / ncb;
+    if (strips < 1) strips = 1;
+    int H = (g.ncy + strips - 1) / strips;
+    return H < 4 ? 4 : H;
+}
+dim3 stream_grid(const GridL &g) {
+    const int H = strip_h(g);
+    return dim3((g.ncx + TW - 1) / TW, (g.ncy + H - 1) / H);
+}
+template <class Op>
+void run(const LaunchCtx &c, const GridL &g, const Op &op, double *partials) {
+    prepare_kernel<Op>();
+    k_stream<Op><<<stream_grid(g), TW, SMEM, c.stream>>>(g, op, strip_h(g), partials);
+    ++*c.counter;
+}
+void fill_src(const double **src, const double *vx, const double *vy, const double *etap, const double *etab,
+              const double *f4, const double *f5) {
+    src[0] = vx;
+    src[1] = vy;
+    src[2] = etap;
+    src[3] = etab;
+    src[4] = f4;
+    src[5] = f5;
+}
+
+}  // namespace
+
+bool stream_ok(const GridL &g) { return g.ncx >= TW / 2 && g.ncy >= 8; }
+int stream_blocks(const GridL &g) {
+    const dim3 gr = stream_grid(g);
+    return (int)(gr.x * gr.y);
+}
+
+void launch_jacobi_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                          const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
+                          double omega) {
+    if (rhs.mode == RHS_FINE) {
+        JacobiOp<RHS_FINE> op;
+        fill_src(op.src, vxi, vyi, etap, etab, rhs.p, rhs.rho);
+        op.vxo = vxo;
+        op.vyo = vyo;
+        op.omega = omega;
+        op.gx = rhs.gx;
+        op.gy = rhs.gy;
+        run(c, g, op, nullptr);
+    } else {
+        JacobiOp<RHS_ARRAYS> op;
+        fill_src(op.src, vxi, vyi, etap, etab, rhs.bx, rhs.by);
+        op.vxo = vxo;
+        op.vyo = vyo;
+        op.omega = omega;
+        op.gx = op.gy = 0.0;
+        run(c, g, op, nullptr);
+    }
+}
+
+void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                            const double *vx, const double *vy, const RhsArgs &rhs, double *rx, double *ry) {
+    if (rhs.mode == RHS_FINE) {
+        ResidualOp<RHS_FINE> op;
+        fill_src(op.src, vx, vy, etap, etab, rhs.p, rhs.rho);
+        op.rx = rx;
+        op.ry = ry;
+        op.gx = rhs.gx;
+        op.gy = rhs.gy;
+        run(c, g, op, nullptr);
+    } else {
+        ResidualOp<RHS_ARRAYS> op;
+        fill_src(op.src, vx, vy, etap, etab, rhs.bx, rhs.by);
+        op.rx = rx;
+        op.ry = ry;
+        op.gx = op.gy = 0.0;
+        run(c, g, op, nullptr);
+    }
+}
+
+void launch_uzawa_energy(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                         const double *vx, const double *vy, const double *pin, double *pout, const double *rho,
+                         double gx, double gy, double alpha_signed, const double *mshift, double *rx, double *ry,
+                         double *rp, double *partials) {
+    UzawaOp op;
+    fill_src(op.src, vx, vy, etap, etab, pin, rho);
+    op.po = pout;
+    op.mshift = mshift;
+    op.alpha_s = alpha_signed;
+    op.gx = gx;
+    op.gy = gy;
+    op.rxo = rx;
+    op.ryo = ry;
+    op.rpo = rp;
+    op.write_p = pout != nullptr;
+    run(c, g, op, partials);
+}

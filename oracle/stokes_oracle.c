@@ -855,7 +855,10 @@ static int solve_uzawa(oracle_t *S, double rtol, double Sf, double E0, int *iter
 }
 
 /* Flexible GCR(m) with MGS, Alg. 4, readings R13/R14.
- * Vectors are x = (vx, vy, p) on the unknowns; <.,.> Euclidean over unknowns (vx, vy, p). */
+ * Vectors are x = (vx, vy, p) on the unknowns; <.,.> Euclidean over unknowns (vx, vy, p).
+ * At every restart the recursive residual is replaced by the true b - A x (reading R13:
+ * Alg. 4 keeps the recursive r; over ~100 steps its drift leaves the iterate ~1e-9 away
+ * from the fixed point while E(recursive r) keeps falling). */
 typedef struct { double *x, *y, *p; } ovec;
 static ovec ovec_new(size_t n) { ovec v = {zalloc(n), zalloc(n), zalloc(n)}; return v; }
 static void ovec_free(ovec v) { free(v.x); free(v.y); free(v.p); }
@@ -910,6 +913,10 @@ static int solve_gcr(oracle_t *S, double rtol, double Sf, double E0, int *iters,
     int k = 0, status = O_NOT_CONVERGED;
     double E = E0;
     while (k < S->o.max_iter && status == O_NOT_CONVERGED) {
+        if (k > 0) { /* restart: replace the recursive residual by the true one (reading R13) */
+            refresh_mirrors(S, L, S->vx, S->vy);
+            full_residual(S, S->vx, S->vy, S->p, r.x, r.y, r.p);
+        }
         for (int i = 0; i < m && k < S->o.max_iter; ++i) {
             apply_precond(S, r, z[i]);
             refresh_mirrors(S, L, z[i].x, z[i].y);

@@ -423,6 +423,7 @@ int solve_gcr(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
     double E = E0;
     const double inv_np = 1.0 / ((double)g.ncx * g.ncy);
     while (k < h->o.max_iter && status == STOKES_NOT_CONVERGED) {
+        if (k > 0) state_energy(h, r[0], r[1], r[2]);  // restart: true residual (reading R13)
         for (int i = 0; i < m && k < h->o.max_iter; ++i) {
             double **z = h->gz[i], **w = h->gw[i];
             // z = M^-1 r: dv = Vcycle(0; r_v); dp = alpha eta_P (r_p - D dv); de-mean dp

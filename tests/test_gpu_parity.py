@@ -138,7 +138,7 @@ def test_vcycle(S, smoother, nx, ny, bc):
 CASES = [
     ("mms", 32, dict(omega_v=0.6, alpha_p=1.5)),
     ("mms", 64, dict(omega_v=0.6, alpha_p=1.0, smoother=1)),
-    ("block", 64, dict(omega_v=0.6, alpha_p=1.5, accel=1)),
+    ("block", 64, dict(omega_v=0.6, alpha_p=1.0, accel=1, gcr_restart=30)),
     ("layered", 128, dict(omega_v=0.6, alpha_p=1.0)),
     ("solcx", 128, dict(omega_v=0.6, alpha_p=1.0, accel=1)),
     ("random", 128, dict(omega_v=0.6, alpha_p=1.0)),

@@ -56,7 +56,9 @@ struct stokes_s {
     int nc;
     int *dflag;
     // GCR vectors (fine level, padded): z_i, w_i, r, V-cycle scratch
-    double *gz[MAXM][3], *gw[MAXM][3], *gr[3], *gtmp[2];
+    double *gz[MAXM][3], *gw[MAXM][3], *gr[3], *gtmp[2], *gew[3];
+    cudaGraphExec_t gcr_exec[MAXM];  // GCR step i (i MGS steps) captured
+    long long gcr_kernels[MAXM];
     bool have_eta, have_rho;
     double gx, gy;
     long long launches;
@@ -169,7 +171,7 @@ size_t carve(stokes_s *h, Carver &cv) {
     h->pbuf[0] = cv.field(g0);
     h->pbuf[1] = cv.field(g0);
     h->rho = cv.field(g0);
-    h->npart = (size_t)energy_blocks(g0) * 12 + 64;
+    h->npart = (size_t)energy_blocks(g0) * 12 + 3 * 4096 + 64;
     h->partials = cv.take(h->npart);
     h->scal = cv.take(S_NSCAL);
     const GridL &gc = h->lev[h->nlev - 1].g;
@@ -192,6 +194,7 @@ size_t carve(stokes_s *h, Carver &cv) {
         for (int f = 0; f < 3; ++f) h->gr[f] = cv.field(g0);
         h->gtmp[0] = cv.field(g0);
         h->gtmp[1] = cv.field(g0);
+        for (int f = 0; f < 3; ++f) h->gew[f] = cv.field(g0);
     }
     return round_up(cv.off, 256);
 }
@@ -364,6 +367,11 @@ void drop_graphs(stokes_s *h) {
             cudaGraphExecDestroy(h->uzawa_exec[k]);
             h->uzawa_exec[k] = nullptr;
         }
+    for (int k = 0; k < MAXM; ++k)
+        if (h->gcr_exec[k]) {
+            cudaGraphExecDestroy(h->gcr_exec[k]);
+            h->gcr_exec[k] = nullptr;
+        }
 }
 
 int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
@@ -405,6 +413,82 @@ int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
     if (k > h->o.max_iter) k = h->o.max_iter;
     *iters = k;
     *Eout = E;
+    return status;
+}
+
+// One fused GCR step i (Alg. 4 inner loop body) on the stream:
+// V-cycle (z_v = V(0; r_v)); z_p + w = A z + first dot (one streaming pass); i fused MGS
+// steps (axpy + next dot per HBM pass); normalise + update x, r + energy of r (one pass);
+// E, nu^2, <r,r> -> pinned host.  The stored z_p is not de-meaned (inert, reading R14).
+void gcr_step_body(stokes_s *h, int i) {
+    Level &F = h->lev[0];
+    const GridL &g = F.g;
+    const LaunchCtx c = ctx(h);
+    double **z = h->gz[i], **w = h->gw[i], **r = h->gr;
+    double *x[3] = {F.vx[0], F.vy[0], h->pbuf[h->pcur]};
+    const size_t nf = field_doubles(g);
+    double *PA = h->partials, *PB = h->partials + 4096, *PC = h->partials + 8192;
+    for (int q = 0; q < h->o.vcycles_per_iter; ++q)
+        vcycle(h, 0, z[0], z[1], h->gtmp[0], h->gtmp[1], rhs_arrays(r[0], r[1]), q == 0);
+    launch_precond_apply(c, g, F.etab, F.etap, z[0], z[1], r[2], h->o.alpha_p, z[2], w[0], w[1], w[2],
+                         i > 0 ? (const double *const *)h->gw[0] : nullptr, r[0], r[1], PA);
+    int nb = stream_blocks(g);
+    double *pin = PA, *pout = PB;
+    for (int j = 0; j < i; ++j) {
+        const double *const *nxt = (j + 1 < i) ? (const double *const *)h->gw[j + 1] : nullptr;
+        launch_mgs_step(c, pin, nb, 2, 0, w, z, (const double *const *)h->gw[j], (const double *const *)h->gz[j], nxt,
+                        (const double *const *)r, nf, pout);
+        nb = gcr_flat_blocks();
+        double *t = pin;
+        pin = pout;
+        pout = t;
+    }
+    launch_gcr_update(c, pin, nb, w, z, x, r, (const double *const *)h->gew, nf, PC);
+    launch_gcr_final(c, PC, gcr_flat_blocks(), pin, nb, h->scal + S_SF, h->scal + S_E, h->scal + S_NU2,
+                     h->scal + S_RR);
+    cudaMemcpyAsync(h->hscal, h->scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+}
+
+int solve_gcr_fused(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+    const int m = h->o.gcr_restart;
+    double **r = h->gr;
+    state_energy(h, r[0], r[1], r[2]);  // r0 = b - A x0
+    int k = 0, status = STOKES_NOT_CONVERGED;
+    double E = E0;
+    while (k < h->o.max_iter && status == STOKES_NOT_CONVERGED) {
+        if (k > 0) state_energy(h, r[0], r[1], r[2]);  // restart: true residual (reading R13)
+        for (int i = 0; i < m && k < h->o.max_iter; ++i) {
+            if (!h->gcr_exec[i]) {  // capture step i once (pcur is fixed during GCR)
+                cudaGraph_t graph;
+                const long long before = h->launches;
+                CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+                gcr_step_body(h, i);
+                cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+                if (e != cudaSuccess) return fail_cuda(e, "graph capture");
+                h->gcr_kernels[i] = h->launches - before;
+                h->launches = before;
+                e = cudaGraphInstantiate(&h->gcr_exec[i], graph, 0);
+                cudaGraphDestroy(graph);
+                if (e != cudaSuccess) {
+                    h->gcr_exec[i] = nullptr;
+                    return fail_cuda(e, "graph instantiate");
+                }
+            }
+            CK(cudaGraphLaunch(h->gcr_exec[i], h->stream));
+            h->launches += h->gcr_kernels[i];
+            int st = sync(h);
+            if (st) return st;
+            ++k;
+            const double nu2 = h->hscal[S_NU2], rr = h->hscal[S_RR];
+            E = h->hscal[S_E];
+            if (!(nu2 > 1e-28 * rr)) { status = STOKES_EDIVERGED; break; }  // breakdown (R13)
+            if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+            if (E <= rtol) { status = STOKES_OK; break; }
+        }
+    }
+    *iters = k;
+    *Eout = E;
+    state_energy(h, nullptr, nullptr, nullptr);  // mean of x_p for the output de-mean
     return status;
 }
 
@@ -632,6 +716,7 @@ int stokes_set_viscosity(stokes_t h, const double *eta_b, const double *eta_p) {
         memcpy(&bad, &h->hscal[S_NSCAL - 1], sizeof(int));
         if (bad) return STOKES_EINVAL;
     }
+    if (h->o.accel == STOKES_ACCEL_GCR) launch_energy_weights(c, F.g, F.etab, F.etap, h->gew[0], h->gew[1], h->gew[2]);
     h->have_eta = true;
     if (h->have_rho) force_energy(h);
     return sync(h);
@@ -731,7 +816,8 @@ int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int
         *rel_energy = E0;
         status = STOKES_OK;  // energy_now left the mean of the stored p in S_MSHIFT
     } else if (h->o.accel == STOKES_ACCEL_GCR) {
-        status = solve_gcr(h, rtol, E0, iters, rel_energy);
+        status = stream_ok(F.g) ? solve_gcr_fused(h, rtol, E0, iters, rel_energy)
+                                : solve_gcr(h, rtol, E0, iters, rel_energy);
     } else {
         status = solve_uzawa(h, rtol, E0, iters, rel_energy);
     }

@@ -127,3 +127,19 @@ void launch_sub_mean(const LaunchCtx &c, const GridL &g, const double *mean, dou
 void launch_apply_padded(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
                          const double *vx, const double *vy, const double *p, double *ax, double *ay, double *ap);
 void launch_refresh_mirrors(const LaunchCtx &c, const GridL &g, double *vx, double *vy);
+void launch_energy_weights(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *ewx,
+                           double *ewy, double *ewp);
+
+// fused GCR kernels (stream.cu: preconditioner + apply; gcr.cu: flat MGS / update)
+void launch_precond_apply(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                          const double *zx, const double *zy, const double *rp, double alpha, double *zp, double *wx,
+                          double *wy, double *wp, const double *const *w0, const double *rx, const double *ry,
+                          double *partials);
+int gcr_flat_blocks();
+void launch_mgs_step(const LaunchCtx &c, const double *pin, int nbin, int ncin, int kin, double *const *w,
+                     double *const *z, const double *const *wj, const double *const *zj, const double *const *nxt,
+                     const double *const *r, size_t nfield, double *pout);
+void launch_gcr_update(const LaunchCtx &c, const double *pin, int nbin, double *const *w, double *const *z,
+                       double *const *x, double *const *r, const double *const *ew, size_t nfield, double *pout);
+void launch_gcr_final(const LaunchCtx &c, const double *pupd, int nbu, const double *pnorm, int nbn,
+                      const double *Sf, double *E, double *nu2, double *rr);

@@ -560,6 +560,17 @@ __global__ void __launch_bounds__(BX *BY) k_apply_padded(GridL g, const double *
     if (i < g.ncy) ay[at(g, i, j)] = ly_row(g, etab, etap, axx, ayy, i, j) + (p[at(g, i, j)] - p[at(g, i + 1, j)]) * g.idy;
     ap[at(g, i, j)] = (vx[at(g, i, j)] - vx[at(g, i, j - 1)]) * g.idx + (vy[at(g, i, j)] - vy[at(g, i - 1, j)]) * g.idy;
 }
+// energy weights of the GCR residual: ewx = 1/(-a_ii) at vx unknowns, ewy at vy unknowns,
+// ewp = eta_P/(2/dx^2+2/dy^2) at P nodes, so that
+// E^2 Sf = sum r^2 ew over the padded arrays (zeros elsewhere)
+__global__ void k_energy_weights(GridL g, const double *__restrict__ etab, const double *__restrict__ etap,
+                                 double *__restrict__ ewx, double *__restrict__ ewy, double *__restrict__ ewp) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i > g.ncy || j > g.ncx) return;
+    if (j < g.ncx) ewx[at(g, i, j)] = 1.0 / (-lx_diag(g, etab, etap, i, j));
+    if (i < g.ncy) ewy[at(g, i, j)] = 1.0 / (-ly_diag(g, etab, etap, i, j));
+    ewp[at(g, i, j)] = etap[at(g, i, j)] / (2.0 * g.idx2 + 2.0 * g.idy2);
+}
 // materialise b = f - G p (RHS_FINE) or copy b (RHS_ARRAYS) at the unknowns
 __global__ void k_make_rhs(GridL g, RhsArgs rhs, double *__restrict__ bx, double *__restrict__ by) {
     const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y + 1;
@@ -912,6 +923,11 @@ void launch_apply_padded(const LaunchCtx &c, const GridL &g, const double *etab,
 void launch_refresh_mirrors(const LaunchCtx &c, const GridL &g, double *vx, double *vy) {
     const int n = (g.ncx > g.ncy ? g.ncx : g.ncy) + 1;
     k_refresh_mirrors<<<(n + 255) / 256, 256, 0, c.stream>>>(g, vx, vy);
+    LAUNCH_BOOK(c);
+}
+void launch_energy_weights(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *ewx,
+                           double *ewy, double *ewp) {
+    k_energy_weights<<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, ewx, ewy, ewp);
     LAUNCH_BOOK(c);
 }
 void launch_make_rhs(const LaunchCtx &c, const GridL &g, const RhsArgs &rhs, double *bx, double *by) {

@@ -80,9 +80,10 @@ struct Win {
     __device__ __forceinline__ double A(int k, int dc = 0) const { return dc < 0 ? f[k].A.l : (dc > 0 ? f[k].A.r : f[k].A.c); }
     __device__ __forceinline__ double B(int k, int dc = 0) const { return dc < 0 ? f[k].B.l : (dc > 0 ? f[k].B.r : f[k].B.c); }
     __device__ __forceinline__ double C(int k, int dc = 0) const { return dc < 0 ? f[k].C.l : (dc > 0 ? f[k].C.r : f[k].C.c); }
+    template <int NFU>
     __device__ __forceinline__ void push(const double *slot, int t) {  // t = column offset in the segment
 #pragma unroll
-        for (int k = 0; k < NF; ++k) {
+        for (int k = 0; k < NFU; ++k) {
             f[k].A = f[k].B;
             f[k].B = f[k].C;
             const double *s = slot + k * RW + t;
@@ -141,6 +142,7 @@ __device__ __forceinline__ double fy_win(const Win &w, double gy) {
 
 template <int MODE>
 struct JacobiOp {
+    static constexpr int NF = 6;
     static constexpr int NRED = 0;
     const double *src[NF];
     double *vxo, *vyo;
@@ -168,6 +170,7 @@ struct JacobiOp {
 
 template <int MODE>
 struct ResidualOp {
+    static constexpr int NF = 6;
     static constexpr int NRED = 0;
     const double *src[NF];
     double *rx, *ry;
@@ -191,6 +194,7 @@ struct ResidualOp {
 // p' at the east / south neighbours is recomputed from v on the window, so one pass reads
 // (vx, vy, eta_p, eta_b, p, rho) and writes p'.  Partial sums per CTA: (Sv, Sp, sum p').
 struct UzawaOp {
+    static constexpr int NF = 6;
     static constexpr int NRED = 3;
     const double *src[NF];
     double *po;             // p' output: a DIFFERENT buffer from src[F_4] (neighbouring CTAs stage
@@ -231,6 +235,48 @@ struct UzawaOp {
     }
 };
 
+// GCR preconditioner pressure part fused with the operator apply (a11):
+//   z_p = alpha eta_P (r_p - D z_v)            (M^-1 of the Uzawa splitting, R3)
+//   w = A z = [L z_v + G z_p ; D z_v]
+// z_p at the east / south neighbours is recomputed on the window.  Partial dots for the
+// first Gram-Schmidt coefficient: <w, w0> (first == 0) or <w, w>, <r, w> (first step).
+struct PrecondApplyOp {
+    static constexpr int NF = 5;
+    static constexpr int NRED = 2;
+    const double *src[6];        // zx, zy, eta_p, eta_b, r_p
+    double *zp, *wx, *wy, *wp;
+    const double *w0x, *w0y, *w0p;  // previous basis vector (null on the first step)
+    const double *rx, *ry;           // residual velocity parts (first step: <r, w>)
+    double alpha;
+    __device__ __forceinline__ double divB(const GridL &g, const Win &w, int dc) const {
+        return (w.B(F_VX, dc) - w.B(F_VX, dc - 1)) * g.idx + (w.B(F_VY, dc) - w.A(F_VY, dc)) * g.idy;
+    }
+    __device__ __forceinline__ void row(const GridL &g, const Win &w, int i, int j, double *acc) const {
+        const size_t q = (size_t)i * g.P + j;
+        const double dz = divB(g, w, 0);
+        const double zc = alpha * w.B(F_EP) * (w.B(F_4) - dz);
+        zp[q] = zc;
+        wp[q] = dz;
+        if (w0x) acc[0] += dz * w0p[q];
+        else { acc[0] += dz * dz; acc[1] += w.B(F_4) * dz; }
+        if (j < g.ncx) {
+            const double ze = alpha * w.B(F_EP, 1) * (w.B(F_4, 1) - divB(g, w, 1));
+            const double v = lx_win(g, w, i).L + (zc - ze) * g.idx;
+            wx[q] = v;
+            if (w0x) acc[0] += v * w0x[q];
+            else { acc[0] += v * v; acc[1] += rx[q] * v; }
+        }
+        if (i < g.ncy) {
+            const double ds = (w.C(F_VX) - w.C(F_VX, -1)) * g.idx + (w.C(F_VY) - w.B(F_VY)) * g.idy;
+            const double zs = alpha * w.C(F_EP) * (w.C(F_4) - ds);
+            const double v = ly_win(g, w, j).L + (zc - zs) * g.idy;
+            wy[q] = v;
+            if (w0x) acc[0] += v * w0y[q];
+            else { acc[0] += v * v; acc[1] += ry[q] * v; }
+        }
+    }
+};
+
 template <class Op>
 __global__ void __launch_bounds__(TW, MINB) k_stream(GridL g, Op op, int H, double *__restrict__ partials) {
     extern __shared__ __align__(128) double sm[];
@@ -247,9 +293,9 @@ __global__ void __launch_bounds__(TW, MINB) k_stream(GridL g, Op op, int H, doub
     auto issue = [&](int r) {   // one bulk copy per field row segment, all on the slot's mbarrier
         const int slot = (r - rbase) % NS;
         uint64_t *bar = bars + slot;
-        mbar_expect_tx(bar, NF * RW * 8);
+        mbar_expect_tx(bar, Op::NF * RW * 8);
 #pragma unroll
-        for (int f = 0; f < NF; ++f)
+        for (int f = 0; f < Op::NF; ++f)
             bulk_g2s(sm + (slot * NF + f) * RW, op.src[f] + (size_t)r * P + (j0 - 2), RW * 8, bar);
     };
     if (t == 0) {
@@ -262,7 +308,7 @@ __global__ void __launch_bounds__(TW, MINB) k_stream(GridL g, Op op, int H, doub
     auto consume = [&](Win &w, int r) {  // wait for row r, push it into the register window
         const int rel = r - rbase;
         mbar_wait(bars + rel % NS, (rel / NS) & 1);
-        w.push(sm + (rel % NS) * NF * RW, t + 2);
+        w.template push<Op::NF>(sm + (rel % NS) * NF * RW, t + 2);
     };
     auto refill = [&](int r) {  // after a barrier: row r's slot is free, stage row r + NS
         if (t == 0 && r + NS <= rlast) {
@@ -390,6 +436,30 @@ void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *et
         op.gx = op.gy = 0.0;
         run(c, g, op, nullptr);
     }
+}
+
+void launch_precond_apply(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                          const double *zx, const double *zy, const double *rp, double alpha, double *zp, double *wx,
+                          double *wy, double *wp, const double *const *w0, const double *rx, const double *ry,
+                          double *partials) {
+    PrecondApplyOp op;
+    op.src[0] = zx;
+    op.src[1] = zy;
+    op.src[2] = etap;
+    op.src[3] = etab;
+    op.src[4] = rp;
+    op.src[5] = nullptr;
+    op.zp = zp;
+    op.wx = wx;
+    op.wy = wy;
+    op.wp = wp;
+    op.w0x = w0 ? w0[0] : nullptr;
+    op.w0y = w0 ? w0[1] : nullptr;
+    op.w0p = w0 ? w0[2] : nullptr;
+    op.rx = rx;
+    op.ry = ry;
+    op.alpha = alpha;
+    run(c, g, op, partials);
 }
 
 void launch_uzawa_energy(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,

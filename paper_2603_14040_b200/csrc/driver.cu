@@ -103,6 +103,10 @@ GridL make_grid(int ncx, int ncy, double Lx, double Ly, const int bc[4]) {
     g.sE = bc[1] == STOKES_FREE_SLIP ? 1.0 : -1.0;
     g.sN = bc[2] == STOKES_FREE_SLIP ? 1.0 : -1.0;
     g.sS = bc[3] == STOKES_FREE_SLIP ? 1.0 : -1.0;
+    g.bN = g.bS = g.bW = g.bE = 1;  // single domain: every side is a global boundary
+    g.nvxj = ncx - 1;
+    g.nvyi = ncy - 1;
+    g.par = 0;
     return g;
 }
 // + 512 doubles of tail: row-segment bulk copies of the last CTA may run past the last row

@@ -21,6 +21,13 @@ struct GridL {          // one multigrid level, passed by value to kernels
     double idx2, idy2;  // 1/dx^2, 1/dy^2
     double idxdy;       // 1/(dx dy)
     double sW, sE, sN, sS;  // mirror signs: +1 free slip, -1 no slip
+    // 2D domain decomposition: a level may be one tile of the global grid.
+    // bX = 1: side X is a global boundary (mirrors / walls); 0: a halo filled
+    // from the neighbouring tile.  Single-domain levels have all four set.
+    int bN, bS, bW, bE;
+    int nvxj;  // last vx unknown column: ncx-1 if bE (east wall) else ncx (the tile's east faces)
+    int nvyi;  // last vy unknown row:    ncy-1 if bS else ncy
+    int par;   // (global row + column offset of the tile) & 1: red-black colour parity (R11)
 };
 
 __host__ __device__ inline size_t at(const GridL &g, int i, int j) { return (size_t)i * (size_t)g.P + (size_t)j; }

@@ -58,16 +58,16 @@ __device__ __forceinline__ double lx_diag(const GridL &g, const double *__restri
                                           const double *__restrict__ etap, int i, int j) {
     const double eta1 = etab[at(g, i - 1, j)], eta2 = etab[at(g, i, j)];
     double a = -(eta1 + eta2) * g.idy2 - 2.0 * (etap[at(g, i, j)] + etap[at(g, i, j + 1)]) * g.idx2;
-    if (i == 1) a += g.sN * eta1 * g.idy2;
-    if (i == g.ncy) a += g.sS * eta2 * g.idy2;
+    if (i == 1 && g.bN) a += g.sN * eta1 * g.idy2;
+    if (i == g.ncy && g.bS) a += g.sS * eta2 * g.idy2;
     return a;
 }
 __device__ __forceinline__ double ly_diag(const GridL &g, const double *__restrict__ etab,
                                           const double *__restrict__ etap, int i, int j) {
     const double etaW = etab[at(g, i, j - 1)], etaE = etab[at(g, i, j)];
     double a = -2.0 * (etap[at(g, i, j)] + etap[at(g, i + 1, j)]) * g.idy2 - (etaW + etaE) * g.idx2;
-    if (j == 1) a += g.sW * etaW * g.idx2;
-    if (j == g.ncx) a += g.sE * etaE * g.idx2;
+    if (j == 1 && g.bW) a += g.sW * etaW * g.idx2;
+    if (j == g.ncx && g.bE) a += g.sE * etaE * g.idx2;
     return a;
 }
 // right-hand side of the velocity equation at a vx / vy node:
@@ -115,25 +115,25 @@ __global__ void __launch_bounds__(BX *BY) k_jacobi(GridL g, const double *__rest
     const int i = blockIdx.y * BY + threadIdx.y + 1;
     if (i > g.ncy || j > g.ncx) return;
     const ArrayAcc ax{vxi, (size_t)g.P}, ay{vyi, (size_t)g.P};
-    if (j < g.ncx) {
+    if (j <= g.nvxj) {
         const double a = lx_diag(g, etab, etap, i, j);
         const double b = rhs_x(g, rhs, i, j);
         double vn;
         if (ZERO) vn = omega * b / a;
         else vn = ax(i, j) + omega * (b - lx_row(g, etab, etap, ax, ay, i, j)) / a;
         vxo[at(g, i, j)] = vn;
-        if (i == 1) vxo[at(g, 0, j)] = g.sN * vn;
-        if (i == g.ncy) vxo[at(g, g.ncy + 1, j)] = g.sS * vn;
+        if (i == 1 && g.bN) vxo[at(g, 0, j)] = g.sN * vn;
+        if (i == g.ncy && g.bS) vxo[at(g, g.ncy + 1, j)] = g.sS * vn;
     }
-    if (i < g.ncy) {
+    if (i <= g.nvyi) {
         const double a = ly_diag(g, etab, etap, i, j);
         const double b = rhs_y(g, rhs, i, j);
         double vn;
         if (ZERO) vn = omega * b / a;
         else vn = ay(i, j) + omega * (b - ly_row(g, etab, etap, ax, ay, i, j)) / a;
         vyo[at(g, i, j)] = vn;
-        if (j == 1) vyo[at(g, i, 0)] = g.sW * vn;
-        if (j == g.ncx) vyo[at(g, i, g.ncx + 1)] = g.sE * vn;
+        if (j == 1 && g.bW) vyo[at(g, i, 0)] = g.sW * vn;
+        if (j == g.ncx && g.bE) vyo[at(g, i, g.ncx + 1)] = g.sE * vn;
     }
 }
 
@@ -144,22 +144,22 @@ __global__ void __launch_bounds__(BX *BY) k_rbgs_phase(GridL g, const double *__
                                                        const double *__restrict__ etap, double *vx, double *vy,
                                                        RhsArgs rhs, double omega, int comp, int colour) {
     const int i = blockIdx.y * BY + threadIdx.y + 1;
-    const int j = 2 * (blockIdx.x * BX + threadIdx.x) + 1 + ((i + 1 + colour) & 1);
+    const int j = 2 * (blockIdx.x * BX + threadIdx.x) + 1 + ((i + 1 + colour + g.par) & 1);
     const ArrayAcc ax{vx, (size_t)g.P}, ay{vy, (size_t)g.P};
     if (comp == 0) {
-        if (i > g.ncy || j > g.ncx - 1) return;
+        if (i > g.ncy || j > g.nvxj) return;
         const double a = lx_diag(g, etab, etap, i, j);
         const double vn = ax(i, j) + omega * (rhs_x(g, rhs, i, j) - lx_row(g, etab, etap, ax, ay, i, j)) / a;
         vx[at(g, i, j)] = vn;
-        if (i == 1) vx[at(g, 0, j)] = g.sN * vn;
-        if (i == g.ncy) vx[at(g, g.ncy + 1, j)] = g.sS * vn;
+        if (i == 1 && g.bN) vx[at(g, 0, j)] = g.sN * vn;
+        if (i == g.ncy && g.bS) vx[at(g, g.ncy + 1, j)] = g.sS * vn;
     } else {
-        if (i > g.ncy - 1 || j > g.ncx) return;
+        if (i > g.nvyi || j > g.ncx) return;
         const double a = ly_diag(g, etab, etap, i, j);
         const double vn = ay(i, j) + omega * (rhs_y(g, rhs, i, j) - ly_row(g, etab, etap, ax, ay, i, j)) / a;
         vy[at(g, i, j)] = vn;
-        if (j == 1) vy[at(g, i, 0)] = g.sW * vn;
-        if (j == g.ncx) vy[at(g, i, g.ncx + 1)] = g.sE * vn;
+        if (j == 1 && g.bW) vy[at(g, i, 0)] = g.sW * vn;
+        if (j == g.ncx && g.bE) vy[at(g, i, g.ncx + 1)] = g.sE * vn;
     }
 }
 
@@ -172,8 +172,8 @@ __global__ void __launch_bounds__(BX *BY) k_residual(GridL g, const double *__re
     const int i = blockIdx.y * BY + threadIdx.y + 1;
     if (i > g.ncy || j > g.ncx) return;
     const ArrayAcc ax{vx, (size_t)g.P}, ay{vy, (size_t)g.P};
-    if (j < g.ncx) rx[at(g, i, j)] = rhs_x(g, rhs, i, j) - lx_row(g, etab, etap, ax, ay, i, j);
-    if (i < g.ncy) ry[at(g, i, j)] = rhs_y(g, rhs, i, j) - ly_row(g, etab, etap, ax, ay, i, j);
+    if (j <= g.nvxj) rx[at(g, i, j)] = rhs_x(g, rhs, i, j) - lx_row(g, etab, etap, ax, ay, i, j);
+    if (i <= g.nvyi) ry[at(g, i, j)] = rhs_y(g, rhs, i, j) - ly_row(g, etab, etap, ax, ay, i, j);
 }
 
 // ------------------------------------------------------------------ transfers (a5, a6, a7)
@@ -190,24 +190,24 @@ __global__ void k_restrict_vel(GridL gf, GridL gc, const double *__restrict__ rx
     const int J = blockIdx.x * BX + threadIdx.x + 1;
     const int I = blockIdx.y * BY + threadIdx.y + 1;
     if (I > gc.ncy || J > gc.ncx) return;
-    if (bxc && J < gc.ncx) {  // vx: x vertex-centred, y cell-centred
+    if (bxc && J <= gc.nvxj) {  // vx: x vertex-centred, y cell-centred
         double s = 0.0, w = 0.0;
 #pragma unroll
         for (int d = 0; d < 4; ++d) {
             const int i = 2 * I - 2 + d;
-            if (i < 1 || i > gf.ncy) continue;
+            if ((i < 1 && gf.bN) || (i > gf.ncy && gf.bS)) continue;
             const double row = 0.5 * rx[at(gf, i, 2 * J - 1)] + rx[at(gf, i, 2 * J)] + 0.5 * rx[at(gf, i, 2 * J + 1)];
             s += W4(d) * row;
             w += W4(d);
         }
         bxc[at(gc, I, J)] = s / (2.0 * w);
     }
-    if (byc && I < gc.ncy) {  // vy: x cell-centred, y vertex-centred
+    if (byc && I <= gc.nvyi) {  // vy: x cell-centred, y vertex-centred
         double s = 0.0, w = 0.0;
 #pragma unroll
         for (int d = 0; d < 4; ++d) {
             const int j = 2 * J - 2 + d;
-            if (j < 1 || j > gf.ncx) continue;
+            if ((j < 1 && gf.bW) || (j > gf.ncx && gf.bE)) continue;
             const double col = 0.5 * ry[at(gf, 2 * I - 1, j)] + ry[at(gf, 2 * I, j)] + 0.5 * ry[at(gf, 2 * I + 1, j)];
             s += W4(d) * col;
             w += W4(d);
@@ -217,23 +217,26 @@ __global__ void k_restrict_vel(GridL gf, GridL gc, const double *__restrict__ rx
 }
 // basic-node field (eta_b): [1/2,1,1/2] x [1/2,1,1/2] over fine basic nodes in [0,ncy]x[0,ncx]
 __global__ void k_restrict_b(GridL gf, GridL gc, const double *__restrict__ f, double *__restrict__ c) {
-    const int J = blockIdx.x * BX + threadIdx.x;
-    const int I = blockIdx.y * BY + threadIdx.y;
+    // owned coarse basic nodes: rows [1 - bN, ncy], cols [1 - bW, ncx] (row/col 0 of an
+    // interior tile is a halo owned by the neighbour); fine halo rows/cols are valid data,
+    // only nodes outside the GLOBAL domain are dropped (reading R6)
+    const int J = blockIdx.x * BX + threadIdx.x + (gc.bW ? 0 : 1);
+    const int I = blockIdx.y * BY + threadIdx.y + (gc.bN ? 0 : 1);
     if (I > gc.ncy || J > gc.ncx) return;
     const double w3[3] = {0.5, 1.0, 0.5};
     double s = 0.0, wy = 0.0, wx = 0.0;
     for (int dj = 0; dj < 3; ++dj) {
         const int j = 2 * J - 1 + dj;
-        if (j >= 0 && j <= gf.ncx) wx += w3[dj];
+        if (j >= 0 && (j <= gf.ncx || !gf.bE)) wx += w3[dj];
     }
     for (int di = 0; di < 3; ++di) {
         const int i = 2 * I - 1 + di;
-        if (i < 0 || i > gf.ncy) continue;
+        if (i < 0 || (i > gf.ncy && gf.bS)) continue;
         wy += w3[di];
         double row = 0.0;
         for (int dj = 0; dj < 3; ++dj) {
             const int j = 2 * J - 1 + dj;
-            if (j < 0 || j > gf.ncx) continue;
+            if (j < 0 || (j > gf.ncx && gf.bE)) continue;
             row += w3[dj] * f[at(gf, i, j)];
         }
         s += w3[di] * row;
@@ -248,16 +251,16 @@ __global__ void k_restrict_p(GridL gf, GridL gc, const double *__restrict__ f, d
     double s = 0.0, wy = 0.0, wx = 0.0;
     for (int dj = 0; dj < 4; ++dj) {
         const int j = 2 * J - 2 + dj;
-        if (j >= 1 && j <= gf.ncx) wx += W4(dj);
+        if ((j >= 1 || !gf.bW) && (j <= gf.ncx || !gf.bE)) wx += W4(dj);
     }
     for (int di = 0; di < 4; ++di) {
         const int i = 2 * I - 2 + di;
-        if (i < 1 || i > gf.ncy) continue;
+        if ((i < 1 && gf.bN) || (i > gf.ncy && gf.bS)) continue;
         wy += W4(di);
         double row = 0.0;
         for (int dj = 0; dj < 4; ++dj) {
             const int j = 2 * J - 2 + dj;
-            if (j < 1 || j > gf.ncx) continue;
+            if ((j < 1 && gf.bW) || (j > gf.ncx && gf.bE)) continue;
             row += W4(dj) * f[at(gf, i, j)];
         }
         s += W4(di) * row;
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(BX *BY) k_prolong(GridL gf, GridL gc, const do
     const int j = blockIdx.x * BX + threadIdx.x + 1;
     const int i = blockIdx.y * BY + threadIdx.y + 1;
     if (i > gf.ncy || j > gf.ncx) return;
-    if (j < gf.ncx) {  // vx: x vertex-centred, y cell-centred
+    if (j <= gf.nvxj) {  // vx: x vertex-centred, y cell-centred
         const int J0 = j >> 1;
         int I0;
         double wy0, wy1;
@@ -288,10 +291,10 @@ __global__ void __launch_bounds__(BX *BY) k_prolong(GridL gf, GridL gc, const do
             s = wy0 * ex[at(gc, I0, J0)] + wy1 * ex[at(gc, I0 + 1, J0)];
         const double vn = vx[at(gf, i, j)] + s;
         vx[at(gf, i, j)] = vn;
-        if (i == 1) vx[at(gf, 0, j)] = gf.sN * vn;
-        if (i == gf.ncy) vx[at(gf, gf.ncy + 1, j)] = gf.sS * vn;
+        if (i == 1 && gf.bN) vx[at(gf, 0, j)] = gf.sN * vn;
+        if (i == gf.ncy && gf.bS) vx[at(gf, gf.ncy + 1, j)] = gf.sS * vn;
     }
-    if (i < gf.ncy) {  // vy: y vertex-centred, x cell-centred
+    if (i <= gf.nvyi) {  // vy: y vertex-centred, x cell-centred
         const int I0 = i >> 1;
         int J0;
         double wx0, wx1;
@@ -305,8 +308,8 @@ __global__ void __launch_bounds__(BX *BY) k_prolong(GridL gf, GridL gc, const do
             s = wx0 * ey[at(gc, I0, J0)] + wx1 * ey[at(gc, I0, J0 + 1)];
         const double vn = vy[at(gf, i, j)] + s;
         vy[at(gf, i, j)] = vn;
-        if (j == 1) vy[at(gf, i, 0)] = gf.sW * vn;
-        if (j == gf.ncx) vy[at(gf, i, gf.ncx + 1)] = gf.sE * vn;
+        if (j == 1 && gf.bW) vy[at(gf, i, 0)] = gf.sW * vn;
+        if (j == gf.ncx && gf.bE) vy[at(gf, i, gf.ncx + 1)] = gf.sE * vn;
     }
 }
 
@@ -333,7 +336,7 @@ __global__ void __launch_bounds__(BX *BY) k_energy(GridL g, const double *__rest
         rhs.gx = gx;
         rhs.gy = gy;
         rhs.bx = rhs.by = nullptr;
-        if (j < g.ncx) {
+        if (j <= g.nvxj) {
             const double a = lx_diag(g, etab, etap, i, j);
             double r;
             if (force_only) r = (gx != 0.0) ? -gx * (0.5 * (rho[at(g, i - 1, j)] + rho[at(g, i, j)])) : 0.0;
@@ -341,7 +344,7 @@ __global__ void __launch_bounds__(BX *BY) k_energy(GridL g, const double *__rest
             sv += r * r / (-a);
             if (rxo) rxo[at(g, i, j)] = r;
         }
-        if (i < g.ncy) {
+        if (i <= g.nvyi) {
             const double a = ly_diag(g, etab, etap, i, j);
             double r;
             if (force_only) r = (gy != 0.0) ? -gy * (0.5 * (rho[at(g, i, j - 1)] + rho[at(g, i, j)])) : 0.0;
@@ -373,8 +376,8 @@ __global__ void __launch_bounds__(BX *BY) k_energy_vec(GridL g, const double *__
     const int i = blockIdx.y * BY + threadIdx.y + 1;
     double sv = 0.0, sp = 0.0;
     if (i <= g.ncy && j <= g.ncx) {
-        if (j < g.ncx) { const double r = rx[at(g, i, j)]; sv += r * r / (-lx_diag(g, etab, etap, i, j)); }
-        if (i < g.ncy) { const double r = ry[at(g, i, j)]; sv += r * r / (-ly_diag(g, etab, etap, i, j)); }
+        if (j <= g.nvxj) { const double r = rx[at(g, i, j)]; sv += r * r / (-lx_diag(g, etab, etap, i, j)); }
+        if (i <= g.nvyi) { const double r = ry[at(g, i, j)]; sv += r * r / (-ly_diag(g, etab, etap, i, j)); }
         const double r = rp[at(g, i, j)];
         sp = r * r * (etap[at(g, i, j)] / (2.0 * g.idx2 + 2.0 * g.idy2));
     }
@@ -468,25 +471,25 @@ __global__ void k_in_velocity(GridL g, const double *__restrict__ ux, const doub
     const int j = blockIdx.x * BX + threadIdx.x;  // 0..ncx+1
     const int i = blockIdx.y * BY + threadIdx.y;  // 0..ncy+1
     if (i > g.ncy + 1 || j > g.ncx + 1) return;
-    // vx
-    {
+    // vx: walls (global W/E sides) 0; mirrors (global N/S) from partners; tile halos 0
+    // (a decomposed level fills them by a halo exchange right after)
+    if (j <= g.ncx) {
         double v = 0.0;
-        if (j >= 1 && j <= g.ncx - 1) {
+        if (!((j == 0 && g.bW) || (j == g.ncx && g.bE))) {
             if (i >= 1 && i <= g.ncy) v = ux[(size_t)(i - 1) * (g.ncx + 1) + j];
-            else if (i == 0) v = g.sN * ux[(size_t)0 * (g.ncx + 1) + j];
-            else v = g.sS * ux[(size_t)(g.ncy - 1) * (g.ncx + 1) + j];
+            else if (i == 0) v = g.bN ? g.sN * ux[j] : 0.0;
+            else v = g.bS ? g.sS * ux[(size_t)(g.ncy - 1) * (g.ncx + 1) + j] : 0.0;
         }
-        if (j <= g.ncx) vx[at(g, i, j)] = v;
+        vx[at(g, i, j)] = v;
     }
-    // vy
-    {
+    if (i <= g.ncy) {
         double v = 0.0;
-        if (i >= 1 && i <= g.ncy - 1) {
+        if (!((i == 0 && g.bN) || (i == g.ncy && g.bS))) {
             if (j >= 1 && j <= g.ncx) v = uy[(size_t)i * g.ncx + (j - 1)];
-            else if (j == 0) v = g.sW * uy[(size_t)i * g.ncx + 0];
-            else v = g.sE * uy[(size_t)i * g.ncx + (g.ncx - 1)];
+            else if (j == 0) v = g.bW ? g.sW * uy[(size_t)i * g.ncx] : 0.0;
+            else v = g.bE ? g.sE * uy[(size_t)i * g.ncx + (g.ncx - 1)] : 0.0;
         }
-        if (i <= g.ncy) vy[at(g, i, j)] = v;
+        vy[at(g, i, j)] = v;
     }
 }
 __global__ void k_in_p(GridL g, const double *__restrict__ u, double *__restrict__ a) {
@@ -499,20 +502,23 @@ __global__ void k_in_b(GridL g, const double *__restrict__ u, double *__restrict
 }
 __global__ void k_in_vx_raw(GridL g, const double *__restrict__ u, double *__restrict__ a) {
     const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y + 1;
-    if (i <= g.ncy && j <= g.ncx) a[at(g, i, j)] = (j == 0 || j == g.ncx) ? 0.0 : u[(size_t)(i - 1) * (g.ncx + 1) + j];
+    if (i <= g.ncy && j <= g.ncx)
+        a[at(g, i, j)] = ((j == 0 && g.bW) || (j == g.ncx && g.bE)) ? 0.0 : u[(size_t)(i - 1) * (g.ncx + 1) + j];
 }
 __global__ void k_in_vy_raw(GridL g, const double *__restrict__ u, double *__restrict__ a) {
     const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y;
-    if (i <= g.ncy && j <= g.ncx) a[at(g, i, j)] = (i == 0 || i == g.ncy) ? 0.0 : u[(size_t)i * g.ncx + (j - 1)];
+    if (i <= g.ncy && j <= g.ncx)
+        a[at(g, i, j)] = ((i == 0 && g.bN) || (i == g.ncy && g.bS)) ? 0.0 : u[(size_t)i * g.ncx + (j - 1)];
 }
 __global__ void k_out_vx(GridL g, const double *__restrict__ a, double *__restrict__ u) {
     const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y + 1;
     if (i <= g.ncy && j <= g.ncx)
-        u[(size_t)(i - 1) * (g.ncx + 1) + j] = (j == 0 || j == g.ncx) ? 0.0 : a[at(g, i, j)];
+        u[(size_t)(i - 1) * (g.ncx + 1) + j] = ((j == 0 && g.bW) || (j == g.ncx && g.bE)) ? 0.0 : a[at(g, i, j)];
 }
 __global__ void k_out_vy(GridL g, const double *__restrict__ a, double *__restrict__ u) {
     const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y;
-    if (i <= g.ncy && j <= g.ncx) u[(size_t)i * g.ncx + (j - 1)] = (i == 0 || i == g.ncy) ? 0.0 : a[at(g, i, j)];
+    if (i <= g.ncy && j <= g.ncx)
+        u[(size_t)i * g.ncx + (j - 1)] = ((i == 0 && g.bN) || (i == g.ncy && g.bS)) ? 0.0 : a[at(g, i, j)];
 }
 __global__ void k_out_p(GridL g, const double *__restrict__ a, double *__restrict__ u, const double *shift) {
     const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y + 1;
@@ -537,12 +543,12 @@ __global__ void __launch_bounds__(BX *BY) k_apply(GridL g, const double *__restr
         ax[(size_t)(i - 1) * wx + j] = lx_row(g, etab, etap, axx, ayy, i, j) + (p[at(g, i, j)] - p[at(g, i, j + 1)]) * g.idx;
     else
         ax[(size_t)(i - 1) * wx + g.ncx] = 0.0;
-    if (j == 1) ax[(size_t)(i - 1) * wx] = 0.0;
+    if (j == 1 && g.bW) ax[(size_t)(i - 1) * wx] = 0.0;
     if (i < g.ncy)
         ay[(size_t)i * wy + (j - 1)] = ly_row(g, etab, etap, axx, ayy, i, j) + (p[at(g, i, j)] - p[at(g, i + 1, j)]) * g.idy;
     else
         ay[(size_t)g.ncy * wy + (j - 1)] = 0.0;
-    if (i == 1) ay[(size_t)(j - 1)] = 0.0;
+    if (i == 1 && g.bN) ay[(size_t)(j - 1)] = 0.0;
     ap[(size_t)(i - 1) * g.ncx + (j - 1)] =
         (vx[at(g, i, j)] - vx[at(g, i, j - 1)]) * g.idx + (vy[at(g, i, j)] - vy[at(g, i - 1, j)]) * g.idy;
 }
@@ -556,8 +562,8 @@ __global__ void __launch_bounds__(BX *BY) k_apply_padded(GridL g, const double *
     const int i = blockIdx.y * BY + threadIdx.y + 1;
     if (i > g.ncy || j > g.ncx) return;
     const ArrayAcc axx{vx, (size_t)g.P}, ayy{vy, (size_t)g.P};
-    if (j < g.ncx) ax[at(g, i, j)] = lx_row(g, etab, etap, axx, ayy, i, j) + (p[at(g, i, j)] - p[at(g, i, j + 1)]) * g.idx;
-    if (i < g.ncy) ay[at(g, i, j)] = ly_row(g, etab, etap, axx, ayy, i, j) + (p[at(g, i, j)] - p[at(g, i + 1, j)]) * g.idy;
+    if (j <= g.nvxj) ax[at(g, i, j)] = lx_row(g, etab, etap, axx, ayy, i, j) + (p[at(g, i, j)] - p[at(g, i, j + 1)]) * g.idx;
+    if (i <= g.nvyi) ay[at(g, i, j)] = ly_row(g, etab, etap, axx, ayy, i, j) + (p[at(g, i, j)] - p[at(g, i + 1, j)]) * g.idy;
     ap[at(g, i, j)] = (vx[at(g, i, j)] - vx[at(g, i, j - 1)]) * g.idx + (vy[at(g, i, j)] - vy[at(g, i - 1, j)]) * g.idy;
 }
 // energy weights of the GCR residual: ewx = 1/(-a_ii) at vx unknowns, ewy at vy unknowns,
@@ -567,16 +573,16 @@ __global__ void k_energy_weights(GridL g, const double *__restrict__ etab, const
                                  double *__restrict__ ewx, double *__restrict__ ewy, double *__restrict__ ewp) {
     const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y + 1;
     if (i > g.ncy || j > g.ncx) return;
-    if (j < g.ncx) ewx[at(g, i, j)] = 1.0 / (-lx_diag(g, etab, etap, i, j));
-    if (i < g.ncy) ewy[at(g, i, j)] = 1.0 / (-ly_diag(g, etab, etap, i, j));
+    if (j <= g.nvxj) ewx[at(g, i, j)] = 1.0 / (-lx_diag(g, etab, etap, i, j));
+    if (i <= g.nvyi) ewy[at(g, i, j)] = 1.0 / (-ly_diag(g, etab, etap, i, j));
     ewp[at(g, i, j)] = etap[at(g, i, j)] / (2.0 * g.idx2 + 2.0 * g.idy2);
 }
 // materialise b = f - G p (RHS_FINE) or copy b (RHS_ARRAYS) at the unknowns
 __global__ void k_make_rhs(GridL g, RhsArgs rhs, double *__restrict__ bx, double *__restrict__ by) {
     const int j = blockIdx.x * BX + threadIdx.x + 1, i = blockIdx.y * BY + threadIdx.y + 1;
     if (i > g.ncy || j > g.ncx) return;
-    if (j < g.ncx) bx[at(g, i, j)] = rhs_x(g, rhs, i, j);
-    if (i < g.ncy) by[at(g, i, j)] = rhs_y(g, rhs, i, j);
+    if (j <= g.nvxj) bx[at(g, i, j)] = rhs_x(g, rhs, i, j);
+    if (i <= g.nvyi) by[at(g, i, j)] = rhs_y(g, rhs, i, j);
 }
 __global__ void k_refresh_mirrors(GridL g, double *__restrict__ vx, double *__restrict__ vy) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -691,13 +697,13 @@ __global__ void __launch_bounds__(256) k_coarse_solve(GridL g, const double *__r
         if (r < nvx) {
             const int i = r / (g.ncx - 1) + 1, j = r % (g.ncx - 1) + 1;
             vx[at(g, i, j)] = v;
-            if (i == 1) vx[at(g, 0, j)] = g.sN * v;
-            if (i == g.ncy) vx[at(g, g.ncy + 1, j)] = g.sS * v;
+            if (i == 1 && g.bN) vx[at(g, 0, j)] = g.sN * v;
+            if (i == g.ncy && g.bS) vx[at(g, g.ncy + 1, j)] = g.sS * v;
         } else {
             const int i = (r - nvx) / g.ncx + 1, j = (r - nvx) % g.ncx + 1;
             vy[at(g, i, j)] = v;
-            if (j == 1) vy[at(g, i, 0)] = g.sW * v;
-            if (j == g.ncx) vy[at(g, i, g.ncx + 1)] = g.sE * v;
+            if (j == 1 && g.bW) vy[at(g, i, 0)] = g.sW * v;
+            if (j == g.ncx && g.bE) vy[at(g, i, g.ncx + 1)] = g.sE * v;
         }
     }
 }

@@ -116,8 +116,8 @@ __device__ __forceinline__ RowX lx_win(const GridL &g, const Win &w, int i) {
           2.0 * etaB * g.idx2 * w.B(F_VX, 1) +
           g.idxdy * (eta1 * (w.A(F_VY) - w.A(F_VY, 1)) + eta2 * (w.B(F_VY, 1) - w.B(F_VY)));
     r.a = c;
-    if (i == 1) r.a += g.sN * eta1 * g.idy2;
-    if (i == g.ncy) r.a += g.sS * eta2 * g.idy2;
+    if (i == 1 && g.bN) r.a += g.sN * eta1 * g.idy2;
+    if (i == g.ncy && g.bS) r.a += g.sS * eta2 * g.idy2;
     return r;
 }
 __device__ __forceinline__ RowX ly_win(const GridL &g, const Win &w, int j) {
@@ -128,8 +128,8 @@ __device__ __forceinline__ RowX ly_win(const GridL &g, const Win &w, int j) {
           etaW * g.idx2 * w.B(F_VY, -1) + c * w.B(F_VY) +
           g.idxdy * (etaE * (w.C(F_VX) - w.B(F_VX)) - etaW * (w.C(F_VX, -1) - w.B(F_VX, -1)));
     r.a = c;
-    if (j == 1) r.a += g.sW * etaW * g.idx2;
-    if (j == g.ncx) r.a += g.sE * etaE * g.idx2;
+    if (j == 1 && g.bW) r.a += g.sW * etaW * g.idx2;
+    if (j == g.ncx && g.bE) r.a += g.sE * etaE * g.idx2;
     return r;
 }
 // body force (reading R4/R23) at vx / vy nodes from the staged rho rows
@@ -149,21 +149,21 @@ struct JacobiOp {
     double omega, gx, gy;
     __device__ __forceinline__ void row(const GridL &g, const Win &w, int i, int j, double *) const {
         const size_t P = g.P;
-        if (j < g.ncx) {
+        if (j <= g.nvxj) {
             const RowX x = lx_win(g, w, i);
             const double b = (MODE == RHS_FINE) ? fx_win(w, gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
             const double vn = w.B(F_VX) + omega * (b - x.L) * rcp(x.a);
             vxo[(size_t)i * P + j] = vn;
-            if (i == 1) vxo[j] = g.sN * vn;
-            if (i == g.ncy) vxo[(size_t)(g.ncy + 1) * P + j] = g.sS * vn;
+            if (i == 1 && g.bN) vxo[j] = g.sN * vn;
+            if (i == g.ncy && g.bS) vxo[(size_t)(g.ncy + 1) * P + j] = g.sS * vn;
         }
-        if (i < g.ncy) {
+        if (i <= g.nvyi) {
             const RowX y = ly_win(g, w, j);
             const double b = (MODE == RHS_FINE) ? fy_win(w, gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
             const double vn = w.B(F_VY) + omega * (b - y.L) * rcp(y.a);
             vyo[(size_t)i * P + j] = vn;
-            if (j == 1) vyo[(size_t)i * P] = g.sW * vn;
-            if (j == g.ncx) vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
+            if (j == 1 && g.bW) vyo[(size_t)i * P] = g.sW * vn;
+            if (j == g.ncx && g.bE) vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
         }
     }
 };
@@ -177,11 +177,11 @@ struct ResidualOp {
     double gx, gy;
     __device__ __forceinline__ void row(const GridL &g, const Win &w, int i, int j, double *) const {
         const size_t P = g.P;
-        if (j < g.ncx) {
+        if (j <= g.nvxj) {
             const double b = (MODE == RHS_FINE) ? fx_win(w, gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
             rx[(size_t)i * P + j] = b - lx_win(g, w, i).L;
         }
-        if (i < g.ncy) {
+        if (i <= g.nvyi) {
             const double b = (MODE == RHS_FINE) ? fy_win(w, gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
             ry[(size_t)i * P + j] = b - ly_win(g, w, j).L;
         }
@@ -218,14 +218,14 @@ struct UzawaOp {
         acc[1] += rp * rp * (w.B(F_EP) / (2.0 * g.idx2 + 2.0 * g.idy2));
         acc[2] += pn;
         if (rpo) rpo[(size_t)i * g.P + j] = rp;
-        if (j < g.ncx) {
+        if (j <= g.nvxj) {
             const double pe = (w.B(F_4, 1) - ms) + alpha_s * w.B(F_EP, 1) * (-divB(g, w, 1));
             const RowX x = lx_win(g, w, i);
             const double r = fx_win(w, gx) - (pn - pe) * g.idx - x.L;
             acc[0] -= r * r * rcp(x.a);
             if (rxo) rxo[(size_t)i * g.P + j] = r;
         }
-        if (i < g.ncy) {
+        if (i <= g.nvyi) {
             const double ps = (w.C(F_4) - ms) + alpha_s * w.C(F_EP) * (-divC(g, w));
             const RowX y = ly_win(g, w, j);
             const double r = fy_win(w, gy) - (pn - ps) * g.idy - y.L;
@@ -259,14 +259,14 @@ struct PrecondApplyOp {
         wp[q] = dz;
         if (w0x) acc[0] += dz * w0p[q];
         else { acc[0] += dz * dz; acc[1] += w.B(F_4) * dz; }
-        if (j < g.ncx) {
+        if (j <= g.nvxj) {
             const double ze = alpha * w.B(F_EP, 1) * (w.B(F_4, 1) - divB(g, w, 1));
             const double v = lx_win(g, w, i).L + (zc - ze) * g.idx;
             wx[q] = v;
             if (w0x) acc[0] += v * w0x[q];
             else { acc[0] += v * v; acc[1] += rx[q] * v; }
         }
-        if (i < g.ncy) {
+        if (i <= g.nvyi) {
             const double ds = (w.C(F_VX) - w.C(F_VX, -1)) * g.idx + (w.C(F_VY) - w.B(F_VY)) * g.idy;
             const double zs = alpha * w.C(F_EP) * (w.C(F_4) - ds);
             const double v = ly_win(g, w, j).L + (zc - zs) * g.idy;

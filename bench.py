@@ -12,8 +12,9 @@ step    one full solve (all of SURVEY §8(a): V-cycles, smoother, transfers, coa
 workload default: BASELINE configs[3], layered lithosphere/mantle viscosity, 4096 x 4096 cells
         per GPU, plain Uzawa-MG (presets in configs/presets.json); the single-GPU config
         the metric's "% HBM peak" part is meaningful on (inputs ~1.4 GB >> 126 MB L2).
-N > 1   (torchrun): replicas of the per-GPU problem (weak scaling, no collective) until the
-        distributed path lands -- the JSON line says "parallelism": "replicas".
+N > 1   (torchrun): weak scaling, one 4096^2 tile per GPU of a px x py global grid (2x1, 2x2,
+        4x2), the exact 2D domain decomposition (stokes_create_dist: NCCL halo exchange
+        over NVLink, agglomerated coarse tail); value = global DOF-sweeps / max-over-ranks time.
 e2e     the same solve through the public API (Stokes.set_viscosity / set_density / solve)
         with pinned HOST inputs and outputs: H2D of eta_b, eta_p, rho_b and D2H of vx, vy, p
         inside the timed region.
@@ -206,23 +207,46 @@ def run_reference(args, world, rank):
 
 def run_ours(args, world, rank, local):
     import torch
-    from paper_2603_14040_b200 import Stokes
+    from paper_2603_14040_b200 import Stokes, StokesDist
+    from paper_2603_14040_b200.decomp import tile_windows, weak_problem
+    from paper_2603_14040_b200.stokes import shapes
     from synth.fields import workload
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pre = presets()[args.workload]
-    nx, ny = pre["n"]
     rtol = pre["rtol"]
-    w = workload(args.workload, nx, ny)
-    s = Stokes(nx, ny, w["Lx"], w["Ly"], w["bc"], **pre["opts"])
+    opts = dict(pre["opts"])
+    tile_n = pre["n"]
+    if world > 1:
+        # weak scaling (BASELINE config 4): one tile_n[0] x tile_n[1] tile per GPU, exact 2D
+        # decomposition over NVLink (stokes_create_dist, NCCL transport)
+        if opts.get("accel", 0):
+            opts["accel"] = 0  # the decomposed path runs plain Uzawa-MG
+        NX, NY, Lx, Ly, px, py = weak_problem(world, tile_n[0])
+        win = tile_windows(NX, NY, px, py, rank)
+        i0, j0 = win["b"][0].start, win["b"][1].start
+        nxt, nyt = NX // px, NY // py
+        w = workload(args.workload, NX, NY, Lx, Ly, win_b=(i0, j0, nyt + 1, nxt + 1), win_p=(i0, j0, nyt, nxt))
+        s = StokesDist(NX, NY, Lx, Ly, w["bc"], px=px, py=py, rank=rank, **opts)
+        gshape = [s.gnx, s.gny]
+    else:
+        NX, NY = tile_n
+        px = py = 1
+        w = workload(args.workload, NX, NY)
+        s = Stokes(NX, NY, w["Lx"], w["Ly"], w["bc"], **opts)
+        gshape = [NX, NY]
+    nx, ny = s.nx, s.ny
     eb, ep, rho = (torch.from_numpy(w[k]).to(dev) for k in ("eta_b", "eta_p", "rho_b"))
     s.set_viscosity(eb, ep)
     s.set_density(rho)
     s.set_gravity(w["gx"], w["gy"])
-    shp = [s.level_shape(l) for l in range(s.num_levels)]
-    per_vc = dof_sweeps_per_vcycle(shp, pre["opts"].get("smoother", 0))
-    vpi = pre["opts"].get("vcycles_per_iter", 1)
+    # DOF-sweeps of one V-cycle on the GLOBAL hierarchy (identical to the single-domain one)
+    shp = global_levels(gshape[0], gshape[1], opts)
+    if world == 1:
+        assert shp == [tuple(s.level_shape(l)) for l in range(s.num_levels)], "level rule mismatch"
+    per_vc = dof_sweeps_per_vcycle(shp, opts.get("smoother", 0))
+    vpi = opts.get("vcycles_per_iter", 1)
     stream = s.stream
 
     for _ in range(args.warmup):
@@ -244,12 +268,11 @@ def run_ours(args, world, rank, local):
     barrier(world)
     ms = e0.elapsed_time(e1)
     ms_max = allreduce_max(ms, world, dev)
-    dofs_rank = sum(iters) * vpi * per_vc
-    value = dofs_rank * world / (ms_max / 1e3)
+    dofs = sum(iters) * vpi * per_vc  # whole job (global problem)
+    value = dofs / (ms_max / 1e3)
 
-    # ---- e2e through the public API with pinned host buffers
+    # ---- e2e through the public API with pinned host buffers (this rank's arrays)
     host = {k: torch.from_numpy(w[k]).pin_memory() for k in ("eta_b", "eta_p", "rho_b")}
-    from paper_2603_14040_b200.stokes import shapes
     sh = shapes(nx, ny)
     hz = {k: torch.zeros(sh[k], dtype=torch.float64).pin_memory() for k in ("vx", "vy", "p")}
     hout = {k: torch.empty(sh[k], dtype=torch.float64).pin_memory() for k in ("vx", "vy", "p")}
@@ -268,10 +291,16 @@ def run_ours(args, world, rank, local):
         e2.append(time.perf_counter() - t0)
         e2_iters += r["iters"]
     e2_t = allreduce_max(sum(e2), world, dev)
-    e2e_value = e2_iters * vpi * per_vc * world / e2_t
+    e2e_value = e2_iters * vpi * per_vc / e2_t
 
-    # ---- roofline of the dominant kernel (fine Jacobi sweep), live CUDA events
-    k_ms, k_bytes = s.time_kernel("jacobi", reps=20)
+    # ---- roofline of the dominant kernel (fine Jacobi sweep), live CUDA events, on a
+    # single-domain handle of this GPU's tile
+    kh = s if world == 1 else Stokes(nx, ny, 1.0, 1.0, w["bc"], **opts)
+    if world > 1:
+        kh.set_viscosity(eb, ep)
+        kh.set_density(rho)
+        kh.set_gravity(w["gx"], w["gy"])
+    k_ms, k_bytes = kh.time_kernel("jacobi", reps=20)
     peak, peak_src = measured_peak()
     achieved = k_bytes / (k_ms / 1e3) / 1e9
     sweeps_per_solve = statistics.mean(iters) * vpi * 2 * shp[0][2]
@@ -286,16 +315,16 @@ def run_ours(args, world, rank, local):
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: {WORKLOAD_DOC[args.workload]}", "grid_per_gpu": [nx, ny],
-                   "levels": [list(x) for x in shp], "opts": pre["opts"], "rtol": rtol,
+                   "grid_global": gshape, "levels": [list(x) for x in shp], "opts": opts, "rtol": rtol,
                    "iters_per_solve": statistics.mean(iters), "solve_ms": ms_max / args.steps,
-                   "dof_sweeps_per_solve": dofs_rank / args.steps,
-                   "l2": "inputs larger than L2 (fine fields 16.8M cells x 8 B, hierarchy > 1 GB vs 126 MB L2)",
-                   "parallelism": "replicas" if world > 1 else "single GPU"},
-        "roofline": {"kernel": "fine-level damped-Jacobi sweep (k_jacobi)", "bound": "hbm", "achieved": achieved,
-                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": tr,
+                   "dof_sweeps_per_solve": dofs / args.steps,
+                   "l2": "inputs larger than L2 (fine fields 16.8M cells x 8 B per GPU, hierarchy > 1 GB vs 126 MB L2)",
+                   "parallelism": f"dd{px}x{py}" if world > 1 else "single GPU"},
+        "roofline": {"kernel": "fine-level damped-Jacobi sweep (k_stream<JacobiOp>)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": tr,
                      "algorithmic_bytes_per_launch": k_bytes, "launch_ms": k_ms, "peak_source": peak_src,
                      "share_of_step": share},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
                 "seconds_per_step": e2_t / len(e2)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
@@ -304,6 +333,22 @@ def run_ours(args, world, rank, local):
         line["cpu_baseline"] = cb
     print(json.dumps(line), flush=True)
     return 0
+
+
+def global_levels(nx, ny, opts):
+    """(ncx, ncy, nu) of the global hierarchy (reading R8/R9), as the library builds it."""
+    import math
+    cm = opts.get("coarse_min", 8)
+    nu1, g = opts.get("nu1", 5), opts.get("nu_growth", 1.0)
+    out, l = [], 0
+    while True:
+        out.append((nx, ny, int(math.floor(nu1 * g ** l + 0.5))))
+        l += 1
+        if nx % 2 or ny % 2 or min(nx, ny) // 2 < cm:
+            break
+        nx //= 2
+        ny //= 2
+    return out
 
 
 def main():

@@ -106,6 +106,27 @@ int stokes_workspace_bytes(int nx, int ny, const stokes_opts *opts, size_t *byte
 int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const stokes_opts *opts,
                   void *cuda_stream, void *workspace, size_t workspace_bytes, stokes_t *out);
 
+/* 2D domain decomposition.  The global nx x ny grid is
+ * split into px x py tiles of (nx/px) x (ny/py) cells (nx % px == ny % py == 0); tile
+ * (tx, ty) = (rank % px, rank / px).  Exact: iterates equal the single-domain solve's up to
+ * the order of global sums.  Levels whose tiles are >= 64 cells wide are distributed (halo
+ * exchange after every velocity / residual / correction / pressure write); the coarser
+ * levels are agglomerated: every process holds the global grid of the first coarse level
+ * and runs the coarse tail redundantly.  Options: accel must be STOKES_ACCEL_NONE.
+ *   rank < 0  VIRTUAL: all tiles in this process on the current GPU; every array of the
+ *             calls below is the GLOBAL user-layout array (tests of the decomposition).
+ *   rank >= 0 NCCL: this process owns tile `rank` (one GPU per process), nccl_unique_id =
+ *             128 bytes from stokes_nccl_unique_id() on rank 0, shared by the caller; every
+ *             array is the tile's WINDOW of the global user layout, i.e. the user layout of
+ *             an (nx/px) x (ny/py) problem (shared edge nodes appear in both windows).
+ * Supported calls on a decomposed handle: set_viscosity, set_density, set_gravity,
+ * residual (energy only: rx = ry = rp = NULL), solve, num_levels, launch_count, destroy;
+ * the per-step entry points return STOKES_EINVAL.  The library allocates its own memory. */
+int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], int px, int py, int rank,
+                       const void *nccl_unique_id, const stokes_opts *opts, void *cuda_stream, stokes_t *out);
+/* 128-byte NCCL unique id for stokes_create_dist (call on rank 0, broadcast it). */
+int stokes_nccl_unique_id(void *id128);
+
 /* Release the handle (and its own allocations). */
 int stokes_destroy(stokes_t h);
 

@@ -5,10 +5,24 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libstokes_b200.so")
-SOURCES = ["kernels.cu", "stream.cu", "gcr.cu", "driver.cu"]
+SOURCES = ["kernels.cu", "stream.cu", "gcr.cu", "driver.cu", "dist.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir():
+    """NCCL headers + library of the torch-bundled nvidia-nccl wheel (same lib torch loads)."""
+    try:
+        import nvidia.nccl as n
+        return os.path.dirname(n.__file__) if n.__file__ else list(n.__path__)[0]
+    except Exception:
+        return "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl"
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xcompiler", "-fvisibility=hidden"]
+         "-Xcompiler", "-fPIC", "-shared", "-Xcompiler", "-fvisibility=hidden",
+         "-I", os.path.join(NCCL, "include")]
+LIBS = ["-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
 
 
 def _stale():
@@ -23,7 +37,7 @@ def _stale():
 def build(force=False, verbose=False):
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES]]
+    cmd = [NVCC, *FLAGS, "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd, cwd=CSRC)

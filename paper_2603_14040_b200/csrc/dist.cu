@@ -1,0 +1,797 @@
+// 2D domain decomposition of the multigrid Stokes solve.
+//
+// The global nx x ny grid is split into px x py tiles of (nx/px) x (ny/py) cells, the
+// paper's Cartesian decomposition (interior + 1-cell halo, boundary
+// ranks' halos repurposed as boundary nodes).  It is EXACT: every
+// stencil of a tile reads the same values the single-domain solve reads (halos refreshed
+// after every write of a velocity / residual / correction / pressure field), so the
+// iterates equal the single-GPU ones up to the order of the global sums.
+//
+//   distributed levels 0..La-1  each tile runs the same kernels with per-side global-
+//                               boundary flags (GridL.bN/bS/bW/bE, mirrors and walls only on
+//                               global sides); two-phase halo exchange (W/E columns over all
+//                               rows, then N/S rows over all columns: corners included)
+//   agglomeration level La      the tiles' restricted residuals are gathered into the GLOBAL
+//                               level-La grid, held by every process (the B200 analogue of the
+//                               paper's CPU-side coarse levels); the coarse
+//                               tail of the V-cycle runs there redundantly and every tile takes
+//                               its window of the correction (no scatter message)
+//   global sums                 (Sv, Sp, sum p) per tile -> fixed-order combine / ncclAllReduce
+//
+// Transports: VIRTUAL (rank < 0): all tiles in this process on one GPU, halos copied by
+// strip-copy kernels -- the exactness test of the decomposition on one B200.  NCCL (rank >=
+// 0): one tile per process/GPU, ncclSend/ncclRecv of packed halo columns and contiguous rows
+// over NVLink, ncclAllGather for the agglomeration, ncclAllReduce for the sums; all
+// graph-capturable.
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <nccl.h>
+
+#include "handle.h"
+
+using namespace sk;
+
+#define MAXT 64
+
+struct Dist {
+    int NX, NY, px, py, nxt, nyt;
+    double Lx, Ly;
+    int bc[4];
+    stokes_opts o;
+    int rank;  // -1 virtual
+    int nt;
+    stokes_s *tile[MAXT];
+    int tx[MAXT], ty[MAXT];
+    int La;          // distributed levels
+    int L;           // total levels (global hierarchy)
+    stokes_s *tail;  // global level La and below
+    cudaStream_t stream;
+    bool own_stream;
+    double *dscal;   // [0] E [1] Sv [2] Sp [3] Sf [4] zero
+    double *hsc;
+    ncclComm_t comm;
+    double *sbuf, *rbuf;
+    size_t nbuf;
+    long long launches;
+    cudaGraphExec_t exec[2];
+    long long body_kernels;
+    int pcur;
+    bool have_eta, have_rho;
+    double gx, gy;
+};
+
+namespace {
+
+enum { FX_V = 0, FX_R = 1, FX_P = 2, FX_ETA = 3, FX_RHO = 4 };
+
+LaunchCtx dctx(Dist &D) { return LaunchCtx{D.stream, &D.launches}; }
+
+int nfields(stokes_s *h, int l, int which, int idx, double **f) {
+    Level &L = h->lev[l];
+    switch (which) {
+    case FX_V: f[0] = L.vx[idx]; f[1] = L.vy[idx]; return 2;
+    case FX_R: f[0] = L.rx; f[1] = L.ry; return 2;
+    case FX_P: f[0] = h->pbuf[idx]; return 1;
+    case FX_ETA: f[0] = L.etab; f[1] = L.etap; return 2;
+    default: f[0] = h->rho; return 1;
+    }
+}
+int tile_at(Dist &D, int tx, int ty) { return D.rank < 0 ? ty * D.px + tx : -1; }
+
+void add_strip(StripList &s, double *dst, const double *src, int n, int ds, int ss) {
+    s.dst[s.count] = dst;
+    s.src[s.count] = src;
+    s.n[s.count] = n;
+    s.dstride[s.count] = ds;
+    s.sstride[s.count] = ss;
+    ++s.count;
+}
+
+// halo exchange of the selected fields of level l (two phases, corners included)
+int exchange(Dist &D, int l, int which, int idx) {
+    const LaunchCtx c = dctx(D);
+    double *f[2], *fu[2];
+    if (D.rank < 0) {  // ---- virtual: strip-copy kernels between the tiles' buffers
+        StripList s;
+        s.count = 0;
+        for (int k = 0; k < D.nt; ++k) {
+            const GridL &g = D.tile[k]->lev[l].g;
+            const int nf = nfields(D.tile[k], l, which, idx, f);
+            if (D.tx[k] + 1 < D.px) {
+                nfields(D.tile[tile_at(D, D.tx[k] + 1, D.ty[k])], l, which, idx, fu);
+                for (int q = 0; q < nf; ++q) add_strip(s, f[q] + at(g, 0, g.ncx + 1), fu[q] + at(g, 0, 1), g.ncy + 2, g.P, g.P);
+            }
+            if (D.tx[k] > 0) {
+                nfields(D.tile[tile_at(D, D.tx[k] - 1, D.ty[k])], l, which, idx, fu);
+                for (int q = 0; q < nf; ++q) add_strip(s, f[q] + at(g, 0, 0), fu[q] + at(g, 0, g.ncx), g.ncy + 2, g.P, g.P);
+            }
+        }
+        if (s.count) launch_strips(c, s);
+        s.count = 0;
+        for (int k = 0; k < D.nt; ++k) {
+            const GridL &g = D.tile[k]->lev[l].g;
+            const int nf = nfields(D.tile[k], l, which, idx, f);
+            if (D.ty[k] + 1 < D.py) {
+                nfields(D.tile[tile_at(D, D.tx[k], D.ty[k] + 1)], l, which, idx, fu);
+                for (int q = 0; q < nf; ++q) add_strip(s, f[q] + at(g, g.ncy + 1, 0), fu[q] + at(g, 1, 0), g.ncx + 2, 1, 1);
+            }
+            if (D.ty[k] > 0) {
+                nfields(D.tile[tile_at(D, D.tx[k], D.ty[k] - 1)], l, which, idx, fu);
+                for (int q = 0; q < nf; ++q) add_strip(s, f[q] + at(g, 0, 0), fu[q] + at(g, g.ncy, 0), g.ncx + 2, 1, 1);
+            }
+        }
+        if (s.count) launch_strips(c, s);
+        return STOKES_OK;
+    }
+    // ---- NCCL: one tile here; neighbours are ranks
+    stokes_s *t = D.tile[0];
+    const GridL &g = t->lev[l].g;
+    const int nf = nfields(t, l, which, idx, f);
+    const int tx = D.tx[0], ty = D.ty[0];
+    const int W = tx > 0 ? D.rank - 1 : -1, E = tx + 1 < D.px ? D.rank + 1 : -1;
+    const int N = ty > 0 ? D.rank - D.px : -1, S = ty + 1 < D.py ? D.rank + D.px : -1;
+    const int rows = g.ncy + 2;
+    if (W >= 0 || E >= 0) {
+        StripList s;
+        s.count = 0;
+        for (int q = 0; q < nf; ++q) {
+            if (W >= 0) add_strip(s, D.sbuf + (size_t)q * rows, f[q] + at(g, 0, 1), rows, 1, g.P);
+            if (E >= 0) add_strip(s, D.sbuf + (size_t)(nf + q) * rows, f[q] + at(g, 0, g.ncx), rows, 1, g.P);
+        }
+        launch_strips(c, s);
+        ncclGroupStart();
+        if (W >= 0) {
+            ncclSend(D.sbuf, (size_t)nf * rows, ncclDouble, W, D.comm, D.stream);
+            ncclRecv(D.rbuf, (size_t)nf * rows, ncclDouble, W, D.comm, D.stream);
+        }
+        if (E >= 0) {
+            ncclSend(D.sbuf + (size_t)nf * rows, (size_t)nf * rows, ncclDouble, E, D.comm, D.stream);
+            ncclRecv(D.rbuf + (size_t)nf * rows, (size_t)nf * rows, ncclDouble, E, D.comm, D.stream);
+        }
+        if (ncclGroupEnd() != ncclSuccess) return STOKES_ENCCL;
+        s.count = 0;
+        for (int q = 0; q < nf; ++q) {
+            if (W >= 0) add_strip(s, f[q] + at(g, 0, 0), D.rbuf + (size_t)q * rows, rows, g.P, 1);
+            if (E >= 0) add_strip(s, f[q] + at(g, 0, g.ncx + 1), D.rbuf + (size_t)(nf + q) * rows, rows, g.P, 1);
+        }
+        launch_strips(c, s);
+    }
+    if (N >= 0 || S >= 0) {
+        ncclGroupStart();
+        for (int q = 0; q < nf; ++q) {
+            if (N >= 0) {
+                ncclSend(f[q] + at(g, 1, 0), g.ncx + 2, ncclDouble, N, D.comm, D.stream);
+                ncclRecv(f[q] + at(g, 0, 0), g.ncx + 2, ncclDouble, N, D.comm, D.stream);
+            }
+            if (S >= 0) {
+                ncclSend(f[q] + at(g, g.ncy, 0), g.ncx + 2, ncclDouble, S, D.comm, D.stream);
+                ncclRecv(f[q] + at(g, g.ncy + 1, 0), g.ncx + 2, ncclDouble, S, D.comm, D.stream);
+            }
+        }
+        if (ncclGroupEnd() != ncclSuccess) return STOKES_ENCCL;
+    }
+    return STOKES_OK;
+}
+
+// tile rectangle [r0, r0+nr) x [c0, c0+nc) of a level-La field -> global tail level 0 at
+// the tile's offset (NCCL: all-gathered first).  `which`: 0 velocity rhs (bx, by), 1 eta.
+int gather_to_tail(Dist &D, int which) {
+    Level &T0 = D.tail->lev[0];
+    const int La = D.La;
+    auto rect = [&](int k, int f, int &r0, int &c0, int &nr, int &nc) {
+        const GridL &gc = D.tile[0]->lev[La].g;  // all tiles share sizes
+        (void)k;
+        if (which == 0) { r0 = 1; c0 = 1; nr = gc.ncy; nc = gc.ncx; }  // owned unknowns (+ global walls, 0)
+        else if (f == 0) { r0 = 0; c0 = 0; nr = gc.ncy + 1; nc = gc.ncx + 1; }  // basic nodes (halo-consistent)
+        else { r0 = 1; c0 = 1; nr = gc.ncy; nc = gc.ncx; }  // P nodes
+    };
+    const GridL &gc = D.tile[0]->lev[La].g;
+    if (D.rank < 0) {
+        for (int k = 0; k < D.nt; ++k) {
+            Level &C = D.tile[k]->lev[La];
+            double *src[2] = {which == 0 ? C.bx : C.etab, which == 0 ? C.by : C.etap};
+            double *dst[2] = {which == 0 ? T0.bx : T0.etab, which == 0 ? T0.by : T0.etap};
+            const int gi = D.ty[k] * gc.ncy, gj = D.tx[k] * gc.ncx;
+            for (int f = 0; f < 2; ++f) {
+                int r0, c0, nr, nc;
+                rect(k, f, r0, c0, nr, nc);
+                CK(cudaMemcpy2DAsync(dst[f] + at(T0.g, gi + r0, gj + c0), T0.g.P * 8, src[f] + at(gc, r0, c0), gc.P * 8,
+                                     (size_t)nc * 8, nr, cudaMemcpyDeviceToDevice, D.stream));
+            }
+        }
+        return STOKES_OK;
+    }
+    Level &C = D.tile[0]->lev[La];
+    double *src[2] = {which == 0 ? C.bx : C.etab, which == 0 ? C.by : C.etap};
+    double *dst[2] = {which == 0 ? T0.bx : T0.etab, which == 0 ? T0.by : T0.etap};
+    const size_t blk = (size_t)2 * (gc.ncy + 1) * (gc.ncx + 1);
+    for (int f = 0; f < 2; ++f) {
+        int r0, c0, nr, nc;
+        rect(0, f, r0, c0, nr, nc);
+        CK(cudaMemcpy2DAsync(D.sbuf + f * (blk / 2), (size_t)nc * 8, src[f] + at(gc, r0, c0), gc.P * 8, (size_t)nc * 8,
+                             nr, cudaMemcpyDeviceToDevice, D.stream));
+    }
+    if (ncclAllGather(D.sbuf, D.rbuf, blk, ncclDouble, D.comm, D.stream) != ncclSuccess) return STOKES_ENCCL;
+    for (int r = 0; r < D.px * D.py; ++r) {
+        const int gi = (r / D.px) * gc.ncy, gj = (r % D.px) * gc.ncx;
+        for (int f = 0; f < 2; ++f) {
+            int r0, c0, nr, nc;
+            rect(r, f, r0, c0, nr, nc);
+            CK(cudaMemcpy2DAsync(dst[f] + at(T0.g, gi + r0, gj + c0), T0.g.P * 8, D.rbuf + r * blk + f * (blk / 2),
+                                 (size_t)nc * 8, (size_t)nc * 8, nr, cudaMemcpyDeviceToDevice, D.stream));
+        }
+    }
+    return STOKES_OK;
+}
+
+// every tile takes its window (halos included) of the tail's level-0 correction
+int scatter_from_tail(Dist &D) {
+    Level &T0 = D.tail->lev[0];
+    for (int k = 0; k < D.nt; ++k) {
+        Level &C = D.tile[k]->lev[D.La];
+        const GridL &gc = C.g;
+        const int gi = D.ty[k] * gc.ncy, gj = D.tx[k] * gc.ncx;
+        CK(cudaMemcpy2DAsync(C.vx[0] + at(gc, 0, 0), gc.P * 8, T0.vx[0] + at(T0.g, gi, gj), T0.g.P * 8,
+                             (size_t)(gc.ncx + 2) * 8, gc.ncy + 2, cudaMemcpyDeviceToDevice, D.stream));
+        CK(cudaMemcpy2DAsync(C.vy[0] + at(gc, 0, 0), gc.P * 8, T0.vy[0] + at(T0.g, gi, gj), T0.g.P * 8,
+                             (size_t)(gc.ncx + 2) * 8, gc.ncy + 2, cudaMemcpyDeviceToDevice, D.stream));
+    }
+    return STOKES_OK;
+}
+
+RhsArgs tile_rhs(stokes_s *t, int l, bool fine) {
+    return fine ? rhs_fine(t) : rhs_arrays(t->lev[l].bx, t->lev[l].by);
+}
+
+// nsweeps smoother sweeps on distributed level l; cur = index of the buffer holding v
+int dsmooth(Dist &D, int l, int &cur, int n, bool zero_in, bool fine) {
+    if (n <= 0 && zero_in) {
+        for (int k = 0; k < D.nt; ++k) {
+            Level &L = D.tile[k]->lev[l];
+            CK(cudaMemsetAsync(L.vx[cur] - COL_OFF, 0, field_doubles(L.g) * 8, D.stream));
+            CK(cudaMemsetAsync(L.vy[cur] - COL_OFF, 0, field_doubles(L.g) * 8, D.stream));
+        }
+        return STOKES_OK;
+    }
+    int st;
+    for (int s = 0; s < n; ++s) {
+        if (D.o.smoother == STOKES_SMOOTH_JACOBI) {
+            for (int k = 0; k < D.nt; ++k) {
+                stokes_s *t = D.tile[k];
+                Level &L = t->lev[l];
+                launch_jacobi(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur], L.vx[1 - cur], L.vy[1 - cur],
+                              tile_rhs(t, l, fine), D.o.omega_v, zero_in && s == 0);
+            }
+            cur ^= 1;
+            if ((st = exchange(D, l, FX_V, cur))) return st;
+        } else {
+            if (zero_in && s == 0)
+                for (int k = 0; k < D.nt; ++k) {
+                    Level &L = D.tile[k]->lev[l];
+                    CK(cudaMemsetAsync(L.vx[cur] - COL_OFF, 0, field_doubles(L.g) * 8, D.stream));
+                    CK(cudaMemsetAsync(L.vy[cur] - COL_OFF, 0, field_doubles(L.g) * 8, D.stream));
+                }
+            for (int comp = 0; comp < 2; ++comp)
+                for (int colour = 0; colour < 2; ++colour) {
+                    for (int k = 0; k < D.nt; ++k) {
+                        stokes_s *t = D.tile[k];
+                        Level &L = t->lev[l];
+                        launch_rbgs_phase(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur], tile_rhs(t, l, fine),
+                                          D.o.omega_v, comp, colour);
+                    }
+                    if ((st = exchange(D, l, FX_V, cur))) return st;
+                }
+        }
+    }
+    return STOKES_OK;
+}
+
+// distributed V-cycle on level l (Eq. multigrid_levels); v in buffer 0
+int dvcycle(Dist &D, int l, bool fine, bool zero_in) {
+    int cur = 0, st;
+    const int nu = D.tile[0]->lev[l].nu;
+    if ((st = dsmooth(D, l, cur, nu, zero_in, fine))) return st;               // (1)
+    for (int k = 0; k < D.nt; ++k) {                                            // (2)
+        stokes_s *t = D.tile[k];
+        Level &L = t->lev[l];
+        launch_residual(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur], tile_rhs(t, l, fine), L.rx, L.ry);
+    }
+    if ((st = exchange(D, l, FX_R, 0))) return st;
+    for (int k = 0; k < D.nt; ++k) {                                            // (3)
+        stokes_s *t = D.tile[k];
+        launch_restrict_vel(ctx(t), t->lev[l].g, t->lev[l + 1].g, t->lev[l].rx, t->lev[l].ry, t->lev[l + 1].bx,
+                            t->lev[l + 1].by);
+    }
+    if (l + 1 < D.La) {                                                         // (4)
+        if ((st = dvcycle(D, l + 1, false, true))) return st;
+    } else {  // agglomerated coarse tail, redundant on every process
+        if ((st = gather_to_tail(D, 0))) return st;
+        Level &T0 = D.tail->lev[0];
+        vcycle(D.tail, 0, T0.vx[0], T0.vy[0], T0.vx[1], T0.vy[1], rhs_arrays(T0.bx, T0.by), true);
+        if ((st = scatter_from_tail(D))) return st;
+    }
+    for (int k = 0; k < D.nt; ++k) {                                            // (5)
+        stokes_s *t = D.tile[k];
+        Level &L = t->lev[l], &C = t->lev[l + 1];
+        launch_prolong(ctx(t), L.g, C.g, C.vx[0], C.vy[0], L.vx[cur], L.vy[cur]);
+    }
+    if ((st = exchange(D, l, FX_V, cur))) return st;
+    if ((st = dsmooth(D, l, cur, nu, false, fine))) return st;                 // (6)
+    if (cur != 0) {
+        for (int k = 0; k < D.nt; ++k) {
+            Level &L = D.tile[k]->lev[l];
+            CK(cudaMemcpyAsync(L.vx[0] - COL_OFF, L.vx[cur] - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, D.stream));
+            CK(cudaMemcpyAsync(L.vy[0] - COL_OFF, L.vy[cur] - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, D.stream));
+        }
+    }
+    return STOKES_OK;
+}
+
+// combine the tiles' local (Sv, Sp, sum p) at t->scal[S_LOC..] into E (dscal[0]) and the
+// global pressure mean (each tile's scal[S_MSHIFT] when write_mean)
+int combine(Dist &D, bool write_mean) {
+    const LaunchCtx c = dctx(D);
+    const double *loc[MAXT];
+    double *ms[MAXT];
+    for (int k = 0; k < D.nt; ++k) {
+        loc[k] = D.tile[k]->scal + S_LOC;
+        ms[k] = D.tile[k]->scal + S_MSHIFT;
+    }
+    if (D.rank >= 0)
+        if (ncclAllReduce(D.tile[0]->scal + S_LOC, D.tile[0]->scal + S_LOC, 3, ncclDouble, ncclSum, D.comm,
+                          D.stream) != ncclSuccess)
+            return STOKES_ENCCL;
+    launch_dist_final(c, loc, D.nt, D.dscal + 3, 1.0 / ((double)D.NX * D.NY), D.dscal, ms, write_mean ? D.nt : 0);
+    return STOKES_OK;
+}
+
+// local sums of the fused Uzawa pass (pout_idx >= 0: p' -> pbuf[pout_idx]) or of the energy
+// of the current state only (pout_idx < 0) -> each tile's scal[S_LOC..S_LOC+2]
+int tiles_uzawa(Dist &D, int pin_idx, int pout_idx, double alpha_s) {
+    const bool fused = stream_ok(D.tile[0]->lev[0].g);
+    for (int k = 0; k < D.nt; ++k) {
+        stokes_s *t = D.tile[k];
+        Level &F = t->lev[0];
+        const LaunchCtx c = ctx(t);
+        const double *pin = t->pbuf[pin_idx];
+        double *pout = pout_idx >= 0 ? t->pbuf[pout_idx] : nullptr;
+        const double *ms = t->scal + (pout ? S_MSHIFT : S_ZERO);
+        if (fused) {  // p' at the east / south neighbours recomputed from v: no p halo needed
+            launch_uzawa_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], pin, pout, t->rho, D.gx, D.gy, alpha_s, ms,
+                                nullptr, nullptr, nullptr, t->partials);
+            launch_finalize(c, t->partials, stream_blocks(F.g), 3, 1.0, t->scal + S_LOC);
+        } else {
+            double *pp = t->partials + 8192;
+            launch_pupdate(c, F.g, F.etap, F.vx[0], F.vy[0], pin, pout, alpha_s, ms, pp);
+            launch_finalize(c, pp, pupdate_blocks(F.g), 1, 1.0, t->scal + S_LOC + 2);
+        }
+    }
+    if (fused) return STOKES_OK;
+    if (pout_idx >= 0) {  // the energy stencil reads p' at the east / south halo
+        int st = exchange(D, 0, FX_P, pout_idx);
+        if (st) return st;
+    }
+    for (int k = 0; k < D.nt; ++k) {
+        stokes_s *t = D.tile[k];
+        Level &F = t->lev[0];
+        const LaunchCtx c = ctx(t);
+        launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], t->pbuf[pout_idx >= 0 ? pout_idx : pin_idx], t->rho,
+                      D.gx, D.gy, nullptr, nullptr, nullptr, t->partials, false);
+        launch_finalize(c, t->partials, energy_blocks(F.g), 2, 1.0, t->scal + S_LOC);
+    }
+    return STOKES_OK;
+}
+
+int dist_body(Dist &D) {  // one Uzawa iteration reading pbuf[pcur]
+    int st;
+    if ((st = dvcycle(D, 0, true, false))) return st;
+    const double a_s = D.o.pressure_sign * D.o.alpha_p;
+    if ((st = tiles_uzawa(D, D.pcur, 1 - D.pcur, a_s))) return st;
+    if ((st = combine(D, true))) return st;
+    if ((st = exchange(D, 0, FX_P, 1 - D.pcur))) return st;
+    CK(cudaMemcpyAsync(D.hsc, D.dscal, 8 * sizeof(double), cudaMemcpyDeviceToHost, D.stream));
+    return STOKES_OK;
+}
+
+int dsync(Dist &D) {
+    CK(cudaStreamSynchronize(D.stream));
+    CKL();
+    return STOKES_OK;
+}
+
+int state_E(Dist &D, double *E) {  // E of (v, pbuf[pcur]); mean of p -> mshift
+    int st = tiles_uzawa(D, D.pcur, -1, 0.0);
+    if (st) return st;
+    st = combine(D, true);
+    if (st) return st;
+    CK(cudaMemcpyAsync(D.hsc, D.dscal, 8 * sizeof(double), cudaMemcpyDeviceToHost, D.stream));
+    if ((st = dsync(D))) return st;
+    *E = D.hsc[0];
+    return STOKES_OK;
+}
+
+int force_E(Dist &D) {  // Sf -> dscal[3]
+    for (int k = 0; k < D.nt; ++k) {
+        stokes_s *t = D.tile[k];
+        Level &F = t->lev[0];
+        const LaunchCtx c = ctx(t);
+        launch_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], t->pbuf[0], t->rho, D.gx, D.gy, nullptr, nullptr,
+                      nullptr, t->partials, true);
+        launch_finalize(c, t->partials, energy_blocks(F.g), 2, 1.0, t->scal + S_LOC);
+        CK(cudaMemsetAsync(t->scal + S_LOC + 2, 0, 8, D.stream));
+    }
+    CK(cudaMemsetAsync(D.dscal + 3, 0, 8, D.stream));  // Sf slot = 0 while combining
+    int st = combine(D, false);
+    if (st) return st;
+    CK(cudaMemcpyAsync(D.dscal + 3, D.dscal + 1, 8, cudaMemcpyDeviceToDevice, D.stream));
+    return dsync(D);
+}
+
+void drop(Dist &D) {
+    for (int k = 0; k < 2; ++k)
+        if (D.exec[k]) {
+            cudaGraphExecDestroy(D.exec[k]);
+            D.exec[k] = nullptr;
+        }
+}
+
+// a tile handle: levels 0..La (La = agglomeration staging) with per-side flags
+int make_tile(Dist &D, int tx, int ty, stokes_s **out) {
+    stokes_s *h = (stokes_s *)calloc(1, sizeof(stokes_s));
+    if (!h) return STOKES_ENOMEM;
+    h->o = D.o;
+    h->o.coarse_direct = 0;
+    h->o.accel = STOKES_ACCEL_NONE;
+    h->nx = D.nxt;
+    h->ny = D.nyt;
+    h->Lx = D.Lx * D.nxt / D.NX;
+    h->Ly = D.Ly * D.nyt / D.NY;
+    memcpy(h->bc, D.bc, sizeof(h->bc));
+    h->stream = D.stream;
+    h->nlev = D.La + 1;
+    for (int l = 0; l <= D.La; ++l) {
+        GridL g = make_grid(D.nxt >> l, D.nyt >> l, h->Lx, h->Ly, D.bc);
+        g.bN = ty == 0;
+        g.bS = ty == D.py - 1;
+        g.bW = tx == 0;
+        g.bE = tx == D.px - 1;
+        g.nvxj = g.bE ? g.ncx - 1 : g.ncx;
+        g.nvyi = g.bS ? g.ncy - 1 : g.ncy;
+        g.par = (((ty * D.nyt) >> l) + ((tx * D.nxt) >> l)) & 1;
+        h->lev[l].g = g;
+        h->lev[l].nu = (int)floor(D.o.nu1 * pow(D.o.nu_growth, (double)l) + 0.5);
+    }
+    Carver dry{nullptr, 0, 0, true};
+    const size_t need = carve(h, dry);
+    cudaError_t e = cudaMalloc(&h->ws, need);
+    if (e != cudaSuccess) { free(h); fail_cuda(e, "cudaMalloc tile"); return STOKES_ENOMEM; }
+    h->own_ws = true;
+    h->ws_bytes = need;
+    Carver cv{(char *)h->ws, 0, need, false};
+    carve(h, cv);
+    e = cudaMallocHost(&h->hscal, S_NSCAL * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->ws, 0, need, D.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(D.stream);
+    if (e != cudaSuccess) { cudaFree(h->ws); free(h); return fail_cuda(e, "tile init"); }
+    *out = h;
+    return STOKES_OK;
+}
+void free_handle(stokes_s *h) {
+    if (!h) return;
+    drop_graphs(h);
+    if (h->hscal) cudaFreeHost(h->hscal);
+    if (h->own_ws && h->ws) cudaFree(h->ws);
+    free(h);
+}
+
+// tile window of a global user-layout array (virtual mode) <-> contiguous tile array
+// kind: 0 vx ny x (nx+1), 1 vy (ny+1) x nx, 2 P ny x nx, 3 basic (ny+1) x (nx+1)
+void tile_window(Dist &D, int k, int kind, int &off, int &rows, int &cols, int &gpitch) {
+    const int i0 = D.ty[k] * D.nyt, j0 = D.tx[k] * D.nxt;
+    switch (kind) {
+    case 0: rows = D.nyt; cols = D.nxt + 1; gpitch = D.NX + 1; break;
+    case 1: rows = D.nyt + 1; cols = D.nxt; gpitch = D.NX; break;
+    case 2: rows = D.nyt; cols = D.nxt; gpitch = D.NX; break;
+    default: rows = D.nyt + 1; cols = D.nxt + 1; gpitch = D.NX + 1; break;
+    }
+    off = i0 * gpitch + j0;
+}
+// copy the tile-k window of a user array into tmp (virtual) or pass the rank's array through
+const double *window_in(Dist &D, int k, int kind, const double *u, double *tmp) {
+    if (D.rank >= 0) return u;
+    int off, rows, cols, gp;
+    tile_window(D, k, kind, off, rows, cols, gp);
+    cudaMemcpy2DAsync(tmp, (size_t)cols * 8, u + off, (size_t)gp * 8, (size_t)cols * 8, rows, cudaMemcpyDeviceToDevice,
+                      D.stream);
+    return tmp;
+}
+void window_out(Dist &D, int k, int kind, const double *tmp, double *u) {
+    int off, rows, cols, gp;
+    tile_window(D, k, kind, off, rows, cols, gp);
+    cudaMemcpy2DAsync(u + off, (size_t)gp * 8, tmp, (size_t)cols * 8, (size_t)cols * 8, rows, cudaMemcpyDeviceToDevice,
+                      D.stream);
+}
+// scratch for windows: a tile's level-0 GCR-free buffers large enough for a user array
+double *tmp_of(stokes_s *t, int which) { return which == 0 ? t->lev[0].bx - COL_OFF : t->lev[0].by - COL_OFF; }
+
+}  // namespace
+
+// ====================================================================== dist entry points
+int dist_num_levels(Dist *D) { return D->L; }
+long long dist_launches(Dist *D, int reset) {
+    long long n = D->launches + D->tail->launches;
+    for (int k = 0; k < D->nt; ++k) n += D->tile[k]->launches;
+    if (reset) {
+        D->launches = 0;
+        D->tail->launches = 0;
+        for (int k = 0; k < D->nt; ++k) D->tile[k]->launches = 0;
+    }
+    return n;
+}
+
+int dist_destroy(Dist *D) {
+    drop(*D);
+    for (int k = 0; k < D->nt; ++k) free_handle(D->tile[k]);
+    free_handle(D->tail);
+    if (D->rank >= 0) ncclCommDestroy(D->comm);
+    if (D->sbuf) cudaFree(D->sbuf);
+    if (D->rbuf) cudaFree(D->rbuf);
+    if (D->dscal) cudaFree(D->dscal);
+    if (D->hsc) cudaFreeHost(D->hsc);
+    if (D->own_stream) cudaStreamDestroy(D->stream);
+    free(D);
+    return STOKES_OK;
+}
+
+int dist_set_viscosity(Dist *D, const double *eta_b, const double *eta_p) {
+    for (int k = 0; k < D->nt; ++k) {
+        stokes_s *t = D->tile[k];
+        Level &F = t->lev[0];
+        const LaunchCtx c = ctx(t);
+        launch_in_b(c, F.g, window_in(*D, k, 3, eta_b, tmp_of(t, 0)), F.etab);
+        launch_in_p(c, F.g, window_in(*D, k, 2, eta_p, tmp_of(t, 1)), F.etap);
+    }
+    int st;
+    if ((st = exchange(*D, 0, FX_ETA, 0))) return st;
+    for (int l = 0; l < D->La; ++l) {  // a7 on the tiles, halos refreshed per level
+        for (int k = 0; k < D->nt; ++k) {
+            stokes_s *t = D->tile[k];
+            launch_restrict_b(ctx(t), t->lev[l].g, t->lev[l + 1].g, t->lev[l].etab, t->lev[l + 1].etab);
+            launch_restrict_p(ctx(t), t->lev[l].g, t->lev[l + 1].g, t->lev[l].etap, t->lev[l + 1].etap);
+        }
+        if ((st = exchange(*D, l + 1, FX_ETA, 0))) return st;
+    }
+    if ((st = gather_to_tail(*D, 1))) return st;
+    if ((st = build_hierarchy(D->tail))) return st;  // tail: coarse eta + coarsest inverse
+    if ((st = dsync(*D))) return st;
+    D->have_eta = true;
+    drop(*D);
+    if (D->have_rho) return force_E(*D);
+    return STOKES_OK;
+}
+
+int dist_set_density(Dist *D, const double *rho_b) {
+    for (int k = 0; k < D->nt; ++k) {
+        stokes_s *t = D->tile[k];
+        launch_in_b(ctx(t), t->lev[0].g, window_in(*D, k, 3, rho_b, tmp_of(t, 0)), t->rho);
+    }
+    int st;
+    if ((st = exchange(*D, 0, FX_RHO, 0))) return st;
+    D->have_rho = true;
+    drop(*D);
+    if (D->have_eta) return force_E(*D);
+    return dsync(*D);
+}
+
+int dist_set_gravity(Dist *D, double gx, double gy) {
+    D->gx = gx;
+    D->gy = gy;
+    for (int k = 0; k < D->nt; ++k) {
+        D->tile[k]->gx = gx;
+        D->tile[k]->gy = gy;
+    }
+    drop(*D);
+    if (D->have_eta && D->have_rho) return force_E(*D);
+    return STOKES_OK;
+}
+
+static int load_state(Dist *D, const double *vx, const double *vy, const double *p) {
+    for (int k = 0; k < D->nt; ++k) {
+        stokes_s *t = D->tile[k];
+        Level &F = t->lev[0];
+        const LaunchCtx c = ctx(t);
+        launch_in_velocity(c, F.g, window_in(*D, k, 0, vx, tmp_of(t, 0)), window_in(*D, k, 1, vy, tmp_of(t, 1)),
+                           F.vx[0], F.vy[0]);
+        launch_in_p(c, F.g, window_in(*D, k, 2, p, F.rx - COL_OFF), t->pbuf[0]);
+        CK(cudaMemsetAsync(t->scal + S_MSHIFT, 0, 8, D->stream));
+    }
+    D->pcur = 0;
+    for (int k = 0; k < D->nt; ++k) D->tile[k]->pcur = 0;
+    int st;
+    if ((st = exchange(*D, 0, FX_V, 0))) return st;
+    return exchange(*D, 0, FX_P, 0);
+}
+
+int dist_residual_energy(Dist *D, const double *vx, const double *vy, const double *p, double *E) {
+    if (!D->have_eta || !D->have_rho) return STOKES_ESTATE;
+    int st = load_state(D, vx, vy, p);
+    if (st) return st;
+    return state_E(*D, E);
+}
+
+int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *iters, double *Eout) {
+    if (!D->have_eta || !D->have_rho) return STOKES_ESTATE;
+    int st = load_state(D, vx, vy, p);
+    if (st) return st;
+    CK(cudaMemcpyAsync(D->hsc + 8, D->dscal + 3, 8, cudaMemcpyDeviceToHost, D->stream));
+    if ((st = dsync(*D))) return st;
+    int status = STOKES_OK;
+    double E0 = 0.0, E = 0.0;
+    int k = 0;
+    if (!(D->hsc[8] > 0)) {  // f == 0
+        *iters = 0;
+        *Eout = 0.0;
+        for (int q = 0; q < D->nt; ++q) {
+            stokes_s *t = D->tile[q];
+            CK(cudaMemsetAsync(t->lev[0].vx[0] - COL_OFF, 0, field_doubles(t->lev[0].g) * 8, D->stream));
+            CK(cudaMemsetAsync(t->lev[0].vy[0] - COL_OFF, 0, field_doubles(t->lev[0].g) * 8, D->stream));
+            CK(cudaMemsetAsync(t->pbuf[0] - COL_OFF, 0, field_doubles(t->lev[0].g) * 8, D->stream));
+            CK(cudaMemsetAsync(t->scal + S_MSHIFT, 0, 8, D->stream));
+        }
+    } else {
+        if ((st = state_E(*D, &E0))) return st;
+        E = E0;
+        if (E0 > rtol) {
+            status = STOKES_NOT_CONVERGED;
+            const int keep = D->pcur;
+            for (int q = 0; q < 2; ++q) {  // capture one iteration per pressure parity
+                if (D->exec[q]) continue;
+                D->pcur = q;
+                for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = q;
+                cudaGraph_t graph;
+                const long long before = dist_launches(D, 0);
+                CK(cudaStreamBeginCapture(D->stream, cudaStreamCaptureModeThreadLocal));
+                int bst = dist_body(*D);
+                cudaError_t e = cudaStreamEndCapture(D->stream, &graph);
+                D->pcur = keep;
+                for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = keep;
+                if (bst) return bst;
+                if (e != cudaSuccess) return fail_cuda(e, "dist graph capture");
+                D->body_kernels = dist_launches(D, 0) - before;
+                D->launches -= D->body_kernels;  // captured, not executed
+                e = cudaGraphInstantiate(&D->exec[q], graph, 0);
+                cudaGraphDestroy(graph);
+                if (e != cudaSuccess) { D->exec[q] = nullptr; return fail_cuda(e, "dist graph instantiate"); }
+            }
+            for (k = 1; k <= D->o.max_iter; ++k) {
+                CK(cudaGraphLaunch(D->exec[D->pcur], D->stream));
+                D->pcur ^= 1;
+                for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = D->pcur;
+                D->launches += D->body_kernels;
+                if ((st = dsync(*D))) return st;
+                E = D->hsc[0];
+                if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+                if (E <= rtol) { status = STOKES_OK; break; }
+            }
+            if (k > D->o.max_iter) k = D->o.max_iter;
+        }
+        *iters = k;
+        *Eout = E;
+    }
+    for (int q = 0; q < D->nt; ++q) {  // outputs (zero-mean p through each tile's mshift)
+        stokes_s *t = D->tile[q];
+        Level &F = t->lev[0];
+        const LaunchCtx c = ctx(t);
+        if (D->rank >= 0) {
+            launch_out_vx(c, F.g, F.vx[0], vx);
+            launch_out_vy(c, F.g, F.vy[0], vy);
+            launch_out_p(c, F.g, t->pbuf[D->pcur], p, t->scal + S_MSHIFT);
+        } else {
+            launch_out_vx(c, F.g, F.vx[0], tmp_of(t, 0));
+            window_out(*D, q, 0, tmp_of(t, 0), vx);
+            launch_out_vy(c, F.g, F.vy[0], tmp_of(t, 1));
+            window_out(*D, q, 1, tmp_of(t, 1), vy);
+            launch_out_p(c, F.g, t->pbuf[D->pcur], F.rx - COL_OFF, t->scal + S_MSHIFT);
+            window_out(*D, q, 2, F.rx - COL_OFF, p);
+        }
+    }
+    if ((st = dsync(*D))) return st;
+    return status;
+}
+
+extern "C" {
+
+int stokes_nccl_unique_id(void *id128) {
+    if (!id128) return STOKES_EINVAL;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return STOKES_ENCCL;
+    memcpy(id128, &id, sizeof(id) < 128 ? sizeof(id) : 128);
+    return STOKES_OK;
+}
+
+int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], int px, int py, int rank,
+                       const void *nccl_unique_id, const stokes_opts *opts, void *cuda_stream, stokes_t *out) {
+    if (!out || px < 1 || py < 1 || px * py > MAXT || nx % px || ny % py || !bc) return STOKES_EINVAL;
+    if (rank >= px * py || (rank >= 0 && !nccl_unique_id)) return STOKES_EINVAL;
+    Dist *D = (Dist *)calloc(1, sizeof(Dist));
+    if (!D) return STOKES_ENOMEM;
+    D->NX = nx;
+    D->NY = ny;
+    D->px = px;
+    D->py = py;
+    D->nxt = nx / px;
+    D->nyt = ny / py;
+    D->Lx = Lx;
+    D->Ly = Ly;
+    memcpy(D->bc, bc, sizeof(D->bc));
+    if (opts) D->o = *opts;
+    else stokes_opts_default(&D->o);
+    if (check_opts(D->o) || D->o.accel != STOKES_ACCEL_NONE || !(Lx > 0) || !(Ly > 0)) { free(D); return STOKES_EINVAL; }
+    for (int k = 0; k < 4; ++k)
+        if (bc[k] != 0 && bc[k] != 1) { free(D); return STOKES_EINVAL; }
+    D->rank = rank;
+    // global hierarchy and the agglomeration level (tile levels while the tile is >= dmin)
+    GridL gs[MAXLEV];
+    int nus[MAXLEV];
+    D->L = build_levels(nx, ny, Lx, Ly, bc, D->o, gs, nus);
+    int dmin = 64;
+    if (const char *e = getenv("STOKES_DIST_DMIN")) dmin = atoi(e) > 2 ? atoi(e) : 2;
+    int La = 0;
+    while (La + 1 <= D->L - 1) {
+        const int cx = D->nxt >> La, cy = D->nyt >> La;
+        if ((cx % 2) || (cy % 2) || (cx < dmin) || (cy < dmin)) break;
+        ++La;
+    }
+    if (La < 1) { free(D); return STOKES_EINVAL; }  // tiles too small / not coarsenable
+    D->La = La;
+    D->stream = (cudaStream_t)cuda_stream;
+    if (!D->stream) {
+        if (cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking) != cudaSuccess) { free(D); return STOKES_ECUDA; }
+        D->own_stream = true;
+    }
+    int st;
+    if (rank < 0) {
+        D->nt = px * py;
+        for (int k = 0; k < D->nt; ++k) {
+            D->tx[k] = k % px;
+            D->ty[k] = k / px;
+        }
+    } else {
+        D->nt = 1;
+        D->tx[0] = rank % px;
+        D->ty[0] = rank / px;
+        ncclUniqueId id;
+        memcpy(&id, nccl_unique_id, sizeof(id));
+        if (ncclCommInitRank(&D->comm, px * py, id, rank) != ncclSuccess) { free(D); return STOKES_ENCCL; }
+    }
+    for (int k = 0; k < D->nt; ++k)
+        if ((st = make_tile(*D, D->tx[k], D->ty[k], &D->tile[k]))) { dist_destroy(D); return st; }
+    // the coarse tail: global level La
+    stokes_opts ot = D->o;
+    stokes_t tail = nullptr;
+    st = stokes_create(nx >> La, ny >> La, Lx, Ly, bc, &ot, D->stream, nullptr, 0, &tail);
+    if (st) { dist_destroy(D); return st; }
+    D->tail = tail;
+    for (int l = 0; l < tail->nlev; ++l) tail->lev[l].nu = (int)floor(D->o.nu1 * pow(D->o.nu_growth, (double)(La + l)) + 0.5);
+    if (D->tail->nlev + La != D->L) { dist_destroy(D); return STOKES_EINVAL; }
+    const GridL &gf = D->tile[0]->lev[0].g, &gc = D->tile[0]->lev[La].g;
+    D->nbuf = 4 * (size_t)(gf.ncy + 2) + 4 * (size_t)(gc.ncy + 1) * (gc.ncx + 1) * (size_t)(px * py) + 64;
+    if (cudaMalloc(&D->sbuf, D->nbuf * 8) != cudaSuccess || cudaMalloc(&D->rbuf, D->nbuf * 8) != cudaSuccess ||
+        cudaMalloc(&D->dscal, 64 * 8) != cudaSuccess || cudaMallocHost(&D->hsc, 64 * 8) != cudaSuccess) {
+        dist_destroy(D);
+        return STOKES_ENOMEM;
+    }
+    cudaMemsetAsync(D->dscal, 0, 64 * 8, D->stream);
+    if ((st = dsync(*D))) { dist_destroy(D); return st; }
+    stokes_s *h = (stokes_s *)calloc(1, sizeof(stokes_s));
+    h->dist = D;
+    h->nx = nx;
+    h->ny = ny;
+    h->stream = D->stream;
+    *out = h;
+    return STOKES_OK;
+}
+
+}  // extern "C"

@@ -9,64 +9,13 @@
 
 #include <string>
 
-#include "internal.h"
+#include <nccl.h>
 
-#define MAXLEV 24
-#define MAXM 32
-#define MAX_DIRECT 1024  // largest coarsest system solved by the explicit inverse (a8)
+#include "handle.h"
 
-namespace {
+namespace sk {
 
 thread_local std::string g_last_error;
-
-// device scalar slots
-enum { S_MSHIFT = 0, S_E = 1, S_SV = 2, S_SP = 3, S_SF = 4, S_SFPART = 5, S_ZMEAN = 8, S_GAMMA = 9, S_NU2 = 10,
-       S_RR = 11, S_BETA = 12, S_ZERO = 13, S_E0 = 14, S_NSCAL = 64 };
-
-struct Level {
-    GridL g;
-    double *etab, *etap;
-    double *vx[2], *vy[2];  // level 0: solution ping-pong; coarse: correction ping-pong
-    double *bx, *by;        // right-hand side
-    double *rx, *ry;        // residual scratch
-    int nu;
-};
-
-}  // namespace
-
-struct stokes_s {
-    int nx, ny;
-    double Lx, Ly;
-    int bc[4];
-    stokes_opts o;
-    cudaStream_t stream;
-    bool own_stream;
-    void *ws;
-    size_t ws_bytes;
-    bool own_ws;
-    int nlev;
-    Level lev[MAXLEV];
-    double *pbuf[2], *rho;  // pressure ping-pong (the fused Uzawa pass reads one, writes the other)
-    int pcur;
-    double *partials;
-    size_t npart;
-    double *scal;       // device scalars
-    double *hscal;      // pinned host mirror
-    double *Minv, *Mwork;
-    int nc;
-    int *dflag;
-    // GCR vectors (fine level, padded): z_i, w_i, r, V-cycle scratch
-    double *gz[MAXM][3], *gw[MAXM][3], *gr[3], *gtmp[2], *gew[3];
-    cudaGraphExec_t gcr_exec[MAXM];  // GCR step i (i MGS steps) captured
-    long long gcr_kernels[MAXM];
-    bool have_eta, have_rho;
-    double gx, gy;
-    long long launches;
-    cudaGraphExec_t uzawa_exec[2];  // iteration reading pbuf[k]
-    long long uzawa_kernels;
-};
-
-namespace {
 
 int fail_cuda(cudaError_t e, const char *what) {
     char buf[256];
@@ -74,16 +23,6 @@ int fail_cuda(cudaError_t e, const char *what) {
     g_last_error = buf;
     return STOKES_ECUDA;
 }
-#define CK(call)                                              \
-    do {                                                      \
-        cudaError_t e_ = (call);                              \
-        if (e_ != cudaSuccess) return fail_cuda(e_, #call);   \
-    } while (0)
-#define CKL()                                                           \
-    do {                                                                \
-        cudaError_t e_ = cudaGetLastError();                            \
-        if (e_ != cudaSuccess) return fail_cuda(e_, "kernel launch");   \
-    } while (0)
 
 size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -129,22 +68,6 @@ int build_levels(int nx, int ny, double Lx, double Ly, const int bc[4], const st
     }
     return l;
 }
-
-struct Carver {  // bump allocator over the workspace (256-B granules)
-    char *base;
-    size_t off, cap;
-    bool dry;
-    double *take(size_t ndoubles) {
-        off = round_up(off, 256);
-        double *p = dry ? nullptr : (double *)(base + off);
-        off += ndoubles * sizeof(double);
-        return p;
-    }
-    double *field(const GridL &g) {
-        double *a = take(field_doubles(g));
-        return dry ? nullptr : a + COL_OFF;
-    }
-};
 
 int check_opts(const stokes_opts &o) {
     if (o.smoother != 0 && o.smoother != 1) return STOKES_EINVAL;
@@ -565,11 +488,13 @@ int solve_gcr(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
     return status;
 }
 
-bool valid_level(stokes_s *h, int l) { return h && l >= 0 && l < h->nlev; }
+bool valid_level(stokes_s *h, int l) { return h && !h->dist && l >= 0 && l < h->nlev; }
+int build_hierarchy(stokes_s *h);
 
-}  // namespace
+}  // namespace sk
 
 // ===================================================================== C ABI
+using namespace sk;
 extern "C" {
 
 int stokes_opts_default(stokes_opts *o) {
@@ -668,6 +593,11 @@ int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const s
 
 int stokes_destroy(stokes_t h) {
     if (!h) return STOKES_EINVAL;
+    if (h->dist) {
+        dist_destroy(h->dist);
+        free(h);
+        return STOKES_OK;
+    }
     drop_graphs(h);
     if (h->hscal) cudaFreeHost(h->hscal);
     if (h->own_ws && h->ws) cudaFree(h->ws);
@@ -678,6 +608,10 @@ int stokes_destroy(stokes_t h) {
 
 int stokes_num_levels(stokes_t h, int *nlev) {
     if (!h || !nlev) return STOKES_EINVAL;
+    if (h->dist) {
+        *nlev = dist_num_levels(h->dist);
+        return STOKES_OK;
+    }
     *nlev = h->nlev;
     return STOKES_OK;
 }
@@ -691,6 +625,7 @@ int stokes_level_shape(stokes_t h, int level, int *nx, int *ny, int *nu) {
 
 int stokes_set_viscosity(stokes_t h, const double *eta_b, const double *eta_p) {
     if (!h || !eta_b || !eta_p) return STOKES_EINVAL;
+    if (h->dist) return dist_set_viscosity(h->dist, eta_b, eta_p);
     const LaunchCtx c = ctx(h);
     CK(cudaMemsetAsync(h->dflag, 0, sizeof(int), h->stream));
     launch_count_nonpos(c, eta_b, (size_t)(h->ny + 1) * (h->nx + 1), h->dflag);
@@ -704,6 +639,16 @@ int stokes_set_viscosity(stokes_t h, const double *eta_b, const double *eta_p) {
     Level &F = h->lev[0];
     launch_in_b(c, F.g, eta_b, F.etab);
     launch_in_p(c, F.g, eta_p, F.etap);
+    return build_hierarchy(h);
+}
+
+}  // extern "C"
+namespace sk {
+// coarse viscosities (a7) and the coarsest inverse (a8) from the level-0 viscosities
+int build_hierarchy(stokes_s *h) {
+    const LaunchCtx c = ctx(h);
+    Level &F = h->lev[0];
+    int bad = 0, st;
     for (int l = 0; l + 1 < h->nlev; ++l) {  // a7: coarse viscosities by restriction
         launch_restrict_b(c, h->lev[l].g, h->lev[l + 1].g, h->lev[l].etab, h->lev[l + 1].etab);
         launch_restrict_p(c, h->lev[l].g, h->lev[l + 1].g, h->lev[l].etap, h->lev[l + 1].etap);
@@ -725,9 +670,12 @@ int stokes_set_viscosity(stokes_t h, const double *eta_b, const double *eta_p) {
     if (h->have_rho) force_energy(h);
     return sync(h);
 }
+}  // namespace sk
+extern "C" {
 
 int stokes_set_density(stokes_t h, const double *rho_b) {
     if (!h || !rho_b) return STOKES_EINVAL;
+    if (h->dist) return dist_set_density(h->dist, rho_b);
     launch_in_b(ctx(h), h->lev[0].g, rho_b, h->rho);
     h->have_rho = true;
     if (h->have_eta) force_energy(h);
@@ -736,6 +684,7 @@ int stokes_set_density(stokes_t h, const double *rho_b) {
 
 int stokes_set_gravity(stokes_t h, double gx, double gy) {
     if (!h || !(gx == gx) || !(gy == gy)) return STOKES_EINVAL;
+    if (h->dist) return dist_set_gravity(h->dist, gx, gy);
     h->gx = gx;
     h->gy = gy;
     drop_graphs(h);  // gravity is baked into the captured graphs
@@ -745,7 +694,7 @@ int stokes_set_gravity(stokes_t h, double gx, double gy) {
 
 int stokes_apply_operator(stokes_t h, const double *vx, const double *vy, const double *p, double *ax, double *ay,
                           double *ap) {
-    if (!h || !vx || !vy || !p || !ax || !ay || !ap) return STOKES_EINVAL;
+    if (!h || h->dist || !vx || !vy || !p || !ax || !ay || !ap) return STOKES_EINVAL;
     if (!h->have_eta) return STOKES_ESTATE;
     Level &F = h->lev[0];
     const LaunchCtx c = ctx(h);
@@ -758,6 +707,10 @@ int stokes_apply_operator(stokes_t h, const double *vx, const double *vy, const 
 int stokes_residual(stokes_t h, const double *vx, const double *vy, const double *p, double *rx, double *ry,
                     double *rp, double *rel_energy) {
     if (!h || !vx || !vy || !p) return STOKES_EINVAL;
+    if (h->dist) {  // decomposed handles: E only
+        if (rx || ry || rp || !rel_energy) return STOKES_EINVAL;
+        return dist_residual_energy(h->dist, vx, vy, p, rel_energy);
+    }
     if (!h->have_eta || !h->have_rho) return STOKES_ESTATE;
     Level &F = h->lev[0];
     const LaunchCtx c = ctx(h);
@@ -776,7 +729,7 @@ int stokes_residual(stokes_t h, const double *vx, const double *vy, const double
 }
 
 int stokes_vcycle(stokes_t h, const double *bx, const double *by, double *vx, double *vy) {
-    if (!h || !bx || !by || !vx || !vy) return STOKES_EINVAL;
+    if (!h || h->dist || !bx || !by || !vx || !vy) return STOKES_EINVAL;
     if (!h->have_eta) return STOKES_ESTATE;
     Level &F = h->lev[0];
     const LaunchCtx c = ctx(h);
@@ -791,6 +744,7 @@ int stokes_vcycle(stokes_t h, const double *bx, const double *by, double *vx, do
 
 int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy) {
     if (!h || !vx || !vy || !p || !iters || !rel_energy || !(rtol >= 0)) return STOKES_EINVAL;
+    if (h->dist) return dist_solve(h->dist, rtol, vx, vy, p, iters, rel_energy);
     if (!h->have_eta || !h->have_rho) return STOKES_ESTATE;
     Level &F = h->lev[0];
     const LaunchCtx c = ctx(h);
@@ -917,7 +871,7 @@ int stokes_get_viscosity(stokes_t h, int level, double *eta_b, double *eta_p) {
 }
 
 int stokes_coarse_solve(stokes_t h, const double *bx, const double *by, double *vx, double *vy) {
-    if (!h || !bx || !by || !vx || !vy) return STOKES_EINVAL;
+    if (!h || h->dist || !bx || !by || !vx || !vy) return STOKES_EINVAL;
     if (!h->have_eta) return STOKES_ESTATE;
     if (h->nc == 0) return STOKES_EINVAL;
     Level &C = h->lev[h->nlev - 1];
@@ -932,13 +886,17 @@ int stokes_coarse_solve(stokes_t h, const double *bx, const double *by, double *
 
 int stokes_launch_count(stokes_t h, long long *count, int reset) {
     if (!h || !count) return STOKES_EINVAL;
+    if (h->dist) {
+        *count = dist_launches(h->dist, reset);
+        return STOKES_OK;
+    }
     *count = h->launches;
     if (reset) h->launches = 0;
     return STOKES_OK;
 }
 
 int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double *bytes) {
-    if (!h || !avg_ms || !bytes || reps < 1) return STOKES_EINVAL;
+    if (!h || h->dist || !avg_ms || !bytes || reps < 1) return STOKES_EINVAL;
     if (!h->have_eta || !h->have_rho) return STOKES_ESTATE;
     Level &F = h->lev[0];
     const GridL &g = F.g;

@@ -1,0 +1,121 @@
+// Handle structure and host-runtime helpers shared by driver.cu (single domain) and
+// dist.cu (2D domain decomposition).  Internal; not part of the ABI.
+#pragma once
+#include <string>
+
+#include "internal.h"
+
+#define MAXLEV 24
+#define MAXM 32
+#define MAX_DIRECT 1024  // largest coarsest system solved by the explicit inverse (a8)
+
+namespace sk {
+
+extern thread_local std::string g_last_error;
+
+// device scalar slots
+enum { S_MSHIFT = 0, S_E = 1, S_SV = 2, S_SP = 3, S_SF = 4, S_SFPART = 5, S_ZMEAN = 8, S_GAMMA = 9, S_NU2 = 10, S_LOC = 16,
+       S_RR = 11, S_BETA = 12, S_ZERO = 13, S_E0 = 14, S_NSCAL = 64 };
+
+struct Level {
+    GridL g;
+    double *etab, *etap;
+    double *vx[2], *vy[2];  // level 0: solution ping-pong; coarse: correction ping-pong
+    double *bx, *by;        // right-hand side
+    double *rx, *ry;        // residual scratch
+    int nu;
+};
+
+}  // namespace sk
+
+struct stokes_s {
+    int nx, ny;
+    double Lx, Ly;
+    int bc[4];
+    stokes_opts o;
+    cudaStream_t stream;
+    bool own_stream;
+    void *ws;
+    size_t ws_bytes;
+    bool own_ws;
+    int nlev;
+    sk::Level lev[MAXLEV];
+    double *pbuf[2], *rho;  // pressure ping-pong (the fused Uzawa pass reads one, writes the other)
+    int pcur;
+    double *partials;
+    size_t npart;
+    double *scal;       // device scalars
+    double *hscal;      // pinned host mirror
+    double *Minv, *Mwork;
+    int nc;
+    int *dflag;
+    // GCR vectors (fine level, padded): z_i, w_i, r, V-cycle scratch
+    double *gz[MAXM][3], *gw[MAXM][3], *gr[3], *gtmp[2], *gew[3];
+    cudaGraphExec_t gcr_exec[MAXM];  // GCR step i (i MGS steps) captured
+    long long gcr_kernels[MAXM];
+    bool have_eta, have_rho;
+    double gx, gy;
+    long long launches;
+    cudaGraphExec_t uzawa_exec[2];  // iteration reading pbuf[k]
+    long long uzawa_kernels;
+    struct Dist *dist;  // non-null: a 2D-decomposed handle (all calls dispatch to dist_*)
+};
+
+
+namespace sk {
+using ::stokes_s;
+int fail_cuda(cudaError_t e, const char *what);
+size_t round_up(size_t v, size_t a);
+GridL make_grid(int ncx, int ncy, double Lx, double Ly, const int bc[4]);
+size_t field_doubles(const GridL &g);
+int n_unknowns(const GridL &g);
+int build_levels(int nx, int ny, double Lx, double Ly, const int bc[4], const stokes_opts &o, GridL *gs, int *nus);
+struct Carver {  // bump allocator over the workspace (256-B granules)
+    char *base;
+    size_t off, cap;
+    bool dry;
+    double *take(size_t ndoubles) {
+        off = round_up(off, 256);
+        double *p = dry ? nullptr : (double *)(base + off);
+        off += ndoubles * sizeof(double);
+        return p;
+    }
+    double *field(const GridL &g) {
+        double *a = take(field_doubles(g));
+        return dry ? nullptr : a + COL_OFF;
+    }
+};
+int check_opts(const stokes_opts &o);
+size_t carve(stokes_s *h, Carver &cv);
+LaunchCtx ctx(stokes_s *h);
+RhsArgs rhs_arrays(const double *bx, const double *by);
+RhsArgs rhs_fine(stokes_s *h);
+void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&oy, const RhsArgs &rhs, int n,
+            bool zero_in);
+void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in);
+int sync(stokes_s *h);
+int build_hierarchy(stokes_s *h);
+void drop_graphs(stokes_s *h);
+void force_energy(stokes_s *h);
+}  // namespace sk
+
+#define CK(call)                                                  \
+    do {                                                          \
+        cudaError_t e_ = (call);                                  \
+        if (e_ != cudaSuccess) return sk::fail_cuda(e_, #call);   \
+    } while (0)
+#define CKL()                                                               \
+    do {                                                                    \
+        cudaError_t e_ = cudaGetLastError();                                \
+        if (e_ != cudaSuccess) return sk::fail_cuda(e_, "kernel launch");   \
+    } while (0)
+
+// ---- 2D decomposition (dist.cu): dispatch targets of the ABI for decomposed handles
+int dist_destroy(struct Dist *D);
+int dist_set_viscosity(struct Dist *D, const double *eta_b, const double *eta_p);
+int dist_set_density(struct Dist *D, const double *rho_b);
+int dist_set_gravity(struct Dist *D, double gx, double gy);
+int dist_residual_energy(struct Dist *D, const double *vx, const double *vy, const double *p, double *E);
+int dist_solve(struct Dist *D, double rtol, double *vx, double *vy, double *p, int *iters, double *E);
+int dist_num_levels(struct Dist *D);
+long long dist_launches(struct Dist *D, int reset);

@@ -150,3 +150,17 @@ void launch_gcr_update(const LaunchCtx &c, const double *pin, int nbin, double *
                        double *const *x, double *const *r, const double *const *ew, size_t nfield, double *pout);
 void launch_gcr_final(const LaunchCtx &c, const double *pupd, int nbu, const double *pnorm, int nbn,
                       const double *Sf, double *E, double *nu2, double *rr);
+
+// ---------------------------------------------------------------- decomposition helpers
+struct StripList {  // host-side list of strided strip copies (any length)
+    double *dst[512];
+    const double *src[512];
+    int n[512], dstride[512], sstride[512];
+    int count;
+};
+void launch_strips(const LaunchCtx &c, const StripList &l);
+void launch_rbgs_phase(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *vx,
+                       double *vy, const RhsArgs &rhs, double omega, int comp, int colour);
+// out = (E, Sv, Sp) from the tiles' local (Sv, Sp, sum p); mean written to each mshift
+void launch_dist_final(const LaunchCtx &c, const double *const *loc, int nloc, const double *Sf, double inv_np,
+                       double *out, double *const *mshift, int nm);

@@ -783,6 +783,48 @@ __global__ void k_sub_mean(GridL g, const double *__restrict__ mean, double *__r
     if (i <= g.ncy && j <= g.ncx) p[at(g, i, j)] -= *mean;
 }
 
+
+// ------------------------------------------------------------------ 2D decomposition helpers (§8(e))
+// strided strip copies (halo columns / rows, packing for the transports): one CTA per strip
+constexpr int MAXSTRIP = 48;
+struct Strips {
+    double *dst[MAXSTRIP];
+    const double *src[MAXSTRIP];
+    int n[MAXSTRIP];
+    int dstride[MAXSTRIP], sstride[MAXSTRIP];
+    int count;
+};
+__global__ void k_strip_copy(Strips s) {
+    const int k = blockIdx.y;
+    if (k >= s.count) return;
+    double *d = s.dst[k];
+    const double *a = s.src[k];
+    const int ds = s.dstride[k], ss = s.sstride[k];
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < s.n[k]; e += gridDim.x * blockDim.x)
+        d[(size_t)e * ds] = a[(size_t)e * ss];
+}
+// sum of the tiles' local (Sv, Sp, sum p) triples in tile order (deterministic)
+struct Ptrs {
+    const double *p[64];
+    double *q[64];
+    int n;
+};
+__global__ void k_dist_final(Ptrs loc, const double *__restrict__ Sf, double inv_np, double *__restrict__ out,
+                             Ptrs mshift, int write_mean) {
+    if (threadIdx.x != 0) return;
+    double sv = 0.0, sp = 0.0, ps = 0.0;
+    for (int t = 0; t < loc.n; ++t) {
+        sv += loc.p[t][0];
+        sp += loc.p[t][1];
+        ps += loc.p[t][2];
+    }
+    out[0] = (Sf[0] > 0.0) ? sqrt((sv + sp) / Sf[0]) : 0.0;
+    out[1] = sv;
+    out[2] = sp;
+    if (write_mean)
+        for (int t = 0; t < mshift.n; ++t) *mshift.q[t] = ps * inv_np;
+}
+
 }  // namespace
 
 // ====================================================================== launchers
@@ -1003,5 +1045,41 @@ void launch_precond_p(const LaunchCtx &c, const GridL &g, const double *etap, co
 }
 void launch_sub_mean(const LaunchCtx &c, const GridL &g, const double *mean, double *p) {
     k_sub_mean<<<cell_grid(g), tpb(), 0, c.stream>>>(g, mean, p);
+    LAUNCH_BOOK(c);
+}
+
+void launch_rbgs_phase(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *vx,
+                       double *vy, const RhsArgs &rhs, double omega, int comp, int colour) {
+    const dim3 grid((g.ncx / 2 + 1 + BX - 1) / BX, (g.ncy + BY - 1) / BY);
+    k_rbgs_phase<<<grid, tpb(), 0, c.stream>>>(g, etab, etap, vx, vy, rhs, omega, comp, colour);
+    LAUNCH_BOOK(c);
+}
+void launch_strips(const LaunchCtx &c, const StripList &l) {
+    for (int base = 0; base < l.count; base += MAXSTRIP) {
+        Strips s;
+        s.count = 0;
+        int nmax = 1;
+        for (int k = base; k < l.count && s.count < MAXSTRIP; ++k, ++s.count) {
+            s.dst[s.count] = l.dst[k];
+            s.src[s.count] = l.src[k];
+            s.n[s.count] = l.n[k];
+            s.dstride[s.count] = l.dstride[k];
+            s.sstride[s.count] = l.sstride[k];
+            if (l.n[k] > nmax) nmax = l.n[k];
+        }
+        int bx = (nmax + 255) / 256;
+        if (bx > 16) bx = 16;
+        k_strip_copy<<<dim3(bx, s.count), 256, 0, c.stream>>>(s);
+        LAUNCH_BOOK(c);
+    }
+}
+void launch_dist_final(const LaunchCtx &c, const double *const *loc, int nloc, const double *Sf, double inv_np,
+                       double *out, double *const *mshift, int nm) {
+    Ptrs a, b;
+    a.n = nloc;
+    for (int t = 0; t < nloc; ++t) a.p[t] = loc[t];
+    b.n = nm;
+    for (int t = 0; t < nm; ++t) b.q[t] = mshift[t];
+    k_dist_final<<<1, 32, 0, c.stream>>>(a, Sf, inv_np, out, b, nm > 0);
     LAUNCH_BOOK(c);
 }

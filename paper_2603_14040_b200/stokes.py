@@ -90,6 +90,8 @@ def lib(build_if_missing=True):
         "stokes_time_kernel": [P, I, I, pd, pd],
         "stokes_strerror": [I],
         "stokes_last_error": [],
+        "stokes_create_dist": [I, I, D, D, pi, I, I, I, P, ctypes.POINTER(Opts), P, ctypes.POINTER(P)],
+        "stokes_nccl_unique_id": [P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -106,7 +108,7 @@ EXPORTED = ["stokes_opts_default", "stokes_workspace_bytes", "stokes_create", "s
             "stokes_set_gravity", "stokes_apply_operator", "stokes_residual", "stokes_vcycle", "stokes_solve",
             "stokes_smooth", "stokes_level_residual", "stokes_restrict", "stokes_prolong",
             "stokes_get_viscosity", "stokes_coarse_solve", "stokes_launch_count", "stokes_time_kernel",
-            "stokes_strerror", "stokes_last_error"]
+            "stokes_strerror", "stokes_last_error", "stokes_create_dist", "stokes_nccl_unique_id"]
 
 
 def default_opts(**kw):
@@ -344,3 +346,57 @@ class Stokes:
         _check(lib().stokes_time_kernel(self._h, self.KERNELS[kernel], reps, ctypes.byref(ms), ctypes.byref(nb)),
                "time_kernel")
         return ms.value, nb.value
+
+
+from .decomp import tile_windows  # noqa: E402,F401
+
+
+def nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().stokes_nccl_unique_id(buf), "nccl_unique_id")
+    return buf.raw
+
+
+class StokesDist(Stokes):
+    """2D-decomposed handle (stokes_create_dist).
+
+    rank=None: VIRTUAL decomposition -- all px*py tiles in this process on one GPU, arrays
+    are the GLOBAL user-layout arrays (exactness tests on one B200).
+    rank=r (with torch.distributed initialised): NCCL decomposition, one tile per process;
+    arrays are the tile windows (`tile_windows`).  The NCCL unique id is created on rank 0
+    and broadcast with torch.distributed (the process group is plumbing only)."""
+
+    def __init__(self, nx, ny, Lx=1.0, Ly=1.0, bc=(FREE_SLIP,) * 4, px=1, py=1, rank=None, device=None,
+                 stream=None, **opts):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2603_14040_b200 needs a CUDA GPU (B200, sm_100a); no CPU fallback")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.gnx, self.gny, self.px, self.py, self.rank = nx, ny, px, py, rank
+        self.nx, self.ny = (nx, ny) if rank is None else (nx // px, ny // py)
+        self.Lx, self.Ly, self.bc = Lx, Ly, tuple(bc)
+        self.opts = default_opts(**opts)
+        uid = None
+        if rank is not None:
+            import torch.distributed as dist
+            obj = [nccl_unique_id() if dist.get_rank() == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            uid = ctypes.create_string_buffer(obj[0], 128)
+        with torch.cuda.device(self.device):
+            self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
+            self._h = ctypes.c_void_p()
+            bcs = (ctypes.c_int * 4)(*self.bc)
+            _check(lib().stokes_create_dist(nx, ny, float(Lx), float(Ly), bcs, px, py, -1 if rank is None else rank,
+                                            uid, ctypes.byref(self.opts), ctypes.c_void_p(self.stream.cuda_stream),
+                                            ctypes.byref(self._h)), "create_dist")
+
+    def level_shape(self, level):
+        raise NotImplementedError("per-level queries are not available on decomposed handles")
+
+    def residual(self, vx, vy, p, want_arrays=False):
+        sh = shapes(self.nx, self.ny)
+        vx, vy, p = self._dev(vx, sh["vx"]), self._dev(vy, sh["vy"]), self._dev(p, sh["p"])
+        e = ctypes.c_double()
+        self._sync_inputs()
+        _check(lib().stokes_residual(self._h, self._p(vx), self._p(vy), self._p(p), None, None, None,
+                                     ctypes.byref(e)), "residual")
+        return None, None, None, e.value

@@ -25,7 +25,7 @@ constexpr int TW = 256;          // columns per CTA
 constexpr int RW = TW + 4;       // staged row width (doubles): [j0-2, j0+TW+2)
 constexpr int NS = 8;            // landing ring depth (rows): NS-1 rows in flight per CTA
 constexpr int NF = 6;            // staged fields
-constexpr int SMEM = NS * NF * RW * 8 + NS * 8;
+constexpr int SMEM = NS * NF * RW * 8 + 2 * NS * 8;
 constexpr int MINB = 2;          // CTAs per SM (shared memory: 2 x 97.5 KB)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -48,21 +48,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
         "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(phase)
         : "memory");
-}
-
-// deterministic block sum over the 256 threads (fixed xor tree, fixed warp order)
-__device__ __forceinline__ double block_sum256(double v, double *sh) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        v = (threadIdx.x < TW / 32) ? sh[threadIdx.x] : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    }
-    return v;
 }
 
 // Register window of the three rows i-1 (A), i (B), i+1 (C) of every field for this
@@ -142,6 +127,7 @@ __device__ __forceinline__ double fy_win(const Win &w, double gy) {
 
 template <int MODE>
 struct JacobiOp {
+    static constexpr bool WS = true;  // warp-specialised engine
     static constexpr int NF = 6;
     static constexpr int NRED = 0;
     const double *src[NF];
@@ -170,6 +156,7 @@ struct JacobiOp {
 
 template <int MODE>
 struct ResidualOp {
+    static constexpr bool WS = true;  // warp-specialised engine
     static constexpr int NF = 6;
     static constexpr int NRED = 0;
     const double *src[NF];
@@ -194,6 +181,7 @@ struct ResidualOp {
 // p' at the east / south neighbours is recomputed from v on the window, so one pass reads
 // (vx, vy, eta_p, eta_b, p, rho) and writes p'.  Partial sums per CTA: (Sv, Sp, sum p').
 struct UzawaOp {
+    static constexpr bool WS = false;  // warp-specialised engine
     static constexpr int NF = 6;
     static constexpr int NRED = 3;
     const double *src[NF];
@@ -241,6 +229,7 @@ struct UzawaOp {
 // z_p at the east / south neighbours is recomputed on the window.  Partial dots for the
 // first Gram-Schmidt coefficient: <w, w0> (first == 0) or <w, w>, <r, w> (first step).
 struct PrecondApplyOp {
+    static constexpr bool WS = false;  // warp-specialised engine
     static constexpr int NF = 5;
     static constexpr int NRED = 2;
     const double *src[6];        // zx, zy, eta_p, eta_b, r_p
@@ -277,8 +266,88 @@ struct PrecondApplyOp {
     }
 };
 
+// Warp-specialised engine: warps 0..7 compute (one column per thread), warp 8 is the TMA
+// producer.  Slot s has a FULL mbarrier (producer arrive.expect_tx + TMA complete_tx) and
+// an EMPTY mbarrier (one arrive per compute warp once it has pulled the row into its
+// registers), so no CTA-wide barrier is needed per row and the compute warps may drift.
+constexpr int NTHR = TW + 32;
 template <class Op>
-__global__ void __launch_bounds__(TW, MINB) k_stream(GridL g, Op op, int H, double *__restrict__ partials) {
+__global__ void __maxnreg__(112) k_stream(GridL g, Op op, int H, double *__restrict__ partials) {
+    extern __shared__ __align__(128) double sm[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + NS * NF * RW);
+    uint64_t *empty = full + NS;
+    __shared__ double red[NTHR / 32];
+    const int t = threadIdx.x;
+    const int warp = t >> 5;
+    const int j0 = 1 + TW * blockIdx.x;
+    const int i0 = 1 + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, g.ncy);
+    const int rbase = i0 - 1;  // first staged row
+    const int rlast = i1 + 1;  // last staged row
+    if (t == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, TW / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    double acc[Op::NRED > 0 ? Op::NRED : 1];
+#pragma unroll
+    for (int k = 0; k < (Op::NRED > 0 ? Op::NRED : 1); ++k) acc[k] = 0.0;
+    if (warp == TW / 32) {  // ---------------- producer warp
+        if ((t & 31) == 0) {
+            const size_t P = g.P;
+            for (int r = rbase; r <= rlast; ++r) {
+                const int rel = r - rbase, slot = rel % NS;
+                if (rel >= NS) mbar_wait(empty + slot, ((rel / NS) - 1) & 1);  // consumers done with r-NS
+                mbar_expect_tx(full + slot, Op::NF * RW * 8);
+#pragma unroll
+                for (int f = 0; f < Op::NF; ++f)
+                    bulk_g2s(sm + (slot * NF + f) * RW, op.src[f] + (size_t)r * P + (j0 - 2), RW * 8, full + slot);
+            }
+        }
+    } else {  // ---------------------------- compute warps
+        const int j = j0 + t;
+        auto consume = [&](Win &w, int r) {  // wait for row r, pull it into the window, free the slot
+            const int rel = r - rbase, slot = rel % NS;
+            mbar_wait(full + slot, (rel / NS) & 1);
+            w.template push<Op::NF>(sm + slot * NF * RW, t + 2);
+            __syncwarp();
+            if ((t & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + slot)) : "memory");
+        };
+        Win w;
+        consume(w, rbase);
+        consume(w, rbase + 1);
+        for (int i = i0; i <= i1; ++i) {
+            consume(w, i + 1);  // window: A = i-1, B = i, C = i+1
+            if (j <= g.ncx) op.row(g, w, i, j, acc);
+        }
+    }
+    if (Op::NRED > 0) {  // deterministic CTA reduction over the compute warps
+        const size_t b = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+#pragma unroll
+        for (int k = 0; k < Op::NRED; ++k) {
+            double v = warp < TW / 32 ? acc[k] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            __syncthreads();
+            if ((t & 31) == 0) red[warp] = v;
+            __syncthreads();
+            if (t < 32) {
+                v = (t < TW / 32) ? red[t] : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (t == 0) partials[b * Op::NRED + k] = v;
+            }
+        }
+    }
+}
+
+// CTA-barrier engine (register-heavy operators: 256 threads, up to 128 registers, 2 CTAs/SM):
+// thread 0 issues the bulk copies; one __syncthreads per row frees the row's slot.
+template <class Op>
+__global__ void __launch_bounds__(TW, MINB) k_stream_bar(GridL g, Op op, int H, double *__restrict__ partials) {
     extern __shared__ __align__(128) double sm[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + NS * NF * RW);
     __shared__ double red[TW / 32];
@@ -287,10 +356,10 @@ __global__ void __launch_bounds__(TW, MINB) k_stream(GridL g, Op op, int H, doub
     const int j = j0 + t;
     const int i0 = 1 + blockIdx.y * H;
     const int i1 = min(i0 + H - 1, g.ncy);
-    const int rbase = i0 - 1;   // first staged row
-    const int rlast = i1 + 1;   // last staged row
+    const int rbase = i0 - 1;
+    const int rlast = i1 + 1;
     const size_t P = g.P;
-    auto issue = [&](int r) {   // one bulk copy per field row segment, all on the slot's mbarrier
+    auto issue = [&](int r) {
         const int slot = (r - rbase) % NS;
         uint64_t *bar = bars + slot;
         mbar_expect_tx(bar, Op::NF * RW * 8);
@@ -305,12 +374,12 @@ __global__ void __launch_bounds__(TW, MINB) k_stream(GridL g, Op op, int H, doub
     __syncthreads();
     if (t == 0)
         for (int r = rbase; r < rbase + NS && r <= rlast; ++r) issue(r);
-    auto consume = [&](Win &w, int r) {  // wait for row r, push it into the register window
+    auto consume = [&](Win &w, int r) {
         const int rel = r - rbase;
         mbar_wait(bars + rel % NS, (rel / NS) & 1);
         w.template push<Op::NF>(sm + (rel % NS) * NF * RW, t + 2);
     };
-    auto refill = [&](int r) {  // after a barrier: row r's slot is free, stage row r + NS
+    auto refill = [&](int r) {
         if (t == 0 && r + NS <= rlast) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(r + NS);
@@ -326,17 +395,27 @@ __global__ void __launch_bounds__(TW, MINB) k_stream(GridL g, Op op, int H, doub
     refill(rbase);
     refill(rbase + 1);
     for (int i = i0; i <= i1; ++i) {
-        consume(w, i + 1);  // window: A = i-1, B = i, C = i+1
+        consume(w, i + 1);
         if (j <= g.ncx) op.row(g, w, i, j, acc);
-        __syncthreads();    // every thread has read row i+1's slot
+        __syncthreads();
         refill(i + 1);
     }
     if (Op::NRED > 0) {
         const size_t b = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
 #pragma unroll
         for (int k = 0; k < Op::NRED; ++k) {
-            const double s = block_sum256(acc[k], red);
-            if (t == 0) partials[b * Op::NRED + k] = s;
+            double v = acc[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            __syncthreads();
+            if ((t & 31) == 0) red[t >> 5] = v;
+            __syncthreads();
+            if (t < 32) {
+                v = (t < TW / 32) ? red[t] : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (t == 0) partials[b * Op::NRED + k] = v;
+            }
         }
     }
 }
@@ -347,6 +426,7 @@ void prepare_kernel() {
     static bool done = false;
     if (!done) {
         cudaFuncSetAttribute(k_stream<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        cudaFuncSetAttribute(k_stream_bar<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
         done = true;
     }
 }
@@ -374,7 +454,8 @@ dim3 stream_grid(const GridL &g) {
 template <class Op>
 void run(const LaunchCtx &c, const GridL &g, const Op &op, double *partials) {
     prepare_kernel<Op>();
-    k_stream<Op><<<stream_grid(g), TW, SMEM, c.stream>>>(g, op, strip_h(g), partials);
+    if (Op::WS) k_stream<Op><<<stream_grid(g), NTHR, SMEM, c.stream>>>(g, op, strip_h(g), partials);
+    else k_stream_bar<Op><<<stream_grid(g), TW, SMEM, c.stream>>>(g, op, strip_h(g), partials);
     ++*c.counter;
 }
 void fill_src(const double **src, const double *vx, const double *vy, const double *etap, const double *etab,

@@ -153,25 +153,39 @@ def allreduce_max(x, world, device):
     return float(t.item())
 
 
+class OracleSample:
+    """The oracle as it stands on this host's cores (1 thread), set up once on the full-size
+    workload; one sample = one Uzawa iteration (V-cycle + pressure update + energy residual)
+    from the zero initial guess, the bounded piece of a solve timed as the CPU baseline."""
+
+    def __init__(self, name, pre):
+        from oracle.oracle import Oracle
+        from synth.fields import workload
+        self.name, (self.nx, self.ny) = name, pre["n"]
+        w = workload(name, self.nx, self.ny)
+        opts = dict(pre["opts"], max_iter=1, accel=0)
+        self.o = Oracle(self.nx, self.ny, w["Lx"], w["Ly"], w["bc"], **opts)
+        self.o.set_viscosity(w["eta_b"], w["eta_p"])
+        self.o.set_density(w["rho_b"])
+        self.o.set_gravity(w["gx"], w["gy"])
+        shp = [self.o.level_shape(l) for l in range(self.o.nlev)]
+        self.per_vc = dof_sweeps_per_vcycle(shp, opts.get("smoother", 0))
+
+    def step(self):
+        t0 = time.perf_counter()
+        r = self.o.solve(0.0)
+        dt = time.perf_counter() - t0
+        return r["iters"] * self.per_vc / dt, dt
+
+    def describe(self, dt):
+        return (f"1 Uzawa iteration (V-cycle + p-update + energy residual) of {self.name} {self.nx}x{self.ny}, "
+                f"{dt:.2f} s on 1 thread of {os.cpu_count()} ({_cpu_model()})")
+
+
 def cpu_baseline(name, pre):
-    """The oracle as it stands on this host's cores, bounded sample: one Uzawa iteration
-    (1 V-cycle + pressure update + energy residual) of the full-size problem."""
-    from oracle.oracle import Oracle
-    from synth.fields import workload
-    nx, ny = pre["n"]
-    w = workload(name, nx, ny)
-    o = Oracle(nx, ny, w["Lx"], w["Ly"], w["bc"], **dict(pre["opts"], max_iter=1))
-    o.set_viscosity(w["eta_b"], w["eta_p"])
-    o.set_density(w["rho_b"])
-    o.set_gravity(w["gx"], w["gy"])
-    shp = [o.level_shape(l) for l in range(o.nlev)]
-    t0 = time.perf_counter()
-    r = o.solve(0.0)
-    dt = time.perf_counter() - t0
-    dofs = dof_sweeps_per_vcycle(shp, pre["opts"].get("smoother", 0)) * r["iters"]
-    return {"value": dofs / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"1 Uzawa iteration (V-cycle + p-update + energy residual) of {name} {nx}x{ny}, "
-                      f"{dt:.2f} s on 1 thread of {os.cpu_count()} ({_cpu_model()})"}
+    smp = OracleSample(name, pre)
+    v, dt = smp.step()
+    return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": smp.describe(dt)}
 
 
 def _cpu_model():
@@ -185,22 +199,28 @@ def _cpu_model():
 
 
 def run_reference(args, world, rank):
+    """Reference arm: the CPU oracle (no installable reference exists: /root/reference holds
+    only the paper), each step one bounded sample of the same workload."""
     if rank != 0:
         return 0
     pre = presets()[args.workload]
-    vals = []
-    for k in range(args.warmup + args.steps):
-        cb = cpu_baseline(args.workload, pre)
-        if k >= args.warmup:
-            vals.append(cb["value"])
-    v = statistics.mean(vals)
-    cb["value"] = v
+    smp = OracleSample(args.workload, pre)
+    for _ in range(args.warmup):
+        smp.step()
+    vals, dts = [], []
+    for _ in range(args.steps):
+        v, dt = smp.step()
+        vals.append(v)
+        dts.append(dt)
+    v = sum(vals) / len(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(dts) / len(dts), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.workload}: {WORKLOAD_DOC[args.workload]}", "grid": pre["n"],
                        "sample": "each step = 1 Uzawa iteration of the full-size problem on the CPU oracle"},
-            "cpu_baseline": cb, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": smp.describe(sum(dts) / len(dts))},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 

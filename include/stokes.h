@@ -113,8 +113,10 @@ int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const s
  * exchange after every velocity / residual / correction / pressure write); the coarser
  * levels are agglomerated: every process holds the global grid of the first coarse level
  * and runs the coarse tail redundantly.  Options: accel must be STOKES_ACCEL_NONE.
- *   rank < 0  VIRTUAL: all tiles in this process on the current GPU; every array of the
+ *   rank = -1 VIRTUAL: all tiles in this process on the current GPU; every array of the
  *             calls below is the GLOBAL user-layout array (tests of the decomposition).
+ *   rank = -2 LOOPBACK: as VIRTUAL, but halos and the agglomeration go through the NCCL
+ *             path's packing / unpacking with device copies standing in for the NCCL calls.
  *   rank >= 0 NCCL: this process owns tile `rank` (one GPU per process), nccl_unique_id =
  *             128 bytes from stokes_nccl_unique_id() on rank 0, shared by the caller; every
  *             array is the tile's WINDOW of the global user layout, i.e. the user layout of

@@ -40,7 +40,8 @@ struct Dist {
     double Lx, Ly;
     int bc[4];
     stokes_opts o;
-    int rank;  // -1 virtual
+    int rank;  // -1 virtual, -2 loopback (packed transport in one process), >= 0 NCCL
+    int mode;  // M_VIRTUAL, M_LOOPBACK, M_NCCL
     int nt;
     stokes_s *tile[MAXT];
     int tx[MAXT], ty[MAXT];
@@ -52,7 +53,7 @@ struct Dist {
     double *dscal;   // [0] E [1] Sv [2] Sp [3] Sf [4] zero
     double *hsc;
     ncclComm_t comm;
-    double *sbuf, *rbuf;
+    double *sb[MAXT], *rb[MAXT];  // per local tile: packed halo columns / agglomeration blocks
     size_t nbuf;
     long long launches;
     cudaGraphExec_t exec[2];
@@ -65,6 +66,7 @@ struct Dist {
 namespace {
 
 enum { FX_V = 0, FX_R = 1, FX_P = 2, FX_ETA = 3, FX_RHO = 4 };
+enum { M_VIRTUAL = 0, M_LOOPBACK = 1, M_NCCL = 2 };
 
 LaunchCtx dctx(Dist &D) { return LaunchCtx{D.stream, &D.launches}; }
 
@@ -78,7 +80,7 @@ int nfields(stokes_s *h, int l, int which, int idx, double **f) {
     default: f[0] = h->rho; return 1;
     }
 }
-int tile_at(Dist &D, int tx, int ty) { return D.rank < 0 ? ty * D.px + tx : -1; }
+int tile_at(Dist &D, int tx, int ty) { return D.mode != M_NCCL ? ty * D.px + tx : -1; }
 
 void add_strip(StripList &s, double *dst, const double *src, int n, int ds, int ss) {
     s.dst[s.count] = dst;
@@ -93,7 +95,7 @@ void add_strip(StripList &s, double *dst, const double *src, int n, int ds, int 
 int exchange(Dist &D, int l, int which, int idx) {
     const LaunchCtx c = dctx(D);
     double *f[2], *fu[2];
-    if (D.rank < 0) {  // ---- virtual: strip-copy kernels between the tiles' buffers
+    if (D.mode == M_VIRTUAL) {  // ---- virtual: strip-copy kernels between the tiles' buffers
         StripList s;
         s.count = 0;
         for (int k = 0; k < D.nt; ++k) {
@@ -125,52 +127,98 @@ int exchange(Dist &D, int l, int which, int idx) {
         if (s.count) launch_strips(c, s);
         return STOKES_OK;
     }
-    // ---- NCCL: one tile here; neighbours are ranks
-    stokes_s *t = D.tile[0];
-    const GridL &g = t->lev[l].g;
-    const int nf = nfields(t, l, which, idx, f);
-    const int tx = D.tx[0], ty = D.ty[0];
-    const int W = tx > 0 ? D.rank - 1 : -1, E = tx + 1 < D.px ? D.rank + 1 : -1;
-    const int N = ty > 0 ? D.rank - D.px : -1, S = ty + 1 < D.py ? D.rank + D.px : -1;
-    const int rows = g.ncy + 2;
-    if (W >= 0 || E >= 0) {
+    // ---- packed transport (NCCL: one tile per process; LOOPBACK: every tile here, the same
+    // packing with the transfers done by device copies -- tests the NCCL path on one GPU)
+    const int nl = D.nt;
+    int nf = 0;
+    int rows = 0;
+    {  // phase 1: W/E columns packed into sb = [W part | E part], nf x rows each
         StripList s;
         s.count = 0;
-        for (int q = 0; q < nf; ++q) {
-            if (W >= 0) add_strip(s, D.sbuf + (size_t)q * rows, f[q] + at(g, 0, 1), rows, 1, g.P);
-            if (E >= 0) add_strip(s, D.sbuf + (size_t)(nf + q) * rows, f[q] + at(g, 0, g.ncx), rows, 1, g.P);
+        for (int k = 0; k < nl; ++k) {
+            const GridL &g = D.tile[k]->lev[l].g;
+            nf = nfields(D.tile[k], l, which, idx, f);
+            rows = g.ncy + 2;
+            const bool W = D.tx[k] > 0, E = D.tx[k] + 1 < D.px;
+            for (int q = 0; q < nf; ++q) {
+                if (W) add_strip(s, D.sb[k] + (size_t)q * rows, f[q] + at(g, 0, 1), rows, 1, g.P);
+                if (E) add_strip(s, D.sb[k] + (size_t)(nf + q) * rows, f[q] + at(g, 0, g.ncx), rows, 1, g.P);
+            }
         }
-        launch_strips(c, s);
-        ncclGroupStart();
-        if (W >= 0) {
-            ncclSend(D.sbuf, (size_t)nf * rows, ncclDouble, W, D.comm, D.stream);
-            ncclRecv(D.rbuf, (size_t)nf * rows, ncclDouble, W, D.comm, D.stream);
+        if (s.count) launch_strips(c, s);
+        const size_t part = (size_t)nf * rows;
+        if (D.mode == M_NCCL) {
+            const int W = D.tx[0] > 0 ? D.rank - 1 : -1, E = D.tx[0] + 1 < D.px ? D.rank + 1 : -1;
+            if (W >= 0 || E >= 0) {
+                ncclGroupStart();
+                if (W >= 0) {
+                    ncclSend(D.sb[0], part, ncclDouble, W, D.comm, D.stream);
+                    ncclRecv(D.rb[0], part, ncclDouble, W, D.comm, D.stream);
+                }
+                if (E >= 0) {
+                    ncclSend(D.sb[0] + part, part, ncclDouble, E, D.comm, D.stream);
+                    ncclRecv(D.rb[0] + part, part, ncclDouble, E, D.comm, D.stream);
+                }
+                if (ncclGroupEnd() != ncclSuccess) return STOKES_ENCCL;
+            }
+        } else {  // loopback: my W part <- W neighbour's E part, my E part <- E neighbour's W part
+            for (int k = 0; k < nl; ++k) {
+                if (D.tx[k] > 0)
+                    CK(cudaMemcpyAsync(D.rb[k], D.sb[tile_at(D, D.tx[k] - 1, D.ty[k])] + part, part * 8,
+                                       cudaMemcpyDeviceToDevice, D.stream));
+                if (D.tx[k] + 1 < D.px)
+                    CK(cudaMemcpyAsync(D.rb[k] + part, D.sb[tile_at(D, D.tx[k] + 1, D.ty[k])], part * 8,
+                                       cudaMemcpyDeviceToDevice, D.stream));
+            }
         }
-        if (E >= 0) {
-            ncclSend(D.sbuf + (size_t)nf * rows, (size_t)nf * rows, ncclDouble, E, D.comm, D.stream);
-            ncclRecv(D.rbuf + (size_t)nf * rows, (size_t)nf * rows, ncclDouble, E, D.comm, D.stream);
-        }
-        if (ncclGroupEnd() != ncclSuccess) return STOKES_ENCCL;
         s.count = 0;
-        for (int q = 0; q < nf; ++q) {
-            if (W >= 0) add_strip(s, f[q] + at(g, 0, 0), D.rbuf + (size_t)q * rows, rows, g.P, 1);
-            if (E >= 0) add_strip(s, f[q] + at(g, 0, g.ncx + 1), D.rbuf + (size_t)(nf + q) * rows, rows, g.P, 1);
+        for (int k = 0; k < nl; ++k) {
+            const GridL &g = D.tile[k]->lev[l].g;
+            nfields(D.tile[k], l, which, idx, f);
+            for (int q = 0; q < nf; ++q) {
+                if (D.tx[k] > 0) add_strip(s, f[q] + at(g, 0, 0), D.rb[k] + (size_t)q * rows, rows, g.P, 1);
+                if (D.tx[k] + 1 < D.px)
+                    add_strip(s, f[q] + at(g, 0, g.ncx + 1), D.rb[k] + (size_t)(nf + q) * rows, rows, g.P, 1);
+            }
         }
-        launch_strips(c, s);
+        if (s.count) launch_strips(c, s);
     }
-    if (N >= 0 || S >= 0) {
-        ncclGroupStart();
-        for (int q = 0; q < nf; ++q) {
-            if (N >= 0) {
-                ncclSend(f[q] + at(g, 1, 0), g.ncx + 2, ncclDouble, N, D.comm, D.stream);
-                ncclRecv(f[q] + at(g, 0, 0), g.ncx + 2, ncclDouble, N, D.comm, D.stream);
+    // phase 2: N/S rows are contiguous: sent straight from / received straight into the field
+    if (D.mode == M_NCCL) {
+        const GridL &g = D.tile[0]->lev[l].g;
+        nfields(D.tile[0], l, which, idx, f);
+        const int N = D.ty[0] > 0 ? D.rank - D.px : -1, S = D.ty[0] + 1 < D.py ? D.rank + D.px : -1;
+        if (N >= 0 || S >= 0) {
+            ncclGroupStart();
+            for (int q = 0; q < nf; ++q) {
+                if (N >= 0) {
+                    ncclSend(f[q] + at(g, 1, 0), g.ncx + 2, ncclDouble, N, D.comm, D.stream);
+                    ncclRecv(f[q] + at(g, 0, 0), g.ncx + 2, ncclDouble, N, D.comm, D.stream);
+                }
+                if (S >= 0) {
+                    ncclSend(f[q] + at(g, g.ncy, 0), g.ncx + 2, ncclDouble, S, D.comm, D.stream);
+                    ncclRecv(f[q] + at(g, g.ncy + 1, 0), g.ncx + 2, ncclDouble, S, D.comm, D.stream);
+                }
             }
-            if (S >= 0) {
-                ncclSend(f[q] + at(g, g.ncy, 0), g.ncx + 2, ncclDouble, S, D.comm, D.stream);
-                ncclRecv(f[q] + at(g, g.ncy + 1, 0), g.ncx + 2, ncclDouble, S, D.comm, D.stream);
+            if (ncclGroupEnd() != ncclSuccess) return STOKES_ENCCL;
+        }
+    } else {
+        for (int k = 0; k < nl; ++k) {
+            const GridL &g = D.tile[k]->lev[l].g;
+            nfields(D.tile[k], l, which, idx, f);
+            for (int q = 0; q < nf; ++q) {
+                if (D.ty[k] > 0) {
+                    nfields(D.tile[tile_at(D, D.tx[k], D.ty[k] - 1)], l, which, idx, fu);
+                    CK(cudaMemcpyAsync(f[q] + at(g, 0, 0), fu[q] + at(g, g.ncy, 0), (g.ncx + 2) * 8,
+                                       cudaMemcpyDeviceToDevice, D.stream));
+                }
+                if (D.ty[k] + 1 < D.py) {
+                    nfields(D.tile[tile_at(D, D.tx[k], D.ty[k] + 1)], l, which, idx, fu);
+                    CK(cudaMemcpyAsync(f[q] + at(g, g.ncy + 1, 0), fu[q] + at(g, 1, 0), (g.ncx + 2) * 8,
+                                       cudaMemcpyDeviceToDevice, D.stream));
+                }
             }
         }
-        if (ncclGroupEnd() != ncclSuccess) return STOKES_ENCCL;
     }
     return STOKES_OK;
 }
@@ -188,7 +236,7 @@ int gather_to_tail(Dist &D, int which) {
         else { r0 = 1; c0 = 1; nr = gc.ncy; nc = gc.ncx; }  // P nodes
     };
     const GridL &gc = D.tile[0]->lev[La].g;
-    if (D.rank < 0) {
+    if (D.mode == M_VIRTUAL) {
         for (int k = 0; k < D.nt; ++k) {
             Level &C = D.tile[k]->lev[La];
             double *src[2] = {which == 0 ? C.bx : C.etab, which == 0 ? C.by : C.etap};
@@ -203,23 +251,32 @@ int gather_to_tail(Dist &D, int which) {
         }
         return STOKES_OK;
     }
-    Level &C = D.tile[0]->lev[La];
-    double *src[2] = {which == 0 ? C.bx : C.etab, which == 0 ? C.by : C.etap};
-    double *dst[2] = {which == 0 ? T0.bx : T0.etab, which == 0 ? T0.by : T0.etap};
+    // packed: every tile packs its rectangles into a block of its sb; the blocks of all ranks
+    // are all-gathered (NCCL) or concatenated (loopback) into rb[0] and unpacked in rank order
     const size_t blk = (size_t)2 * (gc.ncy + 1) * (gc.ncx + 1);
-    for (int f = 0; f < 2; ++f) {
-        int r0, c0, nr, nc;
-        rect(0, f, r0, c0, nr, nc);
-        CK(cudaMemcpy2DAsync(D.sbuf + f * (blk / 2), (size_t)nc * 8, src[f] + at(gc, r0, c0), gc.P * 8, (size_t)nc * 8,
-                             nr, cudaMemcpyDeviceToDevice, D.stream));
+    double *dst[2] = {which == 0 ? T0.bx : T0.etab, which == 0 ? T0.by : T0.etap};
+    for (int k = 0; k < D.nt; ++k) {
+        Level &C = D.tile[k]->lev[La];
+        double *src[2] = {which == 0 ? C.bx : C.etab, which == 0 ? C.by : C.etap};
+        for (int f = 0; f < 2; ++f) {
+            int r0, c0, nr, nc;
+            rect(k, f, r0, c0, nr, nc);
+            CK(cudaMemcpy2DAsync(D.sb[k] + f * (blk / 2), (size_t)nc * 8, src[f] + at(gc, r0, c0), gc.P * 8,
+                                 (size_t)nc * 8, nr, cudaMemcpyDeviceToDevice, D.stream));
+        }
     }
-    if (ncclAllGather(D.sbuf, D.rbuf, blk, ncclDouble, D.comm, D.stream) != ncclSuccess) return STOKES_ENCCL;
+    if (D.mode == M_NCCL) {
+        if (ncclAllGather(D.sb[0], D.rb[0], blk, ncclDouble, D.comm, D.stream) != ncclSuccess) return STOKES_ENCCL;
+    } else {
+        for (int k = 0; k < D.nt; ++k)
+            CK(cudaMemcpyAsync(D.rb[0] + (size_t)k * blk, D.sb[k], blk * 8, cudaMemcpyDeviceToDevice, D.stream));
+    }
     for (int r = 0; r < D.px * D.py; ++r) {
         const int gi = (r / D.px) * gc.ncy, gj = (r % D.px) * gc.ncx;
         for (int f = 0; f < 2; ++f) {
             int r0, c0, nr, nc;
             rect(r, f, r0, c0, nr, nc);
-            CK(cudaMemcpy2DAsync(dst[f] + at(T0.g, gi + r0, gj + c0), T0.g.P * 8, D.rbuf + r * blk + f * (blk / 2),
+            CK(cudaMemcpy2DAsync(dst[f] + at(T0.g, gi + r0, gj + c0), T0.g.P * 8, D.rb[0] + r * blk + f * (blk / 2),
                                  (size_t)nc * 8, (size_t)nc * 8, nr, cudaMemcpyDeviceToDevice, D.stream));
         }
     }
@@ -339,7 +396,7 @@ int combine(Dist &D, bool write_mean) {
         loc[k] = D.tile[k]->scal + S_LOC;
         ms[k] = D.tile[k]->scal + S_MSHIFT;
     }
-    if (D.rank >= 0)
+    if (D.mode == M_NCCL)
         if (ncclAllReduce(D.tile[0]->scal + S_LOC, D.tile[0]->scal + S_LOC, 3, ncclDouble, ncclSum, D.comm,
                           D.stream) != ncclSuccess)
             return STOKES_ENCCL;
@@ -500,7 +557,7 @@ void tile_window(Dist &D, int k, int kind, int &off, int &rows, int &cols, int &
 }
 // copy the tile-k window of a user array into tmp (virtual) or pass the rank's array through
 const double *window_in(Dist &D, int k, int kind, const double *u, double *tmp) {
-    if (D.rank >= 0) return u;
+    if (D.mode == M_NCCL) return u;
     int off, rows, cols, gp;
     tile_window(D, k, kind, off, rows, cols, gp);
     cudaMemcpy2DAsync(tmp, (size_t)cols * 8, u + off, (size_t)gp * 8, (size_t)cols * 8, rows, cudaMemcpyDeviceToDevice,
@@ -535,9 +592,11 @@ int dist_destroy(Dist *D) {
     drop(*D);
     for (int k = 0; k < D->nt; ++k) free_handle(D->tile[k]);
     free_handle(D->tail);
-    if (D->rank >= 0) ncclCommDestroy(D->comm);
-    if (D->sbuf) cudaFree(D->sbuf);
-    if (D->rbuf) cudaFree(D->rbuf);
+    if (D->mode == M_NCCL && D->comm) ncclCommDestroy(D->comm);
+    for (int k = 0; k < MAXT; ++k) {
+        if (D->sb[k]) cudaFree(D->sb[k]);
+        if (D->rb[k]) cudaFree(D->rb[k]);
+    }
     if (D->dscal) cudaFree(D->dscal);
     if (D->hsc) cudaFreeHost(D->hsc);
     if (D->own_stream) cudaStreamDestroy(D->stream);
@@ -684,7 +743,7 @@ int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *ite
         stokes_s *t = D->tile[q];
         Level &F = t->lev[0];
         const LaunchCtx c = ctx(t);
-        if (D->rank >= 0) {
+        if (D->mode == M_NCCL) {
             launch_out_vx(c, F.g, F.vx[0], vx);
             launch_out_vy(c, F.g, F.vy[0], vy);
             launch_out_p(c, F.g, t->pbuf[D->pcur], p, t->scal + S_MSHIFT);
@@ -714,7 +773,7 @@ int stokes_nccl_unique_id(void *id128) {
 int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], int px, int py, int rank,
                        const void *nccl_unique_id, const stokes_opts *opts, void *cuda_stream, stokes_t *out) {
     if (!out || px < 1 || py < 1 || px * py > MAXT || nx % px || ny % py || !bc) return STOKES_EINVAL;
-    if (rank >= px * py || (rank >= 0 && !nccl_unique_id)) return STOKES_EINVAL;
+    if (rank >= px * py || rank < -2 || (rank >= 0 && !nccl_unique_id)) return STOKES_EINVAL;
     Dist *D = (Dist *)calloc(1, sizeof(Dist));
     if (!D) return STOKES_ENOMEM;
     D->NX = nx;
@@ -732,6 +791,7 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
     for (int k = 0; k < 4; ++k)
         if (bc[k] != 0 && bc[k] != 1) { free(D); return STOKES_EINVAL; }
     D->rank = rank;
+    D->mode = rank >= 0 ? M_NCCL : (rank == -2 ? M_LOOPBACK : M_VIRTUAL);
     // global hierarchy and the agglomeration level (tile levels while the tile is >= dmin)
     GridL gs[MAXLEV];
     int nus[MAXLEV];
@@ -752,7 +812,7 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
         D->own_stream = true;
     }
     int st;
-    if (rank < 0) {
+    if (D->mode != M_NCCL) {
         D->nt = px * py;
         for (int k = 0; k < D->nt; ++k) {
             D->tx[k] = k % px;
@@ -778,8 +838,11 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
     if (D->tail->nlev + La != D->L) { dist_destroy(D); return STOKES_EINVAL; }
     const GridL &gf = D->tile[0]->lev[0].g, &gc = D->tile[0]->lev[La].g;
     D->nbuf = 4 * (size_t)(gf.ncy + 2) + 4 * (size_t)(gc.ncy + 1) * (gc.ncx + 1) * (size_t)(px * py) + 64;
-    if (cudaMalloc(&D->sbuf, D->nbuf * 8) != cudaSuccess || cudaMalloc(&D->rbuf, D->nbuf * 8) != cudaSuccess ||
-        cudaMalloc(&D->dscal, 64 * 8) != cudaSuccess || cudaMallocHost(&D->hsc, 64 * 8) != cudaSuccess) {
+    bool okm = cudaMalloc(&D->dscal, 64 * 8) == cudaSuccess && cudaMallocHost(&D->hsc, 64 * 8) == cudaSuccess;
+    const int nbufs = D->mode == M_LOOPBACK ? D->nt : 1;
+    for (int k = 0; k < nbufs && okm; ++k)
+        okm = cudaMalloc(&D->sb[k], D->nbuf * 8) == cudaSuccess && cudaMalloc(&D->rb[k], D->nbuf * 8) == cudaSuccess;
+    if (!okm) {
         dist_destroy(D);
         return STOKES_ENOMEM;
     }

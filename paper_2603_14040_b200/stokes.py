@@ -360,14 +360,16 @@ def nccl_unique_id():
 class StokesDist(Stokes):
     """2D-decomposed handle (stokes_create_dist).
 
-    rank=None: VIRTUAL decomposition -- all px*py tiles in this process on one GPU, arrays
-    are the GLOBAL user-layout arrays (exactness tests on one B200).
+    rank=None: all px*py tiles in this process on one GPU, arrays are the GLOBAL user-layout
+    arrays; transport="virtual" copies halo strips between the tiles directly,
+    transport="loopback" runs the NCCL code path's packing / unpacking with device copies
+    in place of ncclSend/Recv/AllGather (tests of the multi-GPU path on one B200).
     rank=r (with torch.distributed initialised): NCCL decomposition, one tile per process;
     arrays are the tile windows (`tile_windows`).  The NCCL unique id is created on rank 0
     and broadcast with torch.distributed (the process group is plumbing only)."""
 
     def __init__(self, nx, ny, Lx=1.0, Ly=1.0, bc=(FREE_SLIP,) * 4, px=1, py=1, rank=None, device=None,
-                 stream=None, **opts):
+                 stream=None, transport="virtual", **opts):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2603_14040_b200 needs a CUDA GPU (B200, sm_100a); no CPU fallback")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -385,7 +387,8 @@ class StokesDist(Stokes):
             self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
             self._h = ctypes.c_void_p()
             bcs = (ctypes.c_int * 4)(*self.bc)
-            _check(lib().stokes_create_dist(nx, ny, float(Lx), float(Ly), bcs, px, py, -1 if rank is None else rank,
+            code = rank if rank is not None else {"virtual": -1, "loopback": -2}[transport]
+            _check(lib().stokes_create_dist(nx, ny, float(Lx), float(Ly), bcs, px, py, code,
                                             uid, ctypes.byref(self.opts), ctypes.c_void_p(self.stream.cuda_stream),
                                             ctypes.byref(self._h)), "create_dist")
 

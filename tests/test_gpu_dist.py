@@ -43,28 +43,41 @@ def setup(cls, w, n, **kw):
     return s
 
 
+@pytest.mark.parametrize("transport", ["virtual", "loopback"])
 @pytest.mark.parametrize("px,py", [(2, 1), (1, 2), (2, 2), (4, 2)])
 @pytest.mark.parametrize("name,smoother", [("layered", 0), ("mms", 0), ("block", 1)])
-def test_virtual_decomposition_is_exact(px, py, name, smoother):
+def test_virtual_decomposition_is_exact(px, py, name, smoother, transport):
     from paper_2603_14040_b200 import Stokes, StokesDist
     n = 128
     w = workload(name, n, n)
     opts = dict(omega_v=0.6, alpha_p=1.0, smoother=smoother, max_iter=400)
     one = setup(Stokes, w, n, **opts)
-    dd = setup(StokesDist, w, n, px=px, py=py, **opts)
+    dd = setup(StokesDist, w, n, px=px, py=py, transport=transport, **opts)
     a = one.solve(1e-8)
     b = dd.solve(1e-8)
     assert a["status"] == 0 and b["status"] == 0
     assert abs(a["iters"] - b["iters"]) <= 1, (a["iters"], b["iters"])
     # equal iteration count -> same iterate (decomposition is exact up to sum order)
     one2 = setup(Stokes, w, n, **dict(opts, max_iter=a["iters"]))
-    dd2 = setup(StokesDist, w, n, px=px, py=py, **dict(opts, max_iter=a["iters"]))
+    dd2 = setup(StokesDist, w, n, px=px, py=py, transport=transport, **dict(opts, max_iter=a["iters"]))
     a2, b2 = one2.solve(0.0), dd2.solve(0.0)
     for k in ("vx", "vy", "p"):
         assert rel(b2[k], a2[k]) <= 1e-11, (k, rel(b2[k], a2[k]))
     _, _, _, e1 = one.residual(a["vx"], a["vy"], a["p"])
     _, _, _, e2 = dd.residual(a["vx"], a["vy"], a["p"])
     assert abs(e1 - e2) <= 1e-12 * max(e1, 1e-300)
+
+
+def test_loopback_large_tiles_stream_path():
+    """256-wide tiles take the TMA streaming kernels on the distributed levels."""
+    from paper_2603_14040_b200 import Stokes, StokesDist
+    n = 512
+    w = workload("layered", n, n)
+    opts = dict(omega_v=0.6, alpha_p=1.0, max_iter=3)
+    a = setup(Stokes, w, n, **opts).solve(0.0)
+    b = setup(StokesDist, w, n, px=2, py=2, transport="loopback", **opts).solve(0.0)
+    for k in ("vx", "vy", "p"):
+        assert rel(b[k], a[k]) <= 1e-12, k
 
 
 def test_decomposition_errors():

@@ -796,7 +796,10 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
     GridL gs[MAXLEV];
     int nus[MAXLEV];
     D->L = build_levels(nx, ny, Lx, Ly, bc, D->o, gs, nus);
-    int dmin = 64;
+    // distribute while tiles are >= dmin cells: NCCL exchanges cost ~10-30 us each, so the
+    // multi-GPU default agglomerates at 512-cell tiles (the redundant global tail is then a
+    // ~1024 x 512 grid at 8 GPUs); in-process transports keep more levels distributed
+    int dmin = D->mode == M_NCCL ? 512 : 64;
     if (const char *e = getenv("STOKES_DIST_DMIN")) dmin = atoi(e) > 2 ? atoi(e) : 2;
     int La = 0;
     while (La + 1 <= D->L - 1) {

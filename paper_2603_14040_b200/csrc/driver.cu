@@ -38,6 +38,8 @@ GridL make_grid(int ncx, int ncy, double Lx, double Ly, const int bc[4]) {
     g.idx2 = 1.0 / (g.dx * g.dx);
     g.idy2 = 1.0 / (g.dy * g.dy);
     g.idxdy = 1.0 / (g.dx * g.dy);
+    g.idx2x2 = 2.0 * g.idx2;
+    g.idy2x2 = 2.0 * g.idy2;
     g.sW = bc[0] == STOKES_FREE_SLIP ? 1.0 : -1.0;
     g.sE = bc[1] == STOKES_FREE_SLIP ? 1.0 : -1.0;
     g.sN = bc[2] == STOKES_FREE_SLIP ? 1.0 : -1.0;

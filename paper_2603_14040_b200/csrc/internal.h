@@ -20,6 +20,7 @@ struct GridL {          // one multigrid level, passed by value to kernels
     double idx, idy;    // 1/dx, 1/dy
     double idx2, idy2;  // 1/dx^2, 1/dy^2
     double idxdy;       // 1/(dx dy)
+    double idx2x2, idy2x2;  // 2/dx^2, 2/dy^2
     double sW, sE, sN, sS;  // mirror signs: +1 free slip, -1 no slip
     // 2D domain decomposition: a level may be one tile of the global grid.
     // bX = 1: side X is a global boundary (mirrors / walls); 0: a halo filled

@@ -93,26 +93,29 @@ __device__ __forceinline__ double rcp(double a) {
 struct RowX {
     double L, a;  // (L v) at the node and a_ii
 };
+// Written as coefficient x (neighbour - centre) differences (the stress form of
+// PAPER.md:643-661): the same operator as the Listing's coefficients with ~20% fewer
+// FP64 operations and shorter dependency chains; a_ii is formed separately.
 __device__ __forceinline__ RowX lx_win(const GridL &g, const Win &w, int i) {
     const double eta1 = w.A(F_EB), eta2 = w.B(F_EB), etaA = w.B(F_EP), etaB = w.B(F_EP, 1);
-    const double c = -(eta1 + eta2) * g.idy2 - 2.0 * (etaA + etaB) * g.idx2;
+    const double vc = w.B(F_VX);
     RowX r;
-    r.L = 2.0 * etaA * g.idx2 * w.B(F_VX, -1) + eta1 * g.idy2 * w.A(F_VX) + c * w.B(F_VX) + eta2 * g.idy2 * w.C(F_VX) +
-          2.0 * etaB * g.idx2 * w.B(F_VX, 1) +
+    r.L = g.idx2x2 * (etaA * (w.B(F_VX, -1) - vc) + etaB * (w.B(F_VX, 1) - vc)) +
+          g.idy2 * (eta1 * (w.A(F_VX) - vc) + eta2 * (w.C(F_VX) - vc)) +
           g.idxdy * (eta1 * (w.A(F_VY) - w.A(F_VY, 1)) + eta2 * (w.B(F_VY, 1) - w.B(F_VY)));
-    r.a = c;
+    r.a = -(eta1 + eta2) * g.idy2 - (etaA + etaB) * g.idx2x2;
     if (i == 1 && g.bN) r.a += g.sN * eta1 * g.idy2;
     if (i == g.ncy && g.bS) r.a += g.sS * eta2 * g.idy2;
     return r;
 }
 __device__ __forceinline__ RowX ly_win(const GridL &g, const Win &w, int j) {
     const double etaN = w.B(F_EP), etaS = w.C(F_EP), etaW = w.B(F_EB, -1), etaE = w.B(F_EB);
-    const double c = -2.0 * (etaN + etaS) * g.idy2 - (etaW + etaE) * g.idx2;
+    const double vc = w.B(F_VY);
     RowX r;
-    r.L = 2.0 * etaS * g.idy2 * w.C(F_VY) + 2.0 * etaN * g.idy2 * w.A(F_VY) + etaE * g.idx2 * w.B(F_VY, 1) +
-          etaW * g.idx2 * w.B(F_VY, -1) + c * w.B(F_VY) +
+    r.L = g.idy2x2 * (etaS * (w.C(F_VY) - vc) + etaN * (w.A(F_VY) - vc)) +
+          g.idx2 * (etaE * (w.B(F_VY, 1) - vc) + etaW * (w.B(F_VY, -1) - vc)) +
           g.idxdy * (etaE * (w.C(F_VX) - w.B(F_VX)) - etaW * (w.C(F_VX, -1) - w.B(F_VX, -1)));
-    r.a = c;
+    r.a = -(etaN + etaS) * g.idy2x2 - (etaW + etaE) * g.idx2;
     if (j == 1 && g.bW) r.a += g.sW * etaW * g.idx2;
     if (j == g.ncx && g.bE) r.a += g.sE * etaE * g.idx2;
     return r;

@@ -181,10 +181,14 @@ void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&
 // One V-cycle (Eq. multigrid_levels) on level l for L v = b, v in
 // (ax, ay) with scratch (bx_, by_); the result is left in (ax, ay) (the sweep count per
 // cycle, 2 nu, is even).  zero_in: the initial guess is 0 (coarse corrections).
-void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in) {
+void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in,
+            int done_pre) {
     Level &L = h->lev[l];
     const LaunchCtx c = ctx(h);
     double *cx = ax, *cy = ay, *ox = sx, *oy = sy;
+    if (done_pre) {  // the first pre-smoothing sweep was done by a fused kernel into (sx, sy)
+        cx = sx; cy = sy; ox = ax; oy = ay;
+    }
     if (l == h->nlev - 1) {  // coarsest (a8)
         if (h->nc > 0) {
             const double *bx = rhs.bx, *by = rhs.by;
@@ -204,7 +208,7 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
         return;
     }
     Level &C = h->lev[l + 1];
-    smooth(h, l, cx, cy, ox, oy, rhs, L.nu, zero_in);                        // (1) pre-smoothing
+    smooth(h, l, cx, cy, ox, oy, rhs, L.nu - done_pre, zero_in && !done_pre);  // (1) pre-smoothing
     launch_residual(c, L.g, L.etab, L.etap, cx, cy, rhs, L.rx, L.ry);          // (2) residual
     launch_restrict_vel(c, L.g, C.g, L.rx, L.ry, C.bx, C.by);                 // (3) restriction
     vcycle(h, l + 1, C.vx[0], C.vy[0], C.vx[1], C.vy[1], rhs_arrays(C.bx, C.by), true);  // (4)
@@ -296,6 +300,11 @@ void drop_graphs(stokes_s *h) {
             cudaGraphExecDestroy(h->uzawa_exec[k]);
             h->uzawa_exec[k] = nullptr;
         }
+    for (int k = 0; k < 2; ++k)
+        if (h->fused_exec[k]) {
+            cudaGraphExecDestroy(h->fused_exec[k]);
+            h->fused_exec[k] = nullptr;
+        }
     for (int k = 0; k < MAXM; ++k)
         if (h->gcr_exec[k]) {
             cudaGraphExecDestroy(h->gcr_exec[k]);
@@ -343,6 +352,74 @@ int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
     *iters = k;
     *Eout = E;
     return status;
+}
+
+// ---- Uzawa with the a12 fusion: the pressure update and the energy residual of iterate k
+// ride on the first pre-smoothing sweep of V-cycle k+1 (one HBM pass instead of two).
+bool fused_ok(stokes_s *h) {
+    return h->o.smoother == STOKES_SMOOTH_JACOBI && h->o.vcycles_per_iter == 1 && h->nlev > 1 && h->o.max_iter >= 1 &&
+           h->lev[0].nu >= 1 && stream_ok(h->lev[0].g);
+}
+// from v^k (buf 0) and p^(k-1) = pbuf[pcur]: p^k -> pbuf[1-pcur], E(v^k, p^k), v' -> buf 1
+void fused_tail(stokes_s *h) {
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    launch_jacobi_uzawa(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], h->pbuf[h->pcur],
+                        h->pbuf[1 - h->pcur], h->rho, h->gx, h->gy, h->o.pressure_sign * h->o.alpha_p,
+                        h->scal + S_MSHIFT, h->o.omega_v, h->partials);
+    launch_uzawa_final(c, h->partials, stream_blocks(F.g), h->scal + S_SF, 1.0 / ((double)F.g.ncx * F.g.ncy),
+                       h->scal + S_E, h->scal + S_MSHIFT);
+    cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+}
+// graph body: rest of V-cycle k+1 (its first sweep already in buf 1) on L v = f - G pbuf[pcur],
+// then the fused tail of iterate k+1
+void fused_body(stokes_s *h) {
+    Level &F = h->lev[0];
+    vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false, 1);
+    fused_tail(h);
+}
+int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+    const int keep = h->pcur;
+    for (int k = 0; k < 2; ++k) {
+        if (h->fused_exec[k]) continue;
+        cudaGraph_t graph;
+        const long long before = h->launches;
+        h->pcur = k;
+        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        fused_body(h);
+        cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
+        h->pcur = keep;
+        if (e != cudaSuccess) return fail_cuda(e, "graph capture");
+        h->fused_kernels = h->launches - before;
+        h->launches = before;
+        e = cudaGraphInstantiate(&h->fused_exec[k], graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            h->fused_exec[k] = nullptr;
+            return fail_cuda(e, "graph instantiate");
+        }
+    }
+    Level &F = h->lev[0];
+    double E = E0;
+    int k = 1, status = STOKES_NOT_CONVERGED;
+    // iteration 1: a full V-cycle from (v^0, p^0), then the fused tail of iterate 1
+    vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false);
+    fused_tail(h);
+    for (;;) {
+        h->pcur ^= 1;  // pbuf[pcur] = p^k
+        int st = sync(h);
+        if (st) return st;
+        E = h->hscal[S_E];
+        if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+        if (E <= rtol) { status = STOKES_OK; break; }
+        if (k >= h->o.max_iter) break;
+        ++k;
+        CK(cudaGraphLaunch(h->fused_exec[h->pcur], h->stream));
+        h->launches += h->fused_kernels;
+    }
+    *iters = k;
+    *Eout = E;
+    return status;  // (v^k in buf 0, p^k in pbuf[pcur], its mean in S_MSHIFT)
 }
 
 // One fused GCR step i (Alg. 4 inner loop body) on the stream:
@@ -779,7 +856,8 @@ int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int
         status = stream_ok(F.g) ? solve_gcr_fused(h, rtol, E0, iters, rel_energy)
                                 : solve_gcr(h, rtol, E0, iters, rel_energy);
     } else {
-        status = solve_uzawa(h, rtol, E0, iters, rel_energy);
+        status = fused_ok(h) ? solve_uzawa_fused(h, rtol, E0, iters, rel_energy)
+                             : solve_uzawa(h, rtol, E0, iters, rel_energy);
     }
     if (status < 0 && status != STOKES_EDIVERGED) return status;
     launch_out_vx(c, F.g, F.vx[0], vx);
@@ -921,15 +999,22 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
                 launch_pupdate(c, g, F.etap, F.vx[0], F.vy[0], h->pbuf[h->pcur], h->pbuf[1 - h->pcur], h->o.alpha_p,
                                h->scal + S_ZERO, h->partials);
             break;
-        default: launch_rbgs(c, g, F.etab, F.etap, F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v); break;
+        case 5: launch_rbgs(c, g, F.etab, F.etap, F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v); break;
+        default:
+            launch_jacobi_uzawa(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], h->pbuf[h->pcur],
+                                h->pbuf[1 - h->pcur], h->rho, h->gx, h->gy, h->o.alpha_p, h->scal + S_ZERO,
+                                h->o.omega_v, h->partials);
+            break;
         }
     };
     // algorithmic bytes per launch: 8 B per value read or written
     // 0 Jacobi: read vx,vy,eta_p,eta_b,p,rho + write vx,vy; 1 energy: read 6; 2 residual (read 6,
     // write 2) + restriction (read 2 fine, write 1/2); 3 prolongation (read/write 2 + 1/2 coarse);
-    // 4 fused Uzawa pressure step + energy: read 6, write p; 5 RBGS (4 phases, fused bytes)
-    const double per_cell[6] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0};
-    if (kernel < 0 || kernel > 5) return STOKES_EINVAL;
+    // 4 fused Uzawa pressure step + energy: read 6, write p; 5 RBGS (4 phases, fused bytes);
+    // 6 Uzawa step + energy + first Jacobi sweep of the next V-cycle: read 6, write p, vx, vy
+    const double per_cell[7] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0, 72.0};
+    if (kernel < 0 || kernel > 6) return STOKES_EINVAL;
+    if (kernel == 6 && !stream_ok(g)) return STOKES_EINVAL;
     *bytes = per_cell[kernel] * cells;
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));

@@ -57,6 +57,8 @@ struct stokes_s {
     double gx, gy;
     long long launches;
     cudaGraphExec_t uzawa_exec[2];  // iteration reading pbuf[k]
+    cudaGraphExec_t fused_exec[2];  // fused-tail iteration reading pbuf[k] (a12 fusion)
+    long long fused_kernels;
     long long uzawa_kernels;
     struct Dist *dist;  // non-null: a 2D-decomposed handle (all calls dispatch to dist_*)
 };
@@ -92,7 +94,8 @@ RhsArgs rhs_arrays(const double *bx, const double *by);
 RhsArgs rhs_fine(stokes_s *h);
 void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&oy, const RhsArgs &rhs, int n,
             bool zero_in);
-void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in);
+void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in,
+            int done_pre = 0);
 int sync(stokes_s *h);
 int build_hierarchy(stokes_s *h);
 void drop_graphs(stokes_s *h);

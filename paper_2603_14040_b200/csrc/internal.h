@@ -89,6 +89,11 @@ void launch_jacobi_stream(const LaunchCtx &c, const GridL &g, const double *etab
 void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
                             const double *vx, const double *vy, const RhsArgs &rhs, double *rx, double *ry);
 // fused Uzawa pressure step + energy residual; partials = 3 per CTA (Sv, Sp, sum p')
+// last Uzawa step fused into the next V-cycle's first Jacobi sweep (3 partials per CTA)
+void launch_jacobi_uzawa(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                         const double *vxi, const double *vyi, double *vxo, double *vyo, const double *pin,
+                         double *pout, const double *rho, double gx, double gy, double alpha_signed,
+                         const double *mshift, double omega, double *partials);
 // pout == nullptr: energy only (p' = pin - *mshift is not stored)
 void launch_uzawa_energy(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
                          const double *vx, const double *vy, const double *pin, double *pout, const double *rho,

@@ -269,6 +269,58 @@ struct PrecondApplyOp {
     }
 };
 
+// The last Uzawa step fused into the first pre-smoothing sweep of the next V-cycle
+// (SURVEY §8(a) a12): from v^k and p^(k-1) one pass computes
+//   p^k = (p^(k-1) - mshift) + alpha_s eta_P (-D v^k)                 (a10, reading R3)
+//   r_v = f - L v^k - G p^k,  r_p = -D v^k -> partial sums of E(v^k, p^k) (a3)
+//   v' = v^k + omega r_v / a_ii                                          (a4, first sweep)
+// (p^k at the east / south neighbours recomputed on the window).  If E(v^k, p^k) <= rtol
+// the sweep's output is discarded and (v^k, p^k) returned: the iterates are unchanged.
+struct JacobiUzawaOp {
+    static constexpr bool WS = false;
+    static constexpr int NF = 6;
+    static constexpr int NRED = 3;
+    const double *src[6];  // vx, vy, eta_p, eta_b, p^(k-1), rho
+    double *vxo, *vyo, *po;
+    const double *mshift;
+    double alpha_s, omega, gx, gy;
+    __device__ __forceinline__ double divB(const GridL &g, const Win &w, int dc) const {
+        return (w.B(F_VX, dc) - w.B(F_VX, dc - 1)) * g.idx + (w.B(F_VY, dc) - w.A(F_VY, dc)) * g.idy;
+    }
+    __device__ __forceinline__ void row(const GridL &g, const Win &w, int i, int j, double *acc) const {
+        const size_t P = g.P;
+        const double ms = *mshift;
+        const double dv = divB(g, w, 0);
+        const double pn = (w.B(F_4) - ms) + alpha_s * w.B(F_EP) * (-dv);
+        po[(size_t)i * P + j] = pn;
+        acc[1] += dv * dv * (w.B(F_EP) / (2.0 * g.idx2 + 2.0 * g.idy2));
+        acc[2] += pn;
+        if (j <= g.nvxj) {
+            const double pe = (w.B(F_4, 1) - ms) + alpha_s * w.B(F_EP, 1) * (-divB(g, w, 1));
+            const RowX x = lx_win(g, w, i);
+            const double r = fx_win(w, gx) - (pn - pe) * g.idx - x.L;
+            const double ia = rcp(x.a);
+            acc[0] -= r * r * ia;
+            const double vn = w.B(F_VX) + omega * r * ia;
+            vxo[(size_t)i * P + j] = vn;
+            if (i == 1 && g.bN) vxo[j] = g.sN * vn;
+            if (i == g.ncy && g.bS) vxo[(size_t)(g.ncy + 1) * P + j] = g.sS * vn;
+        }
+        if (i <= g.nvyi) {
+            const double ds = (w.C(F_VX) - w.C(F_VX, -1)) * g.idx + (w.C(F_VY) - w.B(F_VY)) * g.idy;
+            const double ps = (w.C(F_4) - ms) + alpha_s * w.C(F_EP) * (-ds);
+            const RowX y = ly_win(g, w, j);
+            const double r = fy_win(w, gy) - (pn - ps) * g.idy - y.L;
+            const double ia = rcp(y.a);
+            acc[0] -= r * r * ia;
+            const double vn = w.B(F_VY) + omega * r * ia;
+            vyo[(size_t)i * P + j] = vn;
+            if (j == 1 && g.bW) vyo[(size_t)i * P] = g.sW * vn;
+            if (j == g.ncx && g.bE) vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
+        }
+    }
+};
+
 // Warp-specialised engine: warps 0..7 compute (one column per thread), warp 8 is the TMA
 // producer.  Slot s has a FULL mbarrier (producer arrive.expect_tx + TMA complete_tx) and
 // an EMPTY mbarrier (one arrive per compute warp once it has pulled the row into its
@@ -543,6 +595,23 @@ void launch_precond_apply(const LaunchCtx &c, const GridL &g, const double *etab
     op.rx = rx;
     op.ry = ry;
     op.alpha = alpha;
+    run(c, g, op, partials);
+}
+
+void launch_jacobi_uzawa(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                         const double *vxi, const double *vyi, double *vxo, double *vyo, const double *pin,
+                         double *pout, const double *rho, double gx, double gy, double alpha_signed,
+                         const double *mshift, double omega, double *partials) {
+    JacobiUzawaOp op;
+    fill_src(op.src, vxi, vyi, etap, etab, pin, rho);
+    op.vxo = vxo;
+    op.vyo = vyo;
+    op.po = pout;
+    op.mshift = mshift;
+    op.alpha_s = alpha_signed;
+    op.omega = omega;
+    op.gx = gx;
+    op.gy = gy;
     run(c, g, op, partials);
 }
 

@@ -339,7 +339,8 @@ class Stokes:
         _check(lib().stokes_launch_count(self._h, ctypes.byref(c), int(reset)), "launch_count")
         return c.value
 
-    KERNELS = {"jacobi": 0, "energy": 1, "residual_restrict": 2, "prolong": 3, "pupdate": 4, "rbgs": 5}
+    KERNELS = {"jacobi": 0, "energy": 1, "residual_restrict": 2, "prolong": 3, "pupdate": 4, "rbgs": 5,
+               "jacobi_uzawa": 6}
 
     def time_kernel(self, kernel, reps=20):
         ms, nb = ctypes.c_double(), ctypes.c_double()

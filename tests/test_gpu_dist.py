@@ -65,7 +65,10 @@ def test_virtual_decomposition_is_exact(px, py, name, smoother, transport):
         assert rel(b2[k], a2[k]) <= 1e-11, (k, rel(b2[k], a2[k]))
     _, _, _, e1 = one.residual(a["vx"], a["vy"], a["p"])
     _, _, _, e2 = dd.residual(a["vx"], a["vy"], a["p"])
-    assert abs(e1 - e2) <= 1e-12 * max(e1, 1e-300)
+    # E is a squared residual norm: at a converged state each residual entry is a cancellation
+    # of stencil terms ~ eta_max |v| / h^2 ~ n^2 * contrast * |f| (1e3 * 128^2 here), so the two
+    # kernels' (stream vs 2D-block) rounding may differ by ~eps * 1.6e7 ~ 4e-9 in sqrt(E) units
+    assert abs(np.sqrt(e1) - np.sqrt(e2)) <= 1e-8, (e1, e2)
 
 
 def test_loopback_large_tiles_stream_path():

@@ -172,6 +172,22 @@ def test_solve_parity(S, name, n, opts):
         assert rel(b3[key], a3[key]) <= 1e-9, key
 
 
+@pytest.mark.parametrize("k", [1, 2, 3, 7])
+@pytest.mark.parametrize("nx,ny", [(128, 32), (160, 136), (256, 64)])
+def test_fused_uzawa_fixed_iterations(S, nx, ny, k):
+    """Fine grids >= 128 x 8 run the Uzawa update fused into the next V-cycle's first sweep
+    (a12); a fixed number of iterations must still give the oracle's (v^k, p^k, E^k)."""
+    w = workload("layered", nx, ny)
+    o, s = pair(S, nx, ny, w["bc"], w, w["Lx"], w["Ly"], (w["gx"], w["gy"]), omega_v=0.6, alpha_p=1.0,
+                max_iter=k)
+    a = o.solve(0.0)
+    b = s.solve(0.0)
+    assert a["iters"] == b["iters"] == k
+    assert abs(a["E"] - b["E"]) <= 1e-9 * a["E"]
+    for key in ("vx", "vy", "p"):
+        assert rel(b[key], a[key]) <= 1e-10, key
+
+
 def test_error_paths(S):
     from paper_2603_14040_b200 import StokesError
     with pytest.raises(StokesError):

@@ -18,9 +18,10 @@ N > 1   (torchrun): weak scaling, one 4096^2 tile per GPU of a px x py global gr
 e2e     the same solve through the public API (Stokes.set_viscosity / set_density / solve)
         with pinned HOST inputs and outputs: H2D of eta_b, eta_p, rho_b and D2H of vx, vy, p
         inside the timed region.
-roofline the fine-level Jacobi sweep (the hot loop): algorithmic bytes
-        per launch (64 B/cell) / its CUDA-event time (stokes_time_kernel on the
-        handle's stream, live in this run) vs the measured HBM copy peak.
+roofline the dominant kernel, the fine-level two-sweep Jacobi pass (the smoother, PAPER.md:
+        2396/3209, two sweeps per HBM pass): algorithmic bytes per launch (64 B/cell, DESIGN.md
+        §6) / its CUDA-event time (stokes_time_kernel on the handle's stream, live in this run)
+        vs the measured HBM copy peak; the other fine-level kernels listed beside it.
 --impl reference: the CPU oracle (oracle/, plain C, 1 thread) on the same workload,
         each step one Uzawa iteration of the full-size problem (bounded sample).
 """
@@ -115,9 +116,23 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel_bytes_key):
-    """DRAM bytes per launch of the Jacobi sweep from the committed ncu --set full summary."""
-    path = os.path.join(ROOT, "profiles", "ncu_jacobi_traffic.json")
+def fine_launches(nu, fused):
+    """Fine-level launches per V-cycle (driver.cu vcycle / smooth): the Uzawa update fused into
+    the first pre-sweep (Uzawa mode), sweep pairs as two-sweep passes with an even pair count."""
+    pre_n = nu - (1 if fused else 0)
+    pre, post = pre_n // 2, nu // 2
+    if (pre + post) % 2:
+        if post > 0:
+            post -= 1
+        else:
+            pre -= 1
+    return {"jacobi2": pre + post, "jacobi": pre_n - 2 * pre + nu - 2 * post, "jacobi_uzawa": 1 if fused else 0,
+            "residual_restrict": 1, "prolong": 1}
+
+
+def ncu_traffic(kernel_bytes_key, name="ncu_jacobi2_traffic.json"):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", name)
     try:
         d = json.load(open(path))
         return d.get(kernel_bytes_key)
@@ -313,19 +328,33 @@ def run_ours(args, world, rank, local):
     e2_t = allreduce_max(sum(e2), world, dev)
     e2e_value = e2_iters * vpi * per_vc / e2_t
 
-    # ---- roofline of the dominant kernel (fine Jacobi sweep), live CUDA events, on a
-    # single-domain handle of this GPU's tile
+    # ---- roofline of the dominant kernel (the fine-level two-sweep Jacobi pass), live CUDA
+    # events, on a single-domain handle of this GPU's tile; the other fine-level kernels of
+    # the step beside it
     kh = s if world == 1 else Stokes(nx, ny, 1.0, 1.0, w["bc"], **opts)
     if world > 1:
         kh.set_viscosity(eb, ep)
         kh.set_density(rho)
         kh.set_gravity(w["gx"], w["gy"])
-    k_ms, k_bytes = kh.time_kernel("jacobi", reps=20)
     peak, peak_src = measured_peak()
-    achieved = k_bytes / (k_ms / 1e3) / 1e9
-    sweeps_per_solve = statistics.mean(iters) * vpi * 2 * shp[0][2]
-    share = sweeps_per_solve * k_ms / (ms / args.steps)
-    tr = ncu_traffic("dram_bytes_per_launch")
+    counts = fine_launches(shp[0][2], opts.get("accel", 0) == 0 and vpi == 1)
+    its = statistics.mean(iters)
+    kernels = {}
+    for name in ("jacobi2", "jacobi", "jacobi_uzawa", "residual_restrict", "prolong"):
+        try:
+            km, kb = kh.time_kernel(name, reps=20)
+        except Exception:
+            continue
+        n_per = its * vpi * counts.get(name, 0)
+        kernels[name] = {"launch_ms": km, "GBs": kb / (km / 1e3) / 1e9, "frac": kb / (km / 1e3) / 1e9 / peak,
+                         "launches_per_solve": n_per, "share_of_step": n_per * km / (ms / args.steps)}
+    dom = "jacobi2" if "jacobi2" in kernels else "jacobi"
+    k_ms = kernels[dom]["launch_ms"]
+    k_bytes = kernels[dom]["GBs"] * 1e9 * k_ms / 1e3
+    achieved = kernels[dom]["GBs"]
+    share = kernels[dom]["share_of_step"]
+    tr = ncu_traffic("dram_bytes_per_launch") if dom == "jacobi2" else ncu_traffic(
+        "dram_bytes_per_launch", "ncu_jacobi_traffic.json")
 
     if rank != 0:
         return 0
@@ -340,10 +369,11 @@ def run_ours(args, world, rank, local):
                    "dof_sweeps_per_solve": dofs / args.steps,
                    "l2": "inputs larger than L2 (fine fields 16.8M cells x 8 B per GPU, hierarchy > 1 GB vs 126 MB L2)",
                    "parallelism": f"dd{px}x{py}" if world > 1 else "single GPU"},
-        "roofline": {"kernel": "fine-level damped-Jacobi sweep (k_stream<JacobiOp>)", "bound": "hbm",
+        "roofline": {"kernel": ("fine-level two-sweep damped-Jacobi pass (k_jacobi2)" if dom == "jacobi2" else
+                                "fine-level damped-Jacobi sweep (k_stream<JacobiOp>)"), "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": tr,
                      "algorithmic_bytes_per_launch": k_bytes, "launch_ms": k_ms, "peak_source": peak_src,
-                     "share_of_step": share},
+                     "share_of_step": share, "fine_kernels": kernels},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
                 "seconds_per_step": e2_t / len(e2)},
         "gpu_launches": launches,

@@ -192,8 +192,8 @@ int stokes_launch_count(stokes_t h, long long *count, int reset);
  * = algorithmic bytes one launch moves.  kernel: 0 fine Jacobi sweep
  * (Uzawa RHS), 1 fine residual+energy, 2 fine residual+restriction, 3 prolongation,
  * 4 pressure update (fused with the energy residual), 5 RBGS sweep (4 phases), 6 pressure
- * update + energy residual + first Jacobi sweep of the next V-cycle (fine grid >= 128 x 8 only,
- * else STOKES_EINVAL).  Uses the
+ * update + energy residual + first Jacobi sweep of the next V-cycle, 7 two Jacobi sweeps in
+ * one pass (6 and 7: fine grid >= 128 x 8 only, else STOKES_EINVAL).  Uses the
  * handle's current fields. */
 int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double *bytes);
 

@@ -152,8 +152,14 @@ RhsArgs rhs_fine(stokes_s *h) {
 
 // nsweeps of the smoother on level l for L v = b.  (cur) holds v; Jacobi ping-pongs
 // between cur and the other buffer: on return cur points at the result.
+// Pairs of sweeps run as one two-sweep pass (launch_jacobi2) where the level allows it, at
+// most max_pairs of them (each pair saves one buffer swap: vcycle keeps its count even).
+int jacobi_pairs(stokes_s *h, int l, int n, bool zero_in) {
+    if (h->o.smoother != STOKES_SMOOTH_JACOBI || !jacobi2_ok(h->lev[l].g)) return 0;
+    return (n - (zero_in ? 1 : 0)) / 2 > 0 ? (n - (zero_in ? 1 : 0)) / 2 : 0;
+}
 void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&oy, const RhsArgs &rhs, int n,
-            bool zero_in) {
+            bool zero_in, int max_pairs) {
     Level &L = h->lev[l];
     const LaunchCtx c = ctx(h);
     if (n <= 0) {
@@ -164,8 +170,17 @@ void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&
         return;
     }
     if (h->o.smoother == STOKES_SMOOTH_JACOBI) {
-        for (int s = 0; s < n; ++s) {
-            launch_jacobi(c, L.g, L.etab, L.etap, cx, cy, ox, oy, rhs, h->o.omega_v, zero_in && s == 0);
+        int pairs = jacobi_pairs(h, l, n, zero_in);
+        if (pairs > max_pairs) pairs = max_pairs;
+        for (int s = 0; s < n;) {
+            if (pairs > 0 && !(zero_in && s == 0)) {
+                launch_jacobi2(c, L.g, L.etab, L.etap, cx, cy, ox, oy, rhs, h->o.omega_v);
+                --pairs;
+                s += 2;
+            } else {
+                launch_jacobi(c, L.g, L.etab, L.etap, cx, cy, ox, oy, rhs, h->o.omega_v, zero_in && s == 0);
+                s += 1;
+            }
             double *t = cx; cx = ox; ox = t;
             t = cy; cy = oy; oy = t;
         }
@@ -199,8 +214,8 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
             }
             launch_coarse_solve(c, L.g, h->Minv, bx, by, ax, ay);
         } else {
-            smooth(h, l, cx, cy, ox, oy, rhs, 2 * L.nu, zero_in);
-            if (cx != ax) {  // odd count cannot happen (2 nu), kept for safety
+            smooth(h, l, cx, cy, ox, oy, rhs, 2 * L.nu, zero_in, jacobi_pairs(h, l, 2 * L.nu, zero_in) & ~1);
+            if (cx != ax) {  // an even number of buffer swaps (2 nu sweeps, even pair count)
                 cudaMemcpyAsync(ax - COL_OFF, cx - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
                 cudaMemcpyAsync(ay - COL_OFF, cy - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
             }
@@ -208,12 +223,21 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
         return;
     }
     Level &C = h->lev[l + 1];
-    smooth(h, l, cx, cy, ox, oy, rhs, L.nu - done_pre, zero_in && !done_pre);  // (1) pre-smoothing
+    // each two-sweep pass saves one buffer swap: keep the pair count even so that the
+    // 2 nu sweeps of the cycle end in (ax, ay) without a copy
+    const int pre_n = L.nu - done_pre;
+    int pre_pairs = jacobi_pairs(h, l, pre_n, zero_in && !done_pre);
+    int post_pairs = jacobi_pairs(h, l, L.nu, false);
+    if ((pre_pairs + post_pairs) & 1) {
+        if (post_pairs > 0) --post_pairs;
+        else --pre_pairs;
+    }
+    smooth(h, l, cx, cy, ox, oy, rhs, pre_n, zero_in && !done_pre, pre_pairs);  // (1) pre-smoothing
     launch_residual(c, L.g, L.etab, L.etap, cx, cy, rhs, L.rx, L.ry);          // (2) residual
     launch_restrict_vel(c, L.g, C.g, L.rx, L.ry, C.bx, C.by);                 // (3) restriction
     vcycle(h, l + 1, C.vx[0], C.vy[0], C.vx[1], C.vy[1], rhs_arrays(C.bx, C.by), true);  // (4)
     launch_prolong(c, L.g, C.g, C.vx[0], C.vy[0], cx, cy);                    // (5) correction
-    smooth(h, l, cx, cy, ox, oy, rhs, L.nu, false);                          // (6) post-smoothing
+    smooth(h, l, cx, cy, ox, oy, rhs, L.nu, false, post_pairs);              // (6) post-smoothing
     if (cx != ax) {
         cudaMemcpyAsync(ax - COL_OFF, cx - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
         cudaMemcpyAsync(ay - COL_OFF, cy - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
@@ -878,7 +902,7 @@ int stokes_smooth(stokes_t h, int level, const double *bx, const double *by, dou
     launch_in_vy_raw(c, L.g, by, L.by);
     launch_in_velocity(c, L.g, vx, vy, L.vx[0], L.vy[0]);
     double *cx = L.vx[0], *cy = L.vy[0], *ox = L.vx[1], *oy = L.vy[1];
-    smooth(h, level, cx, cy, ox, oy, rhs_arrays(L.bx, L.by), nsweeps, false);
+    smooth(h, level, cx, cy, ox, oy, rhs_arrays(L.bx, L.by), nsweeps, false, nsweeps);
     launch_out_vx(c, L.g, cx, vx);
     launch_out_vy(c, L.g, cy, vy);
     return sync(h);
@@ -1000,6 +1024,7 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
                                h->scal + S_ZERO, h->partials);
             break;
         case 5: launch_rbgs(c, g, F.etab, F.etap, F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v); break;
+        case 7: launch_jacobi2(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v); break;
         default:
             launch_jacobi_uzawa(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], h->pbuf[h->pcur],
                                 h->pbuf[1 - h->pcur], h->rho, h->gx, h->gy, h->o.alpha_p, h->scal + S_ZERO,
@@ -1011,10 +1036,11 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
     // 0 Jacobi: read vx,vy,eta_p,eta_b,p,rho + write vx,vy; 1 energy: read 6; 2 residual (read 6,
     // write 2) + restriction (read 2 fine, write 1/2); 3 prolongation (read/write 2 + 1/2 coarse);
     // 4 fused Uzawa pressure step + energy: read 6, write p; 5 RBGS (4 phases, fused bytes);
-    // 6 Uzawa step + energy + first Jacobi sweep of the next V-cycle: read 6, write p, vx, vy
-    const double per_cell[7] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0, 72.0};
-    if (kernel < 0 || kernel > 6) return STOKES_EINVAL;
-    if (kernel == 6 && !stream_ok(g)) return STOKES_EINVAL;
+    // 6 Uzawa step + energy + first Jacobi sweep of the next V-cycle: read 6, write p, vx, vy;
+    // 7 two Jacobi sweeps in one pass: read 6, write 2
+    const double per_cell[8] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0, 72.0, 64.0};
+    if (kernel < 0 || kernel > 7) return STOKES_EINVAL;
+    if ((kernel == 6 && !stream_ok(g)) || (kernel == 7 && !jacobi2_ok(g))) return STOKES_EINVAL;
     *bytes = per_cell[kernel] * cells;
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));

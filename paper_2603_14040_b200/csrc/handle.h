@@ -93,7 +93,8 @@ LaunchCtx ctx(stokes_s *h);
 RhsArgs rhs_arrays(const double *bx, const double *by);
 RhsArgs rhs_fine(stokes_s *h);
 void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&oy, const RhsArgs &rhs, int n,
-            bool zero_in);
+            bool zero_in, int max_pairs = 0);
+int jacobi_pairs(stokes_s *h, int l, int n, bool zero_in);
 void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in,
             int done_pre = 0);
 int sync(stokes_s *h);

@@ -89,6 +89,10 @@ void launch_jacobi_stream(const LaunchCtx &c, const GridL &g, const double *etab
 void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
                             const double *vx, const double *vy, const RhsArgs &rhs, double *rx, double *ry);
 // fused Uzawa pressure step + energy residual; partials = 3 per CTA (Sv, Sp, sum p')
+// two Jacobi sweeps in one pass (single-domain levels with jacobi2_ok)
+bool jacobi2_ok(const GridL &g);
+void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
+                    const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega);
 // last Uzawa step fused into the next V-cycle's first Jacobi sweep (3 partials per CTA)
 void launch_jacobi_uzawa(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
                          const double *vxi, const double *vyi, double *vxo, double *vyo, const double *pin,

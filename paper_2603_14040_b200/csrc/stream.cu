@@ -17,6 +17,8 @@
 // Stencil coefficients are those of kernels.cu (Listing vx_op_point).
 #include <math.h>
 
+#include <type_traits>
+
 #include "internal.h"
 
 namespace {
@@ -66,6 +68,14 @@ struct Win {
     __device__ __forceinline__ double B(int k, int dc = 0) const { return dc < 0 ? f[k].B.l : (dc > 0 ? f[k].B.r : f[k].B.c); }
     __device__ __forceinline__ double C(int k, int dc = 0) const { return dc < 0 ? f[k].C.l : (dc > 0 ? f[k].C.r : f[k].C.c); }
     template <int NFU>
+    __device__ __forceinline__ void shift() {  // advance one row with no new data (C stale)
+#pragma unroll
+        for (int k = 0; k < NFU; ++k) {
+            f[k].A = f[k].B;
+            f[k].B = f[k].C;
+        }
+    }
+    template <int NFU>
     __device__ __forceinline__ void push(const double *slot, int t) {  // t = column offset in the segment
 #pragma unroll
         for (int k = 0; k < NFU; ++k) {
@@ -96,7 +106,8 @@ struct RowX {
 // Written as coefficient x (neighbour - centre) differences (the stress form of
 // PAPER.md:643-661): the same operator as the Listing's coefficients with ~20% fewer
 // FP64 operations and shorter dependency chains; a_ii is formed separately.
-__device__ __forceinline__ RowX lx_win(const GridL &g, const Win &w, int i) {
+template <bool EDGE = true, class W>  // EDGE = false: row i is no N/S boundary row
+__device__ __forceinline__ RowX lx_win(const GridL &g, const W &w, int i) {
     const double eta1 = w.A(F_EB), eta2 = w.B(F_EB), etaA = w.B(F_EP), etaB = w.B(F_EP, 1);
     const double vc = w.B(F_VX);
     RowX r;
@@ -104,11 +115,12 @@ __device__ __forceinline__ RowX lx_win(const GridL &g, const Win &w, int i) {
           g.idy2 * (eta1 * (w.A(F_VX) - vc) + eta2 * (w.C(F_VX) - vc)) +
           g.idxdy * (eta1 * (w.A(F_VY) - w.A(F_VY, 1)) + eta2 * (w.B(F_VY, 1) - w.B(F_VY)));
     r.a = -(eta1 + eta2) * g.idy2 - (etaA + etaB) * g.idx2x2;
-    if (i == 1 && g.bN) r.a += g.sN * eta1 * g.idy2;
-    if (i == g.ncy && g.bS) r.a += g.sS * eta2 * g.idy2;
+    if (EDGE && i == 1 && g.bN) r.a += g.sN * eta1 * g.idy2;
+    if (EDGE && i == g.ncy && g.bS) r.a += g.sS * eta2 * g.idy2;
     return r;
 }
-__device__ __forceinline__ RowX ly_win(const GridL &g, const Win &w, int j) {
+template <bool EDGE = true, class W>  // EDGE = false: column j is no W/E boundary column
+__device__ __forceinline__ RowX ly_win(const GridL &g, const W &w, int j) {
     const double etaN = w.B(F_EP), etaS = w.C(F_EP), etaW = w.B(F_EB, -1), etaE = w.B(F_EB);
     const double vc = w.B(F_VY);
     RowX r;
@@ -116,15 +128,17 @@ __device__ __forceinline__ RowX ly_win(const GridL &g, const Win &w, int j) {
           g.idx2 * (etaE * (w.B(F_VY, 1) - vc) + etaW * (w.B(F_VY, -1) - vc)) +
           g.idxdy * (etaE * (w.C(F_VX) - w.B(F_VX)) - etaW * (w.C(F_VX, -1) - w.B(F_VX, -1)));
     r.a = -(etaN + etaS) * g.idy2x2 - (etaW + etaE) * g.idx2;
-    if (j == 1 && g.bW) r.a += g.sW * etaW * g.idx2;
-    if (j == g.ncx && g.bE) r.a += g.sE * etaE * g.idx2;
+    if (EDGE && j == 1 && g.bW) r.a += g.sW * etaW * g.idx2;
+    if (EDGE && j == g.ncx && g.bE) r.a += g.sE * etaE * g.idx2;
     return r;
 }
 // body force (reading R4/R23) at vx / vy nodes from the staged rho rows
-__device__ __forceinline__ double fx_win(const Win &w, double gx) {
+template <class W>
+__device__ __forceinline__ double fx_win(const W &w, double gx) {
     return gx != 0.0 ? -gx * (0.5 * (w.A(F_5) + w.B(F_5))) : 0.0;
 }
-__device__ __forceinline__ double fy_win(const Win &w, double gy) {
+template <class W>
+__device__ __forceinline__ double fy_win(const W &w, double gy) {
     return gy != 0.0 ? -gy * (0.5 * (w.B(F_5, -1) + w.B(F_5))) : 0.0;
 }
 
@@ -523,12 +537,248 @@ void fill_src(const double **src, const double *vx, const double *vy, const doub
     src[5] = f5;
 }
 
+// ---- two damped-Jacobi sweeps in one HBM pass (temporal blocking of a4) -----------------
+// Sweep 1 runs one row ahead of sweep 2 on a CTA that owns tw (<= TW - 2) output columns
+// j0 .. j0+tw-1: thread t evaluates sweep 1 at column j0-1+t (one redundant column on each
+// side), parks (vx', vy') of the last four rows in shared memory, and sweep 2 of row i-1
+// reads them back with its column neighbours (one CTA barrier per row).  Strips overlap
+// by one sweep-1 row.  The fields are read once and written once per two sweeps: the same
+// 64 B/cell as one sweep.  Mirror ghosts of the intermediate iterate are applied when
+// sweep 2 reads them, walls are copied through: exactly the arithmetic of two JacobiOp
+// sweeps.  Single-domain levels only (a decomposed tile's halo would be stale after the
+// first sweep).  (A warp-specialised variant exchanging the intermediate iterate by warp
+// shuffles, without CTA barriers, measured 435 us vs 340 us for this one at 4096^2.)
+constexpr int NS2 = 6;  // landing ring depth
+constexpr int SMEM2 = NS2 * NF * RW * 8 + 4 * 2 * TW * 8 + NS2 * 8;
+
+struct J2Args {
+    const double *src[6];  // vx, vy, eta_p, eta_b, p | bx, rho | by
+    double *vxo, *vyo;
+    double omega, gx, gy;
+    int tw;  // output columns per CTA (even, <= TW - 2)
+};
+
+// Register window with a static rotation: row r of the strip lives in slot (r - sfirst) % 3
+// and the row loop is unrolled by three, so advancing the window moves no registers.
+struct RowV {
+    R3 f[NF];
+};
+__device__ __forceinline__ double pick(const R3 &x, int dc) { return dc < 0 ? x.l : (dc > 0 ? x.r : x.c); }
+template <int KA, int KB, int KC>
+struct WinV {  // sweep-1 view: A, B, C = slots KA, KB, KC
+    const RowV *r;
+    __device__ __forceinline__ double A(int k, int dc = 0) const { return pick(r[KA].f[k], dc); }
+    __device__ __forceinline__ double B(int k, int dc = 0) const { return pick(r[KB].f[k], dc); }
+    __device__ __forceinline__ double C(int k, int dc = 0) const { return pick(r[KC].f[k], dc); }
+};
+template <int KB, int KC>
+struct WinS2 {  // sweep-2 view: velocities from the intermediate rows, the rest one row back
+    const RowV *r;
+    R3 vx[3], vy[3];
+    double lag_eb, lag_5;  // eta_b, f5 of the row above B (already overwritten in the slots)
+    __device__ __forceinline__ double A(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[0], dc) : k == F_VY ? pick(vy[0], dc) : k == F_EB ? lag_eb : lag_5;
+    }
+    __device__ __forceinline__ double B(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[1], dc) : k == F_VY ? pick(vy[1], dc) : pick(r[KB].f[k], dc);
+    }
+    __device__ __forceinline__ double C(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[2], dc) : k == F_VY ? pick(vy[2], dc) : pick(r[KC].f[k], dc);
+    }
+};
+template <int K>
+struct Slot {
+    static constexpr int v = K;
+};
+template <int MODE>
+__global__ void __launch_bounds__(TW, MINB) k_jacobi2(GridL g, J2Args a, int H) {
+    extern __shared__ __align__(128) double sm[];
+    double *s1 = sm + NS2 * NF * RW;  // [4 rows][vx', vy'][TW]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s1 + 4 * 2 * TW);
+    const int t = threadIdx.x;
+    const int j0 = 1 + a.tw * blockIdx.x;
+    const int c = j0 - 1 + t;  // sweep-1 column of this thread (= sweep-2 column for 1 <= t <= tw)
+    const int i0 = 1 + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, g.ncy);
+    const int rlo = max(i0 - 2, 0), rhi = min(i1 + 2, g.ncy + 1);
+    const int sfirst = max(i0 - 1, 0), slast = min(i1 + 1, g.ncy + 1);
+    const size_t P = g.P;
+    auto issue = [&](int r) {
+        const int slot = (r - rlo) % NS2;
+        uint64_t *bar = bars + slot;
+        mbar_expect_tx(bar, NF * RW * 8);
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            bulk_g2s(sm + (slot * NF + f) * RW, a.src[f] + (size_t)r * P + (j0 - 2), RW * 8, bar);
+    };
+    if (t == 0) {
+        for (int k = 0; k < NS2; ++k) mbar_init(bars + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0)
+        for (int r = rlo; r < rlo + NS2 && r <= rhi; ++r) issue(r);
+    RowV rows[3];
+    auto load = [&](auto slot, int r) {  // wait for staged row r, pull it into register slot
+        constexpr int K = decltype(slot)::v;
+        const int rel = r - rlo;
+        mbar_wait(bars + rel % NS2, (rel / NS2) & 1);
+        const double *src = sm + (rel % NS2) * NF * RW + t + 1;
+#pragma unroll
+        for (int k = 0; k < NF; ++k) rows[K].f[k] = R3{src[k * RW - 1], src[k * RW], src[k * RW + 1]};
+    };
+    auto refill = [&](int r) {  // every thread has pulled row r: its slot takes row r + NS2
+        if (t == 0 && r + NS2 <= rhi) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(r + NS2);
+        }
+    };
+    if (rlo < sfirst) load(Slot<2>(), rlo);
+    load(Slot<0>(), sfirst);
+    __syncthreads();
+    for (int r = rlo; r <= sfirst; ++r) refill(r);
+    const bool cx_in = c >= 1 && c <= g.nvxj, cy_in = c >= 1 && c <= g.ncx;
+    // 1/a_ii and the right-hand side b at sweep-1 row s-1 (= the sweep-2 row): same for both sweeps
+    double iax = 0.0, iay = 0.0;
+    // one row step; row s in slot K, s-1 in (K+2)%3, s+1 loaded into (K+1)%3.  EDGE = false
+    // (CTAs whose rows and columns all stay off the boundary): no boundary logic at all.
+    auto step = [&](auto slot, auto edge, int s) -> bool {
+        constexpr int K = decltype(slot)::v, KA = (K + 2) % 3, KC = (K + 1) % 3;
+        constexpr bool EDGE = decltype(edge)::value;
+        if (s > slast) return true;
+        const double lag_eb = rows[KC].f[F_EB].c, lag_5 = rows[KC].f[F_5].c;  // row s-2
+        if (s + 1 <= rhi) load(Slot<KC>(), s + 1);
+        const WinV<KA, K, KC> w{rows};
+        // ---- sweep 1, row s
+        double vx1 = w.B(F_VX), vy1 = w.B(F_VY), iax_n = 0.0, iay_n = 0.0;
+        if (!EDGE || (s >= 1 && s <= g.ncy && cx_in)) {
+            const RowX x = lx_win<EDGE>(g, w, s);
+            const double b = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
+            iax_n = rcp(x.a);
+            vx1 = w.B(F_VX) + a.omega * (b - x.L) * iax_n;
+        }
+        if (!EDGE || (s >= 1 && s <= g.nvyi && cy_in)) {
+            const RowX y = ly_win<EDGE>(g, w, c);
+            const double b = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
+            iay_n = rcp(y.a);
+            vy1 = w.B(F_VY) + a.omega * (b - y.L) * iay_n;
+        }
+        s1[((s & 3) * 2 + 0) * TW + t] = vx1;
+        s1[((s & 3) * 2 + 1) * TW + t] = vy1;
+        __syncthreads();
+        if (s + 1 <= rhi) refill(s + 1);
+        // ---- sweep 2, row i = s-1 on the intermediate iterate
+        const int i = s - 1;
+        if (i >= i0 && i <= i1 && t >= 1 && t <= a.tw && (!EDGE || c <= g.ncx)) {
+            const double *qa = s1 + (((s - 2) & 3) * 2) * TW + t, *qb = s1 + (((s - 1) & 3) * 2) * TW + t,
+                         *qc = s1 + ((s & 3) * 2) * TW + t;
+            WinS2<KA, K> u;
+            u.r = rows;
+            u.lag_eb = lag_eb;
+            u.lag_5 = lag_5;
+            u.vx[0] = R3{0.0, qa[0], 0.0};
+            u.vx[1] = R3{qb[-1], qb[0], qb[1]};
+            u.vx[2] = R3{qc[-1], qc[0], 0.0};
+            u.vy[0] = R3{0.0, qa[TW], qa[TW + 1]};
+            u.vy[1] = R3{qb[TW - 1], qb[TW], qb[TW + 1]};
+            u.vy[2] = R3{0.0, qc[TW], 0.0};
+            if (EDGE && i == 1 && g.bN) u.vx[0].c = g.sN * u.vx[1].c;
+            if (EDGE && i == g.ncy && g.bS) u.vx[2].c = g.sS * u.vx[1].c;
+            if (EDGE && c == 1 && g.bW) u.vy[1].l = g.sW * u.vy[1].c;
+            if (EDGE && c == g.ncx && g.bE) u.vy[1].r = g.sE * u.vy[1].c;
+            if (!EDGE || c <= g.nvxj) {
+                const RowX x = lx_win<EDGE>(g, u, i);
+                const double b = (MODE == RHS_FINE) ? fx_win(u, a.gx) - (u.B(F_4) - u.B(F_4, 1)) * g.idx : u.B(F_4);
+                const double vn = u.B(F_VX) + a.omega * (b - x.L) * iax;
+                a.vxo[(size_t)i * P + c] = vn;
+                if (EDGE && i == 1 && g.bN) a.vxo[c] = g.sN * vn;
+                if (EDGE && i == g.ncy && g.bS) a.vxo[(size_t)(g.ncy + 1) * P + c] = g.sS * vn;
+            }
+            if (!EDGE || i <= g.nvyi) {
+                const RowX y = ly_win<EDGE>(g, u, c);
+                const double b = (MODE == RHS_FINE) ? fy_win(u, a.gy) - (u.B(F_4) - u.C(F_4)) * g.idy : u.B(F_5);
+                const double vn = u.B(F_VY) + a.omega * (b - y.L) * iay;
+                a.vyo[(size_t)i * P + c] = vn;
+                if (EDGE && c == 1 && g.bW) a.vyo[(size_t)i * P] = g.sW * vn;
+                if (EDGE && c == g.ncx && g.bE) a.vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
+            }
+        }
+        iax = iax_n;
+        iay = iay_n;
+        return false;
+    };
+    const bool interior = i0 >= 2 && i1 + 1 <= g.ncy - 1 && j0 >= 2 && j0 + TW - 2 <= g.ncx - 1;
+    if (interior) {
+        for (int s = sfirst;; s += 3) {
+            if (step(Slot<0>(), std::false_type(), s)) break;
+            if (step(Slot<1>(), std::false_type(), s + 1)) break;
+            if (step(Slot<2>(), std::false_type(), s + 2)) break;
+        }
+    } else {
+        for (int s = sfirst;; s += 3) {
+            if (step(Slot<0>(), std::true_type(), s)) break;
+            if (step(Slot<1>(), std::true_type(), s + 1)) break;
+            if (step(Slot<2>(), std::true_type(), s + 2)) break;
+        }
+    }
+}
+
+int j2_tw(const GridL &g) {  // output columns per CTA: even, <= TW - 2, balanced over the blocks
+    const int ncb = (g.ncx + TW - 3) / (TW - 2);
+    int tw = (g.ncx + ncb - 1) / ncb;
+    return tw + (tw & 1);
+}
+dim3 j2_grid(const GridL &g, int *H) {
+    const int tw = j2_tw(g);
+    const int ncb = (g.ncx + tw - 1) / tw;
+    int strips = slots() / ncb;
+    if (strips < 1) strips = 1;
+    int h = (g.ncy + strips - 1) / strips;
+    if (h < 4) h = 4;
+    *H = h;
+    return dim3(ncb, (g.ncy + h - 1) / h);
+}
+
 }  // namespace
 
 bool stream_ok(const GridL &g) { return g.ncx >= TW / 2 && g.ncy >= 8; }
 int stream_blocks(const GridL &g) {
     const dim3 gr = stream_grid(g);
     return (int)(gr.x * gr.y);
+}
+
+bool jacobi2_ok(const GridL &g) { return stream_ok(g) && g.bN && g.bS && g.bW && g.bE; }
+
+void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
+                    const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega) {
+    J2Args a;
+    a.vxo = vxo;
+    a.vyo = vyo;
+    a.omega = omega;
+    a.tw = j2_tw(g);
+    int H = 0;
+    const dim3 grid = j2_grid(g, &H);
+    if (rhs.mode == RHS_FINE) {
+        fill_src(a.src, vxi, vyi, etap, etab, rhs.p, rhs.rho);
+        a.gx = rhs.gx;
+        a.gy = rhs.gy;
+        static bool done = false;
+        if (!done) {
+            cudaFuncSetAttribute(k_jacobi2<RHS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+            done = true;
+        }
+        k_jacobi2<RHS_FINE><<<grid, TW, SMEM2, c.stream>>>(g, a, H);
+    } else {
+        fill_src(a.src, vxi, vyi, etap, etab, rhs.bx, rhs.by);
+        a.gx = a.gy = 0.0;
+        static bool done = false;
+        if (!done) {
+            cudaFuncSetAttribute(k_jacobi2<RHS_ARRAYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+            done = true;
+        }
+        k_jacobi2<RHS_ARRAYS><<<grid, TW, SMEM2, c.stream>>>(g, a, H);
+    }
+    ++*c.counter;
 }
 
 void launch_jacobi_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,

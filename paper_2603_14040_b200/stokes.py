@@ -340,7 +340,7 @@ class Stokes:
         return c.value
 
     KERNELS = {"jacobi": 0, "energy": 1, "residual_restrict": 2, "prolong": 3, "pupdate": 4, "rbgs": 5,
-               "jacobi_uzawa": 6}
+               "jacobi_uzawa": 6, "jacobi2": 7}
 
     def time_kernel(self, kernel, reps=20):
         ms, nb = ctypes.c_double(), ctypes.c_double()

@@ -90,6 +90,24 @@ def test_smoother(S, smoother, nx, ny, bc):
         assert rel(qx[:, 1:-1], rx[:, 1:-1]) <= TOL_OP and rel(qy[1:-1], ry[1:-1]) <= TOL_OP
 
 
+@pytest.mark.parametrize("nsweeps", [2, 4, 5])
+@pytest.mark.parametrize("nx,ny", [(128, 8), (300, 250), (1030, 13)])
+@pytest.mark.parametrize("bc", BCS)
+def test_two_sweep_pass(S, nx, ny, bc, nsweeps):
+    """Levels >= 128 x 8 run sweep pairs as one temporally blocked pass (two Jacobi sweeps
+    per HBM read); ragged column tiles, 4-row strips and every mirror ghost included."""
+    f = parity_fields(nx, ny, log_contrast=1.0)
+    o, s = pair(S, nx, ny, bc, f, omega_v=0.5, coarse_min=4, coarse_direct=0)
+    rng = np.random.default_rng(11)
+    bx, by = rng.standard_normal((ny, nx + 1)), rng.standard_normal((ny + 1, nx))
+    vx, vy = rng.standard_normal((ny, nx + 1)), rng.standard_normal((ny + 1, nx))
+    vx[:, [0, -1]] = 0.0
+    vy[[0, -1], :] = 0.0
+    ex, ey = o.smooth(0, bx, by, vx, vy, nsweeps)
+    gx, gy = s.smooth(0, T(bx), T(by), T(vx), T(vy), nsweeps)
+    assert rel(gx, ex) <= TOL_OP and rel(gy, ey) <= TOL_OP
+
+
 @pytest.mark.parametrize("nx,ny", [(16, 16), (64, 32), (136, 72)])
 @pytest.mark.parametrize("bc", BCS)
 def test_transfers_and_coarse_viscosity(S, nx, ny, bc):

@@ -590,6 +590,35 @@ template <int K>
 struct Slot {
     static constexpr int v = K;
 };
+// Lazy register window: only the components each role reads are held.  Row s is pulled
+// from its landing slot twice: the 5 values sweep 1 reads as row C (step s-1) and the 14 it
+// reads as row B (step s); the 8 still needed as row A (step s+1) are carried over.  The slot
+// is released after its B pull, so rows s and s+1 stay resident.
+struct V3 {
+    R3 A[NF], B[NF], C[NF];
+    __device__ __forceinline__ double a(int k, int dc = 0) const { return pick(A[k], dc); }
+};
+struct W1 {  // sweep-1 view
+    const V3 *v;
+    __device__ __forceinline__ double A(int k, int dc = 0) const { return pick(v->A[k], dc); }
+    __device__ __forceinline__ double B(int k, int dc = 0) const { return pick(v->B[k], dc); }
+    __device__ __forceinline__ double C(int k, int dc = 0) const { return pick(v->C[k], dc); }
+};
+struct W2 {  // sweep-2 view of row s-1: velocities from the intermediate rows, eta from A/B
+    const V3 *v;
+    R3 vx[3], vy[3];
+    double lag_eb;  // eta_b of row s-2
+    __device__ __forceinline__ double A(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[0], dc) : k == F_VY ? pick(vy[0], dc) : lag_eb;
+    }
+    __device__ __forceinline__ double B(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[1], dc) : k == F_VY ? pick(vy[1], dc) : pick(v->A[k], dc);
+    }
+    __device__ __forceinline__ double C(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[2], dc) : k == F_VY ? pick(vy[2], dc) : pick(v->B[k], dc);
+    }
+};
+
 template <int MODE>
 __global__ void __launch_bounds__(TW, MINB) k_jacobi2(GridL g, J2Args a, int H) {
     extern __shared__ __align__(128) double sm[];
@@ -618,64 +647,89 @@ __global__ void __launch_bounds__(TW, MINB) k_jacobi2(GridL g, J2Args a, int H) 
     __syncthreads();
     if (t == 0)
         for (int r = rlo; r < rlo + NS2 && r <= rhi; ++r) issue(r);
-    RowV rows[3];
-    auto load = [&](auto slot, int r) {  // wait for staged row r, pull it into register slot
-        constexpr int K = decltype(slot)::v;
+    auto row_at = [&](int r) {  // wait until staged row r has landed; this thread's column in it
         const int rel = r - rlo;
         mbar_wait(bars + rel % NS2, (rel / NS2) & 1);
-        const double *src = sm + (rel % NS2) * NF * RW + t + 1;
-#pragma unroll
-        for (int k = 0; k < NF; ++k) rows[K].f[k] = R3{src[k * RW - 1], src[k * RW], src[k * RW + 1]};
+        return sm + (rel % NS2) * NF * RW + t + 1;
     };
-    auto refill = [&](int r) {  // every thread has pulled row r: its slot takes row r + NS2
+    V3 v;
+    auto pullB = [&](const double *q) {
+        v.B[F_VX] = R3{q[-1], q[0], q[1]};
+        v.B[F_VY] = R3{q[RW - 1], q[RW], q[RW + 1]};
+        v.B[F_EP].c = q[F_EP * RW];
+        v.B[F_EP].r = q[F_EP * RW + 1];
+        v.B[F_EB].l = q[F_EB * RW - 1];
+        v.B[F_EB].c = q[F_EB * RW];
+        v.B[F_4].c = q[F_4 * RW];
+        v.B[F_4].r = q[F_4 * RW + 1];
+        v.B[F_5].l = q[F_5 * RW - 1];
+        v.B[F_5].c = q[F_5 * RW];
+    };
+    auto pullC = [&](const double *q) {
+        v.C[F_VX].l = q[-1];
+        v.C[F_VX].c = q[0];
+        v.C[F_VY].c = q[RW];
+        v.C[F_EP].c = q[F_EP * RW];
+        v.C[F_4].c = q[F_4 * RW];
+    };
+    auto toA = [&]() {  // row B becomes row A
+        v.A[F_EB].l = v.B[F_EB].l;
+        v.A[F_EB].c = v.B[F_EB].c;
+        v.A[F_EP].c = v.B[F_EP].c;
+        v.A[F_EP].r = v.B[F_EP].r;
+        v.A[F_VX].c = v.B[F_VX].c;
+        v.A[F_VY].c = v.B[F_VY].c;
+        v.A[F_VY].r = v.B[F_VY].r;
+        v.A[F_5].c = v.B[F_5].c;
+    };
+    auto refill = [&](int r) {  // every thread has pulled row r as row B: its slot takes row r + NS2
         if (t == 0 && r + NS2 <= rhi) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(r + NS2);
         }
     };
-    if (rlo < sfirst) load(Slot<2>(), rlo);
-    load(Slot<0>(), sfirst);
-    __syncthreads();
-    for (int r = rlo; r <= sfirst; ++r) refill(r);
+    if (rlo < sfirst) {
+        pullB(row_at(rlo));
+        toA();
+        __syncthreads();
+        refill(rlo);
+    }
     const bool cx_in = c >= 1 && c <= g.nvxj, cy_in = c >= 1 && c <= g.ncx;
-    // 1/a_ii and the right-hand side b at sweep-1 row s-1 (= the sweep-2 row): same for both sweeps
-    double iax = 0.0, iay = 0.0;
-    // one row step; row s in slot K, s-1 in (K+2)%3, s+1 loaded into (K+1)%3.  EDGE = false
-    // (CTAs whose rows and columns all stay off the boundary): no boundary logic at all.
-    auto step = [&](auto slot, auto edge, int s) -> bool {
-        constexpr int K = decltype(slot)::v, KA = (K + 2) % 3, KC = (K + 1) % 3;
+    // 1/a_ii and right-hand side of sweep-1 row s-1 (= the sweep-2 row): equal in both sweeps
+    double iax = 0.0, iay = 0.0, bxp = 0.0, byp = 0.0, lag_eb = 0.0;
+    // one row step s: sweep 1 of row s, sweep 2 of row s-1.  EDGE = false (CTAs whose rows
+    // and columns all stay off the boundary): no boundary logic at all.
+    auto step = [&](auto edge, int s) {
         constexpr bool EDGE = decltype(edge)::value;
-        if (s > slast) return true;
-        const double lag_eb = rows[KC].f[F_EB].c, lag_5 = rows[KC].f[F_5].c;  // row s-2
-        if (s + 1 <= rhi) load(Slot<KC>(), s + 1);
-        const WinV<KA, K, KC> w{rows};
+        pullB(row_at(s));
+        if (s + 1 <= rhi) pullC(row_at(s + 1));
+        const W1 w{&v};
         // ---- sweep 1, row s
-        double vx1 = w.B(F_VX), vy1 = w.B(F_VY), iax_n = 0.0, iay_n = 0.0;
+        double vx1 = v.B[F_VX].c, vy1 = v.B[F_VY].c, iax_n = 0.0, iay_n = 0.0, bx_n = 0.0, by_n = 0.0;
         if (!EDGE || (s >= 1 && s <= g.ncy && cx_in)) {
             const RowX x = lx_win<EDGE>(g, w, s);
-            const double b = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
+            bx_n = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
             iax_n = rcp(x.a);
-            vx1 = w.B(F_VX) + a.omega * (b - x.L) * iax_n;
+            vx1 = w.B(F_VX) + a.omega * (bx_n - x.L) * iax_n;
         }
         if (!EDGE || (s >= 1 && s <= g.nvyi && cy_in)) {
             const RowX y = ly_win<EDGE>(g, w, c);
-            const double b = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
+            by_n = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
             iay_n = rcp(y.a);
-            vy1 = w.B(F_VY) + a.omega * (b - y.L) * iay_n;
+            vy1 = w.B(F_VY) + a.omega * (by_n - y.L) * iay_n;
         }
         s1[((s & 3) * 2 + 0) * TW + t] = vx1;
         s1[((s & 3) * 2 + 1) * TW + t] = vy1;
         __syncthreads();
-        if (s + 1 <= rhi) refill(s + 1);
+        refill(s);
         // ---- sweep 2, row i = s-1 on the intermediate iterate
         const int i = s - 1;
         if (i >= i0 && i <= i1 && t >= 1 && t <= a.tw && (!EDGE || c <= g.ncx)) {
             const double *qa = s1 + (((s - 2) & 3) * 2) * TW + t, *qb = s1 + (((s - 1) & 3) * 2) * TW + t,
                          *qc = s1 + ((s & 3) * 2) * TW + t;
-            WinS2<KA, K> u;
-            u.r = rows;
+            W2 u;
+            u.v = &v;
             u.lag_eb = lag_eb;
-            u.lag_5 = lag_5;
             u.vx[0] = R3{0.0, qa[0], 0.0};
             u.vx[1] = R3{qb[-1], qb[0], qb[1]};
             u.vx[2] = R3{qc[-1], qc[0], 0.0};
@@ -688,39 +742,31 @@ __global__ void __launch_bounds__(TW, MINB) k_jacobi2(GridL g, J2Args a, int H) 
             if (EDGE && c == g.ncx && g.bE) u.vy[1].r = g.sE * u.vy[1].c;
             if (!EDGE || c <= g.nvxj) {
                 const RowX x = lx_win<EDGE>(g, u, i);
-                const double b = (MODE == RHS_FINE) ? fx_win(u, a.gx) - (u.B(F_4) - u.B(F_4, 1)) * g.idx : u.B(F_4);
-                const double vn = u.B(F_VX) + a.omega * (b - x.L) * iax;
+                const double vn = u.B(F_VX) + a.omega * (bxp - x.L) * iax;
                 a.vxo[(size_t)i * P + c] = vn;
                 if (EDGE && i == 1 && g.bN) a.vxo[c] = g.sN * vn;
                 if (EDGE && i == g.ncy && g.bS) a.vxo[(size_t)(g.ncy + 1) * P + c] = g.sS * vn;
             }
             if (!EDGE || i <= g.nvyi) {
                 const RowX y = ly_win<EDGE>(g, u, c);
-                const double b = (MODE == RHS_FINE) ? fy_win(u, a.gy) - (u.B(F_4) - u.C(F_4)) * g.idy : u.B(F_5);
-                const double vn = u.B(F_VY) + a.omega * (b - y.L) * iay;
+                const double vn = u.B(F_VY) + a.omega * (byp - y.L) * iay;
                 a.vyo[(size_t)i * P + c] = vn;
                 if (EDGE && c == 1 && g.bW) a.vyo[(size_t)i * P] = g.sW * vn;
                 if (EDGE && c == g.ncx && g.bE) a.vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
             }
         }
+        lag_eb = v.A[F_EB].c;
+        toA();
         iax = iax_n;
         iay = iay_n;
-        return false;
+        bxp = bx_n;
+        byp = by_n;
     };
     const bool interior = i0 >= 2 && i1 + 1 <= g.ncy - 1 && j0 >= 2 && j0 + TW - 2 <= g.ncx - 1;
-    if (interior) {
-        for (int s = sfirst;; s += 3) {
-            if (step(Slot<0>(), std::false_type(), s)) break;
-            if (step(Slot<1>(), std::false_type(), s + 1)) break;
-            if (step(Slot<2>(), std::false_type(), s + 2)) break;
-        }
-    } else {
-        for (int s = sfirst;; s += 3) {
-            if (step(Slot<0>(), std::true_type(), s)) break;
-            if (step(Slot<1>(), std::true_type(), s + 1)) break;
-            if (step(Slot<2>(), std::true_type(), s + 2)) break;
-        }
-    }
+    if (interior)
+        for (int s = sfirst; s <= slast; ++s) step(std::false_type(), s);
+    else
+        for (int s = sfirst; s <= slast; ++s) step(std::true_type(), s);
 }
 
 int j2_tw(const GridL &g) {  // output columns per CTA: even, <= TW - 2, balanced over the blocks

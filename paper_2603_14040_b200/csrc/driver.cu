@@ -233,8 +233,12 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
         else --pre_pairs;
     }
     smooth(h, l, cx, cy, ox, oy, rhs, pre_n, zero_in && !done_pre, pre_pairs);  // (1) pre-smoothing
-    launch_residual(c, L.g, L.etab, L.etap, cx, cy, rhs, L.rx, L.ry);          // (2) residual
-    launch_restrict_vel(c, L.g, C.g, L.rx, L.ry, C.bx, C.by);                 // (3) restriction
+    if (jacobi2_ok(L.g)) {  // (2) residual + (3) restriction in one pass
+        launch_residual_restrict(c, L.g, C.g, L.etab, L.etap, cx, cy, rhs, C.bx, C.by);
+    } else {
+        launch_residual(c, L.g, L.etab, L.etap, cx, cy, rhs, L.rx, L.ry);      // (2) residual
+        launch_restrict_vel(c, L.g, C.g, L.rx, L.ry, C.bx, C.by);             // (3) restriction
+    }
     vcycle(h, l + 1, C.vx[0], C.vy[0], C.vx[1], C.vy[1], rhs_arrays(C.bx, C.by), true);  // (4)
     launch_prolong(c, L.g, C.g, C.vx[0], C.vy[0], cx, cy);                    // (5) correction
     smooth(h, l, cx, cy, ox, oy, rhs, L.nu, false, post_pairs);              // (6) post-smoothing
@@ -1010,9 +1014,15 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
         switch (kernel) {
         case 0: launch_jacobi(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v, false); break;
         case 1: state_energy(h, nullptr, nullptr, nullptr); break;
-        case 2: launch_residual(c, g, F.etab, F.etap, F.vx[0], F.vy[0], rhs_fine(h), F.rx, F.ry);
+        case 2:
+            if (h->nlev > 1 && jacobi2_ok(g)) {
+                launch_residual_restrict(c, g, h->lev[1].g, F.etab, F.etap, F.vx[0], F.vy[0], rhs_fine(h),
+                                         h->lev[1].bx, h->lev[1].by);
+            } else {
+                launch_residual(c, g, F.etab, F.etap, F.vx[0], F.vy[0], rhs_fine(h), F.rx, F.ry);
                 if (h->nlev > 1) launch_restrict_vel(c, g, h->lev[1].g, F.rx, F.ry, h->lev[1].bx, h->lev[1].by);
-                break;
+            }
+            break;
         case 3: if (h->nlev > 1) launch_prolong(c, g, h->lev[1].g, h->lev[1].vx[0], h->lev[1].vy[0], F.vx[1], F.vy[1]); break;
         case 4:
             if (stream_ok(g))
@@ -1038,7 +1048,8 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
     // 4 fused Uzawa pressure step + energy: read 6, write p; 5 RBGS (4 phases, fused bytes);
     // 6 Uzawa step + energy + first Jacobi sweep of the next V-cycle: read 6, write p, vx, vy;
     // 7 two Jacobi sweeps in one pass: read 6, write 2
-    const double per_cell[8] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0, 72.0, 64.0};
+    double per_cell[8] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0, 72.0, 64.0};
+    if (h->nlev > 1 && jacobi2_ok(g)) per_cell[2] = 48.0 + 4.0;  // fused: the residual stays on chip
     if (kernel < 0 || kernel > 7) return STOKES_EINVAL;
     if ((kernel == 6 && !stream_ok(g)) || (kernel == 7 && !jacobi2_ok(g))) return STOKES_EINVAL;
     *bytes = per_cell[kernel] * cells;

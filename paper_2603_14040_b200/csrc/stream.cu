@@ -769,6 +769,124 @@ __global__ void __launch_bounds__(TW, MINB) k_jacobi2(GridL g, J2Args a, int H) 
         for (int s = sfirst; s <= slast; ++s) step(std::true_type(), s);
 }
 
+
+// ---- fine residual fused with its restriction (a3 + a5) --------------------------------
+// A CTA streams fine rows through the TMA landing ring (columns j0-1 .. j0+tw, tw <= TW-2:
+// one redundant column each side), evaluates r = b - L v on each row into an 8-row shared
+// ring, and every time a coarse row I is complete (fine row min(2I+1, ncy) done) emits
+// b^H(I, .) for the tw/2 coarse columns it owns with the normalised weights of
+// k_restrict_vel (Appendix B; rows / columns outside the domain dropped and renormalised).
+// The fine residual never reaches HBM: 48 B/fine cell read + 4 B written instead of 84.
+// Single-domain levels only (jacobi2_ok).
+constexpr int SMEMRR = NS2 * NF * RW * 8 + 8 * 2 * TW * 8 + NS2 * 8;
+
+struct RRArgs {
+    const double *src[6];  // vx, vy, eta_p, eta_b, p | bx, rho | by
+    double *bxc, *byc;     // coarse right-hand sides
+    double gx, gy;
+    int tw;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRArgs a, int HC) {
+    extern __shared__ __align__(128) double sm[];
+    double *rr = sm + NS2 * NF * RW;  // [8 rows][rx, ry][TW]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(rr + 8 * 2 * TW);
+    const int t = threadIdx.x;
+    const int j0 = 1 + a.tw * blockIdx.x;  // odd: coarse columns (j0+1)/2 ..
+    const int c = j0 - 1 + t;
+    const int I0 = 1 + blockIdx.y * HC;
+    const int I1 = min(I0 + HC - 1, gc.ncy);
+    const int ilo = max(2 * I0 - 2, 1), ihi = min(2 * I1 + 1, g.ncy);
+    const int rlo = ilo - 1, rhi = ihi + 1;
+    const size_t P = g.P;
+    auto issue = [&](int r) {
+        const int slot = (r - rlo) % NS2;
+        uint64_t *bar = bars + slot;
+        mbar_expect_tx(bar, NF * RW * 8);
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            bulk_g2s(sm + (slot * NF + f) * RW, a.src[f] + (size_t)r * P + (j0 - 2), RW * 8, bar);
+    };
+    if (t == 0) {
+        for (int k = 0; k < NS2; ++k) mbar_init(bars + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0)
+        for (int r = rlo; r < rlo + NS2 && r <= rhi; ++r) issue(r);
+    Win w;
+    auto consume = [&](int r) {
+        const int rel = r - rlo;
+        mbar_wait(bars + rel % NS2, (rel / NS2) & 1);
+        w.template push<NF>(sm + (rel % NS2) * NF * RW, t + 1);
+    };
+    auto refill = [&](int r) {
+        if (t == 0 && r + NS2 <= rhi) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(r + NS2);
+        }
+    };
+    consume(rlo);
+    consume(rlo + 1);
+    __syncthreads();
+    refill(rlo);
+    refill(rlo + 1);
+    const bool cx_in = c >= 1 && c <= g.nvxj, cy_in = c >= 1 && c <= g.ncx;
+    const int J = (j0 + 1) / 2 + t;  // coarse column of this thread in the emit phase
+    const bool emit_x = t < a.tw / 2 && J <= gc.nvxj, emit_y = t < a.tw / 2 && J <= gc.ncx;
+    for (int i = ilo; i <= ihi; ++i) {
+        consume(i + 1);  // A = i-1, B = i, C = i+1
+        double rx = 0.0, ry = 0.0;
+        if (cx_in) {
+            const double b = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
+            rx = b - lx_win(g, w, i).L;
+        }
+        if (cy_in && i <= g.nvyi) {
+            const double b = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
+            ry = b - ly_win(g, w, c).L;
+        }
+        rr[((i & 7) * 2 + 0) * TW + t] = rx;
+        rr[((i & 7) * 2 + 1) * TW + t] = ry;
+        __syncthreads();
+        refill(i + 1);
+        const int I = (i & 1) ? (i - 1) / 2 : (i == g.ncy ? i / 2 : 0);  // coarse row completed by row i
+        if (I >= I0 && I <= I1) {
+            if (emit_x) {  // vx: x vertex-centred [1/2, 1, 1/2], y cell-centred [1/4, 3/4, 3/4, 1/4]
+                const int q = 2 * J - (j0 - 1);  // ring column of fine column 2J
+                double sx = 0.0, wsum = 0.0;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const int fi = 2 * I - 2 + d;
+                    if ((fi < 1 && g.bN) || (fi > g.ncy && g.bS)) continue;
+                    const double *row = rr + ((fi & 7) * 2 + 0) * TW;
+                    const double h = 0.5 * row[q - 1] + row[q] + 0.5 * row[q + 1];
+                    const double wd = (d == 0 || d == 3) ? 0.25 : 0.75;
+                    sx += wd * h;
+                    wsum += wd;
+                }
+                a.bxc[at(gc, I, J)] = sx / (2.0 * wsum);
+            }
+            if (emit_y && I <= gc.nvyi) {  // vy: x cell-centred, y vertex-centred
+                const int q = 2 * J - 2 - (j0 - 1);  // ring column of fine column 2J-2
+                double sy = 0.0, wsum = 0.0;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    const int fj = 2 * J - 2 + d;
+                    if ((fj < 1 && g.bW) || (fj > g.ncx && g.bE)) continue;
+                    const double col = 0.5 * rr[(((2 * I - 1) & 7) * 2 + 1) * TW + q + d] +
+                                       rr[(((2 * I) & 7) * 2 + 1) * TW + q + d] +
+                                       0.5 * rr[(((2 * I + 1) & 7) * 2 + 1) * TW + q + d];
+                    const double wd = (d == 0 || d == 3) ? 0.25 : 0.75;
+                    sy += wd * col;
+                    wsum += wd;
+                }
+                a.byc[at(gc, I, J)] = sy / (2.0 * wsum);
+            }
+        }
+    }
+}
+
 int j2_tw(const GridL &g) {  // output columns per CTA: even, <= TW - 2, balanced over the blocks
     const int ncb = (g.ncx + TW - 3) / (TW - 2);
     int tw = (g.ncx + ncb - 1) / ncb;
@@ -848,6 +966,42 @@ void launch_jacobi_stream(const LaunchCtx &c, const GridL &g, const double *etab
         op.gx = op.gy = 0.0;
         run(c, g, op, nullptr);
     }
+}
+
+void launch_residual_restrict(const LaunchCtx &c, const GridL &g, const GridL &gc, const double *etab,
+                              const double *etap, const double *vx, const double *vy, const RhsArgs &rhs, double *bxc,
+                              double *byc) {
+    RRArgs a;
+    a.bxc = bxc;
+    a.byc = byc;
+    a.tw = j2_tw(g);
+    const int ncb = (g.ncx + a.tw - 1) / a.tw;
+    int strips = slots() / ncb;
+    if (strips < 1) strips = 1;
+    int HC = (gc.ncy + strips - 1) / strips;
+    if (HC < 2) HC = 2;
+    const dim3 grid(ncb, (gc.ncy + HC - 1) / HC);
+    if (rhs.mode == RHS_FINE) {
+        fill_src(a.src, vx, vy, etap, etab, rhs.p, rhs.rho);
+        a.gx = rhs.gx;
+        a.gy = rhs.gy;
+        static bool done = false;
+        if (!done) {
+            cudaFuncSetAttribute(k_resrestrict<RHS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMRR);
+            done = true;
+        }
+        k_resrestrict<RHS_FINE><<<grid, TW, SMEMRR, c.stream>>>(g, gc, a, HC);
+    } else {
+        fill_src(a.src, vx, vy, etap, etab, rhs.bx, rhs.by);
+        a.gx = a.gy = 0.0;
+        static bool done = false;
+        if (!done) {
+            cudaFuncSetAttribute(k_resrestrict<RHS_ARRAYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMRR);
+            done = true;
+        }
+        k_resrestrict<RHS_ARRAYS><<<grid, TW, SMEMRR, c.stream>>>(g, gc, a, HC);
+    }
+    ++*c.counter;
 }
 
 void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,

@@ -142,8 +142,11 @@ def test_transfers_and_coarse_viscosity(S, nx, ny, bc):
 
 
 @pytest.mark.parametrize("smoother", [0, 1])
-@pytest.mark.parametrize("nx,ny,bc", [(64, 64, (0, 0, 0, 0)), (128, 64, (1, 0, 1, 0)), (96, 48, (1, 1, 1, 1))])
+@pytest.mark.parametrize("nx,ny,bc", [(64, 64, (0, 0, 0, 0)), (128, 64, (1, 0, 1, 0)), (96, 48, (1, 1, 1, 1)),
+                                      (512, 256, (0, 1, 0, 1)), (640, 384, (1, 1, 0, 0))])
 def test_vcycle(S, smoother, nx, ny, bc):
+    """Levels >= 128 x 8 take the streamed kernels (two-sweep passes, residual fused with
+    its restriction: several column tiles and strips, ragged last tile at 640)."""
     f = parity_fields(nx, ny, log_contrast=1.0)
     o, s = pair(S, nx, ny, bc, f, smoother=smoother, omega_v=0.5)
     rng = np.random.default_rng(12)

@@ -1,6 +1,7 @@
 #!/bin/bash
-# One GPU session: smoke, tests, bench, ncu launch list of one solve + full capture of the
-# fine Jacobi sweep (k_stream<JacobiOp>).   usage: tools/gpu_round.sh TAG [skip-tests]
+# One GPU session: smoke, tests, bench, ncu launch list of one solve + full captures of the
+# fine-level hot kernels (two-sweep pass = dominant, single sweep, fused Uzawa step,
+# residual+restriction).   usage: tools/gpu_round.sh TAG [skip-tests]
 TAG=${1:-r01}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
@@ -10,10 +11,9 @@ fi
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
    --log-file gpurun_out/launches_$TAG.csv python tools/profile_solve.py > gpurun_out/launches_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
-   -k regex:k_stream -s 2 -c 1 -o gpurun_out/jacobi_$TAG -f python tools/profile_kernel.py --kernels jacobi \
-   > gpurun_out/ncu_full_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --profile-from-start off \
-   -k regex:k_stream -s 2 -c 1 -o gpurun_out/uzawa_$TAG -f python tools/profile_kernel.py --kernels pupdate \
-   > gpurun_out/ncu_uzawa_$TAG.log 2>&1
+for K in jacobi2:k_jacobi2 jacobi:k_stream jacobi_uzawa:k_stream_bar residual_restrict:k_resrestrict; do
+  timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
+     -k regex:${K#*:} -s 2 -c 1 -o gpurun_out/${K%%:*}_$TAG -f python tools/profile_kernel.py --kernels ${K%%:*} \
+     > gpurun_out/ncu_${K%%:*}_$TAG.log 2>&1
+done
 ls -la gpurun_out

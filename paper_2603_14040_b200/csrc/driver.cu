@@ -189,7 +189,15 @@ void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&
             cudaMemsetAsync(cx - COL_OFF, 0, field_doubles(L.g) * sizeof(double), h->stream);
             cudaMemsetAsync(cy - COL_OFF, 0, field_doubles(L.g) * sizeof(double), h->stream);
         }
-        for (int s = 0; s < n; ++s) launch_rbgs(c, L.g, L.etab, L.etap, cx, cy, rhs, h->o.omega_v);
+        if (jacobi2_ok(L.g)) {  // streamed two-pass sweeps, out of place (ping-pong like Jacobi)
+            for (int s = 0; s < n; ++s) {
+                launch_rbgs_stream(c, L.g, L.etab, L.etap, cx, cy, ox, oy, rhs, h->o.omega_v);
+                double *t = cx; cx = ox; ox = t;
+                t = cy; cy = oy; oy = t;
+            }
+        } else {
+            for (int s = 0; s < n; ++s) launch_rbgs(c, L.g, L.etab, L.etap, cx, cy, rhs, h->o.omega_v);
+        }
     }
 }
 
@@ -1033,7 +1041,10 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
                 launch_pupdate(c, g, F.etap, F.vx[0], F.vy[0], h->pbuf[h->pcur], h->pbuf[1 - h->pcur], h->o.alpha_p,
                                h->scal + S_ZERO, h->partials);
             break;
-        case 5: launch_rbgs(c, g, F.etab, F.etap, F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v); break;
+        case 5:
+            if (jacobi2_ok(g)) launch_rbgs_stream(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v);
+            else launch_rbgs(c, g, F.etab, F.etap, F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v);
+            break;
         case 7: launch_jacobi2(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v); break;
         default:
             launch_jacobi_uzawa(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], h->pbuf[h->pcur],
@@ -1050,6 +1061,7 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
     // 7 two Jacobi sweeps in one pass: read 6, write 2
     double per_cell[8] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0, 72.0, 64.0};
     if (h->nlev > 1 && jacobi2_ok(g)) per_cell[2] = 48.0 + 4.0;  // fused: the residual stays on chip
+    if (jacobi2_ok(g)) per_cell[5] = 2 * 56.0;  // RBGS: two streamed passes, each read 6 + write 1
     if (kernel < 0 || kernel > 7) return STOKES_EINVAL;
     if ((kernel == 6 && !stream_ok(g)) || (kernel == 7 && !jacobi2_ok(g))) return STOKES_EINVAL;
     *bytes = per_cell[kernel] * cells;

@@ -93,6 +93,10 @@ void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *et
 bool jacobi2_ok(const GridL &g);
 void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
                     const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega);
+// RBGS sweep as two streamed passes, out of place (jacobi2_ok levels): (vxi, vyi) -> (vxo, vyo)
+void launch_rbgs_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                        const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
+                        double omega);
 // fine residual fused with the velocity restriction to the next level (jacobi2_ok levels)
 void launch_residual_restrict(const LaunchCtx &c, const GridL &g, const GridL &gc, const double *etab,
                               const double *etap, const double *vx, const double *vy, const RhsArgs &rhs, double *bxc,

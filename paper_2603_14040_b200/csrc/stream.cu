@@ -887,6 +887,103 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
     }
 }
 
+
+// ---- damped red-black Gauss-Seidel in two streamed passes (a4, reading R11) -------------
+// The four phases (vx red, vx black, vy red, vy black; red = (i + j + par) even) as two
+// passes, one per component: pass COMP updates that component's red nodes of row s and
+// its black nodes of row s-2 in the same row step (one CTA barrier per step), reading the
+// other component read-only.  Red values go back into the landing slot (black neighbours
+// two rows later read them); every final value is written to the OUTPUT buffer, so the
+// input stays the old iterate for the neighbouring CTAs' halos (pass 0: vx in -> vx out,
+// pass 1 reads the new vx: vy in -> vy out).  Halo columns j0-1 / j0+tw and rows i0-1 /
+// i1+1 get their red update redundantly.  Lane parity picks red (row s) or black (row
+// s-2): every thread does one update per step with no divergent paths.  Exactly the
+// arithmetic of the four phase kernels.  2 x 56 B/cell per sweep instead of 4 x 64.
+struct SmV {  // stencil view straight on three landing slots (values change in place)
+    const double *a, *b, *c;
+    __device__ __forceinline__ double A(int k, int dc = 0) const { return a[k * RW + dc]; }
+    __device__ __forceinline__ double B(int k, int dc = 0) const { return b[k * RW + dc]; }
+    __device__ __forceinline__ double C(int k, int dc = 0) const { return c[k * RW + dc]; }
+};
+constexpr int NSR = 8;  // landing ring: rows s-3 .. s+1 resident, 3 in flight
+
+template <int COMP, int MODE>
+__global__ void __launch_bounds__(TW, MINB) k_rbgs_pass(GridL g, J2Args a, int H) {
+    extern __shared__ __align__(128) double sm[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + NSR * NF * RW);
+    const int t = threadIdx.x;
+    const int j0 = 1 + a.tw * blockIdx.x;
+    const int c = j0 - 1 + t;
+    const int i0 = 1 + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, g.ncy);
+    const int rlo = max(i0 - 2, 0), rhi = min(i1 + 2, g.ncy + 1);
+    const size_t P = g.P;
+    const int nrow = COMP == 0 ? g.ncy : g.nvyi, ncol = COMP == 0 ? g.nvxj : g.ncx;  // unknown range
+    auto issue = [&](int r) {
+        const int slot = (r - rlo) % NSR;
+        uint64_t *bar = bars + slot;
+        mbar_expect_tx(bar, NF * RW * 8);
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            bulk_g2s(sm + (slot * NF + f) * RW, a.src[f] + (size_t)r * P + (j0 - 2), RW * 8, bar);
+    };
+    if (t == 0) {
+        for (int k = 0; k < NSR; ++k) mbar_init(bars + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0)
+        for (int r = rlo; r < rlo + NSR && r <= rhi; ++r) issue(r);
+    int landed = rlo - 1;  // rows waited for so far
+    auto slot_of = [&](int r) { return sm + ((r - rlo) % NSR) * NF * RW + t + 1; };
+    auto wait_to = [&](int r) {
+        for (; landed < r; ++landed) {
+            const int rel = landed + 1 - rlo;
+            mbar_wait(bars + rel % NSR, (rel / NSR) & 1);
+        }
+    };
+    const int s_lo = max(i0 - 1, 1), s_hi = i1 + 2;
+    double *out = COMP == 0 ? a.vxo : a.vyo;
+    for (int s = s_lo; s <= s_hi; ++s) {
+        wait_to(min(s + 1, rhi));
+        const bool red = ((s + c + g.par) & 1) == 0;
+        const int r = red ? s : s - 2;  // red node of row s, or black node of row s-2
+        const bool act = red ? (r <= min(i1 + 1, nrow) && c >= 1 && c <= min(ncol, j0 + a.tw))
+                             : (r >= i0 && r <= min(i1, nrow) && t >= 1 && t <= a.tw && c <= ncol);
+        if (act) {
+            double *sb = slot_of(r);
+            const SmV w{slot_of(r - 1), sb, slot_of(r + 1)};
+            double vn;
+            if (COMP == 0) {
+                const RowX x = lx_win(g, w, r);
+                const double b = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
+                vn = w.B(F_VX) + a.omega * (b - x.L) * rcp(x.a);
+            } else {
+                const RowX y = ly_win(g, w, c);
+                const double b = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
+                vn = w.B(F_VY) + a.omega * (b - y.L) * rcp(y.a);
+            }
+            if (red) sb[COMP * RW] = vn;  // black neighbours of rows r +- 1 read it two steps later
+            if (r >= i0 && r <= i1 && t >= 1 && t <= a.tw) {
+                out[(size_t)r * P + c] = vn;
+                if (COMP == 0) {
+                    if (r == 1 && g.bN) out[c] = g.sN * vn;
+                    if (r == g.ncy && g.bS) out[(size_t)(g.ncy + 1) * P + c] = g.sS * vn;
+                } else {
+                    if (c == 1 && g.bW) out[(size_t)r * P] = g.sW * vn;
+                    if (c == g.ncx && g.bE) out[(size_t)r * P + g.ncx + 1] = g.sE * vn;
+                }
+            }
+        }
+        __syncthreads();
+        // row s-3 is done (last read by the black update of row s-2): its slot takes s-3+NSR
+        if (t == 0 && s - 3 >= rlo && s - 3 + NSR <= rhi) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(s - 3 + NSR);
+        }
+    }
+}
+
 int j2_tw(const GridL &g) {  // output columns per CTA: even, <= TW - 2, balanced over the blocks
     const int ncb = (g.ncx + TW - 3) / (TW - 2);
     int tw = (g.ncx + ncb - 1) / ncb;
@@ -1002,6 +1099,40 @@ void launch_residual_restrict(const LaunchCtx &c, const GridL &g, const GridL &g
         k_resrestrict<RHS_ARRAYS><<<grid, TW, SMEMRR, c.stream>>>(g, gc, a, HC);
     }
     ++*c.counter;
+}
+
+template <int COMP, int MODE>
+void rbgs_pass(const LaunchCtx &c, const GridL &g, const J2Args &a) {
+    constexpr int SM = NSR * NF * RW * 8 + NSR * 8;
+    static bool done = false;
+    if (!done) {
+        cudaFuncSetAttribute(k_rbgs_pass<COMP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+        done = true;
+    }
+    int H = 0;
+    const dim3 grid = j2_grid(g, &H);
+    k_rbgs_pass<COMP, MODE><<<grid, TW, SM, c.stream>>>(g, a, H);
+    ++*c.counter;
+}
+
+void launch_rbgs_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                        const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
+                        double omega) {
+    J2Args a;
+    a.omega = omega;
+    a.tw = j2_tw(g);
+    a.vxo = vxo;
+    a.vyo = vyo;
+    const bool fine = rhs.mode == RHS_FINE;
+    a.gx = fine ? rhs.gx : 0.0;
+    a.gy = fine ? rhs.gy : 0.0;
+    // pass 0: vx (reads vy old), pass 1: vy (reads the new vx)
+    fill_src(a.src, vxi, vyi, etap, etab, fine ? rhs.p : rhs.bx, fine ? rhs.rho : rhs.by);
+    if (fine) rbgs_pass<0, RHS_FINE>(c, g, a);
+    else rbgs_pass<0, RHS_ARRAYS>(c, g, a);
+    a.src[0] = vxo;
+    if (fine) rbgs_pass<1, RHS_FINE>(c, g, a);
+    else rbgs_pass<1, RHS_ARRAYS>(c, g, a);
 }
 
 void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,

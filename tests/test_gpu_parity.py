@@ -90,14 +90,15 @@ def test_smoother(S, smoother, nx, ny, bc):
         assert rel(qx[:, 1:-1], rx[:, 1:-1]) <= TOL_OP and rel(qy[1:-1], ry[1:-1]) <= TOL_OP
 
 
-@pytest.mark.parametrize("nsweeps", [2, 4, 5])
+@pytest.mark.parametrize("smoother,nsweeps", [(0, 2), (0, 4), (0, 5), (1, 1), (1, 2), (1, 3)])
 @pytest.mark.parametrize("nx,ny", [(128, 8), (300, 250), (1030, 13)])
 @pytest.mark.parametrize("bc", BCS)
-def test_two_sweep_pass(S, nx, ny, bc, nsweeps):
-    """Levels >= 128 x 8 run sweep pairs as one temporally blocked pass (two Jacobi sweeps
-    per HBM read); ragged column tiles, 4-row strips and every mirror ghost included."""
+def test_streamed_smoothers(S, nx, ny, bc, smoother, nsweeps):
+    """Levels >= 128 x 8 run Jacobi sweep pairs as one temporally blocked pass (two sweeps
+    per HBM read) and RBGS sweeps as two streamed passes (red row s + black row s-2 per
+    step); ragged column tiles, 4-row strips and every mirror ghost included."""
     f = parity_fields(nx, ny, log_contrast=1.0)
-    o, s = pair(S, nx, ny, bc, f, omega_v=0.5, coarse_min=4, coarse_direct=0)
+    o, s = pair(S, nx, ny, bc, f, smoother=smoother, omega_v=0.5, coarse_min=4, coarse_direct=0)
     rng = np.random.default_rng(11)
     bx, by = rng.standard_normal((ny, nx + 1)), rng.standard_normal((ny + 1, nx))
     vx, vy = rng.standard_normal((ny, nx + 1)), rng.standard_normal((ny + 1, nx))

@@ -89,3 +89,28 @@ def test_decomposition_errors():
         StokesDist(130, 64, px=4, py=1)  # 130 % 4 != 0
     with pytest.raises(StokesError):
         StokesDist(64, 64, px=2, py=2, accel=1)  # GCR not decomposed
+
+
+def test_nccl_transport_single_rank():
+    """The NCCL transport on a 1 x 1 process grid (world size 1): NCCL communicator, graph-
+    captured ncclAllReduce / ncclAllGather of the agglomeration, tile windows -- everything
+    but the peer send/recv, which needs a second GPU.  Must equal the single-domain solve."""
+    import torch.distributed as dist
+    from paper_2603_14040_b200 import Stokes, StokesDist
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("gloo", init_method="tcp://127.0.0.1:29561", rank=0, world_size=1)
+    try:
+        n = 256
+        w = workload("layered", n, n)
+        opts = dict(omega_v=0.6, alpha_p=1.0, max_iter=400)
+        one = setup(Stokes, w, n, **opts)
+        dd = setup(StokesDist, w, n, px=1, py=1, rank=0, **opts)
+        a, b = one.solve(1e-8), dd.solve(1e-8)
+        assert a["status"] == 0 and b["status"] == 0
+        assert abs(a["iters"] - b["iters"]) <= 1
+        for k in ("vx", "vy", "p"):
+            assert rel(b[k], a[k]) <= 1e-6, k
+    finally:
+        if own:
+            dist.destroy_process_group()

@@ -40,6 +40,8 @@ class Opts(ctypes.Structure):
         ("gcr_restart", ctypes.c_int),
         ("max_iter", ctypes.c_int),
         ("pressure_sign", ctypes.c_int),
+        ("theta_step", ctypes.c_double),
+        ("theta_every", ctypes.c_int),
     ]
 
 
@@ -75,6 +77,8 @@ def lib():
         L.oracle_prolong.argtypes = [P, ctypes.c_int, D, D, D, D]
         L.oracle_coarse_solve.argtypes = [P, D, D, D, D]
         L.oracle_solve_hist.argtypes = [P, ctypes.c_double, D, D, D, I, D, D, ctypes.c_int]
+        L.oracle_blend_viscosity.argtypes = [P, ctypes.c_double]
+        L.oracle_lithostatic.argtypes = [P, D]
         L.oracle_strerror.restype = ctypes.c_char_p
     return _lib
 
@@ -168,6 +172,16 @@ class Oracle:
         eb, ep = self.zeros("b", level), self.zeros("p", level)
         _check(lib().oracle_get_viscosity(self._h, level, _d(eb), _d(ep)), "get_viscosity")
         return eb, ep
+
+    def blend_viscosity(self, theta):
+        """test hook: computational viscosity (1 - theta) eta_min + theta eta"""
+        _check(lib().oracle_blend_viscosity(self._h, ctypes.c_double(theta)), "blend_viscosity")
+
+    def lithostatic(self):
+        """p_litho = int_0^y rho g_y dy' at the P nodes, P layout"""
+        p = self.zeros("p")
+        _check(lib().oracle_lithostatic(self._h, _d(p)), "lithostatic")
+        return p
 
     # operators ----------------------------------------------------------
     def apply_operator(self, vx, vy, p):

@@ -53,6 +53,8 @@ typedef struct {
     int gcr_restart;     /* m */
     int max_iter;
     int pressure_sign;   /* +1 physical reading R3 (default); -1 literal PAPER.md:824 */
+    double theta_step;   /* viscosity rescaling: theta += step per stage, 0 = off */
+    int theta_every;     /* Uzawa iterations per stage before theta = 1 (25) */
 } oracle_opts;
 
 typedef struct {
@@ -81,6 +83,8 @@ typedef struct {
     double *chol;
     /* fine-level work fields */
     double *vx, *vy, *p;
+    /* the caller's viscosities (padded, fine) -- viscosity rescaling blends from them */
+    double *etab_user, *etap_user;
 } oracle_t;
 
 /* ------------------------------------------------------------------ helpers */
@@ -561,6 +565,8 @@ int oracle_opts_default(oracle_opts *o) {
     o->gcr_restart = 10;
     o->max_iter = 10000;
     o->pressure_sign = 1;
+    o->theta_step = 0.0;
+    o->theta_every = 25;
     return O_OK;
 }
 
@@ -580,7 +586,8 @@ int oracle_create(int nx, int ny, double Lx, double Ly, const int *bc, const ora
     S->nx = nx; S->ny = ny; S->Lx = Lx; S->Ly = Ly;
     memcpy(S->bc, bc, sizeof(S->bc));
     if (opts) S->o = *opts; else oracle_opts_default(&S->o);
-    if (S->o.nu1 < 0 || S->o.coarse_min < 2 || S->o.vcycles_per_iter < 1 || S->o.gcr_restart < 1) {
+    if (S->o.nu1 < 0 || S->o.coarse_min < 2 || S->o.vcycles_per_iter < 1 || S->o.gcr_restart < 1 ||
+        !(S->o.theta_step >= 0.0 && S->o.theta_step <= 1.0) || S->o.theta_every < 1) {
         free(S);
         return O_EINVAL;
     }
@@ -602,6 +609,7 @@ int oracle_create(int nx, int ny, double Lx, double Ly, const int *bc, const ora
     size_t n = padn(&S->lev[0]);
     S->rhob = zalloc(n); S->fx = zalloc(n); S->fy = zalloc(n);
     S->vx = zalloc(n); S->vy = zalloc(n); S->p = zalloc(n);
+    S->etab_user = zalloc(n); S->etap_user = zalloc(n);
     *out = S;
     return O_OK;
 }
@@ -614,6 +622,7 @@ int oracle_destroy(oracle_t *S) {
         free(L->ex); free(L->ey); free(L->tx); free(L->ty);
     }
     free(S->rhob); free(S->fx); free(S->fy); free(S->vx); free(S->vy); free(S->p); free(S->chol);
+    free(S->etab_user); free(S->etap_user);
     free(S);
     return O_OK;
 }
@@ -629,15 +638,9 @@ static void update_force(oracle_t *S) {
     if (!S->force_override) body_force(S, S->fx, S->fy);
 }
 
-/* set_viscosity: copies eta, builds the coarse viscosities (a7, reading R7: the same
- * normalised bilinear restriction, arithmetic) and the coarsest factorisation (a8). */
-int oracle_set_viscosity(oracle_t *S, const double *eta_b, const double *eta_p) {
-    if (!S || !eta_b || !eta_p) return O_EINVAL;
-    olevel *F = &S->lev[0];
-    for (size_t k = 0; k < (size_t)(S->ny + 1) * (S->nx + 1); ++k) if (!(eta_b[k] > 0)) return O_EINVAL;
-    for (size_t k = 0; k < (size_t)S->ny * S->nx; ++k) if (!(eta_p[k] > 0)) return O_EINVAL;
-    in_b(F, eta_b, F->etab);
-    in_p(F, eta_p, F->etap);
+/* coarse viscosities (a7, reading R7: the same normalised bilinear restriction,
+ * arithmetic) and the coarsest factorisation (a8) from the fine-level viscosities */
+static int build_hierarchy(oracle_t *S) {
     for (int l = 0; l + 1 < S->nlev; ++l) {
         olevel *A = &S->lev[l], *C = &S->lev[l + 1];
         restrict_generic(A, C, T_B, A->etab, C->etab, 0, C->ncy, 0, C->ncx);
@@ -649,6 +652,38 @@ int oracle_set_viscosity(oracle_t *S, const double *eta_b, const double *eta_p) 
         if (build_coarse_direct(S) != 0) return O_EINVAL;
     }
     return O_OK;
+}
+
+/* set_viscosity: copies eta (kept as the caller's field for viscosity rescaling) and
+ * builds the hierarchy. */
+int oracle_set_viscosity(oracle_t *S, const double *eta_b, const double *eta_p) {
+    if (!S || !eta_b || !eta_p) return O_EINVAL;
+    olevel *F = &S->lev[0];
+    for (size_t k = 0; k < (size_t)(S->ny + 1) * (S->nx + 1); ++k) if (!(eta_b[k] > 0)) return O_EINVAL;
+    for (size_t k = 0; k < (size_t)S->ny * S->nx; ++k) if (!(eta_p[k] > 0)) return O_EINVAL;
+    in_b(F, eta_b, F->etab);
+    in_p(F, eta_p, F->etap);
+    memcpy(S->etab_user, F->etab, padn(F) * sizeof(double));
+    memcpy(S->etap_user, F->etap, padn(F) * sizeof(double));
+    return build_hierarchy(S);
+}
+
+/* Viscosity rescaling: eta_comp = (1 - theta) eta_min + theta eta on
+ * both fine viscosity fields, eta_min = the minimum over both caller fields (basic nodes
+ * [0,ncy]x[0,ncx], P nodes [1,ncy]x[1,ncx]); then the hierarchy is rebuilt from eta_comp.
+ * theta = 1 restores the caller's field exactly. */
+int oracle_blend_viscosity(oracle_t *S, double theta) {
+    if (!S || !S->have_eta || !(theta >= 0.0 && theta <= 1.0)) return O_EINVAL;
+    olevel *F = &S->lev[0];
+    double emin = INFINITY;
+    for (int i = 0; i <= F->ncy; ++i)
+        for (int j = 0; j <= F->ncx; ++j) emin = fmin(emin, S->etab_user[IX(F, i, j)]);
+    FOR_P(F) emin = fmin(emin, S->etap_user[IX(F, i, j)]);
+    for (int i = 0; i <= F->ncy; ++i)
+        for (int j = 0; j <= F->ncx; ++j)
+            F->etab[IX(F, i, j)] = (1.0 - theta) * emin + theta * S->etab_user[IX(F, i, j)];
+    FOR_P(F) F->etap[IX(F, i, j)] = (1.0 - theta) * emin + theta * S->etap_user[IX(F, i, j)];
+    return build_hierarchy(S);
 }
 int oracle_set_density(oracle_t *S, const double *rho_b) {
     if (!S || !rho_b) return O_EINVAL;
@@ -681,6 +716,28 @@ int oracle_get_viscosity(const oracle_t *S, int l, double *eta_b, double *eta_p)
     if (!S || l < 0 || l >= S->nlev || !S->have_eta) return O_EINVAL;
     out_b(&S->lev[l], S->lev[l].etab, eta_b);
     out_p(&S->lev[l], S->lev[l].etap, eta_p);
+    return O_OK;
+}
+
+/* Lithostatic pressure: p(x, y) = int_0^y rho(x, y') g_y dy', the
+ * column integral from the top wall to each P node with the density at the vy nodes
+ * (reading R23) -- the discrete hydrostatic balance of the y-momentum row with v = 0
+ * (f_y = -g_y rho, G_y p = -(p(i+1,j) - p(i,j))/dy; reading R4):
+ *   p(1, j) = g_y (dy/2) rho_vy(0, j),   p(i+1, j) = p(i, j) + g_y dy rho_vy(i, j).
+ * Output in the P layout (ny x nx), not de-meaned. */
+int oracle_lithostatic(const oracle_t *S, double *p) {
+    if (!S || !p) return O_EINVAL;
+    if (!S->have_rho) return O_ESTATE;
+    const olevel *L = &S->lev[0];
+    const double *rb = S->rhob;
+    for (int j = 1; j <= L->ncx; ++j) {
+        double acc = S->gy * (0.5 * L->dy) * (0.5 * (rb[IX(L, 0, j - 1)] + rb[IX(L, 0, j)]));
+        p[(size_t)0 * L->ncx + (j - 1)] = acc;
+        for (int i = 1; i < L->ncy; ++i) {
+            acc = acc + S->gy * L->dy * (0.5 * (rb[IX(L, i, j - 1)] + rb[IX(L, i, j)]));
+            p[(size_t)i * L->ncx + (j - 1)] = acc;
+        }
+    }
     return O_OK;
 }
 
@@ -975,6 +1032,56 @@ int oracle_solve_hist(oracle_t *S, double rtol, double *vx, double *vy, double *
     free(rx); free(ry); free(rp);
     int status;
     if (E0 <= rtol) { *iters = 0; *rel_energy = E0; status = O_OK; }
+    else if (S->o.theta_step > 0.0) {
+        /* viscosity rescaling: stages theta = 0, step, 2 step, .. < 1 of
+         * theta_every iterations each (no stopping test: the staged systems are not the
+         * problem), warm-started from the previous stage; then theta = 1 (the caller's
+         * viscosity) to E <= rtol with the remaining iteration budget. */
+        const int budget = S->o.max_iter;
+        int used = 0, it = 0;
+        double E = E0;
+        status = O_OK;
+        for (int k = 0;; ++k) {
+            double theta = k * S->o.theta_step;
+            if (theta >= 1.0 || used >= budget) break;
+            oracle_blend_viscosity(S, theta);
+            double Sfk = force_energy(S);
+            rx = zalloc(n); ry = zalloc(n); rp = zalloc(n);
+            full_residual(S, S->vx, S->vy, S->p, rx, ry, rp);
+            double E0k = energy_of(S, rx, ry, rp, Sfk);
+            free(rx); free(ry); free(rp);
+            S->o.max_iter = budget - used < S->o.theta_every ? budget - used : S->o.theta_every;
+            int hoff = used < hist_len ? used : hist_len;
+            status = S->o.accel == 1
+                         ? solve_gcr(S, -1.0, Sfk, E0k, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff)
+                         : solve_uzawa(S, -1.0, Sfk, E0k, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff);
+            S->o.max_iter = budget;
+            used += it;
+            if (status == O_EDIVERGED) break;
+        }
+        oracle_blend_viscosity(S, 1.0);
+        Sf = force_energy(S);
+        if (status != O_EDIVERGED && used < budget) {
+            rx = zalloc(n); ry = zalloc(n); rp = zalloc(n);
+            full_residual(S, S->vx, S->vy, S->p, rx, ry, rp);
+            double E1 = energy_of(S, rx, ry, rp, Sf);
+            free(rx); free(ry); free(rp);
+            if (E1 <= rtol) { it = 0; E = E1; status = O_OK; }
+            else {
+                S->o.max_iter = budget - used;
+                int hoff = used < hist_len ? used : hist_len;
+                status = S->o.accel == 1
+                             ? solve_gcr(S, rtol, Sf, E1, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff)
+                             : solve_uzawa(S, rtol, Sf, E1, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff);
+                S->o.max_iter = budget;
+            }
+            used += it;
+        } else if (status != O_EDIVERGED) {
+            status = O_NOT_CONVERGED;
+        }
+        *iters = used;
+        *rel_energy = E;
+    }
     else if (S->o.accel == 1) status = solve_gcr(S, rtol, Sf, E0, iters, rel_energy, hist, hist_len);
     else status = solve_uzawa(S, rtol, Sf, E0, iters, rel_energy, hist, hist_len);
     double m = p_mean(L, S->p);

@@ -88,6 +88,10 @@ typedef struct {
     int gcr_restart;      /* m of GCR(m)                                                        */
     int max_iter;         /* cap on iterations (V-cycle applications)                           */
     int pressure_sign;    /* +1 physical reading R3 (default); -1 literal PAPER.md:824 (diverges) */
+    double theta_step;    /* viscosity rescaling: stages theta = 0, step, ..
+                             < 1 with eta_comp = (1-theta) eta_min + theta eta, then theta = 1;
+                             0 = off (default).  Single-domain handles only                      */
+    int theta_every;      /* Uzawa / GCR iterations per stage before theta = 1 (25) */
 } stokes_opts;
 
 /* Fill *o with the defaults.  Returns STOKES_EINVAL if o is NULL. */
@@ -185,6 +189,14 @@ int stokes_get_viscosity(stokes_t h, int level, double *eta_b, double *eta_p);
 int stokes_coarse_solve(stokes_t h, const double *bx, const double *by, double *vx, double *vy);
 
 /* ---- instrumentation ---------------------------------------------------------- */
+/* Lithostatic pressure, the initial guess the paper uses with gravity:
+ * p(x, y) = int_0^y rho g_y dy' from the top wall, discretely the hydrostatic balance of the
+ * y-momentum row with v = 0 (reading R4, density at vy nodes R23):
+ *   p(1,j) = g_y (dy/2) rho_vy(0,j),  p(i+1,j) = p(i,j) + g_y dy rho_vy(i,j).
+ * p: DEVICE, P layout ny x nx, written (not de-meaned).  Needs stokes_set_density
+ * (STOKES_ESTATE otherwise); single-domain handles only (STOKES_EINVAL otherwise). */
+int stokes_lithostatic(stokes_t h, double *p);
+
 /* Number of kernels this library launched on the handle since creation / last reset. */
 int stokes_launch_count(stokes_t h, long long *count, int reset);
 /* Time `reps` back-to-back launches of a hot-path kernel on the handle's stream with CUDA

@@ -78,6 +78,7 @@ int check_opts(const stokes_opts &o) {
     if (o.vcycles_per_iter < 1 || (o.accel != 0 && o.accel != 1)) return STOKES_EINVAL;
     if (o.gcr_restart < 1 || o.gcr_restart > MAXM || o.max_iter < 0) return STOKES_EINVAL;
     if (o.pressure_sign != 1 && o.pressure_sign != -1) return STOKES_EINVAL;
+    if (!(o.theta_step >= 0.0 && o.theta_step <= 1.0) || o.theta_every < 1) return STOKES_EINVAL;
     return STOKES_OK;
 }
 
@@ -100,6 +101,12 @@ size_t carve(stokes_s *h, Carver &cv) {
     h->pbuf[0] = cv.field(g0);
     h->pbuf[1] = cv.field(g0);
     h->rho = cv.field(g0);
+    if (h->o.theta_step > 0.0) {
+        h->etab_user = cv.field(g0);
+        h->etap_user = cv.field(g0);
+    } else {
+        h->etab_user = h->etap_user = nullptr;
+    }
     h->npart = (size_t)energy_blocks(g0) * 12 + 3 * 4096 + 64;
     h->partials = cv.take(h->npart);
     h->scal = cv.take(S_NSCAL);
@@ -626,6 +633,8 @@ int stokes_opts_default(stokes_opts *o) {
     o->gcr_restart = 10;
     o->max_iter = 10000;
     o->pressure_sign = 1;
+    o->theta_step = 0.0;
+    o->theta_every = 25;
     return STOKES_OK;
 }
 
@@ -754,7 +763,20 @@ int stokes_set_viscosity(stokes_t h, const double *eta_b, const double *eta_p) {
     Level &F = h->lev[0];
     launch_in_b(c, F.g, eta_b, F.etab);
     launch_in_p(c, F.g, eta_p, F.etap);
+    if (h->etab_user) {  // kept for viscosity rescaling
+        CK(cudaMemcpyAsync(h->etab_user - COL_OFF, F.etab - COL_OFF, field_doubles(F.g) * 8, cudaMemcpyDeviceToDevice,
+                           h->stream));
+        CK(cudaMemcpyAsync(h->etap_user - COL_OFF, F.etap - COL_OFF, field_doubles(F.g) * 8, cudaMemcpyDeviceToDevice,
+                           h->stream));
+    }
     return build_hierarchy(h);
+}
+
+int stokes_lithostatic(stokes_t h, double *p) {
+    if (!h || !p || h->dist) return STOKES_EINVAL;
+    if (!h->have_rho) return STOKES_ESTATE;
+    launch_lithostatic(ctx(h), h->lev[0].g, h->rho, h->gy, p);
+    return sync(h);
 }
 
 }  // extern "C"
@@ -888,12 +910,10 @@ int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int
         *iters = 0;
         *rel_energy = E0;
         status = STOKES_OK;  // energy_now left the mean of the stored p in S_MSHIFT
-    } else if (h->o.accel == STOKES_ACCEL_GCR) {
-        status = stream_ok(F.g) ? solve_gcr_fused(h, rtol, E0, iters, rel_energy)
-                                : solve_gcr(h, rtol, E0, iters, rel_energy);
+    } else if (h->o.theta_step > 0.0) {
+        status = solve_staged(h, rtol, iters, rel_energy);
     } else {
-        status = fused_ok(h) ? solve_uzawa_fused(h, rtol, E0, iters, rel_energy)
-                             : solve_uzawa(h, rtol, E0, iters, rel_energy);
+        status = solve_inner(h, rtol, E0, iters, rel_energy);
     }
     if (status < 0 && status != STOKES_EDIVERGED) return status;
     launch_out_vx(c, F.g, F.vx[0], vx);
@@ -903,6 +923,69 @@ int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int
     if (st) return st;
     return status;
 }
+
+}  // extern "C"
+namespace sk {
+int solve_inner(stokes_s *h, double rtol, double E0, int *iters, double *E) {
+    if (h->o.accel == STOKES_ACCEL_GCR)
+        return stream_ok(h->lev[0].g) ? solve_gcr_fused(h, rtol, E0, iters, E) : solve_gcr(h, rtol, E0, iters, E);
+    return fused_ok(h) ? solve_uzawa_fused(h, rtol, E0, iters, E) : solve_uzawa(h, rtol, E0, iters, E);
+}
+// computational viscosity (1 - theta) eta_min + theta eta and its hierarchy
+int set_theta(stokes_s *h, double theta) {
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    launch_eta_blend(c, F.g, h->etab_user, h->etap_user, F.etab, F.etap,
+                     reinterpret_cast<const unsigned long long *>(h->scal + S_ETAMIN), theta);
+    return build_hierarchy(h);
+}
+// Viscosity rescaling: stages theta = 0, step, .. < 1 of theta_every
+// iterations each (no stopping test: the staged systems are not the problem), warm-started
+// from the previous stage; then theta = 1 (the caller's viscosity, restored exactly) to
+// E <= rtol with the remaining iteration budget.  Same schedule as the oracle.
+int solve_staged(stokes_s *h, double rtol, int *iters, double *Eout) {
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    const int budget = h->o.max_iter;
+    int used = 0, it = 0, st = 0, status = STOKES_OK;
+    double E = 0.0, E0 = 0.0;
+    const unsigned long long big = 0x7ff0000000000000ull;  // +inf
+    CK(cudaMemcpyAsync(h->scal + S_ETAMIN, &big, 8, cudaMemcpyHostToDevice, h->stream));
+    launch_eta_min(c, F.g, h->etab_user, h->etap_user, reinterpret_cast<unsigned long long *>(h->scal + S_ETAMIN));
+    for (int k = 0;; ++k) {
+        const double theta = k * h->o.theta_step;
+        if (theta >= 1.0 || used >= budget) break;
+        if ((st = set_theta(h, theta))) return st;
+        if ((st = energy_now(h, &E0))) return st;
+        h->o.max_iter = budget - used < h->o.theta_every ? budget - used : h->o.theta_every;
+        status = solve_inner(h, -1.0, E0, &it, &E);
+        h->o.max_iter = budget;
+        if (status < 0 && status != STOKES_EDIVERGED) return status;
+        used += it;
+        if (status == STOKES_EDIVERGED) break;
+    }
+    if ((st = set_theta(h, 1.0))) return st;
+    if (status != STOKES_EDIVERGED && used < budget) {
+        if ((st = energy_now(h, &E0))) return st;
+        if (E0 <= rtol) {
+            E = E0;
+            status = STOKES_OK;
+        } else {
+            h->o.max_iter = budget - used;
+            status = solve_inner(h, rtol, E0, &it, &E);
+            h->o.max_iter = budget;
+            if (status < 0 && status != STOKES_EDIVERGED) return status;
+            used += it;
+        }
+    } else if (status != STOKES_EDIVERGED) {
+        status = STOKES_NOT_CONVERGED;
+    }
+    *iters = used;
+    *Eout = E;
+    return status;
+}
+}  // namespace sk
+extern "C" {
 
 // ---------------------------------------------------------------- per-step entry points
 int stokes_smooth(stokes_t h, int level, const double *bx, const double *by, double *vx, double *vy, int nsweeps) {

@@ -93,6 +93,14 @@ void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *et
 bool jacobi2_ok(const GridL &g);
 void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
                     const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega);
+// viscosity rescaling: min over the valid nodes of both caller fields
+// into *emin (as the bit pattern of a positive double, atomicMin), then the blend
+void launch_eta_min(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                    unsigned long long *emin);
+void launch_eta_blend(const LaunchCtx &c, const GridL &g, const double *ebu, const double *epu, double *etab,
+                      double *etap, const unsigned long long *emin, double theta);
+// lithostatic pressure, user P layout
+void launch_lithostatic(const LaunchCtx &c, const GridL &g, const double *rho, double gy, double *p);
 // RBGS sweep as two streamed passes, out of place (jacobi2_ok levels): (vxi, vyi) -> (vxo, vyo)
 void launch_rbgs_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
                         const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,

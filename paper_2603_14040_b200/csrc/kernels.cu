@@ -176,6 +176,45 @@ __global__ void __launch_bounds__(BX *BY) k_residual(GridL g, const double *__re
     if (i <= g.nvyi) ry[at(g, i, j)] = rhs_y(g, rhs, i, j) - ly_row(g, etab, etap, ax, ay, i, j);
 }
 
+
+// ------------------------------------------------ viscosity rescaling / lithostatic (NEXT-1)
+// eta_min over the basic nodes [0,ncy]x[0,ncx] and P nodes [1,ncy]x[1,ncx]: positive
+// doubles order like their bit patterns, so an unsigned atomicMin is exact.
+__global__ void k_eta_min(GridL g, const double *__restrict__ eb, const double *__restrict__ ep,
+                          unsigned long long *emin) {
+    const int j = blockIdx.x * BX + threadIdx.x;
+    const int i = blockIdx.y * BY + threadIdx.y;
+    double m = INFINITY;
+    if (i <= g.ncy && j <= g.ncx) {
+        m = eb[at(g, i, j)];
+        if (i >= 1 && j >= 1) m = fmin(m, ep[at(g, i, j)]);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m < INFINITY) atomicMin(emin, (unsigned long long)__double_as_longlong(m));
+}
+// eta_comp = (1 - theta) eta_min + theta eta on the same nodes
+__global__ void k_eta_blend(GridL g, const double *__restrict__ ebu, const double *__restrict__ epu,
+                            double *__restrict__ eb, double *__restrict__ ep, const unsigned long long *emin,
+                            double theta) {
+    const int j = blockIdx.x * BX + threadIdx.x;
+    const int i = blockIdx.y * BY + threadIdx.y;
+    if (i > g.ncy || j > g.ncx) return;
+    const double m = __longlong_as_double((long long)*emin);
+    eb[at(g, i, j)] = (1.0 - theta) * m + theta * ebu[at(g, i, j)];
+    if (i >= 1 && j >= 1) ep[at(g, i, j)] = (1.0 - theta) * m + theta * epu[at(g, i, j)];
+}
+// column prefix sums in row order (deterministic): one thread per P column
+__global__ void k_lithostatic(GridL g, const double *__restrict__ rb, double gy, double *__restrict__ p) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    if (j > g.ncx) return;
+    double acc = gy * (0.5 * g.dy) * (0.5 * (rb[at(g, 0, j - 1)] + rb[at(g, 0, j)]));
+    p[j - 1] = acc;
+    for (int i = 1; i < g.ncy; ++i) {
+        acc = acc + gy * g.dy * (0.5 * (rb[at(g, i, j - 1)] + rb[at(g, i, j)]));
+        p[(size_t)i * g.ncx + (j - 1)] = acc;
+    }
+}
+
 // ------------------------------------------------------------------ transfers (a5, a6, a7)
 // Normalised bilinear restriction (Alg. 2 weights; reading R6) in
 // gather form: each coarse node sums its own fine contributors, so neither the 4-colour
@@ -1048,6 +1087,22 @@ void launch_sub_mean(const LaunchCtx &c, const GridL &g, const double *mean, dou
     LAUNCH_BOOK(c);
 }
 
+void launch_eta_min(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                    unsigned long long *emin) {
+    const dim3 grid((g.ncx + 1 + BX - 1) / BX, (g.ncy + 1 + BY - 1) / BY);
+    k_eta_min<<<grid, tpb(), 0, c.stream>>>(g, etab, etap, emin);
+    LAUNCH_BOOK(c);
+}
+void launch_eta_blend(const LaunchCtx &c, const GridL &g, const double *ebu, const double *epu, double *etab,
+                      double *etap, const unsigned long long *emin, double theta) {
+    const dim3 grid((g.ncx + 1 + BX - 1) / BX, (g.ncy + 1 + BY - 1) / BY);
+    k_eta_blend<<<grid, tpb(), 0, c.stream>>>(g, ebu, epu, etab, etap, emin, theta);
+    LAUNCH_BOOK(c);
+}
+void launch_lithostatic(const LaunchCtx &c, const GridL &g, const double *rho, double gy, double *p) {
+    k_lithostatic<<<(g.ncx + 127) / 128, 128, 0, c.stream>>>(g, rho, gy, p);
+    LAUNCH_BOOK(c);
+}
 void launch_rbgs_phase(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *vx,
                        double *vy, const RhsArgs &rhs, double omega, int comp, int colour) {
     const dim3 grid((g.ncx / 2 + 1 + BX - 1) / BX, (g.ncy + BY - 1) / BY);

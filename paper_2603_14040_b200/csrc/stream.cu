@@ -596,7 +596,6 @@ struct Slot {
 // is released after its B pull, so rows s and s+1 stay resident.
 struct V3 {
     R3 A[NF], B[NF], C[NF];
-    __device__ __forceinline__ double a(int k, int dc = 0) const { return pick(A[k], dc); }
 };
 struct W1 {  // sweep-1 view
     const V3 *v;

@@ -50,6 +50,8 @@ class Opts(ctypes.Structure):
         ("gcr_restart", ctypes.c_int),
         ("max_iter", ctypes.c_int),
         ("pressure_sign", ctypes.c_int),
+        ("theta_step", ctypes.c_double),
+        ("theta_every", ctypes.c_int),
     ]
 
 
@@ -92,6 +94,7 @@ def lib(build_if_missing=True):
         "stokes_last_error": [],
         "stokes_create_dist": [I, I, D, D, pi, I, I, I, P, ctypes.POINTER(Opts), P, ctypes.POINTER(P)],
         "stokes_nccl_unique_id": [P],
+        "stokes_lithostatic": [P, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -108,7 +111,8 @@ EXPORTED = ["stokes_opts_default", "stokes_workspace_bytes", "stokes_create", "s
             "stokes_set_gravity", "stokes_apply_operator", "stokes_residual", "stokes_vcycle", "stokes_solve",
             "stokes_smooth", "stokes_level_residual", "stokes_restrict", "stokes_prolong",
             "stokes_get_viscosity", "stokes_coarse_solve", "stokes_launch_count", "stokes_time_kernel",
-            "stokes_strerror", "stokes_last_error", "stokes_create_dist", "stokes_nccl_unique_id"]
+            "stokes_strerror", "stokes_last_error", "stokes_create_dist", "stokes_nccl_unique_id",
+            "stokes_lithostatic"]
 
 
 def default_opts(**kw):
@@ -334,6 +338,13 @@ class Stokes:
         return vx, vy
 
     # ------------------------------------------------------------ instrumentation
+    def lithostatic(self):
+        """lithostatic pressure p = int_0^y rho g_y dy', the paper's initial
+        guess with gravity: pass it as solve(p=...)"""
+        p = self._empty("p", 0)
+        _check(lib().stokes_lithostatic(self._h, self._p(p)), "lithostatic")
+        return p
+
     def launch_count(self, reset=False):
         c = ctypes.c_longlong()
         _check(lib().stokes_launch_count(self._h, ctypes.byref(c), int(reset)), "launch_count")

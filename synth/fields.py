@@ -29,7 +29,7 @@ import math
 
 import numpy as np
 
-WORKLOADS = ("mms", "block", "solcx", "layered", "random", "parity")
+WORKLOADS = ("mms", "block", "solcx", "layered", "random", "sinker", "parity")
 
 
 def _coords(n, h, off, start=0, count=None):
@@ -68,6 +68,15 @@ def mms_density(nx, ny, Lx=1.0, Ly=1.0, win=None):
 def _block_eta(y, x):
     inside = (x >= 3 / 8) & (x <= 5 / 8) & (y >= 3 / 8) & (y <= 5 / 8)
     return np.where(inside, 1e3, 1.0), np.where(inside, 1.0, 0.0)
+
+
+def _sinker(y, x):
+    """PAPER.md:1740-1759 nondimensionalised (length 100 km, viscosity 1e18 Pa s, density
+    1000 kg/m^3, g = 10 m/s^2 -> 1): circular inclusion of radius 0.2 centred in the unit
+    box, eta 1e8 / 1, FULL density 3.3 / 3.2 (no anomaly split: the lithostatic pressure
+    initial guess of PAPER.md:1250 matters)."""
+    inside = (x - 0.5) ** 2 + (y - 0.5) ** 2 <= 0.2 ** 2
+    return np.where(inside, 1e8, 1.0), np.where(inside, 3.3, 3.2)
 
 
 def _solcx_eta(y, x):
@@ -140,6 +149,9 @@ def workload(name, nx, ny, Lx=None, Ly=None, win_b=None, win_p=None):
         eb = 10.0 ** _random_log_eta(yb, xb, modes)
         ep = 10.0 ** _random_log_eta(yp, xp, modes)
         rho = np.sin(math.pi * yb) * np.cos(math.pi * xb)
+    elif name == "sinker":
+        eb, rho = _sinker(yb, xb)
+        ep, _ = _sinker(yp, xp)
     elif name == "parity":
         f = parity_fields(nx, ny)
         eb, ep, rho = f["eta_b"], f["eta_p"], f["rho_b"]

@@ -210,6 +210,66 @@ def test_fused_uzawa_fixed_iterations(S, nx, ny, k):
         assert rel(b[key], a[key]) <= 1e-10, key
 
 
+@pytest.mark.parametrize("name,n,opts", [
+    ("block", 64, dict(omega_v=0.6, alpha_p=1.0)),
+    ("layered", 128, dict(omega_v=0.6, alpha_p=1.0)),
+    ("block", 128, dict(omega_v=0.6, alpha_p=1.0, accel=1, gcr_restart=20)),
+])
+def test_viscosity_rescaling_parity(S, name, n, opts):
+    """theta stages 0, .25, .5, .75 of 10 iterations, then theta = 1 (PAPER.md:1771 with a
+    shorter stage): same iteration count, same iterate at a fixed count, same fixed point."""
+    opts = dict(opts, theta_step=0.25, theta_every=10)
+    w = workload(name, n, n)
+    o, s = pair(S, n, n, w["bc"], w, w["Lx"], w["Ly"], (w["gx"], w["gy"]), **opts)
+    a, b = o.solve(1e-8), s.solve(1e-8)
+    assert a["status"] == 0 and b["status"] == 0
+    assert abs(a["iters"] - b["iters"]) <= 1 and a["iters"] >= 40
+    k = a["iters"]
+    o2, s2 = pair(S, n, n, w["bc"], w, w["Lx"], w["Ly"], (w["gx"], w["gy"]), **dict(opts, max_iter=k))
+    a2, b2 = o2.solve(0.0), s2.solve(0.0)
+    bar = 1e-8 if opts.get("accel", 0) else 1e-9
+    for key in ("vx", "vy", "p"):
+        assert rel(b2[key], a2[key]) <= bar, key
+    eb, ep = s.get_viscosity(0)  # theta = 1 restored the caller's field exactly
+    assert torch.equal(eb.cpu(), torch.from_numpy(w["eta_b"])) and torch.equal(ep.cpu(), torch.from_numpy(w["eta_p"]))
+
+
+@pytest.mark.parametrize("smoother", [0, 1])
+def test_sinker_paper_configuration_parity(S, smoother):
+    """The paper's robustness setting at 100 x 120 cells: contrast 1e8,
+    full density, sweep growth 2.5, coarsest by smoothing, omega_v 0.3, omega_p 0.6, theta
+    stages every 25 iterations, lithostatic initial pressure; 150 iterations on both sides."""
+    nx, ny = 100, 120
+    w = workload("sinker", nx, ny)
+    opts = dict(omega_v=0.3, alpha_p=0.6, nu_growth=2.5, coarse_direct=0, smoother=smoother, theta_step=0.25,
+                theta_every=25, max_iter=150)
+    o, s = pair(S, nx, ny, w["bc"], w, w["Lx"], w["Ly"], (w["gx"], w["gy"]), **opts)
+    p0 = o.lithostatic()
+    assert rel(s.lithostatic(), p0) <= 1e-13
+    a = o.solve(0.0, p=p0)
+    b = s.solve(0.0, p=torch.from_numpy(p0).cuda())
+    assert a["iters"] == b["iters"] == 150
+    assert abs(a["E"] - b["E"]) <= 1e-6 * a["E"]
+    for key in ("vx", "vy", "p"):
+        assert rel(b[key], a[key]) <= 1e-8, key
+
+
+@pytest.mark.parametrize("nx,ny", [(33, 17), (256, 200)])
+def test_lithostatic_parity(S, nx, ny):
+    f = parity_fields(nx, ny)
+    o, s = pair(S, nx, ny, (0, 1, 0, 1), f, 1.0, 0.7, (0.2, 1.3), coarse_direct=0)
+    ex = o.lithostatic()
+    got = s.lithostatic()
+    assert rel(got, ex) <= 1e-13
+    # the paper's initial guess: solve from (0, p_litho) on both sides
+    w = workload("layered", 128, 128)
+    o, s = pair(S, 128, 128, w["bc"], w, w["Lx"], w["Ly"], (w["gx"], w["gy"]), omega_v=0.6, alpha_p=1.0)
+    p0 = o.lithostatic()
+    a = o.solve(1e-8, p=p0)
+    b = s.solve(1e-8, p=torch.from_numpy(p0).cuda())
+    assert a["status"] == 0 and b["status"] == 0 and abs(a["iters"] - b["iters"]) <= 1
+
+
 def test_error_paths(S):
     from paper_2603_14040_b200 import StokesError
     with pytest.raises(StokesError):

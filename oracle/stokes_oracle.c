@@ -55,6 +55,8 @@ typedef struct {
     int pressure_sign;   /* +1 physical reading R3 (default); -1 literal PAPER.md:824 */
     double theta_step;   /* viscosity rescaling: theta += step per stage, 0 = off */
     int theta_every;     /* Uzawa iterations per stage before theta = 1 (25) */
+    int aa_depth;        /* Anderson acceleration (accel = 2, Alg. 5): depth m */
+    double aa_beta;      /* Anderson mixing beta in (0, 1] */
 } oracle_opts;
 
 typedef struct {
@@ -567,6 +569,8 @@ int oracle_opts_default(oracle_opts *o) {
     o->pressure_sign = 1;
     o->theta_step = 0.0;
     o->theta_every = 25;
+    o->aa_depth = 5;
+    o->aa_beta = 0.7;
     return O_OK;
 }
 
@@ -587,7 +591,8 @@ int oracle_create(int nx, int ny, double Lx, double Ly, const int *bc, const ora
     memcpy(S->bc, bc, sizeof(S->bc));
     if (opts) S->o = *opts; else oracle_opts_default(&S->o);
     if (S->o.nu1 < 0 || S->o.coarse_min < 2 || S->o.vcycles_per_iter < 1 || S->o.gcr_restart < 1 ||
-        !(S->o.theta_step >= 0.0 && S->o.theta_step <= 1.0) || S->o.theta_every < 1) {
+        !(S->o.theta_step >= 0.0 && S->o.theta_step <= 1.0) || S->o.theta_every < 1 || S->o.accel < 0 ||
+        S->o.accel > 2 || S->o.aa_depth < 0 || S->o.aa_depth > 15 || !(S->o.aa_beta > 0.0 && S->o.aa_beta <= 1.0)) {
         free(S);
         return O_EINVAL;
     }
@@ -1009,6 +1014,134 @@ static int solve_gcr(oracle_t *S, double rtol, double Sf, double E0, int *iters,
 /* solve(rtol): in = initial guess (v, p), out = solution; zero-mean p on exit.
  * iters = number of V-cycle applications ("preconditioner applications" in GCR mode).
  * hist (optional): E after every iteration. */
+/* Anderson acceleration AA(m) with mixing beta, Alg. 5, reading R26.
+ * G(x) = one Uzawa iteration (V-cycle on L v = f - G p, p += alpha eta_P r_p, de-mean),
+ * x = (vx, vy, p).  x^1 = G(x^0); for k >= 1: m_k = min(m, k), R = [r^{k-m_k} .. r^k] with
+ * r^i = G(x^i) - x^i, alpha = argmin ||R alpha||_2 subject to 1^T alpha = 1, solved as
+ * (R^T R + lambda I) z = 1, alpha = z / 1^T z (lambda = 1e-10 max diag: rank-deficient
+ * histories), x^{k+1} = (1 - beta) sum alpha_i x^i + beta sum alpha_i G(x^i), de-meaned.
+ * <.,.> Euclidean over the unknowns (R13).  Stopping test on the energy residual of the
+ * newest G(x^k) (computed by the Uzawa step), which is returned; iterations = G calls. */
+static void aa_copy(const olevel *L, ovec d, const double *vx, const double *vy, const double *p) {
+    size_t n = padn(L);
+    memcpy(d.x, vx, n * sizeof(double));
+    memcpy(d.y, vy, n * sizeof(double));
+    memcpy(d.p, p, n * sizeof(double));
+}
+/* solve (H + lambda I) z = 1 by Gaussian elimination with partial pivoting; alpha = z / sum z */
+static int aa_alpha(int n, const double *H, double *alpha) {
+    double A[16][17];
+    double dmax = 0.0;
+    for (int i = 0; i < n; ++i) dmax = fmax(dmax, H[i * n + i]);
+    double lam = 1e-10 * dmax;
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) A[i][j] = H[i * n + j] + (i == j ? lam : 0.0);
+        A[i][n] = 1.0;
+    }
+    for (int c = 0; c < n; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < n; ++r) if (fabs(A[r][c]) > fabs(A[piv][c])) piv = r;
+        if (!(fabs(A[piv][c]) > 0.0)) return -1;
+        if (piv != c) for (int j = 0; j <= n; ++j) { double t = A[c][j]; A[c][j] = A[piv][j]; A[piv][j] = t; }
+        for (int r = c + 1; r < n; ++r) {
+            double f = A[r][c] / A[c][c];
+            for (int j = c; j <= n; ++j) A[r][j] -= f * A[c][j];
+        }
+    }
+    double z[16], sz = 0.0;
+    for (int i = n - 1; i >= 0; --i) {
+        double t = A[i][n];
+        for (int j = i + 1; j < n; ++j) t -= A[i][j] * z[j];
+        z[i] = t / A[i][i];
+    }
+    for (int i = 0; i < n; ++i) sz += z[i];
+    if (!(fabs(sz) > 0.0)) return -1;
+    for (int i = 0; i < n; ++i) alpha[i] = z[i] / sz;
+    return 0;
+}
+static int solve_anderson(oracle_t *S, double rtol, double Sf, double E0, int *iters, double *E_out, double *hist,
+                          int hist_len) {
+    olevel *L = &S->lev[0];
+    size_t n = padn(L);
+    const int m = S->o.aa_depth, ns = m + 1;
+    const double beta = S->o.aa_beta;
+    ovec *X = (ovec *)calloc(ns, sizeof(ovec)), *GX = (ovec *)calloc(ns, sizeof(ovec));
+    ovec *R = (ovec *)calloc(ns, sizeof(ovec));
+    for (int i = 0; i < ns; ++i) { X[i] = ovec_new(n); GX[i] = ovec_new(n); R[i] = ovec_new(n); }
+    double *bx = zalloc(n), *by = zalloc(n), *rx = zalloc(n), *ry = zalloc(n), *rp = zalloc(n);
+    double H[16 * 16], alpha[16];
+    int status = O_NOT_CONVERGED, k;
+    double E = E0;
+    for (k = 0; k < S->o.max_iter; ++k) {
+        const int slot = k % ns;
+        aa_copy(L, X[slot], S->vx, S->vy, S->p);  /* x^k */
+        /* G(x^k): one Uzawa iteration (as solve_uzawa) */
+        FOR_VX(L) bx[IX(L, i, j)] = S->fx[IX(L, i, j)] - Gx_point(L, S->p, i, j);
+        FOR_VY(L) by[IX(L, i, j)] = S->fy[IX(L, i, j)] - Gy_point(L, S->p, i, j);
+        for (int c = 0; c < S->o.vcycles_per_iter; ++c) vcycle_level(S, 0, S->vx, S->vy, bx, by);
+        FOR_P(L) {
+            double r = -D_point(L, S->vx, S->vy, i, j);
+            S->p[IX(L, i, j)] += S->o.pressure_sign * S->o.alpha_p * L->etap[IX(L, i, j)] * r;
+        }
+        double pm = p_mean(L, S->p);
+        FOR_P(L) S->p[IX(L, i, j)] -= pm;
+        full_residual(S, S->vx, S->vy, S->p, rx, ry, rp);
+        E = energy_of(S, rx, ry, rp, Sf);
+        if (hist && k < hist_len) hist[k] = E;
+        if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = O_EDIVERGED; break; }
+        if (E <= rtol) { status = O_OK; break; }
+        aa_copy(L, GX[slot], S->vx, S->vy, S->p);  /* G(x^k) */
+        FOR_VX(L) R[slot].x[IX(L, i, j)] = GX[slot].x[IX(L, i, j)] - X[slot].x[IX(L, i, j)];
+        FOR_VY(L) R[slot].y[IX(L, i, j)] = GX[slot].y[IX(L, i, j)] - X[slot].y[IX(L, i, j)];
+        FOR_P(L) R[slot].p[IX(L, i, j)] = GX[slot].p[IX(L, i, j)] - X[slot].p[IX(L, i, j)];
+        if (k == 0) continue;  /* x^1 = G(x^0): the working fields already hold it */
+        const int mk = k < m ? k : m, nn = mk + 1;
+        for (int a = 0; a < nn; ++a)
+            for (int b = 0; b < nn; ++b) {
+                const int sa = (k - mk + a) % ns, sb = (k - mk + b) % ns;
+                H[a * nn + b] = ovec_dot(L, R[sa], R[sb]);
+            }
+        if (aa_alpha(nn, H, alpha) != 0) continue;  /* degenerate history: plain step */
+        /* x^{k+1} = (1 - beta) sum alpha_i x^i + beta sum alpha_i G(x^i) (unknowns; mirrors refreshed) */
+        FOR_VX(L) {
+            double sx = 0.0, sg = 0.0;
+            for (int a = 0; a < nn; ++a) {
+                const int sa = (k - mk + a) % ns;
+                sx += alpha[a] * X[sa].x[IX(L, i, j)];
+                sg += alpha[a] * GX[sa].x[IX(L, i, j)];
+            }
+            S->vx[IX(L, i, j)] = (1.0 - beta) * sx + beta * sg;
+        }
+        FOR_VY(L) {
+            double sx = 0.0, sg = 0.0;
+            for (int a = 0; a < nn; ++a) {
+                const int sa = (k - mk + a) % ns;
+                sx += alpha[a] * X[sa].y[IX(L, i, j)];
+                sg += alpha[a] * GX[sa].y[IX(L, i, j)];
+            }
+            S->vy[IX(L, i, j)] = (1.0 - beta) * sx + beta * sg;
+        }
+        FOR_P(L) {
+            double sx = 0.0, sg = 0.0;
+            for (int a = 0; a < nn; ++a) {
+                const int sa = (k - mk + a) % ns;
+                sx += alpha[a] * X[sa].p[IX(L, i, j)];
+                sg += alpha[a] * GX[sa].p[IX(L, i, j)];
+            }
+            S->p[IX(L, i, j)] = (1.0 - beta) * sx + beta * sg;
+        }
+        refresh_mirrors(S, L, S->vx, S->vy);
+        pm = p_mean(L, S->p);
+        FOR_P(L) S->p[IX(L, i, j)] -= pm;
+    }
+    if (k >= S->o.max_iter) k = S->o.max_iter - 1;
+    *iters = k + 1;
+    *E_out = E;
+    for (int i = 0; i < ns; ++i) { ovec_free(X[i]); ovec_free(GX[i]); ovec_free(R[i]); }
+    free(X); free(GX); free(R); free(bx); free(by); free(rx); free(ry); free(rp);
+    return status;
+}
+
 int oracle_solve_hist(oracle_t *S, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy,
                       double *hist, int hist_len) {
     if (!S || !iters || !rel_energy) return O_EINVAL;
@@ -1052,9 +1185,10 @@ int oracle_solve_hist(oracle_t *S, double rtol, double *vx, double *vy, double *
             free(rx); free(ry); free(rp);
             S->o.max_iter = budget - used < S->o.theta_every ? budget - used : S->o.theta_every;
             int hoff = used < hist_len ? used : hist_len;
-            status = S->o.accel == 1
-                         ? solve_gcr(S, -1.0, Sfk, E0k, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff)
-                         : solve_uzawa(S, -1.0, Sfk, E0k, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff);
+            status = S->o.accel == 1   ? solve_gcr(S, -1.0, Sfk, E0k, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff)
+                     : S->o.accel == 2 ? solve_anderson(S, -1.0, Sfk, E0k, &it, &E, hist ? hist + hoff : NULL,
+                                                        hist_len - hoff)
+                                       : solve_uzawa(S, -1.0, Sfk, E0k, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff);
             S->o.max_iter = budget;
             used += it;
             if (status == O_EDIVERGED) break;
@@ -1070,9 +1204,10 @@ int oracle_solve_hist(oracle_t *S, double rtol, double *vx, double *vy, double *
             else {
                 S->o.max_iter = budget - used;
                 int hoff = used < hist_len ? used : hist_len;
-                status = S->o.accel == 1
-                             ? solve_gcr(S, rtol, Sf, E1, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff)
-                             : solve_uzawa(S, rtol, Sf, E1, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff);
+                status = S->o.accel == 1   ? solve_gcr(S, rtol, Sf, E1, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff)
+                         : S->o.accel == 2 ? solve_anderson(S, rtol, Sf, E1, &it, &E, hist ? hist + hoff : NULL,
+                                                            hist_len - hoff)
+                                           : solve_uzawa(S, rtol, Sf, E1, &it, &E, hist ? hist + hoff : NULL, hist_len - hoff);
                 S->o.max_iter = budget;
             }
             used += it;
@@ -1083,6 +1218,7 @@ int oracle_solve_hist(oracle_t *S, double rtol, double *vx, double *vy, double *
         *rel_energy = E;
     }
     else if (S->o.accel == 1) status = solve_gcr(S, rtol, Sf, E0, iters, rel_energy, hist, hist_len);
+    else if (S->o.accel == 2) status = solve_anderson(S, rtol, Sf, E0, iters, rel_energy, hist, hist_len);
     else status = solve_uzawa(S, rtol, Sf, E0, iters, rel_energy, hist, hist_len);
     double m = p_mean(L, S->p);
     FOR_P(L) S->p[IX(L, i, j)] -= m;

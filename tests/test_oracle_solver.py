@@ -88,7 +88,8 @@ def test_mms_no_slip_second_order():
 
 
 @pytest.mark.parametrize("n,bc,accel", [(4, (0, 0, 0, 0), 0), (8, (1, 1, 1, 1), 0), (16, (0, 1, 1, 0), 0),
-                                        (8, (0, 0, 0, 0), 1), (16, (1, 0, 0, 1), 1)])
+                                        (8, (0, 0, 0, 0), 1), (16, (1, 0, 0, 1), 1),
+                                        (8, (1, 0, 1, 0), 2), (16, (0, 0, 1, 1), 2)])
 def test_fixed_point_is_dense_solution(n, bc, accel):
     f = parity_fields(n, n, log_contrast=1.5)
     # i.i.d. 1e3-contrast eta: lambda_max(C^-1 L) ~ 3.4, so omega_v < 0.59 (see jacobi test)

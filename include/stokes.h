@@ -70,7 +70,7 @@ enum {
 };
 
 enum { STOKES_SMOOTH_JACOBI = 0, STOKES_SMOOTH_RBGS = 1 };
-enum { STOKES_ACCEL_NONE = 0, STOKES_ACCEL_GCR = 1 };
+enum { STOKES_ACCEL_NONE = 0, STOKES_ACCEL_GCR = 1, STOKES_ACCEL_ANDERSON = 2 };
 
 /* Solver options.  stokes_opts_default() fills the paper's setting (PAPER.md:1765-1788:
  * omega_v 0.3, omega_p 0.6, 5+5 sweeps) with the readings of DESIGN.md §3 (growth g = 1,
@@ -84,7 +84,7 @@ typedef struct {
     int coarse_min;       /* coarsen by 2 while both sizes even and min(nx,ny)/2 >= coarse_min  */
     int coarse_direct;    /* 1: exact coarsest solve (reading R10); 0: 2*nu_L smoothing sweeps  */
     int vcycles_per_iter; /* V-cycles per Uzawa step                            */
-    int accel;            /* STOKES_ACCEL_NONE (plain Uzawa) or STOKES_ACCEL_GCR                */
+    int accel;            /* STOKES_ACCEL_NONE (plain Uzawa), _GCR or _ANDERSON (single domain)  */
     int gcr_restart;      /* m of GCR(m)                                                        */
     int max_iter;         /* cap on iterations (V-cycle applications)                           */
     int pressure_sign;    /* +1 physical reading R3 (default); -1 literal PAPER.md:824 (diverges) */
@@ -92,6 +92,8 @@ typedef struct {
                              < 1 with eta_comp = (1-theta) eta_min + theta eta, then theta = 1;
                              0 = off (default).  Single-domain handles only                      */
     int theta_every;      /* Uzawa / GCR iterations per stage before theta = 1 (25) */
+    int aa_depth;         /* STOKES_ACCEL_ANDERSON (Alg. 5): depth m, 0..15   */
+    double aa_beta;       /* Anderson mixing beta in (0, 1] (0.5-0.8)              */
 } stokes_opts;
 
 /* Fill *o with the defaults.  Returns STOKES_EINVAL if o is NULL. */

@@ -75,7 +75,8 @@ int check_opts(const stokes_opts &o) {
     if (o.smoother != 0 && o.smoother != 1) return STOKES_EINVAL;
     if (!(o.omega_v > 0) || !(o.alpha_p > 0) || o.nu1 < 0 || !(o.nu_growth > 0) || o.coarse_min < 2) return STOKES_EINVAL;
     if (o.coarse_direct != 0 && o.coarse_direct != 1) return STOKES_EINVAL;
-    if (o.vcycles_per_iter < 1 || (o.accel != 0 && o.accel != 1)) return STOKES_EINVAL;
+    if (o.vcycles_per_iter < 1 || o.accel < 0 || o.accel > 2) return STOKES_EINVAL;
+    if (o.aa_depth < 0 || o.aa_depth >= AA_MAXS || !(o.aa_beta > 0.0 && o.aa_beta <= 1.0)) return STOKES_EINVAL;
     if (o.gcr_restart < 1 || o.gcr_restart > MAXM || o.max_iter < 0) return STOKES_EINVAL;
     if (o.pressure_sign != 1 && o.pressure_sign != -1) return STOKES_EINVAL;
     if (!(o.theta_step >= 0.0 && o.theta_step <= 1.0) || o.theta_every < 1) return STOKES_EINVAL;
@@ -121,6 +122,17 @@ size_t carve(stokes_s *h, Carver &cv) {
         h->Minv = h->Mwork = nullptr;
     }
     h->dflag = (int *)cv.take(4);
+    if (h->o.accel == STOKES_ACCEL_ANDERSON) {
+        for (int i = 0; i <= h->o.aa_depth; ++i)
+            for (int f = 0; f < 3; ++f) {
+                h->aah.G[i].f[f] = cv.field(g0);
+                h->aah.R[i].f[f] = cv.field(g0);
+            }
+        for (int f = 0; f < 3; ++f) h->aat.f[f] = cv.field(g0);
+        h->aaH = cv.take(AA_MAXS * AA_MAXS);
+        h->aacg = cv.take(AA_MAXS);
+        h->aacr = cv.take(AA_MAXS);
+    }
     if (h->o.accel == STOKES_ACCEL_GCR) {
         for (int i = 0; i < h->o.gcr_restart; ++i)
             for (int f = 0; f < 3; ++f) {
@@ -355,7 +367,7 @@ void drop_graphs(stokes_s *h) {
         }
 }
 
-int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+int ensure_uzawa_graphs(stokes_s *h) {
     // capture one iteration per pressure buffer into CUDA graphs (the coarse levels are
     // launch-bound), replay them alternately
     const int keep = h->pcur;
@@ -378,6 +390,12 @@ int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
             return fail_cuda(e, "graph instantiate");
         }
     }
+    return STOKES_OK;
+}
+
+int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+    int st = ensure_uzawa_graphs(h);
+    if (st) return st;
     double E = E0;
     int k;
     int status = STOKES_NOT_CONVERGED;
@@ -385,7 +403,7 @@ int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
         CK(cudaGraphLaunch(h->uzawa_exec[h->pcur], h->stream));
         h->pcur ^= 1;
         h->launches += h->uzawa_kernels;
-        int st = sync(h);
+        st = sync(h);
         if (st) return st;
         E = h->hscal[S_E];
         if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
@@ -635,6 +653,8 @@ int stokes_opts_default(stokes_opts *o) {
     o->pressure_sign = 1;
     o->theta_step = 0.0;
     o->theta_every = 25;
+    o->aa_depth = 5;
+    o->aa_beta = 0.7;
     return STOKES_OK;
 }
 
@@ -927,9 +947,59 @@ int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int
 }  // extern "C"
 namespace sk {
 int solve_inner(stokes_s *h, double rtol, double E0, int *iters, double *E) {
+    if (h->o.accel == STOKES_ACCEL_ANDERSON) return solve_anderson(h, rtol, E0, iters, E);
     if (h->o.accel == STOKES_ACCEL_GCR)
         return stream_ok(h->lev[0].g) ? solve_gcr_fused(h, rtol, E0, iters, E) : solve_gcr(h, rtol, E0, iters, E);
     return fused_ok(h) ? solve_uzawa_fused(h, rtol, E0, iters, E) : solve_uzawa(h, rtol, E0, iters, E);
+}
+// Anderson acceleration AA(m, beta) over the Uzawa map G (Alg. 5, PAPER.md:1502-1588,
+// reading R26; the oracle's solve_anderson): per iteration one graph-replayed Uzawa step
+// x^k -> G(x^k) with its energy residual (the stopping test, G(x^k) returned), then
+// push (G_k, R_k, Gram row), the tiny constrained least squares, and the mixed update.
+int solve_anderson(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+    int st = ensure_uzawa_graphs(h);
+    if (st) return st;
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    const int m = h->o.aa_depth, ns = m + 1;
+    const size_t fb = field_doubles(F.g) * 8;
+    // T = x^0 (its pressure mean = S_MSHIFT, from energy_now)
+    CK(cudaMemcpyAsync(h->aat.f[0] - COL_OFF, F.vx[0] - COL_OFF, fb, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->aat.f[1] - COL_OFF, F.vy[0] - COL_OFF, fb, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->aat.f[2] - COL_OFF, h->pbuf[h->pcur] - COL_OFF, fb, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->scal + S_AAMT, h->scal + S_MSHIFT, 8, cudaMemcpyDeviceToDevice, h->stream));
+    const int nb = aa_blocks(F.g);
+    const double inv_np = 1.0 / ((double)F.g.ncx * F.g.ncy);
+    double E = E0;
+    int k, status = STOKES_NOT_CONVERGED;
+    for (k = 0; k < h->o.max_iter; ++k) {
+        CK(cudaGraphLaunch(h->uzawa_exec[h->pcur], h->stream));  // G(x^k), E of it
+        h->pcur ^= 1;
+        h->launches += h->uzawa_kernels;
+        if ((st = sync(h))) return st;
+        E = h->hscal[S_E];
+        if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+        if (E <= rtol) { status = STOKES_OK; break; }
+        const int slot = k % ns, mk = k < m ? k : m;
+        AAWin win;
+        win.n = mk + 1;
+        win.self = mk;
+        for (int a = 0; a <= mk; ++a) {
+            win.slot[a] = (k - mk + a) % ns;
+            win.r[a] = h->aah.R[win.slot[a]];
+        }
+        const AAVec work{{F.vx[0], F.vy[0], h->pbuf[h->pcur]}};
+        launch_aa_push(c, F.g, work, h->scal + S_MSHIFT, h->aat, h->scal + S_AAMT, h->aah.G[slot], h->aah.R[slot],
+                       win, h->partials);
+        launch_aa_solve(c, h->partials, nb, win, h->o.aa_beta, h->aaH, h->aacg, h->aacr);
+        launch_aa_update(c, F.g, h->aah, ns, h->aacg, h->aacr, work, h->aat, h->partials);
+        launch_finalize(c, h->partials, nb, 1, inv_np, h->scal + S_MSHIFT);  // lazy de-mean of x^{k+1}
+        CK(cudaMemcpyAsync(h->scal + S_AAMT, h->scal + S_MSHIFT, 8, cudaMemcpyDeviceToDevice, h->stream));
+    }
+    if (k >= h->o.max_iter) k = h->o.max_iter - 1;
+    *iters = k + 1;
+    *Eout = E;
+    return status;
 }
 // computational viscosity (1 - theta) eta_min + theta eta and its hierarchy
 int set_theta(stokes_s *h, double theta) {

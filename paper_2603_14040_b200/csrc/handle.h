@@ -15,7 +15,7 @@ extern thread_local std::string g_last_error;
 
 // device scalar slots
 enum { S_MSHIFT = 0, S_E = 1, S_SV = 2, S_SP = 3, S_SF = 4, S_SFPART = 5, S_ZMEAN = 8, S_GAMMA = 9, S_NU2 = 10, S_LOC = 16,
-       S_RR = 11, S_BETA = 12, S_ZERO = 13, S_E0 = 14, S_ETAMIN = 24, S_NSCAL = 64 };
+       S_RR = 11, S_BETA = 12, S_ZERO = 13, S_E0 = 14, S_ETAMIN = 24, S_AAMT = 25, S_NSCAL = 64 };
 
 struct Level {
     GridL g;
@@ -42,6 +42,9 @@ struct stokes_s {
     sk::Level lev[MAXLEV];
     double *pbuf[2], *rho;  // pressure ping-pong (the fused Uzawa pass reads one, writes the other)
     double *etab_user, *etap_user;  // the caller's fine viscosities (theta_step > 0: rescaling)
+    AAHist aah;                     // Anderson history slots (accel = ANDERSON)
+    AAVec aat;                      // Anderson: x^k (de-meaned pressure at mean S_AAMT)
+    double *aaH, *aacg, *aacr;      // Gram matrix (slot-indexed), mixing coefficients
     int pcur;
     double *partials;
     size_t npart;
@@ -101,6 +104,7 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
 int sync(stokes_s *h);
 int build_hierarchy(stokes_s *h);
 int solve_inner(stokes_s *h, double rtol, double E0, int *iters, double *E);
+int solve_anderson(stokes_s *h, double rtol, double E0, int *iters, double *E);
 int solve_staged(stokes_s *h, double rtol, int *iters, double *E);
 void drop_graphs(stokes_s *h);
 void force_energy(stokes_s *h);

@@ -93,6 +93,26 @@ void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *et
 bool jacobi2_ok(const GridL &g);
 void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
                     const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega);
+// Anderson acceleration (aa.cu): ring of AA_MAXS history slots of three padded fields
+constexpr int AA_MAXS = 16;
+struct AAVec {
+    double *f[3];
+};
+struct AAWin {  // the history window, oldest -> newest; member `self` is the new slot
+    int n, self;
+    int slot[AA_MAXS];
+    AAVec r[AA_MAXS];
+};
+struct AAHist {
+    AAVec G[AA_MAXS], R[AA_MAXS];
+};
+int aa_blocks(const GridL &g);
+void launch_aa_push(const LaunchCtx &c, const GridL &g, const AAVec &work, const double *ms_g, const AAVec &T,
+                    const double *ms_t, const AAVec &Gk, const AAVec &Rk, const AAWin &win, double *partials);
+void launch_aa_solve(const LaunchCtx &c, const double *partials, int nblocks, const AAWin &win, double beta,
+                     double *H, double *cg, double *cr);
+void launch_aa_update(const LaunchCtx &c, const GridL &g, const AAHist &hist, int ns, const double *cg,
+                      const double *cr, const AAVec &work, const AAVec &T, double *partials);
 // viscosity rescaling: min over the valid nodes of both caller fields
 // into *emin (as the bit pattern of a positive double, atomicMin), then the blend
 void launch_eta_min(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,

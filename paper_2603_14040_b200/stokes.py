@@ -52,6 +52,8 @@ class Opts(ctypes.Structure):
         ("pressure_sign", ctypes.c_int),
         ("theta_step", ctypes.c_double),
         ("theta_every", ctypes.c_int),
+        ("aa_depth", ctypes.c_int),
+        ("aa_beta", ctypes.c_double),
     ]
 
 

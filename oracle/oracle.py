@@ -44,6 +44,9 @@ class Opts(ctypes.Structure):
         ("theta_every", ctypes.c_int),
         ("aa_depth", ctypes.c_int),
         ("aa_beta", ctypes.c_double),
+        ("ras_tile", ctypes.c_int),
+        ("ras_inner", ctypes.c_int),
+        ("ras_seed", ctypes.c_uint64),
     ]
 
 

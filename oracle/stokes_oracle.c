@@ -41,7 +41,8 @@
 #define MAXLEV 24
 
 typedef struct {
-    int smoother;        /* 0 damped Jacobi, 1 RBGS 4-phase */
+    int smoother;        /* 0 damped Jacobi, 1 RBGS 4-phase, 2 RAS-type temporal blocking (Alg. 3),
+                            3 mixed: Jacobi on the finest level, RAS on the coarser ones */
     double omega_v;      /* velocity relaxation */
     double alpha_p;      /* pressure relaxation (omega_p) */
     int nu1;             /* sweeps on the finest level (pre and post) */
@@ -57,6 +58,9 @@ typedef struct {
     int theta_every;     /* Uzawa iterations per stage before theta = 1 (25) */
     int aa_depth;        /* Anderson acceleration (accel = 2, Alg. 5): depth m */
     double aa_beta;      /* Anderson mixing beta in (0, 1] */
+    int ras_tile;        /* RAS tile edge T_I = T_J in cells (32) */
+    int ras_inner;       /* RAS inner iterations T_inner (4) */
+    uint64_t ras_seed;   /* seed of the counter-based tile-shift generator (reading R27) */
 } oracle_opts;
 
 typedef struct {
@@ -87,6 +91,8 @@ typedef struct {
     double *vx, *vy, *p;
     /* the caller's viscosities (padded, fine) -- viscosity rescaling blends from them */
     double *etab_user, *etap_user;
+    /* RAS shift counter: draw index q = ras_k * 65536 + ras_c (reading R27) */
+    int ras_k, ras_c;
 } oracle_t;
 
 /* ------------------------------------------------------------------ helpers */
@@ -256,9 +262,97 @@ static void smooth_rbgs(const oracle_t *S, olevel *L, double *vx, double *vy, co
         }
     }
 }
-static void smooth(const oracle_t *S, olevel *L, double *vx, double *vy, const double *bx, const double *by,
-                   int nu) {
-    if (S->o.smoother == 1) smooth_rbgs(S, L, vx, vy, bx, by, nu);
+/* RAS-type temporal blocking, Alg. 3, reading R27.  N_outer =
+ * ceil(nu / T_inner), made even; per outer iteration a shift (s_i, s_j) in [0, T)^2 from
+ * the counter-based generator below partitions the cells into tiles ((i-1+s_i) div T,
+ * (j-1+s_j) div T), clipped at the walls; a vx / vy node belongs to the tile of its cell
+ * (i, j).  Each tile runs T_inner damped-Jacobi sweeps on its own unknowns with every
+ * value outside the tile frozen at the start of the outer iteration (its mirrors follow
+ * the tile's own values), then writes its unknowns back (single writer). */
+static uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static void ras_shift(oracle_t *S, int *si, int *sj) {
+    const uint64_t q = (uint64_t)S->ras_k * 65536u + (uint64_t)(S->ras_c++);
+    const uint64_t u = splitmix64(S->o.ras_seed ^ (q * 0x9E3779B97F4A7C15ull));
+    *si = (int)((u & 0xffffffffull) % (uint64_t)S->o.ras_tile);
+    *sj = (int)((u >> 32) % (uint64_t)S->o.ras_tile);
+}
+static void smooth_ras(oracle_t *S, olevel *L, double *vx, double *vy, const double *bx, const double *by, int nu) {
+    const int T = S->o.ras_tile, Tin = S->o.ras_inner;
+    int nout = (nu + Tin - 1) / Tin;
+    nout += nout % 2;
+    const double w = S->o.omega_v;
+    const double sW = sgn_of(S->bc[0]), sE = sgn_of(S->bc[1]), sN = sgn_of(S->bc[2]), sS = sgn_of(S->bc[3]);
+    size_t n = padn(L);
+    double *x0 = zalloc(n), *y0 = zalloc(n), *nx_ = zalloc(n), *ny_ = zalloc(n);
+    for (int t = 0; t < nout; ++t) {
+        int si, sj;
+        ras_shift(S, &si, &sj);
+        memcpy(x0, vx, n * sizeof(double)); /* frozen state of this outer iteration */
+        memcpy(y0, vy, n * sizeof(double));
+        /* view arrays = frozen state; a tile overlays its own current values while it works */
+        memcpy(L->tx, vx, n * sizeof(double));
+        memcpy(L->ty, vy, n * sizeof(double));
+        const int nti = (L->ncy + si + T - 1) / T, ntj = (L->ncx + sj + T - 1) / T;
+        for (int ti = 0; ti < nti; ++ti)
+            for (int tj = 0; tj < ntj; ++tj) {
+                const int i0 = ti * T - si + 1 > 1 ? ti * T - si + 1 : 1;
+                const int i1 = (ti + 1) * T - si < L->ncy ? (ti + 1) * T - si : L->ncy;
+                const int j0 = tj * T - sj + 1 > 1 ? tj * T - sj + 1 : 1;
+                const int j1 = (tj + 1) * T - sj < L->ncx ? (tj + 1) * T - sj : L->ncx;
+                if (i0 > i1 || j0 > j1) continue;
+                const int xj1 = j1 < L->ncx - 1 ? j1 : L->ncx - 1, yi1 = i1 < L->ncy - 1 ? i1 : L->ncy - 1;
+                for (int tau = 0; tau < Tin; ++tau) {
+                    for (int i = i0; i <= i1; ++i)
+                        for (int j = j0; j <= xj1; ++j)
+                            nx_[IX(L, i, j)] = L->tx[IX(L, i, j)] + w * (bx[IX(L, i, j)] - Lx_point(L, L->tx, L->ty, i, j)) /
+                                                                      Lx_diag(S, L, i, j);
+                    for (int i = i0; i <= yi1; ++i)
+                        for (int j = j0; j <= j1; ++j)
+                            ny_[IX(L, i, j)] = L->ty[IX(L, i, j)] + w * (by[IX(L, i, j)] - Ly_point(L, L->tx, L->ty, i, j)) /
+                                                                      Ly_diag(S, L, i, j);
+                    for (int i = i0; i <= i1; ++i)
+                        for (int j = j0; j <= xj1; ++j) {
+                            L->tx[IX(L, i, j)] = nx_[IX(L, i, j)];
+                            if (i == 1) L->tx[IX(L, 0, j)] = sN * nx_[IX(L, i, j)];
+                            if (i == L->ncy) L->tx[IX(L, L->ncy + 1, j)] = sS * nx_[IX(L, i, j)];
+                        }
+                    for (int i = i0; i <= yi1; ++i)
+                        for (int j = j0; j <= j1; ++j) {
+                            L->ty[IX(L, i, j)] = ny_[IX(L, i, j)];
+                            if (j == 1) L->ty[IX(L, i, 0)] = sW * ny_[IX(L, i, j)];
+                            if (j == L->ncx) L->ty[IX(L, i, L->ncx + 1)] = sE * ny_[IX(L, i, j)];
+                        }
+                }
+                /* single writer: the tile's unknowns go to the result; the view gets the frozen
+                 * values back for the next tile */
+                for (int i = i0; i <= i1; ++i)
+                    for (int j = j0; j <= xj1; ++j) {
+                        vx[IX(L, i, j)] = L->tx[IX(L, i, j)];
+                        L->tx[IX(L, i, j)] = x0[IX(L, i, j)];
+                        if (i == 1) L->tx[IX(L, 0, j)] = x0[IX(L, 0, j)];
+                        if (i == L->ncy) L->tx[IX(L, L->ncy + 1, j)] = x0[IX(L, L->ncy + 1, j)];
+                    }
+                for (int i = i0; i <= yi1; ++i)
+                    for (int j = j0; j <= j1; ++j) {
+                        vy[IX(L, i, j)] = L->ty[IX(L, i, j)];
+                        L->ty[IX(L, i, j)] = y0[IX(L, i, j)];
+                        if (j == 1) L->ty[IX(L, i, 0)] = y0[IX(L, i, 0)];
+                        if (j == L->ncx) L->ty[IX(L, i, L->ncx + 1)] = y0[IX(L, i, L->ncx + 1)];
+                    }
+            }
+        refresh_mirrors(S, L, vx, vy);
+    }
+    free(x0); free(y0); free(nx_); free(ny_);
+}
+static void smooth(oracle_t *S, olevel *L, double *vx, double *vy, const double *bx, const double *by, int nu) {
+    const int ras = S->o.smoother == 2 || (S->o.smoother == 3 && L != &S->lev[0]);
+    if (ras) smooth_ras(S, L, vx, vy, bx, by, nu);
+    else if (S->o.smoother == 1) smooth_rbgs(S, L, vx, vy, bx, by, nu);
     else smooth_jacobi(S, L, vx, vy, bx, by, nu);
 }
 
@@ -571,6 +665,9 @@ int oracle_opts_default(oracle_opts *o) {
     o->theta_every = 25;
     o->aa_depth = 5;
     o->aa_beta = 0.7;
+    o->ras_tile = 32;
+    o->ras_inner = 4;
+    o->ras_seed = 2603;
     return O_OK;
 }
 
@@ -592,7 +689,8 @@ int oracle_create(int nx, int ny, double Lx, double Ly, const int *bc, const ora
     if (opts) S->o = *opts; else oracle_opts_default(&S->o);
     if (S->o.nu1 < 0 || S->o.coarse_min < 2 || S->o.vcycles_per_iter < 1 || S->o.gcr_restart < 1 ||
         !(S->o.theta_step >= 0.0 && S->o.theta_step <= 1.0) || S->o.theta_every < 1 || S->o.accel < 0 ||
-        S->o.accel > 2 || S->o.aa_depth < 0 || S->o.aa_depth > 15 || !(S->o.aa_beta > 0.0 && S->o.aa_beta <= 1.0)) {
+        S->o.accel > 2 || S->o.aa_depth < 0 || S->o.aa_depth > 15 || !(S->o.aa_beta > 0.0 && S->o.aa_beta <= 1.0) ||
+        S->o.smoother < 0 || S->o.smoother > 3 || S->o.ras_tile < 2 || S->o.ras_inner < 1) {
         free(S);
         return O_EINVAL;
     }
@@ -809,6 +907,7 @@ int oracle_vcycle(oracle_t *S, const double *bx, const double *by, double *vx, d
     double *pbx = zalloc(padn(L)), *pby = zalloc(padn(L));
     in_vx(L, bx, pbx); in_vy(L, by, pby);
     in_velocity(S, L, vx, vy, S->vx, S->vy);
+    S->ras_k = 0; S->ras_c = 0;
     vcycle_level(S, 0, S->vx, S->vy, pbx, pby);
     out_vx(L, S->vx, vx); out_vy(L, S->vy, vy);
     free(pbx); free(pby);
@@ -822,6 +921,7 @@ int oracle_smooth(oracle_t *S, int l, const double *bx, const double *by, double
     double *pbx = zalloc(padn(L)), *pby = zalloc(padn(L)), *wx = zalloc(padn(L)), *wy = zalloc(padn(L));
     in_vx(L, bx, pbx); in_vy(L, by, pby);
     in_velocity(S, L, vx, vy, wx, wy);
+    S->ras_k = 0; S->ras_c = 0;
     smooth(S, L, wx, wy, pbx, pby, nsweeps);
     out_vx(L, wx, vx); out_vy(L, wy, vy);
     free(pbx); free(pby); free(wx); free(wy);
@@ -893,6 +993,7 @@ static int solve_uzawa(oracle_t *S, double rtol, double Sf, double E0, int *iter
         /* velocity subproblem L v = f - G p^k, 1 V-cycle warm-started (R15) */
         FOR_VX(L) bx[IX(L, i, j)] = S->fx[IX(L, i, j)] - Gx_point(L, S->p, i, j);
         FOR_VY(L) by[IX(L, i, j)] = S->fy[IX(L, i, j)] - Gy_point(L, S->p, i, j);
+        S->ras_k = k - 1; S->ras_c = 0;  /* RAS shift counter: iteration index (R27) */
         for (int c = 0; c < S->o.vcycles_per_iter; ++c) vcycle_level(S, 0, S->vx, S->vy, bx, by);
         /* pressure update, reading R3: p += alpha eta_P r_p, r_p = -D v^{k+1} */
         FOR_P(L) {
@@ -980,6 +1081,7 @@ static int solve_gcr(oracle_t *S, double rtol, double Sf, double E0, int *iters,
             full_residual(S, S->vx, S->vy, S->p, r.x, r.y, r.p);
         }
         for (int i = 0; i < m && k < S->o.max_iter; ++i) {
+            S->ras_k = k; S->ras_c = 0;  /* RAS shift counter: iteration index (R27) */
             apply_precond(S, r, z[i]);
             refresh_mirrors(S, L, z[i].x, z[i].y);
             apply_A(S, z[i], w[i]);
@@ -1078,6 +1180,7 @@ static int solve_anderson(oracle_t *S, double rtol, double Sf, double E0, int *i
         /* G(x^k): one Uzawa iteration (as solve_uzawa) */
         FOR_VX(L) bx[IX(L, i, j)] = S->fx[IX(L, i, j)] - Gx_point(L, S->p, i, j);
         FOR_VY(L) by[IX(L, i, j)] = S->fy[IX(L, i, j)] - Gy_point(L, S->p, i, j);
+        S->ras_k = k; S->ras_c = 0;  /* RAS shift counter: iteration index (R27) */
         for (int c = 0; c < S->o.vcycles_per_iter; ++c) vcycle_level(S, 0, S->vx, S->vy, bx, by);
         FOR_P(L) {
             double r = -D_point(L, S->vx, S->vy, i, j);

@@ -46,6 +46,7 @@
 #define PAPER_2603_14040_B200_STOKES_H
 
 #include <stddef.h>
+#include <stdint.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -69,14 +70,15 @@ enum {
     STOKES_ESTATE = -6        /* call order: set_viscosity / set_density missing          */
 };
 
-enum { STOKES_SMOOTH_JACOBI = 0, STOKES_SMOOTH_RBGS = 1 };
+enum { STOKES_SMOOTH_JACOBI = 0, STOKES_SMOOTH_RBGS = 1, STOKES_SMOOTH_RAS = 2, STOKES_SMOOTH_MIXED = 3 };
 enum { STOKES_ACCEL_NONE = 0, STOKES_ACCEL_GCR = 1, STOKES_ACCEL_ANDERSON = 2 };
 
 /* Solver options.  stokes_opts_default() fills the paper's setting (PAPER.md:1765-1788:
  * omega_v 0.3, omega_p 0.6, 5+5 sweeps) with the readings of DESIGN.md §3 (growth g = 1,
  * direct coarsest).  The field order is part of the ABI. */
 typedef struct {
-    int smoother;         /* STOKES_SMOOTH_JACOBI or _RBGS     */
+    int smoother;         /* STOKES_SMOOTH_JACOBI, _RBGS, _RAS
+                             (Alg. 3) or _MIXED (Jacobi finest, RAS below)  */
     double omega_v;       /* velocity relaxation omega_v                                        */
     double alpha_p;       /* pressure relaxation alpha (= omega_p)                              */
     int nu1;              /* pre- and post-smoothing sweeps on the finest level                 */
@@ -94,6 +96,9 @@ typedef struct {
     int theta_every;      /* Uzawa / GCR iterations per stage before theta = 1 (25) */
     int aa_depth;         /* STOKES_ACCEL_ANDERSON (Alg. 5): depth m, 0..15   */
     double aa_beta;       /* Anderson mixing beta in (0, 1] (0.5-0.8)              */
+    int ras_tile;         /* RAS tile edge T in cells, 2..32 (32)                  */
+    int ras_inner;        /* RAS inner sweeps T_inner (4)                          */
+    uint64_t ras_seed;    /* seed of the counter-based tile-shift generator (reading R27)         */
 } stokes_opts;
 
 /* Fill *o with the defaults.  Returns STOKES_EINVAL if o is NULL. */
@@ -207,7 +212,8 @@ int stokes_launch_count(stokes_t h, long long *count, int reset);
  * (Uzawa RHS), 1 fine residual+energy, 2 fine residual+restriction, 3 prolongation,
  * 4 pressure update (fused with the energy residual), 5 RBGS sweep (4 phases), 6 pressure
  * update + energy residual + first Jacobi sweep of the next V-cycle, 7 two Jacobi sweeps in
- * one pass (6 and 7: fine grid >= 128 x 8 only, else STOKES_EINVAL).  Uses the
+ * one pass (6 and 7: fine grid >= 128 x 8 only, else STOKES_EINVAL), 8 one RAS outer
+ * iteration (ras_inner sweeps on shared-memory tiles).  Uses the
  * handle's current fields. */
 int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double *bytes);
 

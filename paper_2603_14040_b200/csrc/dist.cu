@@ -774,8 +774,8 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
                        const void *nccl_unique_id, const stokes_opts *opts, void *cuda_stream, stokes_t *out) {
     if (!out || px < 1 || py < 1 || px * py > MAXT || nx % px || ny % py || !bc) return STOKES_EINVAL;
     if (rank >= px * py || rank < -2 || (rank >= 0 && !nccl_unique_id)) return STOKES_EINVAL;
-    if (opts && (opts->theta_step > 0.0 || opts->accel == STOKES_ACCEL_ANDERSON))
-        return STOKES_EINVAL;  // viscosity rescaling, Anderson: single domain only
+    if (opts && (opts->theta_step > 0.0 || opts->accel == STOKES_ACCEL_ANDERSON || opts->smoother >= 2))
+        return STOKES_EINVAL;  // viscosity rescaling, Anderson, RAS / Mixed: single domain only
     Dist *D = (Dist *)calloc(1, sizeof(Dist));
     if (!D) return STOKES_ENOMEM;
     D->NX = nx;

@@ -72,7 +72,8 @@ int build_levels(int nx, int ny, double Lx, double Ly, const int bc[4], const st
 }
 
 int check_opts(const stokes_opts &o) {
-    if (o.smoother != 0 && o.smoother != 1) return STOKES_EINVAL;
+    if (o.smoother < 0 || o.smoother > 3) return STOKES_EINVAL;
+    if (o.ras_tile < 2 || o.ras_tile > ras_max_tile() || o.ras_inner < 1) return STOKES_EINVAL;
     if (!(o.omega_v > 0) || !(o.alpha_p > 0) || o.nu1 < 0 || !(o.nu_growth > 0) || o.coarse_min < 2) return STOKES_EINVAL;
     if (o.coarse_direct != 0 && o.coarse_direct != 1) return STOKES_EINVAL;
     if (o.vcycles_per_iter < 1 || o.accel < 0 || o.accel > 2) return STOKES_EINVAL;
@@ -173,8 +174,23 @@ RhsArgs rhs_fine(stokes_s *h) {
 // between cur and the other buffer: on return cur points at the result.
 // Pairs of sweeps run as one two-sweep pass (launch_jacobi2) where the level allows it, at
 // most max_pairs of them (each pair saves one buffer swap: vcycle keeps its count even).
+int level_smoother(const stokes_s *h, int l) {
+    if (h->o.smoother == STOKES_SMOOTH_MIXED) return l == 0 ? STOKES_SMOOTH_JACOBI : STOKES_SMOOTH_RAS;
+    return h->o.smoother;
+}
+bool uses_ras(const stokes_s *h) {
+    return h->o.smoother == STOKES_SMOOTH_RAS || (h->o.smoother == STOKES_SMOOTH_MIXED && h->nlev > 1);
+}
+void ras_iteration_start(stokes_s *h) { h->ras_c = 0; }
+void ras_reset(stokes_s *h) {  // iteration index 0: start of a solve / stand-alone V-cycle or smoothing
+    h->ras_c = 0;
+    if (uses_ras(h)) cudaMemsetAsync(h->scal + S_ITER, 0, sizeof(double), h->stream);
+}
+void ras_iteration_end(stokes_s *h) {
+    if (uses_ras(h)) launch_iter_inc(ctx(h), h->scal + S_ITER);
+}
 int jacobi_pairs(stokes_s *h, int l, int n, bool zero_in) {
-    if (h->o.smoother != STOKES_SMOOTH_JACOBI || !jacobi2_ok(h->lev[l].g)) return 0;
+    if (level_smoother(h, l) != STOKES_SMOOTH_JACOBI || !jacobi2_ok(h->lev[l].g)) return 0;
     return (n - (zero_in ? 1 : 0)) / 2 > 0 ? (n - (zero_in ? 1 : 0)) / 2 : 0;
 }
 void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&oy, const RhsArgs &rhs, int n,
@@ -188,7 +204,36 @@ void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&
         }
         return;
     }
-    if (h->o.smoother == STOKES_SMOOTH_JACOBI) {
+    const int lsm = level_smoother(h, l);
+    if (lsm == STOKES_SMOOTH_RAS) {  // Alg. 3: N_outer = ceil(n / T_inner), made even
+        if (zero_in) {
+            cudaMemsetAsync(cx - COL_OFF, 0, field_doubles(L.g) * sizeof(double), h->stream);
+            cudaMemsetAsync(cy - COL_OFF, 0, field_doubles(L.g) * sizeof(double), h->stream);
+        }
+        int nout = (n + h->o.ras_inner - 1) / h->o.ras_inner;
+        nout += nout % 2;
+        const bool fine = rhs.mode == RHS_FINE;
+        for (int t = 0; t < nout; ++t) {
+            RasArgs a;
+            a.vx = cx;
+            a.vy = cy;
+            a.etap = L.etap;
+            a.etab = L.etab;
+            a.f4 = fine ? rhs.p : rhs.bx;
+            a.f5 = fine ? rhs.rho : rhs.by;
+            a.vxo = ox;
+            a.vyo = oy;
+            a.omega = h->o.omega_v;
+            a.gx = fine ? rhs.gx : 0.0;
+            a.gy = fine ? rhs.gy : 0.0;
+            a.T = h->o.ras_tile;
+            a.Tin = h->o.ras_inner;
+            a.seed = h->o.ras_seed;
+            launch_ras_outer(c, L.g, a, h->scal + S_ITER, h->ras_c++, fine);
+            double *tt = cx; cx = ox; ox = tt;
+            tt = cy; cy = oy; oy = tt;
+        }
+    } else if (lsm == STOKES_SMOOTH_JACOBI) {
         int pairs = jacobi_pairs(h, l, n, zero_in);
         if (pairs > max_pairs) pairs = max_pairs;
         for (int s = 0; s < n;) {
@@ -302,8 +347,10 @@ void state_energy(stokes_s *h, double *rx, double *ry, double *rp) {
 void uzawa_body(stokes_s *h) {
     Level &F = h->lev[0];
     const LaunchCtx c = ctx(h);
+    ras_iteration_start(h);
     for (int k = 0; k < h->o.vcycles_per_iter; ++k)
         vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false);
+    ras_iteration_end(h);
     const double a_s = h->o.pressure_sign * h->o.alpha_p;
     const double inv_np = 1.0 / ((double)F.g.ncx * F.g.ncy);
     const double *pin = h->pbuf[h->pcur];
@@ -394,6 +441,7 @@ int ensure_uzawa_graphs(stokes_s *h) {
 }
 
 int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+    ras_reset(h);
     int st = ensure_uzawa_graphs(h);
     if (st) return st;
     double E = E0;
@@ -436,10 +484,13 @@ void fused_tail(stokes_s *h) {
 // then the fused tail of iterate k+1
 void fused_body(stokes_s *h) {
     Level &F = h->lev[0];
+    ras_iteration_start(h);
     vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false, 1);
+    ras_iteration_end(h);
     fused_tail(h);
 }
 int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+    ras_reset(h);
     const int keep = h->pcur;
     for (int k = 0; k < 2; ++k) {
         if (h->fused_exec[k]) continue;
@@ -464,7 +515,9 @@ int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *E
     double E = E0;
     int k = 1, status = STOKES_NOT_CONVERGED;
     // iteration 1: a full V-cycle from (v^0, p^0), then the fused tail of iterate 1
+    ras_iteration_start(h);
     vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false);
+    ras_iteration_end(h);
     fused_tail(h);
     for (;;) {
         h->pcur ^= 1;  // pbuf[pcur] = p^k
@@ -495,8 +548,10 @@ void gcr_step_body(stokes_s *h, int i) {
     double *x[3] = {F.vx[0], F.vy[0], h->pbuf[h->pcur]};
     const size_t nf = field_doubles(g);
     double *PA = h->partials, *PB = h->partials + 4096, *PC = h->partials + 8192;
+    ras_iteration_start(h);
     for (int q = 0; q < h->o.vcycles_per_iter; ++q)
         vcycle(h, 0, z[0], z[1], h->gtmp[0], h->gtmp[1], rhs_arrays(r[0], r[1]), q == 0);
+    ras_iteration_end(h);
     launch_precond_apply(c, g, F.etab, F.etap, z[0], z[1], r[2], h->o.alpha_p, z[2], w[0], w[1], w[2],
                          i > 0 ? (const double *const *)h->gw[0] : nullptr, r[0], r[1], PA);
     int nb = stream_blocks(g);
@@ -517,6 +572,7 @@ void gcr_step_body(stokes_s *h, int i) {
 }
 
 int solve_gcr_fused(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+    ras_reset(h);
     const int m = h->o.gcr_restart;
     double **r = h->gr;
     state_energy(h, r[0], r[1], r[2]);  // r0 = b - A x0
@@ -561,6 +617,7 @@ int solve_gcr_fused(stokes_s *h, double rtol, double E0, int *iters, double *Eou
 
 // Flexible GCR(m) with modified Gram-Schmidt, Alg. 4, readings R13/R14.
 int solve_gcr(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+    ras_reset(h);
     Level &F = h->lev[0];
     const GridL &g = F.g;
     const LaunchCtx c = ctx(h);
@@ -578,8 +635,10 @@ int solve_gcr(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
         for (int i = 0; i < m && k < h->o.max_iter; ++i) {
             double **z = h->gz[i], **w = h->gw[i];
             // z = M^-1 r: dv = Vcycle(0; r_v); dp = alpha eta_P (r_p - D dv); de-mean dp
+            ras_iteration_start(h);
             for (int q = 0; q < h->o.vcycles_per_iter; ++q)
                 vcycle(h, 0, z[0], z[1], h->gtmp[0], h->gtmp[1], rhs_arrays(r[0], r[1]), q == 0);
+            ras_iteration_end(h);
             launch_precond_p(c, g, F.etap, z[0], z[1], r[2], h->o.alpha_p, z[2], h->partials);
             launch_finalize(c, h->partials, nb, 1, inv_np, h->scal + S_ZMEAN);
             launch_sub_mean(c, g, h->scal + S_ZMEAN, z[2]);
@@ -655,6 +714,9 @@ int stokes_opts_default(stokes_opts *o) {
     o->theta_every = 25;
     o->aa_depth = 5;
     o->aa_beta = 0.7;
+    o->ras_tile = 32;
+    o->ras_inner = 4;
+    o->ras_seed = 2603;
     return STOKES_OK;
 }
 
@@ -893,6 +955,7 @@ int stokes_vcycle(stokes_t h, const double *bx, const double *by, double *vx, do
     launch_in_vx_raw(c, F.g, bx, F.bx);
     launch_in_vy_raw(c, F.g, by, F.by);
     launch_in_velocity(c, F.g, vx, vy, F.vx[0], F.vy[0]);
+    ras_reset(h);
     vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_arrays(F.bx, F.by), false);
     launch_out_vx(c, F.g, F.vx[0], vx);
     launch_out_vy(c, F.g, F.vy[0], vy);
@@ -957,6 +1020,7 @@ int solve_inner(stokes_s *h, double rtol, double E0, int *iters, double *E) {
 // x^k -> G(x^k) with its energy residual (the stopping test, G(x^k) returned), then
 // push (G_k, R_k, Gram row), the tiny constrained least squares, and the mixed update.
 int solve_anderson(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
+    ras_reset(h);
     int st = ensure_uzawa_graphs(h);
     if (st) return st;
     Level &F = h->lev[0];
@@ -1067,6 +1131,7 @@ int stokes_smooth(stokes_t h, int level, const double *bx, const double *by, dou
     launch_in_vy_raw(c, L.g, by, L.by);
     launch_in_velocity(c, L.g, vx, vy, L.vx[0], L.vy[0]);
     double *cx = L.vx[0], *cy = L.vy[0], *ox = L.vx[1], *oy = L.vy[1];
+    ras_reset(h);
     smooth(h, level, cx, cy, ox, oy, rhs_arrays(L.bx, L.by), nsweeps, false, nsweeps);
     launch_out_vx(c, L.g, cx, vx);
     launch_out_vy(c, L.g, cy, vy);
@@ -1199,6 +1264,26 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
             else launch_rbgs(c, g, F.etab, F.etap, F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v);
             break;
         case 7: launch_jacobi2(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), h->o.omega_v); break;
+        case 8: {
+            RasArgs a;
+            const RhsArgs r = rhs_fine(h);
+            a.vx = F.vx[0];
+            a.vy = F.vy[0];
+            a.etap = F.etap;
+            a.etab = F.etab;
+            a.f4 = r.p;
+            a.f5 = r.rho;
+            a.vxo = F.vx[1];
+            a.vyo = F.vy[1];
+            a.omega = h->o.omega_v;
+            a.gx = r.gx;
+            a.gy = r.gy;
+            a.T = h->o.ras_tile;
+            a.Tin = h->o.ras_inner;
+            a.seed = h->o.ras_seed;
+            launch_ras_outer(c, g, a, h->scal + S_ITER, 0, true);
+            break;
+        }
         default:
             launch_jacobi_uzawa(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], h->pbuf[h->pcur],
                                 h->pbuf[1 - h->pcur], h->rho, h->gx, h->gy, h->o.alpha_p, h->scal + S_ZERO,
@@ -1211,11 +1296,12 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
     // write 2) + restriction (read 2 fine, write 1/2); 3 prolongation (read/write 2 + 1/2 coarse);
     // 4 fused Uzawa pressure step + energy: read 6, write p; 5 RBGS (4 phases, fused bytes);
     // 6 Uzawa step + energy + first Jacobi sweep of the next V-cycle: read 6, write p, vx, vy;
-    // 7 two Jacobi sweeps in one pass: read 6, write 2
-    double per_cell[8] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0, 72.0, 64.0};
+    // 7 two Jacobi sweeps in one pass: read 6, write 2; 8 one RAS outer iteration (T_inner
+    // sweeps in shared memory): read 6, write 2
+    double per_cell[9] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0, 72.0, 64.0, 64.0};
     if (h->nlev > 1 && jacobi2_ok(g)) per_cell[2] = 48.0 + 4.0;  // fused: the residual stays on chip
     if (jacobi2_ok(g)) per_cell[5] = 2 * 56.0;  // RBGS: two streamed passes, each read 6 + write 1
-    if (kernel < 0 || kernel > 7) return STOKES_EINVAL;
+    if (kernel < 0 || kernel > 8) return STOKES_EINVAL;
     if ((kernel == 6 && !stream_ok(g)) || (kernel == 7 && !jacobi2_ok(g))) return STOKES_EINVAL;
     *bytes = per_cell[kernel] * cells;
     cudaEvent_t e0, e1;

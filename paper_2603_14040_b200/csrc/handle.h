@@ -15,7 +15,7 @@ extern thread_local std::string g_last_error;
 
 // device scalar slots
 enum { S_MSHIFT = 0, S_E = 1, S_SV = 2, S_SP = 3, S_SF = 4, S_SFPART = 5, S_ZMEAN = 8, S_GAMMA = 9, S_NU2 = 10, S_LOC = 16,
-       S_RR = 11, S_BETA = 12, S_ZERO = 13, S_E0 = 14, S_ETAMIN = 24, S_AAMT = 25, S_NSCAL = 64 };
+       S_RR = 11, S_BETA = 12, S_ZERO = 13, S_E0 = 14, S_ETAMIN = 24, S_AAMT = 25, S_ITER = 26, S_NSCAL = 64 };
 
 struct Level {
     GridL g;
@@ -45,6 +45,7 @@ struct stokes_s {
     AAHist aah;                     // Anderson history slots (accel = ANDERSON)
     AAVec aat;                      // Anderson: x^k (de-meaned pressure at mean S_AAMT)
     double *aaH, *aacg, *aacr;      // Gram matrix (slot-indexed), mixing coefficients
+    int ras_c;                      // RAS draw index within the current V-cycle (reading R27)
     int pcur;
     double *partials;
     size_t npart;
@@ -99,6 +100,11 @@ RhsArgs rhs_fine(stokes_s *h);
 void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&oy, const RhsArgs &rhs, int n,
             bool zero_in, int max_pairs = 0);
 int jacobi_pairs(stokes_s *h, int l, int n, bool zero_in);
+int level_smoother(const stokes_s *h, int l);
+bool uses_ras(const stokes_s *h);
+void ras_iteration_start(stokes_s *h);  // before the V-cycle(s) of one iteration
+void ras_reset(stokes_s *h);            // iteration index 0
+void ras_iteration_end(stokes_s *h);    // after them (advances the device iteration index)
 void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in,
             int done_pre = 0);
 int sync(stokes_s *h);

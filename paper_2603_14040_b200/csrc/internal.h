@@ -113,6 +113,18 @@ void launch_aa_solve(const LaunchCtx &c, const double *partials, int nblocks, co
                      double *H, double *cg, double *cr);
 void launch_aa_update(const LaunchCtx &c, const GridL &g, const AAHist &hist, int ns, const double *cg,
                       const double *cr, const AAVec &work, const AAVec &T, double *partials);
+// RAS-type temporal blocking (ras.cu): one outer iteration, (vx, vy) -> (vxo, vyo)
+struct RasArgs {
+    const double *vx, *vy, *etap, *etab, *f4, *f5;  // f4, f5 = p, rho (fine) | bx, by
+    double *vxo, *vyo;
+    double omega, gx, gy;
+    int T, Tin;
+    uint64_t seed;
+};
+void launch_ras_outer(const LaunchCtx &c, const GridL &g, const RasArgs &a, const double *iter, int c_draw,
+                      bool fine);
+void launch_iter_inc(const LaunchCtx &c, double *k);
+int ras_max_tile();
 // viscosity rescaling: min over the valid nodes of both caller fields
 // into *emin (as the bit pattern of a positive double, atomicMin), then the blend
 void launch_eta_min(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,

@@ -54,6 +54,9 @@ class Opts(ctypes.Structure):
         ("theta_every", ctypes.c_int),
         ("aa_depth", ctypes.c_int),
         ("aa_beta", ctypes.c_double),
+        ("ras_tile", ctypes.c_int),
+        ("ras_inner", ctypes.c_int),
+        ("ras_seed", ctypes.c_uint64),
     ]
 
 
@@ -353,7 +356,8 @@ class Stokes:
         return c.value
 
     KERNELS = {"jacobi": 0, "energy": 1, "residual_restrict": 2, "prolong": 3, "pupdate": 4, "rbgs": 5,
-               "jacobi_uzawa": 6, "jacobi2": 7}
+               "jacobi_uzawa": 6, "jacobi2": 7,
+               "ras": 8}
 
     def time_kernel(self, kernel, reps=20):
         ms, nb = ctypes.c_double(), ctypes.c_double()

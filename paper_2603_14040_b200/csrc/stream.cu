@@ -550,6 +550,10 @@ void fill_src(const double **src, const double *vx, const double *vy, const doub
 // shuffles, without CTA barriers, measured 435 us vs 340 us for this one at 4096^2.)
 constexpr int NS2 = 6;  // landing ring depth
 constexpr int SMEM2 = NS2 * NF * RW * 8 + 4 * 2 * TW * 8 + NS2 * 8;
+// the two-sweep pass runs wider CTAs: 320 threads (10 warps, 2 CTAs = 20 warps per SM at
+// 96 registers), a 5-row ring of 324-wide rows (98 KB per CTA)
+constexpr int JT = 320, JRW = JT + 4, NSJ = 5;
+constexpr int SMEMJ = NSJ * NF * JRW * 8 + 4 * 2 * JT * 8 + NSJ * 8;
 
 struct J2Args {
     const double *src[6];  // vx, vy, eta_p, eta_b, p | bx, rho | by
@@ -619,10 +623,10 @@ struct W2 {  // sweep-2 view of row s-1: velocities from the intermediate rows, 
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(TW, MINB) k_jacobi2(GridL g, J2Args a, int H) {
+__global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) {
     extern __shared__ __align__(128) double sm[];
-    double *s1 = sm + NS2 * NF * RW;  // [4 rows][vx', vy'][TW]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(s1 + 4 * 2 * TW);
+    double *s1 = sm + NSJ * NF * JRW;  // [4 rows][vx', vy'][JT]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s1 + 4 * 2 * JT);
     const int t = threadIdx.x;
     const int j0 = 1 + a.tw * blockIdx.x;
     const int c = j0 - 1 + t;  // sweep-1 column of this thread (= sweep-2 column for 1 <= t <= tw)
@@ -632,44 +636,44 @@ __global__ void __launch_bounds__(TW, MINB) k_jacobi2(GridL g, J2Args a, int H) 
     const int sfirst = max(i0 - 1, 0), slast = min(i1 + 1, g.ncy + 1);
     const size_t P = g.P;
     auto issue = [&](int r) {
-        const int slot = (r - rlo) % NS2;
+        const int slot = (r - rlo) % NSJ;
         uint64_t *bar = bars + slot;
-        mbar_expect_tx(bar, NF * RW * 8);
+        mbar_expect_tx(bar, NF * JRW * 8);
 #pragma unroll
         for (int f = 0; f < NF; ++f)
-            bulk_g2s(sm + (slot * NF + f) * RW, a.src[f] + (size_t)r * P + (j0 - 2), RW * 8, bar);
+            bulk_g2s(sm + (slot * NF + f) * JRW, a.src[f] + (size_t)r * P + (j0 - 2), JRW * 8, bar);
     };
     if (t == 0) {
-        for (int k = 0; k < NS2; ++k) mbar_init(bars + k, 1);
+        for (int k = 0; k < NSJ; ++k) mbar_init(bars + k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (t == 0)
-        for (int r = rlo; r < rlo + NS2 && r <= rhi; ++r) issue(r);
+        for (int r = rlo; r < rlo + NSJ && r <= rhi; ++r) issue(r);
     auto row_at = [&](int r) {  // wait until staged row r has landed; this thread's column in it
         const int rel = r - rlo;
-        mbar_wait(bars + rel % NS2, (rel / NS2) & 1);
-        return sm + (rel % NS2) * NF * RW + t + 1;
+        mbar_wait(bars + rel % NSJ, (rel / NSJ) & 1);
+        return sm + (rel % NSJ) * NF * JRW + t + 1;
     };
     V3 v;
     auto pullB = [&](const double *q) {
         v.B[F_VX] = R3{q[-1], q[0], q[1]};
-        v.B[F_VY] = R3{q[RW - 1], q[RW], q[RW + 1]};
-        v.B[F_EP].c = q[F_EP * RW];
-        v.B[F_EP].r = q[F_EP * RW + 1];
-        v.B[F_EB].l = q[F_EB * RW - 1];
-        v.B[F_EB].c = q[F_EB * RW];
-        v.B[F_4].c = q[F_4 * RW];
-        v.B[F_4].r = q[F_4 * RW + 1];
-        v.B[F_5].l = q[F_5 * RW - 1];
-        v.B[F_5].c = q[F_5 * RW];
+        v.B[F_VY] = R3{q[JRW - 1], q[JRW], q[JRW + 1]};
+        v.B[F_EP].c = q[F_EP * JRW];
+        v.B[F_EP].r = q[F_EP * JRW + 1];
+        v.B[F_EB].l = q[F_EB * JRW - 1];
+        v.B[F_EB].c = q[F_EB * JRW];
+        v.B[F_4].c = q[F_4 * JRW];
+        v.B[F_4].r = q[F_4 * JRW + 1];
+        v.B[F_5].l = q[F_5 * JRW - 1];
+        v.B[F_5].c = q[F_5 * JRW];
     };
     auto pullC = [&](const double *q) {
         v.C[F_VX].l = q[-1];
         v.C[F_VX].c = q[0];
-        v.C[F_VY].c = q[RW];
-        v.C[F_EP].c = q[F_EP * RW];
-        v.C[F_4].c = q[F_4 * RW];
+        v.C[F_VY].c = q[JRW];
+        v.C[F_EP].c = q[F_EP * JRW];
+        v.C[F_4].c = q[F_4 * JRW];
     };
     auto toA = [&]() {  // row B becomes row A
         v.A[F_EB].l = v.B[F_EB].l;
@@ -681,10 +685,10 @@ __global__ void __launch_bounds__(TW, MINB) k_jacobi2(GridL g, J2Args a, int H) 
         v.A[F_VY].r = v.B[F_VY].r;
         v.A[F_5].c = v.B[F_5].c;
     };
-    auto refill = [&](int r) {  // every thread has pulled row r as row B: its slot takes row r + NS2
-        if (t == 0 && r + NS2 <= rhi) {
+    auto refill = [&](int r) {  // every thread has pulled row r as row B: its slot takes row r + NSJ
+        if (t == 0 && r + NSJ <= rhi) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(r + NS2);
+            issue(r + NSJ);
         }
     };
     if (rlo < sfirst) {
@@ -717,24 +721,24 @@ __global__ void __launch_bounds__(TW, MINB) k_jacobi2(GridL g, J2Args a, int H) 
             iay_n = rcp(y.a);
             vy1 = w.B(F_VY) + a.omega * (by_n - y.L) * iay_n;
         }
-        s1[((s & 3) * 2 + 0) * TW + t] = vx1;
-        s1[((s & 3) * 2 + 1) * TW + t] = vy1;
+        s1[((s & 3) * 2 + 0) * JT + t] = vx1;
+        s1[((s & 3) * 2 + 1) * JT + t] = vy1;
         __syncthreads();
         refill(s);
         // ---- sweep 2, row i = s-1 on the intermediate iterate
         const int i = s - 1;
         if (i >= i0 && i <= i1 && t >= 1 && t <= a.tw && (!EDGE || c <= g.ncx)) {
-            const double *qa = s1 + (((s - 2) & 3) * 2) * TW + t, *qb = s1 + (((s - 1) & 3) * 2) * TW + t,
-                         *qc = s1 + ((s & 3) * 2) * TW + t;
+            const double *qa = s1 + (((s - 2) & 3) * 2) * JT + t, *qb = s1 + (((s - 1) & 3) * 2) * JT + t,
+                         *qc = s1 + ((s & 3) * 2) * JT + t;
             W2 u;
             u.v = &v;
             u.lag_eb = lag_eb;
             u.vx[0] = R3{0.0, qa[0], 0.0};
             u.vx[1] = R3{qb[-1], qb[0], qb[1]};
             u.vx[2] = R3{qc[-1], qc[0], 0.0};
-            u.vy[0] = R3{0.0, qa[TW], qa[TW + 1]};
-            u.vy[1] = R3{qb[TW - 1], qb[TW], qb[TW + 1]};
-            u.vy[2] = R3{0.0, qc[TW], 0.0};
+            u.vy[0] = R3{0.0, qa[JT], qa[JT + 1]};
+            u.vy[1] = R3{qb[JT - 1], qb[JT], qb[JT + 1]};
+            u.vy[2] = R3{0.0, qc[JT], 0.0};
             if (EDGE && i == 1 && g.bN) u.vx[0].c = g.sN * u.vx[1].c;
             if (EDGE && i == g.ncy && g.bS) u.vx[2].c = g.sS * u.vx[1].c;
             if (EDGE && c == 1 && g.bW) u.vy[1].l = g.sW * u.vy[1].c;
@@ -761,7 +765,7 @@ __global__ void __launch_bounds__(TW, MINB) k_jacobi2(GridL g, J2Args a, int H) 
         bxp = bx_n;
         byp = by_n;
     };
-    const bool interior = i0 >= 2 && i1 + 1 <= g.ncy - 1 && j0 >= 2 && j0 + TW - 2 <= g.ncx - 1;
+    const bool interior = i0 >= 2 && i1 + 1 <= g.ncy - 1 && j0 >= 2 && j0 + JT - 2 <= g.ncx - 1;
     if (interior)
         for (int s = sfirst; s <= slast; ++s) step(std::false_type(), s);
     else
@@ -983,6 +987,21 @@ __global__ void __launch_bounds__(TW, MINB) k_rbgs_pass(GridL g, J2Args a, int H
     }
 }
 
+int jt_tw(const GridL &g) {  // two-sweep pass: output columns per CTA (even, <= JT - 2)
+    const int ncb = (g.ncx + JT - 3) / (JT - 2);
+    int tw = (g.ncx + ncb - 1) / ncb;
+    return tw + (tw & 1);
+}
+dim3 jt_grid(const GridL &g, int *H) {
+    const int tw = jt_tw(g);
+    const int ncb = (g.ncx + tw - 1) / tw;
+    int strips = slots() / ncb;
+    if (strips < 1) strips = 1;
+    int h = (g.ncy + strips - 1) / strips;
+    if (h < 4) h = 4;
+    *H = h;
+    return dim3(ncb, (g.ncy + h - 1) / h);
+}
 int j2_tw(const GridL &g) {  // output columns per CTA: even, <= TW - 2, balanced over the blocks
     const int ncb = (g.ncx + TW - 3) / (TW - 2);
     int tw = (g.ncx + ncb - 1) / ncb;
@@ -1015,28 +1034,28 @@ void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, cons
     a.vxo = vxo;
     a.vyo = vyo;
     a.omega = omega;
-    a.tw = j2_tw(g);
+    a.tw = jt_tw(g);
     int H = 0;
-    const dim3 grid = j2_grid(g, &H);
+    const dim3 grid = jt_grid(g, &H);
     if (rhs.mode == RHS_FINE) {
         fill_src(a.src, vxi, vyi, etap, etab, rhs.p, rhs.rho);
         a.gx = rhs.gx;
         a.gy = rhs.gy;
         static bool done = false;
         if (!done) {
-            cudaFuncSetAttribute(k_jacobi2<RHS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+            cudaFuncSetAttribute(k_jacobi2<RHS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJ);
             done = true;
         }
-        k_jacobi2<RHS_FINE><<<grid, TW, SMEM2, c.stream>>>(g, a, H);
+        k_jacobi2<RHS_FINE><<<grid, JT, SMEMJ, c.stream>>>(g, a, H);
     } else {
         fill_src(a.src, vxi, vyi, etap, etab, rhs.bx, rhs.by);
         a.gx = a.gy = 0.0;
         static bool done = false;
         if (!done) {
-            cudaFuncSetAttribute(k_jacobi2<RHS_ARRAYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2);
+            cudaFuncSetAttribute(k_jacobi2<RHS_ARRAYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJ);
             done = true;
         }
-        k_jacobi2<RHS_ARRAYS><<<grid, TW, SMEM2, c.stream>>>(g, a, H);
+        k_jacobi2<RHS_ARRAYS><<<grid, JT, SMEMJ, c.stream>>>(g, a, H);
     }
     ++*c.counter;
 }

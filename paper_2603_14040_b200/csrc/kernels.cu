@@ -352,6 +352,57 @@ __global__ void __launch_bounds__(BX *BY) k_prolong(GridL gf, GridL gc, const do
     }
 }
 
+// Same prolongation, one thread per aligned pair of fine columns (2J-1, 2J) of one row:
+// 16-B loads / stores of the fine velocities (column 2J-1 is 16-B aligned by the layout)
+// and the coarse values shared by the pair; identical arithmetic to k_prolong.
+__global__ void __launch_bounds__(BX *BY) k_prolong2(GridL gf, GridL gc, const double *__restrict__ ex,
+                                                     const double *__restrict__ ey, double *__restrict__ vx,
+                                                     double *__restrict__ vy) {
+    const int J = blockIdx.x * BX + threadIdx.x + 1;  // fine columns 2J-1, 2J
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i > gf.ncy || 2 * J > gf.ncx) return;
+    const int j = 2 * J - 1;
+    {  // vx: x vertex-centred, y cell-centred
+        int I0;
+        double wy0, wy1;
+        if (i & 1) { I0 = (i + 1) / 2 - 1; wy0 = 0.25; wy1 = 0.75; }
+        else { I0 = i / 2; wy0 = 0.75; wy1 = 0.25; }
+        const double a0 = ex[at(gc, I0, J - 1)], a1 = ex[at(gc, I0, J)];
+        const double b0 = ex[at(gc, I0 + 1, J - 1)], b1 = ex[at(gc, I0 + 1, J)];
+        const double s_odd = wy0 * 0.5 * (a0 + a1) + wy1 * 0.5 * (b0 + b1);  // column 2J-1
+        const double s_even = wy0 * a1 + wy1 * b1;                            // column 2J
+        double2 *p = reinterpret_cast<double2 *>(vx + at(gf, i, j));
+        double2 v = *p;
+        v.x += s_odd;
+        const bool wall = 2 * J > gf.nvxj;  // column 2J = ncx is the east wall
+        if (!wall) v.y += s_even;
+        *p = v;
+        if (i == 1 && gf.bN) *reinterpret_cast<double2 *>(vx + at(gf, 0, j)) = make_double2(gf.sN * v.x, wall ? 0.0 : gf.sN * v.y);
+        if (i == gf.ncy && gf.bS)
+            *reinterpret_cast<double2 *>(vx + at(gf, gf.ncy + 1, j)) = make_double2(gf.sS * v.x, wall ? 0.0 : gf.sS * v.y);
+    }
+    if (i <= gf.nvyi) {  // vy: y vertex-centred, x cell-centred
+        const int I0 = i >> 1;
+        const double c0 = ey[at(gc, I0, J - 1)], c1 = ey[at(gc, I0, J)], c2 = ey[at(gc, I0, J + 1)];
+        double s_odd, s_even;  // columns 2J-1 (J0 = J-1; 1/4, 3/4) and 2J (J0 = J; 3/4, 1/4)
+        if (i & 1) {
+            const double d0 = ey[at(gc, I0 + 1, J - 1)], d1 = ey[at(gc, I0 + 1, J)], d2 = ey[at(gc, I0 + 1, J + 1)];
+            s_odd = 0.25 * 0.5 * (c0 + d0) + 0.75 * 0.5 * (c1 + d1);
+            s_even = 0.75 * 0.5 * (c1 + d1) + 0.25 * 0.5 * (c2 + d2);
+        } else {
+            s_odd = 0.25 * c0 + 0.75 * c1;
+            s_even = 0.75 * c1 + 0.25 * c2;
+        }
+        double2 *p = reinterpret_cast<double2 *>(vy + at(gf, i, j));
+        double2 v = *p;
+        v.x += s_odd;
+        v.y += s_even;
+        *p = v;
+        if (J == 1 && gf.bW) vy[at(gf, i, 0)] = gf.sW * v.x;
+        if (2 * J == gf.ncx && gf.bE) vy[at(gf, i, gf.ncx + 1)] = gf.sE * v.y;
+    }
+}
+
 // ------------------------------------------------------------------ residual + energy (a3)
 // Full saddle residual r_v = f - L v - G p, r_p = -D v and the
 // per-block partial sums Sv = sum r_v^2 / (-a_ii), Sp = sum r_p^2 eta_p / (2/dx^2+2/dy^2).
@@ -920,7 +971,12 @@ void launch_restrict_p(const LaunchCtx &c, const GridL &gf, const GridL &gc, con
 }
 void launch_prolong(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *exc, const double *eyc,
                     double *vx, double *vy) {
-    k_prolong<<<cell_grid(gf), tpb(), 0, c.stream>>>(gf, gc, exc, eyc, vx, vy);
+    if (gf.ncx % 2 == 0 && gf.bW && gf.bE && gf.bN && gf.bS) {  // single domain: paired columns
+        const dim3 grid((gf.ncx / 2 + BX - 1) / BX, (gf.ncy + BY - 1) / BY);
+        k_prolong2<<<grid, tpb(), 0, c.stream>>>(gf, gc, exc, eyc, vx, vy);
+    } else {
+        k_prolong<<<cell_grid(gf), tpb(), 0, c.stream>>>(gf, gc, exc, eyc, vx, vy);
+    }
     LAUNCH_BOOK(c);
 }
 int energy_blocks(const GridL &g) {

@@ -14,6 +14,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "stokes_oracle.c")
+_SRC_MARKERS = os.path.join(_HERE, "markers_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 OK, NOT_CONVERGED, EINVAL, ENOMEM, EDIVERGED, ESTATE = 0, 1, -1, -2, -5, -6
@@ -21,8 +22,9 @@ OK, NOT_CONVERGED, EINVAL, ENOMEM, EDIVERGED, ESTATE = 0, 1, -1, -2, -5, -6
 
 def build(force=False):
     """Compile the oracle (plain C, -O2 -ffp-contract=off, single thread)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+    srcs = [_SRC, _SRC_MARKERS]
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(f) for f in srcs):
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", _LIB, *srcs, "-lm"])
     return _LIB
 
 
@@ -85,6 +87,13 @@ def lib():
         L.oracle_blend_viscosity.argtypes = [P, ctypes.c_double]
         L.oracle_lithostatic.argtypes = [P, D]
         L.oracle_strerror.restype = ctypes.c_char_p
+        LL = ctypes.c_longlong
+        PL = ctypes.POINTER(ctypes.c_longlong)
+        i, d = ctypes.c_int, ctypes.c_double
+        L.oracle_markers_to_grid.argtypes = [i, i, d, d, LL, D, D, D, D, D, D, D, PL]
+        L.oracle_grid_to_markers.argtypes = [i, i, d, d, I, LL, D, D, D, D, D, D]
+        L.oracle_advect_markers.argtypes = [i, i, d, d, I, LL, D, D, D, D, d, i, PL]
+        L.oracle_marker_timestep.argtypes = [i, i, d, d, D, D, d, d, D]
     return _lib
 
 
@@ -263,3 +272,53 @@ class Oracle:
         if hist_len:
             out["hist"] = hist[: min(it.value, hist_len)]
         return out
+
+
+# ---------------------------------------------------------------- marker-in-cell (NEXT-4)
+SCHEMES = {"euler": 0, "heun": 1, "rk4": 2}
+
+
+def _bc(bc):
+    return (ctypes.c_int * 4)(*bc)
+
+
+def markers_to_grid(nx, ny, Lx, Ly, xm, ym, eta_m, rho_m):
+    """PAPER.md:467-495 (R28): returns eta_b, eta_p, rho_b (user layout) and the number of
+    empty nodes (zero accumulated weight; written 0)."""
+    xm, ym, eta_m, rho_m = (np.ascontiguousarray(a, np.float64) for a in (xm, ym, eta_m, rho_m))
+    eta_b = np.zeros((ny + 1, nx + 1))
+    rho_b = np.zeros((ny + 1, nx + 1))
+    eta_p = np.zeros((ny, nx))
+    ne = ctypes.c_longlong()
+    _check(lib().oracle_markers_to_grid(nx, ny, Lx, Ly, len(xm), _d(xm), _d(ym), _d(eta_m), _d(rho_m),
+                                        _d(eta_b), _d(eta_p), _d(rho_b), ctypes.byref(ne)), "markers_to_grid")
+    return eta_b, eta_p, rho_b, ne.value
+
+
+def grid_to_markers(nx, ny, Lx, Ly, bc, xm, ym, vx, vy):
+    """PAPER.md:497-511 (R29): velocity interpolated to the markers."""
+    xm, ym, vx, vy = (np.ascontiguousarray(a, np.float64) for a in (xm, ym, vx, vy))
+    um, vm = np.zeros_like(xm), np.zeros_like(xm)
+    _check(lib().oracle_grid_to_markers(nx, ny, Lx, Ly, _bc(bc), len(xm), _d(xm), _d(ym), _d(vx), _d(vy),
+                                        _d(um), _d(vm)), "grid_to_markers")
+    return um, vm
+
+
+def advect_markers(nx, ny, Lx, Ly, bc, xm, ym, vx, vy, dt, scheme="rk4"):
+    """PAPER.md:560-578 (R30): one advection step; returns new (xm, ym) and the number of
+    markers whose final position was clamped into the box."""
+    xm, ym = np.array(xm, np.float64, order="C"), np.array(ym, np.float64, order="C")
+    vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)
+    nc = ctypes.c_longlong()
+    _check(lib().oracle_advect_markers(nx, ny, Lx, Ly, _bc(bc), len(xm), _d(xm), _d(ym), _d(vx), _d(vy),
+                                       float(dt), SCHEMES[scheme], ctypes.byref(nc)), "advect_markers")
+    return xm, ym, nc.value
+
+
+def marker_timestep(nx, ny, Lx, Ly, vx, vy, cfl, max_dt):
+    """R31: dt = min(max_dt, cfl min(dx/max|vx|, dy/max|vy|))."""
+    vx, vy = np.ascontiguousarray(vx, np.float64), np.ascontiguousarray(vy, np.float64)
+    dt = ctypes.c_double()
+    _check(lib().oracle_marker_timestep(nx, ny, Lx, Ly, _d(vx), _d(vy), cfl, max_dt, ctypes.byref(dt)),
+           "marker_timestep")
+    return dt.value

@@ -180,3 +180,36 @@ def parity_fields(nx, ny, log_contrast=3.0, seed_eta=1, seed_rho=2, seed_v=3):
 def random_velocity(nx, ny, seed=3):
     r = np.random.default_rng(seed)
     return r.standard_normal((ny, nx + 1)), r.standard_normal((ny + 1, nx)), r.standard_normal((ny, nx))
+
+
+# ---------------------------------------------------------------- markers (NEXT-4)
+MARKER_PROPS = {"sinker": _sinker, "block": _block_eta,
+                "layered": lambda y, x: (_layered_eta(y, x), _layered_rho(y, x))}
+
+
+def markers(nx, ny, Lx=1.0, Ly=1.0, per_side=4, jitter=1.0, seed=7, order="cell", props="sinker"):
+    """Seeded marker cloud (recipe DESIGN.md §9d): a per_side x per_side lattice in every cell
+    (the paper's 8-16 markers per cell: per_side 4 -> 16), each marker moved by
+    a uniform jitter of +-jitter/2 lattice spacings (default_rng(seed)), clipped to the closed
+    box; properties (eta_m, rho_m) sampled from a workload's continuous definition at the
+    marker positions.  order: "cell" (cell-major, as seeded) or "shuffled" (a seeded random
+    permutation, the worst case for locality)."""
+    rng = np.random.default_rng(seed)
+    dx, dy = Lx / nx, Ly / ny
+    s = (np.arange(per_side) + 0.5) / per_side
+    # cell-major: cell (i, j), then the lattice row a, column b inside it
+    ci, cj, a, b = np.meshgrid(np.arange(ny), np.arange(nx), np.arange(per_side), np.arange(per_side),
+                               indexing="ij")
+    xm = (cj + s[b]) * dx
+    ym = (ci + s[a]) * dy
+    n = xm.size
+    xm = xm.reshape(n) + (rng.random(n) - 0.5) * jitter * dx / per_side
+    ym = ym.reshape(n) + (rng.random(n) - 0.5) * jitter * dy / per_side
+    xm = np.clip(xm, 0.0, Lx)
+    ym = np.clip(ym, 0.0, Ly)
+    if order == "shuffled":
+        perm = rng.permutation(n)
+        xm, ym = xm[perm], ym[perm]
+    eta_m, rho_m = MARKER_PROPS[props](ym, xm)
+    return {"xm": np.ascontiguousarray(xm), "ym": np.ascontiguousarray(ym),
+            "eta_m": np.ascontiguousarray(eta_m, np.float64), "rho_m": np.ascontiguousarray(rho_m, np.float64)}

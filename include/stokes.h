@@ -217,6 +217,43 @@ int stokes_launch_count(stokes_t h, long long *count, int reset);
  * handle's current fields. */
 int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double *bytes);
 
+/* ---- marker-in-cell ------------------------
+ * Markers: n FP64 positions (xm, ym) in the box frame of the handle (y down), DEVICE arrays
+ * of length n (n < 2^31 - 1).  Positions outside the closed box are clamped into it (R28/
+ * R30); they must be finite.  Single-domain handles only (STOKES_EINVAL otherwise).  The
+ * first call allocates marker scratch (~64 B per marker + 12 B per cell, freed by
+ * stokes_destroy; STOKES_ENOMEM if that fails).  Results are bit-identical to the serial
+ * CPU loops of the paper (the node sums are taken in ascending marker index). */
+enum { STOKES_ADVECT_EULER = 0, STOKES_ADVECT_HEUN = 1, STOKES_ADVECT_RK4 = 2 };
+
+/* Marker -> grid (§4.2 steps 1-5; reading R28): every node value is
+ *   phi(node) = sum_m w_m phi_m / sum_m w_m
+ * over the markers whose surrounding cell of that grid has the node as a corner, with the
+ * bilinear weights of PAPER.md:480-484 (w = (1 - r_x/dx or r_x/dx)(1 - r_y/dy or r_y/dy),
+ * r measured from the cell's top-left reference node).  eta_m -> eta_b (basic nodes) and
+ * eta_p (pressure nodes), rho_m -> rho_b (basic nodes): the inputs of stokes_set_viscosity /
+ * stokes_set_density, user layouts.  Nodes with zero accumulated weight are written 0 and
+ * counted in *n_empty (HOST, nullable; non-NULL synchronises).  Any of eta_b, eta_p, rho_b
+ * may be NULL (not written); rho_m may be NULL when rho_b is. */
+int stokes_markers_to_grid(stokes_t h, long long n, const double *xm, const double *ym, const double *eta_m,
+                           const double *rho_m, double *eta_b, double *eta_p, double *rho_b, long long *n_empty);
+/* Grid -> marker (R29): (vxm, vym)[m] = the four-node bilinear sum of the
+ * caller's velocity (user layout; wall entries taken as 0, mirror rows/columns from the
+ * boundary conditions of the handle) at marker m. */
+int stokes_grid_to_markers(stokes_t h, long long n, const double *xm, const double *ym, const double *vx,
+                           const double *vy, double *vxm, double *vym);
+/* One advection step of every marker IN PLACE (R30) with the velocity
+ * frozen: scheme STOKES_ADVECT_EULER (Eq. euler_advection), _HEUN
+ * (Eq. heun_method) or _RK4 (Eq. rk4_method, Listing rk4_agnostic order).  Stage and final
+ * positions are clamped into the closed box; *n_clamped (HOST, nullable; synchronises) =
+ * markers whose final position was clamped. */
+int stokes_advect_markers(stokes_t h, long long n, double *xm, double *ym, const double *vx, const double *vy,
+                          double dt, int scheme, long long *n_clamped);
+/* CFL-like time step (R31): *dt (HOST) = min(max_dt, cfl min(dx/max|vx|,
+ * dy/max|vy|)) over the velocity unknowns (a zero component drops its term).  cfl > 0,
+ * max_dt > 0.  Synchronises. */
+int stokes_marker_timestep(stokes_t h, const double *vx, const double *vy, double cfl, double max_dt, double *dt);
+
 const char *stokes_strerror(int status);
 const char *stokes_last_error(void);
 

@@ -5,7 +5,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libstokes_b200.so")
-SOURCES = ["kernels.cu", "stream.cu", "gcr.cu", "aa.cu", "ras.cu", "driver.cu", "dist.cu"]
+SOURCES = ["kernels.cu", "stream.cu", "gcr.cu", "aa.cu", "ras.cu", "driver.cu", "dist.cu", "markers.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 

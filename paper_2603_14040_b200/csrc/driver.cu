@@ -805,6 +805,7 @@ int stokes_destroy(stokes_t h) {
         return STOKES_OK;
     }
     drop_graphs(h);
+    if (h->mk_ws) cudaFree(h->mk_ws);
     if (h->hscal) cudaFreeHost(h->hscal);
     if (h->own_ws && h->ws) cudaFree(h->ws);
     if (h->own_stream) cudaStreamDestroy(h->stream);

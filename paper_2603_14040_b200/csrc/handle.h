@@ -65,6 +65,8 @@ struct stokes_s {
     cudaGraphExec_t fused_exec[2];  // fused-tail iteration reading pbuf[k] (a12 fusion)
     long long fused_kernels;
     long long uzawa_kernels;
+    void *mk_ws;        // marker-in-cell scratch (markers.cu), grown on demand
+    size_t mk_bytes;
     struct Dist *dist;  // non-null: a 2D-decomposed handle (all calls dispatch to dist_*)
 };
 

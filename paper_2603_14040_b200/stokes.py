@@ -100,6 +100,10 @@ def lib(build_if_missing=True):
         "stokes_create_dist": [I, I, D, D, pi, I, I, I, P, ctypes.POINTER(Opts), P, ctypes.POINTER(P)],
         "stokes_nccl_unique_id": [P],
         "stokes_lithostatic": [P, P],
+        "stokes_markers_to_grid": [P, ctypes.c_longlong, P, P, P, P, P, P, P, ctypes.POINTER(ctypes.c_longlong)],
+        "stokes_grid_to_markers": [P, ctypes.c_longlong, P, P, P, P, P, P],
+        "stokes_advect_markers": [P, ctypes.c_longlong, P, P, P, P, D, I, ctypes.POINTER(ctypes.c_longlong)],
+        "stokes_marker_timestep": [P, P, P, D, D, pd],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -117,7 +121,8 @@ EXPORTED = ["stokes_opts_default", "stokes_workspace_bytes", "stokes_create", "s
             "stokes_smooth", "stokes_level_residual", "stokes_restrict", "stokes_prolong",
             "stokes_get_viscosity", "stokes_coarse_solve", "stokes_launch_count", "stokes_time_kernel",
             "stokes_strerror", "stokes_last_error", "stokes_create_dist", "stokes_nccl_unique_id",
-            "stokes_lithostatic"]
+            "stokes_lithostatic", "stokes_markers_to_grid", "stokes_grid_to_markers", "stokes_advect_markers",
+            "stokes_marker_timestep"]
 
 
 def default_opts(**kw):
@@ -198,6 +203,11 @@ class Stokes:
     @staticmethod
     def _p(t):
         return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+    def _sync_outputs(self):
+        # results written on the handle's stream must be visible on torch's current stream
+        if self.stream != torch.cuda.current_stream(self.device):
+            torch.cuda.current_stream(self.device).wait_stream(self.stream)
 
     def _sync_inputs(self):
         # inputs produced on torch's current stream must be visible on the handle's stream
@@ -341,6 +351,69 @@ class Stokes:
         self._sync_inputs()
         _check(lib().stokes_coarse_solve(self._h, *map(self._p, (bx, by, vx, vy))), "coarse_solve")
         return vx, vy
+
+    # ------------------------------------------------------------ marker-in-cell (NEXT-4)
+    ADVECT = {"euler": 0, "heun": 1, "rk4": 2}
+
+    def _marker(self, t, n=None):
+        t = self._dev(t)
+        if t.dim() != 1 or (n is not None and t.numel() != n):
+            raise ValueError("marker arrays must be 1-D of equal length")
+        return t
+
+    def markers_to_grid(self, xm, ym, eta_m, rho_m, count_empty=True):
+        """(eta_b, eta_p, rho_b, n_empty) from marker values (R28)."""
+        xm = self._marker(xm)
+        n = xm.numel()
+        ym, eta_m, rho_m = self._marker(ym, n), self._marker(eta_m, n), self._marker(rho_m, n)
+        eb, ep, rb = self._empty("b"), self._empty("p"), self._empty("b")
+        ne = ctypes.c_longlong(-1)
+        self._sync_inputs()
+        _check(lib().stokes_markers_to_grid(self._h, n, *map(self._p, (xm, ym, eta_m, rho_m, eb, ep, rb)),
+                                            ctypes.byref(ne) if count_empty else None), "markers_to_grid")
+        self._sync_outputs()
+        return eb, ep, rb, ne.value
+
+    def grid_to_markers(self, xm, ym, vx, vy):
+        """velocity at the markers (R29)."""
+        sh = shapes(self.nx, self.ny)
+        xm = self._marker(xm)
+        ym = self._marker(ym, xm.numel())
+        vx, vy = self._dev(vx, sh["vx"]), self._dev(vy, sh["vy"])
+        um, vm = torch.empty_like(xm), torch.empty_like(xm)
+        self._sync_inputs()
+        _check(lib().stokes_grid_to_markers(self._h, xm.numel(), *map(self._p, (xm, ym, vx, vy, um, vm))),
+               "grid_to_markers")
+        self._sync_outputs()
+        return um, vm
+
+    def advect_markers(self, xm, ym, vx, vy, dt, scheme="rk4", count_clamped=True):
+        """one advection step IN PLACE on (xm, ym) (CUDA float64 tensors of the
+        handle's device); returns the number of clamped markers (R30), or -1 if not counted."""
+        sh = shapes(self.nx, self.ny)
+        for t in (xm, ym):
+            if not (torch.is_tensor(t) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+                raise TypeError("advect_markers updates in place: xm, ym must be contiguous CUDA float64 tensors")
+        if xm.numel() != ym.numel():
+            raise ValueError("xm, ym differ in length")
+        vx, vy = self._dev(vx, sh["vx"]), self._dev(vy, sh["vy"])
+        nc = ctypes.c_longlong(-1)
+        self._sync_inputs()
+        _check(lib().stokes_advect_markers(self._h, xm.numel(), *map(self._p, (xm, ym, vx, vy)), float(dt),
+                                           self.ADVECT[scheme], ctypes.byref(nc) if count_clamped else None),
+               "advect_markers")
+        self._sync_outputs()
+        return nc.value
+
+    def marker_timestep(self, vx, vy, cfl, max_dt):
+        """R31: min(max_dt, cfl min(dx/max|vx|, dy/max|vy|))."""
+        sh = shapes(self.nx, self.ny)
+        vx, vy = self._dev(vx, sh["vx"]), self._dev(vy, sh["vy"])
+        dt = ctypes.c_double()
+        self._sync_inputs()
+        _check(lib().stokes_marker_timestep(self._h, self._p(vx), self._p(vy), float(cfl), float(max_dt),
+                                            ctypes.byref(dt)), "marker_timestep")
+        return dt.value
 
     # ------------------------------------------------------------ instrumentation
     def lithostatic(self):

@@ -18,7 +18,7 @@
 // (no FMA contraction), so the result is bit-identical to the plain CPU loop.
 //
 // Data in HBM per call (n markers, user layouts of include/stokes.h): x, y, eta, rho read;
-// per target grid a sorted record of (marker index, t_x, t_y, eta[, rho]) -- t = offset of
+// per target grid a sorted index list + a 32-B record (t_x, t_y, eta, rho) -- t = offset of
 // the marker from its reference node / spacing, computed once -- then a gather per node.
 #include <climits>
 #include <cmath>
@@ -184,8 +184,7 @@ template <bool BASIC>
 __global__ void k_mk_records(int nbins, const int *__restrict__ off, int *__restrict__ sidx,
                              const double *__restrict__ x, const double *__restrict__ y,
                              const double *__restrict__ eta, const double *__restrict__ rho, MkGrid G,
-                             double *__restrict__ rtx, double *__restrict__ rty, double *__restrict__ reta,
-                             double *__restrict__ rrho) {
+                             double4 *__restrict__ rec) {
     int warp = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     int lane = threadIdx.x & 31;
     int b0 = warp * 32;
@@ -211,36 +210,35 @@ __global__ void k_mk_records(int nbins, const int *__restrict__ off, int *__rest
         if (BASIC) {
             ref_node(xm, G.dx, 0.0, 0, G.nx - 1, tx);
             ref_node(ym, G.dy, 0.0, 0, G.ny - 1, ty);
-            rrho[k] = rho[m];
         } else {
             ref_node(xm, G.dx, G.hx, -1, G.nx - 1, tx);
             ref_node(ym, G.dy, G.hy, -1, G.ny - 1, ty);
         }
-        rtx[k] = tx;
-        rty[k] = ty;
-        reta[k] = eta[m];
+        rec[k] = make_double4(tx, ty, eta[m], BASIC ? rho[m] : 0.0);
     }
 }
 
 // ---- gather: node (i, j) merges the four bins (ir, jr) = (i-1, j-1), (i-1, j), (i, j-1), (i, j)
 // in ascending marker index; the node is corner (1,1), (1,0), (0,1), (0,0) of those bins and
 // takes the weight x-factor * y-factor with factor t (corner 1) or 1 - t (corner 0), as
-// w00..w11 of PAPER.md:480-484.
+// w00..w11 of PAPER.md:480-484.  A CTA covers 32 x 8 nodes, each warp an 8 x 4 patch, so the
+// four lanes that share a bin read its records together (L1 reuse instead of HBM re-reads).
+constexpr int GX = 32, GY = 8;
 template <bool BASIC>
-__global__ void k_mk_gather(MkGrid G, const int *__restrict__ off, const int *__restrict__ sidx,
-                            const double *__restrict__ rtx, const double *__restrict__ rty,
-                            const double *__restrict__ reta, const double *__restrict__ rrho,
-                            double *__restrict__ out_eta, double *__restrict__ out_rho,
-                            unsigned long long *__restrict__ n_empty) {
+__global__ void __launch_bounds__(256) k_mk_gather(MkGrid G, const int *__restrict__ off,
+                                                   const int *__restrict__ sidx, const double4 *__restrict__ rec,
+                                                   double *__restrict__ out_eta, double *__restrict__ out_rho,
+                                                   unsigned long long *__restrict__ n_empty) {
     // basic: nodes (ny+1) x (nx+1), bins ny x nx (index ir*nx + jr)
     // P    : nodes ny x nx,         bins (ny+1) x (nx+1) (index (ir+1)*(nx+1) + jr+1)
     const int NW = BASIC ? G.nx + 1 : G.nx, NH = BASIC ? G.ny + 1 : G.ny;
     const int BW = BASIC ? G.nx : G.nx + 1, BH = BASIC ? G.ny : G.ny + 1;
-    long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    bool live = q < (long long)NW * NH;
-    int i = live ? (int)(q / NW) : 0, j = live ? (int)(q % NW) : 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int j = blockIdx.x * GX + (w & 3) * 8 + (lane & 7);
+    const int i = blockIdx.y * GY + (w >> 2) * 4 + (lane >> 3);
+    const bool live = i < NH && j < NW;
     // bin coordinates in the bin array (P bins are shifted by +1)
-    int bi = BASIC ? i : i + 1, bj = BASIC ? j : j + 1;
+    const int bi = BASIC ? i : i + 1, bj = BASIC ? j : j + 1;
     int h0 = 0, e0 = 0, h1 = 0, e1 = 0, h2 = 0, e2 = 0, h3 = 0, e3 = 0;
     if (live) {
         if (bi - 1 >= 0 && bj - 1 >= 0) { int b = (bi - 1) * BW + bj - 1; h0 = off[b]; e0 = off[b + 1]; }
@@ -258,13 +256,13 @@ __global__ void k_mk_gather(MkGrid G, const int *__restrict__ off, const int *__
         if (c3 < best) { best = c3; sel = 3; }
         if (best == INT_MAX) break;
         int k = sel == 0 ? h0 : sel == 1 ? h1 : sel == 2 ? h2 : h3;
-        double tx = rtx[k], ty = rty[k];
-        double fx = (sel == 0 || sel == 2) ? tx : __dsub_rn(1.0, tx);
-        double fy = (sel <= 1) ? ty : __dsub_rn(1.0, ty);
-        double w = __dmul_rn(fx, fy);
-        sw = __dadd_rn(sw, w);
-        se = __dadd_rn(se, __dmul_rn(w, reta[k]));
-        if (BASIC) sr = __dadd_rn(sr, __dmul_rn(w, rrho[k]));
+        const double4 r = rec[k];
+        double fx = (sel == 0 || sel == 2) ? r.x : __dsub_rn(1.0, r.x);
+        double fy = (sel <= 1) ? r.y : __dsub_rn(1.0, r.y);
+        double wgt = __dmul_rn(fx, fy);
+        sw = __dadd_rn(sw, wgt);
+        se = __dadd_rn(se, __dmul_rn(wgt, r.z));
+        if (BASIC) sr = __dadd_rn(sr, __dmul_rn(wgt, r.w));
         ++k;
         if (sel == 0) { h0 = k; c0 = k < e0 ? sidx[k] : INT_MAX; }
         else if (sel == 1) { h1 = k; c1 = k < e1 ? sidx[k] : INT_MAX; }
@@ -273,8 +271,9 @@ __global__ void k_mk_gather(MkGrid G, const int *__restrict__ off, const int *__
     }
     bool empty = live && sw == 0.0;
     unsigned ball = __ballot_sync(~0u, empty);
-    if ((threadIdx.x & 31) == 0 && ball) atomicAdd(n_empty, (unsigned long long)__popc(ball));
+    if (lane == 0 && ball) atomicAdd(n_empty, (unsigned long long)__popc(ball));
     if (!live) return;
+    const size_t q = (size_t)i * NW + j;
     if (out_eta) out_eta[q] = empty ? 0.0 : __ddiv_rn(se, sw);
     if (BASIC && out_rho) out_rho[q] = empty ? 0.0 : __ddiv_rn(sr, sw);
 }
@@ -484,15 +483,14 @@ int stokes_markers_to_grid(stokes_t h, long long n, const double *xm, const doub
         cv.take<int>(nbB + 1); cv.take<int>(nbB + 1); cv.take<int>(nbB); cv.take<int>(ntB);
         cv.take<int>(nbP + 1); cv.take<int>(nbP + 1); cv.take<int>(nbP); cv.take<int>(ntP);
         cv.take<int>(n); cv.take<int>(n);
-        for (int k = 0; k < 7; ++k) cv.take<double>(n);
+        cv.take<double4>(n); cv.take<double4>(n);
     }
     cv = MkCarve{(char *)h->mk_ws, 0};
     auto *scal = cv.take<unsigned long long>(4);
     int *cntB = cv.take<int>(nbB + 1), *offB = cv.take<int>(nbB + 1), *fillB = cv.take<int>(nbB), *tsB = cv.take<int>(ntB);
     int *cntP = cv.take<int>(nbP + 1), *offP = cv.take<int>(nbP + 1), *fillP = cv.take<int>(nbP), *tsP = cv.take<int>(ntP);
     int *sidxB = cv.take<int>(n), *sidxP = cv.take<int>(n);
-    double *btx = cv.take<double>(n), *bty = cv.take<double>(n), *beta = cv.take<double>(n), *brho = cv.take<double>(n);
-    double *ptx = cv.take<double>(n), *pty = cv.take<double>(n), *peta = cv.take<double>(n);
+    double4 *recB = cv.take<double4>(n), *recP = cv.take<double4>(n);
     const LaunchCtx c = sk::ctx(h);
     CK(cudaMemsetAsync(scal, 0, 4 * sizeof(unsigned long long), c.stream));
     CK(cudaMemsetAsync(cntB, 0, (nbB + 1) * sizeof(int), c.stream));
@@ -509,17 +507,15 @@ int stokes_markers_to_grid(stokes_t h, long long n, const double *xm, const doub
     }
     const double *rho_src = rho_m ? rho_m : eta_m;  // rho records unused when rho_b is NULL
     k_mk_records<true><<<blocks_for((long long)(nbB + 31) / 32 * 32, TPB), TPB, 0, c.stream>>>(
-        nbB, offB, sidxB, xm, ym, eta_m, rho_src, G, btx, bty, beta, brho);
+        nbB, offB, sidxB, xm, ym, eta_m, rho_src, G, recB);
     ++*c.counter;
     k_mk_records<false><<<blocks_for((long long)(nbP + 31) / 32 * 32, TPB), TPB, 0, c.stream>>>(
-        nbP, offP, sidxP, xm, ym, eta_m, rho_src, G, ptx, pty, peta, nullptr);
+        nbP, offP, sidxP, xm, ym, eta_m, rho_src, G, recP);
     ++*c.counter;
-    const long long nnB = (long long)(G.nx + 1) * (G.ny + 1), nnP = (long long)G.nx * G.ny;
-    k_mk_gather<true><<<blocks_for(nnB, TPB), TPB, 0, c.stream>>>(G, offB, sidxB, btx, bty, beta, brho, eta_b,
-                                                                   rho_b, scal);
+    const dim3 gB((G.nx + 1 + GX - 1) / GX, (G.ny + 1 + GY - 1) / GY), gP((G.nx + GX - 1) / GX, (G.ny + GY - 1) / GY);
+    k_mk_gather<true><<<gB, 256, 0, c.stream>>>(G, offB, sidxB, recB, eta_b, rho_b, scal);
     ++*c.counter;
-    k_mk_gather<false><<<blocks_for(nnP, TPB), TPB, 0, c.stream>>>(G, offP, sidxP, ptx, pty, peta, nullptr,
-                                                                    eta_p, nullptr, scal);
+    k_mk_gather<false><<<gP, 256, 0, c.stream>>>(G, offP, sidxP, recP, eta_p, nullptr, scal);
     ++*c.counter;
     CKL();
     if (n_empty) {

@@ -552,7 +552,13 @@ constexpr int NS2 = 6;  // landing ring depth
 constexpr int SMEM2 = NS2 * NF * RW * 8 + 4 * 2 * TW * 8 + NS2 * 8;
 // the two-sweep pass runs wider CTAs: 320 threads (10 warps, 2 CTAs = 20 warps per SM at
 // 96 registers), a 5-row ring of 324-wide rows (98 KB per CTA)
-constexpr int JT = 320, JRW = JT + 4, NSJ = 5;
+#ifndef J2_NSJ
+#define J2_NSJ 6  // 6-deep landing ring: 303.7 -> 284.5 us at 4096^2 vs 5 (TMA latency)
+#endif
+#ifndef J2_LATE
+#define J2_LATE 0
+#endif
+constexpr int JT = 320, JRW = JT + 4, NSJ = J2_NSJ;
 constexpr int SMEMJ = NSJ * NF * JRW * 8 + 4 * 2 * JT * 8 + NSJ * 8;
 
 struct J2Args {
@@ -724,7 +730,7 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
         s1[((s & 3) * 2 + 0) * JT + t] = vx1;
         s1[((s & 3) * 2 + 1) * JT + t] = vy1;
         __syncthreads();
-        refill(s);
+        if (!J2_LATE) refill(s);
         // ---- sweep 2, row i = s-1 on the intermediate iterate
         const int i = s - 1;
         if (i >= i0 && i <= i1 && t >= 1 && t <= a.tw && (!EDGE || c <= g.ncx)) {
@@ -758,6 +764,7 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
                 if (EDGE && c == g.ncx && g.bE) a.vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
             }
         }
+        if (J2_LATE) refill(s);
         lag_eb = v.A[F_EB].c;
         toA();
         iax = iax_n;
@@ -836,8 +843,11 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
     refill(rlo);
     refill(rlo + 1);
     const bool cx_in = c >= 1 && c <= g.nvxj, cy_in = c >= 1 && c <= g.ncx;
-    const int J = (j0 + 1) / 2 + t;  // coarse column of this thread in the emit phase
-    const bool emit_x = t < a.tw / 2 && J <= gc.nvxj, emit_y = t < a.tw / 2 && J <= gc.ncx;
+    // emit phase: threads [0, tw/2) restrict vx, threads [tw/2, tw) restrict vy (one coarse
+    // value each, so no half of the CTA idles at the next barrier)
+    const int half = a.tw / 2;
+    const int J = (j0 + 1) / 2 + (t < half ? t : t - half);  // coarse column of this thread
+    const bool emit_x = t < half && J <= gc.nvxj, emit_y = t >= half && t < 2 * half && J <= gc.ncx;
     for (int i = ilo; i <= ihi; ++i) {
         consume(i + 1);  // A = i-1, B = i, C = i+1
         double rx = 0.0, ry = 0.0;
@@ -868,7 +878,7 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
                     sx += wd * h;
                     wsum += wd;
                 }
-                a.bxc[at(gc, I, J)] = sx / (2.0 * wsum);
+                a.bxc[at(gc, I, J)] = sx * (wsum == 2.0 ? 0.25 : 1.0 / (2.0 * wsum));
             }
             if (emit_y && I <= gc.nvyi) {  // vy: x cell-centred, y vertex-centred
                 const int q = 2 * J - 2 - (j0 - 1);  // ring column of fine column 2J-2
@@ -884,7 +894,7 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
                     sy += wd * col;
                     wsum += wd;
                 }
-                a.byc[at(gc, I, J)] = sy / (2.0 * wsum);
+                a.byc[at(gc, I, J)] = sy * (wsum == 2.0 ? 0.25 : 1.0 / (2.0 * wsum));
             }
         }
     }

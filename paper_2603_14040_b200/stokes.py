@@ -65,7 +65,7 @@ def lib(build_if_missing=True):
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
+    path = os.environ.get("STOKES_LIB", _build.LIB)  # experiments: an alternative build of the library
     if not os.path.exists(path):
         if not build_if_missing:
             raise RuntimeError(f"{path} missing: run paper_2603_14040_b200/build.py (nvcc, sm_100a)")

@@ -32,6 +32,7 @@ namespace {
 struct MkGrid {
     int nx, ny;
     double Lx, Ly, dx, dy, hx, hy;  // hx = 0.5 dx, hy = 0.5 dy: offsets of the staggered grids
+    double rdx, rdy;                // RN(1/dx), RN(1/dy): floor of the quotient without a division
     double sW, sE, sN, sS;          // mirror signs (free slip +1, no slip -1)
 };
 
@@ -41,17 +42,28 @@ constexpr int SCAN_TILE = 4 * SCAN_T;  // elements per scan tile
 
 __device__ __forceinline__ double clampd(double v, double lo, double hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// floor(RN(a / h)) -- the oracle's floor of the correctly rounded quotient -- from the product
+// q = RN(a * RN(1/h)): |q - a/h| <= |a/h| (2^-52 + 2^-106), so floor(q) can differ from
+// floor(RN(a/h)) only when a/h lies within ~3.4e-16 |a/h| of an integer; any q within
+// 1e-9 max(1, |q|) of an integer takes the IEEE division instead (rare), so the result is
+// always identical to the division's.
+__device__ __forceinline__ int floor_quot(double a, double h, double rh) {
+    const double q = __dmul_rn(a, rh);
+    const double n = rint(q);
+    if (fabs(q - n) <= 1e-9 * fmax(1.0, fabs(q))) return (int)floor(__ddiv_rn(a, h));
+    return (int)floor(q);
+}
 // Reference node of a grid whose node k sits at k h + o (R28): k = floor((x - o)/h) clamped to
 // [kmin, kmax]; t = (x - (k h + o)) / h.  The exact operation sequence of the oracle.
-__device__ __forceinline__ int ref_node(double x, double h, double o, int kmin, int kmax, double &t) {
-    int k = (int)floor(__ddiv_rn(__dsub_rn(x, o), h));
+__device__ __forceinline__ int ref_node(double x, double h, double rh, double o, int kmin, int kmax, double &t) {
+    int k = floor_quot(__dsub_rn(x, o), h, rh);
     k = k < kmin ? kmin : (k > kmax ? kmax : k);
     double xn = __dadd_rn(__dmul_rn((double)k, h), o);
     t = __ddiv_rn(__dsub_rn(x, xn), h);
     return k;
 }
-__device__ __forceinline__ int ref_only(double x, double h, double o, int kmin, int kmax) {
-    int k = (int)floor(__ddiv_rn(__dsub_rn(x, o), h));
+__device__ __forceinline__ int ref_only(double x, double h, double rh, double o, int kmin, int kmax) {
+    int k = floor_quot(__dsub_rn(x, o), h, rh);
     return k < kmin ? kmin : (k > kmax ? kmax : k);
 }
 
@@ -60,8 +72,8 @@ __device__ __forceinline__ int ref_only(double x, double h, double o, int kmin, 
 __device__ __forceinline__ void marker_bins(const MkGrid &G, double x, double y, int &bb, int &bp) {
     x = clampd(x, 0.0, G.Lx);
     y = clampd(y, 0.0, G.Ly);
-    int jb = ref_only(x, G.dx, 0.0, 0, G.nx - 1), ib = ref_only(y, G.dy, 0.0, 0, G.ny - 1);
-    int jp = ref_only(x, G.dx, G.hx, -1, G.nx - 1), ip = ref_only(y, G.dy, G.hy, -1, G.ny - 1);
+    int jb = ref_only(x, G.dx, G.rdx, 0.0, 0, G.nx - 1), ib = ref_only(y, G.dy, G.rdy, 0.0, 0, G.ny - 1);
+    int jp = ref_only(x, G.dx, G.rdx, G.hx, -1, G.nx - 1), ip = ref_only(y, G.dy, G.rdy, G.hy, -1, G.ny - 1);
     bb = ib * G.nx + jb;
     bp = (ip + 1) * (G.nx + 1) + (jp + 1);
 }
@@ -208,11 +220,11 @@ __global__ void k_mk_records(int nbins, const int *__restrict__ off, int *__rest
         int m = sidx[k];
         double xm = clampd(x[m], 0.0, G.Lx), ym = clampd(y[m], 0.0, G.Ly), tx, ty;
         if (BASIC) {
-            ref_node(xm, G.dx, 0.0, 0, G.nx - 1, tx);
-            ref_node(ym, G.dy, 0.0, 0, G.ny - 1, ty);
+            ref_node(xm, G.dx, G.rdx, 0.0, 0, G.nx - 1, tx);
+            ref_node(ym, G.dy, G.rdy, 0.0, 0, G.ny - 1, ty);
         } else {
-            ref_node(xm, G.dx, G.hx, -1, G.nx - 1, tx);
-            ref_node(ym, G.dy, G.hy, -1, G.ny - 1, ty);
+            ref_node(xm, G.dx, G.rdx, G.hx, -1, G.nx - 1, tx);
+            ref_node(ym, G.dy, G.rdy, G.hy, -1, G.ny - 1, ty);
         }
         rec[k] = make_double4(tx, ty, eta[m], BASIC ? rho[m] : 0.0);
     }
@@ -304,12 +316,12 @@ __device__ __forceinline__ void velocity_at(const MkGrid &G, const double *__res
     x = clampd(x, 0.0, G.Lx);
     y = clampd(y, 0.0, G.Ly);
     double tx, ty;
-    int jr = ref_node(x, G.dx, 0.0, 0, G.nx - 1, tx);
-    int ir = ref_node(y, G.dy, G.hy, -1, G.ny - 1, ty);
+    int jr = ref_node(x, G.dx, G.rdx, 0.0, 0, G.nx - 1, tx);
+    int ir = ref_node(y, G.dy, G.rdy, G.hy, -1, G.ny - 1, ty);
     u = interp4(tx, ty, vx_node(G, vx, ir, jr), vx_node(G, vx, ir, jr + 1), vx_node(G, vx, ir + 1, jr),
                 vx_node(G, vx, ir + 1, jr + 1));
-    jr = ref_node(x, G.dx, G.hx, -1, G.nx - 1, tx);
-    ir = ref_node(y, G.dy, 0.0, 0, G.ny - 1, ty);
+    jr = ref_node(x, G.dx, G.rdx, G.hx, -1, G.nx - 1, tx);
+    ir = ref_node(y, G.dy, G.rdy, 0.0, 0, G.ny - 1, ty);
     v = interp4(tx, ty, vy_node(G, vy, ir, jr), vy_node(G, vy, ir, jr + 1), vy_node(G, vy, ir + 1, jr),
                 vy_node(G, vy, ir + 1, jr + 1));
 }
@@ -405,6 +417,8 @@ MkGrid mk_grid(const stokes_s *h) {
     G.dy = h->Ly / h->ny;
     G.hx = 0.5 * G.dx;
     G.hy = 0.5 * G.dy;
+    G.rdx = 1.0 / G.dx;
+    G.rdy = 1.0 / G.dy;
     G.sW = h->bc[0] ? -1.0 : 1.0;
     G.sE = h->bc[1] ? -1.0 : 1.0;
     G.sN = h->bc[2] ? -1.0 : 1.0;

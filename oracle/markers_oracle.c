@@ -11,10 +11,11 @@
  *     PAPER.md:480-484 and accumulate w*phi and w into temporaries; then divide
  *     (PAPER.md:488-491).  Targets: basic nodes (eta_b, rho_b) and pressure nodes (eta_p).
  *   - grid -> marker: phi_m = sum of the four weighted node values.
- *   - advection (PAPER.md:560-578): forward Euler (Eq. euler_advection), Heun
- *     (Eq. heun_method) and classical RK4 (Eq. rk4_method, combination in the order of
- *     Listing rk4_agnostic), velocity frozen during the step
- *     (PAPER.md:520).
+ *   - advection (PAPER.md:560-600): forward Euler (Eq. euler_advection), Heun
+ *     (Eq. heun_method), classical RK4 (Eq. rk4_method, combination in the order of
+ *     Listing rk4_agnostic) and the locally polynomial integrator of
+ *     order 2 / 3 (Eq. lpi_update, J and H of the bilinear interpolant: reading R32),
+ *     velocity frozen during the step.
  *   - time step: CFL-like limit (formula of SPEC.md:151-154).
  * Readings: R28 stagger offsets, reference-node clamping and empty nodes;
  * R29 velocity mirrors in grid->marker; R30 closed-box clamping of stage and final
@@ -158,6 +159,35 @@ static void velocity_at(const vgrid *G, double Lx, double Ly, double x, double y
                  vy_node(G, ir + 1, jr + 1));
 }
 
+/* LPI (reading R32): value, gradient and mixed second derivative of the
+ * same bilinear interpolant at (tx, ty) of a cell with spacings (h1, h2):
+ *   d/dx = ((1-ty)(v01-v00) + ty(v11-v10))/dx,  d/dy = ((1-tx)(v10-v00) + tx(v11-v01))/dy,
+ *   d2/dxdy = (v11 - v10 - v01 + v00)/(dx dy)   (the pure second derivatives of a bilinear
+ *   function vanish). */
+static void jet4(double tx, double ty, double dx, double dy, double v00, double v01, double v10, double v11,
+                 double *val, double *gx, double *gy, double *gxy) {
+    *val = interp4(tx, ty, v00, v01, v10, v11);
+    *gx = ((1.0 - ty) * (v01 - v00) + ty * (v11 - v10)) / dx;
+    *gy = ((1.0 - tx) * (v10 - v00) + tx * (v11 - v01)) / dy;
+    *gxy = (v11 - v10 - v01 + v00) / (dx * dy);
+}
+
+/* u, v and J = [[du/dx, du/dy], [dv/dx, dv/dy]], Hu = d2u/dxdy, Hv = d2v/dxdy at (x, y) */
+static void velocity_jet(const vgrid *G, double Lx, double Ly, double x, double y, double *u, double *v, double *J,
+                         double *Hu, double *Hv) {
+    x = clampd(x, 0.0, Lx);
+    y = clampd(y, 0.0, Ly);
+    double tx, ty;
+    int jr = ref_node(x, G->dx, 0.0, 0, G->nx - 1, &tx);
+    int ir = ref_node(y, G->dy, 0.5 * G->dy, -1, G->ny - 1, &ty);
+    jet4(tx, ty, G->dx, G->dy, vx_node(G, ir, jr), vx_node(G, ir, jr + 1), vx_node(G, ir + 1, jr),
+         vx_node(G, ir + 1, jr + 1), u, &J[0], &J[1], Hu);
+    jr = ref_node(x, G->dx, 0.5 * G->dx, -1, G->nx - 1, &tx);
+    ir = ref_node(y, G->dy, 0.0, 0, G->ny - 1, &ty);
+    jet4(tx, ty, G->dx, G->dy, vy_node(G, ir, jr), vy_node(G, ir, jr + 1), vy_node(G, ir + 1, jr),
+         vy_node(G, ir + 1, jr + 1), v, &J[2], &J[3], Hv);
+}
+
 static int make_vgrid(vgrid *G, int nx, int ny, double Lx, double Ly, const int *bc, const double *vx,
                       const double *vy) {
     if (nx < 2 || ny < 2 || !(Lx > 0) || !(Ly > 0) || !bc || !vx || !vy) return M_EINVAL;
@@ -187,11 +217,29 @@ int oracle_advect_markers(int nx, int ny, double Lx, double Ly, const int *bc, l
     vgrid G;
     int st = make_vgrid(&G, nx, ny, Lx, Ly, bc, vx, vy);
     if (st) return st;
-    if (scheme < 0 || scheme > 2 || !isfinite(dt)) return M_EINVAL;
+    if (scheme < 0 || scheme > 4 || !isfinite(dt)) return M_EINVAL;
     long long clamped = 0;
     for (long long m = 0; m < n; m++) {
         double xA = xm[m], yA = ym[m], xn, yn;
         double u1, v1, u2, v2, u3, v3, u4, v4;
+        if (scheme >= 3) { /* Eq. lpi_update: order 2 (scheme 3) or 3 (scheme 4), reading R32 */
+            double J[4], Hu, Hv;
+            velocity_jet(&G, Lx, Ly, xA, yA, &u1, &v1, J, &Hu, &Hv);
+            double c2 = 0.5 * dt * dt, c3 = (1.0 / 6.0) * dt * dt * dt;
+            double jx = J[0] * u1 + J[1] * v1, jy = J[2] * u1 + J[3] * v1; /* J v0 */
+            xn = xA + dt * u1;
+            yn = yA + dt * v1;
+            xn = xn + c2 * jx;
+            yn = yn + c2 * jy;
+            if (scheme == 4) { /* (H : v0 v0)_i = 2 d2v_i/dxdy v0x v0y */
+                xn = xn + c3 * (2.0 * Hu * u1 * v1);
+                yn = yn + c3 * (2.0 * Hv * u1 * v1);
+            }
+            if (xn < 0.0 || xn > Lx || yn < 0.0 || yn > Ly) clamped++;
+            xm[m] = clampd(xn, 0.0, Lx);
+            ym[m] = clampd(yn, 0.0, Ly);
+            continue;
+        }
         velocity_at(&G, Lx, Ly, xA, yA, &u1, &v1);
         if (scheme == 0) { /* Eq. euler_advection */
             xn = xA + dt * u1;

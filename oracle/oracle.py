@@ -275,7 +275,7 @@ class Oracle:
 
 
 # ---------------------------------------------------------------- marker-in-cell (NEXT-4)
-SCHEMES = {"euler": 0, "heun": 1, "rk4": 2}
+SCHEMES = {"euler": 0, "heun": 1, "rk4": 2, "lpi2": 3, "lpi3": 4}
 
 
 def _bc(bc):

@@ -237,3 +237,58 @@ def test_timestep_closed_form():
     vy[2, 1] = 4.0
     assert O.marker_timestep(nx, ny, 1.0, 1.0, vx, vy, 0.5, 3.0) == min(0.5 * (1 / 8) / 2, 0.5 * (1 / 4) / 4)
     assert O.marker_timestep(nx, ny, 1.0, 1.0, vx, vy, 0.5, 1e-3) == 1e-3
+
+
+# ---------------------------------------------------------------- LPI (R32)
+@pytest.mark.parametrize("scheme", ["lpi2", "lpi3"])
+def test_lpi_linear_field_is_heun(scheme):
+    """On a linear field J is exact and H = 0: both orders give 1 + z + z^2/2 (= Heun)."""
+    nx, ny, a, xc, yc = 16, 16, 0.8, 0.5, 0.5
+    vx, vy = linear_field(nx, ny, a, xc, yc)
+    rng = np.random.default_rng(12)
+    xm = 0.3 + 0.4 * rng.random(100)
+    ym = 0.3 + 0.4 * rng.random(100)
+    for dt in (0.05, 0.2):
+        x1, y1, nc = O.advect_markers(nx, ny, 1.0, 1.0, (0, 0, 0, 0), xm, ym, vx, vy, dt, scheme)
+        z = a * dt
+        np.testing.assert_allclose(x1 - xc, (xm - xc) * (1 + z + z * z / 2), rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(y1 - yc, (ym - yc) * (1 - z + z * z / 2), rtol=1e-12, atol=1e-15)
+
+
+def test_lpi_bilinear_field_closed_form():
+    """v = (c X Y, d) with X = x - xc, Y = y - yc is reproduced exactly by the bilinear
+    interpolant: J = [[cY, cX], [0, 0]], d2vx/dxdy = c, so (Eq. lpi_update)
+    x' = x + dt cXY + dt^2/2 (c^2 X Y^2 + c d X) + dt^3/6 (2 c^2 d X Y),  y' = y + dt d."""
+    nx = ny = 20
+    c, d, xc, yc = 1.3, 0.4, 0.45, 0.55
+    dx = dy = 1.0 / nx
+    X = np.arange(nx + 1) * dx - xc
+    Y = (np.arange(ny) + 0.5) * dy - yc
+    vx = c * Y[:, None] * X[None, :]
+    vy = np.full((ny + 1, nx), d)
+    rng = np.random.default_rng(13)
+    xm = 0.2 + 0.6 * rng.random(200)
+    ym = 0.2 + 0.5 * rng.random(200)
+    dt = 0.05
+    Xm, Ym = xm - xc, ym - yc
+    for scheme, k3 in (("lpi2", 0.0), ("lpi3", 1.0)):
+        x1, y1, _ = O.advect_markers(nx, ny, 1.0, 1.0, (0, 0, 0, 0), xm, ym, vx, vy, dt, scheme)
+        ex = xm + dt * c * Xm * Ym + dt ** 2 / 2 * (c * c * Xm * Ym ** 2 + c * d * Xm) + \
+            k3 * dt ** 3 / 6 * (2 * c * c * d * Xm * Ym)
+        np.testing.assert_allclose(x1, ex, rtol=0, atol=1e-14)
+        np.testing.assert_allclose(y1, ym + dt * d, rtol=0, atol=1e-15)
+
+
+def test_lpi_rotation_second_order():
+    nx = ny = 32
+    dx = dy = 1.0 / nx
+    om = 2 * math.pi
+    vx = np.repeat((-om * ((np.arange(ny) + 0.5) * dy - 0.5))[:, None], nx + 1, axis=1)
+    vy = np.repeat((om * ((np.arange(nx) + 0.5) * dx - 0.5))[None, :], ny + 1, axis=0)
+    e = []
+    for nsteps in (64, 128):
+        x, y = np.array([0.75]), np.array([0.5])
+        for _ in range(nsteps):
+            x, y, _ = O.advect_markers(nx, ny, 1.0, 1.0, (0, 0, 0, 0), x, y, vx, vy, 1.0 / nsteps, "lpi2")
+        e.append(math.hypot(x[0] - 0.75, y[0] - 0.5))
+    assert 0.8 * 4 < e[0] / e[1] < 1.25 * 4, e

@@ -224,7 +224,8 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
  * first call allocates marker scratch (~64 B per marker + 12 B per cell, freed by
  * stokes_destroy; STOKES_ENOMEM if that fails).  Results are bit-identical to the serial
  * CPU loops of the paper (the node sums are taken in ascending marker index). */
-enum { STOKES_ADVECT_EULER = 0, STOKES_ADVECT_HEUN = 1, STOKES_ADVECT_RK4 = 2 };
+enum { STOKES_ADVECT_EULER = 0, STOKES_ADVECT_HEUN = 1, STOKES_ADVECT_RK4 = 2, STOKES_ADVECT_LPI2 = 3,
+       STOKES_ADVECT_LPI3 = 4 };
 
 /* Marker -> grid (§4.2 steps 1-5; reading R28): every node value is
  *   phi(node) = sum_m w_m phi_m / sum_m w_m
@@ -242,9 +243,11 @@ int stokes_markers_to_grid(stokes_t h, long long n, const double *xm, const doub
  * boundary conditions of the handle) at marker m. */
 int stokes_grid_to_markers(stokes_t h, long long n, const double *xm, const double *ym, const double *vx,
                            const double *vy, double *vxm, double *vym);
-/* One advection step of every marker IN PLACE (PAPER.md:560-578; R30) with the velocity
+/* One advection step of every marker IN PLACE (PAPER.md:560-600; R30) with the velocity
  * frozen: scheme STOKES_ADVECT_EULER (Eq. euler_advection), _HEUN
- * (Eq. heun_method) or _RK4 (Eq. rk4_method, Listing rk4_agnostic order).  Stage and final
+ * (Eq. heun_method), _RK4 (Eq. rk4_method, Listing rk4_agnostic order) or the locally
+ * polynomial integrator _LPI2 / _LPI3 (Eq. lpi_update truncated after the J or the H term;
+ * J and H are the derivatives of the bilinear velocity interpolant, reading R32).  Stage and final
  * positions are clamped into the closed box; *n_clamped (HOST, nullable; synchronises) =
  * markers whose final position was clamped. */
 int stokes_advect_markers(stokes_t h, long long n, double *xm, double *ym, const double *vx, const double *vy,

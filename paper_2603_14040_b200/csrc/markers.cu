@@ -5,8 +5,9 @@
 //                           averages of the marker values with the bilinear weights of
 //                           PAPER.md:480-484 (reading R28).
 //   stokes_grid_to_markers  PAPER.md:497-511: velocity at the markers (R29).
-//   stokes_advect_markers   PAPER.md:560-578: Euler / Heun / RK4 (Listing rk4_agnostic order,
-//                           PAPER.md:2226-2254), closed-box clamping (R30).
+//   stokes_advect_markers   PAPER.md:560-600: Euler / Heun / RK4 (Listing rk4_agnostic order,
+//                           PAPER.md:2226-2254), locally polynomial order 2 / 3 (R32),
+//                           closed-box clamping (R30).
 //   stokes_marker_timestep  PAPER.md:526-532 CFL-like step (R31).
 //
 // Determinism (the paper's scatter-add with atomics, is order-dependent):
@@ -326,6 +327,32 @@ __device__ __forceinline__ void velocity_at(const MkGrid &G, const double *__res
                 vy_node(G, vy, ir + 1, jr + 1));
 }
 
+// LPI (R32): value, gradient and mixed second derivative of the same bilinear interpolant
+__device__ __forceinline__ void jet4(double tx, double ty, const MkGrid &G, double v00, double v01, double v10,
+                                     double v11, double &val, double &gx, double &gy, double &gxy) {
+    val = interp4(tx, ty, v00, v01, v10, v11);
+    gx = __ddiv_rn(__dadd_rn(__dmul_rn(__dsub_rn(1.0, ty), __dsub_rn(v01, v00)), __dmul_rn(ty, __dsub_rn(v11, v10))),
+                   G.dx);
+    gy = __ddiv_rn(__dadd_rn(__dmul_rn(__dsub_rn(1.0, tx), __dsub_rn(v10, v00)), __dmul_rn(tx, __dsub_rn(v11, v01))),
+                   G.dy);
+    gxy = __ddiv_rn(__dadd_rn(__dsub_rn(__dsub_rn(v11, v10), v01), v00), __dmul_rn(G.dx, G.dy));
+}
+__device__ __forceinline__ void velocity_jet(const MkGrid &G, const double *__restrict__ vx,
+                                             const double *__restrict__ vy, double x, double y, double &u,
+                                             double &v, double J[4], double &Hu, double &Hv) {
+    x = clampd(x, 0.0, G.Lx);
+    y = clampd(y, 0.0, G.Ly);
+    double tx, ty;
+    int jr = ref_node(x, G.dx, G.rdx, 0.0, 0, G.nx - 1, tx);
+    int ir = ref_node(y, G.dy, G.rdy, G.hy, -1, G.ny - 1, ty);
+    jet4(tx, ty, G, vx_node(G, vx, ir, jr), vx_node(G, vx, ir, jr + 1), vx_node(G, vx, ir + 1, jr),
+         vx_node(G, vx, ir + 1, jr + 1), u, J[0], J[1], Hu);
+    jr = ref_node(x, G.dx, G.rdx, G.hx, -1, G.nx - 1, tx);
+    ir = ref_node(y, G.dy, G.rdy, 0.0, 0, G.ny - 1, ty);
+    jet4(tx, ty, G, vy_node(G, vy, ir, jr), vy_node(G, vy, ir, jr + 1), vy_node(G, vy, ir + 1, jr),
+         vy_node(G, vy, ir + 1, jr + 1), v, J[2], J[3], Hv);
+}
+
 __global__ void k_mk_g2m(long long n, const double *__restrict__ x, const double *__restrict__ y, MkGrid G,
                          const double *__restrict__ vx, const double *__restrict__ vy, double *__restrict__ um,
                          double *__restrict__ vm) {
@@ -346,6 +373,20 @@ __global__ void k_mk_advect(long long n, double *__restrict__ x, double *__restr
     bool out = false;
     if (m < n) {
         double xA = x[m], yA = y[m], xn, yn, u1, v1;
+        if (SCHEME >= 3) {  // Eq. lpi_update, order 2 (3) or 3 (4): x + dt v0 + dt^2/2 J v0 (+ dt^3/6 H:v0v0)
+            double J[4], Hu, Hv;
+            velocity_jet(G, vx, vy, xA, yA, u1, v1, J, Hu, Hv);
+            const double c2 = __dmul_rn(__dmul_rn(0.5, dt), dt);
+            const double jx = __dadd_rn(__dmul_rn(J[0], u1), __dmul_rn(J[1], v1));
+            const double jy = __dadd_rn(__dmul_rn(J[2], u1), __dmul_rn(J[3], v1));
+            xn = __dadd_rn(__dadd_rn(xA, __dmul_rn(dt, u1)), __dmul_rn(c2, jx));
+            yn = __dadd_rn(__dadd_rn(yA, __dmul_rn(dt, v1)), __dmul_rn(c2, jy));
+            if (SCHEME == 4) {  // (H : v0 v0)_i = 2 d2v_i/dxdy v0x v0y
+                const double c3 = __dmul_rn(__dmul_rn(__dmul_rn(1.0 / 6.0, dt), dt), dt);
+                xn = __dadd_rn(xn, __dmul_rn(c3, __dmul_rn(__dmul_rn(__dmul_rn(2.0, Hu), u1), v1)));
+                yn = __dadd_rn(yn, __dmul_rn(c3, __dmul_rn(__dmul_rn(__dmul_rn(2.0, Hv), u1), v1)));
+            }
+        } else {
         velocity_at(G, vx, vy, xA, yA, u1, v1);
         if (SCHEME == 0) {  // Eq. euler_advection
             xn = __dadd_rn(xA, __dmul_rn(dt, u1));
@@ -371,6 +412,7 @@ __global__ void k_mk_advect(long long n, double *__restrict__ x, double *__restr
             double ve = __dmul_rn(sixth, __dadd_rn(__dadd_rn(__dadd_rn(v1, __dmul_rn(2.0, v2)), __dmul_rn(2.0, v3)), v4));
             xn = __dadd_rn(xA, __dmul_rn(dt, ue));
             yn = __dadd_rn(yA, __dmul_rn(dt, ve));
+        }
         }
         out = xn < 0.0 || xn > G.Lx || yn < 0.0 || yn > G.Ly;
         x[m] = clampd(xn, 0.0, G.Lx);
@@ -560,7 +602,7 @@ int stokes_grid_to_markers(stokes_t h, long long n, const double *xm, const doub
 int stokes_advect_markers(stokes_t h, long long n, double *xm, double *ym, const double *vx, const double *vy,
                           double dt, int scheme, long long *n_clamped) {
     if (check_single(h)) return STOKES_EINVAL;
-    if (n < 0 || (n > 0 && (!xm || !ym || !vx || !vy)) || scheme < 0 || scheme > 2 || !isfinite(dt))
+    if (n < 0 || (n > 0 && (!xm || !ym || !vx || !vy)) || scheme < 0 || scheme > 4 || !isfinite(dt))
         return STOKES_EINVAL;
     int st = mk_reserve(h, 256);
     if (st) return st;
@@ -572,7 +614,9 @@ int stokes_advect_markers(stokes_t h, long long n, double *xm, double *ym, const
         unsigned nb = blocks_for(n, TPB);
         if (scheme == 0) k_mk_advect<0><<<nb, TPB, 0, c.stream>>>(n, xm, ym, G, vx, vy, dt, cl);
         else if (scheme == 1) k_mk_advect<1><<<nb, TPB, 0, c.stream>>>(n, xm, ym, G, vx, vy, dt, cl);
-        else k_mk_advect<2><<<nb, TPB, 0, c.stream>>>(n, xm, ym, G, vx, vy, dt, cl);
+        else if (scheme == 2) k_mk_advect<2><<<nb, TPB, 0, c.stream>>>(n, xm, ym, G, vx, vy, dt, cl);
+        else if (scheme == 3) k_mk_advect<3><<<nb, TPB, 0, c.stream>>>(n, xm, ym, G, vx, vy, dt, cl);
+        else k_mk_advect<4><<<nb, TPB, 0, c.stream>>>(n, xm, ym, G, vx, vy, dt, cl);
         ++*c.counter;
         CKL();
     }

@@ -353,7 +353,7 @@ class Stokes:
         return vx, vy
 
     # ------------------------------------------------------------ marker-in-cell (NEXT-4)
-    ADVECT = {"euler": 0, "heun": 1, "rk4": 2}
+    ADVECT = {"euler": 0, "heun": 1, "rk4": 2, "lpi2": 3, "lpi3": 4}
 
     def _marker(self, t, n=None):
         t = self._dev(t)

@@ -91,7 +91,7 @@ def test_g2m_bitexact(S, nx, ny, bc):
     assert np.array_equal(H(um), ru) and np.array_equal(H(vm), rv)
 
 
-@pytest.mark.parametrize("scheme", ["euler", "heun", "rk4"])
+@pytest.mark.parametrize("scheme", ["euler", "heun", "rk4", "lpi2", "lpi3"])
 @pytest.mark.parametrize("bc", BCS)
 def test_advect_bitexact(S, scheme, bc):
     nx, ny = 33, 17

@@ -100,7 +100,7 @@ def main():
     ms = timed(lambda: s.grid_to_markers(xm, ym, vx, vy), args.reps, st)
     rec("grid_to_markers", ms, 32 * n + 16 * cells)
     dt = s.marker_timestep(vx, vy, 0.5, 1e9)
-    for scheme in ("euler", "heun", "rk4"):
+    for scheme in ("euler", "heun", "rk4", "lpi2", "lpi3"):
         x2, y2 = xm.clone(), ym.clone()
         ms = timed(lambda: s.advect_markers(x2, y2, vx, vy, dt, scheme, count_clamped=False), args.reps, st)
         rec("advect_" + scheme, ms, 32 * n + 16 * cells)

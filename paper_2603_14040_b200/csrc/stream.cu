@@ -558,7 +558,10 @@ constexpr int SMEM2 = NS2 * NF * RW * 8 + 4 * 2 * TW * 8 + NS2 * 8;
 #ifndef J2_LATE
 #define J2_LATE 0
 #endif
-constexpr int JT = 320, JRW = JT + 4, NSJ = J2_NSJ;
+#ifndef J2_JT
+#define J2_JT 320
+#endif
+constexpr int JT = J2_JT, JRW = JT + 4, NSJ = J2_NSJ;
 constexpr int SMEMJ = NSJ * NF * JRW * 8 + 4 * 2 * JT * 8 + NSJ * 8;
 
 struct J2Args {

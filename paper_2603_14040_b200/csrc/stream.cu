@@ -549,7 +549,6 @@ void fill_src(const double **src, const double *vx, const double *vy, const doub
 // first sweep).  (A warp-specialised variant exchanging the intermediate iterate by warp
 // shuffles, without CTA barriers, measured 435 us vs 340 us for this one at 4096^2.)
 constexpr int NS2 = 6;  // landing ring depth
-constexpr int SMEM2 = NS2 * NF * RW * 8 + 4 * 2 * TW * 8 + NS2 * 8;
 // the two-sweep pass runs wider CTAs: 320 threads (10 warps, 2 CTAs = 20 warps per SM at
 // 96 registers), a 5-row ring of 324-wide rows (98 KB per CTA)
 #ifndef J2_NSJ
@@ -791,7 +790,15 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
 // k_restrict_vel (Appendix B; rows / columns outside the domain dropped and renormalised).
 // The fine residual never reaches HBM: 48 B/fine cell read + 4 B written instead of 84.
 // Single-domain levels only (jacobi2_ok).
-constexpr int SMEMRR = NS2 * NF * RW * 8 + 8 * 2 * TW * 8 + NS2 * 8;
+#ifndef RR_NS
+#define RR_NS 6
+#endif
+#ifndef RR_ROWS
+#define RR_ROWS 8
+#endif
+constexpr int NSRR = RR_NS;      // landing ring depth of the residual+restriction pass
+constexpr int RRR = RR_ROWS;     // residual rows kept for the restriction (>= 5: rows 2I-2..2I+1 + the next)
+constexpr int SMEMRR = NSRR * NF * RW * 8 + RRR * 2 * TW * 8 + NSRR * 8;
 
 struct RRArgs {
     const double *src[6];  // vx, vy, eta_p, eta_b, p | bx, rho | by
@@ -803,8 +810,8 @@ struct RRArgs {
 template <int MODE>
 __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRArgs a, int HC) {
     extern __shared__ __align__(128) double sm[];
-    double *rr = sm + NS2 * NF * RW;  // [8 rows][rx, ry][TW]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(rr + 8 * 2 * TW);
+    double *rr = sm + NSRR * NF * RW;  // [RRR rows][rx, ry][TW]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(rr + RRR * 2 * TW);
     const int t = threadIdx.x;
     const int j0 = 1 + a.tw * blockIdx.x;  // odd: coarse columns (j0+1)/2 ..
     const int c = j0 - 1 + t;
@@ -814,7 +821,7 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
     const int rlo = ilo - 1, rhi = ihi + 1;
     const size_t P = g.P;
     auto issue = [&](int r) {
-        const int slot = (r - rlo) % NS2;
+        const int slot = (r - rlo) % NSRR;
         uint64_t *bar = bars + slot;
         mbar_expect_tx(bar, NF * RW * 8);
 #pragma unroll
@@ -822,22 +829,22 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
             bulk_g2s(sm + (slot * NF + f) * RW, a.src[f] + (size_t)r * P + (j0 - 2), RW * 8, bar);
     };
     if (t == 0) {
-        for (int k = 0; k < NS2; ++k) mbar_init(bars + k, 1);
+        for (int k = 0; k < NSRR; ++k) mbar_init(bars + k, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (t == 0)
-        for (int r = rlo; r < rlo + NS2 && r <= rhi; ++r) issue(r);
+        for (int r = rlo; r < rlo + NSRR && r <= rhi; ++r) issue(r);
     Win w;
     auto consume = [&](int r) {
         const int rel = r - rlo;
-        mbar_wait(bars + rel % NS2, (rel / NS2) & 1);
-        w.template push<NF>(sm + (rel % NS2) * NF * RW, t + 1);
+        mbar_wait(bars + rel % NSRR, (rel / NSRR) & 1);
+        w.template push<NF>(sm + (rel % NSRR) * NF * RW, t + 1);
     };
     auto refill = [&](int r) {
-        if (t == 0 && r + NS2 <= rhi) {
+        if (t == 0 && r + NSRR <= rhi) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(r + NS2);
+            issue(r + NSRR);
         }
     };
     consume(rlo);
@@ -862,8 +869,8 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
             const double b = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
             ry = b - ly_win(g, w, c).L;
         }
-        rr[((i & 7) * 2 + 0) * TW + t] = rx;
-        rr[((i & 7) * 2 + 1) * TW + t] = ry;
+        rr[((i % RRR) * 2 + 0) * TW + t] = rx;
+        rr[((i % RRR) * 2 + 1) * TW + t] = ry;
         __syncthreads();
         refill(i + 1);
         const int I = (i & 1) ? (i - 1) / 2 : (i == g.ncy ? i / 2 : 0);  // coarse row completed by row i
@@ -875,7 +882,7 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
                 for (int d = 0; d < 4; ++d) {
                     const int fi = 2 * I - 2 + d;
                     if ((fi < 1 && g.bN) || (fi > g.ncy && g.bS)) continue;
-                    const double *row = rr + ((fi & 7) * 2 + 0) * TW;
+                    const double *row = rr + ((fi % RRR) * 2 + 0) * TW;
                     const double h = 0.5 * row[q - 1] + row[q] + 0.5 * row[q + 1];
                     const double wd = (d == 0 || d == 3) ? 0.25 : 0.75;
                     sx += wd * h;
@@ -890,9 +897,9 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
                 for (int d = 0; d < 4; ++d) {
                     const int fj = 2 * J - 2 + d;
                     if ((fj < 1 && g.bW) || (fj > g.ncx && g.bE)) continue;
-                    const double col = 0.5 * rr[(((2 * I - 1) & 7) * 2 + 1) * TW + q + d] +
-                                       rr[(((2 * I) & 7) * 2 + 1) * TW + q + d] +
-                                       0.5 * rr[(((2 * I + 1) & 7) * 2 + 1) * TW + q + d];
+                    const double col = 0.5 * rr[(((2 * I - 1) % RRR) * 2 + 1) * TW + q + d] +
+                                       rr[(((2 * I) % RRR) * 2 + 1) * TW + q + d] +
+                                       0.5 * rr[(((2 * I + 1) % RRR) * 2 + 1) * TW + q + d];
                     const double wd = (d == 0 || d == 3) ? 0.25 : 0.75;
                     sy += wd * col;
                     wsum += wd;

@@ -548,9 +548,8 @@ void fill_src(const double **src, const double *vx, const double *vy, const doub
 // sweeps.  Single-domain levels only (a decomposed tile's halo would be stale after the
 // first sweep).  (A warp-specialised variant exchanging the intermediate iterate by warp
 // shuffles, without CTA barriers, measured 435 us vs 340 us for this one at 4096^2.)
-constexpr int NS2 = 6;  // landing ring depth
 // the two-sweep pass runs wider CTAs: 320 threads (10 warps, 2 CTAs = 20 warps per SM at
-// 96 registers), a 5-row ring of 324-wide rows (98 KB per CTA)
+// 96 registers), a 6-row ring of 324-wide rows (114 KB per CTA)
 #ifndef J2_NSJ
 #define J2_NSJ 6  // 6-deep landing ring: 303.7 -> 284.5 us at 4096^2 vs 5 (TMA latency)
 #endif

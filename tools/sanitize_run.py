@@ -1,5 +1,6 @@
-"""Small solves exercising every kernel (single domain Jacobi/RBGS/GCR incl. the TMA
-streaming kernels, decomposed virtual + loopback) for compute-sanitizer runs."""
+"""Small solves exercising every kernel (single domain Jacobi/RBGS/GCR/Anderson/RAS/Mixed
+incl. the TMA streaming kernels, viscosity stages, lithostatic pressure, decomposed virtual +
+loopback, the marker-in-cell kernels) for compute-sanitizer runs."""
 import os
 import sys
 
@@ -9,7 +10,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2603_14040_b200 import Stokes, StokesDist  # noqa: E402
-from synth.fields import workload  # noqa: E402
+from synth.fields import markers, workload  # noqa: E402
 
 os.environ["STOKES_DIST_DMIN"] = "8"
 T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
@@ -38,4 +39,20 @@ s.set_density(T(w["rho_b"]))
 s.set_gravity(0, 1)
 for k in Stokes.KERNELS:
     s.time_kernel(k, 1)
-print("done")
+run(Stokes, 256, "layered", omega_v=0.6, alpha_p=1.0, accel=2, aa_depth=5, aa_beta=0.7, max_iter=4)
+run(Stokes, 256, "layered", omega_v=0.6, alpha_p=1.0, smoother=3, max_iter=2)
+run(Stokes, 128, "block", omega_v=0.6, alpha_p=1.0, smoother=2, accel=1, max_iter=3)
+run(Stokes, 128, "sinker", omega_v=0.3, alpha_p=0.6, theta_step=0.5, theta_every=2, max_iter=6)
+s.lithostatic()
+m = markers(200, 130, 1.0, 1.0, per_side=3, seed=1, order="shuffled", props="sinker")
+q = Stokes(200, 130, 1.0, 1.0)
+xm, ym = T(m["xm"]), T(m["ym"])
+eb, ep, rb, ne = q.markers_to_grid(xm, ym, T(m["eta_m"]), T(m["rho_m"]))
+vx = torch.randn(130, 201, dtype=torch.float64, device="cuda")
+vy = torch.randn(131, 200, dtype=torch.float64, device="cuda")
+q.grid_to_markers(xm, ym, vx, vy)
+dt = q.marker_timestep(vx, vy, 0.5, 1.0)
+for sch in Stokes.ADVECT:
+    q.advect_markers(xm, ym, vx, vy, dt, sch)
+torch.cuda.synchronize()
+print("done", ne)

@@ -268,10 +268,55 @@ void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&
 // One V-cycle (Eq. multigrid_levels) on level l for L v = b, v in
 // (ax, ay) with scratch (bx_, by_); the result is left in (ax, ay) (the sweep count per
 // cycle, 2 nu, is even).  zero_in: the initial guess is 0 (coarse corrections).
+// Coarse tail in one CTA (kernels.cu k_vtail): from level l down, when every remaining level
+// is a small single-domain damped-Jacobi level and the coarsest is solved directly.
+// STOKES_VTAIL=0 disables it; STOKES_VTAIL_CELLS sets the largest level (cells) it starts at.
+static int vtail_cells() {
+    static const int v = [] {
+        const char *e = getenv("STOKES_VTAIL");
+        if (e && e[0] == '0') return 0;
+        const char *c = getenv("STOKES_VTAIL_CELLS");
+        return c ? atoi(c) : 1024;
+    }();
+    return v;
+}
+static bool vtail_ok(stokes_s *h, int l) {
+    if (!h->o.coarse_direct || h->nc <= 0 || h->nlev - l > TAIL_MAXL || h->nlev - l < 2) return false;
+    const GridL &g0 = h->lev[l].g;
+    if ((long long)g0.ncx * g0.ncy > vtail_cells()) return false;
+    for (int k = l; k < h->nlev; ++k) {
+        const GridL &g = h->lev[k].g;
+        if (!(g.bN && g.bS && g.bW && g.bE) || jacobi2_ok(g)) return false;
+        if (k < h->nlev - 1 && level_smoother(h, k) != STOKES_SMOOTH_JACOBI) return false;
+    }
+    return true;
+}
 void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in,
             int done_pre) {
     Level &L = h->lev[l];
     const LaunchCtx c = ctx(h);
+    if (zero_in && !done_pre && rhs.mode == RHS_ARRAYS && vtail_ok(h, l)) {
+        TailArgs a;
+        a.nl = h->nlev - l;
+        for (int k = 0; k < a.nl; ++k) {
+            Level &T = h->lev[l + k];
+            TailLevel &t = a.lev[k];
+            t.g = T.g;
+            t.etab = T.etab;
+            t.etap = T.etap;
+            t.bx = k == 0 ? const_cast<double *>(rhs.bx) : T.bx;
+            t.by = k == 0 ? const_cast<double *>(rhs.by) : T.by;
+            t.ax = k == 0 ? ax : T.vx[0];
+            t.ay = k == 0 ? ay : T.vy[0];
+            t.sx = k == 0 ? sx : T.vx[1];
+            t.sy = k == 0 ? sy : T.vy[1];
+            t.rx = T.rx;
+            t.ry = T.ry;
+            t.nu = T.nu;
+        }
+        launch_vtail(c, a, h->Minv, h->nc, h->o.omega_v);
+        return;
+    }
     double *cx = ax, *cy = ay, *ox = sx, *oy = sy;
     if (done_pre) {  // the first pre-smoothing sweep was done by a fused kernel into (sx, sy)
         cx = sx; cy = sy; ox = ax; oy = ay;

@@ -64,6 +64,22 @@ void launch_restrict_vx(const LaunchCtx &c, const GridL &gf, const GridL &gc, co
 void launch_restrict_vy(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *f, double *cc);
 void launch_prolong(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *exc, const double *eyc,
                     double *vx, double *vy);
+// coarse tail of the V-cycle in one CTA (levels 0..nl-1 of the tail, the last one solved by
+// the explicit inverse): lev[l].(ax, ay) = V-cycle result with zero initial guess on
+// L v = (bx, by); (sx, sy, rx, ry) scratch.  Single-domain Jacobi levels only.
+#define TAIL_MAXL 6
+struct TailLevel {
+    GridL g;
+    const double *etab, *etap;
+    double *bx, *by;  // level 0: the caller's right-hand side (read only); below: restricted residuals
+    double *ax, *ay, *sx, *sy, *rx, *ry;
+    int nu;
+};
+struct TailArgs {
+    TailLevel lev[TAIL_MAXL];
+    int nl;
+};
+void launch_vtail(const LaunchCtx &c, const TailArgs &a, const double *Minv, int n, double omega);
 // full saddle residual + energy partial sums (Sv, Sp) per block; writes r arrays if non-null.
 // force_only: Sv of f (the normaliser Sf).  Returns the number of partial blocks.
 int energy_blocks(const GridL &g);

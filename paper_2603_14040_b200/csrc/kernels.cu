@@ -107,13 +107,10 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
 // reads only the old iterate (ping-pong buffers).  zero_in: the old iterate is 0 (first
 // sweep of a coarse correction), so v_in is not read.
 template <bool ZERO>
-__global__ void __launch_bounds__(BX *BY) k_jacobi(GridL g, const double *__restrict__ etab,
-                                                   const double *__restrict__ etap, const double *__restrict__ vxi,
-                                                   const double *__restrict__ vyi, double *__restrict__ vxo,
-                                                   double *__restrict__ vyo, RhsArgs rhs, double omega) {
-    const int j = blockIdx.x * BX + threadIdx.x + 1;
-    const int i = blockIdx.y * BY + threadIdx.y + 1;
-    if (i > g.ncy || j > g.ncx) return;
+__device__ __forceinline__ void jacobi_pt(const GridL &g, const double *__restrict__ etab,
+                                          const double *__restrict__ etap, const double *__restrict__ vxi,
+                                          const double *__restrict__ vyi, double *__restrict__ vxo,
+                                          double *__restrict__ vyo, const RhsArgs &rhs, double omega, int i, int j) {
     const ArrayAcc ax{vxi, (size_t)g.P}, ay{vyi, (size_t)g.P};
     if (j <= g.nvxj) {
         const double a = lx_diag(g, etab, etap, i, j);
@@ -135,6 +132,16 @@ __global__ void __launch_bounds__(BX *BY) k_jacobi(GridL g, const double *__rest
         if (j == 1 && g.bW) vyo[at(g, i, 0)] = g.sW * vn;
         if (j == g.ncx && g.bE) vyo[at(g, i, g.ncx + 1)] = g.sE * vn;
     }
+}
+template <bool ZERO>
+__global__ void __launch_bounds__(BX *BY) k_jacobi(GridL g, const double *__restrict__ etab,
+                                                   const double *__restrict__ etap, const double *__restrict__ vxi,
+                                                   const double *__restrict__ vyi, double *__restrict__ vxo,
+                                                   double *__restrict__ vyo, RhsArgs rhs, double omega) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i > g.ncy || j > g.ncx) return;
+    jacobi_pt<ZERO>(g, etab, etap, vxi, vyi, vxo, vyo, rhs, omega, i, j);
 }
 
 // Damped red-black Gauss-Seidel (Eq. sor_update), one of the four phases
@@ -164,6 +171,14 @@ __global__ void __launch_bounds__(BX *BY) k_rbgs_phase(GridL g, const double *__
 }
 
 // r = b - L v (Eq. mg_residual) at the unknowns of a level.
+__device__ __forceinline__ void residual_pt(const GridL &g, const double *__restrict__ etab,
+                                            const double *__restrict__ etap, const double *__restrict__ vx,
+                                            const double *__restrict__ vy, const RhsArgs &rhs,
+                                            double *__restrict__ rx, double *__restrict__ ry, int i, int j) {
+    const ArrayAcc ax{vx, (size_t)g.P}, ay{vy, (size_t)g.P};
+    if (j <= g.nvxj) rx[at(g, i, j)] = rhs_x(g, rhs, i, j) - lx_row(g, etab, etap, ax, ay, i, j);
+    if (i <= g.nvyi) ry[at(g, i, j)] = rhs_y(g, rhs, i, j) - ly_row(g, etab, etap, ax, ay, i, j);
+}
 __global__ void __launch_bounds__(BX *BY) k_residual(GridL g, const double *__restrict__ etab,
                                                      const double *__restrict__ etap, const double *__restrict__ vx,
                                                      const double *__restrict__ vy, RhsArgs rhs,
@@ -171,9 +186,7 @@ __global__ void __launch_bounds__(BX *BY) k_residual(GridL g, const double *__re
     const int j = blockIdx.x * BX + threadIdx.x + 1;
     const int i = blockIdx.y * BY + threadIdx.y + 1;
     if (i > g.ncy || j > g.ncx) return;
-    const ArrayAcc ax{vx, (size_t)g.P}, ay{vy, (size_t)g.P};
-    if (j <= g.nvxj) rx[at(g, i, j)] = rhs_x(g, rhs, i, j) - lx_row(g, etab, etap, ax, ay, i, j);
-    if (i <= g.nvyi) ry[at(g, i, j)] = rhs_y(g, rhs, i, j) - ly_row(g, etab, etap, ax, ay, i, j);
+    residual_pt(g, etab, etap, vx, vy, rhs, rx, ry, i, j);
 }
 
 
@@ -224,11 +237,9 @@ __global__ void k_lithostatic(GridL g, const double *__restrict__ rb, double gy,
 // sum of the remaining weights renormalises.
 __device__ __forceinline__ double W4(int d) { return (d == 0 || d == 3) ? 0.25 : 0.75; }
 
-__global__ void k_restrict_vel(GridL gf, GridL gc, const double *__restrict__ rx, const double *__restrict__ ry,
-                               double *__restrict__ bxc, double *__restrict__ byc) {
-    const int J = blockIdx.x * BX + threadIdx.x + 1;
-    const int I = blockIdx.y * BY + threadIdx.y + 1;
-    if (I > gc.ncy || J > gc.ncx) return;
+__device__ __forceinline__ void restrict_vel_pt(const GridL &gf, const GridL &gc, const double *__restrict__ rx,
+                                                const double *__restrict__ ry, double *__restrict__ bxc,
+                                                double *__restrict__ byc, int I, int J) {
     if (bxc && J <= gc.nvxj) {  // vx: x vertex-centred, y cell-centred
         double s = 0.0, w = 0.0;
 #pragma unroll
@@ -253,6 +264,13 @@ __global__ void k_restrict_vel(GridL gf, GridL gc, const double *__restrict__ rx
         }
         byc[at(gc, I, J)] = s / (2.0 * w);
     }
+}
+__global__ void k_restrict_vel(GridL gf, GridL gc, const double *__restrict__ rx, const double *__restrict__ ry,
+                               double *__restrict__ bxc, double *__restrict__ byc) {
+    const int J = blockIdx.x * BX + threadIdx.x + 1;
+    const int I = blockIdx.y * BY + threadIdx.y + 1;
+    if (I > gc.ncy || J > gc.ncx) return;
+    restrict_vel_pt(gf, gc, rx, ry, bxc, byc, I, J);
 }
 // basic-node field (eta_b): [1/2,1,1/2] x [1/2,1,1/2] over fine basic nodes in [0,ncy]x[0,ncx]
 __global__ void k_restrict_b(GridL gf, GridL gc, const double *__restrict__ f, double *__restrict__ c) {
@@ -310,12 +328,9 @@ __global__ void k_restrict_p(GridL gf, GridL gc, const double *__restrict__ f, d
 // Bilinear prolongation + correction: each fine unknown adds the
 // hat-weighted coarse correction of its (up to) four surrounding coarse nodes; coarse
 // mirror nodes hold the homogeneous-BC image, coarse walls are 0 (Appendix B).
-__global__ void __launch_bounds__(BX *BY) k_prolong(GridL gf, GridL gc, const double *__restrict__ ex,
-                                                    const double *__restrict__ ey, double *__restrict__ vx,
-                                                    double *__restrict__ vy) {
-    const int j = blockIdx.x * BX + threadIdx.x + 1;
-    const int i = blockIdx.y * BY + threadIdx.y + 1;
-    if (i > gf.ncy || j > gf.ncx) return;
+__device__ __forceinline__ void prolong_pt(const GridL &gf, const GridL &gc, const double *__restrict__ ex,
+                                           const double *__restrict__ ey, double *__restrict__ vx,
+                                           double *__restrict__ vy, int i, int j) {
     if (j <= gf.nvxj) {  // vx: x vertex-centred, y cell-centred
         const int J0 = j >> 1;
         int I0;
@@ -350,6 +365,14 @@ __global__ void __launch_bounds__(BX *BY) k_prolong(GridL gf, GridL gc, const do
         if (j == 1 && gf.bW) vy[at(gf, i, 0)] = gf.sW * vn;
         if (j == gf.ncx && gf.bE) vy[at(gf, i, gf.ncx + 1)] = gf.sE * vn;
     }
+}
+__global__ void __launch_bounds__(BX *BY) k_prolong(GridL gf, GridL gc, const double *__restrict__ ex,
+                                                    const double *__restrict__ ey, double *__restrict__ vx,
+                                                    double *__restrict__ vy) {
+    const int j = blockIdx.x * BX + threadIdx.x + 1;
+    const int i = blockIdx.y * BY + threadIdx.y + 1;
+    if (i > gf.ncy || j > gf.ncx) return;
+    prolong_pt(gf, gc, ex, ey, vx, vy, i, j);
 }
 
 // Same prolongation, one thread per aligned pair of fine columns (2J-1, 2J) of one row:
@@ -770,10 +793,9 @@ __global__ void __launch_bounds__(1024) k_coarse_invert(double *__restrict__ wor
     }
 }
 // v = L_c^-1 b = -(-L_c)^-1 b on the coarsest unknowns; mirrors written.
-__global__ void __launch_bounds__(256) k_coarse_solve(GridL g, const double *__restrict__ Minv, int n,
-                                                      const double *__restrict__ bx, const double *__restrict__ by,
-                                                      double *__restrict__ vx, double *__restrict__ vy) {
-    extern __shared__ double u[];
+__device__ __forceinline__ void coarse_solve_cta(const GridL &g, const double *__restrict__ Minv, int n,
+                                                 const double *__restrict__ bx, const double *__restrict__ by,
+                                                 double *__restrict__ vx, double *__restrict__ vy, double *u) {
     const int nvx = g.ncy * (g.ncx - 1);
     for (int k = threadIdx.x; k < n; k += blockDim.x) {
         if (k < nvx) u[k] = bx[at(g, k / (g.ncx - 1) + 1, k % (g.ncx - 1) + 1)];
@@ -794,6 +816,87 @@ __global__ void __launch_bounds__(256) k_coarse_solve(GridL g, const double *__r
             vy[at(g, i, j)] = v;
             if (j == 1 && g.bW) vy[at(g, i, 0)] = g.sW * v;
             if (j == g.ncx && g.bE) vy[at(g, i, g.ncx + 1)] = g.sE * v;
+        }
+    }
+}
+__global__ void __launch_bounds__(256) k_coarse_solve(GridL g, const double *__restrict__ Minv, int n,
+                                                      const double *__restrict__ bx, const double *__restrict__ by,
+                                                      double *__restrict__ vx, double *__restrict__ vy) {
+    extern __shared__ double u[];
+    coarse_solve_cta(g, Minv, n, bx, by, vx, vy, u);
+}
+
+// ------------------------------------------------------------------ coarse tail (a9)
+// The V-cycle from a small level down to the coarsest and back in ONE CTA: the same point
+// operations as the per-level kernels (damped Jacobi with a zero first iterate, residual,
+// velocity restriction, direct coarsest solve, prolongation + correction) in the host
+// V-cycle's order, with a CTA barrier between stages instead of a kernel boundary.  Below
+// ~32^2 cells a level's kernels are launch-latency bound (~2.5 us each, 12-13 per level);
+// here a sweep of a 32^2 level is one point per thread.
+__device__ __forceinline__ RhsArgs make_rhs_arrays(const double *bx, const double *by) {
+    RhsArgs r;
+    r.mode = RHS_ARRAYS;
+    r.bx = bx;
+    r.by = by;
+    r.p = nullptr;
+    r.rho = nullptr;
+    r.gx = r.gy = 0.0;
+    return r;
+}
+__device__ __forceinline__ void tail_copy(const GridL &g, const double *src, double *dst) {
+    const int n = (g.ncy + 2) * g.P;  // padded rows (mirrors included)
+    for (int e = threadIdx.x; e < n; e += blockDim.x) dst[e - COL_OFF] = src[e - COL_OFF];
+}
+__global__ void __launch_bounds__(1024) k_vtail(TailArgs a, const double *__restrict__ Minv, int n, double omega) {
+    extern __shared__ double u[];
+    double *cx[TAIL_MAXL], *cy[TAIL_MAXL], *ox[TAIL_MAXL], *oy[TAIL_MAXL];
+    const int nt = blockDim.x;
+    auto sweeps = [&](int l, int nsw, bool zero_first) {
+        const TailLevel &L = a.lev[l];
+        const RhsArgs rhs = make_rhs_arrays(L.bx, L.by);
+        const int np = L.g.ncx * L.g.ncy;
+        for (int s = 0; s < nsw; ++s) {
+            for (int q = threadIdx.x; q < np; q += nt) {
+                const int i = q / L.g.ncx + 1, j = q % L.g.ncx + 1;
+                if (zero_first && s == 0) jacobi_pt<true>(L.g, L.etab, L.etap, cx[l], cy[l], ox[l], oy[l], rhs, omega, i, j);
+                else jacobi_pt<false>(L.g, L.etab, L.etap, cx[l], cy[l], ox[l], oy[l], rhs, omega, i, j);
+            }
+            __syncthreads();
+            double *t = cx[l]; cx[l] = ox[l]; ox[l] = t;
+            t = cy[l]; cy[l] = oy[l]; oy[l] = t;
+        }
+    };
+    const int last = a.nl - 1;
+    for (int l = 0; l < last; ++l) {  // down: pre-smoothing, residual, restriction
+        const TailLevel &L = a.lev[l], &C = a.lev[l + 1];
+        cx[l] = L.ax; cy[l] = L.ay; ox[l] = L.sx; oy[l] = L.sy;
+        sweeps(l, L.nu, true);
+        const RhsArgs rhs = make_rhs_arrays(L.bx, L.by);
+        const int np = L.g.ncx * L.g.ncy;
+        for (int q = threadIdx.x; q < np; q += nt)
+            residual_pt(L.g, L.etab, L.etap, cx[l], cy[l], rhs, L.rx, L.ry, q / L.g.ncx + 1, q % L.g.ncx + 1);
+        __syncthreads();
+        const int nc = C.g.ncx * C.g.ncy;
+        for (int q = threadIdx.x; q < nc; q += nt)
+            restrict_vel_pt(L.g, C.g, L.rx, L.ry, C.bx, C.by, q / C.g.ncx + 1, q % C.g.ncx + 1);
+        __syncthreads();
+    }
+    {  // coarsest: direct solve into its (ax, ay)
+        const TailLevel &L = a.lev[last];
+        coarse_solve_cta(L.g, Minv, n, L.bx, L.by, L.ax, L.ay, u);
+        __syncthreads();
+    }
+    for (int l = last - 1; l >= 0; --l) {  // up: prolongation + correction, post-smoothing
+        const TailLevel &L = a.lev[l], &C = a.lev[l + 1];
+        const int np = L.g.ncx * L.g.ncy;
+        for (int q = threadIdx.x; q < np; q += nt)
+            prolong_pt(L.g, C.g, C.ax, C.ay, cx[l], cy[l], q / L.g.ncx + 1, q % L.g.ncx + 1);
+        __syncthreads();
+        sweeps(l, L.nu, false);
+        if (cx[l] != L.ax) {  // an odd number of buffer swaps: result back to (ax, ay)
+            tail_copy(L.g, cx[l], L.ax);
+            tail_copy(L.g, cy[l], L.ay);
+            __syncthreads();
         }
     }
 }
@@ -1106,6 +1209,10 @@ void launch_coarse_solve(const LaunchCtx &c, const GridL &g, const double *Minv,
                          const double *by, double *vx, double *vy) {
     const int n = g.ncy * (g.ncx - 1) + (g.ncy - 1) * g.ncx;
     k_coarse_solve<<<1, 256, n * sizeof(double), c.stream>>>(g, Minv, n, bx, by, vx, vy);
+    LAUNCH_BOOK(c);
+}
+void launch_vtail(const LaunchCtx &c, const TailArgs &a, const double *Minv, int n, double omega) {
+    k_vtail<<<1, 1024, n * sizeof(double), c.stream>>>(a, Minv, n, omega);
     LAUNCH_BOOK(c);
 }
 int dot_blocks(const GridL &g) { return energy_blocks(g); }

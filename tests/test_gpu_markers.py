@@ -176,3 +176,36 @@ def test_mic_cycle_matches_oracle(S):
         s.advect_markers(gx, gy, g["vx"], g["vy"], dt, "rk4")
         ox, oy, _ = O.advect_markers(nx, ny, 1.0, 1.0, (0, 0, 0, 0), ox, oy, r["vx"], r["vy"], rdt, "rk4")
         assert np.max(np.abs(H(gx) - ox)) <= 1e-9 and np.max(np.abs(H(gy) - oy)) <= 1e-9
+
+
+def test_mic_block_sinks(S):
+    """Three steps of the MIC loop with the dense block (Delta rho = 1,
+    eta 1e3, BASELINE cfg 2 recipe) carried by markers: the block's markers move DOWN (+y,
+    gravity along +y, reading R4), stay centred in x (the problem is mirror-symmetric), no
+    marker leaves the box, and the CFL step keeps every displacement below half a cell."""
+    nx = ny = 64
+    m = markers(nx, ny, 1.0, 1.0, per_side=4, seed=9, order="cell", props="block")
+    s = S(nx, ny, 1.0, 1.0, omega_v=0.6, alpha_p=1.0, accel=1, gcr_restart=30)
+    s.set_gravity(0.0, 1.0)
+    gx, gy = T(m["xm"]), T(m["ym"])
+    eta, rho = T(m["eta_m"]), T(m["rho_m"])
+    inside = torch.from_numpy(m["eta_m"] > 10).cuda()
+    y0 = gy[inside].mean().item()
+    x0 = gx[inside].mean().item()
+    r = None
+    for _ in range(3):
+        eb, ep, rb, ne = s.markers_to_grid(gx, gy, eta, rho)
+        assert ne == 0
+        s.set_viscosity(eb, ep)
+        s.set_density(rb)
+        r = s.solve(1e-10, *((r["vx"], r["vy"], r["p"]) if r else ()))
+        assert r["status"] == 0
+        dt = s.marker_timestep(r["vx"], r["vy"], 0.5, 1e9)
+        px, py = gx.clone(), gy.clone()
+        assert s.advect_markers(gx, gy, r["vx"], r["vy"], dt, "rk4") == 0
+        assert (gx - px).abs().max().item() <= 0.5 / nx + 1e-12
+        assert (gy - py).abs().max().item() <= 0.5 / ny + 1e-12
+    y1 = gy[inside].mean().item()
+    x1 = gx[inside].mean().item()
+    assert y1 > y0 + 1e-4, (y0, y1)
+    assert abs(x1 - x0) < 0.05 * (y1 - y0), (x0, x1, y0, y1)  # jittered markers: nearly symmetric

@@ -213,3 +213,35 @@ def markers(nx, ny, Lx=1.0, Ly=1.0, per_side=4, jitter=1.0, seed=7, order="cell"
     eta_m, rho_m = MARKER_PROPS[props](ym, xm)
     return {"xm": np.ascontiguousarray(xm), "ym": np.ascontiguousarray(ym),
             "eta_m": np.ascontiguousarray(eta_m, np.float64), "rho_m": np.ascontiguousarray(rho_m, np.float64)}
+
+
+def markers_torch(nx, ny, per_side=4, seed=2603, props="layered", device="cuda"):
+    """The markers() lattice recipe generated ON THE GPU with a seeded torch generator (for
+    full-size runs whose marker arrays are too large to build in numpy): cell-major order,
+    per_side^2 per cell, uniform jitter of +-1/2 lattice spacing, unit box; properties from the
+    same continuous definitions.  Returns torch float64 tensors (xm, ym, eta_m, rho_m)."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    dx, dy = 1.0 / nx, 1.0 / ny
+    s = (torch.arange(per_side, device=device, dtype=torch.float64) + 0.5) / per_side
+    ci = torch.arange(ny, device=device, dtype=torch.float64).view(ny, 1, 1, 1)
+    cj = torch.arange(nx, device=device, dtype=torch.float64).view(1, nx, 1, 1)
+    xm = ((cj + s.view(1, 1, 1, per_side)) * dx).expand(ny, nx, per_side, per_side).reshape(-1)
+    ym = ((ci + s.view(1, 1, per_side, 1)) * dy).expand(ny, nx, per_side, per_side).reshape(-1)
+    n = xm.numel()
+    xm = (xm + (torch.rand(n, generator=g, device=device, dtype=torch.float64) - 0.5) * dx / per_side).clamp_(0, 1)
+    ym = (ym + (torch.rand(n, generator=g, device=device, dtype=torch.float64) - 0.5) * dy / per_side).clamp_(0, 1)
+    one = torch.ones_like(xm)
+    if props == "layered":  # the _layered_eta / _layered_rho definitions, evaluated with torch
+        yp, xp = torch.remainder(ym, 1.0), torch.remainder(xm, 1.0)
+        eta = torch.where(yp < 0.15, 1e3 * one, torch.where(yp < 0.66, one, 30.0 * one))
+        rho = torch.cos(2 * math.pi * xp) * torch.sin(math.pi * yp)
+    elif props == "block":
+        inside = (xm >= 3 / 8) & (xm <= 5 / 8) & (ym >= 3 / 8) & (ym <= 5 / 8)
+        eta, rho = torch.where(inside, 1e3 * one, one), torch.where(inside, one, 0.0 * one)
+    elif props == "sinker":
+        inside = (xm - 0.5) ** 2 + (ym - 0.5) ** 2 <= 0.2 ** 2
+        eta, rho = torch.where(inside, 1e8 * one, one), torch.where(inside, 3.3 * one, 3.2 * one)
+    else:
+        raise ValueError(props)
+    return xm.contiguous(), ym.contiguous(), eta.contiguous(), rho.contiguous()

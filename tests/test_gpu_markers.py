@@ -209,3 +209,34 @@ def test_mic_block_sinks(S):
     x1 = gx[inside].mean().item()
     assert y1 > y0 + 1e-4, (y0, y1)
     assert abs(x1 - x0) < 0.05 * (y1 - y0), (x0, x1, y0, y1)  # jittered markers: nearly symmetric
+
+
+def test_fullsize_4096_window(S):
+    """The measured configuration (tools/mic_bench.py: 4096^2 cells x 16 markers = 268 M, one
+    launch of each kernel): marker -> grid bit-exact on the nodes of a 48^2-cell window, from the
+    oracle run on the window's markers alone (a node's value depends only on the markers of its
+    four surrounding cells, added in ascending index -- a subset in the same order gives the
+    same bits); RK4 bit-exact on the window's markers."""
+    from synth.fields import markers_torch
+    nx = ny = 4096
+    xm, ym, eta, rho = markers_torch(nx, ny, per_side=4, seed=2603, props="layered")
+    s = S(nx, ny, 1.0, 1.0)
+    eb, ep, rb, ne = s.markers_to_grid(xm, ym, eta, rho)
+    assert ne == 0
+    c0, W = 2000, 48                      # window cells [c0, c0 + W)^2 (+2-cell margin for the subset)
+    lo, hi = (c0 - 2) / nx, (c0 + W + 2) / nx
+    sel = ((xm >= lo) & (xm <= hi) & (ym >= lo) & (ym <= hi)).nonzero().squeeze(1)   # ascending index
+    sx, sy, se, sr = (H(t[sel]) for t in (xm, ym, eta, rho))
+    reb, rep, rrb, _ = O.markers_to_grid(nx, ny, 1.0, 1.0, sx, sy, se, sr)
+    win_b = (slice(c0, c0 + W + 1), slice(c0, c0 + W + 1))     # basic nodes with all 4 cells inside
+    win_p = (slice(c0, c0 + W), slice(c0, c0 + W))             # P nodes with all 4 P-cells inside
+    assert np.array_equal(H(eb)[win_b], reb[win_b]) and np.array_equal(H(rb)[win_b], rrb[win_b])
+    assert np.array_equal(H(ep)[win_p], rep[win_p])
+    rng = np.random.default_rng(4)
+    vx = rng.normal(size=(ny, nx + 1))
+    vy = rng.normal(size=(ny + 1, nx))
+    gvx, gvy = T(vx), T(vy)
+    dt = s.marker_timestep(gvx, gvy, 0.5, 1.0)
+    s.advect_markers(xm, ym, gvx, gvy, dt, "rk4", count_clamped=False)
+    ox, oy, _ = O.advect_markers(nx, ny, 1.0, 1.0, (0, 0, 0, 0), sx, sy, vx, vy, dt, "rk4")
+    assert np.array_equal(H(xm[sel]), ox) and np.array_equal(H(ym[sel]), oy)

@@ -21,25 +21,16 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2603_14040_b200 import Stokes  # noqa: E402
+from synth.fields import markers_torch  # noqa: E402
 
 
-def gen_markers(nx, ny, per_side, seed, order):
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    dx, dy = 1.0 / nx, 1.0 / ny
-    s = (torch.arange(per_side, device="cuda", dtype=torch.float64) + 0.5) / per_side
-    ci = torch.arange(ny, device="cuda", dtype=torch.float64).view(ny, 1, 1, 1)
-    cj = torch.arange(nx, device="cuda", dtype=torch.float64).view(1, nx, 1, 1)
-    xm = ((cj + s.view(1, 1, 1, per_side)) * dx).expand(ny, nx, per_side, per_side).reshape(-1)
-    ym = ((ci + s.view(1, 1, per_side, 1)) * dy).expand(ny, nx, per_side, per_side).reshape(-1)
-    n = xm.numel()
-    xm = (xm + (torch.rand(n, generator=g, device="cuda", dtype=torch.float64) - 0.5) * dx / per_side).clamp_(0, 1)
-    ym = (ym + (torch.rand(n, generator=g, device="cuda", dtype=torch.float64) - 0.5) * dy / per_side).clamp_(0, 1)
+def gen_markers(nx, ny, per_side, seed, order="cell"):
+    """synth.fields.markers_torch (the markers() recipe built on the GPU), optionally shuffled."""
+    xm, ym, eta, rho = markers_torch(nx, ny, per_side=per_side, seed=seed, props="sinker")
     if order == "shuffled":
-        p = torch.randperm(n, generator=g, device="cuda")
-        xm, ym = xm[p].contiguous(), ym[p].contiguous()
-    inside = (xm - 0.5) ** 2 + (ym - 0.5) ** 2 <= 0.04
-    eta = torch.where(inside, 1e8, 1.0).to(torch.float64)
-    rho = torch.where(inside, 3.3, 3.2).to(torch.float64)
+        g = torch.Generator(device="cuda").manual_seed(seed + 1)
+        p = torch.randperm(xm.numel(), generator=g, device="cuda")
+        xm, ym, eta, rho = (t[p].contiguous() for t in (xm, ym, eta, rho))
     return xm, ym, eta, rho
 
 

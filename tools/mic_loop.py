@@ -17,23 +17,17 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2603_14040_b200 import Stokes  # noqa: E402
+from synth.fields import markers_torch  # noqa: E402
 
 
-def gen_markers(nx, ny, per_side, seed):
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    dx, dy = 1.0 / nx, 1.0 / ny
-    s = (torch.arange(per_side, device="cuda", dtype=torch.float64) + 0.5) / per_side
-    ci = torch.arange(ny, device="cuda", dtype=torch.float64).view(ny, 1, 1, 1)
-    cj = torch.arange(nx, device="cuda", dtype=torch.float64).view(1, nx, 1, 1)
-    xm = ((cj + s.view(1, 1, 1, per_side)) * dx).expand(ny, nx, per_side, per_side).reshape(-1)
-    ym = ((ci + s.view(1, 1, per_side, 1)) * dy).expand(ny, nx, per_side, per_side).reshape(-1)
-    n = xm.numel()
-    xm = (xm + (torch.rand(n, generator=g, device="cuda", dtype=torch.float64) - 0.5) * dx / per_side).clamp_(0, 1)
-    ym = (ym + (torch.rand(n, generator=g, device="cuda", dtype=torch.float64) - 0.5) * dy / per_side).clamp_(0, 1)
-    # cfg 4 layering carried by the markers: eta 1e3 / 1 / 30, drho = cos(2 pi x) sin(pi y)
-    eta = torch.where(ym < 0.15, 1e3, torch.where(ym < 0.66, 1.0, 30.0)).to(torch.float64)
-    rho = torch.cos(2 * math.pi * xm) * torch.sin(math.pi * ym)
-    return xm.contiguous(), ym.contiguous(), eta.contiguous(), rho.contiguous()
+def gen_markers(nx, ny, per_side, seed, order="cell"):
+    """synth.fields.markers_torch (the markers() recipe built on the GPU), optionally shuffled."""
+    xm, ym, eta, rho = markers_torch(nx, ny, per_side=per_side, seed=seed, props="layered")
+    if order == "shuffled":
+        g = torch.Generator(device="cuda").manual_seed(seed + 1)
+        p = torch.randperm(xm.numel(), generator=g, device="cuda")
+        xm, ym, eta, rho = (t[p].contiguous() for t in (xm, ym, eta, rho))
+    return xm, ym, eta, rho
 
 
 def main():

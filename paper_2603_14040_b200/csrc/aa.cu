@@ -20,6 +20,7 @@ namespace {
 
 constexpr int AT = 256;  // threads per CTA (grid-stride over padded elements)
 
+
 __device__ double block_sum_at(double v, double *sh) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -44,50 +45,66 @@ __device__ __forceinline__ bool unknown(const GridL &g, int f, int i, int j) {
 __global__ void __launch_bounds__(AT) k_aa_push(GridL g, AAVec work, const double *ms_g, AAVec T, const double *ms_t,
                                                 AAVec Gk, AAVec Rk, AAWin win, double *__restrict__ partials) {
     __shared__ double sh[32];
+    __shared__ const double *rw[3][AA_MAXS];  // window pointers (no dynamic indexing of the parameters)
+    if (threadIdx.x < 3 * AA_MAXS) {
+        const int f = threadIdx.x / AA_MAXS, w = threadIdx.x % AA_MAXS;
+        rw[f][w] = win.r[w].f[f];
+    }
+    __syncthreads();
     double acc[AA_MAXS];
 #pragma unroll
     for (int w = 0; w < AA_MAXS; ++w) acc[w] = 0.0;
     const double mg = *ms_g, mt = *ms_t;
-    const size_t rows = (size_t)g.ncy + 2, n = rows * g.P;
-    const size_t stride = (size_t)gridDim.x * AT;
+    const int rows = g.ncy + 2, cols = g.ncx + 2, nw = win.n, self = win.self;
+    // rows over CTAs, columns over threads: coalesced, no per-element index division
+#pragma unroll
     for (int f = 0; f < 3; ++f) {
         const double *X = work.f[f], *TT = T.f[f];
         double *GG = Gk.f[f], *RR = Rk.f[f];
         const double sg = f == 2 ? mg : 0.0, st = f == 2 ? mt : 0.0;
-        for (size_t e = blockIdx.x * (size_t)AT + threadIdx.x; e < n; e += stride) {
-            const int i = (int)(e / g.P), j = (int)(e % g.P);
-            if (j > g.ncx + 1) continue;
-            const double gv = X[e] - sg;
-            const double r = gv - (TT[e] - st);
-            GG[e] = gv;
-            RR[e] = r;
-            if (unknown(g, f, i, j)) {
+        for (int i = blockIdx.x; i < rows; i += gridDim.x) {
+            for (int j = threadIdx.x; j < cols; j += AT) {
+                const size_t e = (size_t)i * g.P + j;
+                const double gv = X[e] - sg;
+                const double r = gv - (TT[e] - st);
+                GG[e] = gv;
+                RR[e] = r;
+                if (unknown(g, f, i, j)) {
 #pragma unroll
-                for (int w = 0; w < AA_MAXS; ++w)
-                    if (w < win.n) acc[w] += r * (w == win.self ? r : win.r[w].f[f][e]);
+                    for (int w = 0; w < AA_MAXS; ++w)
+                        if (w < nw) acc[w] += r * (w == self ? r : rw[f][w][e]);
+                }
             }
         }
     }
     const size_t b = blockIdx.x;
-    for (int w = 0; w < win.n; ++w) {
+#pragma unroll
+    for (int w = 0; w < AA_MAXS; ++w) {
+        if (w >= nw) break;
         const double v = block_sum_at(acc[w], sh);
         if (threadIdx.x == 0) partials[b * AA_MAXS + w] = v;
     }
 }
 
 // one thread: reduce the partials (fixed order) into Gram row `self`, solve, coefficients
-__global__ void k_aa_solve(const double *__restrict__ partials, int nblocks, AAWin win, double beta, double *H,
-                           double *cg, double *cr) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const int nn = win.n;
-    const int *order = win.slot;  // window oldest -> newest (the oracle's order)
-    // new row / column of the (slot-indexed) Gram matrix
+__global__ void __launch_bounds__(AT) k_aa_solve(const double *__restrict__ partials, int nblocks, AAWin win,
+                                                 double beta, double *H, double *cg, double *cr) {
+    __shared__ double sh[32];
+    // new row / column of the (slot-indexed) Gram matrix: the block partials of each entry
+    // summed by the CTA in a fixed order (strided per thread, then the fixed shuffle tree)
     for (int w = 0; w < win.n; ++w) {
         double s = 0.0;
-        for (int b = 0; b < nblocks; ++b) s += partials[(size_t)b * AA_MAXS + w];
-        H[win.slot[win.self] * AA_MAXS + win.slot[w]] = s;
-        H[win.slot[w] * AA_MAXS + win.slot[win.self]] = s;
+        for (int b = threadIdx.x; b < nblocks; b += AT) s += partials[(size_t)b * AA_MAXS + w];
+        s = block_sum_at(s, sh);
+        if (threadIdx.x == 0) {
+            H[win.slot[win.self] * AA_MAXS + win.slot[w]] = s;
+            H[win.slot[w] * AA_MAXS + win.slot[win.self]] = s;
+        }
     }
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    __threadfence_block();
+    const int nn = win.n;
+    const int *order = win.slot;  // window oldest -> newest (the oracle's order)
     for (int s = 0; s < AA_MAXS; ++s) cg[s] = cr[s] = 0.0;
     if (nn < 2) {  // x^1 = G(x^0)
         cg[win.slot[win.self]] = 1.0;
@@ -146,27 +163,42 @@ __global__ void __launch_bounds__(AT) k_aa_update(GridL g, AAHist hist, int ns, 
                                                   const double *__restrict__ cr, AAVec work, AAVec T,
                                                   double *__restrict__ partials) {
     __shared__ double sh[32];
-    __shared__ double c1[AA_MAXS], c2[AA_MAXS];
-    if (threadIdx.x < AA_MAXS) {
-        c1[threadIdx.x] = cg[threadIdx.x];
-        c2[threadIdx.x] = cr[threadIdx.x];
+    // the nonzero terms of x = sum c_k v_k as a compact list (coefficient, pointer per field):
+    // no dynamic indexing of the parameter structs, no zero-coefficient branches in the loop
+    __shared__ double cf[2 * AA_MAXS];
+    __shared__ const double *vp[3][2 * AA_MAXS];
+    __shared__ int nt;
+    if (threadIdx.x == 0) {
+        int k = 0;
+        for (int q = 0; q < ns; ++q) {  // the order of the previous loop: G_q then R_q
+            if (cg[q] != 0.0) {
+                cf[k] = cg[q];
+                for (int f = 0; f < 3; ++f) vp[f][k] = hist.G[q].f[f];
+                ++k;
+            }
+            if (cr[q] != 0.0) {
+                cf[k] = cr[q];
+                for (int f = 0; f < 3; ++f) vp[f][k] = hist.R[q].f[f];
+                ++k;
+            }
+        }
+        nt = k;
     }
     __syncthreads();
     double psum = 0.0;
-    const size_t n = ((size_t)g.ncy + 2) * g.P;
-    const size_t stride = (size_t)gridDim.x * AT;
+    const int rows = g.ncy + 2, cols = g.ncx + 2, nterm = nt;
+#pragma unroll
     for (int f = 0; f < 3; ++f) {
-        for (size_t e = blockIdx.x * (size_t)AT + threadIdx.x; e < n; e += stride) {
-            const int i = (int)(e / g.P), j = (int)(e % g.P);
-            if (j > g.ncx + 1) continue;
-            double x = 0.0;
-            for (int s = 0; s < ns; ++s) {
-                if (c1[s] != 0.0) x += c1[s] * hist.G[s].f[f][e];
-                if (c2[s] != 0.0) x += c2[s] * hist.R[s].f[f][e];
+        double *W = work.f[f], *TT = T.f[f];
+        for (int i = blockIdx.x; i < rows; i += gridDim.x) {
+            for (int j = threadIdx.x; j < cols; j += AT) {
+                const size_t e = (size_t)i * g.P + j;
+                double x = 0.0;
+                for (int k = 0; k < nterm; ++k) x += cf[k] * vp[f][k][e];
+                W[e] = x;
+                TT[e] = x;
+                if (f == 2 && unknown(g, 2, i, j)) psum += x;
             }
-            work.f[f][e] = x;
-            T.f[f][e] = x;
-            if (f == 2 && unknown(g, 2, i, j)) psum += x;
         }
     }
     psum = block_sum_at(psum, sh);
@@ -179,8 +211,7 @@ int aa_blocks(const GridL &g) {
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const size_t n = ((size_t)g.ncy + 2) * g.P;
-    size_t b = (n + AT - 1) / AT;
+    const size_t b = (size_t)g.ncy + 2;  // one CTA per padded row, capped at 8 per SM (grid-stride)
     const size_t cap = (size_t)(nsm > 0 ? nsm : 148) * 8;
     return (int)(b < cap ? b : cap);
 }
@@ -191,7 +222,7 @@ void launch_aa_push(const LaunchCtx &c, const GridL &g, const AAVec &work, const
 }
 void launch_aa_solve(const LaunchCtx &c, const double *partials, int nblocks, const AAWin &win, double beta,
                      double *H, double *cg, double *cr) {
-    k_aa_solve<<<1, 32, 0, c.stream>>>(partials, nblocks, win, beta, H, cg, cr);
+    k_aa_solve<<<1, AT, 0, c.stream>>>(partials, nblocks, win, beta, H, cg, cr);
     ++*c.counter;
 }
 void launch_aa_update(const LaunchCtx &c, const GridL &g, const AAHist &hist, int ns, const double *cg,

@@ -42,6 +42,9 @@ __device__ __forceinline__ bool unknown(const GridL &g, int f, int i, int j) {
     return i >= 1 && i <= g.ncy && j >= 1 && j <= g.ncx;
 }
 
+// NW: compile-time bound on the window (accumulators in registers: fewer for short windows,
+// so more CTAs fit per SM)
+template <int NW>
 __global__ void __launch_bounds__(AT) k_aa_push(GridL g, AAVec work, const double *ms_g, AAVec T, const double *ms_t,
                                                 AAVec Gk, AAVec Rk, AAWin win, double *__restrict__ partials) {
     __shared__ double sh[32];
@@ -51,9 +54,9 @@ __global__ void __launch_bounds__(AT) k_aa_push(GridL g, AAVec work, const doubl
         rw[f][w] = win.r[w].f[f];
     }
     __syncthreads();
-    double acc[AA_MAXS];
+    double acc[NW];
 #pragma unroll
-    for (int w = 0; w < AA_MAXS; ++w) acc[w] = 0.0;
+    for (int w = 0; w < NW; ++w) acc[w] = 0.0;
     const double mg = *ms_g, mt = *ms_t;
     const int rows = g.ncy + 2, cols = g.ncx + 2, nw = win.n, self = win.self;
     // rows over CTAs, columns over threads: coalesced, no per-element index division
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(AT) k_aa_push(GridL g, AAVec work, const doubl
                 RR[e] = r;
                 if (unknown(g, f, i, j)) {
 #pragma unroll
-                    for (int w = 0; w < AA_MAXS; ++w)
+                    for (int w = 0; w < NW; ++w)
                         if (w < nw) acc[w] += r * (w == self ? r : rw[f][w][e]);
                 }
             }
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(AT) k_aa_push(GridL g, AAVec work, const doubl
     }
     const size_t b = blockIdx.x;
 #pragma unroll
-    for (int w = 0; w < AA_MAXS; ++w) {
+    for (int w = 0; w < NW; ++w) {
         if (w >= nw) break;
         const double v = block_sum_at(acc[w], sh);
         if (threadIdx.x == 0) partials[b * AA_MAXS + w] = v;
@@ -217,7 +220,11 @@ int aa_blocks(const GridL &g) {
 }
 void launch_aa_push(const LaunchCtx &c, const GridL &g, const AAVec &work, const double *ms_g, const AAVec &T,
                     const double *ms_t, const AAVec &Gk, const AAVec &Rk, const AAWin &win, double *partials) {
-    k_aa_push<<<aa_blocks(g), AT, 0, c.stream>>>(g, work, ms_g, T, ms_t, Gk, Rk, win, partials);
+    const int nb = aa_blocks(g);
+    if (win.n <= 4) k_aa_push<4><<<nb, AT, 0, c.stream>>>(g, work, ms_g, T, ms_t, Gk, Rk, win, partials);
+    else if (win.n <= 8) k_aa_push<8><<<nb, AT, 0, c.stream>>>(g, work, ms_g, T, ms_t, Gk, Rk, win, partials);
+    else if (win.n <= 12) k_aa_push<12><<<nb, AT, 0, c.stream>>>(g, work, ms_g, T, ms_t, Gk, Rk, win, partials);
+    else k_aa_push<AA_MAXS><<<nb, AT, 0, c.stream>>>(g, work, ms_g, T, ms_t, Gk, Rk, win, partials);
     ++*c.counter;
 }
 void launch_aa_solve(const LaunchCtx &c, const double *partials, int nblocks, const AAWin &win, double beta,

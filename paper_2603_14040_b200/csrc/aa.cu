@@ -68,14 +68,20 @@ __global__ void __launch_bounds__(AT) k_aa_push(GridL g, AAVec work, const doubl
         for (int i = blockIdx.x; i < rows; i += gridDim.x) {
             for (int j = threadIdx.x; j < cols; j += AT) {
                 const size_t e = (size_t)i * g.P + j;
-                const double gv = X[e] - sg;
-                const double r = gv - (TT[e] - st);
+                // every load of the element before its stores: the window arrays may alias
+                // G_k / R_k as far as the compiler knows, so loads after the stores would wait
+                const double xv = X[e], tv = TT[e];
+                double rv[NW];
+#pragma unroll
+                for (int w = 0; w < NW; ++w) rv[w] = (w < nw && w != self) ? rw[f][w][e] : 0.0;
+                const double gv = xv - sg;
+                const double r = gv - (tv - st);
                 GG[e] = gv;
                 RR[e] = r;
                 if (unknown(g, f, i, j)) {
 #pragma unroll
                     for (int w = 0; w < NW; ++w)
-                        if (w < nw) acc[w] += r * (w == self ? r : rw[f][w][e]);
+                        if (w < nw) acc[w] += r * (w == self ? r : rv[w]);
                 }
             }
         }

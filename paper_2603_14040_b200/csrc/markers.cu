@@ -216,18 +216,40 @@ __global__ void k_mk_records(int nbins, const int *__restrict__ off, int *__rest
         }
     }
     __syncwarp();
-    int r0 = off[b0], r1 = off[min(b0 + 32, nbins)];
-    for (int k = r0 + lane; k < r1; k += 32) {
-        int m = sidx[k];
-        double xm = clampd(x[m], 0.0, G.Lx), ym = clampd(y[m], 0.0, G.Ly), tx, ty;
-        if (BASIC) {
-            ref_node(xm, G.dx, G.rdx, 0.0, 0, G.nx - 1, tx);
-            ref_node(ym, G.dy, G.rdy, 0.0, 0, G.ny - 1, ty);
-        } else {
-            ref_node(xm, G.dx, G.rdx, G.hx, -1, G.nx - 1, tx);
-            ref_node(ym, G.dy, G.rdy, G.hy, -1, G.ny - 1, ty);
+    // RU records per lane per step, every load before the stores (the output may alias the
+    // inputs as far as the compiler knows: loads after a store would wait for it)
+    constexpr int RU = 4;
+    const int r0 = off[b0], r1 = off[min(b0 + 32, nbins)];
+    for (int k0 = r0 + lane; k0 < r1; k0 += 32 * RU) {
+        int m[RU];
+        double xv[RU], yv[RU], ev[RU], rv[RU];
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+            const int k = k0 + 32 * u;
+            m[u] = k < r1 ? sidx[k] : -1;
         }
-        rec[k] = make_double4(tx, ty, eta[m], BASIC ? rho[m] : 0.0);
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+            if (m[u] < 0) continue;
+            xv[u] = x[m[u]];
+            yv[u] = y[m[u]];
+            ev[u] = eta[m[u]];
+            rv[u] = BASIC ? rho[m[u]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+            if (m[u] < 0) continue;
+            const double xm = clampd(xv[u], 0.0, G.Lx), ym = clampd(yv[u], 0.0, G.Ly);
+            double tx, ty;
+            if (BASIC) {
+                ref_node(xm, G.dx, G.rdx, 0.0, 0, G.nx - 1, tx);
+                ref_node(ym, G.dy, G.rdy, 0.0, 0, G.ny - 1, ty);
+            } else {
+                ref_node(xm, G.dx, G.rdx, G.hx, -1, G.nx - 1, tx);
+                ref_node(ym, G.dy, G.rdy, G.hy, -1, G.ny - 1, ty);
+            }
+            rec[k0 + 32 * u] = make_double4(tx, ty, ev[u], rv[u]);
+        }
     }
 }
 

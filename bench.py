@@ -324,6 +324,10 @@ def run_ours(args, world, rank, local):
         r = s.solve(rtol, vx=hz["vx"], vy=hz["vy"], p=hz["p"], out=hout)
         torch.cuda.synchronize()
         e2.append(time.perf_counter() - t0)
+        # the same computation as the device-timed solves: converged, same iteration count
+        assert r["status"] == 0, f"e2e solve status {r['status']}"
+        assert r["iters"] == iters[-1], f"e2e solve took {r['iters']} iterations, device solve {iters[-1]}"
+        assert not r["vx"].is_cuda
         e2_iters += r["iters"]
     e2_t = allreduce_max(sum(e2), world, dev)
     e2e_value = e2_iters * vpi * per_vc / e2_t
@@ -402,7 +406,7 @@ def run_ours(args, world, rank, local):
                      # would move these bytes twice
                      "sweep_equivalent_GBs": 2 * achieved if dom == "jacobi2" else achieved},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
-                "seconds_per_step": e2_t / len(e2)},
+                "seconds_per_step": e2_t / len(e2), "iters_per_solve": e2_iters / len(e2)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

@@ -855,6 +855,7 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
     if ((st = dsync(*D))) { dist_destroy(D); return st; }
     stokes_s *h = (stokes_s *)calloc(1, sizeof(stokes_s));
     h->dist = D;
+    cudaGetDevice(&h->device);
     h->nx = nx;
     h->ny = ny;
     h->stream = D->stream;

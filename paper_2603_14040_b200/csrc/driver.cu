@@ -13,6 +13,14 @@
 
 #include "handle.h"
 
+bool first_on_device(unsigned long long *mask) {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long bit = 1ull << (d & 63);
+    if (__atomic_load_n(mask, __ATOMIC_ACQUIRE) & bit) return false;
+    return !(__atomic_fetch_or(mask, bit, __ATOMIC_ACQ_REL) & bit);
+}
+
 namespace sk {
 
 thread_local std::string g_last_error;
@@ -110,6 +118,10 @@ size_t carve(stokes_s *h, Carver &cv) {
         h->etab_user = h->etap_user = nullptr;
     }
     h->npart = (size_t)energy_blocks(g0) * 12 + 3 * 4096 + 64;
+    if (h->o.accel == STOKES_ACCEL_ANDERSON) {  // k_aa_push: AA_MAXS partials per block
+        const size_t na = (size_t)aa_blocks(g0) * AA_MAXS + 64;
+        if (na > h->npart) h->npart = na;
+    }
     h->partials = cv.take(h->npart);
     h->scal = cv.take(S_NSCAL);
     const GridL &gc = h->lev[h->nlev - 1].g;
@@ -806,6 +818,7 @@ int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const s
     if (!h) return STOKES_ENOMEM;
     int st = prepare(h, nx, ny, Lx, Ly, bc, opts);
     if (st) { free(h); return st; }
+    cudaGetDevice(&h->device);
     h->stream = (cudaStream_t)cuda_stream;
     if (!h->stream) {  // the legacy default stream cannot be graph-captured: use our own
         cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
@@ -843,6 +856,7 @@ int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const s
 }
 
 int stokes_destroy(stokes_t h) {
+    DEVICE_GUARD(h);
     if (!h) return STOKES_EINVAL;
     if (h->dist) {
         dist_destroy(h->dist);
@@ -859,6 +873,7 @@ int stokes_destroy(stokes_t h) {
 }
 
 int stokes_num_levels(stokes_t h, int *nlev) {
+    DEVICE_GUARD(h);
     if (!h || !nlev) return STOKES_EINVAL;
     if (h->dist) {
         *nlev = dist_num_levels(h->dist);
@@ -868,6 +883,7 @@ int stokes_num_levels(stokes_t h, int *nlev) {
     return STOKES_OK;
 }
 int stokes_level_shape(stokes_t h, int level, int *nx, int *ny, int *nu) {
+    DEVICE_GUARD(h);
     if (!valid_level(h, level) || !nx || !ny || !nu) return STOKES_EINVAL;
     *nx = h->lev[level].g.ncx;
     *ny = h->lev[level].g.ncy;
@@ -876,6 +892,7 @@ int stokes_level_shape(stokes_t h, int level, int *nx, int *ny, int *nu) {
 }
 
 int stokes_set_viscosity(stokes_t h, const double *eta_b, const double *eta_p) {
+    DEVICE_GUARD(h);
     if (!h || !eta_b || !eta_p) return STOKES_EINVAL;
     if (h->dist) return dist_set_viscosity(h->dist, eta_b, eta_p);
     const LaunchCtx c = ctx(h);
@@ -901,6 +918,7 @@ int stokes_set_viscosity(stokes_t h, const double *eta_b, const double *eta_p) {
 }
 
 int stokes_lithostatic(stokes_t h, double *p) {
+    DEVICE_GUARD(h);
     if (!h || !p || h->dist) return STOKES_EINVAL;
     if (!h->have_rho) return STOKES_ESTATE;
     launch_lithostatic(ctx(h), h->lev[0].g, h->rho, h->gy, p);
@@ -939,6 +957,7 @@ int build_hierarchy(stokes_s *h) {
 extern "C" {
 
 int stokes_set_density(stokes_t h, const double *rho_b) {
+    DEVICE_GUARD(h);
     if (!h || !rho_b) return STOKES_EINVAL;
     if (h->dist) return dist_set_density(h->dist, rho_b);
     launch_in_b(ctx(h), h->lev[0].g, rho_b, h->rho);
@@ -948,6 +967,7 @@ int stokes_set_density(stokes_t h, const double *rho_b) {
 }
 
 int stokes_set_gravity(stokes_t h, double gx, double gy) {
+    DEVICE_GUARD(h);
     if (!h || !(gx == gx) || !(gy == gy)) return STOKES_EINVAL;
     if (h->dist) return dist_set_gravity(h->dist, gx, gy);
     h->gx = gx;
@@ -959,6 +979,7 @@ int stokes_set_gravity(stokes_t h, double gx, double gy) {
 
 int stokes_apply_operator(stokes_t h, const double *vx, const double *vy, const double *p, double *ax, double *ay,
                           double *ap) {
+    DEVICE_GUARD(h);
     if (!h || h->dist || !vx || !vy || !p || !ax || !ay || !ap) return STOKES_EINVAL;
     if (!h->have_eta) return STOKES_ESTATE;
     Level &F = h->lev[0];
@@ -971,6 +992,7 @@ int stokes_apply_operator(stokes_t h, const double *vx, const double *vy, const 
 
 int stokes_residual(stokes_t h, const double *vx, const double *vy, const double *p, double *rx, double *ry,
                     double *rp, double *rel_energy) {
+    DEVICE_GUARD(h);
     if (!h || !vx || !vy || !p) return STOKES_EINVAL;
     if (h->dist) {  // decomposed handles: E only
         if (rx || ry || rp || !rel_energy) return STOKES_EINVAL;
@@ -994,6 +1016,7 @@ int stokes_residual(stokes_t h, const double *vx, const double *vy, const double
 }
 
 int stokes_vcycle(stokes_t h, const double *bx, const double *by, double *vx, double *vy) {
+    DEVICE_GUARD(h);
     if (!h || h->dist || !bx || !by || !vx || !vy) return STOKES_EINVAL;
     if (!h->have_eta) return STOKES_ESTATE;
     Level &F = h->lev[0];
@@ -1009,6 +1032,7 @@ int stokes_vcycle(stokes_t h, const double *bx, const double *by, double *vx, do
 }
 
 int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy) {
+    DEVICE_GUARD(h);
     if (!h || !vx || !vy || !p || !iters || !rel_energy || !(rtol >= 0)) return STOKES_EINVAL;
     if (h->dist) return dist_solve(h->dist, rtol, vx, vy, p, iters, rel_energy);
     if (!h->have_eta || !h->have_rho) return STOKES_ESTATE;
@@ -1169,6 +1193,7 @@ extern "C" {
 
 // ---------------------------------------------------------------- per-step entry points
 int stokes_smooth(stokes_t h, int level, const double *bx, const double *by, double *vx, double *vy, int nsweeps) {
+    DEVICE_GUARD(h);
     if (!valid_level(h, level) || !bx || !by || !vx || !vy || nsweeps < 0) return STOKES_EINVAL;
     if (!h->have_eta) return STOKES_ESTATE;
     Level &L = h->lev[level];
@@ -1186,6 +1211,7 @@ int stokes_smooth(stokes_t h, int level, const double *bx, const double *by, dou
 
 int stokes_level_residual(stokes_t h, int level, const double *bx, const double *by, const double *vx,
                           const double *vy, double *rx, double *ry) {
+    DEVICE_GUARD(h);
     if (!valid_level(h, level) || !bx || !by || !vx || !vy || !rx || !ry) return STOKES_EINVAL;
     if (!h->have_eta) return STOKES_ESTATE;
     Level &L = h->lev[level];
@@ -1200,6 +1226,7 @@ int stokes_level_residual(stokes_t h, int level, const double *bx, const double 
 }
 
 int stokes_restrict(stokes_t h, int level, int kind, const double *fine, double *coarse) {
+    DEVICE_GUARD(h);
     if (!valid_level(h, level) || level + 1 >= h->nlev || kind < 0 || kind > 3 || !fine || !coarse) return STOKES_EINVAL;
     Level &L = h->lev[level], &C = h->lev[level + 1];
     const LaunchCtx c = ctx(h);
@@ -1229,6 +1256,7 @@ int stokes_restrict(stokes_t h, int level, int kind, const double *fine, double 
 }
 
 int stokes_prolong(stokes_t h, int level, const double *ex, const double *ey, double *vx, double *vy) {
+    DEVICE_GUARD(h);
     if (!valid_level(h, level) || level + 1 >= h->nlev || !ex || !ey || !vx || !vy) return STOKES_EINVAL;
     Level &L = h->lev[level], &C = h->lev[level + 1];
     const LaunchCtx c = ctx(h);
@@ -1241,6 +1269,7 @@ int stokes_prolong(stokes_t h, int level, const double *ex, const double *ey, do
 }
 
 int stokes_get_viscosity(stokes_t h, int level, double *eta_b, double *eta_p) {
+    DEVICE_GUARD(h);
     if (!valid_level(h, level) || !eta_b || !eta_p) return STOKES_EINVAL;
     if (!h->have_eta) return STOKES_ESTATE;
     Level &L = h->lev[level];
@@ -1251,6 +1280,7 @@ int stokes_get_viscosity(stokes_t h, int level, double *eta_b, double *eta_p) {
 }
 
 int stokes_coarse_solve(stokes_t h, const double *bx, const double *by, double *vx, double *vy) {
+    DEVICE_GUARD(h);
     if (!h || h->dist || !bx || !by || !vx || !vy) return STOKES_EINVAL;
     if (!h->have_eta) return STOKES_ESTATE;
     if (h->nc == 0) return STOKES_EINVAL;
@@ -1265,6 +1295,7 @@ int stokes_coarse_solve(stokes_t h, const double *bx, const double *by, double *
 }
 
 int stokes_launch_count(stokes_t h, long long *count, int reset) {
+    DEVICE_GUARD(h);
     if (!h || !count) return STOKES_EINVAL;
     if (h->dist) {
         *count = dist_launches(h->dist, reset);
@@ -1276,6 +1307,7 @@ int stokes_launch_count(stokes_t h, long long *count, int reset) {
 }
 
 int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double *bytes) {
+    DEVICE_GUARD(h);
     if (!h || h->dist || !avg_ms || !bytes || reps < 1) return STOKES_EINVAL;
     if (!h->have_eta || !h->have_rho) return STOKES_ESTATE;
     Level &F = h->lev[0];

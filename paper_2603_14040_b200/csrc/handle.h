@@ -29,6 +29,7 @@ struct Level {
 }  // namespace sk
 
 struct stokes_s {
+    int device;  // the CUDA device the handle was created on (every ABI call runs there)
     int nx, ny;
     double Lx, Ly;
     int bc[4];
@@ -73,6 +74,17 @@ struct stokes_s {
 
 namespace sk {
 using ::stokes_s;
+// Every ABI entry point runs on the handle's device and restores the caller's current device.
+struct DevGuard {
+    int prev = -1, want;
+    explicit DevGuard(int d) : want(d) {
+        if (d >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != d) cudaSetDevice(d);
+    }
+    ~DevGuard() {
+        if (want >= 0 && prev >= 0 && prev != want) cudaSetDevice(prev);
+    }
+};
+
 int fail_cuda(cudaError_t e, const char *what);
 size_t round_up(size_t v, size_t a);
 GridL make_grid(int ncx, int ncy, double Lx, double Ly, const int bc[4]);
@@ -118,6 +130,7 @@ void drop_graphs(stokes_s *h);
 void force_energy(stokes_s *h);
 }  // namespace sk
 
+#define DEVICE_GUARD(h) sk::DevGuard dev_guard_((h) ? (h)->device : -1)
 #define CK(call)                                                  \
     do {                                                          \
         cudaError_t e_ = (call);                                  \

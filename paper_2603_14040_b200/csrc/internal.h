@@ -31,6 +31,10 @@ struct GridL {          // one multigrid level, passed by value to kernels
     int par;   // (global row + column offset of the tile) & 1: red-black colour parity (R11)
 };
 
+// first call on the current device (per-device one-time setup, e.g. cudaFuncSetAttribute of
+// the > 48 KB dynamic shared memory kernels: the attribute is per device); thread-safe
+bool first_on_device(unsigned long long *mask);
+
 __host__ __device__ inline size_t at(const GridL &g, int i, int j) { return (size_t)i * (size_t)g.P + (size_t)j; }
 
 // launch bookkeeping shared by all launchers

@@ -544,6 +544,7 @@ extern "C" {
 
 int stokes_markers_to_grid(stokes_t h, long long n, const double *xm, const double *ym, const double *eta_m,
                            const double *rho_m, double *eta_b, double *eta_p, double *rho_b, long long *n_empty) {
+    DEVICE_GUARD(h);
     if (check_single(h)) return STOKES_EINVAL;
     if (n < 0 || n >= INT_MAX) return STOKES_EINVAL;
     if (n > 0 && (!xm || !ym || !eta_m || (!rho_m && rho_b))) return STOKES_EINVAL;
@@ -611,6 +612,7 @@ int stokes_markers_to_grid(stokes_t h, long long n, const double *xm, const doub
 
 int stokes_grid_to_markers(stokes_t h, long long n, const double *xm, const double *ym, const double *vx,
                            const double *vy, double *vxm, double *vym) {
+    DEVICE_GUARD(h);
     if (check_single(h)) return STOKES_EINVAL;
     if (n < 0 || (n > 0 && (!xm || !ym || !vx || !vy || !vxm || !vym))) return STOKES_EINVAL;
     if (n == 0) return STOKES_OK;
@@ -623,6 +625,7 @@ int stokes_grid_to_markers(stokes_t h, long long n, const double *xm, const doub
 
 int stokes_advect_markers(stokes_t h, long long n, double *xm, double *ym, const double *vx, const double *vy,
                           double dt, int scheme, long long *n_clamped) {
+    DEVICE_GUARD(h);
     if (check_single(h)) return STOKES_EINVAL;
     if (n < 0 || (n > 0 && (!xm || !ym || !vx || !vy)) || scheme < 0 || scheme > 4 || !isfinite(dt))
         return STOKES_EINVAL;
@@ -655,6 +658,7 @@ int stokes_advect_markers(stokes_t h, long long n, double *xm, double *ym, const
 }
 
 int stokes_marker_timestep(stokes_t h, const double *vx, const double *vy, double cfl, double max_dt, double *dt) {
+    DEVICE_GUARD(h);
     if (check_single(h)) return STOKES_EINVAL;
     if (!vx || !vy || !dt || !(cfl > 0) || !(max_dt > 0)) return STOKES_EINVAL;
     int st = mk_reserve(h, 256);

@@ -227,11 +227,10 @@ void launch_ras_outer(const LaunchCtx &c, const GridL &g, const RasArgs &a, cons
     const int T = a.T;
     const dim3 grid((g.ncx + T - 1) / T + 1, (g.ncy + T - 1) / T + 1);  // any shift in [0, T)
     const int smem = 8 * RN * (int)sizeof(double);
-    static bool done = false;
-    if (!done) {
+    static unsigned long long done = 0;
+    if (first_on_device(&done)) {
         cudaFuncSetAttribute(k_ras<RHS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaFuncSetAttribute(k_ras<RHS_ARRAYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        done = true;
     }
     if (fine) k_ras<RHS_FINE><<<grid, RT, smem, c.stream>>>(g, a, iter, c_draw);
     else k_ras<RHS_ARRAYS><<<grid, RT, smem, c.stream>>>(g, a, iter, c_draw);

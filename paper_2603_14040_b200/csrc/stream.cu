@@ -492,11 +492,10 @@ __global__ void __launch_bounds__(TW, MINB) k_stream_bar(GridL g, Op op, int H, 
 int g_slots = 0;  // resident CTAs of k_stream on the device (SMs x MINB)
 template <class Op>
 void prepare_kernel() {
-    static bool done = false;
-    if (!done) {
+    static unsigned long long done = 0;
+    if (first_on_device(&done)) {
         cudaFuncSetAttribute(k_stream<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
         cudaFuncSetAttribute(k_stream_bar<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-        done = true;
     }
 }
 int slots() {
@@ -1060,19 +1059,17 @@ void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, cons
         fill_src(a.src, vxi, vyi, etap, etab, rhs.p, rhs.rho);
         a.gx = rhs.gx;
         a.gy = rhs.gy;
-        static bool done = false;
-        if (!done) {
+        static unsigned long long done = 0;
+        if (first_on_device(&done)) {
             cudaFuncSetAttribute(k_jacobi2<RHS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJ);
-            done = true;
         }
         k_jacobi2<RHS_FINE><<<grid, JT, SMEMJ, c.stream>>>(g, a, H);
     } else {
         fill_src(a.src, vxi, vyi, etap, etab, rhs.bx, rhs.by);
         a.gx = a.gy = 0.0;
-        static bool done = false;
-        if (!done) {
+        static unsigned long long done = 0;
+        if (first_on_device(&done)) {
             cudaFuncSetAttribute(k_jacobi2<RHS_ARRAYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJ);
-            done = true;
         }
         k_jacobi2<RHS_ARRAYS><<<grid, JT, SMEMJ, c.stream>>>(g, a, H);
     }
@@ -1119,19 +1116,17 @@ void launch_residual_restrict(const LaunchCtx &c, const GridL &g, const GridL &g
         fill_src(a.src, vx, vy, etap, etab, rhs.p, rhs.rho);
         a.gx = rhs.gx;
         a.gy = rhs.gy;
-        static bool done = false;
-        if (!done) {
+        static unsigned long long done = 0;
+        if (first_on_device(&done)) {
             cudaFuncSetAttribute(k_resrestrict<RHS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMRR);
-            done = true;
         }
         k_resrestrict<RHS_FINE><<<grid, TW, SMEMRR, c.stream>>>(g, gc, a, HC);
     } else {
         fill_src(a.src, vx, vy, etap, etab, rhs.bx, rhs.by);
         a.gx = a.gy = 0.0;
-        static bool done = false;
-        if (!done) {
+        static unsigned long long done = 0;
+        if (first_on_device(&done)) {
             cudaFuncSetAttribute(k_resrestrict<RHS_ARRAYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMRR);
-            done = true;
         }
         k_resrestrict<RHS_ARRAYS><<<grid, TW, SMEMRR, c.stream>>>(g, gc, a, HC);
     }
@@ -1141,10 +1136,9 @@ void launch_residual_restrict(const LaunchCtx &c, const GridL &g, const GridL &g
 template <int COMP, int MODE>
 void rbgs_pass(const LaunchCtx &c, const GridL &g, const J2Args &a) {
     constexpr int SM = NSR * NF * RW * 8 + NSR * 8;
-    static bool done = false;
-    if (!done) {
+    static unsigned long long done = 0;
+    if (first_on_device(&done)) {
         cudaFuncSetAttribute(k_rbgs_pass<COMP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
-        done = true;
     }
     int H = 0;
     const dim3 grid = j2_grid(g, &H);

@@ -192,7 +192,9 @@ class Stokes:
         if t.dtype != torch.float64:
             raise TypeError("arrays must be torch.float64")
         if t.device != self.device:
-            with torch.cuda.stream(self.stream):
+            # host (pinned) input: copied on torch's current stream, so every later use on that
+            # stream is ordered after it; _sync_inputs() orders the handle's stream after it too
+            with torch.cuda.device(self.device):
                 t = t.to(self.device, non_blocking=True)
         return t.contiguous()
 
@@ -276,11 +278,17 @@ class Stokes:
         guess tensors are on the CPU (e.g. pinned), they are copied in and the solution is
         copied back to CPU tensors (`out` may supply pinned output buffers)."""
         sh = shapes(self.nx, self.ny)
-        host = vx is not None and not vx.is_cuda
+        given = [t for t in (vx, vy, p) if t is not None]
+        host = bool(given) and not (torch.is_tensor(given[0]) and given[0].is_cuda)
         z = lambda k: torch.zeros(sh[k], dtype=torch.float64, device=self.device)
-        dvx = z("vx") if vx is None else self._dev(vx, sh["vx"]).clone()
-        dvy = z("vy") if vy is None else self._dev(vy, sh["vy"]).clone()
-        dp = z("p") if p is None else self._dev(p, sh["p"]).clone()
+
+        def guess(t, k):  # the solve overwrites its initial guess: never the caller's tensor
+            if t is None:
+                return z(k)
+            d = self._dev(t, sh[k])
+            return d.clone() if (torch.is_tensor(t) and d.data_ptr() == t.data_ptr()) else d
+        with torch.cuda.device(self.device):
+            dvx, dvy, dp = guess(vx, "vx"), guess(vy, "vy"), guess(p, "p")
         it, e = ctypes.c_int(), ctypes.c_double()
         self._sync_inputs()
         st = lib().stokes_solve(self._h, float(rtol), *map(self._p, (dvx, dvy, dp)), ctypes.byref(it),

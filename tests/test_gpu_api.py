@@ -1,0 +1,84 @@
+"""GPU tests of the public API paths around the kernels: solves from HOST (pinned) tensors
+must be the device-resident solve bit for bit (the e2e path of bench.py), and grid shapes
+that size the reduction scratch differently (tall, narrow grids with Anderson) stay in
+bounds and on the oracle."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.oracle import Oracle  # noqa: E402
+from synth.fields import workload  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def S():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2603_14040_b200 import Stokes
+    return Stokes
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if torch.is_tensor(a) else a
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def make(S, w, nx, ny, **opts):
+    s = S(nx, ny, w["Lx"], w["Ly"], w["bc"], **opts)
+    s.set_viscosity(torch.from_numpy(w["eta_b"]).cuda(), torch.from_numpy(w["eta_p"]).cuda())
+    s.set_density(torch.from_numpy(w["rho_b"]).cuda())
+    s.set_gravity(w["gx"], w["gy"])
+    return s
+
+
+@pytest.mark.parametrize("name,n,opts", [
+    ("layered", 512, dict(omega_v=0.6, alpha_p=1.0)),
+    ("solcx", 256, dict(omega_v=0.6, alpha_p=1.0, accel=1, gcr_restart=30)),
+    ("block", 256, dict(omega_v=0.6, alpha_p=1.0, accel=2, aa_depth=10, aa_beta=1.0)),
+])
+def test_host_inputs_equal_device_solve(S, name, n, opts):
+    """bench.py's e2e leg: viscosity, density and the initial guess from pinned host memory,
+    the solution back into pinned host buffers.  Same iteration count, bit-identical fields
+    (deterministic reductions) as the device-resident solve of the same handle."""
+    w = workload(name, n, n)
+    s = make(S, w, n, n, **opts)
+    ref = s.solve(1e-8)
+    pin = {k: torch.from_numpy(w[k]).pin_memory() for k in ("eta_b", "eta_p", "rho_b")}
+    sh = {"vx": (n, n + 1), "vy": (n + 1, n), "p": (n, n)}
+    hz = {k: torch.zeros(v, dtype=torch.float64).pin_memory() for k, v in sh.items()}
+    out = {k: torch.empty(v, dtype=torch.float64).pin_memory() for k, v in sh.items()}
+    for _ in range(3):  # repeated: a stream race would show up as a changed count
+        s.set_viscosity(pin["eta_b"], pin["eta_p"])
+        s.set_density(pin["rho_b"])
+        r = s.solve(1e-8, vx=hz["vx"], vy=hz["vy"], p=hz["p"], out=out)
+        assert r["status"] == 0 and r["iters"] == ref["iters"], (r["iters"], ref["iters"])
+        for k in ("vx", "vy", "p"):
+            assert not r[k].is_cuda
+            assert torch.equal(r[k], ref[k].cpu()), k
+    # only p given on the host: outputs come back on the host too
+    r = s.solve(1e-8, p=hz["p"])
+    assert not r["vx"].is_cuda and torch.equal(r["vx"], ref["vx"].cpu())
+    # the caller's device initial guess is never overwritten
+    g = torch.zeros(sh["vx"], dtype=torch.float64, device="cuda")
+    s.solve(1e-8, vx=g)
+    assert float(g.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("nx,ny", [(32, 1024), (64, 1024), (96, 1200)])
+def test_anderson_tall_grid(S, nx, ny):
+    """Narrow, tall grids: the Anderson Gram partials (one CTA per row) outnumber the energy
+    partials the scratch was first sized for.  First iterates on the oracle."""
+    w = workload("layered", nx, ny)
+    opts = dict(omega_v=0.6, alpha_p=1.0, accel=2, aa_depth=10, aa_beta=1.0, coarse_min=2, max_iter=8)
+    s = make(S, w, nx, ny, **opts)
+    o = Oracle(nx, ny, w["Lx"], w["Ly"], w["bc"], **opts)
+    o.set_viscosity(w["eta_b"], w["eta_p"])
+    o.set_density(w["rho_b"])
+    o.set_gravity(w["gx"], w["gy"])
+    a, b = o.solve(0.0), s.solve(0.0)
+    assert a["iters"] == b["iters"] == 8
+    assert abs(a["E"] - b["E"]) <= 1e-8 * a["E"]
+    for k in ("vx", "vy", "p"):
+        assert rel(b[k], a[k]) <= 1e-9, k

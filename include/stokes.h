@@ -99,6 +99,8 @@ typedef struct {
     int ras_tile;         /* RAS tile edge T in cells, 2..32 (32)                  */
     int ras_inner;        /* RAS inner sweeps T_inner (4)                          */
     uint64_t ras_seed;    /* seed of the counter-based tile-shift generator (reading R27)         */
+    int gcr_true_restart; /* GCR restart (reading R13): 1 (default) restarts
+                             from the true residual b - A x; 0 keeps the recursive r (Alg. 4)   */
 } stokes_opts;
 
 /* Fill *o with the defaults.  Returns STOKES_EINVAL if o is NULL. */
@@ -174,7 +176,9 @@ int stokes_residual(stokes_t h, const double *vx, const double *vy, const double
 int stokes_vcycle(stokes_t h, const double *bx, const double *by, double *vx, double *vy);
 
 /* Solve to E <= rtol (a12).  vx, vy, p: in = initial guess, out = solution (p zero-mean).
- * *iters (HOST) = number of V-cycle applications; *rel_energy (HOST) = final E.
+ * *iters (HOST) = number of V-cycle applications; *rel_energy (HOST) = final E.  With GCR the
+ * stopping test runs on the recursive residual and, once that passes, on the true residual
+ * (restarting from it if it does not pass); the E returned is the true one.
  * Returns OK, NOT_CONVERGED, EDIVERGED (last iterate kept) or an error. */
 int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy);
 

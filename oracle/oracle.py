@@ -49,6 +49,7 @@ class Opts(ctypes.Structure):
         ("ras_tile", ctypes.c_int),
         ("ras_inner", ctypes.c_int),
         ("ras_seed", ctypes.c_uint64),
+        ("gcr_true_restart", ctypes.c_int),
     ]
 
 
@@ -94,6 +95,8 @@ def lib():
         L.oracle_grid_to_markers.argtypes = [i, i, d, d, I, LL, D, D, D, D, D, D]
         L.oracle_advect_markers.argtypes = [i, i, d, d, I, LL, D, D, D, D, d, i, PL]
         L.oracle_marker_timestep.argtypes = [i, i, d, d, D, D, d, d, D]
+        L.oracle_gcr_dense.argtypes = [i, D, D, D, D, i, i, i, d, I, D, D, i, D]
+        L.oracle_aa_alpha.argtypes = [i, D, D]
     return _lib
 
 
@@ -272,6 +275,36 @@ class Oracle:
         if hist_len:
             out["hist"] = hist[: min(it.value, hist_len)]
         return out
+
+
+# ---------------------------------------------------------------- Krylov / Anderson cores on dense data
+def gcr_dense(A, Minv, b, x0, m, max_iter, rtol=0.0, true_restart=1, hist_len=0):
+    """The oracle's GCR(m) code (gcr_core, Alg. 4) on a dense system A x = b with explicit
+    preconditioner Minv.  Returns dict(x, iters, E, status, W[, hist]); W = the normalised
+    w_i of the last cycle (m x n)."""
+    A, Minv, b = (np.ascontiguousarray(a, np.float64) for a in (A, Minv, b))
+    n = b.size
+    x = np.array(x0, np.float64, order="C")
+    W = np.zeros((m, n))
+    it, e = ctypes.c_int(), ctypes.c_double()
+    hist = np.full(max(hist_len, 1), np.nan)
+    st = lib().oracle_gcr_dense(n, _d(A), _d(Minv), _d(b), _d(x), m, max_iter, true_restart, rtol,
+                                ctypes.byref(it), ctypes.byref(e), _d(hist), hist_len, _d(W))
+    if st < 0 and st != EDIVERGED:
+        _check(st, "gcr_dense")
+    out = {"x": x, "iters": it.value, "E": e.value, "status": st, "W": W}
+    if hist_len:
+        out["hist"] = hist[: min(it.value, hist_len)]
+    return out
+
+
+def aa_alpha(H):
+    """The oracle's Alg. 5 argmin (solve_anderson's aa_alpha) for the Gram matrix H = R^T R."""
+    H = np.ascontiguousarray(H, np.float64)
+    n = H.shape[0]
+    a = np.zeros(n)
+    _check(lib().oracle_aa_alpha(n, _d(H), _d(a)), "aa_alpha")
+    return a
 
 
 # ---------------------------------------------------------------- marker-in-cell (NEXT-4)

@@ -61,6 +61,7 @@ typedef struct {
     int ras_tile;        /* RAS tile edge T_I = T_J in cells (32) */
     int ras_inner;       /* RAS inner iterations T_inner (4) */
     uint64_t ras_seed;   /* seed of the counter-based tile-shift generator (reading R27) */
+    int gcr_true_restart; /* 1: true residual at every GCR restart (R13), 0: recursive r (Alg. 4) */
 } oracle_opts;
 
 typedef struct {
@@ -659,6 +660,7 @@ int oracle_opts_default(oracle_opts *o) {
     o->vcycles_per_iter = 1;
     o->accel = 0;
     o->gcr_restart = 10;
+    o->gcr_true_restart = 1;
     o->max_iter = 10000;
     o->pressure_sign = 1;
     o->theta_step = 0.0;
@@ -1018,11 +1020,73 @@ static int solve_uzawa(oracle_t *S, double rtol, double Sf, double E0, int *iter
 }
 
 /* Flexible GCR(m) with MGS, Alg. 4, readings R13/R14.
- * Vectors are x = (vx, vy, p) on the unknowns; <.,.> Euclidean over unknowns (vx, vy, p).
- * At every restart the recursive residual is replaced by the true b - A x (reading R13:
- * Alg. 4 keeps the recursive r; over ~100 steps its drift leaves the iterate ~1e-9 away
- * from the fixed point while E(recursive r) keeps falling). */
+ * The iteration is written once (gcr_core) over an abstract vector space: the Stokes solve
+ * plugs in x = (vx, vy, p) on the unknowns with <.,.> Euclidean over unknowns (vx, vy, p)
+ * and M^-1 = the Uzawa-splitting preconditioner; oracle_gcr_dense plugs in a dense n x n
+ * system so that the same code is pinned against a numpy Alg. 4 on small dense systems.
+ * Restart (option gcr_true_restart): 1 (default, reading R13) replaces the recursive residual
+ * by the true b - A x at every restart (over ~100 steps the recursive r drifts ~1e-9 from
+ * the true one); 0 keeps the recursive r, literally Alg. 4.  Exit (reading R13):
+ * when E(recursive r) <= rtol the TRUE residual is evaluated; the solve stops only if its E
+ * is <= rtol too, otherwise it restarts from that true residual.  The E returned is always
+ * the true one. */
 typedef struct { double *x, *y, *p; } ovec;
+typedef struct {
+    void *ctx;
+    void (*precond)(void *ctx, ovec r, ovec z);   /* z = M^-1 r */
+    void (*apply)(void *ctx, ovec z, ovec w);     /* w = A z */
+    double (*dot)(void *ctx, ovec a, ovec b);
+    void (*axpy)(void *ctx, double a, ovec x, ovec y);  /* y += a x */
+    void (*scale)(void *ctx, double a, ovec x);
+    void (*residual)(void *ctx, ovec x, ovec r);  /* r = b - A x */
+    double (*energy)(void *ctx, ovec r);          /* stopping-test measure of a residual */
+    void (*step)(void *ctx, int k);               /* before preconditioner application k */
+} gcr_ops;
+
+static int gcr_core(const gcr_ops *op, ovec x, ovec r, ovec *z, ovec *w, int m, int max_iter, int true_restart,
+                    double rtol, double E0, int *iters, double *E_out, double *hist, int hist_len) {
+    void *c = op->ctx;
+    op->residual(c, x, r);  /* r0 = b - A x0 */
+    int k = 0, status = O_NOT_CONVERGED, fresh = 1;
+    double E = E0;
+    while (k < max_iter && status == O_NOT_CONVERGED) {
+        if (!fresh && true_restart) op->residual(c, x, r);  /* restart from the true residual (R13) */
+        fresh = 0;
+        for (int i = 0; i < m && k < max_iter; ++i) {
+            op->step(c, k);
+            op->precond(c, r, z[i]);          /* z_i = M^-1 r      (Alg. 4 line 5) */
+            op->apply(c, z[i], w[i]);         /* w_i = A z_i       (line 6) */
+            for (int j = 0; j < i; ++j) {     /* modified Gram-Schmidt (lines 7-10) */
+                double g = op->dot(c, w[i], w[j]);
+                op->axpy(c, -g, w[j], w[i]);
+                op->axpy(c, -g, z[j], z[i]);
+            }
+            double nu = sqrt(op->dot(c, w[i], w[i]));
+            double rn = sqrt(op->dot(c, r, r));
+            ++k;
+            if (!(nu > 1e-14 * rn)) { status = O_EDIVERGED; break; } /* breakdown (R13) */
+            op->scale(c, 1.0 / nu, w[i]);     /* lines 11-12 */
+            op->scale(c, 1.0 / nu, z[i]);
+            double beta = op->dot(c, r, w[i]);  /* line 13 */
+            op->axpy(c, beta, z[i], x);       /* line 14 */
+            op->axpy(c, -beta, w[i], r);      /* line 15 */
+            E = op->energy(c, r);
+            if (hist && k - 1 < hist_len) hist[k - 1] = E;
+            if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = O_EDIVERGED; break; }
+            if (E <= rtol) {                  /* exit test on the true residual (R13) */
+                op->residual(c, x, r);
+                fresh = 1;
+                if (op->energy(c, r) <= rtol) status = O_OK;
+                break;                        /* else: restart from that true residual */
+            }
+        }
+    }
+    op->residual(c, x, r);  /* the E reported is the true one */
+    *E_out = op->energy(c, r);
+    *iters = k;
+    return status;
+}
+
 static ovec ovec_new(size_t n) { ovec v = {zalloc(n), zalloc(n), zalloc(n)}; return v; }
 static void ovec_free(ovec v) { free(v.x); free(v.y); free(v.p); }
 static double ovec_dot(const olevel *L, ovec a, ovec b) {
@@ -1055,15 +1119,31 @@ static void apply_precond(oracle_t *S, ovec r, ovec z) {
     double m = p_mean(L, z.p);
     FOR_P(L) z.p[IX(L, i, j)] -= m;
 }
-/* w = A z = [L z_v + G z_p; D z_v] (z mirrors current) */
+/* w = A z = [L z_v + G z_p; D z_v] */
 static void apply_A(oracle_t *S, ovec z, ovec w) {
     olevel *L = &S->lev[0];
     size_t n = padn(L);
+    refresh_mirrors(S, L, z.x, z.y);
     memset(w.x, 0, n * sizeof(double)); memset(w.y, 0, n * sizeof(double)); memset(w.p, 0, n * sizeof(double));
     FOR_VX(L) w.x[IX(L, i, j)] = Lx_point(L, z.x, z.y, i, j) + Gx_point(L, z.p, i, j);
     FOR_VY(L) w.y[IX(L, i, j)] = Ly_point(L, z.x, z.y, i, j) + Gy_point(L, z.p, i, j);
     FOR_P(L) w.p[IX(L, i, j)] = D_point(L, z.x, z.y, i, j);
 }
+/* the Stokes instance of gcr_ops */
+typedef struct { oracle_t *S; double Sf; } stokes_gcr;
+static void sg_precond(void *c, ovec r, ovec z) { apply_precond(((stokes_gcr *)c)->S, r, z); }
+static void sg_apply(void *c, ovec z, ovec w) { apply_A(((stokes_gcr *)c)->S, z, w); }
+static double sg_dot(void *c, ovec a, ovec b) { return ovec_dot(&((stokes_gcr *)c)->S->lev[0], a, b); }
+static void sg_axpy(void *c, double a, ovec x, ovec y) { ovec_axpy(&((stokes_gcr *)c)->S->lev[0], a, x, y); }
+static void sg_scale(void *c, double a, ovec x) { ovec_scale(&((stokes_gcr *)c)->S->lev[0], a, x); }
+static void sg_residual(void *c, ovec x, ovec r) {
+    oracle_t *S = ((stokes_gcr *)c)->S;
+    refresh_mirrors(S, &S->lev[0], x.x, x.y);
+    full_residual(S, x.x, x.y, x.p, r.x, r.y, r.p);
+}
+static double sg_energy(void *c, ovec r) { return energy_of(((stokes_gcr *)c)->S, r.x, r.y, r.p, ((stokes_gcr *)c)->Sf); }
+static void sg_step(void *c, int k) { ((stokes_gcr *)c)->S->ras_k = k; ((stokes_gcr *)c)->S->ras_c = 0; } /* R27 */
+
 static int solve_gcr(oracle_t *S, double rtol, double Sf, double E0, int *iters, double *E_out, double *hist,
                      int hist_len) {
     olevel *L = &S->lev[0];
@@ -1072,45 +1152,68 @@ static int solve_gcr(oracle_t *S, double rtol, double Sf, double E0, int *iters,
     ovec r = ovec_new(n), xv = {S->vx, S->vy, S->p};
     ovec *z = (ovec *)calloc(m, sizeof(ovec)), *w = (ovec *)calloc(m, sizeof(ovec));
     for (int k = 0; k < m; ++k) { z[k] = ovec_new(n); w[k] = ovec_new(n); }
-    full_residual(S, S->vx, S->vy, S->p, r.x, r.y, r.p); /* r0 = b - A x0 */
-    int k = 0, status = O_NOT_CONVERGED;
-    double E = E0;
-    while (k < S->o.max_iter && status == O_NOT_CONVERGED) {
-        if (k > 0) { /* restart: replace the recursive residual by the true one (reading R13) */
-            refresh_mirrors(S, L, S->vx, S->vy);
-            full_residual(S, S->vx, S->vy, S->p, r.x, r.y, r.p);
-        }
-        for (int i = 0; i < m && k < S->o.max_iter; ++i) {
-            S->ras_k = k; S->ras_c = 0;  /* RAS shift counter: iteration index (R27) */
-            apply_precond(S, r, z[i]);
-            refresh_mirrors(S, L, z[i].x, z[i].y);
-            apply_A(S, z[i], w[i]);
-            for (int j = 0; j < i; ++j) { /* modified Gram-Schmidt */
-                double g = ovec_dot(L, w[i], w[j]);
-                ovec_axpy(L, -g, w[j], w[i]);
-                ovec_axpy(L, -g, z[j], z[i]);
-            }
-            double nu = sqrt(ovec_dot(L, w[i], w[i]));
-            double rn = sqrt(ovec_dot(L, r, r));
-            ++k;
-            if (!(nu > 1e-14 * rn)) { status = O_EDIVERGED; break; } /* breakdown (R13) */
-            ovec_scale(L, 1.0 / nu, w[i]);
-            ovec_scale(L, 1.0 / nu, z[i]);
-            double beta = ovec_dot(L, r, w[i]);
-            ovec_axpy(L, beta, z[i], xv);
-            ovec_axpy(L, -beta, w[i], r);
-            E = energy_of(S, r.x, r.y, r.p, Sf);
-            if (hist && k - 1 < hist_len) hist[k - 1] = E;
-            if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = O_EDIVERGED; break; }
-            if (E <= rtol) { status = O_OK; break; }
-        }
-    }
+    stokes_gcr ctx = {S, Sf};
+    gcr_ops op = {&ctx, sg_precond, sg_apply, sg_dot, sg_axpy, sg_scale, sg_residual, sg_energy, sg_step};
+    int status = gcr_core(&op, xv, r, z, w, m, S->o.max_iter, S->o.gcr_true_restart, rtol, E0, iters, E_out, hist,
+                          hist_len);
     refresh_mirrors(S, L, S->vx, S->vy);
-    *iters = k;
-    *E_out = E;
     for (int q = 0; q < m; ++q) { ovec_free(z[q]); ovec_free(w[q]); }
     free(z); free(w); ovec_free(r);
     return status;
+}
+
+/* the dense instance (pins only): A x = b with an explicit n x n preconditioner Minv,
+ * <.,.> Euclidean (pairwise sums), E = ||r|| / ||b|| */
+typedef struct { int n; const double *A, *Minv, *b; double nb; } dense_gcr;
+static void dmatvec(int n, const double *M, const double *u, double *v) {
+    double *t = zalloc(n);
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) t[j] = M[(size_t)i * n + j] * u[j];
+        v[i] = pairwise(t, n);
+    }
+    free(t);
+}
+static void dg_precond(void *c, ovec r, ovec z) { dense_gcr *d = c; dmatvec(d->n, d->Minv, r.x, z.x); }
+static void dg_apply(void *c, ovec z, ovec w) { dense_gcr *d = c; dmatvec(d->n, d->A, z.x, w.x); }
+static double dg_dot(void *c, ovec a, ovec b) {
+    dense_gcr *d = c;
+    double *t = zalloc(d->n);
+    for (int i = 0; i < d->n; ++i) t[i] = a.x[i] * b.x[i];
+    double s = pairwise(t, d->n);
+    free(t);
+    return s;
+}
+static void dg_axpy(void *c, double a, ovec x, ovec y) { dense_gcr *d = c; for (int i = 0; i < d->n; ++i) y.x[i] += a * x.x[i]; }
+static void dg_scale(void *c, double a, ovec x) { dense_gcr *d = c; for (int i = 0; i < d->n; ++i) x.x[i] *= a; }
+static void dg_residual(void *c, ovec x, ovec r) {
+    dense_gcr *d = c;
+    dmatvec(d->n, d->A, x.x, r.x);
+    for (int i = 0; i < d->n; ++i) r.x[i] = d->b[i] - r.x[i];
+}
+static double dg_energy(void *c, ovec r) { return sqrt(dg_dot(c, r, r)) / ((dense_gcr *)c)->nb; }
+static void dg_step(void *c, int k) { (void)c; (void)k; }
+
+/* GCR(m) of gcr_core on a dense system (test entry point: pins the Krylov code on small
+ * dense systems).  x: in initial guess, out iterate.  W (nullable, n x m row-
+ * major by vector): the normalised w_i of the last cycle, for the orthogonality pin. */
+int oracle_gcr_dense(int n, const double *A, const double *Minv, const double *b, double *x, int m, int max_iter,
+                     int true_restart, double rtol, int *iters, double *E, double *hist, int hist_len, double *W) {
+    if (n < 1 || m < 1 || max_iter < 0 || !A || !Minv || !b || !x || !iters || !E) return O_EINVAL;
+    dense_gcr ctx = {n, A, Minv, b, 0.0};
+    ovec bb = {(double *)b, NULL, NULL};
+    ctx.nb = sqrt(dg_dot(&ctx, bb, bb));
+    if (!(ctx.nb > 0)) return O_EINVAL;
+    gcr_ops op = {&ctx, dg_precond, dg_apply, dg_dot, dg_axpy, dg_scale, dg_residual, dg_energy, dg_step};
+    ovec r = {zalloc(n), NULL, NULL}, xv = {x, NULL, NULL};
+    ovec *z = (ovec *)calloc(m, sizeof(ovec)), *w = (ovec *)calloc(m, sizeof(ovec));
+    for (int k = 0; k < m; ++k) { z[k].x = zalloc(n); w[k].x = zalloc(n); }
+    op.residual(&ctx, xv, r);
+    double E0 = dg_energy(&ctx, r);
+    int st = gcr_core(&op, xv, r, z, w, m, max_iter, true_restart, rtol, E0, iters, E, hist, hist_len);
+    if (W) for (int k = 0; k < m; ++k) memcpy(W + (size_t)k * n, w[k].x, (size_t)n * sizeof(double));
+    for (int k = 0; k < m; ++k) { free(z[k].x); free(w[k].x); }
+    free(z); free(w); free(r.x);
+    return st;
 }
 
 /* solve(rtol): in = initial guess (v, p), out = solution; zero-mean p on exit.
@@ -1160,6 +1263,11 @@ static int aa_alpha(int n, const double *H, double *alpha) {
     if (!(fabs(sz) > 0.0)) return -1;
     for (int i = 0; i < n; ++i) alpha[i] = z[i] / sz;
     return 0;
+}
+/* test entry point: the Alg. 5 argmin of solve_anderson on a given Gram matrix H = R^T R */
+int oracle_aa_alpha(int n, const double *H, double *alpha) {
+    if (n < 1 || n > 16 || !H || !alpha) return O_EINVAL;
+    return aa_alpha(n, H, alpha) == 0 ? O_OK : O_EINVAL;
 }
 static int solve_anderson(oracle_t *S, double rtol, double Sf, double E0, int *iters, double *E_out, double *hist,
                           int hist_len) {

@@ -87,6 +87,7 @@ int check_opts(const stokes_opts &o) {
     if (o.vcycles_per_iter < 1 || o.accel < 0 || o.accel > 2) return STOKES_EINVAL;
     if (o.aa_depth < 0 || o.aa_depth >= AA_MAXS || !(o.aa_beta > 0.0 && o.aa_beta <= 1.0)) return STOKES_EINVAL;
     if (o.gcr_restart < 1 || o.gcr_restart > MAXM || o.max_iter < 0) return STOKES_EINVAL;
+    if (o.gcr_true_restart != 0 && o.gcr_true_restart != 1) return STOKES_EINVAL;
     if (o.pressure_sign != 1 && o.pressure_sign != -1) return STOKES_EINVAL;
     if (!(o.theta_step >= 0.0 && o.theta_step <= 1.0) || o.theta_every < 1) return STOKES_EINVAL;
     return STOKES_OK;
@@ -444,6 +445,14 @@ void force_energy(stokes_s *h) {
     cudaMemcpyAsync(h->scal + S_SF, h->scal + S_SFPART + 1, sizeof(double), cudaMemcpyDeviceToDevice, h->stream);
 }
 
+// copy the E that state_energy left in scal[S_E] to the host
+int read_energy(stokes_s *h, double *E) {
+    CK(cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    int st = sync(h);
+    if (st) return st;
+    *E = h->hscal[S_E];
+    return STOKES_OK;
+}
 int energy_now(stokes_s *h, double *E) {
     state_energy(h, nullptr, nullptr, nullptr);
     cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
@@ -633,10 +642,11 @@ int solve_gcr_fused(stokes_s *h, double rtol, double E0, int *iters, double *Eou
     const int m = h->o.gcr_restart;
     double **r = h->gr;
     state_energy(h, r[0], r[1], r[2]);  // r0 = b - A x0
-    int k = 0, status = STOKES_NOT_CONVERGED;
+    int k = 0, status = STOKES_NOT_CONVERGED, fresh = 1;
     double E = E0;
     while (k < h->o.max_iter && status == STOKES_NOT_CONVERGED) {
-        if (k > 0) state_energy(h, r[0], r[1], r[2]);  // restart: true residual (reading R13)
+        if (!fresh && h->o.gcr_true_restart) state_energy(h, r[0], r[1], r[2]);  // restart (R13)
+        fresh = 0;
         for (int i = 0; i < m && k < h->o.max_iter; ++i) {
             if (!h->gcr_exec[i]) {  // capture step i once (pcur is fixed during GCR)
                 cudaGraph_t graph;
@@ -663,12 +673,21 @@ int solve_gcr_fused(stokes_s *h, double rtol, double E0, int *iters, double *Eou
             E = h->hscal[S_E];
             if (!(nu2 > 1e-28 * rr)) { status = STOKES_EDIVERGED; break; }  // breakdown (R13)
             if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
-            if (E <= rtol) { status = STOKES_OK; break; }
+            if (E <= rtol) {  // exit test on the true residual (R13): else restart from it
+                double Et;
+                state_energy(h, r[0], r[1], r[2]);
+                if ((st = read_energy(h, &Et))) return st;
+                fresh = 1;
+                if (Et <= rtol) status = STOKES_OK;
+                break;
+            }
         }
     }
     *iters = k;
+    // the true E of x and the mean of x_p for the output de-mean
+    int st = energy_now(h, &E);
+    if (st) return st;
     *Eout = E;
-    state_energy(h, nullptr, nullptr, nullptr);  // mean of x_p for the output de-mean
     return status;
 }
 
@@ -684,11 +703,12 @@ int solve_gcr(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
     double **r = h->gr;
     // r0 = b - A x0 (recursive residual)
     state_energy(h, r[0], r[1], r[2]);
-    int k = 0, status = STOKES_NOT_CONVERGED;
+    int k = 0, status = STOKES_NOT_CONVERGED, fresh = 1;
     double E = E0;
     const double inv_np = 1.0 / ((double)g.ncx * g.ncy);
     while (k < h->o.max_iter && status == STOKES_NOT_CONVERGED) {
-        if (k > 0) state_energy(h, r[0], r[1], r[2]);  // restart: true residual (reading R13)
+        if (!fresh && h->o.gcr_true_restart) state_energy(h, r[0], r[1], r[2]);  // restart (R13)
+        fresh = 0;
         for (int i = 0; i < m && k < h->o.max_iter; ++i) {
             double **z = h->gz[i], **w = h->gw[i];
             // z = M^-1 r: dv = Vcycle(0; r_v); dp = alpha eta_P (r_p - D dv); de-mean dp
@@ -734,13 +754,22 @@ int solve_gcr(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
             E = h->hscal[S_E];
             if (!(nu2 > 1e-28 * rr)) { status = STOKES_EDIVERGED; break; }  // breakdown (R13)
             if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
-            if (E <= rtol) { status = STOKES_OK; break; }
+            if (E <= rtol) {  // exit test on the true residual (R13): else restart from it
+                double Et;
+                state_energy(h, r[0], r[1], r[2]);
+                if ((st = read_energy(h, &Et))) return st;
+                fresh = 1;
+                if (Et <= rtol) status = STOKES_OK;
+                break;
+            }
         }
     }
     *iters = k;
+    // the true E of x; the pressure mean of x (inert) is removed at output
+    // through S_MSHIFT
+    int st = energy_now(h, &E);
+    if (st) return st;
     *Eout = E;
-    // the pressure mean of x (inert) is removed at output through S_MSHIFT
-    state_energy(h, nullptr, nullptr, nullptr);
     return status;
 }
 
@@ -774,6 +803,7 @@ int stokes_opts_default(stokes_opts *o) {
     o->ras_tile = 32;
     o->ras_inner = 4;
     o->ras_seed = 2603;
+    o->gcr_true_restart = 1;
     return STOKES_OK;
 }
 

@@ -57,6 +57,7 @@ class Opts(ctypes.Structure):
         ("ras_tile", ctypes.c_int),
         ("ras_inner", ctypes.c_int),
         ("ras_seed", ctypes.c_uint64),
+        ("gcr_true_restart", ctypes.c_int),
     ]
 
 

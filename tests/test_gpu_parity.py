@@ -213,6 +213,24 @@ CASES = [
 ]
 
 
+def rounding_spread(n, w, opts, k):
+    """The ORACLE's own sensitivity to rounding at a fixed iteration count k: the same k
+    iterations with rho perturbed by ~1e-15 relative (a rounding-level change of the input).
+    Krylov and Anderson recurrences amplify such differences; the GPU sums in a different
+    (tree) order, so its fixed-count distance to the oracle is bounded by a small multiple of
+    this measured spread."""
+    rng = np.random.default_rng(99)
+    w2 = dict(w, rho_b=w["rho_b"] * (1.0 + 1e-15 * rng.standard_normal(w["rho_b"].shape)))
+    out = []
+    for ww in (w, w2):
+        o = Oracle(n, n, w["Lx"], w["Ly"], w["bc"], **dict(opts, max_iter=k))
+        o.set_viscosity(ww["eta_b"], ww["eta_p"])
+        o.set_density(ww["rho_b"])
+        o.set_gravity(w["gx"], w["gy"])
+        out.append(o.solve(0.0))
+    return max(rel(out[1][key], out[0][key]) for key in ("vx", "vy", "p"))
+
+
 @pytest.mark.parametrize("name,n,opts", CASES)
 def test_solve_parity(S, name, n, opts):
     w = workload(name, n, n)
@@ -221,23 +239,40 @@ def test_solve_parity(S, name, n, opts):
     b = s.solve(1e-8)
     assert a["status"] == 0 and b["status"] == 0
     assert abs(a["iters"] - b["iters"]) <= 1, (a["iters"], b["iters"])
-    assert b["E"] <= 1e-8
-    # equal iteration count -> the iterates themselves agree.  Uzawa iterates agree to
-    # rounding; GCR's Krylov recurrences amplify reduction-order differences (measured
-    # ~3e-9 after 90 iterations), so its fixed-count bar is 1e-8.
-    k = a["iters"]
-    o2, s2 = pair(S, n, n, w["bc"], w, w["Lx"], w["Ly"], (w["gx"], w["gy"]), **dict(opts, max_iter=k))
+    assert b["E"] <= 1e-8  # the true residual's E (GCR: SURVEY Q13)
+    # the converged GPU solution against the oracle's iterate at the SAME count (north_star:
+    # <= 1e-9).  Uzawa iterates agree to rounding; GCR's Krylov recurrences amplify the
+    # reduction order, so its bar is max(1e-9, 10x the oracle's own rounding spread).
+    k = b["iters"]
+    o2 = Oracle(n, n, w["Lx"], w["Ly"], w["bc"], **dict(opts, max_iter=k))
+    o2.set_viscosity(w["eta_b"], w["eta_p"])
+    o2.set_density(w["rho_b"])
+    o2.set_gravity(w["gx"], w["gy"])
     a2 = o2.solve(0.0)
-    b2 = s2.solve(0.0)
-    bar = 1e-8 if opts.get("accel", 0) else 1e-9
+    bar = max(1e-9, 10 * rounding_spread(n, w, opts, k)) if opts.get("accel", 0) else 1e-9
     for key in ("vx", "vy", "p"):
-        assert rel(b2[key], a2[key]) <= bar, key
-        assert rel(b[key], a[key]) <= 1e-6, key  # +-1 iteration at E ~ 1e-8
+        assert rel(b[key], a2[key]) <= bar, (key, rel(b[key], a2[key]), bar)
     # converged at equal (tight) residual tolerance -> <= 1e-9 (north_star bar)
     a3 = o.solve(1e-11)
     b3 = s.solve(1e-11)
     for key in ("vx", "vy", "p"):
         assert rel(b3[key], a3[key]) <= 1e-9, key
+
+
+@pytest.mark.parametrize("true_restart", [0, 1])
+def test_gcr_restart_readings(S, true_restart):
+    """GCR restart from the true residual (R13, default) and the literal recursive one
+    (Alg. 4): GPU = oracle iterate by iterate across restarts."""
+    n = 64
+    w = workload("solcx", n, n)
+    opts = dict(omega_v=0.6, alpha_p=1.0, accel=1, gcr_restart=5, gcr_true_restart=true_restart)
+    for k in (4, 5, 6, 11, 23):
+        o, s = pair(S, n, n, w["bc"], w, w["Lx"], w["Ly"], (w["gx"], w["gy"]), **dict(opts, max_iter=k))
+        a, b = o.solve(0.0), s.solve(0.0)
+        assert a["iters"] == b["iters"] == k
+        assert abs(a["E"] - b["E"]) <= 1e-9 * a["E"]
+        for key in ("vx", "vy", "p"):
+            assert rel(b[key], a[key]) <= 1e-10, (k, key)
 
 
 @pytest.mark.parametrize("name,n,opts", [
@@ -263,7 +298,12 @@ def test_anderson_parity(S, name, n, opts):
     o, s = pair(*args, **opts)
     a, b = o.solve(1e-8), s.solve(1e-8)
     assert a["status"] == 0 and b["status"] == 0
-    assert abs(a["iters"] - b["iters"]) <= max(2, a["iters"] // 10), (a["iters"], b["iters"])
+    # count band = the oracle's own spread under a rounding-level input change (the
+    # least-squares history is ill-conditioned near convergence), at least +-1
+    w2 = dict(w, rho_b=w["rho_b"] * (1.0 + 1e-15 * np.random.default_rng(99).standard_normal(w["rho_b"].shape)))
+    o2, _ = pair(S, n, n, w["bc"], w2, w["Lx"], w["Ly"], (w["gx"], w["gy"]), **opts)
+    band = max(1, 2 * abs(o2.solve(1e-8)["iters"] - a["iters"]))
+    assert abs(a["iters"] - b["iters"]) <= band, (a["iters"], b["iters"], band)
     a, b = o.solve(1e-11), s.solve(1e-11)
     for key in ("vx", "vy", "p"):
         assert rel(b[key], a[key]) <= 1e-9, key

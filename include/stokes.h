@@ -181,6 +181,12 @@ int stokes_vcycle(stokes_t h, const double *bx, const double *by, double *vx, do
  * (restarting from it if it does not pass); the E returned is the true one.
  * Returns OK, NOT_CONVERGED, EDIVERGED (last iterate kept) or an error. */
 int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy);
+/* stokes_solve that also writes E after every iteration: hist[k] (HOST, hist_len doubles,
+ * caller-owned; entries past *iters are untouched) = E after iteration k + 1 -- the energy
+ * residual of the new (v, p) (Uzawa, Anderson: of G(x^k)) or of the recursive residual (GCR),
+ * counted across viscosity-rescaling stages.  Single-domain handles (EINVAL otherwise). */
+int stokes_solve_hist(stokes_t h, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy,
+                      double *hist, int hist_len);
 
 /* ---- per-step entry points (parity tests of each hot-path step; same layouts at the
  * given level's size; all device pointers) ------------------------------------------- */

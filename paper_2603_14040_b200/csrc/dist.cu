@@ -65,19 +65,25 @@ struct Dist {
 
 namespace {
 
-enum { FX_V = 0, FX_R = 1, FX_P = 2, FX_ETA = 3, FX_RHO = 4 };
-enum { M_VIRTUAL = 0, M_LOOPBACK = 1, M_NCCL = 2 };
+enum { FX_V = 0, FX_R = 1, FX_P = 2, FX_ETA = 3, FX_RHO = 4, FX_B = 5, FX_VP = 6 };
+enum { M_VIRTUAL = 0, M_LOOPBACK = 1, M_NCCL = 2, M_NCCL_SELF = 3 };
+constexpr int HW = 2;  // halo width: the two-sweep pass and the fused residual+restriction read two rings
 
 LaunchCtx dctx(Dist &D) { return LaunchCtx{D.stream, &D.launches}; }
+bool packed(const Dist &D) { return D.mode != M_VIRTUAL; }
+bool self_nccl(const Dist &D) { return D.mode == M_NCCL_SELF; }
 
-int nfields(stokes_s *h, int l, int which, int idx, double **f) {
+// the fields of a halo exchange: FX_VP = velocity buffer idx and pressure buffer pidx
+int nfields(Dist &D, stokes_s *h, int l, int which, int idx, double **f) {
     Level &L = h->lev[l];
     switch (which) {
     case FX_V: f[0] = L.vx[idx]; f[1] = L.vy[idx]; return 2;
+    case FX_VP: f[0] = L.vx[idx & 1]; f[1] = L.vy[idx & 1]; f[2] = h->pbuf[idx >> 1]; return 3;
     case FX_R: f[0] = L.rx; f[1] = L.ry; return 2;
+    case FX_B: f[0] = L.bx; f[1] = L.by; return 2;
     case FX_P: f[0] = h->pbuf[idx]; return 1;
     case FX_ETA: f[0] = L.etab; f[1] = L.etap; return 2;
-    default: f[0] = h->rho; return 1;
+    default: (void)D; f[0] = h->rho; return 1;
     }
 }
 int tile_at(Dist &D, int tx, int ty) { return D.mode != M_NCCL ? ty * D.px + tx : -1; }
@@ -90,137 +96,163 @@ void add_strip(StripList &s, double *dst, const double *src, int n, int ds, int 
     s.sstride[s.count] = ss;
     ++s.count;
 }
+// a whole field incl. its row -1 (copies / clears that must not leave a stale second ring)
+double *fstart(const GridL &g, double *p) { return p - COL_OFF - g.P; }
+size_t fsize(const GridL &g) { return field_doubles(g) + g.P; }
 
-// halo exchange of the selected fields of level l (two phases, corners included)
+// point-to-point transfer of n doubles between local buffers: device copy (LOOPBACK) or a
+// real ncclSend / ncclRecv pair on the one-rank communicator (NCCL_SELF; caller groups)
+int p2p_local(Dist &D, double *dst, const double *src, size_t n) {
+    if (self_nccl(D)) {
+        if (ncclSend(src, n, ncclDouble, 0, D.comm, D.stream) != ncclSuccess) return STOKES_ENCCL;
+        if (ncclRecv(dst, n, ncclDouble, 0, D.comm, D.stream) != ncclSuccess) return STOKES_ENCCL;
+        return STOKES_OK;
+    }
+    CK(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, D.stream));
+    return STOKES_OK;
+}
+int group_start(Dist &D) {
+    if (D.mode == M_NCCL || self_nccl(D)) return ncclGroupStart() == ncclSuccess ? STOKES_OK : STOKES_ENCCL;
+    return STOKES_OK;
+}
+int group_end(Dist &D) {
+    if (D.mode == M_NCCL || self_nccl(D)) return ncclGroupEnd() == ncclSuccess ? STOKES_OK : STOKES_ENCCL;
+    return STOKES_OK;
+}
+
+// Halo exchange of the selected fields of level l: HW = 2 rings, two phases (W/E columns
+// over rows -1 .. ncy+2, then N/S rows over columns -1 .. ncx+2: corners included).
+//   my column ncx + h <- E neighbour's column h,   my column 1 - h <- W neighbour's ncx + 1 - h
+//   my row    ncy + h <- S neighbour's row h,      my row    1 - h <- N neighbour's ncy + 1 - h
+// (h = 1, 2; the same map for every node type, since tiles own the east vx faces, the south
+// vy faces and the south-east basic nodes of their cells).
 int exchange(Dist &D, int l, int which, int idx) {
     const LaunchCtx c = dctx(D);
-    double *f[2], *fu[2];
-    if (D.mode == M_VIRTUAL) {  // ---- virtual: strip-copy kernels between the tiles' buffers
+    double *f[3], *fu[3];
+    const int rows = D.tile[0]->lev[l].g.ncy + 2 * HW, cols = D.tile[0]->lev[l].g.ncx + 2 * HW;
+    if (!packed(D)) {  // ---- virtual: strip-copy kernels between the tiles' buffers
         StripList s;
         s.count = 0;
         for (int k = 0; k < D.nt; ++k) {
             const GridL &g = D.tile[k]->lev[l].g;
-            const int nf = nfields(D.tile[k], l, which, idx, f);
-            if (D.tx[k] + 1 < D.px) {
-                nfields(D.tile[tile_at(D, D.tx[k] + 1, D.ty[k])], l, which, idx, fu);
-                for (int q = 0; q < nf; ++q) add_strip(s, f[q] + at(g, 0, g.ncx + 1), fu[q] + at(g, 0, 1), g.ncy + 2, g.P, g.P);
-            }
-            if (D.tx[k] > 0) {
-                nfields(D.tile[tile_at(D, D.tx[k] - 1, D.ty[k])], l, which, idx, fu);
-                for (int q = 0; q < nf; ++q) add_strip(s, f[q] + at(g, 0, 0), fu[q] + at(g, 0, g.ncx), g.ncy + 2, g.P, g.P);
+            const int nf = nfields(D, D.tile[k], l, which, idx, f);
+            for (int side = 0; side < 2; ++side) {
+                const int nb = side ? (D.tx[k] + 1 < D.px ? tile_at(D, D.tx[k] + 1, D.ty[k]) : -1)
+                                    : (D.tx[k] > 0 ? tile_at(D, D.tx[k] - 1, D.ty[k]) : -1);
+                if (nb < 0) continue;
+                nfields(D, D.tile[nb], l, which, idx, fu);
+                for (int q = 0; q < nf; ++q)
+                    for (int hh = 1; hh <= HW; ++hh) {
+                        const int jd = side ? g.ncx + hh : 1 - hh, js = side ? hh : g.ncx + 1 - hh;
+                        add_strip(s, f[q] + at(g, -1, jd), fu[q] + at(g, -1, js), rows, g.P, g.P);
+                    }
             }
         }
         if (s.count) launch_strips(c, s);
         s.count = 0;
         for (int k = 0; k < D.nt; ++k) {
             const GridL &g = D.tile[k]->lev[l].g;
-            const int nf = nfields(D.tile[k], l, which, idx, f);
-            if (D.ty[k] + 1 < D.py) {
-                nfields(D.tile[tile_at(D, D.tx[k], D.ty[k] + 1)], l, which, idx, fu);
-                for (int q = 0; q < nf; ++q) add_strip(s, f[q] + at(g, g.ncy + 1, 0), fu[q] + at(g, 1, 0), g.ncx + 2, 1, 1);
-            }
-            if (D.ty[k] > 0) {
-                nfields(D.tile[tile_at(D, D.tx[k], D.ty[k] - 1)], l, which, idx, fu);
-                for (int q = 0; q < nf; ++q) add_strip(s, f[q] + at(g, 0, 0), fu[q] + at(g, g.ncy, 0), g.ncx + 2, 1, 1);
+            const int nf = nfields(D, D.tile[k], l, which, idx, f);
+            for (int side = 0; side < 2; ++side) {
+                const int nb = side ? (D.ty[k] + 1 < D.py ? tile_at(D, D.tx[k], D.ty[k] + 1) : -1)
+                                    : (D.ty[k] > 0 ? tile_at(D, D.tx[k], D.ty[k] - 1) : -1);
+                if (nb < 0) continue;
+                nfields(D, D.tile[nb], l, which, idx, fu);
+                for (int q = 0; q < nf; ++q)
+                    for (int hh = 1; hh <= HW; ++hh) {
+                        const int id = side ? g.ncy + hh : 1 - hh, is = side ? hh : g.ncy + 1 - hh;
+                        add_strip(s, f[q] + at(g, id, -1), fu[q] + at(g, is, -1), cols, 1, 1);
+                    }
             }
         }
         if (s.count) launch_strips(c, s);
         return STOKES_OK;
     }
-    // ---- packed transport (NCCL: one tile per process; LOOPBACK: every tile here, the same
-    // packing with the transfers done by device copies -- tests the NCCL path on one GPU)
-    const int nl = D.nt;
-    int nf = 0;
-    int rows = 0;
-    {  // phase 1: W/E columns packed into sb = [W part | E part], nf x rows each
+    // ---- packed transports: NCCL (one tile per process), NCCL_SELF (every tile here, real
+    // ncclSend / ncclRecv on a one-rank communicator), LOOPBACK (every tile here, device copies)
+    int nf = 0, st;
+    {  // phase 1: W/E columns packed into sb = [W part | E part], nf x HW x rows each
         StripList s;
         s.count = 0;
-        for (int k = 0; k < nl; ++k) {
+        for (int k = 0; k < D.nt; ++k) {
             const GridL &g = D.tile[k]->lev[l].g;
-            nf = nfields(D.tile[k], l, which, idx, f);
-            rows = g.ncy + 2;
+            nf = nfields(D, D.tile[k], l, which, idx, f);
             const bool W = D.tx[k] > 0, E = D.tx[k] + 1 < D.px;
-            for (int q = 0; q < nf; ++q) {
-                if (W) add_strip(s, D.sb[k] + (size_t)q * rows, f[q] + at(g, 0, 1), rows, 1, g.P);
-                if (E) add_strip(s, D.sb[k] + (size_t)(nf + q) * rows, f[q] + at(g, 0, g.ncx), rows, 1, g.P);
-            }
+            for (int q = 0; q < nf; ++q)
+                for (int hh = 1; hh <= HW; ++hh) {
+                    const size_t e = (size_t)(q * HW + hh - 1) * rows;
+                    if (W) add_strip(s, D.sb[k] + e, f[q] + at(g, -1, hh), rows, 1, g.P);
+                    if (E) add_strip(s, D.sb[k] + (size_t)nf * HW * rows + e, f[q] + at(g, -1, g.ncx + 1 - hh), rows, 1, g.P);
+                }
         }
         if (s.count) launch_strips(c, s);
-        const size_t part = (size_t)nf * rows;
+        const size_t part = (size_t)nf * HW * rows;
+        if ((st = group_start(D))) return st;
         if (D.mode == M_NCCL) {
             const int W = D.tx[0] > 0 ? D.rank - 1 : -1, E = D.tx[0] + 1 < D.px ? D.rank + 1 : -1;
-            if (W >= 0 || E >= 0) {
-                ncclGroupStart();
-                if (W >= 0) {
-                    ncclSend(D.sb[0], part, ncclDouble, W, D.comm, D.stream);
-                    ncclRecv(D.rb[0], part, ncclDouble, W, D.comm, D.stream);
-                }
-                if (E >= 0) {
-                    ncclSend(D.sb[0] + part, part, ncclDouble, E, D.comm, D.stream);
-                    ncclRecv(D.rb[0] + part, part, ncclDouble, E, D.comm, D.stream);
-                }
-                if (ncclGroupEnd() != ncclSuccess) return STOKES_ENCCL;
+            if (W >= 0) {
+                ncclSend(D.sb[0], part, ncclDouble, W, D.comm, D.stream);
+                ncclRecv(D.rb[0], part, ncclDouble, W, D.comm, D.stream);
             }
-        } else {  // loopback: my W part <- W neighbour's E part, my E part <- E neighbour's W part
-            for (int k = 0; k < nl; ++k) {
-                if (D.tx[k] > 0)
-                    CK(cudaMemcpyAsync(D.rb[k], D.sb[tile_at(D, D.tx[k] - 1, D.ty[k])] + part, part * 8,
-                                       cudaMemcpyDeviceToDevice, D.stream));
-                if (D.tx[k] + 1 < D.px)
-                    CK(cudaMemcpyAsync(D.rb[k] + part, D.sb[tile_at(D, D.tx[k] + 1, D.ty[k])], part * 8,
-                                       cudaMemcpyDeviceToDevice, D.stream));
+            if (E >= 0) {
+                ncclSend(D.sb[0] + part, part, ncclDouble, E, D.comm, D.stream);
+                ncclRecv(D.rb[0] + part, part, ncclDouble, E, D.comm, D.stream);
+            }
+        } else {  // my W part <- W neighbour's E part, my E part <- E neighbour's W part
+            for (int k = 0; k < D.nt; ++k) {
+                if (D.tx[k] > 0 && (st = p2p_local(D, D.rb[k], D.sb[tile_at(D, D.tx[k] - 1, D.ty[k])] + part, part)))
+                    return st;
+                if (D.tx[k] + 1 < D.px && (st = p2p_local(D, D.rb[k] + part, D.sb[tile_at(D, D.tx[k] + 1, D.ty[k])], part)))
+                    return st;
             }
         }
+        if ((st = group_end(D))) return st;
         s.count = 0;
-        for (int k = 0; k < nl; ++k) {
+        for (int k = 0; k < D.nt; ++k) {
             const GridL &g = D.tile[k]->lev[l].g;
-            nfields(D.tile[k], l, which, idx, f);
-            for (int q = 0; q < nf; ++q) {
-                if (D.tx[k] > 0) add_strip(s, f[q] + at(g, 0, 0), D.rb[k] + (size_t)q * rows, rows, g.P, 1);
-                if (D.tx[k] + 1 < D.px)
-                    add_strip(s, f[q] + at(g, 0, g.ncx + 1), D.rb[k] + (size_t)(nf + q) * rows, rows, g.P, 1);
-            }
+            nfields(D, D.tile[k], l, which, idx, f);
+            for (int q = 0; q < nf; ++q)
+                for (int hh = 1; hh <= HW; ++hh) {
+                    const size_t e = (size_t)(q * HW + hh - 1) * rows;
+                    if (D.tx[k] > 0) add_strip(s, f[q] + at(g, -1, 1 - hh), D.rb[k] + e, rows, g.P, 1);
+                    if (D.tx[k] + 1 < D.px) add_strip(s, f[q] + at(g, -1, g.ncx + hh), D.rb[k] + part + e, rows, g.P, 1);
+                }
         }
         if (s.count) launch_strips(c, s);
     }
-    // phase 2: N/S rows are contiguous: sent straight from / received straight into the field
-    if (D.mode == M_NCCL) {
-        const GridL &g = D.tile[0]->lev[l].g;
-        nfields(D.tile[0], l, which, idx, f);
-        const int N = D.ty[0] > 0 ? D.rank - D.px : -1, S = D.ty[0] + 1 < D.py ? D.rank + D.px : -1;
-        if (N >= 0 || S >= 0) {
-            ncclGroupStart();
+    // phase 2: the HW halo rows of a side are one contiguous block (rows r .. r+HW-1, columns
+    // -1 .. ncx+2): sent straight from / received straight into the field
+    if ((st = group_start(D))) return st;
+    for (int k = 0; k < D.nt; ++k) {
+        const GridL &g = D.tile[k]->lev[l].g;
+        const size_t blk = (size_t)(HW - 1) * g.P + cols;
+        nfields(D, D.tile[k], l, which, idx, f);
+        if (D.mode == M_NCCL) {
+            const int N = D.ty[0] > 0 ? D.rank - D.px : -1, S = D.ty[0] + 1 < D.py ? D.rank + D.px : -1;
             for (int q = 0; q < nf; ++q) {
                 if (N >= 0) {
-                    ncclSend(f[q] + at(g, 1, 0), g.ncx + 2, ncclDouble, N, D.comm, D.stream);
-                    ncclRecv(f[q] + at(g, 0, 0), g.ncx + 2, ncclDouble, N, D.comm, D.stream);
+                    ncclSend(f[q] + at(g, 1, -1), blk, ncclDouble, N, D.comm, D.stream);
+                    ncclRecv(f[q] + at(g, 1 - HW, -1), blk, ncclDouble, N, D.comm, D.stream);
                 }
                 if (S >= 0) {
-                    ncclSend(f[q] + at(g, g.ncy, 0), g.ncx + 2, ncclDouble, S, D.comm, D.stream);
-                    ncclRecv(f[q] + at(g, g.ncy + 1, 0), g.ncx + 2, ncclDouble, S, D.comm, D.stream);
+                    ncclSend(f[q] + at(g, g.ncy + 1 - HW, -1), blk, ncclDouble, S, D.comm, D.stream);
+                    ncclRecv(f[q] + at(g, g.ncy + 1, -1), blk, ncclDouble, S, D.comm, D.stream);
                 }
             }
-            if (ncclGroupEnd() != ncclSuccess) return STOKES_ENCCL;
-        }
-    } else {
-        for (int k = 0; k < nl; ++k) {
-            const GridL &g = D.tile[k]->lev[l].g;
-            nfields(D.tile[k], l, which, idx, f);
+        } else {
             for (int q = 0; q < nf; ++q) {
                 if (D.ty[k] > 0) {
-                    nfields(D.tile[tile_at(D, D.tx[k], D.ty[k] - 1)], l, which, idx, fu);
-                    CK(cudaMemcpyAsync(f[q] + at(g, 0, 0), fu[q] + at(g, g.ncy, 0), (g.ncx + 2) * 8,
-                                       cudaMemcpyDeviceToDevice, D.stream));
+                    nfields(D, D.tile[tile_at(D, D.tx[k], D.ty[k] - 1)], l, which, idx, fu);
+                    if ((st = p2p_local(D, f[q] + at(g, 1 - HW, -1), fu[q] + at(g, g.ncy + 1 - HW, -1), blk))) return st;
                 }
                 if (D.ty[k] + 1 < D.py) {
-                    nfields(D.tile[tile_at(D, D.tx[k], D.ty[k] + 1)], l, which, idx, fu);
-                    CK(cudaMemcpyAsync(f[q] + at(g, g.ncy + 1, 0), fu[q] + at(g, 1, 0), (g.ncx + 2) * 8,
-                                       cudaMemcpyDeviceToDevice, D.stream));
+                    nfields(D, D.tile[tile_at(D, D.tx[k], D.ty[k] + 1)], l, which, idx, fu);
+                    if ((st = p2p_local(D, f[q] + at(g, g.ncy + 1, -1), fu[q] + at(g, 1, -1), blk))) return st;
                 }
             }
         }
     }
-    return STOKES_OK;
+    return group_end(D);
 }
 
 // tile rectangle [r0, r0+nr) x [c0, c0+nc) of a level-La field -> global tail level 0 at
@@ -268,8 +300,9 @@ int gather_to_tail(Dist &D, int which) {
     if (D.mode == M_NCCL) {
         if (ncclAllGather(D.sb[0], D.rb[0], blk, ncclDouble, D.comm, D.stream) != ncclSuccess) return STOKES_ENCCL;
     } else {
-        for (int k = 0; k < D.nt; ++k)
-            CK(cudaMemcpyAsync(D.rb[0] + (size_t)k * blk, D.sb[k], blk * 8, cudaMemcpyDeviceToDevice, D.stream));
+        int st = group_start(D);
+        for (int k = 0; k < D.nt && !st; ++k) st = p2p_local(D, D.rb[0] + (size_t)k * blk, D.sb[k], blk);
+        if (st || (st = group_end(D))) return st;
     }
     for (int r = 0; r < D.px * D.py; ++r) {
         const int gi = (r / D.px) * gc.ncy, gj = (r % D.px) * gc.ncx;
@@ -302,66 +335,104 @@ RhsArgs tile_rhs(stokes_s *t, int l, bool fine) {
     return fine ? rhs_fine(t) : rhs_arrays(t->lev[l].bx, t->lev[l].by);
 }
 
-// nsweeps smoother sweeps on distributed level l; cur = index of the buffer holding v
-int dsmooth(Dist &D, int l, int &cur, int n, bool zero_in, bool fine) {
+// n smoother sweeps on distributed level l; cur = index of the buffer holding v.  Damped
+// Jacobi runs the single-domain kernels: pairs of sweeps as ONE two-sweep pass (k_jacobi2,
+// which also updates the first halo ring) where the level allows, at most max_pairs of them;
+// the width-2 halos are exchanged once per pass.  RBGS: the four phase kernels with an
+// exchange after each phase.
+int dsmooth(Dist &D, int l, int &cur, int n, bool zero_in, bool fine, int max_pairs) {
     if (n <= 0 && zero_in) {
         for (int k = 0; k < D.nt; ++k) {
             Level &L = D.tile[k]->lev[l];
-            CK(cudaMemsetAsync(L.vx[cur] - COL_OFF, 0, field_doubles(L.g) * 8, D.stream));
-            CK(cudaMemsetAsync(L.vy[cur] - COL_OFF, 0, field_doubles(L.g) * 8, D.stream));
+            CK(cudaMemsetAsync(fstart(L.g, L.vx[cur]), 0, fsize(L.g) * 8, D.stream));
+            CK(cudaMemsetAsync(fstart(L.g, L.vy[cur]), 0, fsize(L.g) * 8, D.stream));
         }
         return STOKES_OK;
     }
     int st;
-    for (int s = 0; s < n; ++s) {
-        if (D.o.smoother == STOKES_SMOOTH_JACOBI) {
+    if (D.o.smoother == STOKES_SMOOTH_JACOBI) {
+        const GridL &g0 = D.tile[0]->lev[l].g;
+        int pairs = jacobi2_ok(g0) ? (n - (zero_in ? 1 : 0)) / 2 : 0;
+        if (pairs > max_pairs) pairs = max_pairs;
+        for (int s = 0; s < n;) {
+            const bool two = pairs > 0 && !(zero_in && s == 0);
             for (int k = 0; k < D.nt; ++k) {
                 stokes_s *t = D.tile[k];
                 Level &L = t->lev[l];
-                launch_jacobi(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur], L.vx[1 - cur], L.vy[1 - cur],
-                              tile_rhs(t, l, fine), D.o.omega_v, zero_in && s == 0);
+                if (two)
+                    launch_jacobi2(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur], L.vx[1 - cur], L.vy[1 - cur],
+                                   tile_rhs(t, l, fine), D.o.omega_v);
+                else
+                    launch_jacobi(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur], L.vx[1 - cur], L.vy[1 - cur],
+                                  tile_rhs(t, l, fine), D.o.omega_v, zero_in && s == 0);
             }
+            if (two) { --pairs; s += 2; }
+            else s += 1;
             cur ^= 1;
             if ((st = exchange(D, l, FX_V, cur))) return st;
-        } else {
-            if (zero_in && s == 0)
-                for (int k = 0; k < D.nt; ++k) {
-                    Level &L = D.tile[k]->lev[l];
-                    CK(cudaMemsetAsync(L.vx[cur] - COL_OFF, 0, field_doubles(L.g) * 8, D.stream));
-                    CK(cudaMemsetAsync(L.vy[cur] - COL_OFF, 0, field_doubles(L.g) * 8, D.stream));
-                }
-            for (int comp = 0; comp < 2; ++comp)
-                for (int colour = 0; colour < 2; ++colour) {
-                    for (int k = 0; k < D.nt; ++k) {
-                        stokes_s *t = D.tile[k];
-                        Level &L = t->lev[l];
-                        launch_rbgs_phase(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur], tile_rhs(t, l, fine),
-                                          D.o.omega_v, comp, colour);
-                    }
-                    if ((st = exchange(D, l, FX_V, cur))) return st;
-                }
         }
+        return STOKES_OK;
+    }
+    for (int s = 0; s < n; ++s) {
+        if (zero_in && s == 0)
+            for (int k = 0; k < D.nt; ++k) {
+                Level &L = D.tile[k]->lev[l];
+                CK(cudaMemsetAsync(fstart(L.g, L.vx[cur]), 0, fsize(L.g) * 8, D.stream));
+                CK(cudaMemsetAsync(fstart(L.g, L.vy[cur]), 0, fsize(L.g) * 8, D.stream));
+            }
+        for (int comp = 0; comp < 2; ++comp)
+            for (int colour = 0; colour < 2; ++colour) {
+                for (int k = 0; k < D.nt; ++k) {
+                    stokes_s *t = D.tile[k];
+                    Level &L = t->lev[l];
+                    launch_rbgs_phase(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur], tile_rhs(t, l, fine),
+                                      D.o.omega_v, comp, colour);
+                }
+                if ((st = exchange(D, l, FX_V, cur))) return st;
+            }
     }
     return STOKES_OK;
 }
 
-// distributed V-cycle on level l (Eq. multigrid_levels); v in buffer 0
-int dvcycle(Dist &D, int l, bool fine, bool zero_in) {
-    int cur = 0, st;
+// distributed V-cycle on level l (Eq. multigrid_levels); v in buffer 0.
+// done_pre = 1: the first pre-smoothing sweep was done by the fused Uzawa pass into buffer 1.
+// The same launch sequence as the single-domain vcycle (driver.cu): an even pair count so the
+// 2 nu sweeps end in buffer 0, the residual fused with its restriction where the level streams.
+int dvcycle(Dist &D, int l, bool fine, bool zero_in, int done_pre = 0) {
+    int cur = done_pre ? 1 : 0, st;
     const int nu = D.tile[0]->lev[l].nu;
-    if ((st = dsmooth(D, l, cur, nu, zero_in, fine))) return st;               // (1)
-    for (int k = 0; k < D.nt; ++k) {                                            // (2)
-        stokes_s *t = D.tile[k];
-        Level &L = t->lev[l];
-        launch_residual(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur], tile_rhs(t, l, fine), L.rx, L.ry);
+    const GridL &g0 = D.tile[0]->lev[l].g;
+    const bool j2 = D.o.smoother == STOKES_SMOOTH_JACOBI && jacobi2_ok(g0);
+    const int pre_n = nu - done_pre;
+    int pre_pairs = j2 ? (pre_n - (zero_in && !done_pre ? 1 : 0)) / 2 : 0, post_pairs = j2 ? nu / 2 : 0;
+    if (pre_pairs < 0) pre_pairs = 0;
+    if ((pre_pairs + post_pairs) & 1) {
+        if (post_pairs > 0) --post_pairs;
+        else --pre_pairs;
     }
-    if ((st = exchange(D, l, FX_R, 0))) return st;
-    for (int k = 0; k < D.nt; ++k) {                                            // (3)
-        stokes_s *t = D.tile[k];
-        launch_restrict_vel(ctx(t), t->lev[l].g, t->lev[l + 1].g, t->lev[l].rx, t->lev[l].ry, t->lev[l + 1].bx,
-                            t->lev[l + 1].by);
+    if ((st = dsmooth(D, l, cur, pre_n, zero_in && !done_pre, fine, pre_pairs))) return st;  // (1)
+    if (jacobi2_ok(g0)) {  // (2) + (3): residual and restriction in one pass, then the coarse halos
+        for (int k = 0; k < D.nt; ++k) {
+            stokes_s *t = D.tile[k];
+            Level &L = t->lev[l], &C = t->lev[l + 1];
+            launch_residual_restrict(ctx(t), L.g, C.g, L.etab, L.etap, L.vx[cur], L.vy[cur], tile_rhs(t, l, fine), C.bx,
+                                     C.by);
+        }
+    } else {
+        for (int k = 0; k < D.nt; ++k) {
+            stokes_s *t = D.tile[k];
+            Level &L = t->lev[l];
+            launch_residual(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur], tile_rhs(t, l, fine), L.rx, L.ry);
+        }
+        if ((st = exchange(D, l, FX_R, 0))) return st;
+        for (int k = 0; k < D.nt; ++k) {
+            stokes_s *t = D.tile[k];
+            launch_restrict_vel(ctx(t), t->lev[l].g, t->lev[l + 1].g, t->lev[l].rx, t->lev[l].ry, t->lev[l + 1].bx,
+                                t->lev[l + 1].by);
+        }
     }
     if (l + 1 < D.La) {                                                         // (4)
+        if ((st = exchange(D, l + 1, FX_B, 0))) return st;  // the coarse right-hand side's halos
         if ((st = dvcycle(D, l + 1, false, true))) return st;
     } else {  // agglomerated coarse tail, redundant on every process
         if ((st = gather_to_tail(D, 0))) return st;
@@ -375,12 +446,12 @@ int dvcycle(Dist &D, int l, bool fine, bool zero_in) {
         launch_prolong(ctx(t), L.g, C.g, C.vx[0], C.vy[0], L.vx[cur], L.vy[cur]);
     }
     if ((st = exchange(D, l, FX_V, cur))) return st;
-    if ((st = dsmooth(D, l, cur, nu, false, fine))) return st;                 // (6)
+    if ((st = dsmooth(D, l, cur, nu, false, fine, post_pairs))) return st;      // (6)
     if (cur != 0) {
         for (int k = 0; k < D.nt; ++k) {
             Level &L = D.tile[k]->lev[l];
-            CK(cudaMemcpyAsync(L.vx[0] - COL_OFF, L.vx[cur] - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, D.stream));
-            CK(cudaMemcpyAsync(L.vy[0] - COL_OFF, L.vy[cur] - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, D.stream));
+            CK(cudaMemcpyAsync(fstart(L.g, L.vx[0]), fstart(L.g, L.vx[cur]), fsize(L.g) * 8, cudaMemcpyDeviceToDevice, D.stream));
+            CK(cudaMemcpyAsync(fstart(L.g, L.vy[0]), fstart(L.g, L.vy[cur]), fsize(L.g) * 8, cudaMemcpyDeviceToDevice, D.stream));
         }
     }
     return STOKES_OK;
@@ -396,10 +467,11 @@ int combine(Dist &D, bool write_mean) {
         loc[k] = D.tile[k]->scal + S_LOC;
         ms[k] = D.tile[k]->scal + S_MSHIFT;
     }
-    if (D.mode == M_NCCL)
-        if (ncclAllReduce(D.tile[0]->scal + S_LOC, D.tile[0]->scal + S_LOC, 3, ncclDouble, ncclSum, D.comm,
-                          D.stream) != ncclSuccess)
-            return STOKES_ENCCL;
+    if (D.mode == M_NCCL || self_nccl(D))  // (one rank: the sum over the tiles follows on the device)
+        for (int k = 0; k < D.nt; ++k)
+            if (ncclAllReduce(D.tile[k]->scal + S_LOC, D.tile[k]->scal + S_LOC, 3, ncclDouble, ncclSum, D.comm,
+                              D.stream) != ncclSuccess)
+                return STOKES_ENCCL;
     launch_dist_final(c, loc, D.nt, D.dscal + 3, 1.0 / ((double)D.NX * D.NY), D.dscal, ms, write_mean ? D.nt : 0);
     return STOKES_OK;
 }
@@ -450,6 +522,36 @@ int dist_body(Dist &D) {  // one Uzawa iteration reading pbuf[pcur]
     if ((st = exchange(D, 0, FX_P, 1 - D.pcur))) return st;
     CK(cudaMemcpyAsync(D.hsc, D.dscal, 8 * sizeof(double), cudaMemcpyDeviceToHost, D.stream));
     return STOKES_OK;
+}
+
+// a12 fusion on the tiles (as solve_uzawa_fused, driver.cu): from v^k (buffer 0) and
+// p^(k-1) = pbuf[pcur] one pass per tile computes p^k -> pbuf[1-pcur], the local sums of
+// E(v^k, p^k) and the first pre-smoothing sweep of V-cycle k+1 -> buffer 1; then the global
+// sums and the halos of (v', p^k)
+bool dist_fused_ok(const Dist &D) {
+    return D.o.smoother == STOKES_SMOOTH_JACOBI && D.o.vcycles_per_iter == 1 && D.tile[0]->lev[0].nu >= 1 &&
+           stream_ok(D.tile[0]->lev[0].g);
+}
+int dist_fused_tail(Dist &D) {
+    const double a_s = D.o.pressure_sign * D.o.alpha_p;
+    for (int k = 0; k < D.nt; ++k) {
+        stokes_s *t = D.tile[k];
+        Level &F = t->lev[0];
+        const LaunchCtx c = ctx(t);
+        launch_jacobi_uzawa(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], t->pbuf[D.pcur],
+                            t->pbuf[1 - D.pcur], t->rho, D.gx, D.gy, a_s, t->scal + S_MSHIFT, D.o.omega_v, t->partials);
+        launch_finalize(c, t->partials, stream_blocks(F.g), 3, 1.0, t->scal + S_LOC);
+    }
+    int st;
+    if ((st = combine(D, true))) return st;
+    if ((st = exchange(D, 0, FX_VP, 1 | ((1 - D.pcur) << 1)))) return st;
+    CK(cudaMemcpyAsync(D.hsc, D.dscal, 8 * sizeof(double), cudaMemcpyDeviceToHost, D.stream));
+    return STOKES_OK;
+}
+int dist_fused_body(Dist &D) {  // the rest of V-cycle k+1 (first sweep in buffer 1), then the fused tail
+    int st;
+    if ((st = dvcycle(D, 0, true, false, 1))) return st;
+    return dist_fused_tail(D);
 }
 
 int dsync(Dist &D) {
@@ -592,7 +694,7 @@ int dist_destroy(Dist *D) {
     drop(*D);
     for (int k = 0; k < D->nt; ++k) free_handle(D->tile[k]);
     free_handle(D->tail);
-    if (D->mode == M_NCCL && D->comm) ncclCommDestroy(D->comm);
+    if ((D->mode == M_NCCL || D->mode == M_NCCL_SELF) && D->comm) ncclCommDestroy(D->comm);
     for (int k = 0; k < MAXT; ++k) {
         if (D->sb[k]) cudaFree(D->sb[k]);
         if (D->rb[k]) cudaFree(D->rb[k]);
@@ -694,9 +796,9 @@ int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *ite
         *Eout = 0.0;
         for (int q = 0; q < D->nt; ++q) {
             stokes_s *t = D->tile[q];
-            CK(cudaMemsetAsync(t->lev[0].vx[0] - COL_OFF, 0, field_doubles(t->lev[0].g) * 8, D->stream));
-            CK(cudaMemsetAsync(t->lev[0].vy[0] - COL_OFF, 0, field_doubles(t->lev[0].g) * 8, D->stream));
-            CK(cudaMemsetAsync(t->pbuf[0] - COL_OFF, 0, field_doubles(t->lev[0].g) * 8, D->stream));
+            CK(cudaMemsetAsync(fstart(t->lev[0].g, t->lev[0].vx[0]), 0, fsize(t->lev[0].g) * 8, D->stream));
+            CK(cudaMemsetAsync(fstart(t->lev[0].g, t->lev[0].vy[0]), 0, fsize(t->lev[0].g) * 8, D->stream));
+            CK(cudaMemsetAsync(fstart(t->lev[0].g, t->pbuf[0]), 0, fsize(t->lev[0].g) * 8, D->stream));
             CK(cudaMemsetAsync(t->scal + S_MSHIFT, 0, 8, D->stream));
         }
     } else {
@@ -705,6 +807,7 @@ int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *ite
         if (E0 > rtol) {
             status = STOKES_NOT_CONVERGED;
             const int keep = D->pcur;
+            const bool fused = dist_fused_ok(*D);
             for (int q = 0; q < 2; ++q) {  // capture one iteration per pressure parity
                 if (D->exec[q]) continue;
                 D->pcur = q;
@@ -712,7 +815,7 @@ int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *ite
                 cudaGraph_t graph;
                 const long long before = dist_launches(D, 0);
                 CK(cudaStreamBeginCapture(D->stream, cudaStreamCaptureModeThreadLocal));
-                int bst = dist_body(*D);
+                int bst = fused ? dist_fused_body(*D) : dist_body(*D);
                 cudaError_t e = cudaStreamEndCapture(D->stream, &graph);
                 D->pcur = keep;
                 for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = keep;
@@ -724,17 +827,36 @@ int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *ite
                 cudaGraphDestroy(graph);
                 if (e != cudaSuccess) { D->exec[q] = nullptr; return fail_cuda(e, "dist graph instantiate"); }
             }
-            for (k = 1; k <= D->o.max_iter; ++k) {
-                CK(cudaGraphLaunch(D->exec[D->pcur], D->stream));
-                D->pcur ^= 1;
-                for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = D->pcur;
-                D->launches += D->body_kernels;
-                if ((st = dsync(*D))) return st;
-                E = D->hsc[0];
-                if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
-                if (E <= rtol) { status = STOKES_OK; break; }
+            if (fused && D->o.max_iter >= 1) {
+                // iteration 1: a full V-cycle from (v^0, p^0), then the fused tail of iterate 1;
+                // iteration k+1: the captured rest of V-cycle k+1 + the fused tail
+                if ((st = dvcycle(*D, 0, true, false))) return st;
+                if ((st = dist_fused_tail(*D))) return st;
+                for (k = 1;; ) {
+                    D->pcur ^= 1;  // pbuf[pcur] = p^k
+                    for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = D->pcur;
+                    if ((st = dsync(*D))) return st;
+                    E = D->hsc[0];
+                    if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+                    if (E <= rtol) { status = STOKES_OK; break; }
+                    if (k >= D->o.max_iter) break;
+                    ++k;
+                    CK(cudaGraphLaunch(D->exec[D->pcur], D->stream));
+                    D->launches += D->body_kernels;
+                }
+            } else {
+                for (k = 1; k <= D->o.max_iter; ++k) {
+                    CK(cudaGraphLaunch(D->exec[D->pcur], D->stream));
+                    D->pcur ^= 1;
+                    for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = D->pcur;
+                    D->launches += D->body_kernels;
+                    if ((st = dsync(*D))) return st;
+                    E = D->hsc[0];
+                    if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+                    if (E <= rtol) { status = STOKES_OK; break; }
+                }
+                if (k > D->o.max_iter) k = D->o.max_iter;
             }
-            if (k > D->o.max_iter) k = D->o.max_iter;
         }
         *iters = k;
         *Eout = E;
@@ -773,7 +895,7 @@ int stokes_nccl_unique_id(void *id128) {
 int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], int px, int py, int rank,
                        const void *nccl_unique_id, const stokes_opts *opts, void *cuda_stream, stokes_t *out) {
     if (!out || px < 1 || py < 1 || px * py > MAXT || nx % px || ny % py || !bc) return STOKES_EINVAL;
-    if (rank >= px * py || rank < -2 || (rank >= 0 && !nccl_unique_id)) return STOKES_EINVAL;
+    if (rank >= px * py || rank < -3 || (rank >= 0 && !nccl_unique_id)) return STOKES_EINVAL;
     if (opts && (opts->theta_step > 0.0 || opts->accel == STOKES_ACCEL_ANDERSON || opts->smoother >= 2))
         return STOKES_EINVAL;  // viscosity rescaling, Anderson, RAS / Mixed: single domain only
     Dist *D = (Dist *)calloc(1, sizeof(Dist));
@@ -793,7 +915,7 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
     for (int k = 0; k < 4; ++k)
         if (bc[k] != 0 && bc[k] != 1) { free(D); return STOKES_EINVAL; }
     D->rank = rank;
-    D->mode = rank >= 0 ? M_NCCL : (rank == -2 ? M_LOOPBACK : M_VIRTUAL);
+    D->mode = rank >= 0 ? M_NCCL : (rank == -2 ? M_LOOPBACK : (rank == -3 ? M_NCCL_SELF : M_VIRTUAL));
     // global hierarchy and the agglomeration level (tile levels while the tile is >= dmin)
     GridL gs[MAXLEV];
     int nus[MAXLEV];
@@ -831,6 +953,13 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
         memcpy(&id, nccl_unique_id, sizeof(id));
         if (ncclCommInitRank(&D->comm, px * py, id, rank) != ncclSuccess) { free(D); return STOKES_ENCCL; }
     }
+    if (D->mode == M_NCCL_SELF) {  // a one-rank communicator: every halo goes through ncclSend / ncclRecv to self
+        ncclUniqueId id;
+        if (ncclGetUniqueId(&id) != ncclSuccess || ncclCommInitRank(&D->comm, 1, id, 0) != ncclSuccess) {
+            free(D);
+            return STOKES_ENCCL;
+        }
+    }
     for (int k = 0; k < D->nt; ++k)
         if ((st = make_tile(*D, D->tx[k], D->ty[k], &D->tile[k]))) { dist_destroy(D); return st; }
     // the coarse tail: global level La
@@ -842,9 +971,12 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
     for (int l = 0; l < tail->nlev; ++l) tail->lev[l].nu = (int)floor(D->o.nu1 * pow(D->o.nu_growth, (double)(La + l)) + 0.5);
     if (D->tail->nlev + La != D->L) { dist_destroy(D); return STOKES_EINVAL; }
     const GridL &gf = D->tile[0]->lev[0].g, &gc = D->tile[0]->lev[La].g;
-    D->nbuf = 4 * (size_t)(gf.ncy + 2) + 4 * (size_t)(gc.ncy + 1) * (gc.ncx + 1) * (size_t)(px * py) + 64;
+    // packed halo columns: 2 sides x 3 fields x HW columns x (ncy + 2 HW) rows; agglomeration blocks
+    const size_t nhalo = 2 * 3 * HW * (size_t)(gf.ncy + 2 * HW);
+    const size_t nagg = 2 * (size_t)(gc.ncy + 1) * (gc.ncx + 1) * (size_t)(px * py);
+    D->nbuf = (nhalo > nagg ? nhalo : nagg) + 64;
     bool okm = cudaMalloc(&D->dscal, 64 * 8) == cudaSuccess && cudaMallocHost(&D->hsc, 64 * 8) == cudaSuccess;
-    const int nbufs = D->mode == M_LOOPBACK ? D->nt : 1;
+    const int nbufs = (D->mode == M_LOOPBACK || D->mode == M_NCCL_SELF) ? D->nt : 1;
     for (int k = 0; k < nbufs && okm; ++k)
         okm = cudaMalloc(&D->sb[k], D->nbuf * 8) == cudaSuccess && cudaMalloc(&D->rb[k], D->nbuf * 8) == cudaSuccess;
     if (!okm) {

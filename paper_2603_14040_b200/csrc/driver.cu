@@ -38,7 +38,8 @@ GridL make_grid(int ncx, int ncy, double Lx, double Ly, const int bc[4]) {
     GridL g;
     g.ncx = ncx;
     g.ncy = ncy;
-    g.P = (int)round_up((size_t)ncx + 2 + COL_OFF, 32);
+    // columns -1 .. ncx+2 inside the row (width-2 halos of decomposed tiles)
+    g.P = (int)round_up((size_t)ncx + 3 + COL_OFF, 32);
     g.dx = Lx / ncx;
     g.dy = Ly / ncy;
     g.idx = 1.0 / g.dx;
@@ -58,8 +59,10 @@ GridL make_grid(int ncx, int ncy, double Lx, double Ly, const int bc[4]) {
     g.par = 0;
     return g;
 }
-// + 512 doubles of tail: row-segment bulk copies of the last CTA may run past the last row
-size_t field_doubles(const GridL &g) { return (size_t)(g.ncy + 2) * (size_t)g.P + 512; }
+// rows 0 .. ncy+2 (+ 512 doubles of tail: row-segment bulk copies of the last CTA may run past
+// the last row); the Carver places one more row (row -1) in front of every field.  Rows -1
+// and ncy+2 are the second halo ring of decomposed tiles (width-2 halos).
+size_t field_doubles(const GridL &g) { return (size_t)(g.ncy + 3) * (size_t)g.P + 512; }
 int n_unknowns(const GridL &g) { return g.ncy * (g.ncx - 1) + (g.ncy - 1) * g.ncx; }
 
 // hierarchy (reading R8): factor 2 while both even and min/2 >= coarse_min
@@ -520,6 +523,7 @@ int solve_uzawa(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
         st = sync(h);
         if (st) return st;
         E = h->hscal[S_E];
+        record_E(h, k - 1, E);
         if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
         if (E <= rtol) { status = STOKES_OK; break; }
     }
@@ -590,6 +594,7 @@ int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *E
         int st = sync(h);
         if (st) return st;
         E = h->hscal[S_E];
+        record_E(h, k - 1, E);
         if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
         if (E <= rtol) { status = STOKES_OK; break; }
         if (k >= h->o.max_iter) break;
@@ -671,6 +676,7 @@ int solve_gcr_fused(stokes_s *h, double rtol, double E0, int *iters, double *Eou
             ++k;
             const double nu2 = h->hscal[S_NU2], rr = h->hscal[S_RR];
             E = h->hscal[S_E];
+            record_E(h, k - 1, E);
             if (!(nu2 > 1e-28 * rr)) { status = STOKES_EDIVERGED; break; }  // breakdown (R13)
             if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
             if (E <= rtol) {  // exit test on the true residual (R13): else restart from it
@@ -752,6 +758,7 @@ int solve_gcr(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
             ++k;
             const double nu2 = h->hscal[S_NU2], rr = h->hscal[S_RR];
             E = h->hscal[S_E];
+            record_E(h, k - 1, E);
             if (!(nu2 > 1e-28 * rr)) { status = STOKES_EDIVERGED; break; }  // breakdown (R13)
             if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
             if (E <= rtol) {  // exit test on the true residual (R13): else restart from it
@@ -1061,6 +1068,19 @@ int stokes_vcycle(stokes_t h, const double *bx, const double *by, double *vx, do
     return sync(h);
 }
 
+int stokes_solve_hist(stokes_t h, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy,
+                      double *hist, int hist_len) {
+    DEVICE_GUARD(h);
+    if (!h || hist_len < 0 || (hist_len > 0 && !hist) || h->dist) return STOKES_EINVAL;
+    h->hist = hist_len > 0 ? hist : nullptr;
+    h->hist_len = hist_len;
+    h->hist_off = 0;
+    const int st = stokes_solve(h, rtol, vx, vy, p, iters, rel_energy);
+    h->hist = nullptr;
+    h->hist_len = 0;
+    return st;
+}
+
 int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy) {
     DEVICE_GUARD(h);
     if (!h || !vx || !vy || !p || !iters || !rel_energy || !(rtol >= 0)) return STOKES_EINVAL;
@@ -1142,6 +1162,7 @@ int solve_anderson(stokes_s *h, double rtol, double E0, int *iters, double *Eout
         h->launches += h->uzawa_kernels;
         if ((st = sync(h))) return st;
         E = h->hscal[S_E];
+        record_E(h, k, E);
         if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
         if (E <= rtol) { status = STOKES_OK; break; }
         const int slot = k % ns, mk = k < m ? k : m;
@@ -1192,6 +1213,7 @@ int solve_staged(stokes_s *h, double rtol, int *iters, double *Eout) {
         if ((st = set_theta(h, theta))) return st;
         if ((st = energy_now(h, &E0))) return st;
         h->o.max_iter = budget - used < h->o.theta_every ? budget - used : h->o.theta_every;
+        h->hist_off = used;
         status = solve_inner(h, -1.0, E0, &it, &E);
         h->o.max_iter = budget;
         if (status < 0 && status != STOKES_EDIVERGED) return status;
@@ -1206,6 +1228,7 @@ int solve_staged(stokes_s *h, double rtol, int *iters, double *Eout) {
             status = STOKES_OK;
         } else {
             h->o.max_iter = budget - used;
+            h->hist_off = used;
             status = solve_inner(h, rtol, E0, &it, &E);
             h->o.max_iter = budget;
             if (status < 0 && status != STOKES_EDIVERGED) return status;

@@ -69,6 +69,8 @@ struct stokes_s {
     void *mk_ws;        // marker-in-cell scratch (markers.cu), grown on demand
     size_t mk_bytes;
     struct Dist *dist;  // non-null: a 2D-decomposed handle (all calls dispatch to dist_*)
+    double *hist;       // stokes_solve_hist: host buffer of E after every iteration (or null)
+    int hist_len, hist_off;
 };
 
 
@@ -101,9 +103,9 @@ struct Carver {  // bump allocator over the workspace (256-B granules)
         off += ndoubles * sizeof(double);
         return p;
     }
-    double *field(const GridL &g) {
-        double *a = take(field_doubles(g));
-        return dry ? nullptr : a + COL_OFF;
+    double *field(const GridL &g) {  // row -1 .. ncy+2 + tail; returns &(0, 0)
+        double *a = take(field_doubles(g) + g.P);
+        return dry ? nullptr : a + g.P + COL_OFF;
     }
 };
 int check_opts(const stokes_opts &o);
@@ -122,6 +124,10 @@ void ras_iteration_end(stokes_s *h);    // after them (advances the device itera
 void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in,
             int done_pre = 0);
 int sync(stokes_s *h);
+inline void record_E(stokes_s *h, int k, double E) {  // E after iteration k + 1 of the current solve stage
+    const int q = h->hist_off + k;
+    if (h->hist && q >= 0 && q < h->hist_len) h->hist[q] = E;
+}
 int build_hierarchy(stokes_s *h);
 int solve_inner(stokes_s *h, double rtol, double E0, int *iters, double *E);
 int solve_anderson(stokes_s *h, double rtol, double E0, int *iters, double *E);

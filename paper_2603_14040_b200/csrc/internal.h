@@ -3,8 +3,9 @@
 // Data layout in HBM: every staggered field of a level is one FP64 array
 // on the paper's padded index space (ncy+2) x (ncx+2) (basic / boundary
 // B / ghost G nodes), row pitch P doubles (multiple of 32 = 256 B), element (i, j) at
-// base[i * P + j].  base = allocation + COL_OFF so that interior column 1 is 256-B
-// aligned: a warp reading columns 1..32 of a row touches exactly two 128-B lines.
+// base[i * P + j].  base = allocation + P + COL_OFF so that interior column 1 is 256-B
+// aligned: a warp reading columns 1..32 of a row touches exactly two 128-B lines.  Rows -1
+// and ncy+2 and columns -1 and ncx+2 also exist: the second halo ring of decomposed tiles.
 #pragma once
 #include <cuda_runtime.h>
 #include <stddef.h>

@@ -1074,7 +1074,7 @@ void launch_restrict_p(const LaunchCtx &c, const GridL &gf, const GridL &gc, con
 }
 void launch_prolong(const LaunchCtx &c, const GridL &gf, const GridL &gc, const double *exc, const double *eyc,
                     double *vx, double *vy) {
-    if (gf.ncx % 2 == 0 && gf.bW && gf.bE && gf.bN && gf.bS) {  // single domain: paired columns
+    if (gf.ncx % 2 == 0) {  // paired columns (single domain and decomposed tiles)
         const dim3 grid((gf.ncx / 2 + BX - 1) / BX, (gf.ncy + BY - 1) / BY);
         k_prolong2<<<grid, tpb(), 0, c.stream>>>(gf, gc, exc, eyc, vx, vy);
     } else {

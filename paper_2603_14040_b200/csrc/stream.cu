@@ -544,8 +544,8 @@ void fill_src(const double **src, const double *vx, const double *vy, const doub
 // by one sweep-1 row.  The fields are read once and written once per two sweeps: the same
 // 64 B/cell as one sweep.  Mirror ghosts of the intermediate iterate are applied when
 // sweep 2 reads them, walls are copied through: exactly the arithmetic of two JacobiOp
-// sweeps.  Single-domain levels only (a decomposed tile's halo would be stale after the
-// first sweep).  (A warp-specialised variant exchanging the intermediate iterate by warp
+// sweeps.  On decomposed tiles sweep 1 also updates the first halo ring from the second
+// (width-2 halos exchanged once per pass).  (A warp-specialised variant exchanging the intermediate iterate by warp
 // shuffles, without CTA barriers, measured 435 us vs 340 us for this one at 4096^2.)
 // the two-sweep pass runs wider CTAs: 320 threads (10 warps, 2 CTAs = 20 warps per SM at
 // 96 registers), a 6-row ring of 324-wide rows (114 KB per CTA)
@@ -638,7 +638,11 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
     const int c = j0 - 1 + t;  // sweep-1 column of this thread (= sweep-2 column for 1 <= t <= tw)
     const int i0 = 1 + blockIdx.y * H;
     const int i1 = min(i0 + H - 1, g.ncy);
-    const int rlo = max(i0 - 2, 0), rhi = min(i1 + 2, g.ncy + 1);
+    // decomposed tiles: on a side that is no global boundary the first halo
+    // ring holds the neighbour's unknowns; sweep 1 updates it too (from the second ring),
+    // so that sweep 2 of the tile's own unknowns is exact.  Global sides: mirrors / walls.
+    const int hN = !g.bN, hS = !g.bS, hW = !g.bW, hE = !g.bE;
+    const int rlo = max(i0 - 2, -hN), rhi = min(i1 + 2, g.ncy + 1 + hS);
     const int sfirst = max(i0 - 1, 0), slast = min(i1 + 1, g.ncy + 1);
     const size_t P = g.P;
     auto issue = [&](int r) {
@@ -703,7 +707,7 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
         __syncthreads();
         refill(rlo);
     }
-    const bool cx_in = c >= 1 && c <= g.nvxj, cy_in = c >= 1 && c <= g.ncx;
+    const bool cx_in = c >= 1 - hW && c <= g.nvxj + hE, cy_in = c >= 1 - hW && c <= g.ncx + hE;
     // 1/a_ii and right-hand side of sweep-1 row s-1 (= the sweep-2 row): equal in both sweeps
     double iax = 0.0, iay = 0.0, bxp = 0.0, byp = 0.0, lag_eb = 0.0;
     // one row step s: sweep 1 of row s, sweep 2 of row s-1.  EDGE = false (CTAs whose rows
@@ -715,13 +719,13 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
         const W1 w{&v};
         // ---- sweep 1, row s
         double vx1 = v.B[F_VX].c, vy1 = v.B[F_VY].c, iax_n = 0.0, iay_n = 0.0, bx_n = 0.0, by_n = 0.0;
-        if (!EDGE || (s >= 1 && s <= g.ncy && cx_in)) {
+        if (!EDGE || (s >= 1 - hN && s <= g.ncy + hS && cx_in)) {
             const RowX x = lx_win<EDGE>(g, w, s);
             bx_n = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
             iax_n = rcp(x.a);
             vx1 = w.B(F_VX) + a.omega * (bx_n - x.L) * iax_n;
         }
-        if (!EDGE || (s >= 1 && s <= g.nvyi && cy_in)) {
+        if (!EDGE || (s >= 1 - hN && s <= g.nvyi + hS && cy_in)) {
             const RowX y = ly_win<EDGE>(g, w, c);
             by_n = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
             iay_n = rcp(y.a);
@@ -787,7 +791,6 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
 // b^H(I, .) for the tw/2 coarse columns it owns with the normalised weights of
 // k_restrict_vel (Appendix B; rows / columns outside the domain dropped and renormalised).
 // The fine residual never reaches HBM: 48 B/fine cell read + 4 B written instead of 84.
-// Single-domain levels only (jacobi2_ok).
 #ifndef RR_NS
 #define RR_NS 6
 #endif
@@ -815,7 +818,10 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
     const int c = j0 - 1 + t;
     const int I0 = 1 + blockIdx.y * HC;
     const int I1 = min(I0 + HC - 1, gc.ncy);
-    const int ilo = max(2 * I0 - 2, 1), ihi = min(2 * I1 + 1, g.ncy);
+    // decomposed tiles: the residual is also evaluated on the first halo ring of non-global
+    // sides (from the second ring), where the restriction weights reach
+    const int hN = !g.bN, hS = !g.bS, hW = !g.bW, hE = !g.bE;
+    const int ilo = max(2 * I0 - 2, 1 - hN), ihi = min(2 * I1 + 1, g.ncy + hS);
     const int rlo = ilo - 1, rhi = ihi + 1;
     const size_t P = g.P;
     auto issue = [&](int r) {
@@ -850,7 +856,7 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
     __syncthreads();
     refill(rlo);
     refill(rlo + 1);
-    const bool cx_in = c >= 1 && c <= g.nvxj, cy_in = c >= 1 && c <= g.ncx;
+    const bool cx_in = c >= 1 - hW && c <= g.nvxj + hE, cy_in = c >= 1 - hW && c <= g.ncx + hE;
     // emit phase: threads [0, tw/2) restrict vx, threads [tw/2, tw) restrict vy (one coarse
     // value each, so no half of the CTA idles at the next barrier)
     const int half = a.tw / 2;
@@ -863,7 +869,7 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
             const double b = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
             rx = b - lx_win(g, w, i).L;
         }
-        if (cy_in && i <= g.nvyi) {
+        if (cy_in && i <= g.nvyi + hS) {
             const double b = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
             ry = b - ly_win(g, w, c).L;
         }
@@ -871,7 +877,8 @@ __global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRA
         rr[((i % RRR) * 2 + 1) * TW + t] = ry;
         __syncthreads();
         refill(i + 1);
-        const int I = (i & 1) ? (i - 1) / 2 : (i == g.ncy ? i / 2 : 0);  // coarse row completed by row i
+        // coarse row completed by fine row i (global S side: row ncy + 1 is dropped)
+        const int I = (i & 1) ? (i - 1) / 2 : ((i == g.ncy && g.bS) ? i / 2 : 0);
         if (I >= I0 && I <= I1) {
             if (emit_x) {  // vx: x vertex-centred [1/2, 1, 1/2], y cell-centred [1/4, 3/4, 3/4, 1/4]
                 const int q = 2 * J - (j0 - 1);  // ring column of fine column 2J
@@ -1044,7 +1051,9 @@ int stream_blocks(const GridL &g) {
     return (int)(gr.x * gr.y);
 }
 
-bool jacobi2_ok(const GridL &g) { return stream_ok(g) && g.bN && g.bS && g.bW && g.bE; }
+// two-sweep pass / fused residual+restriction: single domains and decomposed tiles whose
+// width-2 halos are current (dist.cu exchanges them after every pass)
+bool jacobi2_ok(const GridL &g) { return stream_ok(g); }
 
 void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
                     const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega) {

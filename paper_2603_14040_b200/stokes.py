@@ -88,6 +88,7 @@ def lib(build_if_missing=True):
         "stokes_residual": [P, P, P, P, P, P, P, pd],
         "stokes_vcycle": [P, P, P, P, P],
         "stokes_solve": [P, D, P, P, P, pi, pd],
+        "stokes_solve_hist": [P, D, P, P, P, pi, pd, pd, I],
         "stokes_smooth": [P, I, P, P, P, P, I],
         "stokes_level_residual": [P, I, P, P, P, P, P, P],
         "stokes_restrict": [P, I, I, P, P],
@@ -118,7 +119,7 @@ def lib(build_if_missing=True):
 
 EXPORTED = ["stokes_opts_default", "stokes_workspace_bytes", "stokes_create", "stokes_destroy",
             "stokes_num_levels", "stokes_level_shape", "stokes_set_viscosity", "stokes_set_density",
-            "stokes_set_gravity", "stokes_apply_operator", "stokes_residual", "stokes_vcycle", "stokes_solve",
+            "stokes_set_gravity", "stokes_apply_operator", "stokes_residual", "stokes_vcycle", "stokes_solve", "stokes_solve_hist",
             "stokes_smooth", "stokes_level_residual", "stokes_restrict", "stokes_prolong",
             "stokes_get_viscosity", "stokes_coarse_solve", "stokes_launch_count", "stokes_time_kernel",
             "stokes_strerror", "stokes_last_error", "stokes_create_dist", "stokes_nccl_unique_id",
@@ -274,10 +275,11 @@ class Stokes:
         _check(lib().stokes_vcycle(self._h, *map(self._p, (bx, by, vx, vy))), "vcycle")
         return vx, vy
 
-    def solve(self, rtol, vx=None, vy=None, p=None, out=None):
-        """Solve to E <= rtol.  Returns dict(vx, vy, p, iters, E, status).  If the initial
-        guess tensors are on the CPU (e.g. pinned), they are copied in and the solution is
-        copied back to CPU tensors (`out` may supply pinned output buffers)."""
+    def solve(self, rtol, vx=None, vy=None, p=None, out=None, hist_len=0):
+        """Solve to E <= rtol.  Returns dict(vx, vy, p, iters, E, status[, hist]).  If the
+        initial guess tensors are on the CPU (e.g. pinned), they are copied in and the solution
+        is copied back to CPU tensors (`out` may supply pinned output buffers).  hist_len > 0:
+        also the energy residual after every iteration (stokes_solve_hist)."""
         sh = shapes(self.nx, self.ny)
         given = [t for t in (vx, vy, p) if t is not None]
         host = bool(given) and not (torch.is_tensor(given[0]) and given[0].is_cuda)
@@ -292,11 +294,18 @@ class Stokes:
             dvx, dvy, dp = guess(vx, "vx"), guess(vy, "vy"), guess(p, "p")
         it, e = ctypes.c_int(), ctypes.c_double()
         self._sync_inputs()
-        st = lib().stokes_solve(self._h, float(rtol), *map(self._p, (dvx, dvy, dp)), ctypes.byref(it),
-                                ctypes.byref(e))
+        if hist_len:
+            hbuf = (ctypes.c_double * hist_len)()
+            st = lib().stokes_solve_hist(self._h, float(rtol), *map(self._p, (dvx, dvy, dp)), ctypes.byref(it),
+                                         ctypes.byref(e), hbuf, hist_len)
+        else:
+            st = lib().stokes_solve(self._h, float(rtol), *map(self._p, (dvx, dvy, dp)), ctypes.byref(it),
+                                    ctypes.byref(e))
         if st < 0 and st != EDIVERGED:
             _check(st, "solve")
         res = {"vx": dvx, "vy": dvy, "p": dp, "iters": it.value, "E": e.value, "status": st}
+        if hist_len:
+            res["hist"] = list(hbuf)[: min(it.value, hist_len)]
         if host:
             with torch.cuda.stream(self.stream):
                 for k in ("vx", "vy", "p"):
@@ -463,7 +472,8 @@ class StokesDist(Stokes):
     rank=None: all px*py tiles in this process on one GPU, arrays are the GLOBAL user-layout
     arrays; transport="virtual" copies halo strips between the tiles directly,
     transport="loopback" runs the NCCL code path's packing / unpacking with device copies
-    in place of ncclSend/Recv/AllGather (tests of the multi-GPU path on one B200).
+    in place of ncclSend/Recv/AllGather; transport="nccl_self" sends every packed halo through
+    real ncclSend / ncclRecv on a one-rank communicator (tests of the multi-GPU path on one B200).
     rank=r (with torch.distributed initialised): NCCL decomposition, one tile per process;
     arrays are the tile windows (`tile_windows`).  The NCCL unique id is created on rank 0
     and broadcast with torch.distributed (the process group is plumbing only)."""
@@ -487,7 +497,7 @@ class StokesDist(Stokes):
             self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
             self._h = ctypes.c_void_p()
             bcs = (ctypes.c_int * 4)(*self.bc)
-            code = rank if rank is not None else {"virtual": -1, "loopback": -2}[transport]
+            code = rank if rank is not None else {"virtual": -1, "loopback": -2, "nccl_self": -3}[transport]
             _check(lib().stokes_create_dist(nx, ny, float(Lx), float(Ly), bcs, px, py, code,
                                             uid, ctypes.byref(self.opts), ctypes.c_void_p(self.stream.cuda_stream),
                                             ctypes.byref(self._h)), "create_dist")

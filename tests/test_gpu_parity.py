@@ -285,8 +285,8 @@ def test_anderson_parity(S, name, n, opts):
     """Anderson AA(m, beta) (Alg. 5, reading R26).  Its iteration count is sensitive to
     rounding through the least squares: the ORACLE itself moves from 98 to 91 iterations on
     block 64^2 (m 5, beta .7) when rho is perturbed by 1e-15 relative.  So: the first 12
-    iterates agree to 1e-8, the counts to 10 %, and the converged solutions (unique fixed
-    point) to 1e-9."""
+    iterates agree to 1e-8, the count within twice the oracle's own spread over four such
+    perturbations (at least +-1), and the converged solutions (unique fixed point) to 1e-9."""
     opts = dict(opts, omega_v=0.6, alpha_p=1.0, accel=2)
     w = workload(name, n, n)
     args = (S, n, n, w["bc"], w, w["Lx"], w["Ly"], (w["gx"], w["gy"]))
@@ -300,9 +300,15 @@ def test_anderson_parity(S, name, n, opts):
     assert a["status"] == 0 and b["status"] == 0
     # count band = the oracle's own spread under a rounding-level input change (the
     # least-squares history is ill-conditioned near convergence), at least +-1
-    w2 = dict(w, rho_b=w["rho_b"] * (1.0 + 1e-15 * np.random.default_rng(99).standard_normal(w["rho_b"].shape)))
-    o2, _ = pair(S, n, n, w["bc"], w2, w["Lx"], w["Ly"], (w["gx"], w["gy"]), **opts)
-    band = max(1, 2 * abs(o2.solve(1e-8)["iters"] - a["iters"]))
+    spread = 0
+    for seed in range(4):
+        w2 = dict(w, rho_b=w["rho_b"] * (1.0 + 1e-15 * np.random.default_rng(seed).standard_normal(w["rho_b"].shape)))
+        o2 = Oracle(n, n, w["Lx"], w["Ly"], w["bc"], **opts)
+        o2.set_viscosity(w2["eta_b"], w2["eta_p"])
+        o2.set_density(w2["rho_b"])
+        o2.set_gravity(w["gx"], w["gy"])
+        spread = max(spread, abs(o2.solve(1e-8)["iters"] - a["iters"]))
+    band = max(1, 2 * spread)
     assert abs(a["iters"] - b["iters"]) <= band, (a["iters"], b["iters"], band)
     a, b = o.solve(1e-11), s.solve(1e-11)
     for key in ("vx", "vy", "p"):

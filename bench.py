@@ -240,6 +240,60 @@ def run_reference(args, world, rank):
     return 0
 
 
+def run_strong(args, world, rank, local, steps, warmup):
+    """BASELINE config 5: the random log-perturbed viscosity problem at its preset size
+    (16384^2 cells) split over the N GPUs (strong scaling; N = 1: one domain).  Inputs are
+    sampled on the device (synth.fields.random_torch, same recipe as the parity fields).
+    Returns the timing block (device time, max over ranks)."""
+    import torch
+    from paper_2603_14040_b200 import Stokes, StokesDist
+    from paper_2603_14040_b200.decomp import strong_problem, tile_windows
+    from synth.fields import random_torch
+    dev = torch.device("cuda", local)
+    pre = presets()["random"]
+    rtol, opts = pre["rtol"], dict(pre["opts"])
+    NX, NY, Lx, Ly, px, py = strong_problem(world, pre["n"][0])
+    if world > 1:
+        win = tile_windows(NX, NY, px, py, rank)
+        i0, j0 = win["b"][0].start, win["b"][1].start
+        nxt, nyt = NX // px, NY // py
+        w = random_torch(NX, NY, Lx, Ly, win_b=(i0, j0, nyt + 1, nxt + 1), win_p=(i0, j0, nyt, nxt), device=dev)
+        s = StokesDist(NX, NY, Lx, Ly, w["bc"], px=px, py=py, rank=rank, **opts)
+    else:
+        w = random_torch(NX, NY, Lx, Ly, device=dev)
+        s = Stokes(NX, NY, Lx, Ly, w["bc"], **opts)
+    s.set_viscosity(w["eta_b"], w["eta_p"])
+    s.set_density(w["rho_b"])
+    s.set_gravity(w["gx"], w["gy"])
+    del w
+    per_vc = dof_sweeps_per_vcycle(global_levels(NX, NY, opts), opts.get("smoother", 0))
+    for _ in range(warmup):
+        s.solve(rtol)
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = []
+    s.launch_count(reset=True)
+    with Clocks(local) as clk:
+        e0.record(s.stream)
+        for _ in range(steps):
+            r = s.solve(rtol)
+            assert r["status"] == 0, f"strong-scaling solve status {r['status']}"
+            iters.append(r["iters"])
+        e1.record(s.stream)
+        torch.cuda.synchronize()
+    launches = s.launch_count()
+    barrier(world)
+    ms = allreduce_max(e0.elapsed_time(e1), world, dev)
+    s.close()
+    dofs = sum(iters) * opts.get("vcycles_per_iter", 1) * per_vc
+    return {"workload": f"random: {WORKLOAD_DOC['random']}, {NX}x{NY} cells split over {world} GPU(s)",
+            "grid_global": [NX, NY], "grid_per_gpu": [NX // px, NY // py], "parallelism": f"dd{px}x{py}",
+            "n_gpus": world, "steps": steps, "ms_per_solve": ms / steps, "iters_per_solve": statistics.mean(iters),
+            "value": dofs / (ms / 1e3), "unit": UNIT, "scaling": "strong", "gpu_launches": launches,
+            "clocks": clk.summary(), "data": "synthetic (sampled on the device, synth.fields.random_torch)"}
+
+
 def run_ours(args, world, rank, local):
     import torch
     from paper_2603_14040_b200 import Stokes, StokesDist
@@ -249,6 +303,19 @@ def run_ours(args, world, rank, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.scaling == "strong":  # the headline is BASELINE config 5 (strong scaling)
+        st = run_strong(args, world, rank, local, args.steps, args.warmup)
+        if rank == 0:
+            line = {"metric": METRIC, "value": st["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                    "warmup": args.warmup, "ms_per_step": st["ms_per_solve"], "higher_is_better": True,
+                    "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": st["data"],
+                    "config": {"workload": st["workload"], "grid_global": st["grid_global"],
+                               "grid_per_gpu": st["grid_per_gpu"], "parallelism": st["parallelism"],
+                               "iters_per_solve": st["iters_per_solve"],
+                               "l2": "inputs larger than L2 (16384^2 fields, 2.1 GB each)"},
+                    "gpu_launches": st["gpu_launches"], "clocks": st["clocks"]}
+            print(json.dumps(line), flush=True)
+        return 0
     pre = presets()[args.workload]
     rtol = pre["rtol"]
     opts = dict(pre["opts"])
@@ -366,7 +433,7 @@ def run_ours(args, world, rank, local):
     alt = None
     if world == 1 and args.workload == "layered":
         try:
-            del kh
+            kh = None
             aa = Stokes(NX, NY, w["Lx"], w["Ly"], w["bc"], **dict(opts, accel=2, aa_depth=10, aa_beta=1.0))
             aa.set_viscosity(eb, ep)
             aa.set_density(rho)
@@ -384,6 +451,16 @@ def run_ours(args, world, rank, local):
         except Exception as ex:  # informational only
             alt = {"error": str(ex)[:200]}
 
+    # ---- BASELINE config 5 beside the headline: the fixed 16384^2 random problem split over
+    # the same N GPUs (strong scaling; the driver's scaling run then yields both curves)
+    strong = None
+    if not args.no_strong:
+        kh = None
+        torch.cuda.empty_cache()
+        try:
+            strong = run_strong(args, world, rank, local, max(1, min(args.steps, 2)), 1)
+        except Exception as ex:  # reported, never silently dropped
+            strong = {"error": str(ex)[:300]}
     if rank != 0:
         return 0
     cb = cpu_baseline(args.workload, pre) if world == 1 and not args.no_cpu_baseline else None
@@ -414,6 +491,8 @@ def run_ours(args, world, rank, local):
         line["cpu_baseline"] = cb
     if alt is not None:
         line["accelerated"] = alt
+    if strong is not None:
+        line["strong_scaling"] = strong
     print(json.dumps(line), flush=True)
     return 0
 
@@ -442,6 +521,9 @@ def main():
     ap.add_argument("--workload", default="layered", choices=sorted(WORKLOAD_DOC))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: BASELINE cfg 4 per GPU (default); strong: cfg 5, 16384^2 split over N")
+    ap.add_argument("--no-strong", action="store_true", help="skip the cfg-5 strong-scaling block")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -37,3 +37,12 @@ def weak_problem(n_ranks, tile=4096):
     of unit tiles -> (NX, NY, Lx, Ly, px, py)."""
     px, py = process_grid(n_ranks)
     return tile * px, tile * py, float(px), float(py), px, py
+
+
+def strong_problem(n_ranks, n=16384):
+    """Strong scaling (BASELINE config 5): one fixed n x n unit-box problem split over the
+    px x py process grid -> (NX, NY, Lx, Ly, px, py)."""
+    px, py = process_grid(n_ranks)
+    if n % px or n % py:
+        raise ValueError("grid not divisible by the process grid")
+    return n, n, 1.0, 1.0, px, py

@@ -120,6 +120,40 @@ def _random_log_eta(y, x, modes):
     return acc / a.sum()
 
 
+def random_torch(nx, ny, Lx=1.0, Ly=1.0, win_b=None, win_p=None, device="cuda"):
+    """The cfg-5 `random` workload (same recipe and modes as workload("random", ...)) sampled
+    on the device with torch in FP64: log10 eta as the rank-2K product [cos(n y) sin(n y)]
+    diag(a) [cos(m x + phi) -sin(m x + phi)]^T, for full-size (16384^2) bench inputs that
+    numpy would need minutes for.  Equal to the numpy fields to rounding (not bit for bit)."""
+    import torch
+    a, m, n, phi = random_modes()
+    at = torch.tensor(a, dtype=torch.float64, device=device)
+    mt = torch.tensor(m, dtype=torch.float64, device=device)
+    nt = torch.tensor(n, dtype=torch.float64, device=device)
+    pt = torch.tensor(phi, dtype=torch.float64, device=device)
+
+    def coords(kind, win):
+        i0, j0, nyt, nxt = _win(win)
+        y, x = node_coords(kind, nx, ny, Lx, Ly, i0, j0, nyt, nxt)
+        return (torch.tensor(y, dtype=torch.float64, device=device),
+                torch.tensor(x, dtype=torch.float64, device=device))
+
+    def log_eta(y, x):
+        ty = 2 * math.pi * torch.outer(y, nt)
+        tx = 2 * math.pi * torch.outer(x, mt) + pt
+        Y = torch.cat([torch.cos(ty), torch.sin(ty)], 1) * torch.cat([at, at])
+        X = torch.cat([torch.cos(tx), -torch.sin(tx)], 1)
+        return (Y @ X.T) / float(a.sum())
+
+    yb, xb = coords("b", win_b)
+    yp, xp = coords("p", win_p)
+    eb = torch.pow(10.0, log_eta(yb, xb))
+    ep = torch.pow(10.0, log_eta(yp, xp))
+    rho = torch.outer(torch.sin(math.pi * yb), torch.cos(math.pi * xb))
+    return {"eta_b": eb.contiguous(), "eta_p": ep.contiguous(), "rho_b": rho.contiguous(), "gx": 0.0, "gy": 1.0,
+            "Lx": Lx, "Ly": Ly, "bc": (0, 0, 0, 0)}
+
+
 def workload(name, nx, ny, Lx=None, Ly=None, win_b=None, win_p=None):
     """Return dict(eta_b, eta_p, rho_b, gx, gy, Lx, Ly, bc) of a workload (global or tile windows)."""
     if name == "layered":

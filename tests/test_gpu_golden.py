@@ -58,12 +58,13 @@ def test_full_solve_matches_oracle_golden(S, path):
     assert gold["status"] == 0 and r["status"] == 0
     assert abs(r["iters"] - K) <= 1, (r["iters"], K)
     assert r["E"] <= rtol
-    # energy residual history: iteration by iteration on the oracle's trajectory (relative
-    # 1e-6: E is a residual norm, its rounding differences are relative to ||f||, not to E)
+    # energy residual history, iteration by iteration on the oracle's trajectory: E is a
+    # residual norm relative to ||f|| (E_0 = 1), so its rounding differences are absolute
+    # (~1e-14), i.e. relative 1e-6 once E ~ 1e-8: bar |dE_k| <= 1e-9 E_k + 1e-13
     h, hg = np.array(r["hist"]), np.array(gold["hist"])
     m = min(len(h), len(hg))
-    dev = np.abs(h[:m] - hg[:m]) / hg[:m]
-    assert dev.max() <= 1e-6, (int(dev.argmax()), float(dev.max()))
+    dev = np.abs(h[:m] - hg[:m]) - (1e-9 * hg[:m] + 1e-13)
+    assert dev.max() <= 0, (int(dev.argmax()), float(np.abs(h - hg[:len(h)]).max() if len(h) <= len(hg) else 0))
     # the fields at the oracle's count
     if r["iters"] != K:
         r = handle(max_iter=K).solve(0.0)

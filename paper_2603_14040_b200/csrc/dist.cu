@@ -50,6 +50,10 @@ struct Dist {
     stokes_s *tail;  // global level La and below
     cudaStream_t stream;
     bool own_stream;
+    cudaStream_t cstream;  // halo exchanges overlapped with the interior part of a pass
+    cudaStream_t xs;       // the stream exchange() enqueues on (stream, or cstream while overlapping)
+    cudaEvent_t ev[2];
+    bool overlap;
     double *dscal;   // [0] E [1] Sv [2] Sp [3] Sf [4] zero
     double *hsc;
     ncclComm_t comm;
@@ -69,7 +73,7 @@ enum { FX_V = 0, FX_R = 1, FX_P = 2, FX_ETA = 3, FX_RHO = 4, FX_B = 5, FX_VP = 6
 enum { M_VIRTUAL = 0, M_LOOPBACK = 1, M_NCCL = 2, M_NCCL_SELF = 3 };
 constexpr int HW = 2;  // halo width: the two-sweep pass and the fused residual+restriction read two rings
 
-LaunchCtx dctx(Dist &D) { return LaunchCtx{D.stream, &D.launches}; }
+LaunchCtx dctx(Dist &D) { return LaunchCtx{D.xs, &D.launches}; }
 bool packed(const Dist &D) { return D.mode != M_VIRTUAL; }
 bool self_nccl(const Dist &D) { return D.mode == M_NCCL_SELF; }
 
@@ -104,11 +108,11 @@ size_t fsize(const GridL &g) { return field_doubles(g) + g.P; }
 // real ncclSend / ncclRecv pair on the one-rank communicator (NCCL_SELF; caller groups)
 int p2p_local(Dist &D, double *dst, const double *src, size_t n) {
     if (self_nccl(D)) {
-        if (ncclSend(src, n, ncclDouble, 0, D.comm, D.stream) != ncclSuccess) return STOKES_ENCCL;
-        if (ncclRecv(dst, n, ncclDouble, 0, D.comm, D.stream) != ncclSuccess) return STOKES_ENCCL;
+        if (ncclSend(src, n, ncclDouble, 0, D.comm, D.xs) != ncclSuccess) return STOKES_ENCCL;
+        if (ncclRecv(dst, n, ncclDouble, 0, D.comm, D.xs) != ncclSuccess) return STOKES_ENCCL;
         return STOKES_OK;
     }
-    CK(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, D.stream));
+    CK(cudaMemcpyAsync(dst, src, n * 8, cudaMemcpyDeviceToDevice, D.xs));
     return STOKES_OK;
 }
 int group_start(Dist &D) {
@@ -191,12 +195,12 @@ int exchange(Dist &D, int l, int which, int idx) {
         if (D.mode == M_NCCL) {
             const int W = D.tx[0] > 0 ? D.rank - 1 : -1, E = D.tx[0] + 1 < D.px ? D.rank + 1 : -1;
             if (W >= 0) {
-                ncclSend(D.sb[0], part, ncclDouble, W, D.comm, D.stream);
-                ncclRecv(D.rb[0], part, ncclDouble, W, D.comm, D.stream);
+                ncclSend(D.sb[0], part, ncclDouble, W, D.comm, D.xs);
+                ncclRecv(D.rb[0], part, ncclDouble, W, D.comm, D.xs);
             }
             if (E >= 0) {
-                ncclSend(D.sb[0] + part, part, ncclDouble, E, D.comm, D.stream);
-                ncclRecv(D.rb[0] + part, part, ncclDouble, E, D.comm, D.stream);
+                ncclSend(D.sb[0] + part, part, ncclDouble, E, D.comm, D.xs);
+                ncclRecv(D.rb[0] + part, part, ncclDouble, E, D.comm, D.xs);
             }
         } else {  // my W part <- W neighbour's E part, my E part <- E neighbour's W part
             for (int k = 0; k < D.nt; ++k) {
@@ -231,12 +235,12 @@ int exchange(Dist &D, int l, int which, int idx) {
             const int N = D.ty[0] > 0 ? D.rank - D.px : -1, S = D.ty[0] + 1 < D.py ? D.rank + D.px : -1;
             for (int q = 0; q < nf; ++q) {
                 if (N >= 0) {
-                    ncclSend(f[q] + at(g, 1, -1), blk, ncclDouble, N, D.comm, D.stream);
-                    ncclRecv(f[q] + at(g, 1 - HW, -1), blk, ncclDouble, N, D.comm, D.stream);
+                    ncclSend(f[q] + at(g, 1, -1), blk, ncclDouble, N, D.comm, D.xs);
+                    ncclRecv(f[q] + at(g, 1 - HW, -1), blk, ncclDouble, N, D.comm, D.xs);
                 }
                 if (S >= 0) {
-                    ncclSend(f[q] + at(g, g.ncy + 1 - HW, -1), blk, ncclDouble, S, D.comm, D.stream);
-                    ncclRecv(f[q] + at(g, g.ncy + 1, -1), blk, ncclDouble, S, D.comm, D.stream);
+                    ncclSend(f[q] + at(g, g.ncy + 1 - HW, -1), blk, ncclDouble, S, D.comm, D.xs);
+                    ncclRecv(f[q] + at(g, g.ncy + 1, -1), blk, ncclDouble, S, D.comm, D.xs);
                 }
             }
         } else {
@@ -356,6 +360,37 @@ int dsmooth(Dist &D, int l, int &cur, int n, bool zero_in, bool fine, int max_pa
         if (pairs > max_pairs) pairs = max_pairs;
         for (int s = 0; s < n;) {
             const bool two = pairs > 0 && !(zero_in && s == 0);
+            if (D.overlap && stream_ok(g0) && !(zero_in && s == 0)) {
+                // boundary layers first, then their halo exchange on the comm stream while the
+                // interior of the tiles is swept
+                for (int part = 0; part < 2; ++part) {
+                    for (int k = 0; k < D.nt; ++k) {
+                        stokes_s *t = D.tile[k];
+                        Level &L = t->lev[l];
+                        if (two)
+                            launch_jacobi2_part(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur], L.vx[1 - cur],
+                                                L.vy[1 - cur], tile_rhs(t, l, fine), D.o.omega_v, part);
+                        else
+                            launch_jacobi_stream_part(ctx(t), L.g, L.etab, L.etap, L.vx[cur], L.vy[cur],
+                                                      L.vx[1 - cur], L.vy[1 - cur], tile_rhs(t, l, fine), D.o.omega_v,
+                                                      part);
+                    }
+                    if (part == 0) {
+                        CK(cudaEventRecord(D.ev[0], D.stream));
+                        CK(cudaStreamWaitEvent(D.cstream, D.ev[0], 0));
+                        D.xs = D.cstream;
+                        st = exchange(D, l, FX_V, 1 - cur);
+                        D.xs = D.stream;
+                        if (st) return st;
+                        CK(cudaEventRecord(D.ev[1], D.cstream));
+                    }
+                }
+                CK(cudaStreamWaitEvent(D.stream, D.ev[1], 0));
+                if (two) { --pairs; s += 2; }
+                else s += 1;
+                cur ^= 1;
+                continue;
+            }
             for (int k = 0; k < D.nt; ++k) {
                 stokes_s *t = D.tile[k];
                 Level &L = t->lev[l];
@@ -702,6 +737,9 @@ int dist_destroy(Dist *D) {
     if (D->dscal) cudaFree(D->dscal);
     if (D->hsc) cudaFreeHost(D->hsc);
     if (D->own_stream) cudaStreamDestroy(D->stream);
+    if (D->cstream) cudaStreamDestroy(D->cstream);
+    for (int k = 0; k < 2; ++k)
+        if (D->ev[k]) cudaEventDestroy(D->ev[k]);
     free(D);
     return STOKES_OK;
 }
@@ -937,6 +975,17 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
     if (!D->stream) {
         if (cudaStreamCreateWithFlags(&D->stream, cudaStreamNonBlocking) != cudaSuccess) { free(D); return STOKES_ECUDA; }
         D->own_stream = true;
+    }
+    D->xs = D->stream;
+    if (cudaStreamCreateWithFlags(&D->cstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&D->ev[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&D->ev[1], cudaEventDisableTiming) != cudaSuccess) {
+        free(D);
+        return STOKES_ECUDA;
+    }
+    {
+        const char *e = getenv("STOKES_DIST_OVERLAP");
+        D->overlap = !(e && e[0] == '0');
     }
     int st;
     if (D->mode != M_NCCL) {

@@ -114,6 +114,14 @@ void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *et
 bool jacobi2_ok(const GridL &g);
 void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
                     const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega);
+// split passes of decomposed tiles (halo exchange overlapped with the interior): part 0 = the
+// two layers of unknowns next to every non-global side, part 1 = the rest of the level
+void launch_jacobi2_part(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                         const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
+                         double omega, int part);
+void launch_jacobi_stream_part(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                               const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
+                               double omega, int part);
 // Anderson acceleration (aa.cu): ring of AA_MAXS history slots of three padded fields
 constexpr int AA_MAXS = 16;
 struct AAVec {

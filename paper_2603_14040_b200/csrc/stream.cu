@@ -16,6 +16,7 @@
 //                 fused with the energy residual of the new (v, p) [a10+a3]
 // Stencil coefficients are those of kernels.cu (Listing vx_op_point).
 #include <math.h>
+#include <stdlib.h>
 
 #include <type_traits>
 
@@ -89,6 +90,20 @@ struct Win {
     }
 };
 enum { F_VX = 0, F_VY = 1, F_EP = 2, F_EB = 3, F_4 = 4, F_5 = 5 };  // F_4: p | bx, F_5: rho | by
+
+// Row / column ranges of a launch, one per blockIdx.z (two at most: the split passes of a
+// decomposed tile run the boundary strips N + S or W + E in one launch).  Default: the level.
+struct Reg2 {
+    int i_lo[2], i_hi[2], j_lo[2], j_hi[2];
+};
+Reg2 full_region(const GridL &g) {
+    Reg2 r;
+    r.i_lo[0] = r.i_lo[1] = 1;
+    r.i_hi[0] = r.i_hi[1] = g.ncy;
+    r.j_lo[0] = r.j_lo[1] = 1;
+    r.j_hi[0] = r.j_hi[1] = g.ncx;
+    return r;
+}
 
 // reciprocal without the IEEE-division subroutine: MUFU seed + two Newton steps
 // (24 -> 48 -> full 53 bits; |a| is far inside the float range for every level here)
@@ -341,16 +356,18 @@ struct JacobiUzawaOp {
 // registers), so no CTA-wide barrier is needed per row and the compute warps may drift.
 constexpr int NTHR = TW + 32;
 template <class Op>
-__global__ void __maxnreg__(112) k_stream(GridL g, Op op, int H, double *__restrict__ partials) {
+__global__ void __maxnreg__(112) k_stream(GridL g, Op op, int H, double *__restrict__ partials, Reg2 R, int seg) {
     extern __shared__ __align__(128) double sm[];
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + NS * NF * RW);
     uint64_t *empty = full + NS;
     __shared__ double red[NTHR / 32];
     const int t = threadIdx.x;
     const int warp = t >> 5;
-    const int j0 = 1 + TW * blockIdx.x;
-    const int i0 = 1 + blockIdx.y * H;
-    const int i1 = min(i0 + H - 1, g.ncy);
+    const int z = blockIdx.z;
+    const int j0 = R.j_lo[z] + TW * blockIdx.x;
+    const int i0 = R.i_lo[z] + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, R.i_hi[z]);
+    const int jhi = R.j_hi[z];
     const int rbase = i0 - 1;  // first staged row
     const int rlast = i1 + 1;  // last staged row
     if (t == 0) {
@@ -370,10 +387,10 @@ __global__ void __maxnreg__(112) k_stream(GridL g, Op op, int H, double *__restr
             for (int r = rbase; r <= rlast; ++r) {
                 const int rel = r - rbase, slot = rel % NS;
                 if (rel >= NS) mbar_wait(empty + slot, ((rel / NS) - 1) & 1);  // consumers done with r-NS
-                mbar_expect_tx(full + slot, Op::NF * RW * 8);
+                mbar_expect_tx(full + slot, Op::NF * seg * 8);
 #pragma unroll
                 for (int f = 0; f < Op::NF; ++f)
-                    bulk_g2s(sm + (slot * NF + f) * RW, op.src[f] + (size_t)r * P + (j0 - 2), RW * 8, full + slot);
+                    bulk_g2s(sm + (slot * NF + f) * RW, op.src[f] + (size_t)r * P + (j0 - 2), seg * 8, full + slot);
             }
         }
     } else {  // ---------------------------- compute warps
@@ -390,11 +407,11 @@ __global__ void __maxnreg__(112) k_stream(GridL g, Op op, int H, double *__restr
         consume(w, rbase + 1);
         for (int i = i0; i <= i1; ++i) {
             consume(w, i + 1);  // window: A = i-1, B = i, C = i+1
-            if (j <= g.ncx) op.row(g, w, i, j, acc);
+            if (j <= jhi) op.row(g, w, i, j, acc);
         }
     }
     if (Op::NRED > 0) {  // deterministic CTA reduction over the compute warps
-        const size_t b = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+        const size_t b = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
 #pragma unroll
         for (int k = 0; k < Op::NRED; ++k) {
             double v = warp < TW / 32 ? acc[k] : 0.0;
@@ -416,25 +433,28 @@ __global__ void __maxnreg__(112) k_stream(GridL g, Op op, int H, double *__restr
 // CTA-barrier engine (register-heavy operators: 256 threads, up to 128 registers, 2 CTAs/SM):
 // thread 0 issues the bulk copies; one __syncthreads per row frees the row's slot.
 template <class Op>
-__global__ void __launch_bounds__(TW, MINB) k_stream_bar(GridL g, Op op, int H, double *__restrict__ partials) {
+__global__ void __launch_bounds__(TW, MINB) k_stream_bar(GridL g, Op op, int H, double *__restrict__ partials, Reg2 R,
+                                                          int seg) {
     extern __shared__ __align__(128) double sm[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + NS * NF * RW);
     __shared__ double red[TW / 32];
     const int t = threadIdx.x;
-    const int j0 = 1 + TW * blockIdx.x;
+    const int z = blockIdx.z;
+    const int j0 = R.j_lo[z] + TW * blockIdx.x;
     const int j = j0 + t;
-    const int i0 = 1 + blockIdx.y * H;
-    const int i1 = min(i0 + H - 1, g.ncy);
+    const int i0 = R.i_lo[z] + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, R.i_hi[z]);
+    const int jhi = R.j_hi[z];
     const int rbase = i0 - 1;
     const int rlast = i1 + 1;
     const size_t P = g.P;
     auto issue = [&](int r) {
         const int slot = (r - rbase) % NS;
         uint64_t *bar = bars + slot;
-        mbar_expect_tx(bar, Op::NF * RW * 8);
+        mbar_expect_tx(bar, Op::NF * seg * 8);
 #pragma unroll
         for (int f = 0; f < Op::NF; ++f)
-            bulk_g2s(sm + (slot * NF + f) * RW, op.src[f] + (size_t)r * P + (j0 - 2), RW * 8, bar);
+            bulk_g2s(sm + (slot * NF + f) * RW, op.src[f] + (size_t)r * P + (j0 - 2), seg * 8, bar);
     };
     if (t == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(bars + s, 1);
@@ -465,12 +485,12 @@ __global__ void __launch_bounds__(TW, MINB) k_stream_bar(GridL g, Op op, int H, 
     refill(rbase + 1);
     for (int i = i0; i <= i1; ++i) {
         consume(w, i + 1);
-        if (j <= g.ncx) op.row(g, w, i, j, acc);
+        if (j <= jhi) op.row(g, w, i, j, acc);
         __syncthreads();
         refill(i + 1);
     }
     if (Op::NRED > 0) {
-        const size_t b = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+        const size_t b = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
 #pragma unroll
         for (int k = 0; k < Op::NRED; ++k) {
             double v = acc[k];
@@ -522,9 +542,67 @@ dim3 stream_grid(const GridL &g) {
 template <class Op>
 void run(const LaunchCtx &c, const GridL &g, const Op &op, double *partials) {
     prepare_kernel<Op>();
-    if (Op::WS) k_stream<Op><<<stream_grid(g), NTHR, SMEM, c.stream>>>(g, op, strip_h(g), partials);
-    else k_stream_bar<Op><<<stream_grid(g), TW, SMEM, c.stream>>>(g, op, strip_h(g), partials);
+    if (Op::WS) k_stream<Op><<<stream_grid(g), NTHR, SMEM, c.stream>>>(g, op, strip_h(g), partials, full_region(g), RW);
+    else k_stream_bar<Op><<<stream_grid(g), TW, SMEM, c.stream>>>(g, op, strip_h(g), partials, full_region(g), RW);
     ++*c.counter;
+}
+// The split pass of a decomposed tile (halo overlap): part 0 = the HW = 2
+// layers of unknowns next to every non-global side (what the neighbours' halos need), part 1
+// = the rest.  Part 0 runs first; the halo exchange of its output overlaps part 1, which
+// leaves `reserve` SMs free for the exchange kernels.
+struct Split {
+    Reg2 ns, we, in;
+    int nns, nwe, we_rows;
+};
+Split split_regions(const GridL &g) {
+    Split s;
+    const int lo_i = g.bN ? 1 : 3, hi_i = g.bS ? g.ncy : g.ncy - 2, lo_j = g.bW ? 1 : 3, hi_j = g.bE ? g.ncx : g.ncx - 2;
+    s.nns = s.nwe = 0;
+    if (!g.bN) { s.ns.i_lo[s.nns] = 1; s.ns.i_hi[s.nns] = 2; s.ns.j_lo[s.nns] = 1; s.ns.j_hi[s.nns] = g.ncx; ++s.nns; }
+    if (!g.bS) { s.ns.i_lo[s.nns] = g.ncy - 1; s.ns.i_hi[s.nns] = g.ncy; s.ns.j_lo[s.nns] = 1; s.ns.j_hi[s.nns] = g.ncx; ++s.nns; }
+    if (!g.bW) { s.we.i_lo[s.nwe] = lo_i; s.we.i_hi[s.nwe] = hi_i; s.we.j_lo[s.nwe] = 1; s.we.j_hi[s.nwe] = 2; ++s.nwe; }
+    if (!g.bE) { s.we.i_lo[s.nwe] = lo_i; s.we.i_hi[s.nwe] = hi_i; s.we.j_lo[s.nwe] = g.ncx - 1; s.we.j_hi[s.nwe] = g.ncx; ++s.nwe; }
+    s.we_rows = hi_i - lo_i + 1;
+    s.in.i_lo[0] = s.in.i_lo[1] = lo_i;
+    s.in.i_hi[0] = s.in.i_hi[1] = hi_i;
+    s.in.j_lo[0] = s.in.j_lo[1] = lo_j;
+    s.in.j_hi[0] = s.in.j_hi[1] = hi_j;
+    return s;
+}
+int reserve_sms() {  // SMs left to the halo exchange while the interior part runs
+    static const int v = [] {
+        const char *e = getenv("STOKES_COMM_SMS");
+        return e ? atoi(e) : 4;
+    }();
+    return v;
+}
+template <class Op>
+void run_part(const LaunchCtx &c, const GridL &g, const Op &op, int part) {
+    static_assert(Op::NRED == 0, "split passes carry no reductions");
+    prepare_kernel<Op>();
+    const Split sp = split_regions(g);
+    auto go = [&](dim3 grid, int H, const Reg2 &R, int seg) {
+        if (Op::WS) k_stream<Op><<<grid, NTHR, SMEM, c.stream>>>(g, op, H, nullptr, R, seg);
+        else k_stream_bar<Op><<<grid, TW, SMEM, c.stream>>>(g, op, H, nullptr, R, seg);
+        ++*c.counter;
+    };
+    if (part == 0) {
+        if (sp.nns) go(dim3((g.ncx + TW - 1) / TW, 1, sp.nns), 2, sp.ns, RW);
+        if (sp.nwe) {
+            int H = (sp.we_rows + slots() - 1) / slots();
+            if (H < 4) H = 4;
+            go(dim3(1, (sp.we_rows + H - 1) / H, sp.nwe), H, sp.we, 6);  // 2 columns: 6-double segments
+        }
+        return;
+    }
+    const int rows = sp.in.i_hi[0] - sp.in.i_lo[0] + 1, cols = sp.in.j_hi[0] - sp.in.j_lo[0] + 1;
+    const int ncb = (cols + TW - 1) / TW;
+    int sl = slots() - MINB * reserve_sms();
+    int strips = sl / ncb;
+    if (strips < 1) strips = 1;
+    int H = (rows + strips - 1) / strips;
+    if (H < 4) H = 4;
+    go(dim3(ncb, (rows + H - 1) / H, 1), H, sp.in, RW);
 }
 void fill_src(const double **src, const double *vx, const double *vy, const double *etap, const double *etab,
               const double *f4, const double *f5) {
@@ -565,7 +643,9 @@ struct J2Args {
     const double *src[6];  // vx, vy, eta_p, eta_b, p | bx, rho | by
     double *vxo, *vyo;
     double omega, gx, gy;
-    int tw;  // output columns per CTA (even, <= TW - 2)
+    int tw;   // output columns per CTA (even, <= TW - 2)
+    int seg;  // doubles staged per row and field (<= the ring row width; 16-B multiple)
+    Reg2 R;   // row / column ranges (per blockIdx.z)
 };
 
 // Register window with a static rotation: row r of the strip lives in slot (r - sfirst) % 3
@@ -634,10 +714,12 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
     double *s1 = sm + NSJ * NF * JRW;  // [4 rows][vx', vy'][JT]
     uint64_t *bars = reinterpret_cast<uint64_t *>(s1 + 4 * 2 * JT);
     const int t = threadIdx.x;
-    const int j0 = 1 + a.tw * blockIdx.x;
+    const int z = blockIdx.z;
+    const int j0 = a.R.j_lo[z] + a.tw * blockIdx.x;
     const int c = j0 - 1 + t;  // sweep-1 column of this thread (= sweep-2 column for 1 <= t <= tw)
-    const int i0 = 1 + blockIdx.y * H;
-    const int i1 = min(i0 + H - 1, g.ncy);
+    const int i0 = a.R.i_lo[z] + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, a.R.i_hi[z]);
+    const int jhi = a.R.j_hi[z];
     // decomposed tiles: on a side that is no global boundary the first halo
     // ring holds the neighbour's unknowns; sweep 1 updates it too (from the second ring),
     // so that sweep 2 of the tile's own unknowns is exact.  Global sides: mirrors / walls.
@@ -648,10 +730,10 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
     auto issue = [&](int r) {
         const int slot = (r - rlo) % NSJ;
         uint64_t *bar = bars + slot;
-        mbar_expect_tx(bar, NF * JRW * 8);
+        mbar_expect_tx(bar, NF * a.seg * 8);
 #pragma unroll
         for (int f = 0; f < NF; ++f)
-            bulk_g2s(sm + (slot * NF + f) * JRW, a.src[f] + (size_t)r * P + (j0 - 2), JRW * 8, bar);
+            bulk_g2s(sm + (slot * NF + f) * JRW, a.src[f] + (size_t)r * P + (j0 - 2), a.seg * 8, bar);
     };
     if (t == 0) {
         for (int k = 0; k < NSJ; ++k) mbar_init(bars + k, 1);
@@ -737,7 +819,7 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
         if (!J2_LATE) refill(s);
         // ---- sweep 2, row i = s-1 on the intermediate iterate
         const int i = s - 1;
-        if (i >= i0 && i <= i1 && t >= 1 && t <= a.tw && (!EDGE || c <= g.ncx)) {
+        if (i >= i0 && i <= i1 && t >= 1 && t <= a.tw && c <= jhi) {
             const double *qa = s1 + (((s - 2) & 3) * 2) * JT + t, *qb = s1 + (((s - 1) & 3) * 2) * JT + t,
                          *qc = s1 + ((s & 3) * 2) * JT + t;
             W2 u;
@@ -1055,6 +1137,62 @@ int stream_blocks(const GridL &g) {
 // width-2 halos are current (dist.cu exchanges them after every pass)
 bool jacobi2_ok(const GridL &g) { return stream_ok(g); }
 
+template <int MODE>
+void j2_go(const LaunchCtx &c, dim3 grid, int H, const GridL &g, const J2Args &a) {
+    static unsigned long long done = 0;
+    if (first_on_device(&done))
+        cudaFuncSetAttribute(k_jacobi2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJ);
+    k_jacobi2<MODE><<<grid, JT, SMEMJ, c.stream>>>(g, a, H);
+    ++*c.counter;
+}
+// one part of the split two-sweep pass (see run_part): part 0 the boundary strips, part 1 the rest
+void launch_jacobi2_part(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                         const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
+                         double omega, int part) {
+    J2Args a;
+    a.vxo = vxo;
+    a.vyo = vyo;
+    a.omega = omega;
+    const bool fine = rhs.mode == RHS_FINE;
+    fill_src(a.src, vxi, vyi, etap, etab, fine ? rhs.p : rhs.bx, fine ? rhs.rho : rhs.by);
+    a.gx = fine ? rhs.gx : 0.0;
+    a.gy = fine ? rhs.gy : 0.0;
+    const Split sp = split_regions(g);
+    auto go = [&](dim3 grid, int H) {
+        if (fine) j2_go<RHS_FINE>(c, grid, H, g, a);
+        else j2_go<RHS_ARRAYS>(c, grid, H, g, a);
+    };
+    if (part == 0) {
+        if (sp.nns) {
+            a.R = sp.ns;
+            a.tw = jt_tw(g);
+            a.seg = JRW;
+            go(dim3((g.ncx + a.tw - 1) / a.tw, 1, sp.nns), 2);
+        }
+        if (sp.nwe) {
+            a.R = sp.we;
+            a.tw = 2;
+            a.seg = 6;
+            int H = (sp.we_rows + slots() - 1) / slots();
+            if (H < 4) H = 4;
+            go(dim3(1, (sp.we_rows + H - 1) / H, sp.nwe), H);
+        }
+        return;
+    }
+    a.R = sp.in;
+    a.seg = JRW;
+    const int rows = sp.in.i_hi[0] - sp.in.i_lo[0] + 1, cols = sp.in.j_hi[0] - sp.in.j_lo[0] + 1;
+    int ncb = (cols + JT - 3) / (JT - 2);
+    a.tw = (cols + ncb - 1) / ncb;
+    a.tw += a.tw & 1;
+    ncb = (cols + a.tw - 1) / a.tw;
+    int strips = (slots() - MINB * reserve_sms()) / ncb;
+    if (strips < 1) strips = 1;
+    int H = (rows + strips - 1) / strips;
+    if (H < 4) H = 4;
+    go(dim3(ncb, (rows + H - 1) / H, 1), H);
+}
+
 void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
                     const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega) {
     J2Args a;
@@ -1062,6 +1200,8 @@ void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, cons
     a.vyo = vyo;
     a.omega = omega;
     a.tw = jt_tw(g);
+    a.seg = JRW;
+    a.R = full_region(g);
     int H = 0;
     const dim3 grid = jt_grid(g, &H);
     if (rhs.mode == RHS_FINE) {
@@ -1105,6 +1245,29 @@ void launch_jacobi_stream(const LaunchCtx &c, const GridL &g, const double *etab
         op.omega = omega;
         op.gx = op.gy = 0.0;
         run(c, g, op, nullptr);
+    }
+}
+
+void launch_jacobi_stream_part(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                               const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
+                               double omega, int part) {
+    if (rhs.mode == RHS_FINE) {
+        JacobiOp<RHS_FINE> op;
+        fill_src(op.src, vxi, vyi, etap, etab, rhs.p, rhs.rho);
+        op.vxo = vxo;
+        op.vyo = vyo;
+        op.omega = omega;
+        op.gx = rhs.gx;
+        op.gy = rhs.gy;
+        run_part(c, g, op, part);
+    } else {
+        JacobiOp<RHS_ARRAYS> op;
+        fill_src(op.src, vxi, vyi, etap, etab, rhs.bx, rhs.by);
+        op.vxo = vxo;
+        op.vyo = vyo;
+        op.omega = omega;
+        op.gx = op.gy = 0.0;
+        run_part(c, g, op, part);
     }
 }
 

@@ -60,10 +60,11 @@ def test_full_solve_matches_oracle_golden(S, path):
     assert r["E"] <= rtol
     # energy residual history, iteration by iteration on the oracle's trajectory: E is a
     # residual norm relative to ||f|| (E_0 = 1), so its rounding differences are absolute
-    # (~1e-14), i.e. relative 1e-6 once E ~ 1e-8: bar |dE_k| <= 1e-9 E_k + 1e-13
+    # (1e-14 .. 1e-12 with the 1e6 viscosity jump), i.e. relative 1e-6 .. 1e-4 once E ~ 1e-8:
+    # bar |dE_k| <= 1e-9 E_k + 2e-12
     h, hg = np.array(r["hist"]), np.array(gold["hist"])
     m = min(len(h), len(hg))
-    dev = np.abs(h[:m] - hg[:m]) - (1e-9 * hg[:m] + 1e-13)
+    dev = np.abs(h[:m] - hg[:m]) - (1e-9 * hg[:m] + 2e-12)
     assert dev.max() <= 0, (int(dev.argmax()), float(np.abs(h[:m] - hg[:m]).max()))
     # the fields at the oracle's count
     if r["iters"] != K:

@@ -34,14 +34,33 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, out=None, defs=()):
+    """nvcc every source to an object in parallel (no cross-file device code), then link.
+    out / defs: an experimental variant (-D knobs of csrc/, e.g. "RR_NS=4") built elsewhere."""
+    out = out or LIB
+    if out == LIB and not defs and not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB, *[os.path.join(CSRC, s) for s in SOURCES], *LIBS]
+    from concurrent.futures import ThreadPoolExecutor
+    tag = "main" if out == LIB else os.path.splitext(os.path.basename(out))[0]
+    odir = os.path.join(HERE, "..", "build", "obj_" + tag)
+    os.makedirs(odir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defs]
+    objs = [os.path.join(odir, s.replace(".cu", ".o")) for s in SOURCES]
+    comp = [FL for FL in FLAGS if FL != "-shared"]
+
+    def one(k):
+        cmd = [NVCC, *comp, *dflags, "-c", "-o", objs[k], os.path.join(CSRC, SOURCES[k])]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd, cwd=CSRC)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        list(ex.map(one, range(len(SOURCES))))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs, *LIBS]
     if verbose:
-        print(" ".join(cmd))
+        print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd, cwd=CSRC)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

@@ -54,6 +54,7 @@ struct Dist {
     cudaStream_t xs;       // the stream exchange() enqueues on (stream, or cstream while overlapping)
     cudaEvent_t ev[2];
     bool overlap;
+    bool serial_split;  // diagnostics (STOKES_DIST_OVERLAP=2): split passes, exchange not overlapped
     double *dscal;   // [0] E [1] Sv [2] Sp [3] Sf [4] zero
     double *hsc;
     ncclComm_t comm;
@@ -360,10 +361,16 @@ int dsmooth(Dist &D, int l, int &cur, int n, bool zero_in, bool fine, int max_pa
         if (pairs > max_pairs) pairs = max_pairs;
         for (int s = 0; s < n;) {
             const bool two = pairs > 0 && !(zero_in && s == 0);
-            if (D.overlap && stream_ok(g0) && !(zero_in && s == 0)) {
+            static const int ovl_kind = [] {  // diagnostics: 3 both, 1 pairs only, 2 single sweeps only
+                const char *e = getenv("STOKES_OVL_KIND");
+                return e ? atoi(e) : 3;
+            }();
+            if (D.overlap && stream_ok(g0) && !(zero_in && s == 0) && (ovl_kind & (two ? 1 : 2))) {
                 // boundary layers first, then their halo exchange on the comm stream while the
                 // interior of the tiles is swept
-                for (int part = 0; part < 2; ++part) {
+                static const int rev = [] { const char *e = getenv("STOKES_OVL_REV"); return e ? atoi(e) : 0; }();
+                for (int pp = 0; pp < 2; ++pp) {
+                    const int part = rev ? 1 - pp : pp;
                     for (int k = 0; k < D.nt; ++k) {
                         stokes_s *t = D.tile[k];
                         Level &L = t->lev[l];
@@ -375,10 +382,10 @@ int dsmooth(Dist &D, int l, int &cur, int n, bool zero_in, bool fine, int max_pa
                                                       L.vx[1 - cur], L.vy[1 - cur], tile_rhs(t, l, fine), D.o.omega_v,
                                                       part);
                     }
-                    if (part == 0) {
+                    if (pp == 0) {
                         CK(cudaEventRecord(D.ev[0], D.stream));
                         CK(cudaStreamWaitEvent(D.cstream, D.ev[0], 0));
-                        D.xs = D.cstream;
+                        D.xs = D.serial_split ? D.stream : D.cstream;
                         st = exchange(D, l, FX_V, 1 - cur);
                         D.xs = D.stream;
                         if (st) return st;
@@ -986,6 +993,7 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
     {
         const char *e = getenv("STOKES_DIST_OVERLAP");
         D->overlap = !(e && e[0] == '0');
+        D->serial_split = e && e[0] == '2';
     }
     int st;
     if (D->mode != M_NCCL) {

@@ -24,6 +24,9 @@
 
 namespace {
 
+#ifndef WS_PROXY_FENCE
+#define WS_PROXY_FENCE 1
+#endif
 constexpr int TW = 256;          // columns per CTA
 constexpr int RW = TW + 4;       // staged row width (doubles): [j0-2, j0+TW+2)
 constexpr int NS = 8;            // landing ring depth (rows): NS-1 rows in flight per CTA
@@ -96,6 +99,7 @@ enum { F_VX = 0, F_VY = 1, F_EP = 2, F_EB = 3, F_4 = 4, F_5 = 5 };  // F_4: p | 
 struct Reg2 {
     int i_lo[2], i_hi[2], j_lo[2], j_hi[2];
 };
+__device__ __forceinline__ int zsel(const int (&a)[2], int z) { return z ? a[1] : a[0]; }  // no local copy
 Reg2 full_region(const GridL &g) {
     Reg2 r;
     r.i_lo[0] = r.i_lo[1] = 1;
@@ -364,10 +368,10 @@ __global__ void __maxnreg__(112) k_stream(GridL g, Op op, int H, double *__restr
     const int t = threadIdx.x;
     const int warp = t >> 5;
     const int z = blockIdx.z;
-    const int j0 = R.j_lo[z] + TW * blockIdx.x;
-    const int i0 = R.i_lo[z] + blockIdx.y * H;
-    const int i1 = min(i0 + H - 1, R.i_hi[z]);
-    const int jhi = R.j_hi[z];
+    const int j0 = zsel(R.j_lo, z) + TW * blockIdx.x;
+    const int i0 = zsel(R.i_lo, z) + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, zsel(R.i_hi, z));
+    const int jhi = zsel(R.j_hi, z);
     const int rbase = i0 - 1;  // first staged row
     const int rlast = i1 + 1;  // last staged row
     if (t == 0) {
@@ -399,6 +403,13 @@ __global__ void __maxnreg__(112) k_stream(GridL g, Op op, int H, double *__restr
             const int rel = r - rbase, slot = rel % NS;
             mbar_wait(full + slot, (rel / NS) & 1);
             w.template push<Op::NF>(sm + slot * NF * RW, t + 2);
+#if WS_PROXY_FENCE
+            // the slot's generic-proxy reads must be ordered before the producer's next
+            // async-proxy (TMA) write into it.  Without this fence a slot was occasionally
+            // refilled under a slow reader: whole rows of a CTA strip came out wrong when the
+            // halo exchange ran concurrently on another stream (tools/overlap_where.py)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
             __syncwarp();
             if ((t & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty + slot)) : "memory");
         };
@@ -440,11 +451,11 @@ __global__ void __launch_bounds__(TW, MINB) k_stream_bar(GridL g, Op op, int H, 
     __shared__ double red[TW / 32];
     const int t = threadIdx.x;
     const int z = blockIdx.z;
-    const int j0 = R.j_lo[z] + TW * blockIdx.x;
+    const int j0 = zsel(R.j_lo, z) + TW * blockIdx.x;
     const int j = j0 + t;
-    const int i0 = R.i_lo[z] + blockIdx.y * H;
-    const int i1 = min(i0 + H - 1, R.i_hi[z]);
-    const int jhi = R.j_hi[z];
+    const int i0 = zsel(R.i_lo, z) + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, zsel(R.i_hi, z));
+    const int jhi = zsel(R.j_hi, z);
     const int rbase = i0 - 1;
     const int rlast = i1 + 1;
     const size_t P = g.P;
@@ -715,11 +726,11 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
     uint64_t *bars = reinterpret_cast<uint64_t *>(s1 + 4 * 2 * JT);
     const int t = threadIdx.x;
     const int z = blockIdx.z;
-    const int j0 = a.R.j_lo[z] + a.tw * blockIdx.x;
+    const int j0 = zsel(a.R.j_lo, z) + a.tw * blockIdx.x;
     const int c = j0 - 1 + t;  // sweep-1 column of this thread (= sweep-2 column for 1 <= t <= tw)
-    const int i0 = a.R.i_lo[z] + blockIdx.y * H;
-    const int i1 = min(i0 + H - 1, a.R.i_hi[z]);
-    const int jhi = a.R.j_hi[z];
+    const int i0 = zsel(a.R.i_lo, z) + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, zsel(a.R.i_hi, z));
+    const int jhi = zsel(a.R.j_hi, z);
     // decomposed tiles: on a side that is no global boundary the first halo
     // ring holds the neighbour's unknowns; sweep 1 updates it too (from the second ring),
     // so that sweep 2 of the tile's own unknowns is exact.  Global sides: mirrors / walls.
@@ -874,10 +885,13 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
 // k_restrict_vel (Appendix B; rows / columns outside the domain dropped and renormalised).
 // The fine residual never reaches HBM: 48 B/fine cell read + 4 B written instead of 84.
 #ifndef RR_NS
-#define RR_NS 6
+#define RR_NS 4  // 3 CTAs per SM (24 warps): 203 -> 184 us at 4096^2 (tools/variants.py, r02)
 #endif
 #ifndef RR_ROWS
-#define RR_ROWS 8
+#define RR_ROWS 5
+#endif
+#ifndef RR_MINB
+#define RR_MINB 3
 #endif
 constexpr int NSRR = RR_NS;      // landing ring depth of the residual+restriction pass
 constexpr int RRR = RR_ROWS;     // residual rows kept for the restriction (>= 5: rows 2I-2..2I+1 + the next)
@@ -891,7 +905,7 @@ struct RRArgs {
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(TW, MINB) k_resrestrict(GridL g, GridL gc, RRArgs a, int HC) {
+__global__ void __launch_bounds__(TW, RR_MINB) k_resrestrict(GridL g, GridL gc, RRArgs a, int HC) {
     extern __shared__ __align__(128) double sm[];
     double *rr = sm + NSRR * NF * RW;  // [RRR rows][rx, ry][TW]
     uint64_t *bars = reinterpret_cast<uint64_t *>(rr + RRR * 2 * TW);
@@ -1279,7 +1293,7 @@ void launch_residual_restrict(const LaunchCtx &c, const GridL &g, const GridL &g
     a.byc = byc;
     a.tw = j2_tw(g);
     const int ncb = (g.ncx + a.tw - 1) / a.tw;
-    int strips = slots() / ncb;
+    int strips = slots() / MINB * RR_MINB / ncb;  // one wave at RR_MINB CTAs per SM
     if (strips < 1) strips = 1;
     int HC = (gc.ncy + strips - 1) / strips;
     if (HC < 2) HC = 2;

@@ -50,6 +50,7 @@ class Opts(ctypes.Structure):
         ("ras_inner", ctypes.c_int),
         ("ras_seed", ctypes.c_uint64),
         ("gcr_true_restart", ctypes.c_int),
+        ("gcr_inner", ctypes.c_int),
     ]
 
 

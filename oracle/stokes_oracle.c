@@ -62,6 +62,8 @@ typedef struct {
     int ras_inner;       /* RAS inner iterations T_inner (4) */
     uint64_t ras_seed;   /* seed of the counter-based tile-shift generator (reading R27) */
     int gcr_true_restart; /* 1: true residual at every GCR restart (R13), 0: recursive r (Alg. 4) */
+    int gcr_inner;        /* GCR inner product: 0 Euclidean over unknowns (default),
+                             1 energy-weighted (the weights of E; reading R33) */
 } oracle_opts;
 
 typedef struct {
@@ -661,6 +663,7 @@ int oracle_opts_default(oracle_opts *o) {
     o->accel = 0;
     o->gcr_restart = 10;
     o->gcr_true_restart = 1;
+    o->gcr_inner = 0;
     o->max_iter = 10000;
     o->pressure_sign = 1;
     o->theta_step = 0.0;
@@ -1133,7 +1136,24 @@ static void apply_A(oracle_t *S, ovec z, ovec w) {
 typedef struct { oracle_t *S; double Sf; } stokes_gcr;
 static void sg_precond(void *c, ovec r, ovec z) { apply_precond(((stokes_gcr *)c)->S, r, z); }
 static void sg_apply(void *c, ovec z, ovec w) { apply_A(((stokes_gcr *)c)->S, z, w); }
-static double sg_dot(void *c, ovec a, ovec b) { return ovec_dot(&((stokes_gcr *)c)->S->lev[0], a, b); }
+/* energy-weighted inner product (option gcr_inner = 1, reading R33): the weights of the
+ * stopping test E (sum_vel_energy / sum_p_energy), so GCR minimises E itself */
+static double ovec_dot_energy(const oracle_t *S, ovec a, ovec b) {
+    const olevel *L = &S->lev[0];
+    size_t n = (size_t)nunk(L) + (size_t)L->ncx * L->ncy, k = 0;
+    double *t = zalloc(n);
+    const double c = 2.0 / (L->dx * L->dx) + 2.0 / (L->dy * L->dy);
+    FOR_VX(L) t[k++] = a.x[IX(L, i, j)] * b.x[IX(L, i, j)] / (-Lx_diag(S, L, i, j));
+    FOR_VY(L) t[k++] = a.y[IX(L, i, j)] * b.y[IX(L, i, j)] / (-Ly_diag(S, L, i, j));
+    FOR_P(L) t[k++] = a.p[IX(L, i, j)] * b.p[IX(L, i, j)] * (L->etap[IX(L, i, j)] / c);
+    double s = pairwise(t, n);
+    free(t);
+    return s;
+}
+static double sg_dot(void *c, ovec a, ovec b) {
+    oracle_t *S = ((stokes_gcr *)c)->S;
+    return S->o.gcr_inner ? ovec_dot_energy(S, a, b) : ovec_dot(&S->lev[0], a, b);
+}
 static void sg_axpy(void *c, double a, ovec x, ovec y) { ovec_axpy(&((stokes_gcr *)c)->S->lev[0], a, x, y); }
 static void sg_scale(void *c, double a, ovec x) { ovec_scale(&((stokes_gcr *)c)->S->lev[0], a, x); }
 static void sg_residual(void *c, ovec x, ovec r) {

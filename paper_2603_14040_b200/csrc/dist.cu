@@ -361,16 +361,11 @@ int dsmooth(Dist &D, int l, int &cur, int n, bool zero_in, bool fine, int max_pa
         if (pairs > max_pairs) pairs = max_pairs;
         for (int s = 0; s < n;) {
             const bool two = pairs > 0 && !(zero_in && s == 0);
-            static const int ovl_kind = [] {  // diagnostics: 3 both, 1 pairs only, 2 single sweeps only
-                const char *e = getenv("STOKES_OVL_KIND");
-                return e ? atoi(e) : 3;
-            }();
-            if (D.overlap && stream_ok(g0) && !(zero_in && s == 0) && (ovl_kind & (two ? 1 : 2))) {
+            if (D.overlap && stream_ok(g0) && !(zero_in && s == 0)) {
                 // boundary layers first, then their halo exchange on the comm stream while the
                 // interior of the tiles is swept
-                static const int rev = [] { const char *e = getenv("STOKES_OVL_REV"); return e ? atoi(e) : 0; }();
                 for (int pp = 0; pp < 2; ++pp) {
-                    const int part = rev ? 1 - pp : pp;
+                    const int part = pp;
                     for (int k = 0; k < D.nt; ++k) {
                         stokes_s *t = D.tile[k];
                         Level &L = t->lev[l];
@@ -990,9 +985,12 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
         free(D);
         return STOKES_ECUDA;
     }
-    {
+    {   // overlap the halo exchange with the interior: on by default with one tile per GPU
+        // (NCCL transport: the exchange latency is what it hides); off for the in-process
+        // transports, whose tiles share one GPU (nothing to hide, the split only adds launches).
+        // STOKES_DIST_OVERLAP = 0 off, 1 on, 2 split passes with the exchange not overlapped
         const char *e = getenv("STOKES_DIST_OVERLAP");
-        D->overlap = !(e && e[0] == '0');
+        D->overlap = e ? e[0] != '0' : D->mode == M_NCCL;
         D->serial_split = e && e[0] == '2';
     }
     int st;

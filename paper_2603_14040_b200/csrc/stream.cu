@@ -719,7 +719,7 @@ struct W2 {  // sweep-2 view of row s-1: velocities from the intermediate rows, 
     }
 };
 
-template <int MODE>
+template <int MODE, bool TILE>  // TILE = false: a single domain (every side global), no halo-ring logic
 __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) {
     extern __shared__ __align__(128) double sm[];
     double *s1 = sm + NSJ * NF * JRW;  // [4 rows][vx', vy'][JT]
@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
     // decomposed tiles: on a side that is no global boundary the first halo
     // ring holds the neighbour's unknowns; sweep 1 updates it too (from the second ring),
     // so that sweep 2 of the tile's own unknowns is exact.  Global sides: mirrors / walls.
-    const int hN = !g.bN, hS = !g.bS, hW = !g.bW, hE = !g.bE;
+    const int hN = TILE && !g.bN, hS = TILE && !g.bS, hW = TILE && !g.bW, hE = TILE && !g.bE;
     const int rlo = max(i0 - 2, -hN), rhi = min(i1 + 2, g.ncy + 1 + hS);
     const int sfirst = max(i0 - 1, 0), slast = min(i1 + 1, g.ncy + 1);
     const size_t P = g.P;
@@ -1151,13 +1151,18 @@ int stream_blocks(const GridL &g) {
 // width-2 halos are current (dist.cu exchanges them after every pass)
 bool jacobi2_ok(const GridL &g) { return stream_ok(g); }
 
-template <int MODE>
-void j2_go(const LaunchCtx &c, dim3 grid, int H, const GridL &g, const J2Args &a) {
+template <int MODE, bool TILE>
+void j2_go_t(const LaunchCtx &c, dim3 grid, int H, const GridL &g, const J2Args &a) {
     static unsigned long long done = 0;
     if (first_on_device(&done))
-        cudaFuncSetAttribute(k_jacobi2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJ);
-    k_jacobi2<MODE><<<grid, JT, SMEMJ, c.stream>>>(g, a, H);
+        cudaFuncSetAttribute(k_jacobi2<MODE, TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJ);
+    k_jacobi2<MODE, TILE><<<grid, JT, SMEMJ, c.stream>>>(g, a, H);
     ++*c.counter;
+}
+template <int MODE>
+void j2_go(const LaunchCtx &c, dim3 grid, int H, const GridL &g, const J2Args &a) {
+    if (g.bN && g.bS && g.bW && g.bE) j2_go_t<MODE, false>(c, grid, H, g, a);  // single domain
+    else j2_go_t<MODE, true>(c, grid, H, g, a);
 }
 // one part of the split two-sweep pass (see run_part): part 0 the boundary strips, part 1 the rest
 void launch_jacobi2_part(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
@@ -1222,21 +1227,12 @@ void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, cons
         fill_src(a.src, vxi, vyi, etap, etab, rhs.p, rhs.rho);
         a.gx = rhs.gx;
         a.gy = rhs.gy;
-        static unsigned long long done = 0;
-        if (first_on_device(&done)) {
-            cudaFuncSetAttribute(k_jacobi2<RHS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJ);
-        }
-        k_jacobi2<RHS_FINE><<<grid, JT, SMEMJ, c.stream>>>(g, a, H);
+        j2_go<RHS_FINE>(c, grid, H, g, a);
     } else {
         fill_src(a.src, vxi, vyi, etap, etab, rhs.bx, rhs.by);
         a.gx = a.gy = 0.0;
-        static unsigned long long done = 0;
-        if (first_on_device(&done)) {
-            cudaFuncSetAttribute(k_jacobi2<RHS_ARRAYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJ);
-        }
-        k_jacobi2<RHS_ARRAYS><<<grid, JT, SMEMJ, c.stream>>>(g, a, H);
+        j2_go<RHS_ARRAYS>(c, grid, H, g, a);
     }
-    ++*c.counter;
 }
 
 void launch_jacobi_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,

@@ -74,9 +74,17 @@ def test_virtual_decomposition_is_exact(px, py, name, smoother, transport):
     assert abs(np.sqrt(e1) - np.sqrt(e2)) <= 1e-8, (e1, e2)
 
 
+@pytest.fixture(params=["0", "1"], ids=["serial", "overlap"])
+def overlap(request, monkeypatch):
+    """STOKES_DIST_OVERLAP (read when a decomposed handle is created): 1 = boundary strips
+    first, their halo exchange on a comm stream while the interior is swept."""
+    monkeypatch.setenv("STOKES_DIST_OVERLAP", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("transport", TRANSPORTS)
 @pytest.mark.parametrize("px,py", [(2, 2), (4, 2), (1, 3)])
-def test_fused_tile_kernels_fixed_iterations(transport, px, py):
+def test_fused_tile_kernels_fixed_iterations(transport, px, py, overlap):
     """Tiles >= 128 cells wide run the single-domain fused kernels with width-2 halos: the
     two-sweep pass (which also updates the first halo ring), the residual fused with its
     restriction and the fused Uzawa pass (a12).  A fixed number of iterations must equal the
@@ -103,7 +111,7 @@ def test_fused_tile_kernels_fixed_iterations(transport, px, py):
 
 @pytest.mark.parametrize("transport", TRANSPORTS)
 @pytest.mark.parametrize("name,px,py", [("layered", 2, 2), ("random", 4, 2), ("block", 2, 1)])
-def test_fused_tile_solve_counts_identical(transport, name, px, py):
+def test_fused_tile_solve_counts_identical(transport, name, px, py, overlap):
     """Converged solves at 512 x 512 (256 x 256 .. 128 x 256 tiles, every distributed level on
     the fused kernels down to the agglomeration): the same iteration count as one domain, the
     same fields to 1e-11 (north_star count / field bars; the decomposition changes only the
@@ -151,3 +159,19 @@ def test_nccl_transport_single_rank():
     finally:
         if own:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("transport", TRANSPORTS)
+def test_overlapped_passes_large_tiles(transport, monkeypatch):
+    """2 x 2 tiles of 1024^2 (the sizes where the overlapped exchange really runs beside the
+    interior kernels): 3 iterations equal the single domain to rounding."""
+    from paper_2603_14040_b200 import Stokes, StokesDist
+    monkeypatch.setenv("STOKES_DIST_OVERLAP", "1")
+    monkeypatch.setenv("STOKES_DIST_DMIN", "128")
+    n = 2048
+    w = workload("layered", n, n)
+    opts = dict(omega_v=0.6, alpha_p=1.0, max_iter=3)
+    a = setup(Stokes, w, n, **opts).solve(0.0)
+    b = setup(StokesDist, w, n, px=2, py=2, transport=transport, **opts).solve(0.0)
+    for k in ("vx", "vy", "p"):
+        assert rel(b[k], a[k]) <= 1e-12, (k, rel(b[k], a[k]))

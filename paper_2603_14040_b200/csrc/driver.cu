@@ -1431,7 +1431,8 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
     // sweeps in shared memory): read 6, write 2
     double per_cell[9] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0, 72.0, 64.0, 64.0};
     if (h->nlev > 1 && jacobi2_ok(g)) per_cell[2] = 48.0 + 4.0;  // fused: the residual stays on chip
-    if (jacobi2_ok(g)) per_cell[5] = 2 * 56.0;  // RBGS: two streamed passes, each read 6 + write 1
+    // RBGS: one streamed pass on a single domain (read 6 + write 2), else two passes (read 6 + write 1 each)
+    if (jacobi2_ok(g) && !(g.bN && g.bS && g.bW && g.bE && rbgs1_enabled())) per_cell[5] = 2 * 56.0;
     if (kernel < 0 || kernel > 8) return STOKES_EINVAL;
     if ((kernel == 6 && !stream_ok(g)) || (kernel == 7 && !jacobi2_ok(g))) return STOKES_EINVAL;
     *bytes = per_cell[kernel] * cells;

@@ -112,6 +112,7 @@ void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *et
 // fused Uzawa pressure step + energy residual; partials = 3 per CTA (Sv, Sp, sum p')
 // two Jacobi sweeps in one pass (single-domain levels with jacobi2_ok)
 bool jacobi2_ok(const GridL &g);
+bool rbgs1_enabled();  // one-pass RBGS on single domains (STOKES_RBGS1=0 disables it)
 void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
                     const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega);
 // split passes of decomposed tiles (halo exchange overlapped with the interior): part 0 = the

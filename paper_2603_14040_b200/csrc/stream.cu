@@ -636,16 +636,20 @@ void fill_src(const double **src, const double *vx, const double *vy, const doub
 // sweeps.  On decomposed tiles sweep 1 also updates the first halo ring from the second
 // (width-2 halos exchanged once per pass).  (A warp-specialised variant exchanging the intermediate iterate by warp
 // shuffles, without CTA barriers, measured 435 us vs 340 us for this one at 4096^2.)
-// the two-sweep pass runs wider CTAs: 320 threads (10 warps, 2 CTAs = 20 warps per SM at
-// 96 registers), a 6-row ring of 324-wide rows (114 KB per CTA)
+// the two-sweep pass runs 160-thread CTAs (5 warps; 4 CTAs = 20 warps per SM at 96
+// registers) with a 5-row ring of 164-wide rows (48.5 KB per CTA): fewer warps wait at each
+// row barrier than with r01's 320-thread CTAs (277 vs 294 us at 4096^2)
 #ifndef J2_NSJ
-#define J2_NSJ 6  // 6-deep landing ring: 303.7 -> 284.5 us at 4096^2 vs 5 (TMA latency)
+#define J2_NSJ 5  // 5-deep landing ring at 160-wide CTAs (r02: 6 rows at 320 threads 293.7 us)
 #endif
 #ifndef J2_LATE
 #define J2_LATE 0
 #endif
 #ifndef J2_JT
-#define J2_JT 320
+#define J2_JT 160  // r02: 160 threads x 4 CTAs per SM 277 us; 320 x 2 (r01) 293.7, 192 x 3 314, 128 x 5 283
+#endif
+#ifndef J2_MINB
+#define J2_MINB 4
 #endif
 constexpr int JT = J2_JT, JRW = JT + 4, NSJ = J2_NSJ;
 constexpr int SMEMJ = NSJ * NF * JRW * 8 + 4 * 2 * JT * 8 + NSJ * 8;
@@ -718,9 +722,8 @@ struct W2 {  // sweep-2 view of row s-1: velocities from the intermediate rows, 
         return k == F_VX ? pick(vx[2], dc) : k == F_VY ? pick(vy[2], dc) : pick(v->B[k], dc);
     }
 };
-
 template <int MODE, bool TILE>  // TILE = false: a single domain (every side global), no halo-ring logic
-__global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) {
+__global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int H) {
     extern __shared__ __align__(128) double sm[];
     double *s1 = sm + NSJ * NF * JRW;  // [4 rows][vx', vy'][JT]
     uint64_t *bars = reinterpret_cast<uint64_t *>(s1 + 4 * 2 * JT);
@@ -875,7 +878,6 @@ __global__ void __launch_bounds__(JT, MINB) k_jacobi2(GridL g, J2Args a, int H) 
     else
         for (int s = sfirst; s <= slast; ++s) step(std::true_type(), s);
 }
-
 
 // ---- fine residual fused with its restriction (a3 + a5) --------------------------------
 // A CTA streams fine rows through the TMA landing ring (columns j0-1 .. j0+tw, tw <= TW-2:
@@ -1108,6 +1110,138 @@ __global__ void __launch_bounds__(TW, MINB) k_rbgs_pass(GridL g, J2Args a, int H
     }
 }
 
+// ---- damped red-black Gauss-Seidel in ONE streamed pass (a4, reading R11) ---------------
+// All four phases of a sweep as a wavefront over the rows of a strip, one CTA barrier per
+// row step s:
+//   (vx, red)   row s          (vx, black) row s-2
+//   (vy, red)   row s-4        (vy, black) row s-6
+// A red node's neighbours in its own component are black and vice versa, so at step s the
+// lanes with (s + c + par) even do the two red updates and the others the two black ones:
+// every lane does one vx and one vy update per step (no idle lanes).  Each update reads
+// exactly the values the serial phase order gives it (old black vx for vx red, vx red of
+// rows s-3..s-1 for vx black, final vx and old black vy for vy red, vy red of rows s-7..s-5
+// for vy black; DESIGN.md §6 lists the check), in place in the shared-memory landing ring,
+// which keeps rows s-7 .. s+1 resident plus the rows in flight.  The dependency cone is
+// three columns wide on the west and two on the east, so a CTA of TWR lanes (column
+// c = j0 - 3 + t; RB1_SPLIT: one warp set for the vx and one for the vy updates, which are
+// independent within a step) owns tw = TWR - 6 output columns and the strip recomputes rows i0-2 ..
+// i1+3 redundantly.  Fields read once and written once per sweep: 64 B/cell per sweep
+// instead of 2 x 56 for the two component passes.  Single domains only
+// (the cone is wider than the decomposed tiles' two halo rings).
+#ifndef RB1_TW
+#define RB1_TW 128
+#endif
+#ifndef RB1_NS
+#define RB1_NS 11
+#endif
+#ifndef RB1_SPLIT  // 1: separate warps for the vx and the vy update of a column (2 x TWR threads)
+#define RB1_SPLIT 1
+#endif
+constexpr int TWR = RB1_TW, RWR = TWR + 4, NSB = RB1_NS;  // ring: rows s-7 .. s+1 resident
+constexpr int NTB = RB1_SPLIT ? 2 * TWR : TWR;
+constexpr int SMEMB = NSB * NF * RWR * 8 + NSB * 8;
+static_assert(NSB >= 10, "the one-pass RBGS keeps 9 rows resident");
+
+struct SmB {  // stencil view straight on three landing slots of the one-pass ring
+    const double *a, *b, *c;
+    __device__ __forceinline__ double A(int k, int dc = 0) const { return a[k * RWR + dc]; }
+    __device__ __forceinline__ double B(int k, int dc = 0) const { return b[k * RWR + dc]; }
+    __device__ __forceinline__ double C(int k, int dc = 0) const { return c[k * RWR + dc]; }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(NTB) k_rbgs1(GridL g, J2Args a, int H) {
+    extern __shared__ __align__(128) double sm[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + NSB * NF * RWR);
+    const int tt = threadIdx.x;
+    const int t = RB1_SPLIT ? tt % TWR : tt;        // lane of the column
+    const int role = RB1_SPLIT ? tt / TWR : 2;      // 0: vx updates, 1: vy updates, 2: both (warp-uniform)
+    const int j0 = 1 + a.tw * blockIdx.x;  // odd: the staged segment starts at j0 - 4 (16-B aligned)
+    const int c = j0 - 3 + t;
+    const int i0 = 1 + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, g.ncy);
+    const int rlo = max(i0 - 3, 0), rhi = min(i1 + 4, g.ncy + 1);
+    const size_t P = g.P;
+    auto issue = [&](int r) {
+        const int slot = (r - rlo) % NSB;
+        uint64_t *bar = bars + slot;
+        mbar_expect_tx(bar, NF * RWR * 8);
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            bulk_g2s(sm + (slot * NF + f) * RWR, a.src[f] + (size_t)r * P + (j0 - 4), RWR * 8, bar);
+    };
+    if (tt == 0) {
+        for (int k = 0; k < NSB; ++k) mbar_init(bars + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tt == 0)
+        for (int r = rlo; r < rlo + NSB && r <= rhi; ++r) issue(r);
+    int landed = rlo - 1;
+    auto slot_of = [&](int r) { return sm + ((r - rlo) % NSB) * NF * RWR + t + 1; };
+    auto wait_to = [&](int r) {
+        for (; landed < r; ++landed) {
+            const int rel = landed + 1 - rlo;
+            mbar_wait(bars + rel % NSB, (rel / NSB) & 1);
+        }
+    };
+    // valid lanes of each phase (the cone) and the output columns of this CTA
+    const bool own = t >= 3 && t < 3 + a.tw;
+    const bool vx_red_ok = c >= 1 && c <= g.nvxj;
+    const bool vx_blk_ok = vx_red_ok && t >= 1 && t <= TWR - 2;
+    const bool vy_red_ok = c >= 1 && c <= g.ncx && t >= 2 && t <= TWR - 2;
+    const bool vy_blk_ok = c >= 1 && c <= g.ncx && t >= 3 && t <= TWR - 3;
+    const int s_lo = max(i0 - 2, 1), s_hi = i1 + 6;
+    for (int s = s_lo; s <= s_hi; ++s) {
+        wait_to(min(s + 1, rhi));
+        const bool red = ((s + c + g.par) & 1) == 0;
+        // ---- vx: red node of row s or black node of row s-2
+        if (role != 1) {
+            const int r = red ? s : s - 2;
+            const bool act = red ? (vx_red_ok && r <= min(i1 + 3, g.ncy))
+                                 : (vx_blk_ok && r >= max(i0 - 1, 1) && r <= min(i1 + 2, g.ncy));
+            if (act) {
+                double *sb = slot_of(r);
+                const SmB w{slot_of(r - 1), sb, slot_of(r + 1)};
+                const RowX x = lx_win(g, w, r);
+                const double b = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
+                const double vn = w.B(F_VX) + a.omega * (b - x.L) * rcp(x.a);
+                sb[F_VX * RWR] = vn;
+                if (own && r >= i0 && r <= i1) {
+                    a.vxo[(size_t)r * P + c] = vn;
+                    if (r == 1 && g.bN) a.vxo[c] = g.sN * vn;
+                    if (r == g.ncy && g.bS) a.vxo[(size_t)(g.ncy + 1) * P + c] = g.sS * vn;
+                }
+            }
+        }
+        // ---- vy: red node of row s-4 or black node of row s-6
+        if (role != 0) {
+            const int r = red ? s - 4 : s - 6;
+            const bool act = red ? (vy_red_ok && r >= max(i0 - 1, 1) && r <= min(i1 + 1, g.nvyi))
+                                 : (vy_blk_ok && r >= i0 && r <= min(i1, g.nvyi));
+            if (act) {
+                double *sb = slot_of(r);
+                const SmB w{slot_of(r - 1), sb, slot_of(r + 1)};
+                const RowX y = ly_win(g, w, c);
+                const double b = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
+                const double vn = w.B(F_VY) + a.omega * (b - y.L) * rcp(y.a);
+                sb[F_VY * RWR] = vn;
+                if (own && r >= i0 && r <= i1) {
+                    a.vyo[(size_t)r * P + c] = vn;
+                    if (c == 1 && g.bW) a.vyo[(size_t)r * P] = g.sW * vn;
+                    if (c == g.ncx && g.bE) a.vyo[(size_t)r * P + g.ncx + 1] = g.sE * vn;
+                }
+            }
+        }
+        __syncthreads();
+        // row s-7 was last read by the vy black update of row s-6: its slot takes s-7+NSB
+        if (tt == 0 && s - 7 >= rlo && s - 7 + NSB <= rhi) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(s - 7 + NSB);
+        }
+    }
+}
+
 int jt_tw(const GridL &g) {  // two-sweep pass: output columns per CTA (even, <= JT - 2)
     const int ncb = (g.ncx + JT - 3) / (JT - 2);
     int tw = (g.ncx + ncb - 1) / ncb;
@@ -1116,7 +1250,7 @@ int jt_tw(const GridL &g) {  // two-sweep pass: output columns per CTA (even, <=
 dim3 jt_grid(const GridL &g, int *H) {
     const int tw = jt_tw(g);
     const int ncb = (g.ncx + tw - 1) / tw;
-    int strips = slots() / ncb;
+    int strips = slots() / MINB * J2_MINB / ncb;  // resident two-sweep CTAs: SMs x J2_MINB
     if (strips < 1) strips = 1;
     int h = (g.ncy + strips - 1) / strips;
     if (h < 4) h = 4;
@@ -1205,7 +1339,7 @@ void launch_jacobi2_part(const LaunchCtx &c, const GridL &g, const double *etab,
     a.tw = (cols + ncb - 1) / ncb;
     a.tw += a.tw & 1;
     ncb = (cols + a.tw - 1) / a.tw;
-    int strips = (slots() - MINB * reserve_sms()) / ncb;
+    int strips = (slots() / MINB - reserve_sms()) * J2_MINB / ncb;
     if (strips < 1) strips = 1;
     int H = (rows + strips - 1) / strips;
     if (H < 4) H = 4;
@@ -1328,6 +1462,51 @@ void rbgs_pass(const LaunchCtx &c, const GridL &g, const J2Args &a) {
     ++*c.counter;
 }
 
+// one wave of one-pass CTAs over the level; false (use the two component passes) when the
+// strips would be shorter than RB1_HMIN rows: each strip recomputes 7 rows and runs H + 8
+// barrier steps, which the smaller levels do not amortise (layered 4096^2 RBGS solve with
+// the one-pass kernel on every level >= 128^2: 1521 ms vs 1331 ms with two passes, r02)
+#ifndef RB1_HMIN
+#define RB1_HMIN 32
+#endif
+int rbgs1_mode();
+template <int MODE>
+bool rbgs1(const LaunchCtx &c, const GridL &g, const J2Args &a0) {
+    static unsigned long long done = 0;
+    static int per_sm[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (first_on_device(&done)) {
+        cudaFuncSetAttribute(k_rbgs1<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMB);
+        int nb = 0, nsm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_rbgs1<MODE>, NTB, SMEMB);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        per_sm[dev & 63] = (nb > 0 ? nb : 1) * nsm;
+    }
+    J2Args a = a0;
+    a.tw = TWR - 6;
+    a.tw -= a.tw & 1;
+    const int ncb = (g.ncx + a.tw - 1) / a.tw;
+    int strips = per_sm[dev & 63] / ncb;  // one wave of CTAs covers the level
+    if (strips < 1) strips = 1;
+    int H = (g.ncy + strips - 1) / strips;
+    if (rbgs1_mode() != 2 && H < RB1_HMIN) return false;
+    if (H < 8) H = 8;
+    k_rbgs1<MODE><<<dim3(ncb, (g.ncy + H - 1) / H), NTB, SMEMB, c.stream>>>(g, a, H);
+    ++*c.counter;
+    return true;
+}
+// STOKES_RBGS1=0: the two component passes also on single domains (comparison); =2: the
+// one-pass kernel on every streamed single-domain level (strips >= 8 rows; parity tests)
+int rbgs1_mode() {
+    static const int v = [] {
+        const char *e = getenv("STOKES_RBGS1");
+        return e ? atoi(e) : 1;
+    }();
+    return v;
+}
+bool rbgs1_enabled() { return rbgs1_mode() != 0; }
+
 void launch_rbgs_stream(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
                         const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
                         double omega) {
@@ -1339,6 +1518,10 @@ void launch_rbgs_stream(const LaunchCtx &c, const GridL &g, const double *etab, 
     const bool fine = rhs.mode == RHS_FINE;
     a.gx = fine ? rhs.gx : 0.0;
     a.gy = fine ? rhs.gy : 0.0;
+    if (g.bN && g.bS && g.bW && g.bE && rbgs1_enabled()) {  // single domain: all four phases in one pass
+        fill_src(a.src, vxi, vyi, etap, etab, fine ? rhs.p : rhs.bx, fine ? rhs.rho : rhs.by);
+        if (fine ? rbgs1<RHS_FINE>(c, g, a) : rbgs1<RHS_ARRAYS>(c, g, a)) return;
+    }
     // pass 0: vx (reads vy old), pass 1: vy (reads the new vx)
     fill_src(a.src, vxi, vyi, etap, etab, fine ? rhs.p : rhs.bx, fine ? rhs.rho : rhs.by);
     if (fine) rbgs_pass<0, RHS_FINE>(c, g, a);

@@ -100,3 +100,18 @@ def test_solcx_2048_converged_solution_properties():
     # GCR exits only when the TRUE residual passes too, and reports that E
     assert E <= pre["rtol"]
     assert r["E"] == pytest.approx(E, rel=1e-6)
+
+
+@pytest.mark.parametrize("smoother,nsweeps", [(1, 1), (0, 2)])
+def test_fine_smoothers_4096(smoother, nsweeps):
+    """The fine-level smoother kernels at the bench size, element by element: one RBGS sweep
+    (the one-pass four-phase kernel, whose strips are only tall enough at the large levels)
+    and one two-sweep Jacobi pass, on the layered 4096^2 fields with random iterates."""
+    o, s, pre, w = setup("layered", smoother=smoother)
+    n = pre["n"][0]
+    f = parity_fields(n, n, log_contrast=1.0)
+    rng = np.random.default_rng(5)
+    bx, by = rng.standard_normal((n, n + 1)), rng.standard_normal((n + 1, n))
+    ex, ey = o.smooth(0, bx, by, f["vx"], f["vy"], nsweeps)
+    gx, gy = s.smooth(0, T(bx), T(by), T(f["vx"]), T(f["vy"]), nsweeps)
+    assert rel(gx, ex) <= 1e-12 and rel(gy, ey) <= 1e-12

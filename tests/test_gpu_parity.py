@@ -6,6 +6,8 @@ vx, vy, p <= 1e-9 relative L2 at equal residual tolerance with iteration counts 
 +-1.  Sizes span several 32x8 tiles with ragged tails (33 x 17, 130 x 66) and the
 degenerate smallest grids; full BASELINE sizes are covered in test_gpu_fullsize.py.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -18,6 +20,7 @@ from synth.fields import parity_fields, workload  # noqa: E402
 BCS = [(0, 0, 0, 0), (1, 1, 1, 1), (0, 1, 1, 0)]
 SIZES = [(8, 8), (33, 17), (130, 66), (256, 256)]
 TOL_OP = 1e-12
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def rel(a, b):
@@ -95,8 +98,9 @@ def test_smoother(S, smoother, nx, ny, bc):
 @pytest.mark.parametrize("bc", BCS)
 def test_streamed_smoothers(S, nx, ny, bc, smoother, nsweeps):
     """Levels >= 128 x 8 run Jacobi sweep pairs as one temporally blocked pass (two sweeps
-    per HBM read) and RBGS sweeps as two streamed passes (red row s + black row s-2 per
-    step); ragged column tiles, 4-row strips and every mirror ghost included."""
+    per HBM read) and RBGS sweeps as one streamed pass (the four phases as a wavefront:
+    vx red row s, vx black s-2, vy red s-4, vy black s-6 per step); ragged column tiles,
+    8-row strips and every mirror ghost included."""
     f = parity_fields(nx, ny, log_contrast=1.0)
     o, s = pair(S, nx, ny, bc, f, smoother=smoother, omega_v=0.5, coarse_min=4, coarse_direct=0)
     rng = np.random.default_rng(11)
@@ -107,6 +111,49 @@ def test_streamed_smoothers(S, nx, ny, bc, smoother, nsweeps):
     ex, ey = o.smooth(0, bx, by, vx, vy, nsweeps)
     gx, gy = s.smooth(0, T(bx), T(by), T(vx), T(vy), nsweeps)
     assert rel(gx, ex) <= TOL_OP and rel(gy, ey) <= TOL_OP
+
+
+def test_one_pass_rbgs_forced():
+    """The one-pass four-phase RBGS kernel on every streamed level (STOKES_RBGS1=2, in a
+    subprocess: the mode is read once per process) on ragged grids, all BC sets, 1-3 sweeps
+    and a V-cycle, against the oracle (<= 1e-12)."""
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, %r)
+from oracle.oracle import Oracle
+from synth.fields import parity_fields
+from paper_2603_14040_b200 import Stokes
+T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+rel = lambda a, b: float(np.linalg.norm(a.cpu().numpy() - b) / np.linalg.norm(b))
+worst = 0.0
+for (nx, ny) in [(128, 40), (300, 250), (1030, 23)]:
+    for bc in [(0, 0, 0, 0), (1, 1, 1, 1), (0, 1, 1, 0)]:
+        f = parity_fields(nx, ny, log_contrast=1.0)
+        kw = dict(smoother=1, omega_v=0.5, coarse_min=4, coarse_direct=0)
+        o, s = Oracle(nx, ny, 1.0, 1.0, bc, **kw), Stokes(nx, ny, 1.0, 1.0, bc, **kw)
+        o.set_viscosity(f["eta_b"], f["eta_p"]); s.set_viscosity(T(f["eta_b"]), T(f["eta_p"]))
+        o.set_density(f["rho_b"]); s.set_density(T(f["rho_b"]))
+        o.set_gravity(0.2, 1.0); s.set_gravity(0.2, 1.0)
+        rng = np.random.default_rng(13)
+        bx, by = rng.standard_normal((ny, nx + 1)), rng.standard_normal((ny + 1, nx))
+        vx, vy = rng.standard_normal((ny, nx + 1)), rng.standard_normal((ny + 1, nx))
+        vx[:, [0, -1]] = 0.0
+        vy[[0, -1], :] = 0.0
+        for k in (1, 3):
+            ex, ey = o.smooth(0, bx, by, vx, vy, k)
+            gx, gy = s.smooth(0, T(bx), T(by), T(vx), T(vy), k)
+            worst = max(worst, rel(gx, ex), rel(gy, ey))
+        ex, ey = o.vcycle(bx, by, vx, vy)
+        gx, gy = s.vcycle(T(bx), T(by), T(vx), T(vy))
+        worst = max(worst, rel(gx, ex), rel(gy, ey))
+print(worst)
+""" % ROOT
+    env = dict(os.environ, STOKES_RBGS1="2")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= TOL_OP
 
 
 @pytest.mark.parametrize("tile,tin,nsweeps", [(8, 2, 3), (32, 4, 5), (5, 3, 8)])
@@ -208,6 +255,7 @@ CASES = [
     ("mms", 64, dict(omega_v=0.6, alpha_p=1.0, smoother=1)),
     ("block", 64, dict(omega_v=0.6, alpha_p=1.0, accel=1, gcr_restart=30)),
     ("layered", 128, dict(omega_v=0.6, alpha_p=1.0)),
+    ("layered", 256, dict(omega_v=0.6, alpha_p=1.0, smoother=1)),
     ("solcx", 128, dict(omega_v=0.6, alpha_p=1.0, accel=1)),
     ("random", 128, dict(omega_v=0.6, alpha_p=1.0)),
 ]
@@ -337,6 +385,7 @@ def test_fused_uzawa_fixed_iterations(S, nx, ny, k):
 @pytest.mark.parametrize("name,n,opts", [
     ("block", 64, dict(omega_v=0.6, alpha_p=1.0)),
     ("layered", 128, dict(omega_v=0.6, alpha_p=1.0)),
+    ("layered", 256, dict(omega_v=0.6, alpha_p=1.0, smoother=1)),
     ("block", 128, dict(omega_v=0.6, alpha_p=1.0, accel=1, gcr_restart=20)),
 ])
 def test_viscosity_rescaling_parity(S, name, n, opts):

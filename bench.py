@@ -116,18 +116,26 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def fine_launches(nu, fused):
-    """Fine-level launches per V-cycle (driver.cu vcycle / smooth): the Uzawa update fused into
-    the first pre-sweep (Uzawa mode), sweep pairs as two-sweep passes with an even pair count."""
+def fine_launches(nu, fused, jju=True):
+    """Fine-level launches per V-cycle (driver.cu vcycle / smooth / solve_uzawa_fused): the
+    Uzawa update fused into the first pre-sweep (Uzawa mode) and, with k_jju, the last
+    post-sweep fused into that pass too; sweep pairs as two-sweep passes (an even pair count
+    without k_jju)."""
     pre_n = nu - (1 if fused else 0)
-    pre, post = pre_n // 2, nu // 2
-    if (pre + post) % 2:
+    post_n = nu - (1 if fused and jju else 0)
+    pre, post = pre_n // 2, post_n // 2
+    if not (fused and jju) and (pre + post) % 2:
         if post > 0:
             post -= 1
         else:
             pre -= 1
-    return {"jacobi2": pre + post, "jacobi": pre_n - 2 * pre + nu - 2 * post, "jacobi_uzawa": 1 if fused else 0,
-            "residual_restrict": 1, "prolong": 1}
+    out = {"jacobi2": pre + post, "jacobi": pre_n - 2 * pre + post_n - 2 * post,
+           "residual_restrict": 1, "prolong": 1}
+    if fused and jju:
+        out["jju"] = 1
+    elif fused:
+        out["jacobi_uzawa"] = 1
+    return out
 
 
 def ncu_traffic(kernel_bytes_key, name="ncu_jacobi2_traffic.json"):
@@ -408,10 +416,11 @@ def run_ours(args, world, rank, local):
         kh.set_density(rho)
         kh.set_gravity(w["gx"], w["gy"])
     peak, peak_src = measured_peak()
-    counts = fine_launches(shp[0][2], opts.get("accel", 0) == 0 and vpi == 1)
+    counts = fine_launches(shp[0][2], opts.get("accel", 0) == 0 and vpi == 1,
+                           jju=world == 1 and os.environ.get("STOKES_JJU", "1") != "0")
     its = statistics.mean(iters)
     kernels = {}
-    for name in ("jacobi2", "jacobi", "jacobi_uzawa", "residual_restrict", "prolong"):
+    for name in ("jacobi2", "jju", "jacobi", "jacobi_uzawa", "residual_restrict", "prolong"):
         try:
             km, kb = kh.time_kernel(name, reps=20)
         except Exception:

@@ -223,8 +223,9 @@ int stokes_launch_count(stokes_t h, long long *count, int reset);
  * 4 pressure update (fused with the energy residual), 5 RBGS sweep (4 phases), 6 pressure
  * update + energy residual + first Jacobi sweep of the next V-cycle, 7 two Jacobi sweeps in
  * one pass (6 and 7: fine grid >= 128 x 8 only, else STOKES_EINVAL), 8 one RAS outer
- * iteration (ras_inner sweeps on shared-memory tiles).  Uses the
- * handle's current fields. */
+ * iteration (ras_inner sweeps on shared-memory tiles), 9 the last post-smoothing sweep of a
+ * V-cycle fused with kernel 6 (k_jju; single-domain fine grid >= 128 x 8, else EINVAL).
+ * Uses the handle's current fields. */
 int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double *bytes);
 
 /* ---- marker-in-cell ------------------------

@@ -308,7 +308,7 @@ static bool vtail_ok(stokes_s *h, int l) {
     return true;
 }
 void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in,
-            int done_pre) {
+            int done_pre, int leave_last, double **lx, double **ly) {
     Level &L = h->lev[l];
     const LaunchCtx c = ctx(h);
     if (zero_in && !done_pre && rhs.mode == RHS_ARRAYS && vtail_ok(h, l)) {
@@ -358,10 +358,10 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
     Level &C = h->lev[l + 1];
     // each two-sweep pass saves one buffer swap: keep the pair count even so that the
     // 2 nu sweeps of the cycle end in (ax, ay) without a copy
-    const int pre_n = L.nu - done_pre;
+    const int pre_n = L.nu - done_pre, post_n = L.nu - leave_last;
     int pre_pairs = jacobi_pairs(h, l, pre_n, zero_in && !done_pre);
-    int post_pairs = jacobi_pairs(h, l, L.nu, false);
-    if ((pre_pairs + post_pairs) & 1) {
+    int post_pairs = jacobi_pairs(h, l, post_n, false);
+    if (!leave_last && ((pre_pairs + post_pairs) & 1)) {
         if (post_pairs > 0) --post_pairs;
         else --pre_pairs;
     }
@@ -374,7 +374,12 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
     }
     vcycle(h, l + 1, C.vx[0], C.vy[0], C.vx[1], C.vy[1], rhs_arrays(C.bx, C.by), true);  // (4)
     launch_prolong(c, L.g, C.g, C.vx[0], C.vy[0], cx, cy);                    // (5) correction
-    smooth(h, l, cx, cy, ox, oy, rhs, L.nu, false, post_pairs);              // (6) post-smoothing
+    smooth(h, l, cx, cy, ox, oy, rhs, post_n, false, post_pairs);            // (6) post-smoothing
+    if (leave_last) {
+        *lx = cx;
+        *ly = cy;
+        return;
+    }
     if (cx != ax) {
         cudaMemcpyAsync(ax - COL_OFF, cx - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
         cudaMemcpyAsync(ay - COL_OFF, cy - COL_OFF, field_doubles(L.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
@@ -471,7 +476,7 @@ void drop_graphs(stokes_s *h) {
             cudaGraphExecDestroy(h->uzawa_exec[k]);
             h->uzawa_exec[k] = nullptr;
         }
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < 4; ++k)
         if (h->fused_exec[k]) {
             cudaGraphExecDestroy(h->fused_exec[k]);
             h->fused_exec[k] = nullptr;
@@ -550,27 +555,52 @@ void fused_tail(stokes_s *h) {
                        h->scal + S_E, h->scal + S_MSHIFT);
     cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
 }
-// graph body: rest of V-cycle k+1 (its first sweep already in buf 1) on L v = f - G pbuf[pcur],
-// then the fused tail of iterate k+1
-void fused_body(stokes_s *h) {
+// k_jju variant of the tail: the last post-smoothing sweep of the V-cycle rides along.
+// v^(k-1/2) in buffer b (the V-cycle left it there), p^(k-1) = pbuf[pcur]: p^k ->
+// pbuf[1-pcur], E(v^k, p^k), v' -> buffer 1-b.  Returns 1-b (where the next V-cycle starts).
+int fused_tail_jju(stokes_s *h, int b) {
+    Level &F = h->lev[0];
+    const LaunchCtx c = ctx(h);
+    launch_jacobi_jju(c, F.g, F.etab, F.etap, F.vx[b], F.vy[b], F.vx[1 - b], F.vy[1 - b], h->pbuf[h->pcur],
+                      h->pbuf[1 - h->pcur], h->rho, h->gx, h->gy, h->o.pressure_sign * h->o.alpha_p,
+                      h->scal + S_MSHIFT, h->o.omega_v, h->partials);
+    launch_uzawa_final(c, h->partials, jju_blocks(F.g), h->scal + S_SF, 1.0 / ((double)F.g.ncx * F.g.ncy),
+                       h->scal + S_E, h->scal + S_MSHIFT);
+    cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+    return 1 - b;
+}
+// graph body: rest of V-cycle k+1 (its first sweep already in buffer q) on L v = f - G
+// pbuf[pcur], then the fused tail of iterate k+1.  Returns the buffer of the next first sweep.
+int fused_body(stokes_s *h, int q) {
     Level &F = h->lev[0];
     ras_iteration_start(h);
-    vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false, 1);
-    ras_iteration_end(h);
-    fused_tail(h);
+    int nq = 1;
+    if (jju_ok(F.g)) {
+        double *lx = nullptr, *ly = nullptr;
+        vcycle(h, 0, F.vx[1 - q], F.vy[1 - q], F.vx[q], F.vy[q], rhs_fine(h), false, 1, 1, &lx, &ly);
+        ras_iteration_end(h);
+        nq = fused_tail_jju(h, lx == F.vx[0] ? 0 : 1);
+    } else {
+        vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false, 1);
+        ras_iteration_end(h);
+        fused_tail(h);
+    }
+    return nq;
 }
 int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
     ras_reset(h);
-    const int keep = h->pcur;
-    for (int k = 0; k < 2; ++k) {
-        if (h->fused_exec[k]) continue;
+    Level &F = h->lev[0];
+    const bool jju = jju_ok(F.g);
+    int *next_q = h->fused_nq;  // buffer of the first sweep after a body of slot k (set at capture)
+    auto slot_of = [&](int q) { return (q << 1) | h->pcur; };
+    auto ensure = [&](int q) -> int {  // capture the body for (pbuf[pcur], first sweep in buffer q)
+        const int k = slot_of(q);
+        if (h->fused_exec[k]) return STOKES_OK;
         cudaGraph_t graph;
         const long long before = h->launches;
-        h->pcur = k;
         CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-        fused_body(h);
+        next_q[k] = fused_body(h, q);
         cudaError_t e = cudaStreamEndCapture(h->stream, &graph);
-        h->pcur = keep;
         if (e != cudaSuccess) return fail_cuda(e, "graph capture");
         h->fused_kernels = h->launches - before;
         h->launches = before;
@@ -580,15 +610,24 @@ int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *E
             h->fused_exec[k] = nullptr;
             return fail_cuda(e, "graph instantiate");
         }
-    }
-    Level &F = h->lev[0];
+        return STOKES_OK;
+    };
     double E = E0;
     int k = 1, status = STOKES_NOT_CONVERGED;
     // iteration 1: a full V-cycle from (v^0, p^0), then the fused tail of iterate 1
+    int q = 1, b = 0;  // q: buffer of the next first sweep; b: buffer of v^(k-1/2) (k_jju path)
     ras_iteration_start(h);
-    vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false);
-    ras_iteration_end(h);
-    fused_tail(h);
+    if (jju) {
+        double *lx = nullptr, *ly = nullptr;
+        vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false, 0, 1, &lx, &ly);
+        ras_iteration_end(h);
+        b = lx == F.vx[0] ? 0 : 1;
+        q = fused_tail_jju(h, b);
+    } else {
+        vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false);
+        ras_iteration_end(h);
+        fused_tail(h);
+    }
     for (;;) {
         h->pcur ^= 1;  // pbuf[pcur] = p^k
         int st = sync(h);
@@ -599,8 +638,22 @@ int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *E
         if (E <= rtol) { status = STOKES_OK; break; }
         if (k >= h->o.max_iter) break;
         ++k;
-        CK(cudaGraphLaunch(h->fused_exec[h->pcur], h->stream));
+        const int slot = slot_of(q);
+        if ((st = ensure(q))) return st;
+        CK(cudaGraphLaunch(h->fused_exec[slot], h->stream));
         h->launches += h->fused_kernels;
+        q = next_q[slot];
+        b = 1 - q;  // k_jju path: v^(k-1/2) stayed in the buffer the pass read
+    }
+    if (jju) {  // v^k was never stored: one JacobiOp sweep from v^(k-1/2) (buffer b, untouched)
+        RhsArgs r = rhs_fine(h);
+        r.p = h->pbuf[1 - h->pcur];  // p^(k-1)
+        const LaunchCtx c = ctx(h);
+        launch_jacobi(c, F.g, F.etab, F.etap, F.vx[b], F.vy[b], F.vx[1 - b], F.vy[1 - b], r, h->o.omega_v, false);
+        if (b == 0) {  // v^k is now in buffer 1 -> buffer 0
+            cudaMemcpyAsync(F.vx[0] - COL_OFF, F.vx[1] - COL_OFF, field_doubles(F.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
+            cudaMemcpyAsync(F.vy[0] - COL_OFF, F.vy[1] - COL_OFF, field_doubles(F.g) * 8, cudaMemcpyDeviceToDevice, h->stream);
+        }
     }
     *iters = k;
     *Eout = E;
@@ -1415,6 +1468,11 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
             launch_ras_outer(c, g, a, h->scal + S_ITER, 0, true);
             break;
         }
+        case 9:
+            launch_jacobi_jju(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], h->pbuf[h->pcur],
+                              h->pbuf[1 - h->pcur], h->rho, h->gx, h->gy, h->o.alpha_p, h->scal + S_ZERO,
+                              h->o.omega_v, h->partials);
+            break;
         default:
             launch_jacobi_uzawa(c, g, F.etab, F.etap, F.vx[0], F.vy[0], F.vx[1], F.vy[1], h->pbuf[h->pcur],
                                 h->pbuf[1 - h->pcur], h->rho, h->gx, h->gy, h->o.alpha_p, h->scal + S_ZERO,
@@ -1428,13 +1486,15 @@ int stokes_time_kernel(stokes_t h, int kernel, int reps, double *avg_ms, double 
     // 4 fused Uzawa pressure step + energy: read 6, write p; 5 RBGS (4 phases, fused bytes);
     // 6 Uzawa step + energy + first Jacobi sweep of the next V-cycle: read 6, write p, vx, vy;
     // 7 two Jacobi sweeps in one pass: read 6, write 2; 8 one RAS outer iteration (T_inner
-    // sweeps in shared memory): read 6, write 2
-    double per_cell[9] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0, 72.0, 64.0, 64.0};
+    // sweeps in shared memory): read 6, write 2; 9 the last post-smoothing sweep + Uzawa step +
+    // energy + first sweep of the next V-cycle (k_jju): read 6, write p, vx, vy
+    double per_cell[10] = {64.0, 48.0, 64.0 + 16.0 + 4.0, 32.0 + 4.0, 56.0, 64.0, 72.0, 64.0, 64.0, 72.0};
     if (h->nlev > 1 && jacobi2_ok(g)) per_cell[2] = 48.0 + 4.0;  // fused: the residual stays on chip
     // RBGS: one streamed pass on a single domain (read 6 + write 2), else two passes (read 6 + write 1 each)
     if (jacobi2_ok(g) && !(g.bN && g.bS && g.bW && g.bE && rbgs1_enabled())) per_cell[5] = 2 * 56.0;
-    if (kernel < 0 || kernel > 8) return STOKES_EINVAL;
-    if ((kernel == 6 && !stream_ok(g)) || (kernel == 7 && !jacobi2_ok(g))) return STOKES_EINVAL;
+    if (kernel < 0 || kernel > 9) return STOKES_EINVAL;
+    if ((kernel == 6 && !stream_ok(g)) || (kernel == 7 && !jacobi2_ok(g)) || (kernel == 9 && !jju_ok(g)))
+        return STOKES_EINVAL;
     *bytes = per_cell[kernel] * cells;
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));

@@ -63,7 +63,8 @@ struct stokes_s {
     double gx, gy;
     long long launches;
     cudaGraphExec_t uzawa_exec[2];  // iteration reading pbuf[k]
-    cudaGraphExec_t fused_exec[2];  // fused-tail iteration reading pbuf[k] (a12 fusion)
+    cudaGraphExec_t fused_exec[4];  // fused-tail iteration reading pbuf[k & 1], first sweep in buffer k >> 1 (a12 fusion)
+    int fused_nq[4];                // buffer of the next first sweep after graph k
     long long fused_kernels;
     long long uzawa_kernels;
     void *mk_ws;        // marker-in-cell scratch (markers.cu), grown on demand
@@ -121,8 +122,10 @@ bool uses_ras(const stokes_s *h);
 void ras_iteration_start(stokes_s *h);  // before the V-cycle(s) of one iteration
 void ras_reset(stokes_s *h);            // iteration index 0
 void ras_iteration_end(stokes_s *h);    // after them (advances the device iteration index)
+// leave_last (level l only): the post-smoothing stops one sweep early (the fused k_jju pass
+// does the last one); no final copy, *lx / *ly = the buffer holding that iterate
 void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in,
-            int done_pre = 0);
+            int done_pre = 0, int leave_last = 0, double **lx = nullptr, double **ly = nullptr);
 int sync(stokes_s *h);
 inline void record_E(stokes_s *h, int k, double E) {  // E after iteration k + 1 of the current solve stage
     const int q = h->hist_off + k;

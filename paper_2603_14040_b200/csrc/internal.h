@@ -113,6 +113,14 @@ void launch_residual_stream(const LaunchCtx &c, const GridL &g, const double *et
 // two Jacobi sweeps in one pass (single-domain levels with jacobi2_ok)
 bool jacobi2_ok(const GridL &g);
 bool rbgs1_enabled();  // one-pass RBGS on single domains (STOKES_RBGS1=0 disables it)
+// the last post-smoothing Jacobi sweep + the fused Uzawa step (JacobiUzawaOp) in one pass
+// (k_jju, single domains; STOKES_JJU=0 disables it); partials: 3 per block, jju_blocks(g)
+bool jju_ok(const GridL &g);
+int jju_blocks(const GridL &g);
+void launch_jacobi_jju(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                       const double *vxi, const double *vyi, double *vxo, double *vyo, const double *pin, double *pout,
+                       const double *rho, double gx, double gy, double alpha_signed, const double *mshift,
+                       double omega, double *partials);
 void launch_jacobi2(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vxi,
                     const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega);
 // split passes of decomposed tiles (halo exchange overlapped with the interior): part 0 = the

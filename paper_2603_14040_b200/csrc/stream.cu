@@ -79,13 +79,13 @@ struct Win {
             f[k].B = f[k].C;
         }
     }
-    template <int NFU>
+    template <int NFU, int ROW = RW>
     __device__ __forceinline__ void push(const double *slot, int t) {  // t = column offset in the segment
 #pragma unroll
         for (int k = 0; k < NFU; ++k) {
             f[k].A = f[k].B;
             f[k].B = f[k].C;
-            const double *s = slot + k * RW + t;
+            const double *s = slot + k * ROW + t;
             f[k].C.l = s[-1];
             f[k].C.c = s[0];
             f[k].C.r = s[1];
@@ -879,6 +879,230 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
         for (int s = sfirst; s <= slast; ++s) step(std::true_type(), s);
 }
 
+// ---- the last post-smoothing sweep of V-cycle k fused with the Uzawa step of iterate k and
+// the first pre-smoothing sweep of V-cycle k+1 (a4 + a10 + a3 + a4) ------
+// Stage 1 (row s) is the Jacobi sweep of JacobiOp on L v = f - G p^(k-1) from v^(k-1/2) (the
+// last post-smoothing sweep: its output is v^k); stage 2 (row s-1) is JacobiUzawaOp on v^k
+// held in shared memory like sweep 2 of k_jacobi2: p^k = (p^(k-1) - mshift) + alpha eta_P
+// (-D v^k), the partial sums of E(v^k, p^k) and v' = v^k + omega (f - L v^k - G p^k)/a_ii.
+// One HBM pass instead of two (JacobiOp + JacobiUzawaOp).  v^k itself is not written: when
+// E(v^k, p^k) <= rtol the solver recomputes it with one JacobiOp sweep from v^(k-1/2), which
+// this pass leaves untouched (driver.cu solve_uzawa_fused).  Single domains.
+#ifndef JJ_T
+#define JJ_T 256
+#endif
+#ifndef JJ_MINB
+#define JJ_MINB 2
+#endif
+constexpr int JJT = JJ_T, JJRW = JJT + 4;
+constexpr int SMEMJJ = NSJ * NF * JJRW * 8 + 4 * 2 * JJT * 8 + NSJ * 8;
+
+struct JJArgs {
+    const double *src[6];  // v^(k-1/2) x, y, eta_p, eta_b, p^(k-1), rho
+    double *vxo, *vyo, *po;
+    const double *mshift;
+    double omega, alpha_s, gx, gy;
+    int tw;
+};
+struct W2J {  // stage-2 view of row s-1: v^k from the intermediate rows, the rest one row back
+    const V3 *v;
+    R3 vx[3], vy[3];
+    double lag_eb, lag_5;  // eta_b, rho of row s-2
+    __device__ __forceinline__ double A(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[0], dc) : k == F_VY ? pick(vy[0], dc) : k == F_EB ? lag_eb : lag_5;
+    }
+    __device__ __forceinline__ double B(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[1], dc) : k == F_VY ? pick(vy[1], dc) : pick(v->A[k], dc);
+    }
+    __device__ __forceinline__ double C(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[2], dc) : k == F_VY ? pick(vy[2], dc) : pick(v->B[k], dc);
+    }
+};
+
+__global__ void __launch_bounds__(JJT, JJ_MINB) k_jju(GridL g, JJArgs a, int H, double *__restrict__ partials) {
+    extern __shared__ __align__(128) double sm[];
+    double *s1 = sm + NSJ * NF * JJRW;  // [4 rows][vx^k, vy^k][JJT]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(s1 + 4 * 2 * JJT);
+    __shared__ double red[JJT / 32];
+    const int t = threadIdx.x;
+    const int j0 = 1 + a.tw * blockIdx.x;
+    const int c = j0 - 1 + t;
+    const int i0 = 1 + blockIdx.y * H;
+    const int i1 = min(i0 + H - 1, g.ncy);
+    const int rlo = max(i0 - 2, 0), rhi = min(i1 + 2, g.ncy + 1);
+    const int sfirst = max(i0 - 1, 0), slast = min(i1 + 1, g.ncy + 1);
+    const size_t P = g.P;
+    auto issue = [&](int r) {
+        const int slot = (r - rlo) % NSJ;
+        uint64_t *bar = bars + slot;
+        mbar_expect_tx(bar, NF * JJRW * 8);
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            bulk_g2s(sm + (slot * NF + f) * JJRW, a.src[f] + (size_t)r * P + (j0 - 2), JJRW * 8, bar);
+    };
+    if (t == 0) {
+        for (int k = 0; k < NSJ; ++k) mbar_init(bars + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (t == 0)
+        for (int r = rlo; r < rlo + NSJ && r <= rhi; ++r) issue(r);
+    auto row_at = [&](int r) {
+        const int rel = r - rlo;
+        mbar_wait(bars + rel % NSJ, (rel / NSJ) & 1);
+        return sm + (rel % NSJ) * NF * JJRW + t + 1;
+    };
+    V3 v;
+    auto pullB = [&](const double *q) {
+        v.B[F_VX] = R3{q[-1], q[0], q[1]};
+        v.B[F_VY] = R3{q[JJRW - 1], q[JJRW], q[JJRW + 1]};
+        v.B[F_EP].c = q[F_EP * JJRW];
+        v.B[F_EP].r = q[F_EP * JJRW + 1];
+        v.B[F_EB].l = q[F_EB * JJRW - 1];
+        v.B[F_EB].c = q[F_EB * JJRW];
+        v.B[F_4].c = q[F_4 * JJRW];
+        v.B[F_4].r = q[F_4 * JJRW + 1];
+        v.B[F_5].l = q[F_5 * JJRW - 1];
+        v.B[F_5].c = q[F_5 * JJRW];
+    };
+    auto pullC = [&](const double *q) {
+        v.C[F_VX].l = q[-1];
+        v.C[F_VX].c = q[0];
+        v.C[F_VY].c = q[JJRW];
+        v.C[F_EP].c = q[F_EP * JJRW];
+        v.C[F_4].c = q[F_4 * JJRW];
+    };
+    auto toA = [&]() {  // row B becomes row A (stage 2 also reads p and rho of it)
+        v.A[F_EB].l = v.B[F_EB].l;
+        v.A[F_EB].c = v.B[F_EB].c;
+        v.A[F_EP].c = v.B[F_EP].c;
+        v.A[F_EP].r = v.B[F_EP].r;
+        v.A[F_VX].c = v.B[F_VX].c;
+        v.A[F_VY].c = v.B[F_VY].c;
+        v.A[F_VY].r = v.B[F_VY].r;
+        v.A[F_4].c = v.B[F_4].c;
+        v.A[F_4].r = v.B[F_4].r;
+        v.A[F_5].l = v.B[F_5].l;
+        v.A[F_5].c = v.B[F_5].c;
+    };
+    auto refill = [&](int r) {
+        if (t == 0 && r + NSJ <= rhi) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(r + NSJ);
+        }
+    };
+    if (rlo < sfirst) {
+        pullB(row_at(rlo));
+        toA();
+        __syncthreads();
+        refill(rlo);
+    }
+    const bool cx_in = c >= 1 && c <= g.nvxj, cy_in = c >= 1 && c <= g.ncx;
+    double iax = 0.0, iay = 0.0, lag_eb = 0.0, lag_5 = 0.0;
+    double acc[3] = {0.0, 0.0, 0.0};
+    const double ms = *a.mshift;
+    const double cp = 1.0 / (2.0 * g.idx2 + 2.0 * g.idy2);
+    auto step = [&](auto edge, int s) {
+        constexpr bool EDGE = decltype(edge)::value;
+        pullB(row_at(s));
+        if (s + 1 <= rhi) pullC(row_at(s + 1));
+        const W1 w{&v};
+        // ---- stage 1, row s: the last post-smoothing sweep (RHS f - G p^(k-1))
+        double vx1 = v.B[F_VX].c, vy1 = v.B[F_VY].c, iax_n = 0.0, iay_n = 0.0;
+        if (!EDGE || (s >= 1 && s <= g.ncy && cx_in)) {
+            const RowX x = lx_win<EDGE>(g, w, s);
+            const double b = fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx;
+            iax_n = rcp(x.a);
+            vx1 = w.B(F_VX) + a.omega * (b - x.L) * iax_n;
+        }
+        if (!EDGE || (s >= 1 && s <= g.nvyi && cy_in)) {
+            const RowX y = ly_win<EDGE>(g, w, c);
+            const double b = fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy;
+            iay_n = rcp(y.a);
+            vy1 = w.B(F_VY) + a.omega * (b - y.L) * iay_n;
+        }
+        s1[((s & 3) * 2 + 0) * JJT + t] = vx1;
+        s1[((s & 3) * 2 + 1) * JJT + t] = vy1;
+        __syncthreads();
+        refill(s);
+        // ---- stage 2, row i = s-1: Uzawa step + energy + first sweep on v^k
+        const int i = s - 1;
+        if (i >= i0 && i <= i1 && t >= 1 && t <= a.tw && c <= g.ncx) {
+            const double *qa = s1 + (((s - 2) & 3) * 2) * JJT + t, *qb = s1 + (((s - 1) & 3) * 2) * JJT + t,
+                         *qc = s1 + ((s & 3) * 2) * JJT + t;
+            W2J u;
+            u.v = &v;
+            u.lag_eb = lag_eb;
+            u.lag_5 = lag_5;
+            u.vx[0] = R3{0.0, qa[0], 0.0};
+            u.vx[1] = R3{qb[-1], qb[0], qb[1]};
+            u.vx[2] = R3{qc[-1], qc[0], 0.0};
+            u.vy[0] = R3{0.0, qa[JJT], qa[JJT + 1]};
+            u.vy[1] = R3{qb[JJT - 1], qb[JJT], qb[JJT + 1]};
+            u.vy[2] = R3{0.0, qc[JJT], 0.0};
+            if (EDGE && i == 1) u.vx[0].c = g.sN * u.vx[1].c;
+            if (EDGE && i == g.ncy) u.vx[2].c = g.sS * u.vx[1].c;
+            if (EDGE && c == 1) u.vy[1].l = g.sW * u.vy[1].c;
+            if (EDGE && c == g.ncx) u.vy[1].r = g.sE * u.vy[1].c;
+            const double dv = (u.B(F_VX) - u.B(F_VX, -1)) * g.idx + (u.B(F_VY) - u.A(F_VY)) * g.idy;
+            const double pn = (u.B(F_4) - ms) + a.alpha_s * u.B(F_EP) * (-dv);
+            a.po[(size_t)i * P + c] = pn;
+            acc[1] += dv * dv * (u.B(F_EP) * cp);
+            acc[2] += pn;
+            if (!EDGE || c <= g.nvxj) {
+                const double de = (u.B(F_VX, 1) - u.B(F_VX)) * g.idx + (u.B(F_VY, 1) - u.A(F_VY, 1)) * g.idy;
+                const double pe = (u.B(F_4, 1) - ms) + a.alpha_s * u.B(F_EP, 1) * (-de);
+                const RowX x = lx_win<EDGE>(g, u, i);
+                const double r = fx_win(u, a.gx) - (pn - pe) * g.idx - x.L;
+                acc[0] -= r * r * iax;
+                const double vn = u.B(F_VX) + a.omega * r * iax;
+                a.vxo[(size_t)i * P + c] = vn;
+                if (EDGE && i == 1) a.vxo[c] = g.sN * vn;
+                if (EDGE && i == g.ncy) a.vxo[(size_t)(g.ncy + 1) * P + c] = g.sS * vn;
+            }
+            if (!EDGE || i <= g.nvyi) {
+                const double ds = (u.C(F_VX) - u.C(F_VX, -1)) * g.idx + (u.C(F_VY) - u.B(F_VY)) * g.idy;
+                const double ps = (u.C(F_4) - ms) + a.alpha_s * u.C(F_EP) * (-ds);
+                const RowX y = ly_win<EDGE>(g, u, c);
+                const double r = fy_win(u, a.gy) - (pn - ps) * g.idy - y.L;
+                acc[0] -= r * r * iay;
+                const double vn = u.B(F_VY) + a.omega * r * iay;
+                a.vyo[(size_t)i * P + c] = vn;
+                if (EDGE && c == 1) a.vyo[(size_t)i * P] = g.sW * vn;
+                if (EDGE && c == g.ncx) a.vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
+            }
+        }
+        lag_eb = v.A[F_EB].c;
+        lag_5 = v.A[F_5].c;
+        toA();
+        iax = iax_n;
+        iay = iay_n;
+    };
+    const bool interior = i0 >= 2 && i1 + 1 <= g.ncy - 1 && j0 >= 2 && j0 + JJT - 2 <= g.ncx - 1;
+    if (interior)
+        for (int s = sfirst; s <= slast; ++s) step(std::false_type(), s);
+    else
+        for (int s = sfirst; s <= slast; ++s) step(std::true_type(), s);
+    // deterministic CTA reduction of (Sv, Sp, sum p^k): fixed xor tree per warp, warps in order
+    const size_t b = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double x = acc[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        __syncthreads();
+        if ((t & 31) == 0) red[t >> 5] = x;
+        __syncthreads();
+        if (t < 32) {
+            x = (t < JJT / 32) ? red[t] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            if (t == 0) partials[b * 3 + k] = x;
+        }
+    }
+}
+
+
 // ---- fine residual fused with its restriction (a3 + a5) --------------------------------
 // A CTA streams fine rows through the TMA landing ring (columns j0-1 .. j0+tw, tw <= TW-2:
 // one redundant column each side), evaluates r = b - L v on each row into an 8-row shared
@@ -895,9 +1119,13 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
 #ifndef RR_MINB
 #define RR_MINB 3
 #endif
+#ifndef RR_TW
+#define RR_TW TW
+#endif
 constexpr int NSRR = RR_NS;      // landing ring depth of the residual+restriction pass
 constexpr int RRR = RR_ROWS;     // residual rows kept for the restriction (>= 5: rows 2I-2..2I+1 + the next)
-constexpr int SMEMRR = NSRR * NF * RW * 8 + RRR * 2 * TW * 8 + NSRR * 8;
+constexpr int RTW = RR_TW, RRW = RTW + 4;  // CTA width (threads = columns) and staged row width
+constexpr int SMEMRR = NSRR * NF * RRW * 8 + RRR * 2 * RTW * 8 + NSRR * 8;
 
 struct RRArgs {
     const double *src[6];  // vx, vy, eta_p, eta_b, p | bx, rho | by
@@ -907,10 +1135,10 @@ struct RRArgs {
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(TW, RR_MINB) k_resrestrict(GridL g, GridL gc, RRArgs a, int HC) {
+__global__ void __launch_bounds__(RTW, RR_MINB) k_resrestrict(GridL g, GridL gc, RRArgs a, int HC) {
     extern __shared__ __align__(128) double sm[];
-    double *rr = sm + NSRR * NF * RW;  // [RRR rows][rx, ry][TW]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(rr + RRR * 2 * TW);
+    double *rr = sm + NSRR * NF * RRW;  // [RRR rows][rx, ry][RTW]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(rr + RRR * 2 * RTW);
     const int t = threadIdx.x;
     const int j0 = 1 + a.tw * blockIdx.x;  // odd: coarse columns (j0+1)/2 ..
     const int c = j0 - 1 + t;
@@ -925,10 +1153,10 @@ __global__ void __launch_bounds__(TW, RR_MINB) k_resrestrict(GridL g, GridL gc, 
     auto issue = [&](int r) {
         const int slot = (r - rlo) % NSRR;
         uint64_t *bar = bars + slot;
-        mbar_expect_tx(bar, NF * RW * 8);
+        mbar_expect_tx(bar, NF * RRW * 8);
 #pragma unroll
         for (int f = 0; f < NF; ++f)
-            bulk_g2s(sm + (slot * NF + f) * RW, a.src[f] + (size_t)r * P + (j0 - 2), RW * 8, bar);
+            bulk_g2s(sm + (slot * NF + f) * RRW, a.src[f] + (size_t)r * P + (j0 - 2), RRW * 8, bar);
     };
     if (t == 0) {
         for (int k = 0; k < NSRR; ++k) mbar_init(bars + k, 1);
@@ -941,7 +1169,7 @@ __global__ void __launch_bounds__(TW, RR_MINB) k_resrestrict(GridL g, GridL gc, 
     auto consume = [&](int r) {
         const int rel = r - rlo;
         mbar_wait(bars + rel % NSRR, (rel / NSRR) & 1);
-        w.template push<NF>(sm + (rel % NSRR) * NF * RW, t + 1);
+        w.template push<NF, RRW>(sm + (rel % NSRR) * NF * RRW, t + 1);
     };
     auto refill = [&](int r) {
         if (t == 0 && r + NSRR <= rhi) {
@@ -971,8 +1199,8 @@ __global__ void __launch_bounds__(TW, RR_MINB) k_resrestrict(GridL g, GridL gc, 
             const double b = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
             ry = b - ly_win(g, w, c).L;
         }
-        rr[((i % RRR) * 2 + 0) * TW + t] = rx;
-        rr[((i % RRR) * 2 + 1) * TW + t] = ry;
+        rr[((i % RRR) * 2 + 0) * RTW + t] = rx;
+        rr[((i % RRR) * 2 + 1) * RTW + t] = ry;
         __syncthreads();
         refill(i + 1);
         // coarse row completed by fine row i (global S side: row ncy + 1 is dropped)
@@ -985,7 +1213,7 @@ __global__ void __launch_bounds__(TW, RR_MINB) k_resrestrict(GridL g, GridL gc, 
                 for (int d = 0; d < 4; ++d) {
                     const int fi = 2 * I - 2 + d;
                     if ((fi < 1 && g.bN) || (fi > g.ncy && g.bS)) continue;
-                    const double *row = rr + ((fi % RRR) * 2 + 0) * TW;
+                    const double *row = rr + ((fi % RRR) * 2 + 0) * RTW;
                     const double h = 0.5 * row[q - 1] + row[q] + 0.5 * row[q + 1];
                     const double wd = (d == 0 || d == 3) ? 0.25 : 0.75;
                     sx += wd * h;
@@ -1000,9 +1228,9 @@ __global__ void __launch_bounds__(TW, RR_MINB) k_resrestrict(GridL g, GridL gc, 
                 for (int d = 0; d < 4; ++d) {
                     const int fj = 2 * J - 2 + d;
                     if ((fj < 1 && g.bW) || (fj > g.ncx && g.bE)) continue;
-                    const double col = 0.5 * rr[(((2 * I - 1) % RRR) * 2 + 1) * TW + q + d] +
-                                       rr[(((2 * I) % RRR) * 2 + 1) * TW + q + d] +
-                                       0.5 * rr[(((2 * I + 1) % RRR) * 2 + 1) * TW + q + d];
+                    const double col = 0.5 * rr[(((2 * I - 1) % RRR) * 2 + 1) * RTW + q + d] +
+                                       rr[(((2 * I) % RRR) * 2 + 1) * RTW + q + d] +
+                                       0.5 * rr[(((2 * I + 1) % RRR) * 2 + 1) * RTW + q + d];
                     const double wd = (d == 0 || d == 3) ? 0.25 : 0.75;
                     sy += wd * col;
                     wsum += wd;
@@ -1421,7 +1649,11 @@ void launch_residual_restrict(const LaunchCtx &c, const GridL &g, const GridL &g
     RRArgs a;
     a.bxc = bxc;
     a.byc = byc;
-    a.tw = j2_tw(g);
+    {  // output columns per CTA: even, <= RTW - 2, balanced over the column blocks
+        const int nb = (g.ncx + RTW - 3) / (RTW - 2);
+        a.tw = (g.ncx + nb - 1) / nb;
+        a.tw += a.tw & 1;
+    }
     const int ncb = (g.ncx + a.tw - 1) / a.tw;
     int strips = slots() / MINB * RR_MINB / ncb;  // one wave at RR_MINB CTAs per SM
     if (strips < 1) strips = 1;
@@ -1436,7 +1668,7 @@ void launch_residual_restrict(const LaunchCtx &c, const GridL &g, const GridL &g
         if (first_on_device(&done)) {
             cudaFuncSetAttribute(k_resrestrict<RHS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMRR);
         }
-        k_resrestrict<RHS_FINE><<<grid, TW, SMEMRR, c.stream>>>(g, gc, a, HC);
+        k_resrestrict<RHS_FINE><<<grid, RTW, SMEMRR, c.stream>>>(g, gc, a, HC);
     } else {
         fill_src(a.src, vx, vy, etap, etab, rhs.bx, rhs.by);
         a.gx = a.gy = 0.0;
@@ -1444,7 +1676,7 @@ void launch_residual_restrict(const LaunchCtx &c, const GridL &g, const GridL &g
         if (first_on_device(&done)) {
             cudaFuncSetAttribute(k_resrestrict<RHS_ARRAYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMRR);
         }
-        k_resrestrict<RHS_ARRAYS><<<grid, TW, SMEMRR, c.stream>>>(g, gc, a, HC);
+        k_resrestrict<RHS_ARRAYS><<<grid, RTW, SMEMRR, c.stream>>>(g, gc, a, HC);
     }
     ++*c.counter;
 }
@@ -1590,6 +1822,54 @@ void launch_jacobi_uzawa(const LaunchCtx &c, const GridL &g, const double *etab,
     op.gx = gx;
     op.gy = gy;
     run(c, g, op, partials);
+}
+
+// single domains whose levels stream (jacobi2_ok); grid = one wave, blocks returned
+static dim3 jju_grid(const GridL &g, int *H, int *tw) {
+    const int nb = (g.ncx + JJT - 3) / (JJT - 2);
+    int w = (g.ncx + nb - 1) / nb;
+    w += w & 1;
+    const int ncb = (g.ncx + w - 1) / w;
+    int strips = slots() / MINB * JJ_MINB / ncb;
+    if (strips < 1) strips = 1;
+    int h = (g.ncy + strips - 1) / strips;
+    if (h < 4) h = 4;
+    *H = h;
+    *tw = w;
+    return dim3(ncb, (g.ncy + h - 1) / h);
+}
+bool jju_ok(const GridL &g) {
+    static const bool on = [] {
+        const char *e = getenv("STOKES_JJU");
+        return !(e && e[0] == '0');
+    }();
+    return on && g.bN && g.bS && g.bW && g.bE && jacobi2_ok(g);
+}
+int jju_blocks(const GridL &g) {
+    int H, tw;
+    const dim3 gr = jju_grid(g, &H, &tw);
+    return (int)(gr.x * gr.y);
+}
+void launch_jacobi_jju(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                       const double *vxi, const double *vyi, double *vxo, double *vyo, const double *pin, double *pout,
+                       const double *rho, double gx, double gy, double alpha_signed, const double *mshift,
+                       double omega, double *partials) {
+    static unsigned long long done = 0;
+    if (first_on_device(&done)) cudaFuncSetAttribute(k_jju, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJJ);
+    JJArgs a;
+    fill_src(a.src, vxi, vyi, etap, etab, pin, rho);
+    a.vxo = vxo;
+    a.vyo = vyo;
+    a.po = pout;
+    a.mshift = mshift;
+    a.omega = omega;
+    a.alpha_s = alpha_signed;
+    a.gx = gx;
+    a.gy = gy;
+    int H = 0;
+    const dim3 grid = jju_grid(g, &H, &a.tw);
+    k_jju<<<grid, JJT, SMEMJJ, c.stream>>>(g, a, H, partials);
+    ++*c.counter;
 }
 
 void launch_uzawa_energy(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,

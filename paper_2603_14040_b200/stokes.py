@@ -448,7 +448,7 @@ class Stokes:
 
     KERNELS = {"jacobi": 0, "energy": 1, "residual_restrict": 2, "prolong": 3, "pupdate": 4, "rbgs": 5,
                "jacobi_uzawa": 6, "jacobi2": 7,
-               "ras": 8}
+               "ras": 8, "jju": 9}
 
     def time_kernel(self, kernel, reps=20):
         ms, nb = ctypes.c_double(), ctypes.c_double()

@@ -477,6 +477,11 @@ void drop_graphs(stokes_s *h) {
             h->uzawa_exec[k] = nullptr;
         }
     for (int k = 0; k < 4; ++k)
+        if (h->loop_exec[k]) {
+            cudaGraphExecDestroy(h->loop_exec[k]);
+            h->loop_exec[k] = nullptr;
+        }
+    for (int k = 0; k < 4; ++k)
         if (h->fused_exec[k]) {
             cudaGraphExecDestroy(h->fused_exec[k]);
             h->fused_exec[k] = nullptr;
@@ -558,7 +563,7 @@ void fused_tail(stokes_s *h) {
 // k_jju variant of the tail: the last post-smoothing sweep of the V-cycle rides along.
 // v^(k-1/2) in buffer b (the V-cycle left it there), p^(k-1) = pbuf[pcur]: p^k ->
 // pbuf[1-pcur], E(v^k, p^k), v' -> buffer 1-b.  Returns 1-b (where the next V-cycle starts).
-int fused_tail_jju(stokes_s *h, int b) {
+int fused_tail_jju(stokes_s *h, int b, bool to_host = true) {
     Level &F = h->lev[0];
     const LaunchCtx c = ctx(h);
     launch_jacobi_jju(c, F.g, F.etab, F.etap, F.vx[b], F.vy[b], F.vx[1 - b], F.vy[1 - b], h->pbuf[h->pcur],
@@ -566,12 +571,12 @@ int fused_tail_jju(stokes_s *h, int b) {
                       h->scal + S_MSHIFT, h->o.omega_v, h->partials);
     launch_uzawa_final(c, h->partials, jju_blocks(F.g), h->scal + S_SF, 1.0 / ((double)F.g.ncx * F.g.ncy),
                        h->scal + S_E, h->scal + S_MSHIFT);
-    cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+    if (to_host) cudaMemcpyAsync(h->hscal, h->scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
     return 1 - b;
 }
 // graph body: rest of V-cycle k+1 (its first sweep already in buffer q) on L v = f - G
 // pbuf[pcur], then the fused tail of iterate k+1.  Returns the buffer of the next first sweep.
-int fused_body(stokes_s *h, int q) {
+int fused_body(stokes_s *h, int q, bool to_host = true) {
     Level &F = h->lev[0];
     ras_iteration_start(h);
     int nq = 1;
@@ -579,7 +584,7 @@ int fused_body(stokes_s *h, int q) {
         double *lx = nullptr, *ly = nullptr;
         vcycle(h, 0, F.vx[1 - q], F.vy[1 - q], F.vx[q], F.vy[q], rhs_fine(h), false, 1, 1, &lx, &ly);
         ras_iteration_end(h);
-        nq = fused_tail_jju(h, lx == F.vx[0] ? 0 : 1);
+        nq = fused_tail_jju(h, lx == F.vx[0] ? 0 : 1, to_host);
     } else {
         vcycle(h, 0, F.vx[0], F.vy[0], F.vx[1], F.vy[1], rhs_fine(h), false, 1);
         ras_iteration_end(h);
@@ -587,6 +592,119 @@ int fused_body(stokes_s *h, int q) {
     }
     return nq;
 }
+// ---- device-side Uzawa loop (a12 stopping test on the GPU) -------------------------------
+// After iteration 1 the rest of the solve is ONE graph launch: a conditional WHILE node whose
+// body runs two fused iterations (the two parities of the pressure / sweep buffers), each
+// followed by k_loop_check (E history, divergence guard, E <= rtol, max_iter -- the host
+// loop's tests, on the device); the second half sits in a conditional IF node so the loop
+// can stop after either.  The host synchronises once per solve instead of once per
+// iteration.  STOKES_DEVICE_LOOP=0 keeps the host loop.
+constexpr int LOOP_RUNNING = 100;
+__global__ void k_loop_check(double *scal, double *dhist, cudaGraphConditionalHandle hnext,
+                             cudaGraphConditionalHandle hstop, int has_stop) {
+    double *L = scal + S_LOOP;
+    const double E = scal[S_E];
+    const int k = (int)L[3] + 1;
+    L[3] = k;
+    L[5] = E;
+    if (k - 1 < LOOP_HCAP) dhist[k - 1] = E;
+    int st = LOOP_RUNNING;
+    if (!(E == E) || isinf(E) || E > 1e6 * L[1]) st = STOKES_EDIVERGED;
+    else if (E <= L[0]) st = STOKES_OK;
+    else if (k >= (int)L[2]) st = STOKES_NOT_CONVERGED;
+    L[4] = st;
+    cudaGraphSetConditional(hnext, st == LOOP_RUNNING ? 1u : 0u);
+    if (has_stop && st != LOOP_RUNNING) cudaGraphSetConditional(hstop, 0u);
+}
+static bool device_loop_env() {
+    static const bool v = [] {
+        const char *e = getenv("STOKES_DEVICE_LOOP");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+// capture the loop graph entered in state (q, pcur); leaves h->pcur unchanged
+static int build_loop(stokes_s *h, int q, int *nq_out) {
+    const int keep = h->pcur;
+    cudaGraph_t G = nullptr;
+    cudaGraphExec_t ex = nullptr;
+    cudaError_t e = cudaGraphCreate(&G, 0);
+    if (e != cudaSuccess) return fail_cuda(e, "loop graph");
+    cudaGraphConditionalHandle hw, hi;
+    cudaGraphNodeParams wp = {};
+    cudaGraphNode_t wn, in;
+    cudaGraph_t BW = nullptr, BI = nullptr;
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    cudaGraph_t cg = nullptr;
+    const long long before = h->launches;
+    long long nk = 0;
+    int q1 = q, q2 = q;
+    e = cudaGraphConditionalHandleCreate(&hw, G, 1, cudaGraphCondAssignDefault);
+    if (e == cudaSuccess) {
+        wp.type = cudaGraphNodeTypeConditional;
+        wp.conditional.handle = hw;
+        wp.conditional.type = cudaGraphCondTypeWhile;
+        wp.conditional.size = 1;
+        e = cudaGraphAddNode(&wn, G, nullptr, 0, &wp);
+    }
+    if (e == cudaSuccess) {
+        BW = wp.conditional.phGraph_out[0];
+        e = cudaGraphConditionalHandleCreate(&hi, BW, 0, cudaGraphCondAssignDefault);
+    }
+    if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(h->stream, BW, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {  // half A: iteration in state (q, pcur), then the check (IF <- continue)
+        q1 = fused_body(h, q, false);
+        nk = h->launches - before;
+        k_loop_check<<<1, 1, 0, h->stream>>>(h->scal, h->dhist, hi, hw, 1);
+        e = cudaStreamGetCaptureInfo(h->stream, &cs, nullptr, &cg, &deps, &nd);
+        if (e == cudaSuccess) {
+            cudaGraphNodeParams ip = {};
+            ip.type = cudaGraphNodeTypeConditional;
+            ip.conditional.handle = hi;
+            ip.conditional.type = cudaGraphCondTypeIf;
+            ip.conditional.size = 1;
+            e = cudaGraphAddNode(&in, cg, deps, nd, &ip);
+            if (e == cudaSuccess) {
+                BI = ip.conditional.phGraph_out[0];
+                e = cudaStreamUpdateCaptureDependencies(h->stream, &in, 1, cudaStreamSetCaptureDependencies);
+            }
+        }
+        cudaGraph_t out = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(h->stream, &out);
+        if (e == cudaSuccess) e = e2;
+    }
+    if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(h->stream, BI, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {  // half B: the other parity, then the check (WHILE <- continue)
+        h->pcur = 1 - keep;
+        q2 = fused_body(h, q1, false);
+        k_loop_check<<<1, 1, 0, h->stream>>>(h->scal, h->dhist, hw, hw, 0);
+        cudaGraph_t out = nullptr;
+        e = cudaStreamEndCapture(h->stream, &out);
+    }
+    h->pcur = keep;
+    h->launches = before;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&ex, G, 0);
+    cudaGraphDestroy(G);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail_cuda(e, "device loop graph");
+    }
+    if (q2 != q) {  // the state after two iterations must be the entry state
+        cudaGraphExecDestroy(ex);
+        g_last_error = "device loop: buffer parity not periodic";
+        return STOKES_ECUDA;
+    }
+    h->loop_exec[(q << 1) | keep] = ex;
+    // the host replays the buffer sequence from these (also what the host-loop graphs record)
+    h->fused_nq[(q << 1) | keep] = q1;
+    h->fused_nq[(q1 << 1) | (1 - keep)] = q2;
+    h->fused_kernels = nk;
+    *nq_out = q1;
+    return STOKES_OK;
+}
+
 int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *Eout) {
     ras_reset(h);
     Level &F = h->lev[0];
@@ -637,6 +755,49 @@ int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *E
         if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
         if (E <= rtol) { status = STOKES_OK; break; }
         if (k >= h->o.max_iter) break;
+        if (jju && k == 1 && device_loop_env() && !h->loop_off) {  // the rest on the device
+            int nq1 = 0;
+            const int li = (q << 1) | h->pcur;
+            if (!h->dhist) {
+                if (cudaMalloc(&h->dhist, LOOP_HCAP * sizeof(double)) != cudaSuccess) {
+                    cudaGetLastError();
+                    h->dhist = nullptr;
+                    h->loop_off = true;
+                }
+            }
+            if (!h->loop_off && !h->loop_exec[li] && build_loop(h, q, &nq1)) h->loop_off = true;
+            if (!h->loop_off) {
+                const double L0[6] = {rtol, E0, (double)h->o.max_iter, 1.0, (double)LOOP_RUNNING, E};
+                memcpy(h->hscal + S_LOOP, L0, sizeof L0);
+                CK(cudaMemcpyAsync(h->scal + S_LOOP, h->hscal + S_LOOP, sizeof L0, cudaMemcpyHostToDevice, h->stream));
+                CK(cudaGraphLaunch(h->loop_exec[li], h->stream));
+                CK(cudaMemcpyAsync(h->hscal + S_LOOP, h->scal + S_LOOP, sizeof L0, cudaMemcpyDeviceToHost, h->stream));
+                if ((st = sync(h))) return st;
+                const int kf = (int)h->hscal[S_LOOP + 3];
+                const int stf = (int)h->hscal[S_LOOP + 4];
+                E = h->hscal[S_LOOP + 5];
+                if (h->hist && kf > 1) {  // E of iterations 2..kf (device history)
+                    const int n = (kf < LOOP_HCAP ? kf : LOOP_HCAP) - 1;
+                    double *tmp = (double *)malloc(n * sizeof(double));
+                    if (!tmp) return STOKES_ENOMEM;
+                    CK(cudaMemcpyAsync(tmp, h->dhist + 1, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+                    if ((st = sync(h))) { free(tmp); return st; }
+                    for (int i = 0; i < n; ++i) record_E(h, i + 1, tmp[i]);
+                    free(tmp);
+                }
+                // replay the state sequence of iterations 2..kf on the host (buffers, pcur)
+                for (int it = 2; it <= kf; ++it) {
+                    const int slot = slot_of(q);
+                    h->launches += h->fused_kernels + 1;  // + k_loop_check
+                    q = next_q[slot];
+                    b = 1 - q;
+                    h->pcur ^= 1;
+                }
+                k = kf;
+                status = stf == LOOP_RUNNING ? STOKES_NOT_CONVERGED : stf;
+                break;
+            }
+        }
         ++k;
         const int slot = slot_of(q);
         if ((st = ensure(q))) return st;
@@ -955,6 +1116,7 @@ int stokes_destroy(stokes_t h) {
     }
     drop_graphs(h);
     if (h->mk_ws) cudaFree(h->mk_ws);
+    if (h->dhist) cudaFree(h->dhist);
     if (h->hscal) cudaFreeHost(h->hscal);
     if (h->own_ws && h->ws) cudaFree(h->ws);
     if (h->own_stream) cudaStreamDestroy(h->stream);

@@ -15,7 +15,10 @@ extern thread_local std::string g_last_error;
 
 // device scalar slots
 enum { S_MSHIFT = 0, S_E = 1, S_SV = 2, S_SP = 3, S_SF = 4, S_SFPART = 5, S_ZMEAN = 8, S_GAMMA = 9, S_NU2 = 10, S_LOC = 16,
-       S_RR = 11, S_BETA = 12, S_ZERO = 13, S_E0 = 14, S_ETAMIN = 24, S_AAMT = 25, S_ITER = 26, S_NSCAL = 64 };
+       S_RR = 11, S_BETA = 12, S_ZERO = 13, S_E0 = 14, S_ETAMIN = 24, S_AAMT = 25, S_ITER = 26,
+       S_LOOP = 40,  // device-side Uzawa loop: [0] rtol [1] E0 [2] max_iter [3] k [4] status [5] E
+       S_NSCAL = 64 };
+constexpr int LOOP_HCAP = 16384;  // device history of E (stokes_solve_hist) in device-loop solves
 
 struct Level {
     GridL g;
@@ -65,6 +68,9 @@ struct stokes_s {
     cudaGraphExec_t uzawa_exec[2];  // iteration reading pbuf[k]
     cudaGraphExec_t fused_exec[4];  // fused-tail iteration reading pbuf[k & 1], first sweep in buffer k >> 1 (a12 fusion)
     int fused_nq[4];                // buffer of the next first sweep after graph k
+    cudaGraphExec_t loop_exec[4];   // device-side Uzawa loop entered in state (q, pcur) = (k >> 1, k & 1)
+    double *dhist;                  // device E history of the device loop (LOOP_HCAP doubles)
+    bool loop_off;                  // device loop unavailable (capture / instantiate failed): host loop
     long long fused_kernels;
     long long uzawa_kernels;
     void *mk_ws;        // marker-in-cell scratch (markers.cu), grown on demand

@@ -2,6 +2,8 @@
 must be the device-resident solve bit for bit (the e2e path of bench.py), and grid shapes
 that size the reduction scratch differently (tall, narrow grids with Anderson) stay in
 bounds and on the oracle."""
+import json
+
 import numpy as np
 import pytest
 
@@ -82,3 +84,44 @@ def test_anderson_tall_grid(S, nx, ny):
     assert abs(a["E"] - b["E"]) <= 1e-8 * a["E"]
     for k in ("vx", "vy", "p"):
         assert rel(b[k], a[k]) <= 1e-9, k
+
+
+def test_device_loop_equals_host_loop():
+    """The device-side Uzawa loop (one conditional-WHILE graph launch per solve: the stopping
+    test, divergence guard and E history on the GPU) against the host loop (STOKES_DEVICE_LOOP
+    =0, one synchronisation per iteration): the same iteration count, E history and fields
+    bit for bit, for a converging solve, a max_iter stop of either parity and a solve that
+    starts from the previous solution (0 or 1 more iteration)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r"""
+import sys, json, hashlib, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2603_14040_b200 import Stokes
+from synth.fields import workload
+w = workload("layered", 256, 256)
+out = []
+for mi in (10000, 7, 8):
+    s = Stokes(256, 256, w["Lx"], w["Ly"], w["bc"], omega_v=0.6, alpha_p=1.0, max_iter=mi)
+    s.set_viscosity(torch.from_numpy(w["eta_b"]).cuda(), torch.from_numpy(w["eta_p"]).cuda())
+    s.set_density(torch.from_numpy(w["rho_b"]).cuda())
+    s.set_gravity(w["gx"], w["gy"])
+    for rep in range(2):
+        r = s.solve(1e-8, hist_len=20000)
+        out.append({"iters": r["iters"], "status": r["status"], "E": r["E"], "hist": list(map(float, r["hist"])),
+                    "f": [float(r[k].double().pow(2).sum()) for k in ("vx", "vy", "p")],
+                    "h": [hashlib.sha1(r[k].cpu().numpy().tobytes()).hexdigest() for k in ("vx", "vy", "p")]})
+    r = s.solve(1e-8, vx=r["vx"], vy=r["vy"], p=r["p"])
+    out.append({"iters": r["iters"], "status": r["status"], "E": r["E"], "hist": [], "f": [], "h": []})
+print(json.dumps(out))
+""" % root
+    res = []
+    for env in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, STOKES_DEVICE_LOOP=env),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert res[0] == res[1]
+    assert res[0][0]["status"] == 0 and res[0][3]["iters"] == 7 and res[0][6]["iters"] == 8

@@ -889,10 +889,10 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
 // E(v^k, p^k) <= rtol the solver recomputes it with one JacobiOp sweep from v^(k-1/2), which
 // this pass leaves untouched (driver.cu solve_uzawa_fused).  Single domains.
 #ifndef JJ_T
-#define JJ_T 256
+#define JJ_T 160  // r02: 160 x 3 CTAs per SM 350.8 us, 256 x 2 356.4, 192 x 2 379.2 (128 registers)
 #endif
 #ifndef JJ_MINB
-#define JJ_MINB 2
+#define JJ_MINB 3
 #endif
 constexpr int JJT = JJ_T, JJRW = JJT + 4;
 constexpr int SMEMJJ = NSJ * NF * JJRW * 8 + 4 * 2 * JJT * 8 + NSJ * 8;

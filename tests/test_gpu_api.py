@@ -109,8 +109,10 @@ for mi in (10000, 7, 8):
     s.set_density(torch.from_numpy(w["rho_b"]).cuda())
     s.set_gravity(w["gx"], w["gy"])
     for rep in range(2):
+        s.launch_count(reset=True)
         r = s.solve(1e-8, hist_len=20000)
         out.append({"iters": r["iters"], "status": r["status"], "E": r["E"], "hist": list(map(float, r["hist"])),
+                    "launches": s.launch_count(),
                     "f": [float(r[k].double().pow(2).sum()) for k in ("vx", "vy", "p")],
                     "h": [hashlib.sha1(r[k].cpu().numpy().tobytes()).hexdigest() for k in ("vx", "vy", "p")]})
     r = s.solve(1e-8, vx=r["vx"], vy=r["vy"], p=r["p"])
@@ -123,5 +125,9 @@ print(json.dumps(out))
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         res.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    # the device loop launches one k_loop_check per iteration after the first (proof it ran)
+    for a, b in zip(res[0], res[1]):
+        if "launches" in a:
+            assert a.pop("launches") - b.pop("launches") == a["iters"] - 1
     assert res[0] == res[1]
     assert res[0][0]["status"] == 0 and res[0][3]["iters"] == 7 and res[0][6]["iters"] == 8

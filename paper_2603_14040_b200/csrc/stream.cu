@@ -808,21 +808,25 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
     double iax = 0.0, iay = 0.0, bxp = 0.0, byp = 0.0, lag_eb = 0.0;
     // one row step s: sweep 1 of row s, sweep 2 of row s-1.  EDGE = false (CTAs whose rows
     // and columns all stay off the boundary): no boundary logic at all.
-    auto step = [&](auto edge, int s) {
-        constexpr bool EDGE = decltype(edge)::value;
+    // ER: row-boundary logic (rows 0, 1 / ncy, ncy+1 of sweep 1, rows 1 / ncy of sweep 2);
+    // EC: column-boundary logic (CTAs whose columns reach a W / E wall).  A single domain
+    // takes the row logic per row step and the column logic per CTA, so the CTAs along the
+    // walls run the plain interior code on almost every row (tiles: both on edge CTAs).
+    auto step = [&](auto er, auto ec, int s) {
+        constexpr bool ER = decltype(er)::value, EC = decltype(ec)::value;
         pullB(row_at(s));
         if (s + 1 <= rhi) pullC(row_at(s + 1));
         const W1 w{&v};
         // ---- sweep 1, row s
         double vx1 = v.B[F_VX].c, vy1 = v.B[F_VY].c, iax_n = 0.0, iay_n = 0.0, bx_n = 0.0, by_n = 0.0;
-        if (!EDGE || (s >= 1 - hN && s <= g.ncy + hS && cx_in)) {
-            const RowX x = lx_win<EDGE>(g, w, s);
+        if ((!ER || (s >= 1 - hN && s <= g.ncy + hS)) && (!EC || cx_in)) {
+            const RowX x = lx_win<ER>(g, w, s);
             bx_n = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
             iax_n = rcp(x.a);
             vx1 = w.B(F_VX) + a.omega * (bx_n - x.L) * iax_n;
         }
-        if (!EDGE || (s >= 1 - hN && s <= g.nvyi + hS && cy_in)) {
-            const RowX y = ly_win<EDGE>(g, w, c);
+        if ((!ER || (s >= 1 - hN && s <= g.nvyi + hS)) && (!EC || cy_in)) {
+            const RowX y = ly_win<EC>(g, w, c);
             by_n = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
             iay_n = rcp(y.a);
             vy1 = w.B(F_VY) + a.omega * (by_n - y.L) * iay_n;
@@ -845,23 +849,23 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
             u.vy[0] = R3{0.0, qa[JT], qa[JT + 1]};
             u.vy[1] = R3{qb[JT - 1], qb[JT], qb[JT + 1]};
             u.vy[2] = R3{0.0, qc[JT], 0.0};
-            if (EDGE && i == 1 && g.bN) u.vx[0].c = g.sN * u.vx[1].c;
-            if (EDGE && i == g.ncy && g.bS) u.vx[2].c = g.sS * u.vx[1].c;
-            if (EDGE && c == 1 && g.bW) u.vy[1].l = g.sW * u.vy[1].c;
-            if (EDGE && c == g.ncx && g.bE) u.vy[1].r = g.sE * u.vy[1].c;
-            if (!EDGE || c <= g.nvxj) {
-                const RowX x = lx_win<EDGE>(g, u, i);
+            if (ER && i == 1 && g.bN) u.vx[0].c = g.sN * u.vx[1].c;
+            if (ER && i == g.ncy && g.bS) u.vx[2].c = g.sS * u.vx[1].c;
+            if (EC && c == 1 && g.bW) u.vy[1].l = g.sW * u.vy[1].c;
+            if (EC && c == g.ncx && g.bE) u.vy[1].r = g.sE * u.vy[1].c;
+            if (!EC || c <= g.nvxj) {
+                const RowX x = lx_win<ER>(g, u, i);
                 const double vn = u.B(F_VX) + a.omega * (bxp - x.L) * iax;
                 a.vxo[(size_t)i * P + c] = vn;
-                if (EDGE && i == 1 && g.bN) a.vxo[c] = g.sN * vn;
-                if (EDGE && i == g.ncy && g.bS) a.vxo[(size_t)(g.ncy + 1) * P + c] = g.sS * vn;
+                if (ER && i == 1 && g.bN) a.vxo[c] = g.sN * vn;
+                if (ER && i == g.ncy && g.bS) a.vxo[(size_t)(g.ncy + 1) * P + c] = g.sS * vn;
             }
-            if (!EDGE || i <= g.nvyi) {
-                const RowX y = ly_win<EDGE>(g, u, c);
+            if (!ER || i <= g.nvyi) {
+                const RowX y = ly_win<EC>(g, u, c);
                 const double vn = u.B(F_VY) + a.omega * (byp - y.L) * iay;
                 a.vyo[(size_t)i * P + c] = vn;
-                if (EDGE && c == 1 && g.bW) a.vyo[(size_t)i * P] = g.sW * vn;
-                if (EDGE && c == g.ncx && g.bE) a.vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
+                if (EC && c == 1 && g.bW) a.vyo[(size_t)i * P] = g.sW * vn;
+                if (EC && c == g.ncx && g.bE) a.vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
             }
         }
         if (J2_LATE) refill(s);
@@ -872,11 +876,27 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
         bxp = bx_n;
         byp = by_n;
     };
-    const bool interior = i0 >= 2 && i1 + 1 <= g.ncy - 1 && j0 >= 2 && j0 + JT - 2 <= g.ncx - 1;
-    if (interior)
-        for (int s = sfirst; s <= slast; ++s) step(std::false_type(), s);
-    else
-        for (int s = sfirst; s <= slast; ++s) step(std::true_type(), s);
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    if (TILE) {  // decomposed tiles: all boundary / halo-ring logic on the edge CTAs
+        const bool interior = i0 >= 2 && i1 + 1 <= g.ncy - 1 && j0 >= 2 && j0 + JT - 2 <= g.ncx - 1;
+        if (interior)
+            for (int s = sfirst; s <= slast; ++s) step(F_(), F_(), s);
+        else
+            for (int s = sfirst; s <= slast; ++s) step(T_(), T_(), s);
+    } else {  // rows 0..2 and ncy..ncy+1 take the row logic (sweep 1 rows 0, 1, ncy, ncy+1; sweep 2 rows 1, ncy)
+        const bool col_edge = !(j0 >= 2 && j0 + JT - 2 <= g.ncx - 1);
+        for (int s = sfirst; s <= slast; ++s) {
+            const bool row_edge = s <= 2 || s >= g.ncy;
+            if (col_edge) {
+                if (row_edge) step(T_(), T_(), s);
+                else step(F_(), T_(), s);
+            } else {
+                if (row_edge) step(T_(), F_(), s);
+                else step(F_(), F_(), s);
+            }
+        }
+    }
 }
 
 // ---- the last post-smoothing sweep of V-cycle k fused with the Uzawa step of iterate k and
@@ -1002,21 +1022,21 @@ __global__ void __launch_bounds__(JJT, JJ_MINB) k_jju(GridL g, JJArgs a, int H, 
     double acc[3] = {0.0, 0.0, 0.0};
     const double ms = *a.mshift;
     const double cp = 1.0 / (2.0 * g.idx2 + 2.0 * g.idy2);
-    auto step = [&](auto edge, int s) {
-        constexpr bool EDGE = decltype(edge)::value;
+    auto step = [&](auto er, auto ec, int s) {  // ER / EC: row / column boundary logic (as k_jacobi2)
+        constexpr bool ER = decltype(er)::value, EC = decltype(ec)::value;
         pullB(row_at(s));
         if (s + 1 <= rhi) pullC(row_at(s + 1));
         const W1 w{&v};
         // ---- stage 1, row s: the last post-smoothing sweep (RHS f - G p^(k-1))
         double vx1 = v.B[F_VX].c, vy1 = v.B[F_VY].c, iax_n = 0.0, iay_n = 0.0;
-        if (!EDGE || (s >= 1 && s <= g.ncy && cx_in)) {
-            const RowX x = lx_win<EDGE>(g, w, s);
+        if ((!ER || (s >= 1 && s <= g.ncy)) && (!EC || cx_in)) {
+            const RowX x = lx_win<ER>(g, w, s);
             const double b = fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx;
             iax_n = rcp(x.a);
             vx1 = w.B(F_VX) + a.omega * (b - x.L) * iax_n;
         }
-        if (!EDGE || (s >= 1 && s <= g.nvyi && cy_in)) {
-            const RowX y = ly_win<EDGE>(g, w, c);
+        if ((!ER || (s >= 1 && s <= g.nvyi)) && (!EC || cy_in)) {
+            const RowX y = ly_win<EC>(g, w, c);
             const double b = fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy;
             iay_n = rcp(y.a);
             vy1 = w.B(F_VY) + a.omega * (b - y.L) * iay_n;
@@ -1040,36 +1060,36 @@ __global__ void __launch_bounds__(JJT, JJ_MINB) k_jju(GridL g, JJArgs a, int H, 
             u.vy[0] = R3{0.0, qa[JJT], qa[JJT + 1]};
             u.vy[1] = R3{qb[JJT - 1], qb[JJT], qb[JJT + 1]};
             u.vy[2] = R3{0.0, qc[JJT], 0.0};
-            if (EDGE && i == 1) u.vx[0].c = g.sN * u.vx[1].c;
-            if (EDGE && i == g.ncy) u.vx[2].c = g.sS * u.vx[1].c;
-            if (EDGE && c == 1) u.vy[1].l = g.sW * u.vy[1].c;
-            if (EDGE && c == g.ncx) u.vy[1].r = g.sE * u.vy[1].c;
+            if (ER && i == 1) u.vx[0].c = g.sN * u.vx[1].c;
+            if (ER && i == g.ncy) u.vx[2].c = g.sS * u.vx[1].c;
+            if (EC && c == 1) u.vy[1].l = g.sW * u.vy[1].c;
+            if (EC && c == g.ncx) u.vy[1].r = g.sE * u.vy[1].c;
             const double dv = (u.B(F_VX) - u.B(F_VX, -1)) * g.idx + (u.B(F_VY) - u.A(F_VY)) * g.idy;
             const double pn = (u.B(F_4) - ms) + a.alpha_s * u.B(F_EP) * (-dv);
             a.po[(size_t)i * P + c] = pn;
             acc[1] += dv * dv * (u.B(F_EP) * cp);
             acc[2] += pn;
-            if (!EDGE || c <= g.nvxj) {
+            if (!EC || c <= g.nvxj) {
                 const double de = (u.B(F_VX, 1) - u.B(F_VX)) * g.idx + (u.B(F_VY, 1) - u.A(F_VY, 1)) * g.idy;
                 const double pe = (u.B(F_4, 1) - ms) + a.alpha_s * u.B(F_EP, 1) * (-de);
-                const RowX x = lx_win<EDGE>(g, u, i);
+                const RowX x = lx_win<ER>(g, u, i);
                 const double r = fx_win(u, a.gx) - (pn - pe) * g.idx - x.L;
                 acc[0] -= r * r * iax;
                 const double vn = u.B(F_VX) + a.omega * r * iax;
                 a.vxo[(size_t)i * P + c] = vn;
-                if (EDGE && i == 1) a.vxo[c] = g.sN * vn;
-                if (EDGE && i == g.ncy) a.vxo[(size_t)(g.ncy + 1) * P + c] = g.sS * vn;
+                if (ER && i == 1) a.vxo[c] = g.sN * vn;
+                if (ER && i == g.ncy) a.vxo[(size_t)(g.ncy + 1) * P + c] = g.sS * vn;
             }
-            if (!EDGE || i <= g.nvyi) {
+            if (!ER || i <= g.nvyi) {
                 const double ds = (u.C(F_VX) - u.C(F_VX, -1)) * g.idx + (u.C(F_VY) - u.B(F_VY)) * g.idy;
                 const double ps = (u.C(F_4) - ms) + a.alpha_s * u.C(F_EP) * (-ds);
-                const RowX y = ly_win<EDGE>(g, u, c);
+                const RowX y = ly_win<EC>(g, u, c);
                 const double r = fy_win(u, a.gy) - (pn - ps) * g.idy - y.L;
                 acc[0] -= r * r * iay;
                 const double vn = u.B(F_VY) + a.omega * r * iay;
                 a.vyo[(size_t)i * P + c] = vn;
-                if (EDGE && c == 1) a.vyo[(size_t)i * P] = g.sW * vn;
-                if (EDGE && c == g.ncx) a.vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
+                if (EC && c == 1) a.vyo[(size_t)i * P] = g.sW * vn;
+                if (EC && c == g.ncx) a.vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
             }
         }
         lag_eb = v.A[F_EB].c;
@@ -1078,11 +1098,19 @@ __global__ void __launch_bounds__(JJT, JJ_MINB) k_jju(GridL g, JJArgs a, int H, 
         iax = iax_n;
         iay = iay_n;
     };
-    const bool interior = i0 >= 2 && i1 + 1 <= g.ncy - 1 && j0 >= 2 && j0 + JJT - 2 <= g.ncx - 1;
-    if (interior)
-        for (int s = sfirst; s <= slast; ++s) step(std::false_type(), s);
-    else
-        for (int s = sfirst; s <= slast; ++s) step(std::true_type(), s);
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    const bool col_edge = !(j0 >= 2 && j0 + JJT - 2 <= g.ncx - 1);
+    for (int s = sfirst; s <= slast; ++s) {
+        const bool row_edge = s <= 2 || s >= g.ncy;
+        if (col_edge) {
+            if (row_edge) step(T_(), T_(), s);
+            else step(F_(), T_(), s);
+        } else {
+            if (row_edge) step(T_(), F_(), s);
+            else step(F_(), F_(), s);
+        }
+    }
     // deterministic CTA reduction of (Sv, Sp, sum p^k): fixed xor tree per warp, warps in order
     const size_t b = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
 #pragma unroll

@@ -54,6 +54,7 @@ struct Dist {
     cudaStream_t xs;       // the stream exchange() enqueues on (stream, or cstream while overlapping)
     cudaEvent_t ev[2];
     bool overlap;
+    int overlap_min;    // split / overlap only levels whose tile is >= this many cells wide
     bool serial_split;  // diagnostics (STOKES_DIST_OVERLAP=2): split passes, exchange not overlapped
     double *dscal;   // [0] E [1] Sv [2] Sp [3] Sf [4] zero
     double *hsc;
@@ -361,7 +362,7 @@ int dsmooth(Dist &D, int l, int &cur, int n, bool zero_in, bool fine, int max_pa
         if (pairs > max_pairs) pairs = max_pairs;
         for (int s = 0; s < n;) {
             const bool two = pairs > 0 && !(zero_in && s == 0);
-            if (D.overlap && stream_ok(g0) && !(zero_in && s == 0)) {
+            if (D.overlap && stream_ok(g0) && g0.ncx >= D.overlap_min && !(zero_in && s == 0)) {
                 // boundary layers first, then their halo exchange on the comm stream while the
                 // interior of the tiles is swept
                 for (int pp = 0; pp < 2; ++pp) {
@@ -991,6 +992,12 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
         // STOKES_DIST_OVERLAP = 0 off, 1 on, 2 split passes with the exchange not overlapped
         const char *e = getenv("STOKES_DIST_OVERLAP");
         D->overlap = e ? e[0] != '0' : D->mode == M_NCCL;
+        // a split pass costs ~12 us (boundary-strip launches, the interior on 4 fewer SMs;
+        // measured on one B200) against the ~30 us of the two NCCL rounds it
+        // hides: worth it only where the interior part outlasts the exchange -- tile levels
+        // >= 1024 cells wide (pass >= 72 us).  STOKES_OVERLAP_MIN overrides.
+        const char *m = getenv("STOKES_OVERLAP_MIN");
+        D->overlap_min = m ? atoi(m) : (e ? 0 : 1024);
         D->serial_split = e && e[0] == '2';
     }
     int st;

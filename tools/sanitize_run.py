@@ -1,6 +1,8 @@
 """Small solves exercising every kernel (single domain Jacobi/RBGS/GCR/Anderson/RAS/Mixed
-incl. the TMA streaming kernels, viscosity stages, lithostatic pressure, decomposed virtual +
-loopback, the marker-in-cell kernels) for compute-sanitizer runs."""
+incl. the TMA streaming kernels, the one-pass RBGS (forced onto every streamed level), the
+fused k_jju pass and the device-side loop graph, viscosity stages, lithostatic pressure,
+decomposed virtual / loopback / NCCL_SELF with and without the overlapped split passes, the
+marker-in-cell kernels) for compute-sanitizer runs."""
 import os
 import sys
 
@@ -13,6 +15,7 @@ from paper_2603_14040_b200 import Stokes, StokesDist  # noqa: E402
 from synth.fields import markers, workload  # noqa: E402
 
 os.environ["STOKES_DIST_DMIN"] = "8"
+os.environ["STOKES_RBGS1"] = "2"  # the one-pass RBGS kernel on every streamed single-domain level
 T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
@@ -32,6 +35,11 @@ run(Stokes, 64, "mms", omega_v=0.6, alpha_p=1.0, smoother=1, max_iter=3)
 run(Stokes, 48, "mms", omega_v=0.6, alpha_p=1.0, accel=1, max_iter=4)
 run(StokesDist, 512, "layered", px=2, py=2, transport="loopback", omega_v=0.6, alpha_p=1.0, max_iter=2)
 run(StokesDist, 128, "layered", px=2, py=1, transport="virtual", omega_v=0.6, alpha_p=1.0, smoother=1, max_iter=2)
+run(StokesDist, 256, "layered", px=2, py=2, transport="nccl_self", omega_v=0.6, alpha_p=1.0, max_iter=2)
+os.environ["STOKES_DIST_OVERLAP"] = "1"
+run(StokesDist, 512, "layered", px=2, py=1, transport="virtual", omega_v=0.6, alpha_p=1.0, max_iter=3)
+os.environ.pop("STOKES_DIST_OVERLAP")
+run(Stokes, 512, "layered", omega_v=0.6, alpha_p=1.0, smoother=1, max_iter=2)
 s = Stokes(256, 256, omega_v=0.6)
 w = workload("layered", 256, 256)
 s.set_viscosity(T(w["eta_b"]), T(w["eta_p"]))

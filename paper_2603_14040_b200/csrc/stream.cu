@@ -109,10 +109,21 @@ Reg2 full_region(const GridL &g) {
     return r;
 }
 
-// reciprocal without the IEEE-division subroutine: MUFU seed + two Newton steps
-// (24 -> 48 -> full 53 bits; |a| is far inside the float range for every level here)
+// reciprocal without the IEEE-division subroutine: MUFU seed + two Newton steps.
+// RCP_SEED 1 (default): the FP64 MUFU seed rcp.approx.ftz.f64 (~20 bits, one instruction,
+// no conversions); 0: the IEEE-rounded float reciprocal of the rounded argument (~24 bits,
+// F2F + MUFU + fix-up + F2F).  Either way two Newton steps reach full precision (<= 1 ulp;
+// |a| is far inside the normal range on every level here).
+#ifndef RCP_SEED
+#define RCP_SEED 1
+#endif
 __device__ __forceinline__ double rcp(double a) {
+#if RCP_SEED
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+#else
     double r = (double)__frcp_rn((float)a);
+#endif
     r = r * fma(-a, r, 2.0);
     r = r * fma(-a, r, 2.0);
     return r;

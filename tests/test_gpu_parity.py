@@ -191,15 +191,34 @@ def test_ras_solve_parity(S, name, n, opts):
     o, s = pair(*args, **dict(opts, max_iter=15))
     a, b = o.solve(0.0), s.solve(0.0)
     assert a["iters"] == b["iters"] == 15
-    for key in ("vx", "vy", "p"):
-        assert rel(b[key], a[key]) <= 1e-8, (key, rel(b[key], a[key]))
+    d15 = max(rel(b[key], a[key]) for key in ("vx", "vy", "p"))
+    assert d15 <= 1e-8, d15
     o, s = pair(*args, **opts)
     a, b = o.solve(1e-8), s.solve(1e-8)
     assert a["status"] == 0 and b["status"] == 0
-    # Anderson: the oracle itself moves 158 -> 171 / 185 / 162 iterations on block 128^2 with
-    # the Mixed smoother when rho is perturbed by 1e-15 / 3e-15 / 1e-14 (measured): 20 % band
-    band = max(2, a["iters"] // 5) if opts.get("accel", 0) == 2 else 1
-    assert abs(a["iters"] - b["iters"]) <= band, (a["iters"], b["iters"])
+    ka, kb = a["iters"], b["iters"]
+    band = 1
+    if opts.get("accel", 0) == 2:
+        # Anderson's count is rounding-chaotic (reading R26): the ORACLE itself moves 158 ->
+        # 171 / 185 / 162 iterations on block 128^2 with the Mixed smoother under 1e-15 .. 1e-14
+        # perturbations of rho.  Band = twice the oracle's own spread over four perturbations
+        # of rho of the size of the GPU-oracle difference after 15 iterations (d15: the
+        # rounding-order difference the count is exposed to); the unique fixed point is
+        # checked below to 1e-9.
+        spread = 0
+        for seed in range(4):
+            w2 = dict(w, rho_b=w["rho_b"] * (1.0 + max(d15, 1e-15) * np.random.default_rng(seed).standard_normal(
+                w["rho_b"].shape)))
+            o2 = Oracle(n, n, w["Lx"], w["Ly"], w["bc"], **opts)
+            o2.set_viscosity(w2["eta_b"], w2["eta_p"])
+            o2.set_density(w2["rho_b"])
+            o2.set_gravity(w["gx"], w["gy"])
+            spread = max(spread, abs(o2.solve(1e-8)["iters"] - ka))
+        band = max(2, 2 * spread)
+        a, b = o.solve(1e-11), s.solve(1e-11)
+        for key in ("vx", "vy", "p"):
+            assert rel(b[key], a[key]) <= 1e-9, key
+    assert abs(ka - kb) <= band, (ka, kb, band)
 
 
 @pytest.mark.parametrize("nx,ny", [(16, 16), (64, 32), (136, 72)])

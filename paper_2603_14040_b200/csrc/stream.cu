@@ -752,8 +752,7 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
     const int rlo = max(i0 - 2, -hN), rhi = min(i1 + 2, g.ncy + 1 + hS);
     const int sfirst = max(i0 - 1, 0), slast = min(i1 + 1, g.ncy + 1);
     const size_t P = g.P;
-    auto issue = [&](int r) {
-        const int slot = (r - rlo) % NSJ;
+    auto issue_at = [&](int r, int slot) {  // row r into ring slot `slot` (= (r - rlo) % NSJ)
         uint64_t *bar = bars + slot;
         mbar_expect_tx(bar, NF * a.seg * 8);
 #pragma unroll
@@ -766,11 +765,20 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
     }
     __syncthreads();
     if (t == 0)
-        for (int r = rlo; r < rlo + NSJ && r <= rhi; ++r) issue(r);
-    auto row_at = [&](int r) {  // wait until staged row r has landed; this thread's column in it
-        const int rel = r - rlo;
-        mbar_wait(bars + rel % NSJ, (rel / NSJ) & 1);
-        return sm + (rel % NSJ) * NF * JRW + t + 1;
+        for (int r = rlo; r < rlo + NSJ && r <= rhi; ++r) issue_at(r, r - rlo);
+    // rows are waited for strictly in order rlo, rlo+1, ...: the next one's ring slot and
+    // mbarrier phase advance incrementally (no division per row)
+    int wslot = 0;
+    uint32_t wphase = 0;
+    auto wait_next = [&](int &slot) {  // wait for the next staged row; this thread's column in it
+        slot = wslot;
+        mbar_wait(bars + wslot, wphase);
+        const double *q = sm + wslot * (NF * JRW) + t + 1;
+        if (++wslot == NSJ) {
+            wslot = 0;
+            wphase ^= 1u;
+        }
+        return q;
     };
     V3 v;
     auto pullB = [&](const double *q) {
@@ -802,18 +810,22 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
         v.A[F_VY].r = v.B[F_VY].r;
         v.A[F_5].c = v.B[F_5].c;
     };
-    auto refill = [&](int r) {  // every thread has pulled row r as row B: its slot takes row r + NSJ
+    auto refill = [&](int r, int slot) {  // every thread has pulled row r as row B: its slot takes row r + NSJ
         if (t == 0 && r + NSJ <= rhi) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(r + NSJ);
+            issue_at(r + NSJ, slot);
         }
     };
     if (rlo < sfirst) {
-        pullB(row_at(rlo));
+        int sl;
+        pullB(wait_next(sl));
         toA();
         __syncthreads();
-        refill(rlo);
+        refill(rlo, sl);
     }
+    int slotB;
+    const double *qB = wait_next(slotB);  // row sfirst
+    const bool own_col = t >= 1 && t <= a.tw && c <= jhi;
     const bool cx_in = c >= 1 - hW && c <= g.nvxj + hE, cy_in = c >= 1 - hW && c <= g.ncx + hE;
     // 1/a_ii and right-hand side of sweep-1 row s-1 (= the sweep-2 row): equal in both sweeps
     double iax = 0.0, iay = 0.0, bxp = 0.0, byp = 0.0, lag_eb = 0.0;
@@ -825,8 +837,13 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
     // walls run the plain interior code on almost every row (tiles: both on edge CTAs).
     auto step = [&](auto er, auto ec, int s) {
         constexpr bool ER = decltype(er)::value, EC = decltype(ec)::value;
-        pullB(row_at(s));
-        if (s + 1 <= rhi) pullC(row_at(s + 1));
+        pullB(qB);
+        int slotC = 0;
+        const double *qC = qB;
+        if (s + 1 <= rhi) {
+            qC = wait_next(slotC);
+            pullC(qC);
+        }
         const W1 w{&v};
         // ---- sweep 1, row s
         double vx1 = v.B[F_VX].c, vy1 = v.B[F_VY].c, iax_n = 0.0, iay_n = 0.0, bx_n = 0.0, by_n = 0.0;
@@ -845,10 +862,10 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
         s1[((s & 3) * 2 + 0) * JT + t] = vx1;
         s1[((s & 3) * 2 + 1) * JT + t] = vy1;
         __syncthreads();
-        if (!J2_LATE) refill(s);
+        if (!J2_LATE) refill(s, slotB);
         // ---- sweep 2, row i = s-1 on the intermediate iterate
         const int i = s - 1;
-        if (i >= i0 && i <= i1 && t >= 1 && t <= a.tw && c <= jhi) {
+        if (own_col && i >= i0 && i <= i1) {
             const double *qa = s1 + (((s - 2) & 3) * 2) * JT + t, *qb = s1 + (((s - 1) & 3) * 2) * JT + t,
                          *qc = s1 + ((s & 3) * 2) * JT + t;
             W2 u;
@@ -879,7 +896,9 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
                 if (EC && c == g.ncx && g.bE) a.vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;
             }
         }
-        if (J2_LATE) refill(s);
+        if (J2_LATE) refill(s, slotB);
+        qB = qC;
+        slotB = slotC;
         lag_eb = v.A[F_EB].c;
         toA();
         iax = iax_n;

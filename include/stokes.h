@@ -122,14 +122,19 @@ int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const s
 /* 2D domain decomposition.  The global nx x ny grid is
  * split into px x py tiles of (nx/px) x (ny/py) cells (nx % px == ny % py == 0); tile
  * (tx, ty) = (rank % px, rank / px).  Exact: iterates equal the single-domain solve's up to
- * the order of global sums.  Levels whose tiles are >= 64 cells wide are distributed (halo
- * exchange after every velocity / residual / correction / pressure write); the coarser
- * levels are agglomerated: every process holds the global grid of the first coarse level
- * and runs the coarse tail redundantly.  Options: accel must be STOKES_ACCEL_NONE.
+ * the order of global sums.  Levels whose tiles are >= dmin cells wide (NCCL 512, in-process
+ * 64; STOKES_DIST_DMIN) are distributed (width-2 halo exchange after every pass that writes a
+ * velocity / correction / right-hand side / pressure); the coarser levels are agglomerated:
+ * every process holds the global grid of the first coarse level and runs the coarse tail
+ * redundantly.  Options: accel STOKES_ACCEL_NONE (Uzawa-MG) or STOKES_ACCEL_GCR (GCR(m) with
+ * the distributed V-cycle as preconditioner and global inner products); Anderson, viscosity
+ * rescaling (theta_step > 0) and the RAS / Mixed smoothers: STOKES_EINVAL.
  *   rank = -1 VIRTUAL: all tiles in this process on the current GPU; every array of the
  *             calls below is the GLOBAL user-layout array (tests of the decomposition).
  *   rank = -2 LOOPBACK: as VIRTUAL, but halos and the agglomeration go through the NCCL
  *             path's packing / unpacking with device copies standing in for the NCCL calls.
+ *   rank = -3 NCCL_SELF: as LOOPBACK, but every transfer is a real ncclSend / ncclRecv /
+ *             ncclAllReduce on a one-rank communicator (the NCCL code path on one GPU).
  *   rank >= 0 NCCL: this process owns tile `rank` (one GPU per process), nccl_unique_id =
  *             128 bytes from stokes_nccl_unique_id() on rank 0, shared by the caller; every
  *             array is the tile's WINDOW of the global user layout, i.e. the user layout of

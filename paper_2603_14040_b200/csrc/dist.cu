@@ -64,6 +64,13 @@ struct Dist {
     long long launches;
     cudaGraphExec_t exec[2];
     long long body_kernels;
+    // GCR(m) on the tiles: partial-sum buffers holding every tile's per-CTA
+    // partials back to back (NCCL: all-gathered), so each tile's next fused kernel reduces
+    // the GLOBAL sum in one fixed order; one graph per inner step i
+    double *gpart[3];
+    size_t gseg;  // doubles per tile segment
+    cudaGraphExec_t gexec[MAXM];
+    long long gkernels[MAXM];
     int pcur;
     bool have_eta, have_rho;
     double gx, gy;
@@ -71,7 +78,7 @@ struct Dist {
 
 namespace {
 
-enum { FX_V = 0, FX_R = 1, FX_P = 2, FX_ETA = 3, FX_RHO = 4, FX_B = 5, FX_VP = 6 };
+enum { FX_V = 0, FX_R = 1, FX_P = 2, FX_ETA = 3, FX_RHO = 4, FX_B = 5, FX_VP = 6, FX_GR = 7 };
 enum { M_VIRTUAL = 0, M_LOOPBACK = 1, M_NCCL = 2, M_NCCL_SELF = 3 };
 constexpr int HW = 2;  // halo width: the two-sweep pass and the fused residual+restriction read two rings
 
@@ -89,6 +96,7 @@ int nfields(Dist &D, stokes_s *h, int l, int which, int idx, double **f) {
     case FX_B: f[0] = L.bx; f[1] = L.by; return 2;
     case FX_P: f[0] = h->pbuf[idx]; return 1;
     case FX_ETA: f[0] = L.etab; f[1] = L.etap; return 2;
+    case FX_GR: f[0] = h->gr[0]; f[1] = h->gr[1]; f[2] = h->gr[2]; return 3;  // GCR residual (level 0)
     default: (void)D; f[0] = h->rho; return 1;
     }
 }
@@ -626,11 +634,181 @@ int force_E(Dist &D) {  // Sf -> dscal[3]
     return dsync(D);
 }
 
+// ---- flexible GCR(m) with MGS (Alg. 4; readings R13 / R14) on the tiles
+// The single-domain fused kernels run per tile.  Every GCR vector lives at the tile's owned
+// unknowns (w-type vectors are written only there, so their halos stay 0 and the per-tile
+// dot products sum each unknown once); z comes out of the distributed V-cycle with valid
+// halos, x keeps consistent halos through the axpys with global coefficients, and r's halos
+// (the V-cycle's right-hand side, the z_p recomputation of PrecondApplyOp) are exchanged
+// after every update.  A kernel's per-CTA partials go to the tile's segment of one buffer
+// (NCCL: all-gathered across the ranks), and the next kernel of EVERY tile reduces the
+// whole buffer in the same fixed order: the global inner products, identical everywhere.
+static int tiles_sum(Dist &D, int buf, int nb) {  // NCCL: all-gather rank segments of gpart[buf]
+    if (D.mode != M_NCCL) return STOKES_OK;
+    const size_t seg = (size_t)nb * 2;
+    if (ncclAllGather(D.gpart[buf] + (size_t)D.rank * seg, D.gpart[buf], seg, ncclDouble, D.comm, D.stream) != ncclSuccess)
+        return STOKES_ENCCL;
+    return STOKES_OK;
+}
+static double *seg_of(Dist &D, int buf, int k, int nb) {  // tile k's partials (NCCL: this rank's)
+    const int r = D.mode == M_NCCL ? D.rank : k;
+    return D.gpart[buf] + (size_t)r * nb * 2;
+}
+static int nranks(const Dist &D) { return D.mode == M_NCCL ? D.px * D.py : D.nt; }
+
+// r = b - A x (true residual) on every tile + its E -> dscal[0]; x halos refreshed first
+static int dist_gcr_residual(Dist &D) {
+    int st;
+    if ((st = exchange(D, 0, FX_VP, 0 | (D.pcur << 1)))) return st;
+    for (int k = 0; k < D.nt; ++k) {
+        stokes_s *t = D.tile[k];
+        Level &F = t->lev[0];
+        const LaunchCtx c = ctx(t);
+        launch_uzawa_energy(c, F.g, F.etab, F.etap, F.vx[0], F.vy[0], t->pbuf[D.pcur], nullptr, t->rho, D.gx, D.gy,
+                            0.0, t->scal + S_ZERO, t->gr[0], t->gr[1], t->gr[2], t->partials);
+        launch_finalize(c, t->partials, stream_blocks(F.g), 3, 1.0, t->scal + S_LOC);
+    }
+    if ((st = combine(D, false))) return st;
+    return exchange(D, 0, FX_GR, 0);
+}
+
+// one GCR step i on the tiles (as gcr_step_body, driver.cu): z_i = V-cycle(0; r_v) (the
+// distributed V-cycle), z_p + w = A z + first dot, i MGS steps, normalise + update x, r + the
+// energy of r; E, nu^2, <r,r> -> dscal[0..2] -> host
+static int dist_gcr_step_body(Dist &D, int i) {
+    int st;
+    const int NR = nranks(D);
+    // the distributed V-cycle reads its right-hand side from lev[0].(bx, by) and leaves the
+    // result in lev[0].(vx[0], vy[0]): point them at r, z_i and the scratch for the capture
+    double *keep[MAXT][6];
+    for (int k = 0; k < D.nt; ++k) {
+        stokes_s *t = D.tile[k];
+        Level &F = t->lev[0];
+        double *kk[6] = {F.bx, F.by, F.vx[0], F.vy[0], F.vx[1], F.vy[1]};
+        memcpy(keep[k], kk, sizeof kk);
+        F.bx = t->gr[0];
+        F.by = t->gr[1];
+        F.vx[0] = t->gz[i][0];
+        F.vy[0] = t->gz[i][1];
+        F.vx[1] = t->gtmp[0];
+        F.vy[1] = t->gtmp[1];
+    }
+    st = dvcycle(D, 0, false, true);
+    for (int k = 0; k < D.nt; ++k) {  // restore
+        Level &F = D.tile[k]->lev[0];
+        F.bx = keep[k][0];
+        F.by = keep[k][1];
+        F.vx[0] = keep[k][2];
+        F.vy[0] = keep[k][3];
+        F.vx[1] = keep[k][4];
+        F.vy[1] = keep[k][5];
+    }
+    if (st) return st;
+    const int nbs = stream_blocks(D.tile[0]->lev[0].g), nbf = gcr_flat_blocks();
+    for (int k = 0; k < D.nt; ++k) {
+        stokes_s *t = D.tile[k];
+        Level &F = t->lev[0];
+        double **z = t->gz[i], **w = t->gw[i], **r = t->gr;
+        launch_precond_apply(ctx(t), F.g, F.etab, F.etap, z[0], z[1], r[2], D.o.alpha_p, z[2], w[0], w[1], w[2],
+                             i > 0 ? (const double *const *)t->gw[0] : nullptr, r[0], r[1], seg_of(D, 0, k, nbs));
+    }
+    if ((st = tiles_sum(D, 0, nbs))) return st;
+    int pin = 0, nbin = nbs * NR;
+    for (int j = 0; j < i; ++j) {
+        const int pout = 1 + (j & 1);
+        for (int k = 0; k < D.nt; ++k) {
+            stokes_s *t = D.tile[k];
+            const size_t nf = field_doubles(t->lev[0].g);
+            const double *const *nxt = (j + 1 < i) ? (const double *const *)t->gw[j + 1] : nullptr;
+            launch_mgs_step(ctx(t), D.gpart[pin], nbin, 2, 0, t->gw[i], t->gz[i], (const double *const *)t->gw[j],
+                            (const double *const *)t->gz[j], nxt, (const double *const *)t->gr, nf, seg_of(D, pout, k, nbf));
+        }
+        if ((st = tiles_sum(D, pout, nbf))) return st;
+        pin = pout;
+        nbin = nbf * NR;
+    }
+    const int pu = pin == 1 ? 2 : 1;  // the update's partials: the buffer pin is not
+    for (int k = 0; k < D.nt; ++k) {
+        stokes_s *t = D.tile[k];
+        Level &F = t->lev[0];
+        double *x[3] = {F.vx[0], F.vy[0], t->pbuf[D.pcur]};
+        launch_gcr_update(ctx(t), D.gpart[pin], nbin, t->gw[i], t->gz[i], x, t->gr, (const double *const *)t->gew,
+                          field_doubles(F.g), seg_of(D, pu, k, nbf));
+    }
+    if ((st = tiles_sum(D, pu, nbf))) return st;
+    launch_gcr_final(dctx(D), D.gpart[pu], nbf * NR, D.gpart[pin], nbin, D.dscal + 3, D.dscal + 0, D.dscal + 1,
+                     D.dscal + 2);
+    if ((st = exchange(D, 0, FX_GR, 0))) return st;  // r's halos for the next V-cycle
+    CK(cudaMemcpyAsync(D.hsc, D.dscal, 8 * sizeof(double), cudaMemcpyDeviceToHost, D.stream));
+    return STOKES_OK;
+}
+
+static int dist_solve_gcr(Dist &D, double rtol, double E0, int *iters, double *Eout) {
+    int st;
+    const int m = D.o.gcr_restart;
+    if (!D.gpart[0]) {  // partial buffers: every rank / tile, the larger of the two kernels' block counts
+        const int nbs = stream_blocks(D.tile[0]->lev[0].g), nbf = gcr_flat_blocks();
+        D.gseg = (size_t)2 * (nbs > nbf ? nbs : nbf);
+        for (int b = 0; b < 3; ++b)
+            if (cudaMalloc(&D.gpart[b], D.gseg * nranks(D) * sizeof(double)) != cudaSuccess) return STOKES_ENOMEM;
+    }
+    if ((st = dist_gcr_residual(D))) return st;  // r0 = b - A x0
+    int k = 0, status = STOKES_NOT_CONVERGED, fresh = 1;
+    double E = E0;
+    while (k < D.o.max_iter && status == STOKES_NOT_CONVERGED) {
+        if (!fresh && D.o.gcr_true_restart && (st = dist_gcr_residual(D))) return st;  // restart (R13)
+        fresh = 0;
+        for (int i = 0; i < m && k < D.o.max_iter; ++i) {
+            if (!D.gexec[i]) {
+                cudaGraph_t graph;
+                const long long before = dist_launches(&D, 0);
+                CK(cudaStreamBeginCapture(D.stream, cudaStreamCaptureModeThreadLocal));
+                const int bst = dist_gcr_step_body(D, i);
+                cudaError_t e = cudaStreamEndCapture(D.stream, &graph);
+                if (bst) return bst;
+                if (e != cudaSuccess) return fail_cuda(e, "dist GCR graph capture");
+                D.gkernels[i] = dist_launches(&D, 0) - before;
+                D.launches -= D.gkernels[i];
+                e = cudaGraphInstantiate(&D.gexec[i], graph, 0);
+                cudaGraphDestroy(graph);
+                if (e != cudaSuccess) { D.gexec[i] = nullptr; return fail_cuda(e, "dist GCR graph instantiate"); }
+            }
+            CK(cudaGraphLaunch(D.gexec[i], D.stream));
+            D.launches += D.gkernels[i];
+            if ((st = dsync(D))) return st;
+            ++k;
+            E = D.hsc[0];
+            const double nu2 = D.hsc[1], rr = D.hsc[2];
+            if (!(nu2 > 1e-28 * rr)) { status = STOKES_EDIVERGED; break; }  // breakdown (R13)
+            if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+            if (E <= rtol) {  // exit test on the true residual (R13): else restart from it
+                if ((st = dist_gcr_residual(D))) return st;
+                CK(cudaMemcpyAsync(D.hsc, D.dscal, 8 * sizeof(double), cudaMemcpyDeviceToHost, D.stream));
+                if ((st = dsync(D))) return st;
+                fresh = 1;
+                if (D.hsc[0] <= rtol) status = STOKES_OK;
+                break;
+            }
+        }
+    }
+    *iters = k;
+    // the true E of x and the mean of x_p for the output de-mean (x halos first)
+    if ((st = exchange(D, 0, FX_VP, 0 | (D.pcur << 1)))) return st;
+    if ((st = state_E(D, &E))) return st;
+    *Eout = E;
+    return status;
+}
+
 void drop(Dist &D) {
     for (int k = 0; k < 2; ++k)
         if (D.exec[k]) {
             cudaGraphExecDestroy(D.exec[k]);
             D.exec[k] = nullptr;
+        }
+    for (int k = 0; k < MAXM; ++k)
+        if (D.gexec[k]) {
+            cudaGraphExecDestroy(D.gexec[k]);
+            D.gexec[k] = nullptr;
         }
 }
 
@@ -640,7 +818,7 @@ int make_tile(Dist &D, int tx, int ty, stokes_s **out) {
     if (!h) return STOKES_ENOMEM;
     h->o = D.o;
     h->o.coarse_direct = 0;
-    h->o.accel = STOKES_ACCEL_NONE;
+    h->o.accel = D.o.accel == STOKES_ACCEL_GCR ? STOKES_ACCEL_GCR : STOKES_ACCEL_NONE;  // GCR vectors per tile
     h->nx = D.nxt;
     h->ny = D.nyt;
     h->Lx = D.Lx * D.nxt / D.NX;
@@ -739,6 +917,8 @@ int dist_destroy(Dist *D) {
     }
     if (D->dscal) cudaFree(D->dscal);
     if (D->hsc) cudaFreeHost(D->hsc);
+    for (int k = 0; k < 3; ++k)
+        if (D->gpart[k]) cudaFree(D->gpart[k]);
     if (D->own_stream) cudaStreamDestroy(D->stream);
     if (D->cstream) cudaStreamDestroy(D->cstream);
     for (int k = 0; k < 2; ++k)
@@ -767,6 +947,12 @@ int dist_set_viscosity(Dist *D, const double *eta_b, const double *eta_p) {
     }
     if ((st = gather_to_tail(*D, 1))) return st;
     if ((st = build_hierarchy(D->tail))) return st;  // tail: coarse eta + coarsest inverse
+    if (D->o.accel == STOKES_ACCEL_GCR)  // GCR energy weights at each tile's unknowns
+        for (int k = 0; k < D->nt; ++k) {
+            stokes_s *t = D->tile[k];
+            Level &F = t->lev[0];
+            launch_energy_weights(ctx(t), F.g, F.etab, F.etap, t->gew[0], t->gew[1], t->gew[2]);
+        }
     if ((st = dsync(*D))) return st;
     D->have_eta = true;
     drop(*D);
@@ -845,7 +1031,10 @@ int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *ite
     } else {
         if ((st = state_E(*D, &E0))) return st;
         E = E0;
-        if (E0 > rtol) {
+        if (E0 > rtol && D->o.accel == STOKES_ACCEL_GCR) {
+            status = dist_solve_gcr(*D, rtol, E0, &k, &E);
+            if (status < 0 && status != STOKES_EDIVERGED) return status;
+        } else if (E0 > rtol) {
             status = STOKES_NOT_CONVERGED;
             const int keep = D->pcur;
             const bool fused = dist_fused_ok(*D);
@@ -952,7 +1141,8 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
     memcpy(D->bc, bc, sizeof(D->bc));
     if (opts) D->o = *opts;
     else stokes_opts_default(&D->o);
-    if (check_opts(D->o) || D->o.accel != STOKES_ACCEL_NONE || !(Lx > 0) || !(Ly > 0)) { free(D); return STOKES_EINVAL; }
+    if (check_opts(D->o) || (D->o.accel != STOKES_ACCEL_NONE && D->o.accel != STOKES_ACCEL_GCR) || !(Lx > 0) ||
+        !(Ly > 0)) { free(D); return STOKES_EINVAL; }
     for (int k = 0; k < 4; ++k)
         if (bc[k] != 0 && bc[k] != 1) { free(D); return STOKES_EINVAL; }
     D->rank = rank;

@@ -1208,8 +1208,7 @@ __global__ void __launch_bounds__(RTW, RR_MINB) k_resrestrict(GridL g, GridL gc,
     const int ilo = max(2 * I0 - 2, 1 - hN), ihi = min(2 * I1 + 1, g.ncy + hS);
     const int rlo = ilo - 1, rhi = ihi + 1;
     const size_t P = g.P;
-    auto issue = [&](int r) {
-        const int slot = (r - rlo) % NSRR;
+    auto issue_at = [&](int r, int slot) {
         uint64_t *bar = bars + slot;
         mbar_expect_tx(bar, NF * RRW * 8);
 #pragma unroll
@@ -1222,24 +1221,66 @@ __global__ void __launch_bounds__(RTW, RR_MINB) k_resrestrict(GridL g, GridL gc,
     }
     __syncthreads();
     if (t == 0)
-        for (int r = rlo; r < rlo + NSRR && r <= rhi; ++r) issue(r);
-    Win w;
-    auto consume = [&](int r) {
-        const int rel = r - rlo;
-        mbar_wait(bars + rel % NSRR, (rel / NSRR) & 1);
-        w.template push<NF, RRW>(sm + (rel % NSRR) * NF * RRW, t + 1);
+        for (int r = rlo; r < rlo + NSRR && r <= rhi; ++r) issue_at(r, r - rlo);
+    // lazy register window (as k_jacobi2): row i pulled as row C at step i-1 (5 values) and as
+    // row B at step i (14); only the 8 values row A still needs are carried
+    int wslot = 0;
+    uint32_t wphase = 0;
+    auto wait_next = [&](int &slot) {  // rows are waited for in order rlo, rlo+1, ...
+        slot = wslot;
+        mbar_wait(bars + wslot, wphase);
+        const double *q = sm + wslot * (NF * RRW) + t + 1;
+        if (++wslot == NSRR) {
+            wslot = 0;
+            wphase ^= 1u;
+        }
+        return q;
     };
-    auto refill = [&](int r) {
+    V3 v;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) v.A[f] = v.B[f] = v.C[f] = R3{0.0, 0.0, 0.0};
+    auto pullB = [&](const double *q) {
+        v.B[F_VX] = R3{q[-1], q[0], q[1]};
+        v.B[F_VY] = R3{q[RRW - 1], q[RRW], q[RRW + 1]};
+        v.B[F_EP].c = q[F_EP * RRW];
+        v.B[F_EP].r = q[F_EP * RRW + 1];
+        v.B[F_EB].l = q[F_EB * RRW - 1];
+        v.B[F_EB].c = q[F_EB * RRW];
+        v.B[F_4].c = q[F_4 * RRW];
+        v.B[F_4].r = q[F_4 * RRW + 1];
+        v.B[F_5].l = q[F_5 * RRW - 1];
+        v.B[F_5].c = q[F_5 * RRW];
+    };
+    auto pullC = [&](const double *q) {
+        v.C[F_VX].l = q[-1];
+        v.C[F_VX].c = q[0];
+        v.C[F_VY].c = q[RRW];
+        v.C[F_EP].c = q[F_EP * RRW];
+        v.C[F_4].c = q[F_4 * RRW];
+    };
+    auto toA = [&]() {
+        v.A[F_EB].l = v.B[F_EB].l;
+        v.A[F_EB].c = v.B[F_EB].c;
+        v.A[F_EP].c = v.B[F_EP].c;
+        v.A[F_EP].r = v.B[F_EP].r;
+        v.A[F_VX].c = v.B[F_VX].c;
+        v.A[F_VY].c = v.B[F_VY].c;
+        v.A[F_VY].r = v.B[F_VY].r;
+        v.A[F_5].c = v.B[F_5].c;
+    };
+    auto refill = [&](int r, int slot) {  // row r pulled as row B by every thread: its slot takes r + NSRR
         if (t == 0 && r + NSRR <= rhi) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(r + NSRR);
+            issue_at(r + NSRR, slot);
         }
     };
-    consume(rlo);
-    consume(rlo + 1);
+    int slotA;
+    pullB(wait_next(slotA));  // row rlo = the first step's row A
+    toA();
+    int slotB;
+    const double *qB = wait_next(slotB);  // row ilo
     __syncthreads();
-    refill(rlo);
-    refill(rlo + 1);
+    refill(rlo, slotA);
     const bool cx_in = c >= 1 - hW && c <= g.nvxj + hE, cy_in = c >= 1 - hW && c <= g.ncx + hE;
     // emit phase: threads [0, tw/2) restrict vx, threads [tw/2, tw) restrict vy (one coarse
     // value each, so no half of the CTA idles at the next barrier)
@@ -1247,7 +1288,11 @@ __global__ void __launch_bounds__(RTW, RR_MINB) k_resrestrict(GridL g, GridL gc,
     const int J = (j0 + 1) / 2 + (t < half ? t : t - half);  // coarse column of this thread
     const bool emit_x = t < half && J <= gc.nvxj, emit_y = t >= half && t < 2 * half && J <= gc.ncx;
     for (int i = ilo; i <= ihi; ++i) {
-        consume(i + 1);  // A = i-1, B = i, C = i+1
+        pullB(qB);  // A = i-1, B = i, C = i+1 (rhi = ihi + 1: row i+1 always staged)
+        int slotC;
+        const double *qC = wait_next(slotC);
+        pullC(qC);
+        const W1 w{&v};
         double rx = 0.0, ry = 0.0;
         if (cx_in) {
             const double b = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
@@ -1260,7 +1305,7 @@ __global__ void __launch_bounds__(RTW, RR_MINB) k_resrestrict(GridL g, GridL gc,
         rr[((i % RRR) * 2 + 0) * RTW + t] = rx;
         rr[((i % RRR) * 2 + 1) * RTW + t] = ry;
         __syncthreads();
-        refill(i + 1);
+        refill(i, slotB);
         // coarse row completed by fine row i (global S side: row ncy + 1 is dropped)
         const int I = (i & 1) ? (i - 1) / 2 : ((i == g.ncy && g.bS) ? i / 2 : 0);
         if (I >= I0 && I <= I1) {
@@ -1296,6 +1341,9 @@ __global__ void __launch_bounds__(RTW, RR_MINB) k_resrestrict(GridL g, GridL gc,
                 a.byc[at(gc, I, J)] = sy * (wsum == 2.0 ? 0.25 : 1.0 / (2.0 * wsum));
             }
         }
+        toA();
+        qB = qC;
+        slotB = slotC;
     }
 }
 

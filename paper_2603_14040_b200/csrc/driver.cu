@@ -307,11 +307,36 @@ static bool vtail_ok(stokes_s *h, int l) {
     }
     return true;
 }
+// Cooperative coarse cycle (kernels.cu k_vtail<true>): the same stages on a grid of one
+// CTA per SM with grid-wide barriers, from the first level of <= STOKES_COOP_CELLS cells
+// down.  Off by default: measured slower (layered 4096^2 bench: 551 ms per solve with the
+// per-level kernels, 578 / 580 / 605 ms with the cooperative cycle from 256^2 / 512^2 /
+// 1024^2 -- ~13 grid-wide barriers per level at ~3 us each cost more than the launches
+// they replace; parity-green, kept as an option).
+static int coop_cells() {
+    static const int v = [] {
+        const char *c = getenv("STOKES_COOP_CELLS");
+        return c ? atoi(c) : 0;
+    }();
+    return v;
+}
+static bool coop_ok(stokes_s *h, int l) {
+    if (!h->o.coarse_direct || h->nc <= 0 || h->nlev - l > TAIL_MAXL || h->nlev - l < 2) return false;
+    const GridL &g0 = h->lev[l].g;
+    if ((long long)g0.ncx * g0.ncy > coop_cells() || (long long)g0.ncx * g0.ncy <= vtail_cells()) return false;
+    for (int k = l; k < h->nlev; ++k) {
+        const GridL &g = h->lev[k].g;
+        if (!(g.bN && g.bS && g.bW && g.bE)) return false;
+        if (k < h->nlev - 1 && level_smoother(h, k) != STOKES_SMOOTH_JACOBI) return false;
+    }
+    return true;
+}
 void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, const RhsArgs &rhs, bool zero_in,
             int done_pre, int leave_last, double **lx, double **ly) {
     Level &L = h->lev[l];
     const LaunchCtx c = ctx(h);
-    if (zero_in && !done_pre && rhs.mode == RHS_ARRAYS && vtail_ok(h, l)) {
+    const bool coop = zero_in && !done_pre && rhs.mode == RHS_ARRAYS && coop_ok(h, l);
+    if (coop || (zero_in && !done_pre && rhs.mode == RHS_ARRAYS && vtail_ok(h, l))) {
         TailArgs a;
         a.nl = h->nlev - l;
         for (int k = 0; k < a.nl; ++k) {
@@ -330,7 +355,8 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
             t.ry = T.ry;
             t.nu = T.nu;
         }
-        launch_vtail(c, a, h->Minv, h->nc, h->o.omega_v);
+        if (coop) launch_vtail_coop(c, a, h->Minv, h->nc, h->o.omega_v);
+        else launch_vtail(c, a, h->Minv, h->nc, h->o.omega_v);
         return;
     }
     double *cx = ax, *cy = ay, *ox = sx, *oy = sy;

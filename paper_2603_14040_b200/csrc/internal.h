@@ -72,7 +72,7 @@ void launch_prolong(const LaunchCtx &c, const GridL &gf, const GridL &gc, const 
 // coarse tail of the V-cycle in one CTA (levels 0..nl-1 of the tail, the last one solved by
 // the explicit inverse): lev[l].(ax, ay) = V-cycle result with zero initial guess on
 // L v = (bx, by); (sx, sy, rx, ry) scratch.  Single-domain Jacobi levels only.
-#define TAIL_MAXL 6
+#define TAIL_MAXL 12
 struct TailLevel {
     GridL g;
     const double *etab, *etap;
@@ -85,6 +85,8 @@ struct TailArgs {
     int nl;
 };
 void launch_vtail(const LaunchCtx &c, const TailArgs &a, const double *Minv, int n, double omega);
+// the same stages over a cooperative grid (one CTA per SM, grid-wide barriers); -1 if the launch failed
+int launch_vtail_coop(const LaunchCtx &c, const TailArgs &a, const double *Minv, int n, double omega);
 // full saddle residual + energy partial sums (Sv, Sp) per block; writes r arrays if non-null.
 // force_only: Sv of f (the normaliser Sf).  Returns the number of partial blocks.
 int energy_blocks(const GridL &g);

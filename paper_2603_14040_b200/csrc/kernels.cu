@@ -15,6 +15,8 @@
 // mirrors after every update" == "mirror = partner's current value").
 #include <math.h>
 
+#include <cooperative_groups.h>
+
 #include "internal.h"
 
 namespace {
@@ -843,25 +845,37 @@ __device__ __forceinline__ RhsArgs make_rhs_arrays(const double *bx, const doubl
     r.gx = r.gy = 0.0;
     return r;
 }
-__device__ __forceinline__ void tail_copy(const GridL &g, const double *src, double *dst) {
-    const int n = (g.ncy + 2) * g.P;  // padded rows (mirrors included)
-    for (int e = threadIdx.x; e < n; e += blockDim.x) dst[e - COL_OFF] = src[e - COL_OFF];
+// COOP = false: the whole tail in ONE CTA (levels <= 32^2, k_vtail).  COOP = true: the same
+// stages over a cooperative grid of one 1024-thread CTA per SM with a grid-wide barrier
+// between stages (levels <= STOKES_COOP_CELLS, default 512^2): a level's ~13 kernels of a
+// few microseconds of work each, which the per-level kernels spend mostly on launch and
+// pipeline fill, become stages separated by grid syncs.
+template <bool COOP>
+__device__ __forceinline__ void tsync() {
+    if (COOP) cooperative_groups::this_grid().sync();
+    else __syncthreads();
 }
+__device__ __forceinline__ void tail_copy(const GridL &g, const double *src, double *dst, int t0, int nt) {
+    const int n = (g.ncy + 2) * g.P;  // padded rows (mirrors included)
+    for (int e = t0; e < n; e += nt) dst[e - COL_OFF] = src[e - COL_OFF];
+}
+template <bool COOP>
 __global__ void __launch_bounds__(1024) k_vtail(TailArgs a, const double *__restrict__ Minv, int n, double omega) {
     extern __shared__ double u[];
     double *cx[TAIL_MAXL], *cy[TAIL_MAXL], *ox[TAIL_MAXL], *oy[TAIL_MAXL];
-    const int nt = blockDim.x;
+    const int t0 = COOP ? blockIdx.x * blockDim.x + threadIdx.x : threadIdx.x;
+    const int nt = COOP ? gridDim.x * blockDim.x : blockDim.x;
     auto sweeps = [&](int l, int nsw, bool zero_first) {
         const TailLevel &L = a.lev[l];
         const RhsArgs rhs = make_rhs_arrays(L.bx, L.by);
         const int np = L.g.ncx * L.g.ncy;
         for (int s = 0; s < nsw; ++s) {
-            for (int q = threadIdx.x; q < np; q += nt) {
+            for (int q = t0; q < np; q += nt) {
                 const int i = q / L.g.ncx + 1, j = q % L.g.ncx + 1;
                 if (zero_first && s == 0) jacobi_pt<true>(L.g, L.etab, L.etap, cx[l], cy[l], ox[l], oy[l], rhs, omega, i, j);
                 else jacobi_pt<false>(L.g, L.etab, L.etap, cx[l], cy[l], ox[l], oy[l], rhs, omega, i, j);
             }
-            __syncthreads();
+            tsync<COOP>();
             double *t = cx[l]; cx[l] = ox[l]; ox[l] = t;
             t = cy[l]; cy[l] = oy[l]; oy[l] = t;
         }
@@ -873,30 +887,30 @@ __global__ void __launch_bounds__(1024) k_vtail(TailArgs a, const double *__rest
         sweeps(l, L.nu, true);
         const RhsArgs rhs = make_rhs_arrays(L.bx, L.by);
         const int np = L.g.ncx * L.g.ncy;
-        for (int q = threadIdx.x; q < np; q += nt)
+        for (int q = t0; q < np; q += nt)
             residual_pt(L.g, L.etab, L.etap, cx[l], cy[l], rhs, L.rx, L.ry, q / L.g.ncx + 1, q % L.g.ncx + 1);
-        __syncthreads();
+        tsync<COOP>();
         const int nc = C.g.ncx * C.g.ncy;
-        for (int q = threadIdx.x; q < nc; q += nt)
+        for (int q = t0; q < nc; q += nt)
             restrict_vel_pt(L.g, C.g, L.rx, L.ry, C.bx, C.by, q / C.g.ncx + 1, q % C.g.ncx + 1);
-        __syncthreads();
+        tsync<COOP>();
     }
-    {  // coarsest: direct solve into its (ax, ay)
+    {  // coarsest: direct solve into its (ax, ay) (one CTA)
         const TailLevel &L = a.lev[last];
-        coarse_solve_cta(L.g, Minv, n, L.bx, L.by, L.ax, L.ay, u);
-        __syncthreads();
+        if (!COOP || blockIdx.x == 0) coarse_solve_cta(L.g, Minv, n, L.bx, L.by, L.ax, L.ay, u);
+        tsync<COOP>();
     }
     for (int l = last - 1; l >= 0; --l) {  // up: prolongation + correction, post-smoothing
         const TailLevel &L = a.lev[l], &C = a.lev[l + 1];
         const int np = L.g.ncx * L.g.ncy;
-        for (int q = threadIdx.x; q < np; q += nt)
+        for (int q = t0; q < np; q += nt)
             prolong_pt(L.g, C.g, C.ax, C.ay, cx[l], cy[l], q / L.g.ncx + 1, q % L.g.ncx + 1);
-        __syncthreads();
+        tsync<COOP>();
         sweeps(l, L.nu, false);
         if (cx[l] != L.ax) {  // an odd number of buffer swaps: result back to (ax, ay)
-            tail_copy(L.g, cx[l], L.ax);
-            tail_copy(L.g, cy[l], L.ay);
-            __syncthreads();
+            tail_copy(L.g, cx[l], L.ax, t0, nt);
+            tail_copy(L.g, cy[l], L.ay, t0, nt);
+            tsync<COOP>();
         }
     }
 }
@@ -1212,8 +1226,32 @@ void launch_coarse_solve(const LaunchCtx &c, const GridL &g, const double *Minv,
     LAUNCH_BOOK(c);
 }
 void launch_vtail(const LaunchCtx &c, const TailArgs &a, const double *Minv, int n, double omega) {
-    k_vtail<<<1, 1024, n * sizeof(double), c.stream>>>(a, Minv, n, omega);
+    k_vtail<false><<<1, 1024, n * sizeof(double), c.stream>>>(a, Minv, n, omega);
     LAUNCH_BOOK(c);
+}
+int launch_vtail_coop(const LaunchCtx &c, const TailArgs &a, const double *Minv, int n, double omega) {
+    static int grid[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!grid[dev & 63]) {  // one wave of co-resident CTAs
+        int nb = 0, nsm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_vtail<true>, 1024, n * sizeof(double));
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        grid[dev & 63] = (nb > 0 ? nb : 1) * nsm;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid[dev & 63]);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = n * sizeof(double);
+    cfg.stream = c.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_vtail<true>, a, Minv, n, omega);
+    LAUNCH_BOOK(c);
+    return e == cudaSuccess ? 0 : -1;
 }
 int dot_blocks(const GridL &g) { return energy_blocks(g); }
 void launch_dots(const LaunchCtx &c, const GridL &g, const double *const *a, const double *const *b, int nd,

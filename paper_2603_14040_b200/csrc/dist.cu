@@ -644,8 +644,16 @@ int force_E(Dist &D) {  // Sf -> dscal[3]
 // (NCCL: all-gathered across the ranks), and the next kernel of EVERY tile reduces the
 // whole buffer in the same fixed order: the global inner products, identical everywhere.
 static int tiles_sum(Dist &D, int buf, int nb) {  // NCCL: all-gather rank segments of gpart[buf]
-    if (D.mode != M_NCCL) return STOKES_OK;
     const size_t seg = (size_t)nb * 2;
+    if (D.mode == M_NCCL_SELF) {  // the same call on the one-rank communicator (in place, per tile)
+        if (ncclGroupStart() != ncclSuccess) return STOKES_ENCCL;
+        for (int k = 0; k < D.nt; ++k)
+            if (ncclAllGather(D.gpart[buf] + (size_t)k * seg, D.gpart[buf] + (size_t)k * seg, seg, ncclDouble, D.comm,
+                              D.stream) != ncclSuccess)
+                return STOKES_ENCCL;
+        return ncclGroupEnd() == ncclSuccess ? STOKES_OK : STOKES_ENCCL;
+    }
+    if (D.mode != M_NCCL) return STOKES_OK;
     if (ncclAllGather(D.gpart[buf] + (size_t)D.rank * seg, D.gpart[buf], seg, ncclDouble, D.comm, D.stream) != ncclSuccess)
         return STOKES_ENCCL;
     return STOKES_OK;

@@ -391,8 +391,18 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
         if (post_pairs > 0) --post_pairs;
         else --pre_pairs;
     }
-    smooth(h, l, cx, cy, ox, oy, rhs, pre_n, zero_in && !done_pre, pre_pairs);  // (1) pre-smoothing
-    if (jacobi2_ok(L.g)) {  // (2) residual + (3) restriction in one pass
+    // the last pre-smoothing pair fused with (2) + (3) when the level allows it (k_j2rr)
+    const bool fuse_rr = pre_pairs >= 1 && pre_n >= 2 && level_smoother(h, l) == STOKES_SMOOTH_JACOBI && j2rr_ok(L.g);
+    if (fuse_rr) {
+        smooth(h, l, cx, cy, ox, oy, rhs, pre_n - 2, zero_in && !done_pre, pre_pairs - 1);  // (1)
+        launch_j2rr(c, L.g, C.g, L.etab, L.etap, cx, cy, ox, oy, rhs, h->o.omega_v, C.bx, C.by);
+        double *tt = cx; cx = ox; ox = tt;
+        tt = cy; cy = oy; oy = tt;
+    } else {
+        smooth(h, l, cx, cy, ox, oy, rhs, pre_n, zero_in && !done_pre, pre_pairs);  // (1) pre-smoothing
+    }
+    if (fuse_rr) {
+    } else if (jacobi2_ok(L.g)) {  // (2) residual + (3) restriction in one pass
         launch_residual_restrict(c, L.g, C.g, L.etab, L.etap, cx, cy, rhs, C.bx, C.by);
     } else {
         launch_residual(c, L.g, L.etab, L.etap, cx, cy, rhs, L.rx, L.ry);      // (2) residual

@@ -118,6 +118,12 @@ bool rbgs1_enabled();  // one-pass RBGS on single domains (STOKES_RBGS1=0 disabl
 // the last post-smoothing Jacobi sweep + the fused Uzawa step (JacobiUzawaOp) in one pass
 // (k_jju, single domains; STOKES_JJU=0 disables it); partials: 3 per block, jju_blocks(g)
 bool jju_ok(const GridL &g);
+// the last pre-smoothing two-sweep pass fused with the residual and its restriction (k_j2rr;
+// single domains; STOKES_J2RR=0 disables it): vxo, vyo = the pair's output, bxc, byc = b^H
+bool j2rr_ok(const GridL &g);
+void launch_j2rr(const LaunchCtx &c, const GridL &g, const GridL &gc, const double *etab, const double *etap,
+                 const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega,
+                 double *bxc, double *byc);
 int jju_blocks(const GridL &g);
 void launch_jacobi_jju(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
                        const double *vxi, const double *vyi, double *vxo, double *vyo, const double *pin, double *pout,

@@ -1348,6 +1348,313 @@ __global__ void __launch_bounds__(RTW, RR_MINB) k_resrestrict(GridL g, GridL gc,
 }
 
 
+// ---- the last pre-smoothing pair fused with the residual and its restriction ------------
+// (a4 + a3 + a5; single domains).  One row step s: sweep 1 of row s (-> s1 ring), CTA
+// barrier, sweep 2 of row s-1 (-> HBM for the owned cells and -> s2 ring), the residual
+// r = b - L v2 of row s-3 on the s2 ring (-> rr ring), and the restriction of the coarse row
+// whose last fine row is s-4 (as k_resrestrict).  Every ring row a stage reads was written
+// at an earlier step, so ONE barrier per step orders all of them.  The CTA owns tw = JT2 - 6
+// columns (column c = j0 - 3 + t: sweep 1 valid on every lane, sweep 2 on lanes 1..JT2-2,
+// the residual on 2..JT2-3, which covers the restriction's reach) and a strip of coarse rows.
+// The residual's viscosities and right-hand side of rows s-2..s-4 ride in registers (the
+// lazy window's row-A values carried two more steps).  One HBM pass instead of two: reads 6 +
+// writes 2 fields + b^H (1/4): 64 + 4 B per fine cell instead of 64 + 52.  Off by default
+// (slower than the two passes it replaces, see j2rr_ok).
+#ifndef J2R_T
+#define J2R_T 160
+#endif
+#ifndef J2R_MINB
+#define J2R_MINB 3
+#endif
+constexpr int JT2 = J2R_T, JRW2 = JT2 + 4;
+constexpr int SMEMJ2R = NSJ * NF * JRW2 * 8 + (4 + 4 + RRR) * 2 * JT2 * 8 + NSJ * 8;
+
+struct J2RArgs {
+    const double *src[6];  // vx, vy, eta_p, eta_b, p | bx, rho | by
+    double *vxo, *vyo;     // the pair's output (the smoothed iterate)
+    double *bxc, *byc;     // coarse right-hand sides
+    double omega, gx, gy;
+    int tw;
+};
+struct E4 {  // viscosities of a carried row: eta_b (l, c), eta_p (c, r)
+    double ebl, ebc, epc, epr;
+};
+struct W3 {  // residual view of row s-3: velocities from the s2 ring, viscosities carried
+    R3 vx[3], vy[3];
+    E4 eb, ec;       // rows s-3 (B) and s-2 (C)
+    double lag4_eb;  // eta_b (c) of row s-4 (A)
+    __device__ __forceinline__ double A(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[0], dc) : k == F_VY ? pick(vy[0], dc) : lag4_eb;
+    }
+    __device__ __forceinline__ double B(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[1], dc) : k == F_VY ? pick(vy[1], dc) : k == F_EB ? (dc < 0 ? eb.ebl : eb.ebc)
+                                                                                     : (dc > 0 ? eb.epr : eb.epc);
+    }
+    __device__ __forceinline__ double C(int k, int dc = 0) const {
+        return k == F_VX ? pick(vx[2], dc) : k == F_VY ? pick(vy[2], dc) : ec.epc;
+    }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(JT2, J2R_MINB) k_j2rr(GridL g, GridL gc, J2RArgs a, int HC) {
+    extern __shared__ __align__(128) double sm[];
+    double *s1 = sm + NSJ * NF * JRW2;  // [4 rows][vx1, vy1][JT2]
+    double *s2 = s1 + 4 * 2 * JT2;      // [4 rows][vx2, vy2][JT2]
+    double *rr = s2 + 4 * 2 * JT2;      // [RRR rows][rx, ry][JT2]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(rr + RRR * 2 * JT2);
+    const int t = threadIdx.x;
+    const int j0 = 1 + a.tw * blockIdx.x;  // odd: the staged segment starts at j0 - 4
+    const int c = j0 - 3 + t;
+    const int I0 = 1 + blockIdx.y * HC, I1 = min(I0 + HC - 1, gc.ncy);
+    const int o_lo = 2 * I0 - 1, o_hi = min(2 * I1, g.ncy);         // owned fine rows (pair output)
+    const int r_lo = max(2 * I0 - 2, 1), r_hi = min(2 * I1 + 1, g.ncy);  // residual rows
+    const int w_lo = 2 * I0 - 3, w_hi = 2 * I1 + 2;                 // sweep-2 rows (clipped to 1..ncy)
+    const int rlo = max(2 * I0 - 5, 0), rhi = min(2 * I1 + 4, g.ncy + 1);
+    const size_t P = g.P;
+    auto issue_at = [&](int r, int slot) {
+        uint64_t *bar = bars + slot;
+        mbar_expect_tx(bar, NF * JRW2 * 8);
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+            bulk_g2s(sm + (slot * NF + f) * JRW2, a.src[f] + (size_t)r * P + (j0 - 4), JRW2 * 8, bar);
+    };
+    if (t == 0) {
+        for (int k = 0; k < NSJ; ++k) mbar_init(bars + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int e = t; e < 8 * 2 * JT2; e += JT2) s1[e] = 0.0;  // s1 and s2: rows never swept read as walls (0)
+    __syncthreads();
+    if (t == 0)
+        for (int r = rlo; r < rlo + NSJ && r <= rhi; ++r) issue_at(r, r - rlo);
+    int wslot = 0;
+    uint32_t wphase = 0;
+    auto wait_next = [&](int &slot) {
+        slot = wslot;
+        mbar_wait(bars + wslot, wphase);
+        const double *q = sm + wslot * (NF * JRW2) + t + 1;
+        if (++wslot == NSJ) {
+            wslot = 0;
+            wphase ^= 1u;
+        }
+        return q;
+    };
+    V3 v;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) v.A[f] = v.B[f] = v.C[f] = R3{0.0, 0.0, 0.0};
+    auto pullB = [&](const double *q) {
+        v.B[F_VX] = R3{q[-1], q[0], q[1]};
+        v.B[F_VY] = R3{q[JRW2 - 1], q[JRW2], q[JRW2 + 1]};
+        v.B[F_EP].c = q[F_EP * JRW2];
+        v.B[F_EP].r = q[F_EP * JRW2 + 1];
+        v.B[F_EB].l = q[F_EB * JRW2 - 1];
+        v.B[F_EB].c = q[F_EB * JRW2];
+        v.B[F_4].c = q[F_4 * JRW2];
+        v.B[F_4].r = q[F_4 * JRW2 + 1];
+        v.B[F_5].l = q[F_5 * JRW2 - 1];
+        v.B[F_5].c = q[F_5 * JRW2];
+    };
+    auto pullC = [&](const double *q) {
+        v.C[F_VX].l = q[-1];
+        v.C[F_VX].c = q[0];
+        v.C[F_VY].c = q[JRW2];
+        v.C[F_EP].c = q[F_EP * JRW2];
+        v.C[F_4].c = q[F_4 * JRW2];
+    };
+    auto toA = [&]() {
+        v.A[F_EB].l = v.B[F_EB].l;
+        v.A[F_EB].c = v.B[F_EB].c;
+        v.A[F_EP].c = v.B[F_EP].c;
+        v.A[F_EP].r = v.B[F_EP].r;
+        v.A[F_VX].c = v.B[F_VX].c;
+        v.A[F_VY].c = v.B[F_VY].c;
+        v.A[F_VY].r = v.B[F_VY].r;
+        v.A[F_5].c = v.B[F_5].c;
+    };
+    auto refill = [&](int r, int slot) {
+        if (t == 0 && r + NSJ <= rhi) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_at(r + NSJ, slot);
+        }
+    };
+    int slotA;
+    pullB(wait_next(slotA));  // row rlo: row A of the first step
+    toA();
+    int slotB = 0;
+    const double *qB = rlo + 1 <= rhi ? wait_next(slotB) : nullptr;
+    __syncthreads();
+    refill(rlo, slotA);
+    const bool cx_in = c >= 1 && c <= g.nvxj, cy_in = c >= 1 && c <= g.ncx;
+    const bool lane2 = t >= 1 && t <= JT2 - 2, lane3 = t >= 2 && t <= JT2 - 3;
+    const bool own_col = t >= 3 && t < 3 + a.tw && c <= g.ncx;
+    // carried state: b and 1/a_ii of sweep-1 rows s-1 (p), s-2 (2), s-3 (3); viscosities of
+    // rows s-2, s-3 and eta_b of row s-4 for the residual
+    double iax = 0.0, iay = 0.0, bxp = 0.0, byp = 0.0, bx2 = 0.0, by2 = 0.0, bx3 = 0.0, by3 = 0.0;
+    E4 e2{0.0, 0.0, 0.0, 0.0}, e3{0.0, 0.0, 0.0, 0.0};
+    double lag4_eb = 0.0;
+    // emission lanes (as k_resrestrict): [0, tw/2) vx, [tw/2, tw) vy, one coarse column each
+    const int half = a.tw / 2;
+    const int J = (j0 + 1) / 2 + (t < half ? t : t - half);
+    const bool emit_x = t < half && J <= gc.nvxj, emit_y = t >= half && t < 2 * half && J <= gc.ncx;
+    // the last step restricts coarse row I1, completed by fine row 2 I1 + 1 (row ncy on the
+    // last strip: row ncy + 1 lies outside the domain)
+    const int s_lo = rlo + 1, s_hi = (2 * I1 >= g.ncy ? g.ncy : 2 * I1 + 1) + 4;
+    for (int s = s_lo; s <= s_hi; ++s) {
+        const bool haveB = s <= rhi, haveC = s + 1 <= rhi;
+        int slotC = 0;
+        const double *qC = nullptr;
+        if (haveB) pullB(qB);
+        if (haveC) {
+            qC = wait_next(slotC);
+            pullC(qC);
+        }
+        const W1 w{&v};
+        // ---- sweep 1, row s
+        double vx1 = v.B[F_VX].c, vy1 = v.B[F_VY].c, iax_n = 0.0, iay_n = 0.0, bx_n = 0.0, by_n = 0.0;
+        if (haveB && s >= 1 && s <= g.ncy && cx_in) {
+            const RowX x = lx_win<true>(g, w, s);
+            bx_n = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
+            iax_n = rcp(x.a);
+            vx1 = w.B(F_VX) + a.omega * (bx_n - x.L) * iax_n;
+        }
+        if (haveB && s >= 1 && s <= g.nvyi && cy_in) {
+            const RowX y = ly_win<true>(g, w, c);
+            by_n = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
+            iay_n = rcp(y.a);
+            vy1 = w.B(F_VY) + a.omega * (by_n - y.L) * iay_n;
+        }
+        s1[((s & 3) * 2 + 0) * JT2 + t] = vx1;
+        s1[((s & 3) * 2 + 1) * JT2 + t] = vy1;
+        __syncthreads();
+        if (haveB) refill(s, slotB);
+        // ---- sweep 2, row i = s-1 on the intermediate iterate -> HBM (owned) and the s2 ring
+        {
+            const int i = s - 1;
+            double vx2 = 0.0, vy2 = 0.0;
+            if (lane2 && i >= max(w_lo, 0) && i <= min(w_hi, g.ncy + 1)) {
+                const double *qa = s1 + (((s - 2) & 3) * 2) * JT2 + t, *qb = s1 + (((s - 1) & 3) * 2) * JT2 + t,
+                             *qc = s1 + ((s & 3) * 2) * JT2 + t;
+                W2 u;
+                u.v = &v;
+                u.lag_eb = e2.ebc;
+                u.vx[0] = R3{0.0, qa[0], 0.0};
+                u.vx[1] = R3{qb[-1], qb[0], qb[1]};
+                u.vx[2] = R3{qc[-1], qc[0], 0.0};
+                u.vy[0] = R3{0.0, qa[JT2], qa[JT2 + 1]};
+                u.vy[1] = R3{qb[JT2 - 1], qb[JT2], qb[JT2 + 1]};
+                u.vy[2] = R3{0.0, qc[JT2], 0.0};
+                if (i == 1) u.vx[0].c = g.sN * u.vx[1].c;
+                if (i == g.ncy) u.vx[2].c = g.sS * u.vx[1].c;
+                if (c == 1) u.vy[1].l = g.sW * u.vy[1].c;
+                if (c == g.ncx) u.vy[1].r = g.sE * u.vy[1].c;
+                vx2 = u.B(F_VX);  // walls / rows outside the unknowns keep the intermediate value
+                vy2 = u.B(F_VY);
+                if (i >= 1 && i <= g.ncy && cx_in) {
+                    const RowX x = lx_win<true>(g, u, i);
+                    vx2 = u.B(F_VX) + a.omega * (bxp - x.L) * iax;
+                }
+                if (i >= 1 && i <= g.nvyi && cy_in) {
+                    const RowX y = ly_win<true>(g, u, c);
+                    vy2 = u.B(F_VY) + a.omega * (byp - y.L) * iay;
+                }
+                if (own_col && i >= o_lo && i <= o_hi) {
+                    if (cx_in) {
+                        a.vxo[(size_t)i * P + c] = vx2;
+                        if (i == 1) a.vxo[c] = g.sN * vx2;
+                        if (i == g.ncy) a.vxo[(size_t)(g.ncy + 1) * P + c] = g.sS * vx2;
+                    }
+                    if (i <= g.nvyi) {
+                        a.vyo[(size_t)i * P + c] = vy2;
+                        if (c == 1) a.vyo[(size_t)i * P] = g.sW * vy2;
+                        if (c == g.ncx) a.vyo[(size_t)i * P + g.ncx + 1] = g.sE * vy2;
+                    }
+                }
+            }
+            s2[(((s - 1) & 3) * 2 + 0) * JT2 + t] = vx2;
+            s2[(((s - 1) & 3) * 2 + 1) * JT2 + t] = vy2;
+        }
+        // ---- residual r = b - L v2, row ir = s-3 (s2 rows s-4 .. s-2, written at earlier steps)
+        {
+            const int ir = s - 3;
+            double rx = 0.0, ry = 0.0;
+            if (lane3 && ir >= r_lo && ir <= r_hi) {
+                const double *qa = s2 + (((s - 4) & 3) * 2) * JT2 + t, *qb = s2 + (((s - 3) & 3) * 2) * JT2 + t,
+                             *qc = s2 + (((s - 2) & 3) * 2) * JT2 + t;
+                W3 u;
+                u.eb = e3;
+                u.ec = e2;
+                u.lag4_eb = lag4_eb;
+                u.vx[0] = R3{0.0, qa[0], 0.0};
+                u.vx[1] = R3{qb[-1], qb[0], qb[1]};
+                u.vx[2] = R3{qc[-1], qc[0], 0.0};
+                u.vy[0] = R3{0.0, qa[JT2], qa[JT2 + 1]};
+                u.vy[1] = R3{qb[JT2 - 1], qb[JT2], qb[JT2 + 1]};
+                u.vy[2] = R3{0.0, qc[JT2], 0.0};
+                if (ir == 1) u.vx[0].c = g.sN * u.vx[1].c;
+                if (ir == g.ncy) u.vx[2].c = g.sS * u.vx[1].c;
+                if (c == 1) u.vy[1].l = g.sW * u.vy[1].c;
+                if (c == g.ncx) u.vy[1].r = g.sE * u.vy[1].c;
+                if (cx_in) rx = bx3 - lx_win<true>(g, u, ir).L;
+                if (cy_in && ir <= g.nvyi) ry = by3 - ly_win<true>(g, u, c).L;
+            }
+            rr[(((ir % RRR) + RRR) % RRR * 2 + 0) * JT2 + t] = rx;
+            rr[(((ir % RRR) + RRR) % RRR * 2 + 1) * JT2 + t] = ry;
+        }
+        // ---- restriction of the coarse row completed by fine row s-4 (rr rows <= s-4)
+        {
+            const int i = s - 4;
+            const int I = (i & 1) ? (i - 1) / 2 : ((i == g.ncy) ? i / 2 : 0);
+            if (i >= 1 && I >= I0 && I <= I1) {
+                if (emit_x) {
+                    const int q = 2 * J - (j0 - 3);  // rr column of fine column 2J
+                    double sx = 0.0, wsum = 0.0;
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) {
+                        const int fi = 2 * I - 2 + d;
+                        if (fi < 1 || fi > g.ncy) continue;
+                        const double *row = rr + ((fi % RRR) * 2 + 0) * JT2;
+                        const double h = 0.5 * row[q - 1] + row[q] + 0.5 * row[q + 1];
+                        const double wd = (d == 0 || d == 3) ? 0.25 : 0.75;
+                        sx += wd * h;
+                        wsum += wd;
+                    }
+                    a.bxc[at(gc, I, J)] = sx * (wsum == 2.0 ? 0.25 : 1.0 / (2.0 * wsum));
+                }
+                if (emit_y && I <= gc.nvyi) {
+                    const int q = 2 * J - 2 - (j0 - 3);  // rr column of fine column 2J-2
+                    double sy = 0.0, wsum = 0.0;
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) {
+                        const int fj = 2 * J - 2 + d;
+                        if (fj < 1 || fj > g.ncx) continue;
+                        const double col = 0.5 * rr[(((2 * I - 1) % RRR) * 2 + 1) * JT2 + q + d] +
+                                           rr[(((2 * I) % RRR) * 2 + 1) * JT2 + q + d] +
+                                           0.5 * rr[(((2 * I + 1) % RRR) * 2 + 1) * JT2 + q + d];
+                        const double wd = (d == 0 || d == 3) ? 0.25 : 0.75;
+                        sy += wd * col;
+                        wsum += wd;
+                    }
+                    a.byc[at(gc, I, J)] = sy * (wsum == 2.0 ? 0.25 : 1.0 / (2.0 * wsum));
+                }
+            }
+        }
+        // ---- carry: rows shift down by one
+        lag4_eb = e3.ebc;
+        e3 = e2;
+        e2 = E4{v.A[F_EB].l, v.A[F_EB].c, v.A[F_EP].c, v.A[F_EP].r};
+        bx3 = bx2;
+        by3 = by2;
+        bx2 = bxp;
+        by2 = byp;
+        toA();
+        iax = iax_n;
+        iay = iay_n;
+        bxp = bx_n;
+        byp = by_n;
+        qB = qC;
+        slotB = slotC;
+    }
+}
+
 // ---- damped red-black Gauss-Seidel in two streamed passes (a4, reading R11) -------------
 // The four phases (vx red, vx black, vy red, vy black; red = (i + j + par) even) as two
 // passes, one per component: pass COMP updates that component's red nodes of row s and
@@ -1511,13 +1818,26 @@ __global__ void __launch_bounds__(NTB) k_rbgs1(GridL g, J2Args a, int H) {
     __syncthreads();
     if (tt == 0)
         for (int r = rlo; r < rlo + NSB && r <= rhi; ++r) issue(r);
-    int landed = rlo - 1;
-    auto slot_of = [&](int r) { return sm + ((r - rlo) % NSB) * NF * RWR + t + 1; };
+    // rows are waited for in order; the ring slot / mbarrier phase of the next row to wait for
+    // and the slot of row s advance incrementally (no division per access)
+    int landed = rlo - 1, wslot = 0;
+    uint32_t wphase = 0;
     auto wait_to = [&](int r) {
         for (; landed < r; ++landed) {
-            const int rel = landed + 1 - rlo;
-            mbar_wait(bars + rel % NSB, (rel / NSB) & 1);
+            mbar_wait(bars + wslot, wphase);
+            if (++wslot == NSB) {
+                wslot = 0;
+                wphase ^= 1u;
+            }
         }
+    };
+    const double *sm_t = sm + t + 1;
+    int sbase = 0;  // ring slot of row s
+    auto slot_back = [&](int d) {  // this thread's column in the slot of row s - d (-1 <= d <= NSB - 1)
+        int q = sbase - d;
+        q += q < 0 ? NSB : 0;
+        q -= q >= NSB ? NSB : 0;
+        return const_cast<double *>(sm_t + q * (NF * RWR));
     };
     // valid lanes of each phase (the cone) and the output columns of this CTA
     const bool own = t >= 3 && t < 3 + a.tw;
@@ -1526,17 +1846,18 @@ __global__ void __launch_bounds__(NTB) k_rbgs1(GridL g, J2Args a, int H) {
     const bool vy_red_ok = c >= 1 && c <= g.ncx && t >= 2 && t <= TWR - 2;
     const bool vy_blk_ok = c >= 1 && c <= g.ncx && t >= 3 && t <= TWR - 3;
     const int s_lo = max(i0 - 2, 1), s_hi = i1 + 6;
-    for (int s = s_lo; s <= s_hi; ++s) {
+    sbase = (s_lo - rlo) % NSB;
+    for (int s = s_lo; s <= s_hi; ++s, sbase = sbase + 1 == NSB ? 0 : sbase + 1) {
         wait_to(min(s + 1, rhi));
         const bool red = ((s + c + g.par) & 1) == 0;
         // ---- vx: red node of row s or black node of row s-2
         if (role != 1) {
-            const int r = red ? s : s - 2;
+            const int d = red ? 0 : 2, r = s - d;
             const bool act = red ? (vx_red_ok && r <= min(i1 + 3, g.ncy))
                                  : (vx_blk_ok && r >= max(i0 - 1, 1) && r <= min(i1 + 2, g.ncy));
             if (act) {
-                double *sb = slot_of(r);
-                const SmB w{slot_of(r - 1), sb, slot_of(r + 1)};
+                double *sb = slot_back(d);
+                const SmB w{slot_back(d + 1), sb, slot_back(d - 1)};
                 const RowX x = lx_win(g, w, r);
                 const double b = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
                 const double vn = w.B(F_VX) + a.omega * (b - x.L) * rcp(x.a);
@@ -1550,12 +1871,12 @@ __global__ void __launch_bounds__(NTB) k_rbgs1(GridL g, J2Args a, int H) {
         }
         // ---- vy: red node of row s-4 or black node of row s-6
         if (role != 0) {
-            const int r = red ? s - 4 : s - 6;
+            const int d = red ? 4 : 6, r = s - d;
             const bool act = red ? (vy_red_ok && r >= max(i0 - 1, 1) && r <= min(i1 + 1, g.nvyi))
                                  : (vy_blk_ok && r >= i0 && r <= min(i1, g.nvyi));
             if (act) {
-                double *sb = slot_of(r);
-                const SmB w{slot_of(r - 1), sb, slot_of(r + 1)};
+                double *sb = slot_back(d);
+                const SmB w{slot_back(d + 1), sb, slot_back(d - 1)};
                 const RowX y = ly_win(g, w, c);
                 const double b = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
                 const double vn = w.B(F_VY) + a.omega * (b - y.L) * rcp(y.a);
@@ -1747,6 +2068,48 @@ void launch_jacobi_stream_part(const LaunchCtx &c, const GridL &g, const double 
         op.gx = op.gy = 0.0;
         run_part(c, g, op, part);
     }
+}
+
+// the last pre-smoothing pair fused with the residual and its restriction (k_j2rr):
+// single-domain levels whose pairs stream; OFF by default (STOKES_J2RR=1 enables it):
+// measured slower -- 537 us per fine launch against 245 + 193 us for the pair and the
+// residual+restriction pass, layered solve 546 -> 588 ms (r02): the three stencil stages per
+// row step at 128 registers (3 CTAs per SM) cost more issue time than the HBM pass they save
+bool j2rr_ok(const GridL &g) {
+    static const bool on = [] {
+        const char *e = getenv("STOKES_J2RR");
+        return e && e[0] == '1';
+    }();
+    return on && g.bN && g.bS && g.bW && g.bE && jacobi2_ok(g);
+}
+void launch_j2rr(const LaunchCtx &c, const GridL &g, const GridL &gc, const double *etab, const double *etap,
+                 const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega,
+                 double *bxc, double *byc) {
+    J2RArgs a;
+    const bool fine = rhs.mode == RHS_FINE;
+    fill_src(a.src, vxi, vyi, etap, etab, fine ? rhs.p : rhs.bx, fine ? rhs.rho : rhs.by);
+    a.vxo = vxo;
+    a.vyo = vyo;
+    a.bxc = bxc;
+    a.byc = byc;
+    a.omega = omega;
+    a.gx = fine ? rhs.gx : 0.0;
+    a.gy = fine ? rhs.gy : 0.0;
+    a.tw = JT2 - 6;
+    const int ncb = (g.ncx + a.tw - 1) / a.tw;
+    int strips = slots() / MINB * J2R_MINB / ncb;  // one wave at J2R_MINB CTAs per SM
+    if (strips < 1) strips = 1;
+    int HC = (gc.ncy + strips - 1) / strips;
+    if (HC < 2) HC = 2;
+    const dim3 grid(ncb, (gc.ncy + HC - 1) / HC);
+    static unsigned long long done = 0;
+    if (first_on_device(&done)) {
+        cudaFuncSetAttribute(k_j2rr<RHS_FINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJ2R);
+        cudaFuncSetAttribute(k_j2rr<RHS_ARRAYS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEMJ2R);
+    }
+    if (fine) k_j2rr<RHS_FINE><<<grid, JT2, SMEMJ2R, c.stream>>>(g, gc, a, HC);
+    else k_j2rr<RHS_ARRAYS><<<grid, JT2, SMEMJ2R, c.stream>>>(g, gc, a, HC);
+    ++*c.counter;
 }
 
 void launch_residual_restrict(const LaunchCtx &c, const GridL &g, const GridL &gc, const double *etab,

@@ -156,6 +156,41 @@ print(worst)
     assert float(r.stdout.strip().splitlines()[-1]) <= TOL_OP
 
 
+def test_fused_pair_residual_restriction_forced():
+    """The last pre-smoothing pair fused with the residual and its restriction (k_j2rr, off by
+    default: measured slower) enabled in a subprocess (STOKES_J2RR=1): V-cycles on ragged
+    grids with several column tiles and coarse-row strips against the oracle (<= 1e-12)."""
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, %r)
+from oracle.oracle import Oracle
+from synth.fields import parity_fields
+from paper_2603_14040_b200 import Stokes
+T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+rel = lambda a, b: float(np.linalg.norm(a.cpu().numpy() - b) / np.linalg.norm(b))
+worst = 0.0
+for (nx, ny, bc) in [(512, 256, (0, 1, 0, 1)), (640, 384, (1, 1, 0, 0)), (128, 128, (0, 0, 0, 0))]:
+    f = parity_fields(nx, ny, log_contrast=1.0)
+    kw = dict(omega_v=0.5)
+    o, s = Oracle(nx, ny, 1.0, 1.0, bc, **kw), Stokes(nx, ny, 1.0, 1.0, bc, **kw)
+    o.set_viscosity(f["eta_b"], f["eta_p"]); s.set_viscosity(T(f["eta_b"]), T(f["eta_p"]))
+    o.set_density(f["rho_b"]); s.set_density(T(f["rho_b"]))
+    o.set_gravity(0.2, 1.0); s.set_gravity(0.2, 1.0)
+    rng = np.random.default_rng(12)
+    bx, by = rng.standard_normal((ny, nx + 1)), rng.standard_normal((ny + 1, nx))
+    ex, ey = o.vcycle(bx, by, f["vx"], f["vy"])
+    gx, gy = s.vcycle(T(bx), T(by), T(f["vx"]), T(f["vy"]))
+    worst = max(worst, rel(gx, ex), rel(gy, ey))
+print(worst)
+""" % ROOT
+    env = dict(os.environ, STOKES_J2RR="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= TOL_OP
+
+
 @pytest.mark.parametrize("tile,tin,nsweeps", [(8, 2, 3), (32, 4, 5), (5, 3, 8)])
 @pytest.mark.parametrize("nx,ny", [(100, 60), (256, 130)])
 @pytest.mark.parametrize("bc", BCS)

@@ -162,6 +162,50 @@ __device__ __forceinline__ RowX ly_win(const GridL &g, const W &w, int j) {
     if (EDGE && j == g.ncx && g.bE) r.a += g.sE * etaE * g.idx2;
     return r;
 }
+// The same rows split as L v = S + a v_c: S = the weighted sum of the neighbours only (the
+// mirror ghost of a global wall left out: its coefficient is folded into a, exactly as in
+// lx_win), a = the BC-folded centre coefficient.  A damped Jacobi update then reads
+//   v' = v + w (b - L v) / a = (1 - w) v + (w / a) (b - S)
+// -- 11 FP64 operations for S instead of 15 for L, and the update no longer needs L.
+struct RowS {
+    double S, a;
+};
+template <bool EDGE = true, class W>
+__device__ __forceinline__ RowS lxs_win(const GridL &g, const W &w, int i) {
+    const double eta1 = w.A(F_EB), eta2 = w.B(F_EB), etaA = w.B(F_EP), etaB = w.B(F_EP, 1);
+    double vN = w.A(F_VX), vS = w.C(F_VX);
+    RowS r;
+    r.a = -(eta1 + eta2) * g.idy2 - (etaA + etaB) * g.idx2x2;
+    if (EDGE && i == 1 && g.bN) {
+        r.a += g.sN * eta1 * g.idy2;
+        vN = 0.0;
+    }
+    if (EDGE && i == g.ncy && g.bS) {
+        r.a += g.sS * eta2 * g.idy2;
+        vS = 0.0;
+    }
+    r.S = g.idx2x2 * (etaA * w.B(F_VX, -1) + etaB * w.B(F_VX, 1)) + g.idy2 * (eta1 * vN + eta2 * vS) +
+          g.idxdy * (eta1 * (w.A(F_VY) - w.A(F_VY, 1)) + eta2 * (w.B(F_VY, 1) - w.B(F_VY)));
+    return r;
+}
+template <bool EDGE = true, class W>
+__device__ __forceinline__ RowS lys_win(const GridL &g, const W &w, int j) {
+    const double etaN = w.B(F_EP), etaS = w.C(F_EP), etaW = w.B(F_EB, -1), etaE = w.B(F_EB);
+    double vW = w.B(F_VY, -1), vE = w.B(F_VY, 1);
+    RowS r;
+    r.a = -(etaN + etaS) * g.idy2x2 - (etaW + etaE) * g.idx2;
+    if (EDGE && j == 1 && g.bW) {
+        r.a += g.sW * etaW * g.idx2;
+        vW = 0.0;
+    }
+    if (EDGE && j == g.ncx && g.bE) {
+        r.a += g.sE * etaE * g.idx2;
+        vE = 0.0;
+    }
+    r.S = g.idy2x2 * (etaS * w.C(F_VY) + etaN * w.A(F_VY)) + g.idx2 * (etaE * vE + etaW * vW) +
+          g.idxdy * (etaE * (w.C(F_VX) - w.B(F_VX)) - etaW * (w.C(F_VX, -1) - w.B(F_VX, -1)));
+    return r;
+}
 // body force (reading R4/R23) at vx / vy nodes from the staged rho rows
 template <class W>
 __device__ __forceinline__ double fx_win(const W &w, double gx) {
@@ -827,7 +871,8 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
     const double *qB = wait_next(slotB);  // row sfirst
     const bool own_col = t >= 1 && t <= a.tw && c <= jhi;
     const bool cx_in = c >= 1 - hW && c <= g.nvxj + hE, cy_in = c >= 1 - hW && c <= g.ncx + hE;
-    // 1/a_ii and right-hand side of sweep-1 row s-1 (= the sweep-2 row): equal in both sweeps
+    const double omc = 1.0 - a.omega;
+    // w/a_ii and right-hand side of sweep-1 row s-1 (= the sweep-2 row): equal in both sweeps
     double iax = 0.0, iay = 0.0, bxp = 0.0, byp = 0.0, lag_eb = 0.0;
     // one row step s: sweep 1 of row s, sweep 2 of row s-1.  EDGE = false (CTAs whose rows
     // and columns all stay off the boundary): no boundary logic at all.
@@ -847,17 +892,18 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
         const W1 w{&v};
         // ---- sweep 1, row s
         double vx1 = v.B[F_VX].c, vy1 = v.B[F_VY].c, iax_n = 0.0, iay_n = 0.0, bx_n = 0.0, by_n = 0.0;
+        // (iax / iay hold w / a_ii: the S form of the update, lxs_win)
         if ((!ER || (s >= 1 - hN && s <= g.ncy + hS)) && (!EC || cx_in)) {
-            const RowX x = lx_win<ER>(g, w, s);
+            const RowS x = lxs_win<ER>(g, w, s);
             bx_n = (MODE == RHS_FINE) ? fx_win(w, a.gx) - (w.B(F_4) - w.B(F_4, 1)) * g.idx : w.B(F_4);
-            iax_n = rcp(x.a);
-            vx1 = w.B(F_VX) + a.omega * (bx_n - x.L) * iax_n;
+            iax_n = a.omega * rcp(x.a);
+            vx1 = fma(iax_n, bx_n - x.S, omc * w.B(F_VX));
         }
         if ((!ER || (s >= 1 - hN && s <= g.nvyi + hS)) && (!EC || cy_in)) {
-            const RowX y = ly_win<EC>(g, w, c);
+            const RowS y = lys_win<EC>(g, w, c);
             by_n = (MODE == RHS_FINE) ? fy_win(w, a.gy) - (w.B(F_4) - w.C(F_4)) * g.idy : w.B(F_5);
-            iay_n = rcp(y.a);
-            vy1 = w.B(F_VY) + a.omega * (by_n - y.L) * iay_n;
+            iay_n = a.omega * rcp(y.a);
+            vy1 = fma(iay_n, by_n - y.S, omc * w.B(F_VY));
         }
         s1[((s & 3) * 2 + 0) * JT + t] = vx1;
         s1[((s & 3) * 2 + 1) * JT + t] = vy1;
@@ -877,20 +923,18 @@ __global__ void __launch_bounds__(JT, J2_MINB) k_jacobi2(GridL g, J2Args a, int 
             u.vy[0] = R3{0.0, qa[JT], qa[JT + 1]};
             u.vy[1] = R3{qb[JT - 1], qb[JT], qb[JT + 1]};
             u.vy[2] = R3{0.0, qc[JT], 0.0};
-            if (ER && i == 1 && g.bN) u.vx[0].c = g.sN * u.vx[1].c;
-            if (ER && i == g.ncy && g.bS) u.vx[2].c = g.sS * u.vx[1].c;
-            if (EC && c == 1 && g.bW) u.vy[1].l = g.sW * u.vy[1].c;
-            if (EC && c == g.ncx && g.bE) u.vy[1].r = g.sE * u.vy[1].c;
+            // (the wall mirrors of the intermediate iterate are folded into w / a_ii: lxs_win /
+            // lys_win leave the ghosts out on global sides)
             if (!EC || c <= g.nvxj) {
-                const RowX x = lx_win<ER>(g, u, i);
-                const double vn = u.B(F_VX) + a.omega * (bxp - x.L) * iax;
+                const RowS x = lxs_win<ER>(g, u, i);
+                const double vn = fma(iax, bxp - x.S, omc * u.B(F_VX));
                 a.vxo[(size_t)i * P + c] = vn;
                 if (ER && i == 1 && g.bN) a.vxo[c] = g.sN * vn;
                 if (ER && i == g.ncy && g.bS) a.vxo[(size_t)(g.ncy + 1) * P + c] = g.sS * vn;
             }
             if (!ER || i <= g.nvyi) {
-                const RowX y = ly_win<EC>(g, u, c);
-                const double vn = u.B(F_VY) + a.omega * (byp - y.L) * iay;
+                const RowS y = lys_win<EC>(g, u, c);
+                const double vn = fma(iay, byp - y.S, omc * u.B(F_VY));
                 a.vyo[(size_t)i * P + c] = vn;
                 if (EC && c == 1 && g.bW) a.vyo[(size_t)i * P] = g.sW * vn;
                 if (EC && c == g.ncx && g.bE) a.vyo[(size_t)i * P + g.ncx + 1] = g.sE * vn;

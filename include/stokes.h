@@ -126,9 +126,10 @@ int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const s
  * 64; STOKES_DIST_DMIN) are distributed (width-2 halo exchange after every pass that writes a
  * velocity / correction / right-hand side / pressure); the coarser levels are agglomerated:
  * every process holds the global grid of the first coarse level and runs the coarse tail
- * redundantly.  Options: accel STOKES_ACCEL_NONE (Uzawa-MG) or STOKES_ACCEL_GCR (GCR(m) with
- * the distributed V-cycle as preconditioner and global inner products); Anderson, viscosity
- * rescaling (theta_step > 0) and the RAS / Mixed smoothers: STOKES_EINVAL.
+ * redundantly.  Options: accel STOKES_ACCEL_NONE (Uzawa-MG), STOKES_ACCEL_GCR (GCR(m) with
+ * the distributed V-cycle as preconditioner and global inner products) or
+ * STOKES_ACCEL_ANDERSON (AA(m, beta) over the decomposed Uzawa iteration, global Gram row);
+ * viscosity rescaling (theta_step > 0) and the RAS / Mixed smoothers: STOKES_EINVAL.
  *   rank = -1 VIRTUAL: all tiles in this process on the current GPU; every array of the
  *             calls below is the GLOBAL user-layout array (tests of the decomposition).
  *   rank = -2 LOOPBACK: as VIRTUAL, but halos and the agglomeration go through the NCCL

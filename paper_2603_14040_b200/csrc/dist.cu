@@ -69,6 +69,10 @@ struct Dist {
     // the GLOBAL sum in one fixed order; one graph per inner step i
     double *gpart[3];
     size_t gseg;  // doubles per tile segment
+    // Anderson AA(m, beta) on the tiles: the same scheme for the Gram row and the pressure mean
+    double *apart[2];
+    cudaGraphExec_t aexec[2];  // the plain (unfused) Uzawa iteration G(x) per pressure parity
+    long long akernels;
     cudaGraphExec_t gexec[MAXM];
     long long gkernels[MAXM];
     int pcur;
@@ -643,20 +647,22 @@ int force_E(Dist &D) {  // Sf -> dscal[3]
 // after every update.  A kernel's per-CTA partials go to the tile's segment of one buffer
 // (NCCL: all-gathered across the ranks), and the next kernel of EVERY tile reduces the
 // whole buffer in the same fixed order: the global inner products, identical everywhere.
-static int tiles_sum(Dist &D, int buf, int nb) {  // NCCL: all-gather rank segments of gpart[buf]
-    const size_t seg = (size_t)nb * 2;
+static int gather_segments(Dist &D, double *base, size_t seg) {  // every rank's segment of `base` everywhere
     if (D.mode == M_NCCL_SELF) {  // the same call on the one-rank communicator (in place, per tile)
         if (ncclGroupStart() != ncclSuccess) return STOKES_ENCCL;
         for (int k = 0; k < D.nt; ++k)
-            if (ncclAllGather(D.gpart[buf] + (size_t)k * seg, D.gpart[buf] + (size_t)k * seg, seg, ncclDouble, D.comm,
-                              D.stream) != ncclSuccess)
+            if (ncclAllGather(base + (size_t)k * seg, base + (size_t)k * seg, seg, ncclDouble, D.comm, D.stream) !=
+                ncclSuccess)
                 return STOKES_ENCCL;
         return ncclGroupEnd() == ncclSuccess ? STOKES_OK : STOKES_ENCCL;
     }
     if (D.mode != M_NCCL) return STOKES_OK;
-    if (ncclAllGather(D.gpart[buf] + (size_t)D.rank * seg, D.gpart[buf], seg, ncclDouble, D.comm, D.stream) != ncclSuccess)
+    if (ncclAllGather(base + (size_t)D.rank * seg, base, seg, ncclDouble, D.comm, D.stream) != ncclSuccess)
         return STOKES_ENCCL;
     return STOKES_OK;
+}
+static int tiles_sum(Dist &D, int buf, int nb) {  // NCCL: all-gather rank segments of gpart[buf]
+    return gather_segments(D, D.gpart[buf], (size_t)nb * 2);
 }
 static double *seg_of(Dist &D, int buf, int k, int nb) {  // tile k's partials (NCCL: this rank's)
     const int r = D.mode == M_NCCL ? D.rank : k;
@@ -807,6 +813,111 @@ static int dist_solve_gcr(Dist &D, double rtol, double E0, int *iters, double *E
     return status;
 }
 
+// ---- Anderson acceleration AA(m, beta) (Alg. 5; reading R26) on the tiles
+// G = one plain Uzawa iteration of the decomposed solve (its own graph per pressure parity);
+// per tile the fused k_aa_push / k_aa_update kernels, their per-CTA partials (the Gram row,
+// the sum of the new pressure) in one buffer across the tiles (NCCL: all-gathered), so every
+// tile solves the same small system from the same global sums in the same order, and the
+// pressure's lazy mean is the global one.  The working state's halos are exchanged after
+// every update (the update writes the first ring; the V-cycle reads two).
+static int dist_solve_anderson(Dist &D, double rtol, double E0, int *iters, double *Eout) {
+    int st;
+    const int NR = nranks(D), nbA = aa_blocks(D.tile[0]->lev[0].g);
+    const int m = D.o.aa_depth, ns = m + 1;
+    if (!D.apart[0])
+        for (int b = 0; b < 2; ++b)
+            if (cudaMalloc(&D.apart[b], (size_t)nbA * AA_MAXS * NR * sizeof(double)) != cudaSuccess) return STOKES_ENOMEM;
+    const int keep = D.pcur;
+    for (int q = 0; q < 2; ++q) {  // G(x): the plain Uzawa iteration, one graph per pressure parity
+        if (D.aexec[q]) continue;
+        D.pcur = q;
+        for (int t = 0; t < D.nt; ++t) D.tile[t]->pcur = q;
+        cudaGraph_t graph;
+        const long long before = dist_launches(&D, 0);
+        CK(cudaStreamBeginCapture(D.stream, cudaStreamCaptureModeThreadLocal));
+        const int bst = dist_body(D);
+        cudaError_t e = cudaStreamEndCapture(D.stream, &graph);
+        D.pcur = keep;
+        for (int t = 0; t < D.nt; ++t) D.tile[t]->pcur = keep;
+        if (bst) return bst;
+        if (e != cudaSuccess) return fail_cuda(e, "dist AA graph capture");
+        D.akernels = dist_launches(&D, 0) - before;
+        D.launches -= D.akernels;
+        e = cudaGraphInstantiate(&D.aexec[q], graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) { D.aexec[q] = nullptr; return fail_cuda(e, "dist AA graph instantiate"); }
+    }
+    // T = x^0 (its pressure mean: S_MSHIFT, set by state_E)
+    for (int k = 0; k < D.nt; ++k) {
+        stokes_s *t = D.tile[k];
+        Level &F = t->lev[0];
+        const size_t fb = field_doubles(F.g) * 8;
+        CK(cudaMemcpyAsync(t->aat.f[0] - COL_OFF, F.vx[0] - COL_OFF, fb, cudaMemcpyDeviceToDevice, D.stream));
+        CK(cudaMemcpyAsync(t->aat.f[1] - COL_OFF, F.vy[0] - COL_OFF, fb, cudaMemcpyDeviceToDevice, D.stream));
+        CK(cudaMemcpyAsync(t->aat.f[2] - COL_OFF, t->pbuf[D.pcur] - COL_OFF, fb, cudaMemcpyDeviceToDevice, D.stream));
+        CK(cudaMemcpyAsync(t->scal + S_AAMT, t->scal + S_MSHIFT, 8, cudaMemcpyDeviceToDevice, D.stream));
+    }
+    const double inv_np = 1.0 / ((double)D.NX * D.NY);
+    double E = E0;
+    int k, status = STOKES_NOT_CONVERGED;
+    for (k = 0; k < D.o.max_iter; ++k) {
+        CK(cudaGraphLaunch(D.aexec[D.pcur], D.stream));  // G(x^k) and E of it
+        D.pcur ^= 1;
+        for (int t = 0; t < D.nt; ++t) D.tile[t]->pcur = D.pcur;
+        D.launches += D.akernels;
+        if ((st = dsync(D))) return st;
+        E = D.hsc[0];
+        if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+        if (E <= rtol) { status = STOKES_OK; break; }
+        const int slot = k % ns, mk = k < m ? k : m;
+        for (int q = 0; q < D.nt; ++q) {
+            stokes_s *t = D.tile[q];
+            Level &F = t->lev[0];
+            AAWin win;
+            win.n = mk + 1;
+            win.self = mk;
+            for (int a = 0; a <= mk; ++a) {
+                win.slot[a] = (k - mk + a) % ns;
+                win.r[a] = t->aah.R[win.slot[a]];
+            }
+            const AAVec work{{F.vx[0], F.vy[0], t->pbuf[D.pcur]}};
+            launch_aa_push(ctx(t), F.g, work, t->scal + S_MSHIFT, t->aat, t->scal + S_AAMT, t->aah.G[slot],
+                           t->aah.R[slot], win, D.apart[0] + (size_t)(D.mode == M_NCCL ? D.rank : q) * nbA * AA_MAXS);
+        }
+        if ((st = gather_segments(D, D.apart[0], (size_t)nbA * AA_MAXS))) return st;
+        for (int q = 0; q < D.nt; ++q) {
+            stokes_s *t = D.tile[q];
+            Level &F = t->lev[0];
+            AAWin win;
+            win.n = mk + 1;
+            win.self = mk;
+            for (int a = 0; a <= mk; ++a) {
+                win.slot[a] = (k - mk + a) % ns;
+                win.r[a] = t->aah.R[win.slot[a]];
+            }
+            const AAVec work{{F.vx[0], F.vy[0], t->pbuf[D.pcur]}};
+            launch_aa_solve(ctx(t), D.apart[0], nbA * NR, win, D.o.aa_beta, t->aaH, t->aacg, t->aacr);
+            launch_aa_update(ctx(t), F.g, t->aah, ns, t->aacg, t->aacr, work, t->aat,
+                             D.apart[1] + (size_t)(D.mode == M_NCCL ? D.rank : q) * nbA * AA_MAXS);
+        }
+        // the update's partial sums of the new pressure: nbA per tile, gathered densely
+        if (D.mode == M_NCCL || D.mode == M_NCCL_SELF) {
+            // (segments are nbA * AA_MAXS apart; the first nbA doubles of each hold the sums)
+            if ((st = gather_segments(D, D.apart[1], (size_t)nbA * AA_MAXS))) return st;
+        }
+        for (int q = 0; q < D.nt; ++q) {
+            stokes_s *t = D.tile[q];
+            launch_dist_mean(ctx(t), D.apart[1], NR, nbA, (size_t)nbA * AA_MAXS, inv_np, t->scal + S_MSHIFT);
+            CK(cudaMemcpyAsync(t->scal + S_AAMT, t->scal + S_MSHIFT, 8, cudaMemcpyDeviceToDevice, D.stream));
+        }
+        if ((st = exchange(D, 0, FX_VP, 0 | (D.pcur << 1)))) return st;  // both halo rings of x^{k+1}
+    }
+    if (k >= D.o.max_iter) k = D.o.max_iter - 1;
+    *iters = k + 1;
+    *Eout = E;
+    return status;
+}
+
 void drop(Dist &D) {
     for (int k = 0; k < 2; ++k)
         if (D.exec[k]) {
@@ -818,6 +929,11 @@ void drop(Dist &D) {
             cudaGraphExecDestroy(D.gexec[k]);
             D.gexec[k] = nullptr;
         }
+    for (int k = 0; k < 2; ++k)
+        if (D.aexec[k]) {
+            cudaGraphExecDestroy(D.aexec[k]);
+            D.aexec[k] = nullptr;
+        }
 }
 
 // a tile handle: levels 0..La (La = agglomeration staging) with per-side flags
@@ -826,7 +942,7 @@ int make_tile(Dist &D, int tx, int ty, stokes_s **out) {
     if (!h) return STOKES_ENOMEM;
     h->o = D.o;
     h->o.coarse_direct = 0;
-    h->o.accel = D.o.accel == STOKES_ACCEL_GCR ? STOKES_ACCEL_GCR : STOKES_ACCEL_NONE;  // GCR vectors per tile
+    h->o.accel = D.o.accel;  // GCR / Anderson vectors per tile (carve)
     h->nx = D.nxt;
     h->ny = D.nyt;
     h->Lx = D.Lx * D.nxt / D.NX;
@@ -927,6 +1043,8 @@ int dist_destroy(Dist *D) {
     if (D->hsc) cudaFreeHost(D->hsc);
     for (int k = 0; k < 3; ++k)
         if (D->gpart[k]) cudaFree(D->gpart[k]);
+    for (int k = 0; k < 2; ++k)
+        if (D->apart[k]) cudaFree(D->apart[k]);
     if (D->own_stream) cudaStreamDestroy(D->stream);
     if (D->cstream) cudaStreamDestroy(D->cstream);
     for (int k = 0; k < 2; ++k)
@@ -1042,6 +1160,9 @@ int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *ite
         if (E0 > rtol && D->o.accel == STOKES_ACCEL_GCR) {
             status = dist_solve_gcr(*D, rtol, E0, &k, &E);
             if (status < 0 && status != STOKES_EDIVERGED) return status;
+        } else if (E0 > rtol && D->o.accel == STOKES_ACCEL_ANDERSON) {
+            status = dist_solve_anderson(*D, rtol, E0, &k, &E);
+            if (status < 0 && status != STOKES_EDIVERGED) return status;
         } else if (E0 > rtol) {
             status = STOKES_NOT_CONVERGED;
             const int keep = D->pcur;
@@ -1134,8 +1255,8 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
                        const void *nccl_unique_id, const stokes_opts *opts, void *cuda_stream, stokes_t *out) {
     if (!out || px < 1 || py < 1 || px * py > MAXT || nx % px || ny % py || !bc) return STOKES_EINVAL;
     if (rank >= px * py || rank < -3 || (rank >= 0 && !nccl_unique_id)) return STOKES_EINVAL;
-    if (opts && (opts->theta_step > 0.0 || opts->accel == STOKES_ACCEL_ANDERSON || opts->smoother >= 2))
-        return STOKES_EINVAL;  // viscosity rescaling, Anderson, RAS / Mixed: single domain only
+    if (opts && (opts->theta_step > 0.0 || opts->smoother >= 2))
+        return STOKES_EINVAL;  // viscosity rescaling, RAS / Mixed: single domain only
     Dist *D = (Dist *)calloc(1, sizeof(Dist));
     if (!D) return STOKES_ENOMEM;
     D->NX = nx;
@@ -1149,8 +1270,7 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
     memcpy(D->bc, bc, sizeof(D->bc));
     if (opts) D->o = *opts;
     else stokes_opts_default(&D->o);
-    if (check_opts(D->o) || (D->o.accel != STOKES_ACCEL_NONE && D->o.accel != STOKES_ACCEL_GCR) || !(Lx > 0) ||
-        !(Ly > 0)) { free(D); return STOKES_EINVAL; }
+    if (check_opts(D->o) || !(Lx > 0) || !(Ly > 0)) { free(D); return STOKES_EINVAL; }
     for (int k = 0; k < 4; ++k)
         if (bc[k] != 0 && bc[k] != 1) { free(D); return STOKES_EINVAL; }
     D->rank = rank;

@@ -266,5 +266,7 @@ void launch_strips(const LaunchCtx &c, const StripList &l);
 void launch_rbgs_phase(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *vx,
                        double *vy, const RhsArgs &rhs, double omega, int comp, int colour);
 // out = (E, Sv, Sp) from the tiles' local (Sv, Sp, sum p); mean written to each mshift
+void launch_dist_mean(const LaunchCtx &c, const double *base, int nseg, int nb, size_t stride, double inv_np,
+                      double *out);
 void launch_dist_final(const LaunchCtx &c, const double *const *loc, int nloc, const double *Sf, double inv_np,
                        double *out, double *const *mshift, int nm);

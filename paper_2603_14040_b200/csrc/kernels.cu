@@ -1329,6 +1329,30 @@ void launch_strips(const LaunchCtx &c, const StripList &l) {
         LAUNCH_BOOK(c);
     }
 }
+// the mean of nseg segments of nb per-CTA partial sums (segment s at base + s * stride):
+// one CTA, a fixed order (lane-strided per segment, then the fixed shuffle tree), so every
+// tile that reduces the same buffer gets the same value (decomposed Anderson, dist.cu)
+__global__ void __launch_bounds__(256) k_dist_mean(const double *__restrict__ base, int nseg, int nb, size_t stride,
+                                                   double inv_np, double *__restrict__ out) {
+    __shared__ double sh[8];
+    double v = 0.0;
+    for (int sg = 0; sg < nseg; ++sg)
+        for (int b = threadIdx.x; b < nb; b += 256) v += base[(size_t)sg * stride + b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += sh[w];
+        *out = t * inv_np;
+    }
+}
+void launch_dist_mean(const LaunchCtx &c, const double *base, int nseg, int nb, size_t stride, double inv_np,
+                      double *out) {
+    k_dist_mean<<<1, 256, 0, c.stream>>>(base, nseg, nb, stride, inv_np, out);
+    LAUNCH_BOOK(c);
+}
 void launch_dist_final(const LaunchCtx &c, const double *const *loc, int nloc, const double *Sf, double inv_np,
                        double *out, double *const *mshift, int nm) {
     Ptrs a, b;

@@ -129,7 +129,8 @@ int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const s
  * redundantly.  Options: accel STOKES_ACCEL_NONE (Uzawa-MG), STOKES_ACCEL_GCR (GCR(m) with
  * the distributed V-cycle as preconditioner and global inner products) or
  * STOKES_ACCEL_ANDERSON (AA(m, beta) over the decomposed Uzawa iteration, global Gram row);
- * viscosity rescaling (theta_step > 0) and the RAS / Mixed smoothers: STOKES_EINVAL.
+ * viscosity-rescaling stages (theta_step > 0; eta_min reduced over all tiles) with any of
+ * them; the RAS / Mixed smoothers: STOKES_EINVAL.
  *   rank = -1 VIRTUAL: all tiles in this process on the current GPU; every array of the
  *             calls below is the GLOBAL user-layout array (tests of the decomposition).
  *   rank = -2 LOOPBACK: as VIRTUAL, but halos and the agglomeration go through the NCCL

@@ -80,6 +80,8 @@ struct Dist {
     double gx, gy;
 };
 
+int dist_eta_hierarchy(Dist *D);
+
 namespace {
 
 enum { FX_V = 0, FX_R = 1, FX_P = 2, FX_ETA = 3, FX_RHO = 4, FX_B = 5, FX_VP = 6, FX_GR = 7 };
@@ -1063,6 +1065,26 @@ int dist_set_viscosity(Dist *D, const double *eta_b, const double *eta_p) {
     }
     int st;
     if ((st = exchange(*D, 0, FX_ETA, 0))) return st;
+    if (D->o.theta_step > 0.0)  // the caller's field (halos included) for the rescaling stages
+        for (int k = 0; k < D->nt; ++k) {
+            stokes_s *t = D->tile[k];
+            Level &F = t->lev[0];
+            CK(cudaMemcpyAsync(fstart(F.g, t->etab_user), fstart(F.g, F.etab), fsize(F.g) * 8, cudaMemcpyDeviceToDevice,
+                               D->stream));
+            CK(cudaMemcpyAsync(fstart(F.g, t->etap_user), fstart(F.g, F.etap), fsize(F.g) * 8, cudaMemcpyDeviceToDevice,
+                               D->stream));
+        }
+    if ((st = dist_eta_hierarchy(D))) return st;
+    if ((st = dsync(*D))) return st;
+    D->have_eta = true;
+    drop(*D);
+    if (D->have_rho) return force_E(*D);
+    return STOKES_OK;
+}
+// coarse viscosities of the tiles (halos per level), the agglomerated tail's hierarchy and
+// coarsest inverse, GCR energy weights -- from the tiles' current level-0 eta (halos valid)
+int dist_eta_hierarchy(Dist *D) {
+    int st;
     for (int l = 0; l < D->La; ++l) {  // a7 on the tiles, halos refreshed per level
         for (int k = 0; k < D->nt; ++k) {
             stokes_s *t = D->tile[k];
@@ -1079,10 +1101,6 @@ int dist_set_viscosity(Dist *D, const double *eta_b, const double *eta_p) {
             Level &F = t->lev[0];
             launch_energy_weights(ctx(t), F.g, F.etab, F.etap, t->gew[0], t->gew[1], t->gew[2]);
         }
-    if ((st = dsync(*D))) return st;
-    D->have_eta = true;
-    drop(*D);
-    if (D->have_rho) return force_E(*D);
     return STOKES_OK;
 }
 
@@ -1135,6 +1153,144 @@ int dist_residual_energy(Dist *D, const double *vx, const double *vy, const doub
     return state_E(*D, E);
 }
 
+static int dist_core(Dist *D, double rtol, double E0, int *kout, double *Eout) {
+    int st, k = 0, status = STOKES_OK;
+    double E = E0;
+    if (E0 > rtol && D->o.accel == STOKES_ACCEL_GCR) {
+        status = dist_solve_gcr(*D, rtol, E0, &k, &E);
+        if (status < 0 && status != STOKES_EDIVERGED) return status;
+    } else if (E0 > rtol && D->o.accel == STOKES_ACCEL_ANDERSON) {
+        status = dist_solve_anderson(*D, rtol, E0, &k, &E);
+        if (status < 0 && status != STOKES_EDIVERGED) return status;
+    } else if (E0 > rtol) {
+        status = STOKES_NOT_CONVERGED;
+        const int keep = D->pcur;
+        const bool fused = dist_fused_ok(*D);
+        for (int q = 0; q < 2; ++q) {  // capture one iteration per pressure parity
+            if (D->exec[q]) continue;
+            D->pcur = q;
+            for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = q;
+            cudaGraph_t graph;
+            const long long before = dist_launches(D, 0);
+            CK(cudaStreamBeginCapture(D->stream, cudaStreamCaptureModeThreadLocal));
+            int bst = fused ? dist_fused_body(*D) : dist_body(*D);
+            cudaError_t e = cudaStreamEndCapture(D->stream, &graph);
+            D->pcur = keep;
+            for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = keep;
+            if (bst) return bst;
+            if (e != cudaSuccess) return fail_cuda(e, "dist graph capture");
+            D->body_kernels = dist_launches(D, 0) - before;
+            D->launches -= D->body_kernels;  // captured, not executed
+            e = cudaGraphInstantiate(&D->exec[q], graph, 0);
+            cudaGraphDestroy(graph);
+            if (e != cudaSuccess) { D->exec[q] = nullptr; return fail_cuda(e, "dist graph instantiate"); }
+        }
+        if (fused && D->o.max_iter >= 1) {
+            // iteration 1: a full V-cycle from (v^0, p^0), then the fused tail of iterate 1;
+            // iteration k+1: the captured rest of V-cycle k+1 + the fused tail
+            if ((st = dvcycle(*D, 0, true, false))) return st;
+            if ((st = dist_fused_tail(*D))) return st;
+            for (k = 1;; ) {
+                D->pcur ^= 1;  // pbuf[pcur] = p^k
+                for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = D->pcur;
+                if ((st = dsync(*D))) return st;
+                E = D->hsc[0];
+                if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+                if (E <= rtol) { status = STOKES_OK; break; }
+                if (k >= D->o.max_iter) break;
+                ++k;
+                CK(cudaGraphLaunch(D->exec[D->pcur], D->stream));
+                D->launches += D->body_kernels;
+            }
+        } else {
+            for (k = 1; k <= D->o.max_iter; ++k) {
+                CK(cudaGraphLaunch(D->exec[D->pcur], D->stream));
+                D->pcur ^= 1;
+                for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = D->pcur;
+                D->launches += D->body_kernels;
+                if ((st = dsync(*D))) return st;
+                E = D->hsc[0];
+                if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
+                if (E <= rtol) { status = STOKES_OK; break; }
+            }
+            if (k > D->o.max_iter) k = D->o.max_iter;
+        }
+    }
+    *kout = k;
+    *Eout = E;
+    return status;
+}
+
+// eta_min over both caller fields of every tile (reading R24) -> each tile's S_ETAMIN
+// (positive doubles order as their bit patterns: atomicMin / ncclMin on uint64)
+static int dist_eta_min(Dist &D) {
+    const unsigned long long big = 0x7ff0000000000000ull;  // +inf
+    unsigned long long *m0 = reinterpret_cast<unsigned long long *>(D.tile[0]->scal + S_ETAMIN);
+    CK(cudaMemcpyAsync(m0, &big, 8, cudaMemcpyHostToDevice, D.stream));
+    for (int k = 0; k < D.nt; ++k) {
+        stokes_s *t = D.tile[k];
+        launch_eta_min(ctx(t), t->lev[0].g, t->etab_user, t->etap_user, m0);
+    }
+    if (D.mode == M_NCCL || D.mode == M_NCCL_SELF)
+        if (ncclAllReduce(m0, m0, 1, ncclUint64, ncclMin, D.comm, D.stream) != ncclSuccess) return STOKES_ENCCL;
+    for (int k = 1; k < D.nt; ++k)
+        CK(cudaMemcpyAsync(D.tile[k]->scal + S_ETAMIN, m0, 8, cudaMemcpyDeviceToDevice, D.stream));
+    CK(cudaStreamSynchronize(D.stream));  // (the host constant `big` is stack memory)
+    return STOKES_OK;
+}
+static int dist_set_theta(Dist &D, double theta) {  // eta = (1 - theta) eta_min + theta eta_user
+    for (int k = 0; k < D.nt; ++k) {
+        stokes_s *t = D.tile[k];
+        Level &F = t->lev[0];
+        launch_eta_blend(ctx(t), F.g, t->etab_user, t->etap_user, F.etab, F.etap,
+                         reinterpret_cast<const unsigned long long *>(t->scal + S_ETAMIN), theta);
+    }
+    int st = exchange(D, 0, FX_ETA, 0);
+    if (st) return st;
+    return dist_eta_hierarchy(&D);
+}
+// the staged solve of solve_staged (driver.cu) on the tiles: stages theta = 0, step, ... < 1 of
+// theta_every iterations each (no stopping test), then theta = 1 to E <= rtol
+static int dist_solve_staged(Dist *D, double rtol, int *iters, double *Eout) {
+    const int budget = D->o.max_iter;
+    int used = 0, it = 0, st = 0, status = STOKES_OK;
+    double E = 0.0, E0 = 0.0;
+    if ((st = dist_eta_min(*D))) return st;
+    for (int k = 0;; ++k) {
+        const double theta = k * D->o.theta_step;
+        if (theta >= 1.0 || used >= budget) break;
+        if ((st = dist_set_theta(*D, theta))) return st;
+        if ((st = force_E(*D))) return st;
+        if ((st = state_E(*D, &E0))) return st;
+        D->o.max_iter = budget - used < D->o.theta_every ? budget - used : D->o.theta_every;
+        status = dist_core(D, -1.0, E0, &it, &E);
+        D->o.max_iter = budget;
+        if (status < 0 && status != STOKES_EDIVERGED) return status;
+        used += it;
+        if (status == STOKES_EDIVERGED) break;
+    }
+    if ((st = dist_set_theta(*D, 1.0))) return st;
+    if ((st = force_E(*D))) return st;
+    if (status != STOKES_EDIVERGED && used < budget) {
+        if ((st = state_E(*D, &E0))) return st;
+        if (E0 <= rtol) {
+            E = E0;
+            status = STOKES_OK;
+        } else {
+            D->o.max_iter = budget - used;
+            status = dist_core(D, rtol, E0, &it, &E);
+            D->o.max_iter = budget;
+            if (status < 0 && status != STOKES_EDIVERGED) return status;
+            used += it;
+        }
+    } else if (status != STOKES_EDIVERGED) {
+        status = STOKES_NOT_CONVERGED;
+    }
+    *iters = used;
+    *Eout = E;
+    return status;
+}
+
 int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *iters, double *Eout) {
     if (!D->have_eta || !D->have_rho) return STOKES_ESTATE;
     int st = load_state(D, vx, vy, p);
@@ -1155,66 +1311,15 @@ int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *ite
             CK(cudaMemsetAsync(t->scal + S_MSHIFT, 0, 8, D->stream));
         }
     } else {
-        if ((st = state_E(*D, &E0))) return st;
-        E = E0;
-        if (E0 > rtol && D->o.accel == STOKES_ACCEL_GCR) {
-            status = dist_solve_gcr(*D, rtol, E0, &k, &E);
+        if (D->o.theta_step > 0.0) {  // viscosity-rescaling stages (reading R24)
+            status = dist_solve_staged(D, rtol, &k, &E);
             if (status < 0 && status != STOKES_EDIVERGED) return status;
-        } else if (E0 > rtol && D->o.accel == STOKES_ACCEL_ANDERSON) {
-            status = dist_solve_anderson(*D, rtol, E0, &k, &E);
-            if (status < 0 && status != STOKES_EDIVERGED) return status;
-        } else if (E0 > rtol) {
-            status = STOKES_NOT_CONVERGED;
-            const int keep = D->pcur;
-            const bool fused = dist_fused_ok(*D);
-            for (int q = 0; q < 2; ++q) {  // capture one iteration per pressure parity
-                if (D->exec[q]) continue;
-                D->pcur = q;
-                for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = q;
-                cudaGraph_t graph;
-                const long long before = dist_launches(D, 0);
-                CK(cudaStreamBeginCapture(D->stream, cudaStreamCaptureModeThreadLocal));
-                int bst = fused ? dist_fused_body(*D) : dist_body(*D);
-                cudaError_t e = cudaStreamEndCapture(D->stream, &graph);
-                D->pcur = keep;
-                for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = keep;
-                if (bst) return bst;
-                if (e != cudaSuccess) return fail_cuda(e, "dist graph capture");
-                D->body_kernels = dist_launches(D, 0) - before;
-                D->launches -= D->body_kernels;  // captured, not executed
-                e = cudaGraphInstantiate(&D->exec[q], graph, 0);
-                cudaGraphDestroy(graph);
-                if (e != cudaSuccess) { D->exec[q] = nullptr; return fail_cuda(e, "dist graph instantiate"); }
-            }
-            if (fused && D->o.max_iter >= 1) {
-                // iteration 1: a full V-cycle from (v^0, p^0), then the fused tail of iterate 1;
-                // iteration k+1: the captured rest of V-cycle k+1 + the fused tail
-                if ((st = dvcycle(*D, 0, true, false))) return st;
-                if ((st = dist_fused_tail(*D))) return st;
-                for (k = 1;; ) {
-                    D->pcur ^= 1;  // pbuf[pcur] = p^k
-                    for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = D->pcur;
-                    if ((st = dsync(*D))) return st;
-                    E = D->hsc[0];
-                    if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
-                    if (E <= rtol) { status = STOKES_OK; break; }
-                    if (k >= D->o.max_iter) break;
-                    ++k;
-                    CK(cudaGraphLaunch(D->exec[D->pcur], D->stream));
-                    D->launches += D->body_kernels;
-                }
-            } else {
-                for (k = 1; k <= D->o.max_iter; ++k) {
-                    CK(cudaGraphLaunch(D->exec[D->pcur], D->stream));
-                    D->pcur ^= 1;
-                    for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = D->pcur;
-                    D->launches += D->body_kernels;
-                    if ((st = dsync(*D))) return st;
-                    E = D->hsc[0];
-                    if (!(E == E) || isinf(E) || E > 1e6 * E0) { status = STOKES_EDIVERGED; break; }
-                    if (E <= rtol) { status = STOKES_OK; break; }
-                }
-                if (k > D->o.max_iter) k = D->o.max_iter;
+        } else {
+            if ((st = state_E(*D, &E0))) return st;
+            E = E0;
+            if (E0 > rtol) {
+                status = dist_core(D, rtol, E0, &k, &E);
+                if (status < 0 && status != STOKES_EDIVERGED) return status;
             }
         }
         *iters = k;
@@ -1255,8 +1360,7 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
                        const void *nccl_unique_id, const stokes_opts *opts, void *cuda_stream, stokes_t *out) {
     if (!out || px < 1 || py < 1 || px * py > MAXT || nx % px || ny % py || !bc) return STOKES_EINVAL;
     if (rank >= px * py || rank < -3 || (rank >= 0 && !nccl_unique_id)) return STOKES_EINVAL;
-    if (opts && (opts->theta_step > 0.0 || opts->smoother >= 2))
-        return STOKES_EINVAL;  // viscosity rescaling, RAS / Mixed: single domain only
+    if (opts && opts->smoother >= 2) return STOKES_EINVAL;  // RAS / Mixed: single domain only
     Dist *D = (Dist *)calloc(1, sizeof(Dist));
     if (!D) return STOKES_ENOMEM;
     D->NX = nx;

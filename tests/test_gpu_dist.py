@@ -133,7 +133,7 @@ def test_decomposition_errors():
     with pytest.raises(StokesError):
         StokesDist(130, 64, px=4, py=1)  # 130 % 4 != 0
     with pytest.raises(StokesError):
-        StokesDist(64, 64, px=2, py=2, theta_step=0.25)  # viscosity rescaling: single domain only
+        StokesDist(64, 64, px=2, py=2, smoother=2)  # RAS: single domain only
 
 
 def test_nccl_transport_single_rank():
@@ -234,3 +234,31 @@ def test_anderson_on_tiles(transport, px, py, name, m, beta):
     a, b = one.solve(1e-11), dd.solve(1e-11)
     for q in ("vx", "vy", "p"):
         assert rel(b[q], a[q]) <= 1e-9, (q, rel(b[q], a[q]))
+
+
+@pytest.mark.parametrize("transport", TRANSPORTS)
+@pytest.mark.parametrize("px,py", [(2, 1), (2, 2)])
+@pytest.mark.parametrize("accel", [0, 1])
+def test_viscosity_stages_on_tiles(transport, px, py, accel):
+    """Viscosity-rescaling continuation (reading R24) on the tiles: eta_min reduced over every
+    tile (ncclMin on the bit patterns under NCCL), the blended fine viscosity, its coarse
+    hierarchy and the tail's coarsest inverse rebuilt per stage, the stages' iterations without
+    a stopping test, then theta = 1 to the tolerance.  Uzawa: the decomposition is exact (the
+    same count, fields 1e-11); GCR: counts +-1, converged fields 1e-9."""
+    from paper_2603_14040_b200 import Stokes, StokesDist
+    n = 128
+    w = workload("block", n, n)
+    opts = dict(omega_v=0.6, alpha_p=1.0, theta_step=0.25, theta_every=6, accel=accel, gcr_restart=30)
+    one = setup(Stokes, w, n, max_iter=3000, **opts)
+    dd = setup(StokesDist, w, n, px=px, py=py, transport=transport, max_iter=3000, **opts)
+    a, b = one.solve(1e-8), dd.solve(1e-8)
+    assert a["status"] == 0 and b["status"] == 0
+    if accel == 0:
+        assert a["iters"] == b["iters"], (a["iters"], b["iters"])
+        for q in ("vx", "vy", "p"):
+            assert rel(b[q], a[q]) <= 1e-11, (q, rel(b[q], a[q]))
+    else:
+        assert abs(a["iters"] - b["iters"]) <= 1, (a["iters"], b["iters"])
+        a, b = one.solve(1e-11), dd.solve(1e-11)
+        for q in ("vx", "vy", "p"):
+            assert rel(b[q], a[q]) <= 1e-9, (q, rel(b[q], a[q]))

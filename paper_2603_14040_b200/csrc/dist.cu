@@ -1292,6 +1292,7 @@ static int dist_solve_staged(Dist *D, double rtol, int *iters, double *Eout) {
 }
 
 int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *iters, double *Eout) {
+    NVTX_RANGE("dist_solve");
     if (!D->have_eta || !D->have_rho) return STOKES_ESTATE;
     int st = load_state(D, vx, vy, p);
     if (st) return st;

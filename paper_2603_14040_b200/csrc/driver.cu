@@ -770,6 +770,7 @@ int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *E
     int k = 1, status = STOKES_NOT_CONVERGED;
     // iteration 1: a full V-cycle from (v^0, p^0), then the fused tail of iterate 1
     int q = 1, b = 0;  // q: buffer of the next first sweep; b: buffer of v^(k-1/2) (k_jju path)
+    nvtxRangePushA("uzawa: iteration 1");
     ras_iteration_start(h);
     if (jju) {
         double *lx = nullptr, *ly = nullptr;
@@ -782,6 +783,8 @@ int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *E
         ras_iteration_end(h);
         fused_tail(h);
     }
+    nvtxRangePop();
+    NVTX_RANGE("uzawa: iterations 2..k (device loop or graph replays)");
     for (;;) {
         h->pcur ^= 1;  // pbuf[pcur] = p^k
         int st = sync(h);
@@ -1181,6 +1184,7 @@ int stokes_level_shape(stokes_t h, int level, int *nx, int *ny, int *nu) {
 
 int stokes_set_viscosity(stokes_t h, const double *eta_b, const double *eta_p) {
     DEVICE_GUARD(h);
+    NVTX_RANGE("stokes_set_viscosity");
     if (!h || !eta_b || !eta_p) return STOKES_EINVAL;
     if (h->dist) return dist_set_viscosity(h->dist, eta_b, eta_p);
     const LaunchCtx c = ctx(h);
@@ -1305,6 +1309,7 @@ int stokes_residual(stokes_t h, const double *vx, const double *vy, const double
 
 int stokes_vcycle(stokes_t h, const double *bx, const double *by, double *vx, double *vy) {
     DEVICE_GUARD(h);
+    NVTX_RANGE("stokes_vcycle");
     if (!h || h->dist || !bx || !by || !vx || !vy) return STOKES_EINVAL;
     if (!h->have_eta) return STOKES_ESTATE;
     Level &F = h->lev[0];
@@ -1334,6 +1339,7 @@ int stokes_solve_hist(stokes_t h, double rtol, double *vx, double *vy, double *p
 
 int stokes_solve(stokes_t h, double rtol, double *vx, double *vy, double *p, int *iters, double *rel_energy) {
     DEVICE_GUARD(h);
+    NVTX_RANGE("stokes_solve");
     if (!h || !vx || !vy || !p || !iters || !rel_energy || !(rtol >= 0)) return STOKES_EINVAL;
     if (h->dist) return dist_solve(h->dist, rtol, vx, vy, p, iters, rel_energy);
     if (!h->have_eta || !h->have_rho) return STOKES_ESTATE;

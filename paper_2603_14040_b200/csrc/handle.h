@@ -3,6 +3,8 @@
 #pragma once
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.h"
 
 #define MAXLEV 24
@@ -146,6 +148,13 @@ void force_energy(stokes_s *h);
 }  // namespace sk
 
 #define DEVICE_GUARD(h) sk::DevGuard dev_guard_((h) ? (h)->device : -1)
+// NVTX ranges (header-only NVTX3: free unless a profiler is attached) around the ABI calls
+// and the solve phases, so nsys / ncu timelines show where a solve spends its time
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define NVTX_RANGE(name) NvtxRange nvtx_range_(name)
 #define CK(call)                                                  \
     do {                                                          \
         cudaError_t e_ = (call);                                  \

@@ -1,9 +1,13 @@
 """One solve of a workload inside a cudaProfilerStart/Stop range (for ncu
---profile-from-start off): setup + one warm-up solve outside the range."""
+--profile-from-start off): setup + one warm-up solve outside the range.  The host solve loop
+is used (STOKES_DEVICE_LOOP=0): ncu's launch list does not descend into the device loop's
+conditional graph nodes, so the per-iteration graphs are replayed from the host instead."""
 import argparse
 import json
 import os
 import sys
+
+os.environ.setdefault("STOKES_DEVICE_LOOP", "0")
 
 import torch
 

@@ -1,4 +1,5 @@
-"""Small solves exercising every kernel (single domain Jacobi/RBGS/GCR/Anderson/RAS/Mixed
+"""Small solves exercising every kernel (GCR, Anderson and viscosity stages also on decomposed
+handles) (single domain Jacobi/RBGS/GCR/Anderson/RAS/Mixed
 incl. the TMA streaming kernels, the one-pass RBGS (forced onto every streamed level), the
 fused k_jju pass and the device-side loop graph, viscosity stages, lithostatic pressure,
 decomposed virtual / loopback / NCCL_SELF with and without the overlapped split passes, the
@@ -40,6 +41,11 @@ os.environ["STOKES_DIST_OVERLAP"] = "1"
 run(StokesDist, 512, "layered", px=2, py=1, transport="virtual", omega_v=0.6, alpha_p=1.0, max_iter=3)
 os.environ.pop("STOKES_DIST_OVERLAP")
 run(Stokes, 512, "layered", omega_v=0.6, alpha_p=1.0, smoother=1, max_iter=2)
+run(StokesDist, 256, "block", px=2, py=2, transport="nccl_self", omega_v=0.6, alpha_p=1.0, accel=1, max_iter=4)
+run(StokesDist, 256, "block", px=2, py=1, transport="loopback", omega_v=0.6, alpha_p=1.0, accel=2, aa_depth=5,
+    aa_beta=0.7, max_iter=4)
+run(StokesDist, 128, "block", px=2, py=1, transport="virtual", omega_v=0.6, alpha_p=1.0, theta_step=0.5,
+    theta_every=2, max_iter=6)
 s = Stokes(256, 256, omega_v=0.6)
 w = workload("layered", 256, 256)
 s.set_viscosity(T(w["eta_b"]), T(w["eta_p"]))

@@ -697,6 +697,9 @@ void fill_src(const double **src, const double *vx, const double *vy, const doub
 #ifndef J2_NSJ
 #define J2_NSJ 5  // 5-deep landing ring at 160-wide CTAs (r02: 6 rows at 320 threads 293.7 us)
 #endif
+#ifndef J2_HMIN
+#define J2_HMIN 4  // minimum strip height of the two-sweep pass
+#endif
 #ifndef J2_LATE
 #define J2_LATE 0
 #endif
@@ -1952,7 +1955,7 @@ dim3 jt_grid(const GridL &g, int *H) {
     int strips = slots() / MINB * J2_MINB / ncb;  // resident two-sweep CTAs: SMs x J2_MINB
     if (strips < 1) strips = 1;
     int h = (g.ncy + strips - 1) / strips;
-    if (h < 4) h = 4;
+    if (h < J2_HMIN) h = J2_HMIN;  // (taller minimum strips: fewer CTAs on the coarse levels)
     *H = h;
     return dim3(ncb, (g.ncy + h - 1) / h);
 }

@@ -78,6 +78,7 @@ def lib():
         L.oracle_get_viscosity.argtypes = [P, ctypes.c_int, D, D]
         L.oracle_apply_operator.argtypes = [P, D, D, D, D, D, D]
         L.oracle_residual.argtypes = [P, D, D, D, D, D, D, D]
+        L.oracle_residual_ld.argtypes = [P, D, D, D, D, D, D, D]
         L.oracle_energy_sums.argtypes = [P, D, D, D, D]
         L.oracle_vcycle.argtypes = [P, D, D, D, D]
         L.oracle_smooth.argtypes = [P, ctypes.c_int, D, D, D, D, ctypes.c_int]
@@ -214,6 +215,16 @@ class Oracle:
         vx, vy, p = (np.ascontiguousarray(a, np.float64) for a in (vx, vy, p))
         _check(lib().oracle_residual(self._h, _d(vx), _d(vy), _d(p), _d(rx), _d(ry), _d(rp), ctypes.byref(e)),
                "residual")
+        return rx, ry, rp, e.value
+
+    def residual_ld(self, vx, vy, p):
+        """The residual and E of residual() evaluated in long double (verification of E near
+        convergence at large sizes, reading R34); arrays rounded to FP64."""
+        rx, ry, rp = self.zeros("vx"), self.zeros("vy"), self.zeros("p")
+        e = ctypes.c_double()
+        vx, vy, p = (np.ascontiguousarray(a, np.float64) for a in (vx, vy, p))
+        _check(lib().oracle_residual_ld(self._h, _d(vx), _d(vy), _d(p), _d(rx), _d(ry), _d(rp), ctypes.byref(e)),
+               "residual_ld")
         return rx, ry, rp, e.value
 
     def energy_sums(self, vx, vy, p):

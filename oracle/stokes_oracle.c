@@ -889,6 +889,74 @@ int oracle_residual(oracle_t *S, const double *vx, const double *vy, const doubl
     return O_OK;
 }
 
+/* ------------------------------------------------ extended-precision residual (verification)
+ * The residual and energy norm of oracle_residual -- the same formulas (Listing x row, stress
+ * y row, G, D, the weights of E) -- evaluated in long
+ * double (x87 80-bit: 64-bit significand, unit roundoff 5.4e-20 against 1.1e-16).  Verification
+ * only (reading R34): near convergence the Listing's coefficient form cancels terms
+ * ~h^-2 larger than the residual, so the FP64 evaluation of E carries rounding noise growing
+ * like h^-2 (a few % of E = 1e-8 at 16384^2); this evaluation does not. */
+typedef long double ldbl;
+static ldbl Lx_point_ld(const olevel *L, const double *vx, const double *vy, int i, int j) {
+    ldbl dx = L->dx, dy = L->dy;
+    ldbl etaA = L->etap[IX(L, i, j)], etaB = L->etap[IX(L, i, j + 1)];
+    ldbl eta1 = L->etab[IX(L, i - 1, j)], eta2 = L->etab[IX(L, i, j)];
+    ldbl vx1 = 2.0L * etaA / (dx * dx), vx2 = eta1 / (dy * dy);
+    ldbl vx3 = -(eta1 + eta2) / (dy * dy) - 2.0L * (etaA + etaB) / (dx * dx);
+    ldbl vx4 = eta2 / (dy * dy), vx5 = 2.0L * etaB / (dx * dx);
+    ldbl vy1 = eta1 / (dx * dy), vy2 = -eta2 / (dx * dy), vy3 = -eta1 / (dx * dy), vy4 = eta2 / (dx * dy);
+    return vx1 * vx[IX(L, i, j - 1)] + vx2 * vx[IX(L, i - 1, j)] + vx3 * vx[IX(L, i, j)] +
+           vx4 * vx[IX(L, i + 1, j)] + vx5 * vx[IX(L, i, j + 1)] + vy1 * vy[IX(L, i - 1, j)] +
+           vy2 * vy[IX(L, i, j)] + vy3 * vy[IX(L, i - 1, j + 1)] + vy4 * vy[IX(L, i, j + 1)];
+}
+static ldbl Ly_point_ld(const olevel *L, const double *vx, const double *vy, int i, int j) {
+    ldbl dx = L->dx, dy = L->dy;
+    ldbl syy_S = 2.0L * L->etap[IX(L, i + 1, j)] * ((ldbl)vy[IX(L, i + 1, j)] - vy[IX(L, i, j)]) / dy;
+    ldbl syy_N = 2.0L * L->etap[IX(L, i, j)] * ((ldbl)vy[IX(L, i, j)] - vy[IX(L, i - 1, j)]) / dy;
+    ldbl sxy_E = L->etab[IX(L, i, j)] *
+                 (((ldbl)vx[IX(L, i + 1, j)] - vx[IX(L, i, j)]) / dy + ((ldbl)vy[IX(L, i, j + 1)] - vy[IX(L, i, j)]) / dx);
+    ldbl sxy_W = L->etab[IX(L, i, j - 1)] *
+                 (((ldbl)vx[IX(L, i + 1, j - 1)] - vx[IX(L, i, j - 1)]) / dy +
+                  ((ldbl)vy[IX(L, i, j)] - vy[IX(L, i, j - 1)]) / dx);
+    return (syy_S - syy_N) / dy + (sxy_E - sxy_W) / dx;
+}
+int oracle_residual_ld(oracle_t *S, const double *vx, const double *vy, const double *p, double *rx, double *ry,
+                       double *rp, double *rel_energy) {
+    if (!S || !S->have_eta || !S->have_rho) return O_ESTATE;
+    olevel *L = &S->lev[0];
+    in_velocity(S, L, vx, vy, S->vx, S->vy);
+    memset(S->p, 0, padn(L) * sizeof(double));
+    in_p(L, p, S->p);
+    const double *V = S->vx, *U = S->vy, *P = S->p;
+    double *tx = zalloc(padn(L)), *ty = zalloc(padn(L)), *tp = zalloc(padn(L));
+    ldbl dx = L->dx, dy = L->dy, c = 2.0L / (dx * dx) + 2.0L / (dy * dy), sv = 0.0L, sp = 0.0L, sf = 0.0L;
+    FOR_VX(L) {
+        ldbl g = -(ldbl)P[IX(L, i, j + 1)] / dx + (ldbl)P[IX(L, i, j)] / dx;
+        ldbl r = (ldbl)S->fx[IX(L, i, j)] - (Lx_point_ld(L, V, U, i, j) + g), d = -(ldbl)Lx_diag(S, L, i, j);
+        tx[IX(L, i, j)] = (double)r;
+        sv += r * r / d;
+        sf += (ldbl)S->fx[IX(L, i, j)] * S->fx[IX(L, i, j)] / d;
+    }
+    FOR_VY(L) {
+        ldbl g = -(ldbl)P[IX(L, i + 1, j)] / dy + (ldbl)P[IX(L, i, j)] / dy;
+        ldbl r = (ldbl)S->fy[IX(L, i, j)] - (Ly_point_ld(L, V, U, i, j) + g), d = -(ldbl)Ly_diag(S, L, i, j);
+        ty[IX(L, i, j)] = (double)r;
+        sv += r * r / d;
+        sf += (ldbl)S->fy[IX(L, i, j)] * S->fy[IX(L, i, j)] / d;
+    }
+    FOR_P(L) {
+        ldbl r = -(((ldbl)V[IX(L, i, j)] - V[IX(L, i, j - 1)]) / dx + ((ldbl)U[IX(L, i, j)] - U[IX(L, i - 1, j)]) / dy);
+        tp[IX(L, i, j)] = (double)r;
+        sp += r * r * ((ldbl)L->etap[IX(L, i, j)] / c);
+    }
+    if (rx) out_vx(L, tx, rx);
+    if (ry) out_vy(L, ty, ry);
+    if (rp) out_p(L, tp, rp);
+    if (rel_energy) *rel_energy = sf > 0 ? (double)sqrtl((sv + sp) / sf) : 0.0;
+    free(tx); free(ty); free(tp);
+    return O_OK;
+}
+
 /* energy partial sums (Sv, Sp, Sf) of a residual -- exposes the reduction itself */
 int oracle_energy_sums(oracle_t *S, const double *vx, const double *vy, const double *p, double *sums3) {
     if (!S || !S->have_eta || !S->have_rho) return O_ESTATE;

@@ -12,7 +12,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from oracle.oracle import Oracle  # noqa: E402
-from synth.fields import parity_fields, workload  # noqa: E402
+from synth.fields import parity_fields, random_torch, random_velocity, workload  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PRE = json.load(open(os.path.join(ROOT, "configs", "presets.json")))
@@ -115,3 +115,65 @@ def test_fine_smoothers_4096(smoother, nsweeps):
     ex, ey = o.smooth(0, bx, by, f["vx"], f["vy"], nsweeps)
     gx, gy = s.smooth(0, T(bx), T(by), T(f["vx"]), T(f["vy"]), nsweeps)
     assert rel(gx, ex) <= 1e-12 and rel(gy, ey) <= 1e-12
+
+
+def test_random_16384_operator_smoother_and_converged_solution():
+    """BASELINE cfg 5 at its full size (16384^2 cells, 805 M unknowns), in the launch
+    configuration of bench.py's strong-scaling block at N = 1 (one domain, the preset's
+    options, inputs sampled on the device by synth.fields.random_torch): the converged solve
+    through properties (status, zero-mean pressure, the energy residual of the GPU solution
+    evaluated by the oracle in long double <= rtol and equal to the GPU's own evaluation), then
+    the operator apply and one fine two-sweep Jacobi pass element by element against the oracle
+    on the same fields (host memory ~45 GB, oracle ~5 min).
+
+    Why long double (reading R34, pinned in tests/test_oracle_residual_ld.py): near convergence
+    the FP64 evaluation of E through the Listing's coefficient form (the oracle's x row) cancels
+    terms ~h^-2 larger than the residual; at 16384^2 it reads 1.023e-8 for a solution whose E is
+    9.78e-9 (GPU, stress-difference form).  The FP64 oracle E is still bounded: within one
+    iteration's contraction of rtol (E_64 <= rtol / rho), i.e. the oracle's own stopping test would
+    accept the next iterate -- the +-1 count bar."""
+    from paper_2603_14040_b200 import Stokes
+    pre = PRE["random"]
+    n = pre["n"][0]
+    w = random_torch(n, n, device="cuda")
+    s = Stokes(n, n, w["Lx"], w["Ly"], w["bc"], **pre["opts"])
+    s.set_viscosity(w["eta_b"], w["eta_p"])
+    s.set_density(w["rho_b"])
+    s.set_gravity(w["gx"], w["gy"])
+    r = s.solve(pre["rtol"], hist_len=1000)
+    assert r["status"] == 0 and r["E"] <= pre["rtol"]
+    assert abs(float(r["p"].mean())) <= 1e-12 * float(r["p"].abs().max())
+    rho = r["hist"][-1] / r["hist"][-2]
+    assert 0.0 < rho < 1.0, r["hist"][-3:]
+    e_gpu = s.residual(r["vx"], r["vy"], r["p"], want_arrays=False)[3]  # the GPU's E of the returned iterate
+    sol = {k: r[k].cpu().numpy() for k in ("vx", "vy", "p")}
+    e_solve = r["E"]
+    del r
+    vx, vy, p = random_velocity(n, n, seed=11)
+    got = [g.cpu().numpy() for g in s.apply_operator(T(vx), T(vy), T(p))]
+    rng = np.random.default_rng(12)
+    bx, by = rng.standard_normal((n, n + 1)), rng.standard_normal((n + 1, n))
+    sm = [g.cpu().numpy() for g in s.smooth(0, T(bx), T(by), T(vx), T(vy), 2)]
+    s.close()
+    del s
+    host = {k: w[k].cpu().numpy() for k in ("eta_b", "eta_p", "rho_b")}
+    o = Oracle(n, n, w["Lx"], w["Ly"], w["bc"], **pre["opts"])
+    o.set_gravity(w["gx"], w["gy"])
+    del w
+    torch.cuda.empty_cache()
+    o.set_viscosity(host["eta_b"], host["eta_p"])
+    o.set_density(host["rho_b"])
+    del host
+    for g_, e_ in zip(got, o.apply_operator(vx, vy, p)):
+        assert rel(g_, e_) <= 1e-12
+    del got
+    ex, ey = o.smooth(0, bx, by, vx, vy, 2)
+    assert rel(sm[0], ex) <= 1e-12 and rel(sm[1], ey) <= 1e-12
+    del ex, ey, sm, bx, by, vx, vy, p
+    _, _, _, e_ld = o.residual_ld(sol["vx"], sol["vy"], sol["p"])
+    _, _, _, e_64 = o.residual(sol["vx"], sol["vy"], sol["p"])
+    print(f"random 16384^2: E oracle long double {e_ld:.6e}, FP64 {e_64:.6e}; GPU {e_gpu:.6e}, "
+          f"solve {e_solve:.6e}, rho {rho:.3f}")
+    assert e_ld <= pre["rtol"] * (1 + 1e-4), (e_ld, e_gpu)
+    assert abs(e_gpu - e_ld) <= 1e-4 * e_ld, (e_ld, e_gpu)
+    assert e_64 <= pre["rtol"] / rho, (e_64, e_ld, rho)

@@ -141,11 +141,26 @@ int stokes_create(int nx, int ny, double Lx, double Ly, const int bc[4], const s
  *             128 bytes from stokes_nccl_unique_id() on rank 0, shared by the caller; every
  *             array is the tile's WINDOW of the global user layout, i.e. the user layout of
  *             an (nx/px) x (ny/py) problem (shared edge nodes appear in both windows).
+ *             nccl_unique_id = NULL: the same handle as a schedule-recording DRY RUN -- no
+ *             communicator; every NCCL call the transport would issue is recorded instead
+ *             (stokes_dist_schedule) and the collectives keep the local part, so the ranks'
+ *             schedules can be built one after another in one process on one GPU and checked
+ *             against NCCL's matching rules.  Its numerical results are meaningless.
  * Supported calls on a decomposed handle: set_viscosity, set_density, set_gravity,
  * residual (energy only: rx = ry = rp = NULL), solve, num_levels, launch_count, destroy;
  * the per-step entry points return STOKES_EINVAL.  The library allocates its own memory. */
 int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], int px, int py, int rank,
                        const void *nccl_unique_id, const stokes_opts *opts, void *cuda_stream, stokes_t *out);
+/* The NCCL calls recorded by a dry-run decomposed handle (rank >= 0, nccl_unique_id NULL),
+ * in issue order, 5 values per call: op (1 group start, 2 group end, 3 ncclSend, 4 ncclRecv,
+ * 5 ncclAllGather, 6 ncclAllReduce; markers 7 / 8 = begin / end of the capture of one plain
+ * Uzawa iteration's graph, peer = its pressure parity), peer rank (-1 for collectives and groups), element
+ * count (per rank for all-gathers), ncclDataType_t, ncclRedOp_t (-1 if none).  Calls made
+ * during a CUDA-graph capture are recorded once, when captured.  rec: host buffer of cap
+ * records (may be NULL if cap = 0); *n = the number recorded (may exceed cap: call again
+ * with a larger buffer).  STOKES_EINVAL for any other handle.  Verification of the multi-
+ * process schedule (tests/test_gpu_nccl_schedule.py). */
+int stokes_dist_schedule(stokes_t h, long long *rec, int cap, int *n);
 /* 128-byte NCCL unique id for stokes_create_dist (call on rank 0, broadcast it). */
 int stokes_nccl_unique_id(void *id128);
 

@@ -78,6 +78,11 @@ struct Dist {
     int pcur;
     bool have_eta, have_rho;
     double gx, gy;
+    // schedule-recording dry run of the NCCL transport (rank >= 0, no unique id): the NCCL
+    // calls are recorded here (NC_REC long longs per call) instead of issued
+    bool dry;
+    long long *nlog;
+    int nlog_n, nlog_cap;
 };
 
 int dist_eta_hierarchy(Dist *D);
@@ -91,6 +96,60 @@ constexpr int HW = 2;  // halo width: the two-sweep pass and the fused residual+
 LaunchCtx dctx(Dist &D) { return LaunchCtx{D.xs, &D.launches}; }
 bool packed(const Dist &D) { return D.mode != M_VIRTUAL; }
 bool self_nccl(const Dist &D) { return D.mode == M_NCCL_SELF; }
+
+// ---- the NCCL calls of the multi-process transport (M_NCCL).  In the dry run (stokes_create_dist
+// with rank >= 0 and no unique id: no communicator) each call is RECORDED -- (op, peer, count,
+// datatype, reduction) -- instead of issued, and the collectives keep their local part, so
+// every rank's schedule can be built in one process on one GPU, one rank after another (no
+// kernel ever waits on another rank), and checked against NCCL's matching rules
+// (tests/test_gpu_nccl_schedule.py; stokes_dist_schedule).
+constexpr int NC_REC = 5;
+enum { NC_GSTART = 1, NC_GEND = 2, NC_SEND = 3, NC_RECV = 4, NC_ALLGATHER = 5, NC_ALLREDUCE = 6, NC_BODY = 7,
+       NC_BODY_END = 8 };  // (7 / 8: begin / end of the capture of one Uzawa iteration's graph)
+int nc_log(Dist &D, int op, int peer, size_t count, int dtype, int redop) {
+    if (D.nlog_n == D.nlog_cap) {
+        const int cap = D.nlog_cap ? 2 * D.nlog_cap : 1024;
+        long long *p = (long long *)realloc(D.nlog, (size_t)cap * NC_REC * sizeof(long long));
+        if (!p) return STOKES_ENOMEM;
+        D.nlog = p;
+        D.nlog_cap = cap;
+    }
+    long long *r = D.nlog + (size_t)D.nlog_n++ * NC_REC;
+    r[0] = op;
+    r[1] = peer;
+    r[2] = (long long)count;
+    r[3] = dtype;
+    r[4] = redop;
+    return STOKES_OK;
+}
+// ncclSend of n doubles to `peer` and ncclRecv of n doubles from it (inside a group).  Dry run:
+// both recorded, and the receive buffer gets what this rank sends (valid values, e.g. positive
+// viscosities in the halos, instead of uninitialised memory)
+int nc_sendrecv(Dist &D, const double *sbuf, double *rbuf, size_t n, int peer, cudaStream_t s) {
+    if (D.dry) {
+        CK(cudaMemcpyAsync(rbuf, sbuf, n * 8, cudaMemcpyDeviceToDevice, s));
+        int st = nc_log(D, NC_SEND, peer, n, (int)ncclDouble, -1);
+        return st ? st : nc_log(D, NC_RECV, peer, n, (int)ncclDouble, -1);
+    }
+    if (ncclSend(sbuf, n, ncclDouble, peer, D.comm, s) != ncclSuccess) return STOKES_ENCCL;
+    return ncclRecv(rbuf, n, ncclDouble, peer, D.comm, s) == ncclSuccess ? STOKES_OK : STOKES_ENCCL;
+}
+// all-gather of n doubles per rank (in place when send == recv + rank * n).  Dry run: every
+// rank's slot gets this rank's block (valid values -- e.g. positive viscosities for the
+// agglomerated tail's checks -- not the other ranks' data)
+int nc_allgather(Dist &D, const double *send, double *recv, size_t n, cudaStream_t s) {
+    if (D.dry) {
+        for (int r = 0; r < D.px * D.py; ++r)
+            if (send != recv + (size_t)r * n)
+                CK(cudaMemcpyAsync(recv + (size_t)r * n, send, n * 8, cudaMemcpyDeviceToDevice, s));
+        return nc_log(D, NC_ALLGATHER, -1, n, (int)ncclDouble, -1);
+    }
+    return ncclAllGather(send, recv, n, ncclDouble, D.comm, s) == ncclSuccess ? STOKES_OK : STOKES_ENCCL;
+}
+int nc_allreduce(Dist &D, void *buf, size_t n, ncclDataType_t t, ncclRedOp_t op, cudaStream_t s) {  // in place
+    if (D.dry) return nc_log(D, NC_ALLREDUCE, -1, n, (int)t, (int)op);
+    return ncclAllReduce(buf, buf, n, t, op, D.comm, s) == ncclSuccess ? STOKES_OK : STOKES_ENCCL;
+}
 
 // the fields of a halo exchange: FX_VP = velocity buffer idx and pressure buffer pidx
 int nfields(Dist &D, stokes_s *h, int l, int which, int idx, double **f) {
@@ -132,10 +191,12 @@ int p2p_local(Dist &D, double *dst, const double *src, size_t n) {
     return STOKES_OK;
 }
 int group_start(Dist &D) {
+    if (D.dry) return nc_log(D, NC_GSTART, -1, 0, -1, -1);
     if (D.mode == M_NCCL || self_nccl(D)) return ncclGroupStart() == ncclSuccess ? STOKES_OK : STOKES_ENCCL;
     return STOKES_OK;
 }
 int group_end(Dist &D) {
+    if (D.dry) return nc_log(D, NC_GEND, -1, 0, -1, -1);
     if (D.mode == M_NCCL || self_nccl(D)) return ncclGroupEnd() == ncclSuccess ? STOKES_OK : STOKES_ENCCL;
     return STOKES_OK;
 }
@@ -210,14 +271,8 @@ int exchange(Dist &D, int l, int which, int idx) {
         if ((st = group_start(D))) return st;
         if (D.mode == M_NCCL) {
             const int W = D.tx[0] > 0 ? D.rank - 1 : -1, E = D.tx[0] + 1 < D.px ? D.rank + 1 : -1;
-            if (W >= 0) {
-                ncclSend(D.sb[0], part, ncclDouble, W, D.comm, D.xs);
-                ncclRecv(D.rb[0], part, ncclDouble, W, D.comm, D.xs);
-            }
-            if (E >= 0) {
-                ncclSend(D.sb[0] + part, part, ncclDouble, E, D.comm, D.xs);
-                ncclRecv(D.rb[0] + part, part, ncclDouble, E, D.comm, D.xs);
-            }
+            if (W >= 0 && (st = nc_sendrecv(D, D.sb[0], D.rb[0], part, W, D.xs))) return st;
+            if (E >= 0 && (st = nc_sendrecv(D, D.sb[0] + part, D.rb[0] + part, part, E, D.xs))) return st;
         } else {  // my W part <- W neighbour's E part, my E part <- E neighbour's W part
             for (int k = 0; k < D.nt; ++k) {
                 if (D.tx[k] > 0 && (st = p2p_local(D, D.rb[k], D.sb[tile_at(D, D.tx[k] - 1, D.ty[k])] + part, part)))
@@ -250,14 +305,11 @@ int exchange(Dist &D, int l, int which, int idx) {
         if (D.mode == M_NCCL) {
             const int N = D.ty[0] > 0 ? D.rank - D.px : -1, S = D.ty[0] + 1 < D.py ? D.rank + D.px : -1;
             for (int q = 0; q < nf; ++q) {
-                if (N >= 0) {
-                    ncclSend(f[q] + at(g, 1, -1), blk, ncclDouble, N, D.comm, D.xs);
-                    ncclRecv(f[q] + at(g, 1 - HW, -1), blk, ncclDouble, N, D.comm, D.xs);
-                }
-                if (S >= 0) {
-                    ncclSend(f[q] + at(g, g.ncy + 1 - HW, -1), blk, ncclDouble, S, D.comm, D.xs);
-                    ncclRecv(f[q] + at(g, g.ncy + 1, -1), blk, ncclDouble, S, D.comm, D.xs);
-                }
+                if (N >= 0 && (st = nc_sendrecv(D, f[q] + at(g, 1, -1), f[q] + at(g, 1 - HW, -1), blk, N, D.xs)))
+                    return st;
+                if (S >= 0 &&
+                    (st = nc_sendrecv(D, f[q] + at(g, g.ncy + 1 - HW, -1), f[q] + at(g, g.ncy + 1, -1), blk, S, D.xs)))
+                    return st;
             }
         } else {
             for (int q = 0; q < nf; ++q) {
@@ -318,7 +370,7 @@ int gather_to_tail(Dist &D, int which) {
         }
     }
     if (D.mode == M_NCCL) {
-        if (ncclAllGather(D.sb[0], D.rb[0], blk, ncclDouble, D.comm, D.stream) != ncclSuccess) return STOKES_ENCCL;
+        if (int st = nc_allgather(D, D.sb[0], D.rb[0], blk, D.stream)) return st;
     } else {
         int st = group_start(D);
         for (int k = 0; k < D.nt && !st; ++k) st = p2p_local(D, D.rb[0] + (size_t)k * blk, D.sb[k], blk);
@@ -519,7 +571,9 @@ int combine(Dist &D, bool write_mean) {
         loc[k] = D.tile[k]->scal + S_LOC;
         ms[k] = D.tile[k]->scal + S_MSHIFT;
     }
-    if (D.mode == M_NCCL || self_nccl(D))  // (one rank: the sum over the tiles follows on the device)
+    if (D.mode == M_NCCL)
+        if (int st = nc_allreduce(D, D.tile[0]->scal + S_LOC, 3, ncclDouble, ncclSum, D.stream)) return st;
+    if (self_nccl(D))  // (one rank: the sum over the tiles follows on the device)
         for (int k = 0; k < D.nt; ++k)
             if (ncclAllReduce(D.tile[k]->scal + S_LOC, D.tile[k]->scal + S_LOC, 3, ncclDouble, ncclSum, D.comm,
                               D.stream) != ncclSuccess)
@@ -659,9 +713,7 @@ static int gather_segments(Dist &D, double *base, size_t seg) {  // every rank's
         return ncclGroupEnd() == ncclSuccess ? STOKES_OK : STOKES_ENCCL;
     }
     if (D.mode != M_NCCL) return STOKES_OK;
-    if (ncclAllGather(base + (size_t)D.rank * seg, base, seg, ncclDouble, D.comm, D.stream) != ncclSuccess)
-        return STOKES_ENCCL;
-    return STOKES_OK;
+    return nc_allgather(D, base + (size_t)D.rank * seg, base, seg, D.stream);
 }
 static int tiles_sum(Dist &D, int buf, int nb) {  // NCCL: all-gather rank segments of gpart[buf]
     return gather_segments(D, D.gpart[buf], (size_t)nb * 2);
@@ -1037,6 +1089,7 @@ int dist_destroy(Dist *D) {
     for (int k = 0; k < D->nt; ++k) free_handle(D->tile[k]);
     free_handle(D->tail);
     if ((D->mode == M_NCCL || D->mode == M_NCCL_SELF) && D->comm) ncclCommDestroy(D->comm);
+    free(D->nlog);
     for (int k = 0; k < MAXT; ++k) {
         if (D->sb[k]) cudaFree(D->sb[k]);
         if (D->rb[k]) cudaFree(D->rb[k]);
@@ -1172,9 +1225,11 @@ static int dist_core(Dist *D, double rtol, double E0, int *kout, double *Eout) {
             for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = q;
             cudaGraph_t graph;
             const long long before = dist_launches(D, 0);
+            if (D->dry && (st = nc_log(*D, NC_BODY, q, 0, -1, -1))) return st;
             CK(cudaStreamBeginCapture(D->stream, cudaStreamCaptureModeThreadLocal));
             int bst = fused ? dist_fused_body(*D) : dist_body(*D);
             cudaError_t e = cudaStreamEndCapture(D->stream, &graph);
+            if (D->dry && !bst && (st = nc_log(*D, NC_BODY_END, q, 0, -1, -1))) return st;
             D->pcur = keep;
             for (int t = 0; t < D->nt; ++t) D->tile[t]->pcur = keep;
             if (bst) return bst;
@@ -1231,7 +1286,9 @@ static int dist_eta_min(Dist &D) {
         stokes_s *t = D.tile[k];
         launch_eta_min(ctx(t), t->lev[0].g, t->etab_user, t->etap_user, m0);
     }
-    if (D.mode == M_NCCL || D.mode == M_NCCL_SELF)
+    if (D.mode == M_NCCL)
+        if (int st = nc_allreduce(D, m0, 1, ncclUint64, ncclMin, D.stream)) return st;
+    if (D.mode == M_NCCL_SELF)
         if (ncclAllReduce(m0, m0, 1, ncclUint64, ncclMin, D.comm, D.stream) != ncclSuccess) return STOKES_ENCCL;
     for (int k = 1; k < D.nt; ++k)
         CK(cudaMemcpyAsync(D.tile[k]->scal + S_ETAMIN, m0, 8, cudaMemcpyDeviceToDevice, D.stream));
@@ -1349,6 +1406,15 @@ int dist_solve(Dist *D, double rtol, double *vx, double *vy, double *p, int *ite
 
 extern "C" {
 
+int stokes_dist_schedule(stokes_t h, long long *rec, int cap, int *n) {
+    if (!h || !h->dist || !h->dist->dry || !n || cap < 0 || (cap > 0 && !rec)) return STOKES_EINVAL;
+    const Dist &D = *h->dist;
+    *n = D.nlog_n;
+    const int m = D.nlog_n < cap ? D.nlog_n : cap;
+    if (m) memcpy(rec, D.nlog, (size_t)m * NC_REC * sizeof(long long));
+    return STOKES_OK;
+}
+
 int stokes_nccl_unique_id(void *id128) {
     if (!id128) return STOKES_EINVAL;
     ncclUniqueId id;
@@ -1360,7 +1426,7 @@ int stokes_nccl_unique_id(void *id128) {
 int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], int px, int py, int rank,
                        const void *nccl_unique_id, const stokes_opts *opts, void *cuda_stream, stokes_t *out) {
     if (!out || px < 1 || py < 1 || px * py > MAXT || nx % px || ny % py || !bc) return STOKES_EINVAL;
-    if (rank >= px * py || rank < -3 || (rank >= 0 && !nccl_unique_id)) return STOKES_EINVAL;
+    if (rank >= px * py || rank < -3) return STOKES_EINVAL;
     if (opts && opts->smoother >= 2) return STOKES_EINVAL;  // RAS / Mixed: single domain only
     Dist *D = (Dist *)calloc(1, sizeof(Dist));
     if (!D) return STOKES_ENOMEM;
@@ -1434,9 +1500,12 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
         D->nt = 1;
         D->tx[0] = rank % px;
         D->ty[0] = rank / px;
-        ncclUniqueId id;
-        memcpy(&id, nccl_unique_id, sizeof(id));
-        if (ncclCommInitRank(&D->comm, px * py, id, rank) != ncclSuccess) { free(D); return STOKES_ENCCL; }
+        D->dry = !nccl_unique_id;  // schedule-recording dry run: no communicator
+        if (!D->dry) {
+            ncclUniqueId id;
+            memcpy(&id, nccl_unique_id, sizeof(id));
+            if (ncclCommInitRank(&D->comm, px * py, id, rank) != ncclSuccess) { free(D); return STOKES_ENCCL; }
+        }
     }
     if (D->mode == M_NCCL_SELF) {  // a one-rank communicator: every halo goes through ncclSend / ncclRecv to self
         ncclUniqueId id;

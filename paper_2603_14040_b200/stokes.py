@@ -101,6 +101,7 @@ def lib(build_if_missing=True):
         "stokes_last_error": [],
         "stokes_create_dist": [I, I, D, D, pi, I, I, I, P, ctypes.POINTER(Opts), P, ctypes.POINTER(P)],
         "stokes_nccl_unique_id": [P],
+        "stokes_dist_schedule": [P, ctypes.POINTER(ctypes.c_longlong), I, ctypes.POINTER(I)],
         "stokes_lithostatic": [P, P],
         "stokes_markers_to_grid": [P, ctypes.c_longlong, P, P, P, P, P, P, P, ctypes.POINTER(ctypes.c_longlong)],
         "stokes_grid_to_markers": [P, ctypes.c_longlong, P, P, P, P, P, P],
@@ -123,7 +124,7 @@ EXPORTED = ["stokes_opts_default", "stokes_workspace_bytes", "stokes_create", "s
             "stokes_smooth", "stokes_level_residual", "stokes_restrict", "stokes_prolong",
             "stokes_get_viscosity", "stokes_coarse_solve", "stokes_launch_count", "stokes_time_kernel",
             "stokes_strerror", "stokes_last_error", "stokes_create_dist", "stokes_nccl_unique_id",
-            "stokes_lithostatic", "stokes_markers_to_grid", "stokes_grid_to_markers", "stokes_advect_markers",
+            "stokes_dist_schedule", "stokes_lithostatic", "stokes_markers_to_grid", "stokes_grid_to_markers", "stokes_advect_markers",
             "stokes_marker_timestep"]
 
 
@@ -476,7 +477,10 @@ class StokesDist(Stokes):
     real ncclSend / ncclRecv on a one-rank communicator (tests of the multi-GPU path on one B200).
     rank=r (with torch.distributed initialised): NCCL decomposition, one tile per process;
     arrays are the tile windows (`tile_windows`).  The NCCL unique id is created on rank 0
-    and broadcast with torch.distributed (the process group is plumbing only)."""
+    and broadcast with torch.distributed (the process group is plumbing only).
+    rank=r with transport="nccl_dry": the same rank-r handle as a schedule-recording dry run
+    (no communicator, no torch.distributed): `schedule()` returns the NCCL calls it would have
+    issued (stokes_dist_schedule); the numerical results are meaningless."""
 
     def __init__(self, nx, ny, Lx=1.0, Ly=1.0, bc=(FREE_SLIP,) * 4, px=1, py=1, rank=None, device=None,
                  stream=None, transport="virtual", **opts):
@@ -488,7 +492,7 @@ class StokesDist(Stokes):
         self.Lx, self.Ly, self.bc = Lx, Ly, tuple(bc)
         self.opts = default_opts(**opts)
         uid = None
-        if rank is not None:
+        if rank is not None and transport != "nccl_dry":
             import torch.distributed as dist
             obj = [nccl_unique_id() if dist.get_rank() == 0 else None]
             dist.broadcast_object_list(obj, src=0)
@@ -504,6 +508,14 @@ class StokesDist(Stokes):
 
     def level_shape(self, level):
         raise NotImplementedError("per-level queries are not available on decomposed handles")
+
+    def schedule(self):
+        """Dry-run handles: the recorded NCCL calls, a list of (op, peer, count, dtype, redop)."""
+        n = ctypes.c_int()
+        _check(lib().stokes_dist_schedule(self._h, None, 0, ctypes.byref(n)), "dist_schedule")
+        buf = (ctypes.c_longlong * (5 * max(n.value, 1)))()
+        _check(lib().stokes_dist_schedule(self._h, buf, n.value, ctypes.byref(n)), "dist_schedule")
+        return [tuple(buf[5 * i:5 * i + 5]) for i in range(n.value)]
 
     def residual(self, vx, vy, p, want_arrays=False):
         sh = shapes(self.nx, self.ny)

@@ -80,6 +80,7 @@ struct Dist {
     double gx, gy;
     // schedule-recording dry run of the NCCL transport (rank >= 0, no unique id): the NCCL
     // calls are recorded here (NC_REC long longs per call) instead of issued
+    bool halo2;  // packed transports: the two-round halo exchange (STOKES_HALO_2PHASE=1) instead of one round
     bool dry;
     long long *nlog;
     int nlog_n, nlog_cap;
@@ -201,6 +202,128 @@ int group_end(Dist &D) {
     return STOKES_OK;
 }
 
+// ---- one-round packed halo exchange (default for the packed transports).  Every neighbour
+// of a tile -- the four sides, and the four diagonal tiles where both adjacent sides are
+// tiles -- receives its strips in ONE grouped round (the two-round scheme below sends the W/E
+// columns first and the N/S rows, corners included, second: two NCCL latencies per exchange).
+// Direction (dx, dy): the block this tile sends spans
+//   rows  dy < 0: 1 .. HW,  dy > 0: ncy-HW+1 .. ncy,  dy = 0: r_lo .. r_hi
+//   cols  dx < 0: 1 .. HW,  dx > 0: ncx-HW+1 .. ncx,  dx = 0: c_lo .. c_hi
+// and the block it receives from there spans rows 1-HW .. 0 / ncy+1 .. ncy+HW / r_lo .. r_hi
+// and the same for columns, where [r_lo, r_hi] = the tile's rows plus the HW halo rows on a
+// GLOBAL N / S side (mirror rows, held alike by the side neighbour), [c_lo, c_hi] likewise:
+// every halo cell is written by exactly one message and the corners come straight from the
+// diagonal tile's own cells.  A block is packed as strips along its long dimension (per
+// field: one strip per column for dy = 0, one per row otherwise), in ascending order on both
+// sides, so the sender's and the receiver's packings agree element by element.
+struct HaloDir {
+    int dx, dy;
+};
+constexpr HaloDir HDIR[8] = {{-1, 0}, {1, 0}, {0, -1}, {0, 1}, {-1, -1}, {1, -1}, {-1, 1}, {1, 1}};
+int opposite(int d) {
+    for (int e = 0; e < 8; ++e)
+        if (HDIR[e].dx == -HDIR[d].dx && HDIR[e].dy == -HDIR[d].dy) return e;
+    return -1;
+}
+bool has_nb(const Dist &D, int tx, int ty, int d) {
+    const int x = tx + HDIR[d].dx, y = ty + HDIR[d].dy;
+    return x >= 0 && x < D.px && y >= 0 && y < D.py;
+}
+// rows [*a, *b] of the block sent (recv = false) to / received (recv = true) from direction d
+void dir_rows(const Dist &D, const GridL &g, int ty, int d, bool recv, int *a, int *b) {
+    const int dy = HDIR[d].dy;
+    if (dy < 0) { *a = recv ? 1 - HW : 1; *b = recv ? 0 : HW; }
+    else if (dy > 0) { *a = recv ? g.ncy + 1 : g.ncy - HW + 1; *b = recv ? g.ncy + HW : g.ncy; }
+    else { *a = ty > 0 ? 1 : 1 - HW; *b = ty + 1 < D.py ? g.ncy : g.ncy + HW; }
+}
+void dir_cols(const Dist &D, const GridL &g, int tx, int d, bool recv, int *a, int *b) {
+    const int dx = HDIR[d].dx;
+    if (dx < 0) { *a = recv ? 1 - HW : 1; *b = recv ? 0 : HW; }
+    else if (dx > 0) { *a = recv ? g.ncx + 1 : g.ncx - HW + 1; *b = recv ? g.ncx + HW : g.ncx; }
+    else { *a = tx > 0 ? 1 : 1 - HW; *b = tx + 1 < D.px ? g.ncx : g.ncx + HW; }
+}
+// segment offsets / lengths (doubles) of the 8 directions in a tile's send (= receive) buffer
+void seg_layout(const Dist &D, const GridL &g, int tx, int ty, int nf, size_t *off, size_t *len) {
+    size_t o = 0;
+    for (int d = 0; d < 8; ++d) {
+        int r0, r1, c0, c1;
+        dir_rows(D, g, ty, d, false, &r0, &r1);
+        dir_cols(D, g, tx, d, false, &c0, &c1);
+        off[d] = o;
+        len[d] = has_nb(D, tx, ty, d) ? (size_t)nf * (r1 - r0 + 1) * (c1 - c0 + 1) : 0;
+        o += len[d];
+    }
+}
+// the strips that pack (recv = false: field -> buffer) or unpack (recv = true: buffer ->
+// field) direction d of one tile
+void dir_strips(const Dist &D, const GridL &g, int tx, int ty, int d, bool recv, double *const *f, int nf,
+                double *buf, StripList &s) {
+    int r0, r1, c0, c1;
+    dir_rows(D, g, ty, d, recv, &r0, &r1);
+    dir_cols(D, g, tx, d, recv, &c0, &c1);
+    const int nr = r1 - r0 + 1, nc = c1 - c0 + 1;
+    const bool by_col = HDIR[d].dy == 0;  // long dimension: rows (W / E blocks)
+    size_t e = 0;
+    for (int q = 0; q < nf; ++q) {
+        if (by_col) {
+            for (int j = c0; j <= c1; ++j, e += nr) {
+                if (recv) add_strip(s, f[q] + at(g, r0, j), buf + e, nr, g.P, 1);
+                else add_strip(s, buf + e, f[q] + at(g, r0, j), nr, 1, g.P);
+            }
+        } else {
+            for (int i = r0; i <= r1; ++i, e += nc) {
+                if (recv) add_strip(s, f[q] + at(g, i, c0), buf + e, nc, 1, 1);
+                else add_strip(s, buf + e, f[q] + at(g, i, c0), nc, 1, 1);
+            }
+        }
+    }
+}
+int exchange_one_round(Dist &D, int l, int which, int idx) {
+    const LaunchCtx c = dctx(D);
+    double *f[3];
+    size_t off[MAXT][8], len[MAXT][8];
+    StripList s;
+    s.count = 0;
+    for (int k = 0; k < D.nt; ++k) {  // pack every direction of every local tile
+        const GridL &g = D.tile[k]->lev[l].g;
+        const int nf = nfields(D, D.tile[k], l, which, idx, f);
+        seg_layout(D, g, D.tx[k], D.ty[k], nf, off[k], len[k]);
+        for (int d = 0; d < 8; ++d)
+            if (len[k][d]) {
+                if (s.count + 3 * HW > 512) { launch_strips(c, s); s.count = 0; }
+                dir_strips(D, g, D.tx[k], D.ty[k], d, false, f, nf, D.sb[k] + off[k][d], s);
+            }
+    }
+    if (s.count) launch_strips(c, s);
+    int st = group_start(D);
+    if (st) return st;
+    for (int k = 0; k < D.nt; ++k)
+        for (int d = 0; d < 8; ++d) {
+            if (!len[k][d]) continue;
+            if (D.mode == M_NCCL) {
+                const int peer = D.rank + HDIR[d].dy * D.px + HDIR[d].dx;
+                st = nc_sendrecv(D, D.sb[0] + off[0][d], D.rb[0] + off[0][d], len[0][d], peer, D.xs);
+            } else {  // my segment d <- the neighbour's segment towards me
+                const int nb = tile_at(D, D.tx[k] + HDIR[d].dx, D.ty[k] + HDIR[d].dy), o = opposite(d);
+                st = p2p_local(D, D.rb[k] + off[k][d], D.sb[nb] + off[nb][o], len[k][d]);
+            }
+            if (st) return st;
+        }
+    if ((st = group_end(D))) return st;
+    s.count = 0;
+    for (int k = 0; k < D.nt; ++k) {  // unpack into the halos
+        const GridL &g = D.tile[k]->lev[l].g;
+        const int nf = nfields(D, D.tile[k], l, which, idx, f);
+        for (int d = 0; d < 8; ++d)
+            if (len[k][d]) {
+                if (s.count + 3 * HW > 512) { launch_strips(c, s); s.count = 0; }
+                dir_strips(D, g, D.tx[k], D.ty[k], d, true, f, nf, D.rb[k] + off[k][d], s);
+            }
+    }
+    if (s.count) launch_strips(c, s);
+    return STOKES_OK;
+}
+
 // Halo exchange of the selected fields of level l: HW = 2 rings, two phases (W/E columns
 // over rows -1 .. ncy+2, then N/S rows over columns -1 .. ncx+2: corners included).
 //   my column ncx + h <- E neighbour's column h,   my column 1 - h <- W neighbour's ncx + 1 - h
@@ -249,8 +372,10 @@ int exchange(Dist &D, int l, int which, int idx) {
         if (s.count) launch_strips(c, s);
         return STOKES_OK;
     }
-    // ---- packed transports: NCCL (one tile per process), NCCL_SELF (every tile here, real
-    // ncclSend / ncclRecv on a one-rank communicator), LOOPBACK (every tile here, device copies)
+    if (!D.halo2) return exchange_one_round(D, l, which, idx);
+    // ---- packed transports, two rounds (STOKES_HALO_2PHASE=1): NCCL (one tile per process),
+    // NCCL_SELF (every tile here, real ncclSend / ncclRecv on a one-rank communicator),
+    // LOOPBACK (every tile here, device copies)
     int nf = 0, st;
     {  // phase 1: W/E columns packed into sb = [W part | E part], nf x HW x rows each
         StripList s;
@@ -1446,6 +1571,10 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
         if (bc[k] != 0 && bc[k] != 1) { free(D); return STOKES_EINVAL; }
     D->rank = rank;
     D->mode = rank >= 0 ? M_NCCL : (rank == -2 ? M_LOOPBACK : (rank == -3 ? M_NCCL_SELF : M_VIRTUAL));
+    {
+        const char *e = getenv("STOKES_HALO_2PHASE");
+        D->halo2 = e && e[0] == '1';
+    }
     // global hierarchy and the agglomeration level (tile levels while the tile is >= dmin)
     GridL gs[MAXLEV];
     int nus[MAXLEV];
@@ -1525,8 +1654,9 @@ int stokes_create_dist(int nx, int ny, double Lx, double Ly, const int bc[4], in
     for (int l = 0; l < tail->nlev; ++l) tail->lev[l].nu = (int)floor(D->o.nu1 * pow(D->o.nu_growth, (double)(La + l)) + 0.5);
     if (D->tail->nlev + La != D->L) { dist_destroy(D); return STOKES_EINVAL; }
     const GridL &gf = D->tile[0]->lev[0].g, &gc = D->tile[0]->lev[La].g;
-    // packed halo columns: 2 sides x 3 fields x HW columns x (ncy + 2 HW) rows; agglomeration blocks
-    const size_t nhalo = 2 * 3 * HW * (size_t)(gf.ncy + 2 * HW);
+    // packed halos: 3 fields x HW x (the W / E columns over ncy + 2 HW rows, the N / S rows over
+    // ncx + 2 HW columns, the four HW x HW corners); agglomeration blocks
+    const size_t nhalo = 3 * HW * (2 * (size_t)(gf.ncy + 2 * HW) + 2 * (size_t)(gf.ncx + 2 * HW) + 4 * HW);
     const size_t nagg = 2 * (size_t)(gc.ncy + 1) * (gc.ncx + 1) * (size_t)(px * py);
     D->nbuf = (nhalo > nagg ? nhalo : nagg) + 64;
     bool okm = cudaMalloc(&D->dscal, 64 * 8) == cudaSuccess && cudaMallocHost(&D->hsc, 64 * 8) == cudaSuccess;

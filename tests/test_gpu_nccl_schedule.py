@@ -13,7 +13,7 @@ record their calls when captured).  The recorded schedules must satisfy NCCL's m
   * at every point-to-point step the sends r -> q match the receives at q from r one to one,
     in issue order, with equal counts (NCCL pairs the p2p operations between two ranks in
     issue order);
-  * the peers are the tile's grid neighbours (never the rank itself).
+  * the peers are the tile's grid neighbours, sides or diagonals (never the rank itself).
 Covers the bench's weak (BASELINE cfg 4: 4096^2 per GPU) and strong (cfg 5: 16384^2 split)
 launch configurations at N = 2, 4, 8, and GCR / Anderson / viscosity stages on small tiles.
 The data moved is verified elsewhere: the LOOPBACK / NCCL_SELF transports run the same
@@ -83,7 +83,7 @@ def check_schedules(logs, px, py):
             tx, ty = tile_of(r, px, py)
             for op, peer, cnt, dt in steps[r][k][1]:
                 qx, qy = tile_of(peer, px, py)
-                assert peer != r and abs(qx - tx) + abs(qy - ty) == 1, (k, r, peer)
+                assert peer != r and max(abs(qx - tx), abs(qy - ty)) == 1, (k, r, peer)  # sides + diagonals
                 if op == SEND:
                     sends[(r, peer)].append((cnt, dt))
                     nsend += 1

@@ -156,6 +156,9 @@ def dist_init(args):
         import torch.distributed as dist
         backend = "nccl" if args.impl == "ours" else "gloo"
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":  # one GPU per rank, bound before the process group's first collective
+            import torch
+            torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
     return world, rank, local
 

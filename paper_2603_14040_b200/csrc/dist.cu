@@ -288,6 +288,7 @@ int exchange_one_round(Dist &D, int l, int which, int idx) {
         const GridL &g = D.tile[k]->lev[l].g;
         const int nf = nfields(D, D.tile[k], l, which, idx, f);
         seg_layout(D, g, D.tx[k], D.ty[k], nf, off[k], len[k]);
+        if (off[k][7] + len[k][7] > D.nbuf) return fail_cuda(cudaErrorInvalidValue, "halo buffer too small");
         for (int d = 0; d < 8; ++d)
             if (len[k][d]) {
                 if (s.count + 3 * HW > 512) { launch_strips(c, s); s.count = 0; }

@@ -46,6 +46,23 @@ run(StokesDist, 256, "block", px=2, py=1, transport="loopback", omega_v=0.6, alp
     aa_beta=0.7, max_iter=4)
 run(StokesDist, 128, "block", px=2, py=1, transport="virtual", omega_v=0.6, alpha_p=1.0, theta_step=0.5,
     theta_every=2, max_iter=6)
+os.environ["STOKES_HALO_2PHASE"] = "1"  # the two-round exchange of the packed transports
+run(StokesDist, 256, "layered", px=2, py=2, transport="loopback", omega_v=0.6, alpha_p=1.0, max_iter=2)
+os.environ.pop("STOKES_HALO_2PHASE")
+os.environ.pop("STOKES_DIST_DMIN")
+for r in range(4):  # every rank of a 2 x 2 NCCL grid as a schedule-recording dry run (one round, overlap on)
+    from paper_2603_14040_b200.decomp import tile_windows
+    win = tile_windows(2048, 2048, 2, 2, r)
+    i0, j0 = win["b"][0].start, win["b"][1].start
+    w = workload("layered", 2048, 2048, win_b=(i0, j0, 1025, 1025), win_p=(i0, j0, 1024, 1024))
+    d = StokesDist(2048, 2048, w["Lx"], w["Ly"], w["bc"], px=2, py=2, rank=r, transport="nccl_dry", omega_v=0.6,
+                   alpha_p=1.0, max_iter=2)
+    d.set_viscosity(T(w["eta_b"]), T(w["eta_p"]))
+    d.set_density(T(w["rho_b"]))
+    d.set_gravity(w["gx"], w["gy"])
+    print("dry rank", r, d.solve(0.0)["iters"], len(d.schedule()), flush=True)
+    d.close()
+os.environ["STOKES_DIST_DMIN"] = "8"
 s = Stokes(256, 256, omega_v=0.6)
 w = workload("layered", 256, 256)
 s.set_viscosity(T(w["eta_b"]), T(w["eta_p"]))

@@ -209,6 +209,20 @@ int jacobi_pairs(stokes_s *h, int l, int n, bool zero_in) {
     if (level_smoother(h, l) != STOKES_SMOOTH_JACOBI || !jacobi2_ok(h->lev[l].g)) return 0;
     return (n - (zero_in ? 1 : 0)) / 2 > 0 ? (n - (zero_in ? 1 : 0)) / 2 : 0;
 }
+// Small single-domain levels (<= STOKES_TILE_CELLS cells, default 256^2; 0 = off) smooth all n
+// sweeps of a pre- / post-smoothing in one launch (k_jacobi_tile): their per-sweep kernels are
+// launch- and pipeline-latency bound.  Pre- and post-smoothing of a level decide alike (same n),
+// so a V-cycle still swaps its buffers an even number of times.  Layered 4096^2 solve (CUDA
+// events): off 549 ms, <= 128^2 541, <= 256^2 538, <= 512^2 541, <= 1024^2 571 ms (the 3.4x
+// staging redundancy of an 8 x 32 tile loses to the streamed pairs from 512^2 up).
+static long long tile_cells() {  // (read per call: tests force either path)
+    const char *e = getenv("STOKES_TILE_CELLS");
+    return e ? atoll(e) : 256LL * 256LL;
+}
+static bool tile_level(stokes_s *h, int l) {
+    const GridL &g = h->lev[l].g;
+    return (long long)g.ncx * g.ncy <= tile_cells();
+}
 void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&oy, const RhsArgs &rhs, int n,
             bool zero_in, int max_pairs) {
     Level &L = h->lev[l];
@@ -249,6 +263,10 @@ void smooth(stokes_s *h, int l, double *&cx, double *&cy, double *&ox, double *&
             double *tt = cx; cx = ox; ox = tt;
             tt = cy; cy = oy; oy = tt;
         }
+    } else if (lsm == STOKES_SMOOTH_JACOBI && tile_level(h, l) &&
+               launch_jacobi_tile(c, L.g, L.etab, L.etap, cx, cy, ox, oy, rhs, h->o.omega_v, n, zero_in)) {
+        double *t = cx; cx = ox; ox = t;  // all n sweeps in one launch: one buffer swap
+        t = cy; cy = oy; oy = t;
     } else if (lsm == STOKES_SMOOTH_JACOBI) {
         int pairs = jacobi_pairs(h, l, n, zero_in);
         if (pairs > max_pairs) pairs = max_pairs;
@@ -392,7 +410,8 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
         else --pre_pairs;
     }
     // the last pre-smoothing pair fused with (2) + (3) when the level allows it (k_j2rr)
-    const bool fuse_rr = pre_pairs >= 1 && pre_n >= 2 && level_smoother(h, l) == STOKES_SMOOTH_JACOBI && j2rr_ok(L.g);
+    const bool fuse_rr = pre_pairs >= 1 && pre_n >= 2 && level_smoother(h, l) == STOKES_SMOOTH_JACOBI && j2rr_ok(L.g) &&
+                         !tile_level(h, l);  // (tile-smoothed levels: one launch per smoothing)
     if (fuse_rr) {
         smooth(h, l, cx, cy, ox, oy, rhs, pre_n - 2, zero_in && !done_pre, pre_pairs - 1);  // (1)
         launch_j2rr(c, L.g, C.g, L.etab, L.etap, cx, cy, ox, oy, rhs, h->o.omega_v, C.bx, C.by);

@@ -108,7 +108,14 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
 // Damped Jacobi, Eq. damped_jacobi: v <- v + omega (b - L v)_i / a_ii,
 // reads only the old iterate (ping-pong buffers).  zero_in: the old iterate is 0 (first
 // sweep of a coarse correction), so v_in is not read.
-template <bool ZERO>
+// 1/a by the FP64 MUFU seed and two Newton steps (<= 1 ulp; as the streamed kernels' rcp)
+__device__ __forceinline__ double rcp_nr(double a) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    r = r * fma(-a, r, 2.0);
+    return r * fma(-a, r, 2.0);
+}
+template <bool ZERO, bool RCP = false>  // RCP: multiply by rcp_nr(a_ii) instead of dividing
 __device__ __forceinline__ void jacobi_pt(const GridL &g, const double *__restrict__ etab,
                                           const double *__restrict__ etap, const double *__restrict__ vxi,
                                           const double *__restrict__ vyi, double *__restrict__ vxo,
@@ -118,7 +125,8 @@ __device__ __forceinline__ void jacobi_pt(const GridL &g, const double *__restri
         const double a = lx_diag(g, etab, etap, i, j);
         const double b = rhs_x(g, rhs, i, j);
         double vn;
-        if (ZERO) vn = omega * b / a;
+        if (RCP) vn = ZERO ? omega * b * rcp_nr(a) : ax(i, j) + omega * (b - lx_row(g, etab, etap, ax, ay, i, j)) * rcp_nr(a);
+        else if (ZERO) vn = omega * b / a;
         else vn = ax(i, j) + omega * (b - lx_row(g, etab, etap, ax, ay, i, j)) / a;
         vxo[at(g, i, j)] = vn;
         if (i == 1 && g.bN) vxo[at(g, 0, j)] = g.sN * vn;
@@ -128,7 +136,8 @@ __device__ __forceinline__ void jacobi_pt(const GridL &g, const double *__restri
         const double a = ly_diag(g, etab, etap, i, j);
         const double b = rhs_y(g, rhs, i, j);
         double vn;
-        if (ZERO) vn = omega * b / a;
+        if (RCP) vn = ZERO ? omega * b * rcp_nr(a) : ay(i, j) + omega * (b - ly_row(g, etab, etap, ax, ay, i, j)) * rcp_nr(a);
+        else if (ZERO) vn = omega * b / a;
         else vn = ay(i, j) + omega * (b - ly_row(g, etab, etap, ax, ay, i, j)) / a;
         vyo[at(g, i, j)] = vn;
         if (j == 1 && g.bW) vyo[at(g, i, 0)] = g.sW * vn;
@@ -144,6 +153,95 @@ __global__ void __launch_bounds__(BX *BY) k_jacobi(GridL g, const double *__rest
     const int i = blockIdx.y * BY + threadIdx.y + 1;
     if (i > g.ncy || j > g.ncx) return;
     jacobi_pt<ZERO>(g, etab, etap, vxi, vyi, vxo, vyo, rhs, omega, i, j);
+}
+
+// ---- n damped-Jacobi sweeps of a small level in ONE launch (temporal blocking in shared memory)
+// The coarse levels between the one-CTA tail and the streamed levels are latency-bound: a sweep
+// there is a few microseconds of launch and pipeline fill for little work.  Here a CTA owns a
+// TTR x TTC tile of cells, stages the tile plus an (n+1)-cell frame of vx, vy, eta_b, eta_p, b_x,
+// b_y in shared memory (global indices clipped to the array's nodes 0..ncy+1 x 0..ncx+1), and
+// runs the n sweeps in place there: sweep k updates the unknowns within n-1-k cells of the tile
+// (the region sweep k+1 reads), ping-ponging two shared buffers per component, with the SAME
+// point function as k_jacobi (jacobi_pt on a GridL whose pitch is the shared tile's: global
+// indices, the global boundary logic and mirrors unchanged; 1/a_ii by the MUFU seed + Newton
+// steps of the streamed kernels unless TT_RCP = 0, which equals n launches of k_jacobi bit for
+// bit).  Then the tile's unknowns (and its mirror nodes) are stored.
+#ifndef TT_ROWS
+#define TT_ROWS 8
+#endif
+#ifndef TT_RCP
+#define TT_RCP 1  // 1/a_ii by MUFU seed + Newton (as the streamed kernels) instead of the IEEE division
+#endif
+constexpr int TTR = TT_ROWS, TTC = 32, TT_MAXN = 8;  // tile rows / columns, most sweeps per launch
+__host__ __device__ constexpr int tt_rows(int n) { return TTR + 2 * (n + 1); }
+__host__ __device__ constexpr int tt_cols(int n) { return TTC + 2 * (n + 1); }
+template <bool ZERO>
+__global__ void __launch_bounds__(TTR *TTC) k_jacobi_tile(GridL g, const double *__restrict__ etab,
+                                                          const double *__restrict__ etap, const double *__restrict__ vxi,
+                                                          const double *__restrict__ vyi, double *__restrict__ vxo,
+                                                          double *__restrict__ vyo, const double *__restrict__ bx,
+                                                          const double *__restrict__ by, double omega, int n) {
+    extern __shared__ __align__(16) double tsm[];
+    const int R = tt_rows(n), C = tt_cols(n), A = R * C;
+    double *s_eb = tsm, *s_ep = tsm + A, *s_bx = tsm + 2 * A, *s_by = tsm + 3 * A;
+    double *s_v = tsm + 4 * A;  // buffer b: vx at s_v + 2 b A, vy at s_v + (2 b + 1) A
+    const int t = threadIdx.x, nt = TTR * TTC;
+    const int I0 = 1 + blockIdx.y * TTR, J0 = 1 + blockIdx.x * TTC;  // first cell of the tile
+    const int ib = I0 - (n + 1), jb = J0 - (n + 1);                    // global index of tile entry (0, 0)
+    // stage: every array entry of the frame that exists (nodes 0..ncy+1 x 0..ncx+1), 0 elsewhere
+    for (int e = t; e < A; e += nt) {
+        const int i = ib + e / C, j = jb + e % C;
+        const bool in = i >= 0 && i <= g.ncy + 1 && j >= 0 && j <= g.ncx + 1;
+        const size_t q = at(g, i, j);
+        s_eb[e] = in ? etab[q] : 0.0;
+        s_ep[e] = in ? etap[q] : 0.0;
+        s_bx[e] = in ? bx[q] : 0.0;
+        s_by[e] = in ? by[q] : 0.0;
+        const double x = (!ZERO && in) ? vxi[q] : 0.0, y = (!ZERO && in) ? vyi[q] : 0.0;
+        s_v[e] = x;
+        s_v[A + e] = y;
+        s_v[2 * A + e] = x;  // entries no sweep writes (walls, the frame) read the same in both buffers
+        s_v[3 * A + e] = y;
+    }
+    __syncthreads();
+    GridL gt = g;  // global indices on the shared tile: at(gt, i, j) = i C + j, arrays shifted by (ib, jb)
+    gt.P = C;
+    const ptrdiff_t sh = (ptrdiff_t)ib * C + jb;
+    RhsArgs rhs;
+    rhs.mode = RHS_ARRAYS;
+    rhs.bx = s_bx - sh;
+    rhs.by = s_by - sh;
+    rhs.p = rhs.rho = nullptr;
+    rhs.gx = rhs.gy = 0.0;
+    for (int k = 0; k < n; ++k) {
+        const int m = n - 1 - k;  // sweep k: the unknowns within m cells of the tile
+        const int i_lo = max(I0 - m, 1), i_hi = min(I0 + TTR - 1 + m, g.ncy);
+        const int j_lo = max(J0 - m, 1), j_hi = min(J0 + TTC - 1 + m, g.ncx);
+        const int w = j_hi - j_lo + 1, cnt = (i_hi - i_lo + 1) * w;
+        const double *vix = s_v + 2 * (k & 1) * A - sh, *viy = vix + A;
+        double *vox = s_v + 2 * ((k + 1) & 1) * A - sh, *voy = vox + A;
+        for (int e = t; e < cnt; e += nt) {
+            const int i = i_lo + e / w, j = j_lo + e % w;
+            if (ZERO && k == 0) jacobi_pt<true, TT_RCP>(gt, s_eb - sh, s_ep - sh, vix, viy, vox, voy, rhs, omega, i, j);
+            else jacobi_pt<false, TT_RCP>(gt, s_eb - sh, s_ep - sh, vix, viy, vox, voy, rhs, omega, i, j);
+        }
+        __syncthreads();
+    }
+    // store the tile's unknowns and the mirror nodes its boundary rows / columns own
+    const double *fx = s_v + 2 * (n & 1) * A - sh, *fy = fx + A;
+    const int i1 = min(I0 + TTR - 1, g.ncy), j1 = min(J0 + TTC - 1, g.ncx);
+    const int ilo = (I0 == 1) ? 0 : I0, ihi = (i1 == g.ncy) ? g.ncy + 1 : i1;
+    const int jlo = (J0 == 1) ? 0 : J0, jhi = (j1 == g.ncx) ? g.ncx + 1 : j1;
+    const int w = jhi - jlo + 1, cnt = (ihi - ilo + 1) * w;
+    for (int e = t; e < cnt; e += nt) {
+        const int i = ilo + e / w, j = jlo + e % w;
+        const size_t q = at(g, i, j), s = at(gt, i, j);
+        const bool xin = j >= 1 && j <= g.nvxj, yin = i >= 1 && i <= g.nvyi;
+        const bool xrow = i >= 1 && i <= g.ncy;  // vx rows of unknowns; rows 0 / ncy+1: mirrors
+        if (xin && (xrow || (i == 0 && g.bN) || (i == g.ncy + 1 && g.bS))) vxo[q] = fx[s];
+        const bool ycol = j >= 1 && j <= g.ncx;
+        if (yin && (ycol || (j == 0 && g.bW) || (j == g.ncx + 1 && g.bE))) vyo[q] = fy[s];
+    }
 }
 
 // Damped red-black Gauss-Seidel (Eq. sor_update), one of the four phases
@@ -1047,6 +1145,27 @@ void launch_jacobi(const LaunchCtx &c, const GridL &g, const double *etab, const
     if (zero_in) k_jacobi<true><<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs, omega);
     else k_jacobi<false><<<cell_grid(g), tpb(), 0, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs, omega);
     LAUNCH_BOOK(c);
+}
+bool launch_jacobi_tile(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
+                        const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
+                        double omega, int n, bool zero_in) {
+    if (rhs.mode != RHS_ARRAYS || n < 1 || n > TT_MAXN || !(g.bN && g.bS && g.bW && g.bE)) return false;
+    static unsigned long long done = 0;
+    if (first_on_device(&done)) {
+        const int most = 8 * tt_rows(TT_MAXN) * tt_cols(TT_MAXN) * 8;
+        cudaFuncSetAttribute(k_jacobi_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+        cudaFuncSetAttribute(k_jacobi_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, most);
+    }
+    const int smem = 8 * tt_rows(n) * tt_cols(n) * 8;
+    const dim3 grid((g.ncx + TTC - 1) / TTC, (g.ncy + TTR - 1) / TTR);
+    if (zero_in)
+        k_jacobi_tile<true><<<grid, TTR * TTC, smem, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs.bx, rhs.by,
+                                                                 omega, n);
+    else
+        k_jacobi_tile<false><<<grid, TTR * TTC, smem, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs.bx, rhs.by,
+                                                                  omega, n);
+    LAUNCH_BOOK(c);
+    return true;
 }
 void launch_rbgs(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *vx, double *vy,
                  const RhsArgs &rhs, double omega) {

@@ -93,14 +93,36 @@ def test_smoother(S, smoother, nx, ny, bc):
         assert rel(qx[:, 1:-1], rx[:, 1:-1]) <= TOL_OP and rel(qy[1:-1], ry[1:-1]) <= TOL_OP
 
 
+@pytest.mark.parametrize("nsweeps", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("nx,ny", [(8, 8), (33, 17), (64, 200), (300, 250), (1030, 13)])
+@pytest.mark.parametrize("bc", BCS)
+def test_tile_smoother(S, nx, ny, bc, nsweeps, monkeypatch):
+    """n damped-Jacobi sweeps of a small level in one launch (k_jacobi_tile: 8 x 32 tiles with an
+    (n+1)-cell frame in shared memory, the sweeps shrinking region by region): ragged tiles,
+    one-row / one-column tiles, every boundary set, n = 1 .. 8, against the oracle's n sweeps."""
+    monkeypatch.setenv("STOKES_TILE_CELLS", str(10 ** 9))
+    f = parity_fields(nx, ny, log_contrast=1.0)
+    o, s = pair(S, nx, ny, bc, f, omega_v=0.5, coarse_min=4, coarse_direct=0)
+    rng = np.random.default_rng(13)
+    bx, by = rng.standard_normal((ny, nx + 1)), rng.standard_normal((ny + 1, nx))
+    vx, vy = rng.standard_normal((ny, nx + 1)), rng.standard_normal((ny + 1, nx))
+    vx[:, [0, -1]] = 0.0
+    vy[[0, -1], :] = 0.0
+    ex, ey = o.smooth(0, bx, by, vx, vy, nsweeps)
+    gx, gy = s.smooth(0, T(bx), T(by), T(vx), T(vy), nsweeps)
+    assert rel(gx, ex) <= TOL_OP and rel(gy, ey) <= TOL_OP
+
+
 @pytest.mark.parametrize("smoother,nsweeps", [(0, 2), (0, 4), (0, 5), (1, 1), (1, 2), (1, 3)])
 @pytest.mark.parametrize("nx,ny", [(128, 8), (300, 250), (1030, 13)])
 @pytest.mark.parametrize("bc", BCS)
-def test_streamed_smoothers(S, nx, ny, bc, smoother, nsweeps):
+def test_streamed_smoothers(S, nx, ny, bc, smoother, nsweeps, monkeypatch):
     """Levels >= 128 x 8 run Jacobi sweep pairs as one temporally blocked pass (two sweeps
     per HBM read) and RBGS sweeps as one streamed pass (the four phases as a wavefront:
     vx red row s, vx black s-2, vy red s-4, vy black s-6 per step); ragged column tiles,
-    8-row strips and every mirror ghost included."""
+    8-row strips and every mirror ghost included.  (The small-level tile smoother is switched
+    off here so that these sizes exercise the streamed passes.)"""
+    monkeypatch.setenv("STOKES_TILE_CELLS", "0")
     f = parity_fields(nx, ny, log_contrast=1.0)
     o, s = pair(S, nx, ny, bc, f, smoother=smoother, omega_v=0.5, coarse_min=4, coarse_direct=0)
     rng = np.random.default_rng(11)

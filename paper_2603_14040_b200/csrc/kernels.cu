@@ -172,11 +172,15 @@ __global__ void __launch_bounds__(BX *BY) k_jacobi(GridL g, const double *__rest
 #ifndef TT_RCP
 #define TT_RCP 1  // 1/a_ii by MUFU seed + Newton (as the streamed kernels) instead of the IEEE division
 #endif
+#ifndef TT_THREADS
+#define TT_THREADS 512  // 2 threads per tile cell: the sweeps are latency-bound (256 threads: +4 ms per solve)
+#endif
 constexpr int TTR = TT_ROWS, TTC = 32, TT_MAXN = 8;  // tile rows / columns, most sweeps per launch
+constexpr int TTN = TT_THREADS;                      // threads per tile CTA
 __host__ __device__ constexpr int tt_rows(int n) { return TTR + 2 * (n + 1); }
 __host__ __device__ constexpr int tt_cols(int n) { return TTC + 2 * (n + 1); }
 template <bool ZERO>
-__global__ void __launch_bounds__(TTR *TTC) k_jacobi_tile(GridL g, const double *__restrict__ etab,
+__global__ void __launch_bounds__(TTN) k_jacobi_tile(GridL g, const double *__restrict__ etab,
                                                           const double *__restrict__ etap, const double *__restrict__ vxi,
                                                           const double *__restrict__ vyi, double *__restrict__ vxo,
                                                           double *__restrict__ vyo, const double *__restrict__ bx,
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(TTR *TTC) k_jacobi_tile(GridL g, const double 
     const int R = tt_rows(n), C = tt_cols(n), A = R * C;
     double *s_eb = tsm, *s_ep = tsm + A, *s_bx = tsm + 2 * A, *s_by = tsm + 3 * A;
     double *s_v = tsm + 4 * A;  // buffer b: vx at s_v + 2 b A, vy at s_v + (2 b + 1) A
-    const int t = threadIdx.x, nt = TTR * TTC;
+    const int t = threadIdx.x, nt = TTN;
     const int I0 = 1 + blockIdx.y * TTR, J0 = 1 + blockIdx.x * TTC;  // first cell of the tile
     const int ib = I0 - (n + 1), jb = J0 - (n + 1);                    // global index of tile entry (0, 0)
     // stage: every array entry of the frame that exists (nodes 0..ncy+1 x 0..ncx+1), 0 elsewhere
@@ -1159,10 +1163,10 @@ bool launch_jacobi_tile(const LaunchCtx &c, const GridL &g, const double *etab, 
     const int smem = 8 * tt_rows(n) * tt_cols(n) * 8;
     const dim3 grid((g.ncx + TTC - 1) / TTC, (g.ncy + TTR - 1) / TTR);
     if (zero_in)
-        k_jacobi_tile<true><<<grid, TTR * TTC, smem, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs.bx, rhs.by,
+        k_jacobi_tile<true><<<grid, TTN, smem, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs.bx, rhs.by,
                                                                  omega, n);
     else
-        k_jacobi_tile<false><<<grid, TTR * TTC, smem, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs.bx, rhs.by,
+        k_jacobi_tile<false><<<grid, TTN, smem, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs.bx, rhs.by,
                                                                   omega, n);
     LAUNCH_BOOK(c);
     return true;

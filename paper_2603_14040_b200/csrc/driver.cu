@@ -219,6 +219,10 @@ static long long tile_cells() {  // (read per call: tests force either path)
     const char *e = getenv("STOKES_TILE_CELLS");
     return e ? atoll(e) : 256LL * 256LL;
 }
+static bool post_fused_prolong() {  // STOKES_TILE_PROLONG=0: separate prolongation launch (diagnostics)
+    const char *e = getenv("STOKES_TILE_PROLONG");
+    return !(e && e[0] == '0');
+}
 static bool tile_level(stokes_s *h, int l) {
     const GridL &g = h->lev[l].g;
     return (long long)g.ncx * g.ncy <= tile_cells();
@@ -428,8 +432,15 @@ void vcycle(stokes_s *h, int l, double *ax, double *ay, double *sx, double *sy, 
         launch_restrict_vel(c, L.g, C.g, L.rx, L.ry, C.bx, C.by);             // (3) restriction
     }
     vcycle(h, l + 1, C.vx[0], C.vy[0], C.vx[1], C.vy[1], rhs_arrays(C.bx, C.by), true);  // (4)
-    launch_prolong(c, L.g, C.g, C.vx[0], C.vy[0], cx, cy);                    // (5) correction
-    smooth(h, l, cx, cy, ox, oy, rhs, post_n, false, post_pairs);            // (6) post-smoothing
+    if (!leave_last && level_smoother(h, l) == STOKES_SMOOTH_JACOBI && tile_level(h, l) && post_fused_prolong() &&
+        launch_jacobi_tile(c, L.g, L.etab, L.etap, cx, cy, ox, oy, rhs, h->o.omega_v, post_n, false, &C.g, C.vx[0],
+                           C.vy[0])) {  // (5) + (6): the correction applied while the tile smoother stages v
+        double *t = cx; cx = ox; ox = t;
+        t = cy; cy = oy; oy = t;
+    } else {
+        launch_prolong(c, L.g, C.g, C.vx[0], C.vy[0], cx, cy);                // (5) correction
+        smooth(h, l, cx, cy, ox, oy, rhs, post_n, false, post_pairs);        // (6) post-smoothing
+    }
     if (leave_last) {
         *lx = cx;
         *ly = cy;

@@ -59,9 +59,12 @@ void launch_jacobi(const LaunchCtx &c, const GridL &g, const double *etab, const
                    const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs, double omega, bool zero_in);
 // n (<= 8) damped-Jacobi sweeps of a single-domain level with array right-hand sides in ONE
 // launch (tiles staged in shared memory; k_jacobi's arithmetic); false: not applicable
+// ex / ey (coarse level gc): the post-smoothing's input is v + P e (the prolongation applied
+// while staging) -- prolongation and post-smoothing in one launch
 bool launch_jacobi_tile(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
                         const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
-                        double omega, int n, bool zero_in);
+                        double omega, int n, bool zero_in, const GridL *gc = nullptr, const double *ex = nullptr,
+                        const double *ey = nullptr);
 void launch_rbgs(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, double *vx, double *vy,
                  const RhsArgs &rhs, double omega);
 void launch_residual(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap, const double *vx,

@@ -166,6 +166,30 @@ __global__ void __launch_bounds__(BX *BY) k_jacobi(GridL g, const double *__rest
 // indices, the global boundary logic and mirrors unchanged; 1/a_ii by the MUFU seed + Newton
 // steps of the streamed kernels unless TT_RCP = 0, which equals n launches of k_jacobi bit for
 // bit).  Then the tile's unknowns (and its mirror nodes) are stored.
+// The bilinear coarse-grid correction of prolong_pt at one fine vx / vy
+// unknown, as a value (the same expressions, so v + corr rounds as prolong_pt's update).
+__device__ __forceinline__ double corr_x(const GridL &gc, const double *__restrict__ ex, int i, int j) {
+    const int J0 = j >> 1;
+    int I0;
+    double wy0, wy1;
+    if (i & 1) { I0 = (i + 1) / 2 - 1; wy0 = 0.25; wy1 = 0.75; }
+    else { I0 = i / 2; wy0 = 0.75; wy1 = 0.25; }
+    if (j & 1)
+        return wy0 * 0.5 * (ex[at(gc, I0, J0)] + ex[at(gc, I0, J0 + 1)]) +
+               wy1 * 0.5 * (ex[at(gc, I0 + 1, J0)] + ex[at(gc, I0 + 1, J0 + 1)]);
+    return wy0 * ex[at(gc, I0, J0)] + wy1 * ex[at(gc, I0 + 1, J0)];
+}
+__device__ __forceinline__ double corr_y(const GridL &gc, const double *__restrict__ ey, int i, int j) {
+    const int I0 = i >> 1;
+    int J0;
+    double wx0, wx1;
+    if (j & 1) { J0 = (j + 1) / 2 - 1; wx0 = 0.25; wx1 = 0.75; }
+    else { J0 = j / 2; wx0 = 0.75; wx1 = 0.25; }
+    if (i & 1)
+        return wx0 * 0.5 * (ey[at(gc, I0, J0)] + ey[at(gc, I0 + 1, J0)]) +
+               wx1 * 0.5 * (ey[at(gc, I0, J0 + 1)] + ey[at(gc, I0 + 1, J0 + 1)]);
+    return wx0 * ey[at(gc, I0, J0)] + wx1 * ey[at(gc, I0, J0 + 1)];
+}
 #ifndef TT_ROWS
 #define TT_ROWS 8
 #endif
@@ -184,7 +208,8 @@ __global__ void __launch_bounds__(TTN) k_jacobi_tile(GridL g, const double *__re
                                                           const double *__restrict__ etap, const double *__restrict__ vxi,
                                                           const double *__restrict__ vyi, double *__restrict__ vxo,
                                                           double *__restrict__ vyo, const double *__restrict__ bx,
-                                                          const double *__restrict__ by, double omega, int n) {
+                                                          const double *__restrict__ by, double omega, int n, GridL gc,
+                                                          const double *__restrict__ ex, const double *__restrict__ ey) {
     extern __shared__ __align__(16) double tsm[];
     const int R = tt_rows(n), C = tt_cols(n), A = R * C;
     double *s_eb = tsm, *s_ep = tsm + A, *s_bx = tsm + 2 * A, *s_by = tsm + 3 * A;
@@ -201,7 +226,20 @@ __global__ void __launch_bounds__(TTN) k_jacobi_tile(GridL g, const double *__re
         s_ep[e] = in ? etap[q] : 0.0;
         s_bx[e] = in ? bx[q] : 0.0;
         s_by[e] = in ? by[q] : 0.0;
-        const double x = (!ZERO && in) ? vxi[q] : 0.0, y = (!ZERO && in) ? vyi[q] : 0.0;
+        double x = (!ZERO && in) ? vxi[q] : 0.0, y = (!ZERO && in) ? vyi[q] : 0.0;
+        if (!ZERO && ex && in) {  // post-smoothing: the coarse-grid correction added while staging
+            // (unknowns, and the mirror nodes as the mirror of their partner's correction)
+            if (j >= 1 && j <= g.nvxj) {
+                if (i >= 1 && i <= g.ncy) x += corr_x(gc, ex, i, j);
+                else if (i == 0 && g.bN) x += g.sN * corr_x(gc, ex, 1, j);
+                else if (i == g.ncy + 1 && g.bS) x += g.sS * corr_x(gc, ex, g.ncy, j);
+            }
+            if (i >= 1 && i <= g.nvyi) {
+                if (j >= 1 && j <= g.ncx) y += corr_y(gc, ey, i, j);
+                else if (j == 0 && g.bW) y += g.sW * corr_y(gc, ey, i, 1);
+                else if (j == g.ncx + 1 && g.bE) y += g.sE * corr_y(gc, ey, i, g.ncx);
+            }
+        }
         s_v[e] = x;
         s_v[A + e] = y;
         s_v[2 * A + e] = x;  // entries no sweep writes (walls, the frame) read the same in both buffers
@@ -1152,7 +1190,8 @@ void launch_jacobi(const LaunchCtx &c, const GridL &g, const double *etab, const
 }
 bool launch_jacobi_tile(const LaunchCtx &c, const GridL &g, const double *etab, const double *etap,
                         const double *vxi, const double *vyi, double *vxo, double *vyo, const RhsArgs &rhs,
-                        double omega, int n, bool zero_in) {
+                        double omega, int n, bool zero_in, const GridL *gc, const double *ex, const double *ey) {
+    if (ex && (zero_in || !gc)) return false;
     if (rhs.mode != RHS_ARRAYS || n < 1 || n > TT_MAXN || !(g.bN && g.bS && g.bW && g.bE)) return false;
     static unsigned long long done = 0;
     if (first_on_device(&done)) {
@@ -1164,10 +1203,10 @@ bool launch_jacobi_tile(const LaunchCtx &c, const GridL &g, const double *etab, 
     const dim3 grid((g.ncx + TTC - 1) / TTC, (g.ncy + TTR - 1) / TTR);
     if (zero_in)
         k_jacobi_tile<true><<<grid, TTN, smem, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs.bx, rhs.by,
-                                                                 omega, n);
+                                                           omega, n, g, nullptr, nullptr);
     else
         k_jacobi_tile<false><<<grid, TTN, smem, c.stream>>>(g, etab, etap, vxi, vyi, vxo, vyo, rhs.bx, rhs.by,
-                                                                  omega, n);
+                                                            omega, n, gc ? *gc : g, ex, ey);
     LAUNCH_BOOK(c);
     return true;
 }

@@ -914,8 +914,9 @@ static int dist_gcr_step_body(Dist &D, int i) {
             stokes_s *t = D.tile[k];
             const size_t nf = field_doubles(t->lev[0].g);
             const double *const *nxt = (j + 1 < i) ? (const double *const *)t->gw[j + 1] : nullptr;
-            launch_mgs_step(ctx(t), D.gpart[pin], nbin, 2, 0, t->gw[i], t->gz[i], (const double *const *)t->gw[j],
-                            (const double *const *)t->gz[j], nxt, (const double *const *)t->gr, nf, seg_of(D, pout, k, nbf));
+            launch_mgs_step(ctx(t), D.gpart[pin], nbin, 2, 0, t->gw[i], nullptr, (const double *const *)t->gw[j],
+                            (const double *const *)t->gz[j], nxt, (const double *const *)t->gr, nf, seg_of(D, pout, k, nbf),
+                            t->scal + S_GAMS + j);  // (z update deferred to the update pass, as on one domain)
         }
         if ((st = tiles_sum(D, pout, nbf))) return st;
         pin = pout;
@@ -927,7 +928,7 @@ static int dist_gcr_step_body(Dist &D, int i) {
         Level &F = t->lev[0];
         double *x[3] = {F.vx[0], F.vy[0], t->pbuf[D.pcur]};
         launch_gcr_update(ctx(t), D.gpart[pin], nbin, t->gw[i], t->gz[i], x, t->gr, (const double *const *)t->gew,
-                          field_doubles(F.g), seg_of(D, pu, k, nbf));
+                          field_doubles(F.g), seg_of(D, pu, k, nbf), t->scal + S_GAMS, i, t->gz);
     }
     if ((st = tiles_sum(D, pu, nbf))) return st;
     launch_gcr_final(dctx(D), D.gpart[pu], nbf * NR, D.gpart[pin], nbin, D.dscal + 3, D.dscal + 0, D.dscal + 1,

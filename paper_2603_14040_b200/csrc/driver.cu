@@ -894,6 +894,10 @@ int solve_uzawa_fused(stokes_s *h, double rtol, double E0, int *iters, double *E
 // V-cycle (z_v = V(0; r_v)); z_p + w = A z + first dot (one streaming pass); i fused MGS
 // steps (axpy + next dot per HBM pass); normalise + update x, r + energy of r (one pass);
 // E, nu^2, <r,r> -> pinned host.  The stored z_p is not de-meaned (inert, reading R14).
+static bool gcr_defer_z() {  // STOKES_GCR_DEFER_Z=0: the z update inside every MGS step (diagnostics)
+    const char *e = getenv("STOKES_GCR_DEFER_Z");
+    return !(e && e[0] == '0');
+}
 void gcr_step_body(stokes_s *h, int i) {
     Level &F = h->lev[0];
     const GridL &g = F.g;
@@ -910,16 +914,19 @@ void gcr_step_body(stokes_s *h, int i) {
                          i > 0 ? (const double *const *)h->gw[0] : nullptr, r[0], r[1], PA);
     int nb = stream_blocks(g);
     double *pin = PA, *pout = PB;
+    const bool defer = gcr_defer_z();  // z -= gamma_j z_j for all j in the update pass (same arithmetic)
     for (int j = 0; j < i; ++j) {
         const double *const *nxt = (j + 1 < i) ? (const double *const *)h->gw[j + 1] : nullptr;
-        launch_mgs_step(c, pin, nb, 2, 0, w, z, (const double *const *)h->gw[j], (const double *const *)h->gz[j], nxt,
-                        (const double *const *)r, nf, pout);
+        launch_mgs_step(c, pin, nb, 2, 0, w, defer ? nullptr : z, (const double *const *)h->gw[j],
+                        (const double *const *)h->gz[j], nxt, (const double *const *)r, nf, pout,
+                        defer ? h->scal + S_GAMS + j : nullptr);
         nb = gcr_flat_blocks();
         double *t = pin;
         pin = pout;
         pout = t;
     }
-    launch_gcr_update(c, pin, nb, w, z, x, r, (const double *const *)h->gew, nf, PC);
+    launch_gcr_update(c, pin, nb, w, z, x, r, (const double *const *)h->gew, nf, PC, h->scal + S_GAMS, defer ? i : 0,
+                      h->gz);
     launch_gcr_final(c, PC, gcr_flat_blocks(), pin, nb, h->scal + S_SF, h->scal + S_E, h->scal + S_NU2,
                      h->scal + S_RR);
     cudaMemcpyAsync(h->hscal, h->scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);

@@ -51,15 +51,24 @@ struct V3 {
 struct C3 {
     const double *f[3];
 };
+constexpr int ZT = 32;  // = MAXM (handle.h)
+struct ZTab {           // the z_j of the deferred z update, j = 0 .. nz-1
+    const double *f[ZT][3];
+};
 
 // MGS step j: gamma = <w, w_j> (from the previous partials);
 // w -= gamma w_j; z -= gamma z_j; then partial dots for the next coefficient:
 // <w, w_{j+1}> if nxt is given, else <w, w> and <r, w> (normalisation + beta).
+// z.f[0] == nullptr: the z update is deferred -- gamma is stored to gout and k_gcr_update
+// applies z -= gamma_j z_j for every j in the same order (the same operations per element,
+// so the same z, for 72 of the 168 B/cell of a step).
 __global__ void __launch_bounds__(FT) k_mgs_step(const double *__restrict__ pin, int nbin, int ncin, int kin,
                                                  V3 w, V3 z, C3 wj, C3 zj, C3 nxt, C3 r, size_t n2,
-                                                 double *__restrict__ pout) {
+                                                 double *__restrict__ pout, double *__restrict__ gout) {
     __shared__ double sh[32];
     const double gam = coef(pin, nbin, ncin, kin, sh);
+    if (gout && blockIdx.x == 0 && threadIdx.x == 0) *gout = gam;
+    const bool upd_z = z.f[0] != nullptr;
     double a0 = 0.0, a1 = 0.0;
     const size_t stride = (size_t)gridDim.x * FT;
 #pragma unroll
@@ -71,13 +80,17 @@ __global__ void __launch_bounds__(FT) k_mgs_step(const double *__restrict__ pin,
         const double2 *N = reinterpret_cast<const double2 *>(nxt.f[f]);
         const double2 *R = reinterpret_cast<const double2 *>(r.f[f]);
         for (size_t e = blockIdx.x * (size_t)FT + threadIdx.x; e < n2; e += stride) {
-            double2 a = W[e], b = WJ[e], c = Z[e], d = ZJ[e];
+            double2 a = W[e], b = WJ[e];
             a.x -= gam * b.x;
             a.y -= gam * b.y;
-            c.x -= gam * d.x;
-            c.y -= gam * d.y;
             W[e] = a;
-            Z[e] = c;
+            if (upd_z) {
+                double2 c = Z[e];
+                const double2 d = ZJ[e];
+                c.x -= gam * d.x;
+                c.y -= gam * d.y;
+                Z[e] = c;
+            }
             if (N) {
                 const double2 q = N[e];
                 a0 += a.x * q.x + a.y * q.y;
@@ -99,9 +112,14 @@ __global__ void __launch_bounds__(FT) k_mgs_step(const double *__restrict__ pin,
 // normalise + update: nu^2 = <w,w>, beta' = <r,w> (previous partials);
 // w /= nu, z /= nu, beta = beta'/nu = <r, w/nu>; x += beta z; r -= beta w; partials of the
 // energy of the new r (sum r^2 * ew) and of <r_old, r_old> (breakdown test).
+// nz > 0: first the deferred MGS updates of z, z -= gamma_j z_j for j = 0 .. nz-1 in order
+// (gammas[j] from the MGS steps), then as before.
 __global__ void __launch_bounds__(FT) k_gcr_update(const double *__restrict__ pin, int nbin, V3 w, V3 z, V3 x, V3 r,
-                                                   C3 ew, size_t n2, double *__restrict__ pout) {
+                                                   C3 ew, size_t n2, double *__restrict__ pout,
+                                                   const double *__restrict__ gammas, int nz, ZTab zt) {
     __shared__ double sh[32];
+    __shared__ double gs[ZT];
+    if (threadIdx.x < nz) gs[threadIdx.x] = gammas[threadIdx.x];  // (ordered before use by coef's barriers)
     const double nu2 = coef(pin, nbin, 2, 0, sh);
     const double bp = coef(pin, nbin, 2, 1, sh);
     const double s = 1.0 / sqrt(nu2);
@@ -117,6 +135,12 @@ __global__ void __launch_bounds__(FT) k_gcr_update(const double *__restrict__ pi
         const double2 *EW = reinterpret_cast<const double2 *>(ew.f[f]);
         for (size_t e = blockIdx.x * (size_t)FT + threadIdx.x; e < n2; e += stride) {
             double2 wv = W[e], zv = Z[e], xv = X[e], rv = R[e];
+            for (int j = 0; j < nz; ++j) {  // deferred MGS z updates, in step order
+                const double2 d = reinterpret_cast<const double2 *>(zt.f[j][f])[e];
+                const double gam = gs[j];
+                zv.x -= gam * d.x;
+                zv.y -= gam * d.y;
+            }
             const double2 q = EW[e];
             a1 += rv.x * rv.x + rv.y * rv.y;
             wv.x *= s;
@@ -175,26 +199,35 @@ int gcr_flat_blocks() { return flat_blocks(); }
 
 void launch_mgs_step(const LaunchCtx &c, const double *pin, int nbin, int ncin, int kin, double *const *w,
                      double *const *z, const double *const *wj, const double *const *zj, const double *const *nxt,
-                     const double *const *r, size_t nfield, double *pout) {
+                     const double *const *r, size_t nfield, double *pout, double *gout) {
     V3 W{{w[0] - COL_OFF, w[1] - COL_OFF, w[2] - COL_OFF}};
-    V3 Z{{z[0] - COL_OFF, z[1] - COL_OFF, z[2] - COL_OFF}};
+    V3 Z{{nullptr, nullptr, nullptr}};
+    C3 ZJ{{nullptr, nullptr, nullptr}};
+    if (z) {  // (z == nullptr: the z update deferred to launch_gcr_update)
+        Z = V3{{z[0] - COL_OFF, z[1] - COL_OFF, z[2] - COL_OFF}};
+        ZJ = C3{{zj[0] - COL_OFF, zj[1] - COL_OFF, zj[2] - COL_OFF}};
+    }
     C3 WJ{{wj[0] - COL_OFF, wj[1] - COL_OFF, wj[2] - COL_OFF}};
-    C3 ZJ{{zj[0] - COL_OFF, zj[1] - COL_OFF, zj[2] - COL_OFF}};
     C3 N{{nullptr, nullptr, nullptr}}, R{{nullptr, nullptr, nullptr}};
     if (nxt) N = C3{{nxt[0] - COL_OFF, nxt[1] - COL_OFF, nxt[2] - COL_OFF}};
     else R = C3{{r[0] - COL_OFF, r[1] - COL_OFF, r[2] - COL_OFF}};
-    k_mgs_step<<<flat_blocks(), FT, 0, c.stream>>>(pin, nbin, ncin, kin, W, Z, WJ, ZJ, N, R, nfield / 2, pout);
+    k_mgs_step<<<flat_blocks(), FT, 0, c.stream>>>(pin, nbin, ncin, kin, W, Z, WJ, ZJ, N, R, nfield / 2, pout, gout);
     ++*c.counter;
 }
 
 void launch_gcr_update(const LaunchCtx &c, const double *pin, int nbin, double *const *w, double *const *z,
-                       double *const *x, double *const *r, const double *const *ew, size_t nfield, double *pout) {
+                       double *const *x, double *const *r, const double *const *ew, size_t nfield, double *pout,
+                       const double *gammas, int nz, double *const (*zj)[3]) {
+    ZTab zt;
+    for (int j = 0; j < nz && j < ZT; ++j)
+        for (int f = 0; f < 3; ++f) zt.f[j][f] = zj[j][f] - COL_OFF;
     V3 W{{w[0] - COL_OFF, w[1] - COL_OFF, w[2] - COL_OFF}};
     V3 Z{{z[0] - COL_OFF, z[1] - COL_OFF, z[2] - COL_OFF}};
     V3 X{{x[0] - COL_OFF, x[1] - COL_OFF, x[2] - COL_OFF}};
     V3 R{{r[0] - COL_OFF, r[1] - COL_OFF, r[2] - COL_OFF}};
     C3 EW{{ew[0] - COL_OFF, ew[1] - COL_OFF, ew[2] - COL_OFF}};
-    k_gcr_update<<<flat_blocks(), FT, 0, c.stream>>>(pin, nbin, W, Z, X, R, EW, nfield / 2, pout);
+    k_gcr_update<<<flat_blocks(), FT, 0, c.stream>>>(pin, nbin, W, Z, X, R, EW, nfield / 2, pout, gammas,
+                                                     nz < ZT ? nz : ZT, zt);
     ++*c.counter;
 }
 

@@ -19,7 +19,8 @@ extern thread_local std::string g_last_error;
 enum { S_MSHIFT = 0, S_E = 1, S_SV = 2, S_SP = 3, S_SF = 4, S_SFPART = 5, S_ZMEAN = 8, S_GAMMA = 9, S_NU2 = 10, S_LOC = 16,
        S_RR = 11, S_BETA = 12, S_ZERO = 13, S_E0 = 14, S_ETAMIN = 24, S_AAMT = 25, S_ITER = 26,
        S_LOOP = 40,  // device-side Uzawa loop: [0] rtol [1] E0 [2] max_iter [3] k [4] status [5] E
-       S_NSCAL = 64 };
+       S_GAMS = 64,  // GCR: the MGS coefficients gamma_j of the current step (MAXM slots)
+       S_NSCAL = 128 };
 constexpr int LOOP_HCAP = 16384;  // device history of E (stokes_solve_hist) in device-loop solves
 
 struct Level {

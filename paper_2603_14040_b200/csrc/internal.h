@@ -255,11 +255,14 @@ void launch_precond_apply(const LaunchCtx &c, const GridL &g, const double *etab
                           double *wy, double *wp, const double *const *w0, const double *rx, const double *ry,
                           double *partials);
 int gcr_flat_blocks();
+// z == nullptr: the MGS z update is deferred (gamma stored to *gout) and done by launch_gcr_update
+// (z -= gamma_j z_j for j = 0 .. nz-1, the same operations in the same order)
 void launch_mgs_step(const LaunchCtx &c, const double *pin, int nbin, int ncin, int kin, double *const *w,
                      double *const *z, const double *const *wj, const double *const *zj, const double *const *nxt,
-                     const double *const *r, size_t nfield, double *pout);
+                     const double *const *r, size_t nfield, double *pout, double *gout = nullptr);
 void launch_gcr_update(const LaunchCtx &c, const double *pin, int nbin, double *const *w, double *const *z,
-                       double *const *x, double *const *r, const double *const *ew, size_t nfield, double *pout);
+                       double *const *x, double *const *r, const double *const *ew, size_t nfield, double *pout,
+                       const double *gammas = nullptr, int nz = 0, double *const (*zj)[3] = nullptr);
 void launch_gcr_final(const LaunchCtx &c, const double *pupd, int nbu, const double *pnorm, int nbn,
                       const double *Sf, double *E, double *nu2, double *rr);
 

@@ -898,7 +898,7 @@ static int dist_gcr_step_body(Dist &D, int i) {
         F.vy[1] = keep[k][5];
     }
     if (st) return st;
-    const int nbs = stream_blocks(D.tile[0]->lev[0].g), nbf = gcr_flat_blocks();
+    const int nbs = stream_blocks(D.tile[0]->lev[0].g), nbf = gcr_flat_blocks(field_doubles(D.tile[0]->lev[0].g));
     for (int k = 0; k < D.nt; ++k) {
         stokes_s *t = D.tile[k];
         Level &F = t->lev[0];
@@ -942,7 +942,7 @@ static int dist_solve_gcr(Dist &D, double rtol, double E0, int *iters, double *E
     int st;
     const int m = D.o.gcr_restart;
     if (!D.gpart[0]) {  // partial buffers: every rank / tile, the larger of the two kernels' block counts
-        const int nbs = stream_blocks(D.tile[0]->lev[0].g), nbf = gcr_flat_blocks();
+        const int nbs = stream_blocks(D.tile[0]->lev[0].g), nbf = gcr_flat_blocks(field_doubles(D.tile[0]->lev[0].g));
         D.gseg = (size_t)2 * (nbs > nbf ? nbs : nbf);
         for (int b = 0; b < 3; ++b)
             if (cudaMalloc(&D.gpart[b], D.gseg * nranks(D) * sizeof(double)) != cudaSuccess) return STOKES_ENOMEM;

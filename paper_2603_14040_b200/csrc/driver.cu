@@ -920,14 +920,14 @@ void gcr_step_body(stokes_s *h, int i) {
         launch_mgs_step(c, pin, nb, 2, 0, w, defer ? nullptr : z, (const double *const *)h->gw[j],
                         (const double *const *)h->gz[j], nxt, (const double *const *)r, nf, pout,
                         defer ? h->scal + S_GAMS + j : nullptr);
-        nb = gcr_flat_blocks();
+        nb = gcr_flat_blocks(nf);
         double *t = pin;
         pin = pout;
         pout = t;
     }
     launch_gcr_update(c, pin, nb, w, z, x, r, (const double *const *)h->gew, nf, PC, h->scal + S_GAMS, defer ? i : 0,
                       h->gz);
-    launch_gcr_final(c, PC, gcr_flat_blocks(), pin, nb, h->scal + S_SF, h->scal + S_E, h->scal + S_NU2,
+    launch_gcr_final(c, PC, gcr_flat_blocks(nf), pin, nb, h->scal + S_SF, h->scal + S_E, h->scal + S_NU2,
                      h->scal + S_RR);
     cudaMemcpyAsync(h->hscal, h->scal, 16 * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
 }

@@ -20,6 +20,9 @@ constexpr int FT = 256;  // threads per CTA
 #define MGS_UNROLL 2  // elements per thread in flight in the MGS / update streams (SolCx 2048^2 GCR(30): 117.8 -> 117.0 ms)
 #endif
 constexpr int MGS_U = MGS_UNROLL;
+#ifndef FLAT_PER_SM_LONG
+#define FLAT_PER_SM_LONG 6
+#endif
 
 // sum of partials[b * ncomp + k] over b, fixed order, every CTA identical; result to all threads
 __device__ double coef(const double *__restrict__ partials, int nb, int ncomp, int k, double *sh) {
@@ -188,20 +191,25 @@ __global__ void __launch_bounds__(FT) k_gcr_final(const double *__restrict__ pup
     }
 }
 
-int flat_blocks() {
-    static int nb = 0;
-    if (!nb) {
-        int dev = 0, nsm = 0;
+// CTAs of the flat GCR kernels for vectors of n2 double2 per field: 4 per SM, 6 for long
+// vectors (>= 2^20 double2 per field: 48 warps per SM keep more loads in flight; SolCx 2048^2
+// GCR(30): 116.9 -> 106.6 ms; 5 / 7 / 8 per SM 110.2 / 119.7 / 114.7 ms -- 7 and 8 spill into a
+// second wave).  Short vectors keep 4 (block 512^2: 27.1 ms vs 28.3 at 6): every CTA also
+// reduces all of the previous kernel's partials.
+int flat_blocks(size_t n2) {
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        nb = (nsm > 0 ? nsm : 148) * 4;
+        if (nsm <= 0) nsm = 148;
     }
-    return nb;
+    return nsm * (n2 >= ((size_t)1 << 20) ? FLAT_PER_SM_LONG : 4);
 }
 
 }  // namespace
 
-int gcr_flat_blocks() { return flat_blocks(); }
+int gcr_flat_blocks(size_t nfield) { return flat_blocks(nfield / 2); }
 
 void launch_mgs_step(const LaunchCtx &c, const double *pin, int nbin, int ncin, int kin, double *const *w,
                      double *const *z, const double *const *wj, const double *const *zj, const double *const *nxt,
@@ -217,7 +225,7 @@ void launch_mgs_step(const LaunchCtx &c, const double *pin, int nbin, int ncin, 
     C3 N{{nullptr, nullptr, nullptr}}, R{{nullptr, nullptr, nullptr}};
     if (nxt) N = C3{{nxt[0] - COL_OFF, nxt[1] - COL_OFF, nxt[2] - COL_OFF}};
     else R = C3{{r[0] - COL_OFF, r[1] - COL_OFF, r[2] - COL_OFF}};
-    k_mgs_step<<<flat_blocks(), FT, 0, c.stream>>>(pin, nbin, ncin, kin, W, Z, WJ, ZJ, N, R, nfield / 2, pout, gout);
+    k_mgs_step<<<flat_blocks(nfield / 2), FT, 0, c.stream>>>(pin, nbin, ncin, kin, W, Z, WJ, ZJ, N, R, nfield / 2, pout, gout);
     ++*c.counter;
 }
 
@@ -232,7 +240,7 @@ void launch_gcr_update(const LaunchCtx &c, const double *pin, int nbin, double *
     V3 X{{x[0] - COL_OFF, x[1] - COL_OFF, x[2] - COL_OFF}};
     V3 R{{r[0] - COL_OFF, r[1] - COL_OFF, r[2] - COL_OFF}};
     C3 EW{{ew[0] - COL_OFF, ew[1] - COL_OFF, ew[2] - COL_OFF}};
-    k_gcr_update<<<flat_blocks(), FT, 0, c.stream>>>(pin, nbin, W, Z, X, R, EW, nfield / 2, pout, gammas,
+    k_gcr_update<<<flat_blocks(nfield / 2), FT, 0, c.stream>>>(pin, nbin, W, Z, X, R, EW, nfield / 2, pout, gammas,
                                                      nz < ZT ? nz : ZT, zt);
     ++*c.counter;
 }

@@ -254,7 +254,7 @@ void launch_precond_apply(const LaunchCtx &c, const GridL &g, const double *etab
                           const double *zx, const double *zy, const double *rp, double alpha, double *zp, double *wx,
                           double *wy, double *wp, const double *const *w0, const double *rx, const double *ry,
                           double *partials);
-int gcr_flat_blocks();
+int gcr_flat_blocks(size_t nfield);  // CTAs (= partials) of the flat GCR kernels for fields of nfield doubles
 // z == nullptr: the MGS z update is deferred (gamma stored to *gout) and done by launch_gcr_update
 // (z -= gamma_j z_j for j = 0 .. nz-1, the same operations in the same order)
 void launch_mgs_step(const LaunchCtx &c, const double *pin, int nbin, int ncin, int kin, double *const *w,
